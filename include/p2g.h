@@ -1,0 +1,225 @@
+/*
+ * p2g.h — C ABI of the B200-native SPARTan PARAFAC2-ALS engine.
+ *
+ * This is the drop-in boundary.  The reference exposes a
+ * header-only C++ API (/root/reference/proj/include/parafac2); there is no
+ * FFI in the reference, so each entry point below names the reference
+ * function it replaces (file:line).  The C++ drop-in headers in
+ * include/parafac2/ headers re-create the reference's signatures on top of this
+ * ABI; INTEGRATION.md shows how a maintainer binds it.
+ *
+ * Conventions
+ *  - Plain pointers and sizes only.  Host buffers are borrowed for the
+ *    duration of the call.  Dense matrices are column-major (the layout of
+ *    Eigen::MatrixXd, common.hpp:30) unless stated otherwise.
+ *  - Every function returns a status: 0 ok; P2G_EINVAL (std::invalid_argument),
+ *    P2G_EDATA (DataError, CLI exit 2), P2G_ENUM (NumericalError, CLI exit 3),
+ *    P2G_ECUDA (CUDA/NCCL failure).  p2g_last_error() returns the message of
+ *    the last failure on the calling thread (solver/common.hpp messages are
+ *    preserved where the reference defines them).
+ *  - One context drives one GPU.  Multi-GPU: one process (rank) per GPU,
+ *    each with its own context; subjects are sharded by
+ *    partition_weighted(nnz_k + I_k, world) (parallel.hpp:51-79,
+ *    solver.hpp:263-267) and the per-iteration J x R / R x R partials are
+ *    combined with ncclAllReduce.  A context is not thread-safe.
+ *  - There is no CPU fallback: every compute entry point runs on the GPU and
+ *    fails with P2G_ECUDA when no device is usable.
+ *
+ * Data layout of the sparse tensor (flattened CSR):
+ *    subj_row_ptr[K+1]  int64  first global row of subject k
+ *    row_ptr[NR+1]      int64  first entry of global row r (NR = sum_k I_k)
+ *    col_idx[nnz]       int32  column ids, strictly ascending within a row
+ *    val[nnz]           fp64   stored values (non-zero)
+ *  Packed per-subject factors Q_k (I_k x R) are stored as one ROW-MAJOR
+ *  (sum_k I_k) x R array, subject k occupying rows subj_row_ptr[k]...
+ */
+#ifndef P2G_H_
+#define P2G_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define P2G_OK 0
+#define P2G_EINVAL 1
+#define P2G_EDATA 2
+#define P2G_ENUM 3
+#define P2G_ECUDA 4
+
+/* Procrustes flags per subject (canonical rule D5). */
+#define P2G_FLAG_FULL_RANK 0   /* rank(A_k) = R: unique polar factor            */
+#define P2G_FLAG_DEFICIENT 1   /* rank(A_k) < R: canonical completion           */
+#define P2G_FLAG_ACCURATE 2    /* ill-conditioned: solved by the Jacobi-SVD path */
+#define P2G_FLAG_DEGENERATE 3  /* completion itself degenerate (not parity-safe) */
+
+/* Last error message of the calling thread ("" if none). */
+const char* p2g_last_error(void);
+/* Library version / build string. */
+const char* p2g_version(void);
+
+/* ------------------------------------------------------------------------
+ * Host-side utilities (no GPU required)
+ * ------------------------------------------------------------------------ */
+
+/* partition_weighted (parallel.hpp:51-79): contiguous [begin,end) ranges of
+ * roughly equal cumulative weight.  begin_end receives 2*n_out int64 values;
+ * it must hold 2*n_chunks.  Bit-exact with the reference. */
+int p2g_partition_weighted(const uint64_t* weights, int64_t n, int32_t n_chunks, int64_t* begin_end,
+                           int32_t* n_out);
+
+/* Synthetic BASELINE workloads (decisions D1, D10, D11).
+ * Deterministic function of the spec: subject k draws from
+ * Rng(substream_seed(seed, k+1)) (common.hpp:65-121).  */
+typedef struct {
+  int64_t K;           /* subjects                                            */
+  int64_t J;           /* variables (columns)                                 */
+  int32_t rows_dist;   /* 0: I_k ~ U{rows_lo..rows_hi}; 1: Geometric(1/rows_mean) capped at rows_hi */
+  int64_t rows_lo, rows_hi;
+  double rows_mean;
+  int64_t min_rows;    /* D1: I_k <- max(I_k, min_rows) (= R)                 */
+  int32_t nnz_dist;    /* 0: nnz_row ~ U{nnz_lo..nnz_hi}; 1: 1 + Poisson(nnz_lambda) */
+  int64_t nnz_lo, nnz_hi;
+  double nnz_lambda;
+  int32_t col_dist;    /* 0: uniform over [0,J); 1: Zipf(zipf_s), rank = column id */
+  double zipf_s;
+  int32_t val_dist;    /* 0: 1 - uniform() in (0,1]; 1: 1 + below(5)          */
+  uint64_t seed;
+  int32_t threads;     /* host threads (0 = hardware concurrency); result independent of it */
+} p2g_gen_spec;
+
+typedef struct p2g_gen p2g_gen;
+
+/* Fills *spec with BASELINE.json config `config_id` (1..5) at rank R. */
+int p2g_gen_baseline_spec(int32_t config_id, int32_t R, p2g_gen_spec* spec);
+int p2g_gen_create(const p2g_gen_spec* spec, p2g_gen** out, int64_t* n_rows, int64_t* nnz);
+int p2g_gen_export(const p2g_gen* g, int64_t* subj_row_ptr, int64_t* row_ptr, int32_t* col_idx, double* val);
+void p2g_gen_free(p2g_gen* g);
+
+/* Initial factors for the BASELINE configs (D2): H = I_R; V (J x R) from
+ * Rng(seed) r-outer / j-inner exactly as solver.hpp:128-132, then W (K x R)
+ * continuing the same stream r-outer / k-inner.  Column-major outputs. */
+int p2g_init_factors(uint64_t seed, int64_t K, int64_t J, int32_t R, double* H, double* V, double* W);
+
+/* The reference's random initialisation (solver.hpp:124-132): H = I,
+ * S = ones, V from Rng(seed).  Validation of rank/tol/max_iters/I_k/J as in
+ * initialize() (solver.hpp:104-122). */
+int p2g_initialize_random(uint64_t seed, int64_t K, int64_t J, int32_t R, double* H, double* S, double* V);
+
+/* ------------------------------------------------------------------------
+ * Device context
+ * ------------------------------------------------------------------------ */
+typedef struct p2g_ctx p2g_ctx;
+
+/* 128-byte NCCL unique id for multi-GPU contexts (call on rank 0, share). */
+int p2g_nccl_unique_id(char out_id[128]);
+/* world == 1: nccl_id may be NULL (no NCCL).  device: CUDA ordinal. */
+int p2g_create(int32_t device, int32_t rank, int32_t world, const char* nccl_id, p2g_ctx** out);
+int p2g_destroy(p2g_ctx* ctx);
+
+/* Uploads this rank's shard of the full tensor (all K subjects given).
+ * Validates the CSR (DataError on bad indices / empty tensor). */
+int p2g_load_csr(p2g_ctx* ctx, int64_t K, int64_t J, const int64_t* subj_row_ptr, const int64_t* row_ptr,
+                 const int32_t* col_idx, const double* val);
+/* This rank's subject range [k_begin, k_end) and its row / nnz counts. */
+int p2g_shard_info(const p2g_ctx* ctx, int64_t* k_begin, int64_t* k_end, int64_t* n_rows, int64_t* nnz);
+
+/* ------------------------------------------------------------------------
+ * The fused PARAFAC2-ALS loop — replaces fit_parafac2 (solver.hpp:251-321).
+ * ------------------------------------------------------------------------ */
+typedef struct {
+  int32_t rank;       /* R >= 1                                 (solver.hpp:51) */
+  int32_t max_iters;  /* >= 1                                   (solver.hpp:52) */
+  double tol;         /* > 0; relative fit change stop          (solver.hpp:53) */
+  int32_t nonneg;     /* NNLS on V and W                        (solver.hpp:54) */
+  int32_t init;       /* 0: random V from seed, H=I, W=ones (solver.hpp:124-132);
+                         2: explicit H0/V0/W0 (D2).  (eye init: not on GPU.) */
+  uint64_t seed;      /*                                        (solver.hpp:56) */
+} p2g_fit_config;
+
+typedef struct {
+  int32_t iterations;
+  int32_t converged;
+  double total_ms;
+  double norm_x;      /* ||X||_F^2 */
+} p2g_fit_summary;
+
+/* H0 (R x R), V0 (J x R), W0 (K x R, all subjects) used when init == 2.
+ * Outputs (any may be NULL): H_out (R x R), V_out (J x R), W_out (this
+ * rank's shard rows, (k_end-k_begin) x R), Q_out (this rank's packed Q,
+ * row-major), flags_out (per shard subject, last iteration),
+ * fit / resid / ms per iteration (length >= max_iters). */
+int p2g_fit(p2g_ctx* ctx, const p2g_fit_config* cfg, const double* H0, const double* V0, const double* W0,
+            double* H_out, double* V_out, double* W_out, double* Q_out, int32_t* flags_out, double* fit_trace,
+            double* resid_trace, double* ms_trace, p2g_fit_summary* summary);
+
+/* Device-resident variant for benchmarking: runs `iters` iterations from the
+ * state left by the previous call (or from explicit factors when reset != 0),
+ * all inputs already in HBM.  Reports per-iteration device time (ms, CUDA
+ * events, max over ranks when world > 1). */
+int p2g_bench_iterations(p2g_ctx* ctx, const p2g_fit_config* cfg, const double* H0, const double* V0,
+                         const double* W0, int32_t reset, int32_t iters, double* ms_per_iter, double* fit_trace);
+
+/* Process-wide number of CUDA kernels this library has launched so far. */
+int64_t p2g_launch_count(void);
+
+/* Per-kernel device time of the last p2g_bench_iterations call, averaged per
+ * launch: names "procrustes", "mode2", "mode3", "nnls_v", "nnls_w", ... */
+int p2g_kernel_times(const p2g_ctx* ctx, int32_t max_entries, char* names /* max_entries*32 */,
+                     double* ms_per_launch, int64_t* launches, int32_t* n_out);
+
+/* ------------------------------------------------------------------------
+ * Per-step entry points (teacher-forced parity hooks; all on this shard)
+ * ------------------------------------------------------------------------ */
+
+/* procrustes_update over all shard subjects (solver.hpp:173-193 + the
+ * run_chunks loop :279-284), fused with the mode-1 MTTKRP partial
+ * M1 = sum_k Q_k^T (X_k V) diag(W_k) (mttkrp.hpp:81-106 in Q form).
+ * H (R x R), V (J x R), W (K x R full).  Q_out packed row-major; flags per
+ * shard subject; m1_out (R x R, allreduced).  Any output may be NULL. */
+int p2g_procrustes(p2g_ctx* ctx, int32_t R, const double* H, const double* V, const double* W, double* Q_out,
+                   int32_t* flags_out, double* m1_out);
+
+/* Q-based slice-wise MTTKRP (north_star forms) from packed Q of this shard:
+ *  mode 1: sum_k Q_k^T (X_k V) diag(W_k)            -> R x R (allreduced)
+ *  mode 2: sum_k X_k^T (Q_k H diag(W_k))            -> J x R (allreduced)
+ *  mode 3: row k = colwise-dot(Q_k H, X_k V)        -> shard K x R
+ * Equal to mttkrp(project_slices(X, Q), H, V, W, mode) (mttkrp.hpp:187-196). */
+int p2g_mttkrp_q(p2g_ctx* ctx, int32_t mode, int32_t R, const double* Q, const double* H, const double* V,
+                 const double* W, double* out);
+
+/* project_slices (solver.hpp:212-235): packed Y_k = Q_k^T X_k (R x c_k,
+ * column-major per subject, subjects concatenated) and the column ids.
+ * ycol_ptr[K_shard+1] offsets (in columns) are written first; call with
+ * Y_out == NULL to obtain sizes only. */
+int p2g_project(p2g_ctx* ctx, int32_t R, const double* Q, int64_t* ycol_ptr, int32_t* ycols, double* Y_out);
+
+/* mttkrp on packed projected slices — replaces mttkrp(ProjectedSlices,...)
+ * (mttkrp.hpp:187-196) with its shape checks (:170-181).  Standalone: does
+ * not need load_csr.  ycol_ptr[K+1], ycols (ascending per slice), Y packed
+ * (R x c_k column-major blocks).  H R x R, V J x R, W K x R. */
+int p2g_mttkrp_packed(p2g_ctx* ctx, int32_t mode, int64_t K, int64_t J, int32_t R, const int64_t* ycol_ptr,
+                      const int32_t* ycols, const double* Y, const double* H, const double* V, const double* W,
+                      double* out);
+
+/* cp_als_iteration on packed projected slices (cp.hpp:99-145): H, V, W in/out
+ * (column-major), lambda_out (R), m3_out (K x R) optional. */
+int p2g_cp_als_iteration(p2g_ctx* ctx, int64_t K, int64_t J, int32_t R, const int64_t* ycol_ptr,
+                         const int32_t* ycols, const double* Y, double* H, double* V, double* W, int32_t nonneg,
+                         int32_t normalize_w, double* lambda_out, double* m3_out);
+
+/* nnls_rowwise (kernels.hpp:194-211): X (n x R) = argmin_{X>=0} rowwise
+ * x G x^T - 2 x b^T; max_iter 0 -> 30 R.  Column-major G (R x R), B, X. */
+int p2g_nnls_rowwise(p2g_ctx* ctx, const double* G, const double* B, int64_t n, int32_t R, int32_t max_iter,
+                     double* X);
+
+/* pinv_small (kernels.hpp:68-87) and gram (kernels.hpp:57-63) on device. */
+int p2g_pinv_small(p2g_ctx* ctx, const double* G, int32_t n, double* out);
+int p2g_gram(p2g_ctx* ctx, const double* A, int64_t rows, int32_t cols, double* out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* P2G_H_ */

@@ -1,0 +1,553 @@
+"""B200-native SPARTan PARAFAC2-ALS engine — Python host mirror of the C ABI.
+
+The product is ``lib/libp2g.so`` (CUDA sm_100a + host C++), declared in
+``include/p2g.h``.  This module is a thin ctypes binding whose names and
+argument meaning follow the reference's C++ entry points
+(/root/reference/proj/include/parafac2):
+
+    fit_parafac2      solver.hpp:251-321    -> Context.fit
+    procrustes_update solver.hpp:173-193    -> Context.procrustes (all subjects)
+    project_slices    solver.hpp:212-235    -> Context.project
+    mttkrp            mttkrp.hpp:187-196    -> Context.mttkrp_packed / mttkrp_q
+    cp_als_iteration  cp.hpp:99-145         -> Context.cp_als_iteration
+    nnls_rowwise      kernels.hpp:194-211   -> Context.nnls_rowwise
+    pinv_small / gram kernels.hpp:57-87     -> Context.pinv_small / gram
+    partition_weighted parallel.hpp:51-79   -> partition_weighted
+
+Errors map like the reference's exception types: ``InvalidArgument``
+(std::invalid_argument), ``DataError`` (exit code 2), ``NumericalError``
+(exit code 3) and ``CudaError`` (no usable GPU / CUDA / NCCL failure).
+There is no CPU fallback: without the built library or a GPU every compute
+call raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass, field
+from typing import Optional, Sequence
+
+import numpy as np
+
+__all__ = [
+    "InvalidArgument", "DataError", "NumericalError", "CudaError",
+    "CSRTensor", "SolverConfig", "FitResult", "Context", "lib_path", "load_library",
+    "partition_weighted", "generate_baseline", "baseline_spec", "init_factors",
+    "initialize_random", "FLAG_FULL_RANK", "FLAG_DEFICIENT", "FLAG_ACCURATE", "FLAG_DEGENERATE",
+]
+
+FLAG_FULL_RANK, FLAG_DEFICIENT, FLAG_ACCURATE, FLAG_DEGENERATE = 0, 1, 2, 3
+
+
+class InvalidArgument(ValueError):
+    """std::invalid_argument in the reference."""
+
+
+class DataError(RuntimeError):
+    """parafac2::DataError (common.hpp:37-39), CLI exit code 2."""
+
+
+class NumericalError(ArithmeticError):
+    """parafac2::NumericalError (common.hpp:43-45), CLI exit code 3."""
+
+
+class CudaError(RuntimeError):
+    """CUDA / NCCL failure or no usable device (the path has no CPU fallback)."""
+
+
+_ERRORS = {1: InvalidArgument, 2: DataError, 3: NumericalError, 4: CudaError}
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+def lib_path() -> str:
+    return os.path.join(_HERE, "lib", "libp2g.so")
+
+
+class GenSpec(ctypes.Structure):
+    _fields_ = [
+        ("K", ctypes.c_int64), ("J", ctypes.c_int64), ("rows_dist", ctypes.c_int32),
+        ("rows_lo", ctypes.c_int64), ("rows_hi", ctypes.c_int64), ("rows_mean", ctypes.c_double),
+        ("min_rows", ctypes.c_int64), ("nnz_dist", ctypes.c_int32), ("nnz_lo", ctypes.c_int64),
+        ("nnz_hi", ctypes.c_int64), ("nnz_lambda", ctypes.c_double), ("col_dist", ctypes.c_int32),
+        ("zipf_s", ctypes.c_double), ("val_dist", ctypes.c_int32), ("seed", ctypes.c_uint64),
+        ("threads", ctypes.c_int32),
+    ]
+
+
+class _FitConfig(ctypes.Structure):
+    _fields_ = [
+        ("rank", ctypes.c_int32), ("max_iters", ctypes.c_int32), ("tol", ctypes.c_double),
+        ("nonneg", ctypes.c_int32), ("init", ctypes.c_int32), ("seed", ctypes.c_uint64),
+    ]
+
+
+class _FitSummary(ctypes.Structure):
+    _fields_ = [
+        ("iterations", ctypes.c_int32), ("converged", ctypes.c_int32),
+        ("total_ms", ctypes.c_double), ("norm_x", ctypes.c_double),
+    ]
+
+
+_LIB = None
+
+_P = ctypes.c_void_p
+_I32, _I64, _U64, _D = ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64, ctypes.c_double
+
+_SIGS = {
+    "p2g_last_error": (ctypes.c_char_p, []),
+    "p2g_version": (ctypes.c_char_p, []),
+    "p2g_partition_weighted": (ctypes.c_int, [_P, _I64, _I32, _P, _P]),
+    "p2g_gen_baseline_spec": (ctypes.c_int, [_I32, _I32, _P]),
+    "p2g_gen_create": (ctypes.c_int, [_P, _P, _P, _P]),
+    "p2g_gen_export": (ctypes.c_int, [_P, _P, _P, _P, _P]),
+    "p2g_gen_free": (None, [_P]),
+    "p2g_init_factors": (ctypes.c_int, [_U64, _I64, _I64, _I32, _P, _P, _P]),
+    "p2g_initialize_random": (ctypes.c_int, [_U64, _I64, _I64, _I32, _P, _P, _P]),
+    "p2g_nccl_unique_id": (ctypes.c_int, [_P]),
+    "p2g_create": (ctypes.c_int, [_I32, _I32, _I32, _P, _P]),
+    "p2g_destroy": (ctypes.c_int, [_P]),
+    "p2g_load_csr": (ctypes.c_int, [_P, _I64, _I64, _P, _P, _P, _P]),
+    "p2g_shard_info": (ctypes.c_int, [_P, _P, _P, _P, _P]),
+    "p2g_fit": (ctypes.c_int, [_P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
+    "p2g_bench_iterations": (ctypes.c_int, [_P, _P, _P, _P, _P, _I32, _I32, _P, _P]),
+    "p2g_kernel_times": (ctypes.c_int, [_P, _I32, _P, _P, _P, _P]),
+    "p2g_launch_count": (ctypes.c_int64, []),
+    "p2g_procrustes": (ctypes.c_int, [_P, _I32, _P, _P, _P, _P, _P, _P]),
+    "p2g_mttkrp_q": (ctypes.c_int, [_P, _I32, _I32, _P, _P, _P, _P, _P]),
+    "p2g_project": (ctypes.c_int, [_P, _I32, _P, _P, _P, _P]),
+    "p2g_mttkrp_packed": (ctypes.c_int, [_P, _I32, _I64, _I64, _I32, _P, _P, _P, _P, _P, _P, _P]),
+    "p2g_cp_als_iteration": (ctypes.c_int, [_P, _I64, _I64, _I32, _P, _P, _P, _P, _P, _P, _I32, _I32, _P, _P]),
+    "p2g_nnls_rowwise": (ctypes.c_int, [_P, _P, _P, _I64, _I32, _I32, _P]),
+    "p2g_pinv_small": (ctypes.c_int, [_P, _P, _I32, _P]),
+    "p2g_gram": (ctypes.c_int, [_P, _P, _I64, _I32, _P]),
+}
+
+
+def load_library():
+    """Loads lib/libp2g.so (built by ``make -C paper_1703_04219_b200``).
+
+    Raises ``ImportError`` loudly when the extension is missing: there is no
+    Python or CPU fallback for the compute path."""
+    global _LIB
+    if _LIB is not None:
+        return _LIB
+    path = lib_path()
+    if not os.path.exists(path):
+        raise ImportError(f"libp2g.so not built at {path}; run __graft_entry__.build() "
+                          "or `make -C paper_1703_04219_b200`")
+    lib = ctypes.CDLL(path)
+    for name, (res, args) in _SIGS.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _LIB = lib
+    return lib
+
+
+def _check(status: int) -> None:
+    if status != 0:
+        msg = load_library().p2g_last_error().decode()
+        raise _ERRORS.get(status, RuntimeError)(msg)
+
+
+def _ptr(a: Optional[np.ndarray]):
+    return None if a is None else a.ctypes.data_as(ctypes.c_void_p)
+
+
+def _f64(a, shape=None, order="F") -> np.ndarray:
+    a = np.asarray(a, dtype=np.float64)
+    if shape is not None and a.shape != tuple(shape):
+        if a.ndim == 1 and len(shape) == 2 and a.size == shape[0] * shape[1]:
+            a = a.reshape(shape, order=order)
+        else:
+            raise InvalidArgument(f"expected shape {tuple(shape)}, got {a.shape}")
+    return np.require(a, dtype=np.float64, requirements=[order, "A"])
+
+
+# ---------------------------------------------------------------------------
+# Data model
+# ---------------------------------------------------------------------------
+@dataclass
+class CSRTensor:
+    """Irregular tensor {X_k} as one flattened CSR (include/p2g.h layout).
+
+    Equivalent to the reference's IrregularTensor (sparse.hpp:176-215): subject
+    k owns rows subj_row_ptr[k]..subj_row_ptr[k+1]; columns are strictly
+    ascending within a row."""
+
+    J: int
+    subj_row_ptr: np.ndarray
+    row_ptr: np.ndarray
+    col_idx: np.ndarray
+    val: np.ndarray
+
+    def __post_init__(self):
+        self.subj_row_ptr = np.ascontiguousarray(self.subj_row_ptr, dtype=np.int64)
+        self.row_ptr = np.ascontiguousarray(self.row_ptr, dtype=np.int64)
+        self.col_idx = np.ascontiguousarray(self.col_idx, dtype=np.int32)
+        self.val = np.ascontiguousarray(self.val, dtype=np.float64)
+
+    @property
+    def K(self) -> int:
+        return len(self.subj_row_ptr) - 1
+
+    @property
+    def n_rows(self) -> int:
+        return int(self.subj_row_ptr[-1])
+
+    @property
+    def nnz(self) -> int:
+        return int(self.row_ptr[-1])
+
+    def rows_of(self) -> np.ndarray:
+        return np.diff(self.subj_row_ptr)
+
+    def subject_nnz(self) -> np.ndarray:
+        return self.row_ptr[self.subj_row_ptr[1:]] - self.row_ptr[self.subj_row_ptr[:-1]]
+
+    def subset(self, k0: int, k1: int) -> "CSRTensor":
+        """Subjects [k0, k1) as a standalone tensor (rebased)."""
+        r0, r1 = int(self.subj_row_ptr[k0]), int(self.subj_row_ptr[k1])
+        p0, p1 = int(self.row_ptr[r0]), int(self.row_ptr[r1])
+        return CSRTensor(self.J, self.subj_row_ptr[k0:k1 + 1] - r0, self.row_ptr[r0:r1 + 1] - p0,
+                         self.col_idx[p0:p1].copy(), self.val[p0:p1].copy())
+
+    def frobenius_sq(self) -> float:
+        return float(np.dot(self.val, self.val))
+
+
+@dataclass
+class SolverConfig:
+    """solver.hpp:48-58 (threads is host-only and ignored on the GPU path)."""
+
+    rank: int = 1
+    max_iters: int = 200
+    tol: float = 1e-8
+    nonneg: bool = True
+    init: str = "random"   # "random" (solver.hpp:128-132) or "explicit" (D2)
+    seed: int = 0
+    threads: int = 1
+
+
+@dataclass
+class FitResult:
+    H: np.ndarray
+    V: np.ndarray
+    W: np.ndarray            # this rank's rows of S (= W), shard order
+    Q: Optional[np.ndarray]  # packed row-major (sum I_k) x R of this shard
+    flags: Optional[np.ndarray]
+    fit: np.ndarray
+    residual_sq: np.ndarray
+    ms: np.ndarray
+    iterations: int
+    converged: bool
+    total_ms: float
+    norm_x: float
+    k_begin: int = 0
+    k_end: int = 0
+
+
+# ---------------------------------------------------------------------------
+# Host-side utilities (no GPU needed)
+# ---------------------------------------------------------------------------
+def partition_weighted(weights: Sequence[int], n_chunks: int):
+    """parallel.hpp:51-79, bit-exact."""
+    lib = load_library()
+    w = np.ascontiguousarray(np.asarray(weights, dtype=np.uint64))
+    out = np.zeros(2 * max(n_chunks, 1), dtype=np.int64)
+    n = ctypes.c_int32()
+    _check(lib.p2g_partition_weighted(_ptr(w), len(w), n_chunks, _ptr(out), ctypes.byref(n)))
+    return [(int(out[2 * i]), int(out[2 * i + 1])) for i in range(n.value)]
+
+
+def baseline_spec(config_id: int, R: int) -> GenSpec:
+    spec = GenSpec()
+    _check(load_library().p2g_gen_baseline_spec(config_id, R, ctypes.byref(spec)))
+    return spec
+
+
+def generate(spec: GenSpec) -> CSRTensor:
+    lib = load_library()
+    g = ctypes.c_void_p()
+    nr, nz = ctypes.c_int64(), ctypes.c_int64()
+    _check(lib.p2g_gen_create(ctypes.byref(spec), ctypes.byref(g), ctypes.byref(nr), ctypes.byref(nz)))
+    try:
+        srp = np.empty(spec.K + 1, np.int64)
+        rp = np.empty(nr.value + 1, np.int64)
+        ci = np.empty(nz.value, np.int32)
+        v = np.empty(nz.value, np.float64)
+        _check(lib.p2g_gen_export(g, _ptr(srp), _ptr(rp), _ptr(ci), _ptr(v)))
+    finally:
+        lib.p2g_gen_free(g)
+    return CSRTensor(int(spec.J), srp, rp, ci, v)
+
+
+def generate_baseline(config_id: int, R: int, K: Optional[int] = None, threads: int = 0) -> CSRTensor:
+    """BASELINE.json config `config_id`.  K < spec.K gives the
+    first K subjects of the same stream (subject k is a pure function of k)."""
+    spec = baseline_spec(config_id, R)
+    if K is not None:
+        spec.K = int(K)
+    spec.threads = threads
+    return generate(spec)
+
+
+def init_factors(seed: int, K: int, J: int, R: int):
+    """H = I, V then W from one Rng(seed) stream (D2).  Column-major arrays."""
+    H = np.empty((R, R), order="F")
+    V = np.empty((J, R), order="F")
+    W = np.empty((K, R), order="F")
+    _check(load_library().p2g_init_factors(seed, K, J, R, _ptr(H), _ptr(V), _ptr(W)))
+    return H, V, W
+
+
+def initialize_random(seed: int, K: int, J: int, R: int):
+    """initialize() random branch (solver.hpp:124-132): H = I, S = ones, V."""
+    H = np.empty((R, R), order="F")
+    S = np.empty((K, R), order="F")
+    V = np.empty((J, R), order="F")
+    _check(load_library().p2g_initialize_random(seed, K, J, R, _ptr(H), _ptr(S), _ptr(V)))
+    return H, S, V
+
+
+def nccl_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    _check(load_library().p2g_nccl_unique_id(buf))
+    return buf.raw
+
+
+# ---------------------------------------------------------------------------
+# Device context
+# ---------------------------------------------------------------------------
+class Context:
+    """One GPU (rank).  Mirrors the reference's free functions as methods."""
+
+    def __init__(self, device: int = 0, rank: int = 0, world: int = 1, nccl_id: Optional[bytes] = None):
+        self._lib = load_library()
+        self._h = ctypes.c_void_p()
+        idbuf = None if nccl_id is None else ctypes.create_string_buffer(nccl_id, 128)
+        _check(self._lib.p2g_create(device, rank, world, idbuf, ctypes.byref(self._h)))
+        self.rank, self.world = rank, world
+        self.tensor: Optional[CSRTensor] = None
+
+    def close(self):
+        if self._h:
+            _check(self._lib.p2g_destroy(self._h))
+            self._h = ctypes.c_void_p()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- data ---------------------------------------------------------------
+    def load(self, X: CSRTensor) -> None:
+        _check(self._lib.p2g_load_csr(self._h, X.K, X.J, _ptr(X.subj_row_ptr), _ptr(X.row_ptr),
+                                      _ptr(X.col_idx), _ptr(X.val)))
+        self.tensor = X
+
+    def shard_info(self):
+        kb, ke, nr, nz = (ctypes.c_int64() for _ in range(4))
+        _check(self._lib.p2g_shard_info(self._h, ctypes.byref(kb), ctypes.byref(ke), ctypes.byref(nr),
+                                        ctypes.byref(nz)))
+        return kb.value, ke.value, nr.value, nz.value
+
+    # -- fused loop -----------------------------------------------------------
+    def _cfg(self, cfg: SolverConfig, explicit: bool) -> _FitConfig:
+        return _FitConfig(int(cfg.rank), int(cfg.max_iters), float(cfg.tol), 1 if cfg.nonneg else 0,
+                          2 if explicit else 0, int(cfg.seed) & ((1 << 64) - 1))
+
+    def fit(self, cfg: SolverConfig, H0=None, V0=None, W0=None, want_q: bool = True) -> FitResult:
+        """fit_parafac2 (solver.hpp:251-321) on this rank's shard."""
+        X = self.tensor
+        if X is None:
+            raise InvalidArgument("no tensor loaded")
+        R = int(cfg.rank)
+        explicit = H0 is not None
+        if explicit:
+            H0 = _f64(H0, (R, R))
+            V0 = _f64(V0, (X.J, R))
+            W0 = _f64(W0, (X.K, R))
+        kb, ke, nr, _ = self.shard_info()
+        Rv = max(R, 1)
+        H = np.empty((Rv, Rv), order="F")
+        V = np.empty((X.J, Rv), order="F")
+        W = np.empty((ke - kb, Rv), order="F")
+        Q = np.empty((nr, Rv)) if want_q else None
+        flags = np.empty(ke - kb, np.int32)
+        n = max(int(cfg.max_iters), 1)
+        fits, res, ms = np.zeros(n), np.zeros(n), np.zeros(n)
+        summ = _FitSummary()
+        c = self._cfg(cfg, explicit)
+        _check(self._lib.p2g_fit(self._h, ctypes.byref(c), _ptr(H0), _ptr(V0), _ptr(W0), _ptr(H), _ptr(V),
+                                 _ptr(W), _ptr(Q), _ptr(flags), _ptr(fits), _ptr(res), _ptr(ms),
+                                 ctypes.byref(summ)))
+        it = summ.iterations
+        return FitResult(H, V, W, Q, flags, fits[:it], res[:it], ms[:it], it, bool(summ.converged),
+                         summ.total_ms, summ.norm_x, kb, ke)
+
+    def bench_iterations(self, cfg: SolverConfig, iters: int, H0=None, V0=None, W0=None, reset: bool = False):
+        X = self.tensor
+        R = int(cfg.rank)
+        explicit = H0 is not None
+        if explicit:
+            H0, V0, W0 = _f64(H0, (R, R)), _f64(V0, (X.J, R)), _f64(W0, (X.K, R))
+        ms = np.zeros(max(iters, 1))
+        fits = np.zeros(max(iters, 1))
+        c = self._cfg(cfg, explicit)
+        _check(self._lib.p2g_bench_iterations(self._h, ctypes.byref(c), _ptr(H0), _ptr(V0), _ptr(W0),
+                                              1 if reset else 0, iters, _ptr(ms), _ptr(fits)))
+        return ms[:iters], fits[:iters]
+
+    def kernel_times(self):
+        n = 64
+        names = ctypes.create_string_buffer(32 * n)
+        ms = np.zeros(n)
+        cnt = np.zeros(n, np.int64)
+        got = ctypes.c_int32()
+        _check(self._lib.p2g_kernel_times(self._h, n, names, _ptr(ms), _ptr(cnt), ctypes.byref(got)))
+        out = {}
+        for i in range(got.value):
+            nm = names.raw[32 * i:32 * i + 32].split(b"\0", 1)[0].decode()
+            out[nm] = (float(ms[i]), int(cnt[i]))
+        return out
+
+    # -- per-step hooks ---------------------------------------------------------
+    def procrustes(self, H, V, W):
+        """procrustes_update over all shard subjects + fused M1 partial.
+        Returns (Q packed row-major, flags, m1)."""
+        X = self.tensor
+        R = np.asarray(H).shape[0]
+        _, _, nr, _ = self.shard_info()
+        kb, ke = self.shard_info()[:2]
+        Q = np.empty((nr, R))
+        flags = np.empty(ke - kb, np.int32)
+        m1 = np.empty((R, R), order="F")
+        _check(self._lib.p2g_procrustes(self._h, R, _ptr(_f64(H, (R, R))), _ptr(_f64(V, (X.J, R))),
+                                        _ptr(_f64(W, (X.K, R))), _ptr(Q), _ptr(flags), _ptr(m1)))
+        return Q, flags, m1
+
+    def mttkrp_q(self, mode: int, Q, H, V, W):
+        X = self.tensor
+        R = np.asarray(H).shape[0]
+        kb, ke, nr, _ = self.shard_info()
+        rows = {1: R, 2: X.J, 3: ke - kb}.get(mode, 1)
+        out = np.empty((rows, R), order="F")
+        Qc = np.ascontiguousarray(np.asarray(Q, dtype=np.float64).reshape(nr, R))
+        _check(self._lib.p2g_mttkrp_q(self._h, mode, R, _ptr(Qc), _ptr(_f64(H, (R, R))),
+                                      _ptr(_f64(V, (X.J, R))), _ptr(_f64(W, (X.K, R))), _ptr(out)))
+        return out
+
+    def project(self, Q, R: int):
+        """project_slices: returns (ycol_ptr, ycols, list of R x c_k blocks)."""
+        kb, ke, nr, _ = self.shard_info()
+        ptr = np.empty(ke - kb + 1, np.int64)
+        _check(self._lib.p2g_project(self._h, R, None, _ptr(ptr), None, None))
+        nc = int(ptr[-1])
+        cols = np.empty(max(nc, 1), np.int32)
+        Y = np.empty(max(nc * R, 1))
+        Qc = np.ascontiguousarray(np.asarray(Q, dtype=np.float64).reshape(nr, R))
+        _check(self._lib.p2g_project(self._h, R, _ptr(Qc), _ptr(ptr), _ptr(cols), _ptr(Y)))
+        blocks = [Y[ptr[k] * R:ptr[k + 1] * R].reshape((R, ptr[k + 1] - ptr[k]), order="F")
+                  for k in range(ke - kb)]
+        return ptr, cols[:nc], blocks
+
+    def mttkrp_packed(self, mode: int, rank: int, J: int, blocks, cols, H, V, W):
+        """mttkrp(ProjectedSlices, H, V, W, mode) (mttkrp.hpp:187-196)."""
+        ptr, ycols, Y = _pack_projected(rank, blocks, cols)
+        K = len(blocks)
+        H = _f64(H)
+        V = _f64(V)
+        W = _f64(W)
+        R = int(rank)
+        if H.shape != (R, R):
+            raise InvalidArgument("mttkrp: H must be R x R")
+        if V.shape != (J, R):
+            raise InvalidArgument("mttkrp: V must be J x R")
+        if W.shape != (K, R):
+            raise InvalidArgument("mttkrp: W must be K x R")
+        rows = {1: R, 2: J, 3: K}.get(mode, 1)
+        out = np.empty((max(rows, 1), R), order="F")
+        _check(self._lib.p2g_mttkrp_packed(self._h, mode, K, J, R, _ptr(ptr), _ptr(ycols), _ptr(Y), _ptr(H),
+                                           _ptr(V), _ptr(W), _ptr(out)))
+        return out[:rows]
+
+    def cp_als_iteration(self, rank: int, J: int, blocks, cols, H, V, W, nonneg=True, normalize_w=False):
+        """cp_als_iteration (cp.hpp:99-145); returns dict(H, V, W, lambda, m3)."""
+        ptr, ycols, Y = _pack_projected(rank, blocks, cols)
+        K = len(blocks)
+        R = int(rank)
+        H = np.array(_f64(H), order="F", copy=True)
+        V = np.array(_f64(V), order="F", copy=True)
+        W = np.array(_f64(W), order="F", copy=True)
+        if H.shape != (R, R):
+            raise InvalidArgument("cp factors: H must be R x R")
+        if V.shape != (J, R):
+            raise InvalidArgument("cp factors: V must be J x R")
+        if W.shape != (K, R):
+            raise InvalidArgument("cp factors: W must be K x R")
+        lam = np.empty(R)
+        m3 = np.empty((K, R), order="F")
+        _check(self._lib.p2g_cp_als_iteration(self._h, K, J, R, _ptr(ptr), _ptr(ycols), _ptr(Y), _ptr(H), _ptr(V),
+                                              _ptr(W), 1 if nonneg else 0, 1 if normalize_w else 0, _ptr(lam),
+                                              _ptr(m3)))
+        return {"H": H, "V": V, "W": W, "lambda": lam, "m3": m3}
+
+    def nnls_rowwise(self, G, B, max_iter: int = 0):
+        G = _f64(G)
+        B = _f64(B)
+        if G.ndim != 2 or G.shape[0] != G.shape[1]:
+            raise InvalidArgument("nnls_rowwise: G must be square")
+        if B.ndim != 2 or B.shape[1] != G.shape[0]:
+            raise InvalidArgument("nnls_rowwise: B column count must match G")
+        X = np.empty(B.shape, order="F")
+        _check(self._lib.p2g_nnls_rowwise(self._h, _ptr(G), _ptr(B), B.shape[0], G.shape[0], max_iter, _ptr(X)))
+        return X
+
+    def pinv_small(self, G):
+        G = _f64(G)
+        if G.ndim != 2 or G.shape[0] != G.shape[1]:
+            raise InvalidArgument("pinv_small: matrix must be square")
+        out = np.empty(G.shape, order="F")
+        _check(self._lib.p2g_pinv_small(self._h, _ptr(G), G.shape[0], _ptr(out)))
+        return out
+
+    def gram(self, A):
+        A = _f64(A)
+        out = np.empty((A.shape[1], A.shape[1]), order="F")
+        _check(self._lib.p2g_gram(self._h, _ptr(A), A.shape[0], A.shape[1], _ptr(out)))
+        return out
+
+
+def _pack_projected(rank: int, blocks, cols):
+    """(list of R x c_k blocks, list of column lists) -> packed C-ABI arrays."""
+    K = len(blocks)
+    if len(cols) != K:
+        raise InvalidArgument("packed blocks and column lists differ in count")
+    ptr = np.zeros(K + 1, np.int64)
+    for k in range(K):
+        b = np.asarray(blocks[k], dtype=np.float64)
+        c = np.asarray(cols[k])
+        if b.size and b.shape[0] != rank:
+            raise InvalidArgument("packed block row count differs from rank")
+        width = b.shape[1] if b.ndim == 2 else 0
+        if width != len(c):
+            raise InvalidArgument("packed block width differs from column list")
+        ptr[k + 1] = ptr[k] + len(c)
+    nc = int(ptr[-1])
+    ycols = np.zeros(max(nc, 1), np.int32)
+    Y = np.zeros(max(nc * rank, 1))
+    for k in range(K):
+        c = np.asarray(cols[k], dtype=np.int64)
+        ycols[ptr[k]:ptr[k + 1]] = c
+        if len(c):
+            Y[ptr[k] * rank:ptr[k + 1] * rank] = np.asarray(blocks[k], dtype=np.float64).reshape(-1, order="F")
+    return ptr, ycols, Y

@@ -1,0 +1,229 @@
+// Device-side building blocks shared by the libp2g kernels (sm_100a, fp64).
+//
+// All numerics are IEEE binary64 on CUDA cores (DFMA): tcgen05 has no f64
+// kind on sm_100a, so the small dense R x R work runs as
+// warp-cooperative code over shared memory.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace p2g {
+namespace dev {
+
+constexpr unsigned kFull = 0xffffffffu;
+constexpr int kWarp = 32;
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+  return v;
+}
+
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(kFull, v, o));
+  return v;
+}
+
+__device__ __forceinline__ int warp_or(int v) { return __any_sync(kFull, v); }
+
+/// Row-major R-vector gather of V row j (V is J x R row-major).
+template <int RP>
+__device__ __forceinline__ void axpy_row(double (&acc)[RP], const double* __restrict__ vrow, double a, int R) {
+#pragma unroll
+  for (int r = 0; r < RP; ++r)
+    if (r < R) acc[r] = fma(a, __ldg(vrow + r), acc[r]);
+}
+
+/// acc = X_row . V for one CSR row (entries [p0,p1)): the X_k V product of
+/// solver.hpp:182-188 restated row-wise (same per-row accumulation order:
+/// columns ascending).
+template <int RP>
+__device__ __forceinline__ void csr_row_times(double (&acc)[RP], const int32_t* __restrict__ ci,
+                                              const double* __restrict__ val, int64_t p0, int64_t p1,
+                                              const double* __restrict__ V, int R) {
+#pragma unroll
+  for (int r = 0; r < RP; ++r) acc[r] = 0.0;
+  for (int64_t p = p0; p < p1; ++p) {
+    const int j = __ldg(ci + p);
+    const double v = __ldg(val + p);
+    axpy_row<RP>(acc, V + static_cast<int64_t>(j) * R, v, R);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Warp-cooperative small dense algebra on shared memory (row-major, ld = n).
+// ---------------------------------------------------------------------------
+
+/// C = A * B (n x n), all row-major in smem; C must not alias A or B.
+__device__ __forceinline__ void wmm(double* C, const double* A, const double* B, int n, int lane) {
+  for (int e = lane; e < n * n; e += kWarp) {
+    const int i = e / n, j = e - (e / n) * n;
+    double acc = 0.0;
+    for (int k = 0; k < n; ++k) acc = fma(A[i * n + k], B[k * n + j], acc);
+    C[e] = acc;
+  }
+  __syncwarp();
+}
+
+/// C = A^T * B (n x n).
+__device__ __forceinline__ void wmm_tn(double* C, const double* A, const double* B, int n, int lane) {
+  for (int e = lane; e < n * n; e += kWarp) {
+    const int i = e / n, j = e - (e / n) * n;
+    double acc = 0.0;
+    for (int k = 0; k < n; ++k) acc = fma(A[k * n + i], B[k * n + j], acc);
+    C[e] = acc;
+  }
+  __syncwarp();
+}
+
+/// C = A * B^T (n x n).
+__device__ __forceinline__ void wmm_nt(double* C, const double* A, const double* B, int n, int lane) {
+  for (int e = lane; e < n * n; e += kWarp) {
+    const int i = e / n, j = e - (e / n) * n;
+    double acc = 0.0;
+    for (int k = 0; k < n; ++k) acc = fma(A[i * n + k], B[j * n + k], acc);
+    C[e] = acc;
+  }
+  __syncwarp();
+}
+
+/// Cyclic Jacobi eigendecomposition of the symmetric n x n matrix A (smem,
+/// row-major, overwritten: eigenvalues end on the diagonal), eigenvectors
+/// accumulated into the columns of E.  Rotations of one round are disjoint
+/// (round-robin ordering), so the warp applies them simultaneously.
+/// Work arrays: cs[2*ceil(n/2)] doubles, pq[2*ceil(n/2)] ints.
+/// Returns the number of sweeps used.
+__device__ inline int warp_jacobi_eig(double* A, double* E, int n, double* cs, int* pq, int lane,
+                                      int max_sweeps = 40) {
+  for (int e = lane; e < n * n; e += kWarp) E[e] = (e / n == e % n) ? 1.0 : 0.0;
+  __syncwarp();
+  if (n <= 1) return 0;
+  const int m = (n + 1) & ~1;  // players incl. one dummy for odd n
+  const int half = m / 2;
+  int sweep = 0;
+  for (; sweep < max_sweeps; ++sweep) {
+    // Convergence: off-diagonal mass relative to the diagonal.
+    double off = 0.0, dia = 0.0;
+    for (int e = lane; e < n * n; e += kWarp) {
+      const int i = e / n, j = e - i * n;
+      const double a = A[e];
+      if (i == j)
+        dia = fma(a, a, dia);
+      else
+        off = fma(a, a, off);
+    }
+    off = warp_sum(off);
+    dia = warp_sum(dia);
+    if (off == 0.0 || off <= 1e-32 * dia) break;
+    for (int round = 0; round < m - 1; ++round) {
+      if (lane < half) {
+        int p, q;
+        if (lane == 0) {
+          p = round;
+          q = m - 1;
+        } else {
+          p = (round + lane) % (m - 1);
+          q = (round - lane + (m - 1)) % (m - 1);
+        }
+        if (p > q) {
+          const int t = p;
+          p = q;
+          q = t;
+        }
+        double c = 1.0, s = 0.0;
+        if (q < n) {
+          const double apq = A[p * n + q];
+          const double app = A[p * n + p], aqq = A[q * n + q];
+          if (apq != 0.0 && fabs(apq) > 1e-300 && fabs(apq) > 2.2e-16 * 0.01 * sqrt(fabs(app * aqq))) {
+            const double theta = (aqq - app) / (2.0 * apq);
+            const double t = (theta >= 0.0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(fma(theta, theta, 1.0)));
+            c = rsqrt(fma(t, t, 1.0));
+            s = t * c;
+          }
+        } else {
+          q = -1;  // dummy pair
+        }
+        cs[2 * lane] = c;
+        cs[2 * lane + 1] = s;
+        pq[2 * lane] = p;
+        pq[2 * lane + 1] = q;
+      }
+      __syncwarp();
+      // Columns: A <- A J ; E <- E J.
+      for (int it = lane; it < half * n; it += kWarp) {
+        const int pr = it / n, k = it - pr * n;
+        const int p = pq[2 * pr], q = pq[2 * pr + 1];
+        if (q < 0) continue;
+        const double c = cs[2 * pr], s = cs[2 * pr + 1];
+        if (s == 0.0) continue;
+        const double akp = A[k * n + p], akq = A[k * n + q];
+        A[k * n + p] = c * akp - s * akq;
+        A[k * n + q] = s * akp + c * akq;
+        const double ekp = E[k * n + p], ekq = E[k * n + q];
+        E[k * n + p] = c * ekp - s * ekq;
+        E[k * n + q] = s * ekp + c * ekq;
+      }
+      __syncwarp();
+      // Rows: A <- J^T A.
+      for (int it = lane; it < half * n; it += kWarp) {
+        const int pr = it / n, k = it - pr * n;
+        const int p = pq[2 * pr], q = pq[2 * pr + 1];
+        if (q < 0) continue;
+        const double c = cs[2 * pr], s = cs[2 * pr + 1];
+        if (s == 0.0) continue;
+        const double apk = A[p * n + k], aqk = A[q * n + k];
+        A[p * n + k] = c * apk - s * aqk;
+        A[q * n + k] = s * apk + c * aqk;
+      }
+      __syncwarp();
+      if (lane < half) {
+        const int p = pq[2 * lane], q = pq[2 * lane + 1];
+        if (q >= 0 && cs[2 * lane + 1] != 0.0) {
+          A[p * n + q] = 0.0;
+          A[q * n + p] = 0.0;
+        }
+      }
+      __syncwarp();
+    }
+  }
+  return sweep;
+}
+
+/// Moore-Penrose pseudo-inverse of a symmetric PSD n x n matrix (kernels.hpp:
+/// 68-87): symmetrize, eig, keep eigenvalues > 1e-12 * max|lambda| and > 0.
+/// G is read, out written (row-major smem); A, E, T scratch n*n each.
+__device__ inline void warp_pinv_sym(const double* G, double* out, double* A, double* E, double* cs, int* pq, int n,
+                                     int lane) {
+  for (int e = lane; e < n * n; e += kWarp) {
+    const int i = e / n, j = e - i * n;
+    A[e] = 0.5 * (G[i * n + j] + G[j * n + i]);
+  }
+  __syncwarp();
+  warp_jacobi_eig(A, E, n, cs, pq, lane);
+  double amax = 0.0;
+  for (int i = lane; i < n; i += kWarp) amax = fmax(amax, fabs(A[i * n + i]));
+  amax = warp_max(amax);
+  const double cutoff = 1e-12 * amax;
+  for (int e = lane; e < n * n; e += kWarp) {
+    const int i = e / n, j = e - i * n;
+    double acc = 0.0;
+    for (int k = 0; k < n; ++k) {
+      const double ev = A[k * n + k];
+      if (ev > cutoff && ev > 0.0) acc += E[i * n + k] * E[j * n + k] / ev;
+    }
+    out[e] = acc;
+  }
+  __syncwarp();
+  // exact symmetry (kernels.hpp:85)
+  for (int e = lane; e < n * n; e += kWarp) {
+    const int i = e / n, j = e - i * n;
+    if (j > i) out[e] = out[j * n + i];
+  }
+  __syncwarp();
+}
+
+}  // namespace dev
+}  // namespace p2g

@@ -1,0 +1,416 @@
+// K3 — SPARTan slice-wise MTTKRP on the GPU, plus K2 (projection) and the
+// packed-Y boundary kernels.
+//
+// Fused-loop (Q-based) forms, SURVEY.md §3.2 / north_star:
+//   mode 2 (mttkrp.hpp:111-138):  M2 = sum_k X_k^T (Q_k H diag(W_k))   J x R
+//   mode 3 (mttkrp.hpp:143-166):  M3(k,:) = colwise-dot(Q_k H, X_k V)  K x R
+//   mode 1 (mttkrp.hpp:81-106):   M1 = sum_k Q_k^T (X_k V) diag(W_k)  R x R
+// They equal the reference's Y-based kernels on Y_k = Q_k^T X_k
+// (project_slice, solver.hpp:197-208) without materialising Y (F5).
+#include <algorithm>
+
+#include "dev_common.cuh"
+#include "p2g_ctx.hpp"
+
+namespace p2g {
+namespace {
+
+template <int RP>
+__device__ __forceinline__ void stage_rows(double* chunk, const double* __restrict__ src, int nr, int R, int lane) {
+  for (int idx = lane; idx < nr * R; idx += 32) {
+    const int row = idx / R;
+    chunk[row * RP + (idx - row * R)] = __ldg(src + idx);
+  }
+  __syncwarp();
+}
+
+// ---------------------------------------------------------------------------
+// mode 2: one warp per subject; U' = Q_k (H diag(W_k o nH)) row by row, then
+// scattered into M2 with fp64 reductions in L2 (RED.ADD.F64).
+// ---------------------------------------------------------------------------
+template <int RP, int WPB>
+__global__ void __launch_bounds__(WPB * 32)
+    k_mode2(ShardArgs X, int R, const double* __restrict__ Q, const double* __restrict__ H,
+            const double* __restrict__ W, const double* __restrict__ nH, double* __restrict__ M2) {
+  __shared__ double HWs[WPB][RP * RP];
+  __shared__ double chunk[WPB][32 * RP];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  double* HW = HWs[wid];
+  double* ch = chunk[wid];
+  const std::int64_t nwarps = static_cast<std::int64_t>(gridDim.x) * WPB;
+  for (std::int64_t k = static_cast<std::int64_t>(blockIdx.x) * WPB + wid; k < X.K; k += nwarps) {
+    const std::int64_t r0 = X.srp[k];
+    const int I = static_cast<int>(X.srp[k + 1] - r0);
+    for (int e = lane; e < R * R; e += 32) {
+      const int b = e - (e / R) * R;
+      const double w = W[k * R + b] * (nH ? nH[b] : 1.0);
+      HW[e] = H[e] * w;
+    }
+    __syncwarp();
+    for (int b0 = 0; b0 < I; b0 += 32) {
+      const int nr = min(32, I - b0);
+      stage_rows<RP>(ch, Q + (r0 + b0) * R, nr, R, lane);
+      if (lane < nr) {
+        double u[RP];
+#pragma unroll
+        for (int c = 0; c < RP; ++c) {
+          double acc = 0.0;
+          if (c < R) {
+#pragma unroll
+            for (int a = 0; a < RP; ++a)
+              if (a < R) acc = fma(ch[lane * RP + a], HW[a * R + c], acc);
+          }
+          u[c] = acc;
+        }
+        const std::int64_t p0 = X.rp[r0 + b0 + lane], p1 = X.rp[r0 + b0 + lane + 1];
+        for (std::int64_t p = p0; p < p1; ++p) {
+          const int j = __ldg(X.ci + p);
+          const double v = __ldg(X.val + p);
+          double* dst = M2 + static_cast<std::int64_t>(j) * R;
+#pragma unroll
+          for (int c = 0; c < RP; ++c)
+            if (c < R) atomicAdd(dst + c, v * u[c]);
+        }
+      }
+      __syncwarp();
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// mode 3: one warp per subject; M3(k,c) = sum_i (Q_k H)(i,c) (X_k V)(i,c).
+// ---------------------------------------------------------------------------
+template <int RP, int WPB>
+__global__ void __launch_bounds__(WPB * 32)
+    k_mode3(ShardArgs X, int R, const double* __restrict__ Q, const double* __restrict__ H,
+            const double* __restrict__ V, double* __restrict__ M3) {
+  __shared__ double Hs[RP * RP];
+  __shared__ double chunk[WPB][32 * RP];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int e = threadIdx.x; e < R * R; e += blockDim.x) Hs[e] = H[e];
+  __syncthreads();
+  double* ch = chunk[wid];
+  const std::int64_t nwarps = static_cast<std::int64_t>(gridDim.x) * WPB;
+  for (std::int64_t k = static_cast<std::int64_t>(blockIdx.x) * WPB + wid; k < X.K; k += nwarps) {
+    const std::int64_t r0 = X.srp[k];
+    const int I = static_cast<int>(X.srp[k + 1] - r0);
+    double part[RP];
+#pragma unroll
+    for (int c = 0; c < RP; ++c) part[c] = 0.0;
+    for (int b0 = 0; b0 < I; b0 += 32) {
+      const int nr = min(32, I - b0);
+      stage_rows<RP>(ch, Q + (r0 + b0) * R, nr, R, lane);
+      if (lane < nr) {
+        double xv[RP];
+        dev::csr_row_times<RP>(xv, X.ci, X.val, X.rp[r0 + b0 + lane], X.rp[r0 + b0 + lane + 1], V, R);
+#pragma unroll
+        for (int c = 0; c < RP; ++c) {
+          if (c < R) {
+            double qh = 0.0;
+#pragma unroll
+            for (int a = 0; a < RP; ++a)
+              if (a < R) qh = fma(ch[lane * RP + a], Hs[a * R + c], qh);
+            part[c] = fma(qh, xv[c], part[c]);
+          }
+        }
+      }
+      __syncwarp();
+    }
+#pragma unroll
+    for (int c = 0; c < RP; ++c) {
+      if (c < R) {
+        const double t = dev::warp_sum(part[c]);
+        if (lane == 0) M3[k * R + c] = t;
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// mode 1 from a given Q (the p2g_mttkrp_q hook; the fused loop gets M1 from
+// K1): m1 += Q_k^T (XV o W_k) through 32-row chunks.
+// ---------------------------------------------------------------------------
+template <int RP, int WPB>
+__global__ void __launch_bounds__(WPB * 32)
+    k_mode1_q(ShardArgs X, int R, const double* __restrict__ Q, const double* __restrict__ V,
+              const double* __restrict__ W, double* __restrict__ partials) {
+  __shared__ double qch[WPB][32 * RP];
+  __shared__ double xch[WPB][32 * RP];
+  __shared__ double acc_s[WPB][RP * RP];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int RR = R * R;
+  for (int e = lane; e < RR; e += 32) acc_s[wid][e] = 0.0;
+  __syncwarp();
+  const std::int64_t nwarps = static_cast<std::int64_t>(gridDim.x) * WPB;
+  for (std::int64_t k = static_cast<std::int64_t>(blockIdx.x) * WPB + wid; k < X.K; k += nwarps) {
+    const std::int64_t r0 = X.srp[k];
+    const int I = static_cast<int>(X.srp[k + 1] - r0);
+    for (int b0 = 0; b0 < I; b0 += 32) {
+      const int nr = min(32, I - b0);
+      stage_rows<RP>(qch[wid], Q + (r0 + b0) * R, nr, R, lane);
+      double xv[RP];
+      if (lane < nr) {
+        dev::csr_row_times<RP>(xv, X.ci, X.val, X.rp[r0 + b0 + lane], X.rp[r0 + b0 + lane + 1], V, R);
+#pragma unroll
+        for (int c = 0; c < RP; ++c)
+          if (c < R) xch[wid][lane * RP + c] = xv[c] * W[k * R + c];
+      }
+      __syncwarp();
+      for (int e = lane; e < RR; e += 32) {
+        const int x = e / R, y = e - (e / R) * R;
+        double acc = acc_s[wid][e];
+        for (int rr = 0; rr < nr; ++rr) acc = fma(qch[wid][rr * RP + x], xch[wid][rr * RP + y], acc);
+        acc_s[wid][e] = acc;
+      }
+      __syncwarp();
+    }
+  }
+  __syncthreads();
+  if (wid == 0)
+    for (int e = lane; e < RR; e += 32) {
+      double acc = 0.0;
+      for (int w = 0; w < WPB; ++w) acc += acc_s[w][e];
+      partials[static_cast<std::int64_t>(blockIdx.x) * RR + e] = acc;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K2 projection (solver.hpp:197-208): packed Y_k(:, c) = sum over entries of
+// column cols_k[c] of v * Q_k(row, :).  One warp per subject, lane per
+// distinct column, rows visited in ascending order (deterministic).
+// ---------------------------------------------------------------------------
+template <int RP>
+__global__ void k_project(ShardArgs X, int R, const double* __restrict__ Q, const std::int64_t* __restrict__ ycol_ptr,
+                          const std::int32_t* __restrict__ ycols, double* __restrict__ Y) {
+  const int lane = threadIdx.x & 31;
+  const std::int64_t gw = (static_cast<std::int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const std::int64_t nwarps = (static_cast<std::int64_t>(gridDim.x) * blockDim.x) >> 5;
+  for (std::int64_t k = gw; k < X.K; k += nwarps) {
+    const std::int64_t r0 = X.srp[k];
+    const int I = static_cast<int>(X.srp[k + 1] - r0);
+    const std::int64_t c0 = ycol_ptr[k], c1 = ycol_ptr[k + 1];
+    for (std::int64_t cc = c0 + lane; cc < c1; cc += 32) {
+      const int col = ycols[cc];
+      double acc[RP];
+#pragma unroll
+      for (int r = 0; r < RP; ++r) acc[r] = 0.0;
+      for (int i = 0; i < I; ++i) {
+        std::int64_t lo = X.rp[r0 + i], hi = X.rp[r0 + i + 1];
+        while (lo < hi) {  // lower_bound
+          const std::int64_t mid = (lo + hi) >> 1;
+          if (X.ci[mid] < col)
+            lo = mid + 1;
+          else
+            hi = mid;
+        }
+        if (lo < X.rp[r0 + i + 1] && X.ci[lo] == col) {
+          const double v = X.val[lo];
+#pragma unroll
+          for (int r = 0; r < RP; ++r)
+            if (r < R) acc[r] = fma(v, Q[(r0 + i) * R + r], acc[r]);
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < RP; ++r)
+        if (r < R) Y[cc * R + r] = acc[r];
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Packed-Y MTTKRP (the reference's own kernels, mttkrp.hpp:81-166), used by
+// the boundary entry points p2g_mttkrp_packed / p2g_cp_als_iteration.
+// Y: per slice an R x c_k column-major block at Y + ycol_ptr[k]*R.
+// ---------------------------------------------------------------------------
+struct PackedArgs {
+  std::int64_t K, J;
+  int R;
+  const std::int64_t* ycol_ptr;
+  const std::int32_t* ycols;
+  const double* Y;
+  const double* H;
+  const double* V;
+  const double* W;
+};
+
+template <int RP, int WPB>
+__global__ void __launch_bounds__(WPB * 32) k_packed_mode13(PackedArgs a, int mode, double* __restrict__ out) {
+  // mode 1: per-block R x R partials into out[blockIdx]; mode 3: rows of out.
+  __shared__ double prod_s[WPB][RP * RP];
+  __shared__ double acc_s[WPB][RP * RP];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int R = a.R, RR = R * R;
+  for (int e = lane; e < RR; e += 32) acc_s[wid][e] = 0.0;
+  __syncwarp();
+  const std::int64_t nwarps = static_cast<std::int64_t>(gridDim.x) * WPB;
+  for (std::int64_t k = static_cast<std::int64_t>(blockIdx.x) * WPB + wid; k < a.K; k += nwarps) {
+    const std::int64_t c0 = a.ycol_ptr[k], c1 = a.ycol_ptr[k + 1];
+    if (c1 == c0) continue;  // mttkrp.hpp:98,159 skip empty slices
+    // prod = Y_k V(cols_k, :)   (R x R)
+    for (int e = lane; e < RR; e += 32) {
+      const int x = e / R, y = e - (e / R) * R;
+      double acc = 0.0;
+      for (std::int64_t c = c0; c < c1; ++c) acc = fma(a.Y[c * R + x], a.V[static_cast<std::int64_t>(a.ycols[c]) * R + y], acc);
+      prod_s[wid][e] = acc;
+    }
+    __syncwarp();
+    if (mode == 1) {
+      for (int e = lane; e < RR; e += 32) {
+        const int y = e - (e / R) * R;
+        acc_s[wid][e] = fma(prod_s[wid][e], a.W[k * R + y], acc_s[wid][e]);
+      }
+    } else {
+      for (int y = lane; y < R; y += 32) {
+        double acc = 0.0;
+        for (int x = 0; x < R; ++x) acc = fma(a.H[x * R + y], prod_s[wid][x * R + y], acc);
+        out[k * R + y] = acc;
+      }
+    }
+    __syncwarp();
+  }
+  if (mode == 1) {
+    __syncthreads();
+    if (wid == 0)
+      for (int e = lane; e < RR; e += 32) {
+        double acc = 0.0;
+        for (int w = 0; w < WPB; ++w) acc += acc_s[w][e];
+        out[static_cast<std::int64_t>(blockIdx.x) * RR + e] = acc;
+      }
+  }
+}
+
+/// mode 2 on packed Y, deterministic: one warp per output row j walks the
+/// (slice, column) occurrences of j in slice order (col_occ built on host).
+__global__ void k_packed_mode2(PackedArgs a, const std::int64_t* __restrict__ occ_ptr,
+                               const std::int64_t* __restrict__ occ, double* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const std::int64_t gw = (static_cast<std::int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const std::int64_t nwarps = (static_cast<std::int64_t>(gridDim.x) * blockDim.x) >> 5;
+  const int R = a.R;
+  for (std::int64_t j = gw; j < a.J; j += nwarps) {
+    for (int y = lane; y < R; y += 32) {
+      double acc = 0.0;
+      for (std::int64_t t = occ_ptr[j]; t < occ_ptr[j + 1]; ++t) {
+        const std::int64_t c = occ[2 * t], k = occ[2 * t + 1];
+        double tv = 0.0;  // (Y_k^T H)(c, y)
+        for (int x = 0; x < R; ++x) tv = fma(a.Y[c * R + x], a.H[x * R + y], tv);
+        acc = fma(tv, a.W[k * R + y], acc);
+      }
+      out[j * R + y] = acc;
+    }
+  }
+}
+
+/// Warps per block so that static shared memory stays within 48 KB.
+constexpr int fit_wpb(int per_warp_doubles, int fixed_doubles) {
+  int w = 8;
+  while (w > 1 && (w * per_warp_doubles + fixed_doubles) * 8 > 48 * 1024) --w;
+  return w;
+}
+
+int grid_for(std::int64_t warps, int wpb, int num_sms, int per_sm = 8) {
+  const std::int64_t want = (warps + wpb - 1) / wpb;
+  return static_cast<int>(std::max<std::int64_t>(1, std::min<std::int64_t>(want, static_cast<std::int64_t>(num_sms) * per_sm)));
+}
+
+}  // namespace
+
+#define P2G_RP_DISPATCH2(R, CALL)                           \
+  do {                                                      \
+    if ((R) <= 2) {                                         \
+      constexpr int RP_ = 2;                                \
+      CALL;                                                 \
+    } else if ((R) <= 4) {                                  \
+      constexpr int RP_ = 4;                                \
+      CALL;                                                 \
+    } else if ((R) <= 5) {                                  \
+      constexpr int RP_ = 5;                                \
+      CALL;                                                 \
+    } else if ((R) <= 8) {                                  \
+      constexpr int RP_ = 8;                                \
+      CALL;                                                 \
+    } else if ((R) <= 10) {                                 \
+      constexpr int RP_ = 10;                               \
+      CALL;                                                 \
+    } else if ((R) <= 16) {                                 \
+      constexpr int RP_ = 16;                               \
+      CALL;                                                 \
+    } else if ((R) <= 24) {                                 \
+      constexpr int RP_ = 24;                               \
+      CALL;                                                 \
+    } else if ((R) <= 32) {                                 \
+      constexpr int RP_ = 32;                               \
+      CALL;                                                 \
+    } else if ((R) <= 40) {                                 \
+      constexpr int RP_ = 40;                               \
+      CALL;                                                 \
+    } else {                                                \
+      throw InvalidArgument("rank above 40 unsupported");   \
+    }                                                       \
+  } while (0)
+
+static ShardArgs shard_args(p2g_ctx* c) {
+  return ShardArgs{c->srp.get(), c->rp.get(), c->ci.get(), c->val.get(), c->k_end - c->k_begin, c->NR, c->nnz, c->J};
+}
+
+void launch_mode2(p2g_ctx* c, int R, const double* Q, const double* H, const double* W, const double* nH, double* M2,
+                  cudaStream_t s) {
+  const ShardArgs X = shard_args(c);
+  P2G_CUDA(cudaMemsetAsync(M2, 0, sizeof(double) * c->J * R, s));
+  P2G_RP_DISPATCH2(R, ({
+                     constexpr int WPB = fit_wpb(RP_ * RP_ + 32 * RP_, 0);
+                     k_mode2<RP_, WPB><<<grid_for(X.K, WPB, c->num_sms), WPB * 32, 0, s>>>(X, R, Q, H, W, nH, M2);
+                   }));
+  P2G_LAUNCHED(1);
+}
+
+void launch_mode3(p2g_ctx* c, int R, const double* Q, const double* H, const double* V, double* m3,
+                  cudaStream_t s) {
+  const ShardArgs X = shard_args(c);
+  P2G_RP_DISPATCH2(R, ({
+                     constexpr int WPB = fit_wpb(32 * RP_, RP_ * RP_);
+                     k_mode3<RP_, WPB><<<grid_for(X.K, WPB, c->num_sms), WPB * 32, 0, s>>>(X, R, Q, H, V, m3);
+                   }));
+  P2G_LAUNCHED(1);
+}
+
+void launch_mode1_q(p2g_ctx* c, int R, const double* Q, const double* V, const double* W, double* partials,
+                    int nblocks, cudaStream_t s) {
+  const ShardArgs X = shard_args(c);
+  P2G_RP_DISPATCH2(R, ({
+                     constexpr int WPB = fit_wpb(64 * RP_ + RP_ * RP_, 0);
+                     k_mode1_q<RP_, WPB><<<nblocks, WPB * 32, 0, s>>>(X, R, Q, V, W, partials);
+                   }));
+  P2G_LAUNCHED(1);
+}
+
+void launch_project(p2g_ctx* c, int R, const double* Q, const std::int64_t* ycol_ptr, const std::int32_t* ycols,
+                    double* Y, cudaStream_t s) {
+  const ShardArgs X = shard_args(c);
+  P2G_RP_DISPATCH2(R, (k_project<RP_><<<grid_for(X.K, 4, c->num_sms), 128, 0, s>>>(X, R, Q, ycol_ptr, ycols, Y)));
+  P2G_LAUNCHED(1);
+}
+
+int packed_mode1_blocks(int num_sms) { return num_sms * 2; }
+
+void launch_packed_mode13(int mode, std::int64_t K, std::int64_t J, int R, const std::int64_t* ycol_ptr,
+                          const std::int32_t* ycols, const double* Y, const double* H, const double* V,
+                          const double* W, double* out, int nblocks, cudaStream_t s) {
+  PackedArgs a{K, J, R, ycol_ptr, ycols, Y, H, V, W};
+  P2G_RP_DISPATCH2(R, ({
+                     constexpr int WPB = fit_wpb(2 * RP_ * RP_, 0);
+                     k_packed_mode13<RP_, WPB><<<nblocks, WPB * 32, 0, s>>>(a, mode, out);
+                   }));
+  P2G_LAUNCHED(1);
+}
+
+void launch_packed_mode2(std::int64_t K, std::int64_t J, int R, const std::int64_t* ycol_ptr,
+                         const std::int32_t* ycols, const double* Y, const double* H, const double* W,
+                         const std::int64_t* occ_ptr, const std::int64_t* occ, double* out, cudaStream_t s) {
+  PackedArgs a{K, J, R, ycol_ptr, ycols, Y, H, nullptr, W};
+  const int blocks = static_cast<int>(std::max<std::int64_t>(1, std::min<std::int64_t>((J + 3) / 4, 4096)));
+  k_packed_mode2<<<blocks, 128, 0, s>>>(a, occ_ptr, occ, out);
+  P2G_LAUNCHED(1);
+}
+
+}  // namespace p2g

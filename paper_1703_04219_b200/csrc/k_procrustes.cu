@@ -1,0 +1,623 @@
+// K1 — per-subject Procrustes step fused with the mode-1 MTTKRP partial.
+//
+// Replaces procrustes_update (solver.hpp:173-193) over all subjects
+// (solver.hpp:279-284) and mttkrp_mode1 (mttkrp.hpp:81-106) in its Q form
+// M1 = sum_k Q_k^T (X_k V) diag(W_k), which shares X_k V with the Procrustes
+// target (SURVEY.md §3.2 fusion facts).
+//
+// Math (per subject k, D = diag(W_k), T = D H^T):
+//   XV = X_k V                          (CSR gather, V rows via L1/L2)
+//   C  = XV^T XV                        (R x R, lower triangle per lane)
+//   G  = A^T A = T^T C T,  A = XV T     (A = M^T of solver.hpp:189-190)
+//   G  = E diag(lambda) E^T             (warp Jacobi, shared memory)
+//   Q  = A G^{-1/2} = XV P,  P = T E diag(lambda^-1/2) E^T
+//   m1_k = Q^T XV D = P^T C D
+// A is never stored: pass 2 recomputes XV rows and writes Q = XV P.
+//
+// The Gram route squares the condition number, so subjects with
+// lambda_min < kFastRatio * lambda_max (or A == 0, or non-finite G) are
+// flagged and solved by k_procrustes_accurate below: a one-sided Jacobi SVD
+// of A (backward stable like Eigen's JacobiSVD, kernels.hpp:105) with the
+// canonical rank-deficiency rule D5 (oracle/p2_oracle.hpp canonical_polar).
+#include <algorithm>
+
+#include "dev_common.cuh"
+#include "p2g_ctx.hpp"
+
+namespace p2g {
+namespace {
+
+constexpr double kNullRatio = 1e-26;  // sigma^2 <= kNullRatio * sigma_max^2 -> null direction (D5, round-off level)
+constexpr double kFastRatio = 1e-6;   // lambda_min >= kFastRatio * lambda_max -> fast path
+
+struct K1Args {
+  ShardArgs X;
+  int R;
+  const double* H;  // R x R row-major
+  const double* V;  // J x R row-major
+  const double* W;  // K_s x R row-major
+  double* Q;        // NR x R row-major
+  std::int32_t* flags;
+  double* m1_partials;  // gridDim.x x R x R
+  double* scratch;      // accurate path: per-warp I_max x R slabs
+  std::int64_t max_rows;
+  std::int32_t* counters;  // [2] = non-finite operand seen
+};
+
+template <int RP>
+struct K1Smem {
+  static constexpr int kMat = RP * RP;
+  // per warp: C, T, B1, G, E, B2, M1acc + chunk(32*RP) + s(RP) + cs(RP+2) + pq(RP+2 ints)
+  static constexpr int kPerWarpDoubles = 7 * kMat + 32 * RP + RP + (RP + 2) + (RP + 2);
+};
+
+template <int RP, int WPB>
+__global__ void __launch_bounds__(WPB * 32) k_procrustes(K1Args a) {
+  extern __shared__ double smem[];
+  const int lane = threadIdx.x & 31;
+  const int wid = threadIdx.x >> 5;
+  const int R = a.R;
+  const int RR = R * R;
+  double* Hs = smem;  // block-shared H
+  double* base = smem + RP * RP + wid * K1Smem<RP>::kPerWarpDoubles;
+  double* C = base;
+  double* T = C + RP * RP;
+  double* B1 = T + RP * RP;
+  double* G = B1 + RP * RP;
+  double* E = G + RP * RP;
+  double* B2 = E + RP * RP;
+  double* M1 = B2 + RP * RP;
+  double* chunk = M1 + RP * RP;
+  double* s = chunk + 32 * RP;
+  double* cs = s + RP;
+  int* pq = reinterpret_cast<int*>(cs + RP + 2);
+
+  for (int e = threadIdx.x; e < RR; e += blockDim.x) Hs[e] = a.H[e];
+  for (int e = lane; e < RR; e += 32) M1[e] = 0.0;
+  __syncthreads();
+
+  // Lower-triangle entries of C owned by this lane.
+  constexpr int kTri = (RP * (RP + 1) / 2 + 31) / 32;
+  const int ntri = R * (R + 1) / 2;
+  int ea[kTri], eb[kTri];
+#pragma unroll
+  for (int t = 0; t < kTri; ++t) {
+    const int e = lane + 32 * t;
+    int x = 0;
+    while ((x + 1) * (x + 2) / 2 <= e) ++x;
+    ea[t] = x;
+    eb[t] = e - x * (x + 1) / 2;
+  }
+
+  const std::int64_t nwarps = static_cast<std::int64_t>(gridDim.x) * WPB;
+  for (std::int64_t k = static_cast<std::int64_t>(blockIdx.x) * WPB + wid; k < a.X.K; k += nwarps) {
+    const std::int64_t r0 = a.X.srp[k];
+    const int I = static_cast<int>(a.X.srp[k + 1] - r0);
+    if (lane < R) s[lane] = a.W[k * R + lane];
+    __syncwarp();
+
+    // ---- pass 1: C = XV^T XV -------------------------------------------
+    double cacc[kTri];
+#pragma unroll
+    for (int t = 0; t < kTri; ++t) cacc[t] = 0.0;
+    for (int b = 0; b < I; b += 32) {
+      const int i = b + lane;
+      const int nr = min(32, I - b);
+      double xv[RP];
+      if (i < I) {
+        dev::csr_row_times<RP>(xv, a.X.ci, a.X.val, a.X.rp[r0 + i], a.X.rp[r0 + i + 1], a.V, R);
+      } else {
+#pragma unroll
+        for (int r = 0; r < RP; ++r) xv[r] = 0.0;
+      }
+#pragma unroll
+      for (int r = 0; r < RP; ++r) chunk[lane * RP + r] = xv[r];
+      __syncwarp();
+#pragma unroll
+      for (int t = 0; t < kTri; ++t) {
+        if (lane + 32 * t < ntri) {
+          double acc = cacc[t];
+          for (int rr = 0; rr < nr; ++rr) acc = fma(chunk[rr * RP + ea[t]], chunk[rr * RP + eb[t]], acc);
+          cacc[t] = acc;
+        }
+      }
+      __syncwarp();
+    }
+#pragma unroll
+    for (int t = 0; t < kTri; ++t)
+      if (lane + 32 * t < ntri) {
+        C[ea[t] * R + eb[t]] = cacc[t];
+        C[eb[t] * R + ea[t]] = cacc[t];
+      }
+    // T = D H^T
+    for (int e = lane; e < RR; e += 32) {
+      const int i = e / R, j = e - (e / R) * R;
+      T[e] = s[i] * Hs[j * R + i];
+    }
+    __syncwarp();
+    dev::wmm(B1, C, T, R, lane);    // C T
+    dev::wmm_tn(G, T, B1, R, lane);  // T^T C T
+    double gmax = 0.0;
+    bool finite = true;
+    for (int e = lane; e < RR; e += 32) {
+      const double g = G[e];
+      finite &= isfinite(g);
+      gmax = fmax(gmax, fabs(g));
+    }
+    finite = __all_sync(dev::kFull, finite);
+    gmax = dev::warp_max(gmax);
+    if (!finite || gmax == 0.0) {
+      if (lane == 0) a.flags[k] = P2G_FLAG_ACCURATE;  // accurate path decides
+      __syncwarp();
+      continue;
+    }
+    dev::warp_jacobi_eig(G, E, R, cs, pq, lane);
+    double lmax = -1e308, lmin = 1e308;
+    for (int i = lane; i < R; i += 32) {
+      const double l = G[i * R + i];
+      lmax = fmax(lmax, l);
+      lmin = fmin(lmin, l);
+    }
+    lmax = dev::warp_max(lmax);
+    lmin = -dev::warp_max(-lmin);
+    if (!(lmax > 0.0) || !(lmin >= kFastRatio * lmax)) {
+      if (lane == 0) a.flags[k] = P2G_FLAG_ACCURATE;
+      __syncwarp();
+      continue;
+    }
+    // B1 = E diag(lambda^-1/2); B2 = B1 E^T = G^{-1/2}; B1 = T B2 = P
+    for (int e = lane; e < RR; e += 32) {
+      const int j = e - (e / R) * R;
+      B1[e] = E[e] * rsqrt(G[j * R + j]);
+    }
+    __syncwarp();
+    dev::wmm_nt(B2, B1, E, R, lane);
+    dev::wmm(B1, T, B2, R, lane);
+    // m1_k = P^T C D
+    for (int e = lane; e < RR; e += 32) {
+      const int i = e / R, j = e - (e / R) * R;
+      double acc = 0.0;
+      for (int c = 0; c < R; ++c) acc = fma(B1[c * R + i], C[c * R + j], acc);
+      M1[e] = fma(acc, s[j], M1[e]);
+    }
+    // ---- pass 2: Q rows = XV P, staged through smem for coalesced stores
+    for (int b = 0; b < I; b += 32) {
+      const int i = b + lane;
+      const int nr = min(32, I - b);
+      if (i < I) {
+        double xv[RP];
+        dev::csr_row_times<RP>(xv, a.X.ci, a.X.val, a.X.rp[r0 + i], a.X.rp[r0 + i + 1], a.V, R);
+#pragma unroll
+        for (int c = 0; c < RP; ++c) {
+          if (c < R) {
+            double q = 0.0;
+#pragma unroll
+            for (int r = 0; r < RP; ++r)
+              if (r < R) q = fma(xv[r], B1[r * R + c], q);
+            chunk[lane * RP + c] = q;
+          }
+        }
+      }
+      __syncwarp();
+      double* qdst = a.Q + (r0 + b) * R;
+      for (int idx = lane; idx < nr * R; idx += 32) qdst[idx] = chunk[(idx / R) * RP + (idx - (idx / R) * R)];
+      __syncwarp();
+    }
+    if (lane == 0) a.flags[k] = P2G_FLAG_FULL_RANK;
+    __syncwarp();
+  }
+  // Block reduction of the per-warp m1 accumulators, fixed order.
+  __syncthreads();
+  if (wid == 0) {
+    for (int e = lane; e < RR; e += 32) {
+      double acc = 0.0;
+      for (int w = 0; w < WPB; ++w) acc += smem[RP * RP + w * K1Smem<RP>::kPerWarpDoubles + 6 * RP * RP + e];
+      a.m1_partials[static_cast<std::int64_t>(blockIdx.x) * RR + e] = acc;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Accurate path: one-sided Jacobi SVD of A = XV D H^T, canonical rule D5.
+// One warp per flagged subject; A lives in a per-warp global scratch slab
+// (L1/L2 resident: the flagged set is ~1-5% of subjects).
+// ---------------------------------------------------------------------------
+template <int RP>
+struct AccSmem {
+  // per warp: T, Vj, M1, B, Es(eig A), Ee(eig E), TN + qchunk(32*RP) + xchunk(32*RP) + s, sig, cs, pq, idx
+  static constexpr int kPerWarpDoubles = 7 * RP * RP + 64 * RP + 3 * RP + 2 * (RP + 2) + RP;
+};
+
+template <int RP, int WPB>
+__global__ void __launch_bounds__(WPB * 32) k_procrustes_accurate(K1Args a, double* m1_partials_acc) {
+  extern __shared__ double smem[];
+  const int lane = threadIdx.x & 31;
+  const int wid = threadIdx.x >> 5;
+  const int R = a.R;
+  const int RR = R * R;
+  double* Hs = smem;
+  double* base = smem + RP * RP + wid * AccSmem<RP>::kPerWarpDoubles;
+  double* T = base;
+  double* Vj = T + RP * RP;
+  double* M1 = Vj + RP * RP;
+  double* B = M1 + RP * RP;
+  double* EA = B + RP * RP;
+  double* EE = EA + RP * RP;
+  double* TN = EE + RP * RP;
+  double* qch = TN + RP * RP;
+  double* xch = qch + 32 * RP;
+  double* s = xch + 32 * RP;
+  double* sig = s + RP;
+  double* cs = sig + RP;
+  int* pq = reinterpret_cast<int*>(cs + RP + 2);
+  int* strong = reinterpret_cast<int*>(cs + 2 * (RP + 2));  // RP ints: 1 if strong
+  (void)strong;
+
+  for (int e = threadIdx.x; e < RR; e += blockDim.x) Hs[e] = a.H[e];
+  for (int e = lane; e < RR; e += 32) M1[e] = 0.0;
+  __syncthreads();
+
+  const std::int64_t gw = static_cast<std::int64_t>(blockIdx.x) * WPB + wid;
+  const std::int64_t nwarps = static_cast<std::int64_t>(gridDim.x) * WPB;
+  double* A = a.scratch + gw * a.max_rows * R;  // I x R row-major
+
+  for (std::int64_t k = gw; k < a.X.K; k += nwarps) {
+    if (a.flags[k] != P2G_FLAG_ACCURATE) continue;
+    const std::int64_t r0 = a.X.srp[k];
+    const int I = static_cast<int>(a.X.srp[k + 1] - r0);
+    if (lane < R) s[lane] = a.W[k * R + lane];
+    __syncwarp();
+    for (int e = lane; e < RR; e += 32) {
+      const int i = e / R, j = e - (e / R) * R;
+      T[e] = s[i] * Hs[j * R + i];
+    }
+    __syncwarp();
+    // A = XV T (solver.hpp:189-190, transposed)
+    double amax = 0.0;
+    bool finite = true;
+    for (int i = lane; i < I; i += 32) {
+      double xv[RP];
+      dev::csr_row_times<RP>(xv, a.X.ci, a.X.val, a.X.rp[r0 + i], a.X.rp[r0 + i + 1], a.V, R);
+      for (int c = 0; c < R; ++c) {
+        double v = 0.0;
+#pragma unroll
+        for (int r = 0; r < RP; ++r)
+          if (r < R) v = fma(xv[r], T[r * R + c], v);
+        A[i * R + c] = v;
+        finite &= isfinite(v);
+        amax = fmax(amax, fabs(v));
+      }
+    }
+    finite = __all_sync(dev::kFull, finite);
+    amax = dev::warp_max(amax);
+    __syncwarp();
+    if (!finite) {  // common.hpp:50-53 on the svd operand (kernels.hpp:99)
+      if (lane == 0) {
+        atomicAdd(a.counters + 2, 1);
+        a.flags[k] = P2G_FLAG_DEGENERATE;
+      }
+      __syncwarp();
+      continue;
+    }
+    int flag = P2G_FLAG_ACCURATE;
+    int rho = 0;
+    if (amax == 0.0) {
+      // kernels.hpp:101-104: M == 0 -> Q = I(I_k, R).
+      flag = P2G_FLAG_DEFICIENT;
+      for (int e = lane; e < RR; e += 32) Vj[e] = 0.0;  // no strong part
+      if (lane < R) sig[lane] = 0.0;
+      __syncwarp();
+      for (int e = lane; e < RR; e += 32) Vj[e] = (e / R == e % R) ? 1.0 : 0.0;
+      __syncwarp();
+    } else {
+      const double inv = 1.0 / amax;
+      for (int i = lane; i < I; i += 32)
+        for (int c = 0; c < R; ++c) A[i * R + c] *= inv;
+      for (int e = lane; e < RR; e += 32) Vj[e] = (e / R == e % R) ? 1.0 : 0.0;
+      __syncwarp();
+      // Hestenes sweeps (same rotation formulas as oracle one_sided_jacobi).
+      for (int sweep = 0; sweep < 80; ++sweep) {
+        int rotated = 0;
+        for (int p = 0; p < R - 1; ++p)
+          for (int q = p + 1; q < R; ++q) {
+            double al = 0.0, be = 0.0, ga = 0.0;
+            for (int i = lane; i < I; i += 32) {
+              const double x = A[i * R + p], y = A[i * R + q];
+              al = fma(x, x, al);
+              be = fma(y, y, be);
+              ga = fma(x, y, ga);
+            }
+            al = dev::warp_sum(al);
+            be = dev::warp_sum(be);
+            ga = dev::warp_sum(ga);
+            if (ga == 0.0 || fabs(ga) <= 1e-15 * sqrt(al * be)) continue;
+            rotated = 1;
+            const double zeta = (be - al) / (2.0 * ga);
+            const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+            const double c = 1.0 / sqrt(1.0 + t * t);
+            const double sn = c * t;
+            for (int i = lane; i < I; i += 32) {
+              const double x = A[i * R + p], y = A[i * R + q];
+              A[i * R + p] = c * x - sn * y;
+              A[i * R + q] = sn * x + c * y;
+            }
+            if (lane < R) {
+              const double x = Vj[lane * R + p], y = Vj[lane * R + q];
+              Vj[lane * R + p] = c * x - sn * y;
+              Vj[lane * R + q] = sn * x + c * y;
+            }
+            __syncwarp();
+          }
+        if (!rotated) break;
+      }
+      // singular values (of the scaled A), U columns in place
+      for (int c = 0; c < R; ++c) {
+        double acc = 0.0;
+        for (int i = lane; i < I; i += 32) acc = fma(A[i * R + c], A[i * R + c], acc);
+        acc = dev::warp_sum(acc);
+        if (lane == 0) sig[c] = sqrt(acc);
+      }
+      __syncwarp();
+      double smax = 0.0;
+      for (int c = 0; c < R; ++c) smax = fmax(smax, sig[c]);
+      for (int c = 0; c < R; ++c)
+        if (sig[c] * sig[c] > kNullRatio * smax * smax) ++rho;
+      for (int i = lane; i < I; i += 32)
+        for (int c = 0; c < R; ++c) {
+          const double sc = sig[c];
+          A[i * R + c] = (sc * sc > kNullRatio * smax * smax) ? A[i * R + c] / sc : 0.0;
+        }
+      __syncwarp();
+      flag = rho == R ? P2G_FLAG_ACCURATE : P2G_FLAG_DEFICIENT;
+    }
+    // Completion for rho < R (D5): Q = U Vs^T + polar(N) Vn^T,
+    // N = L Vn - U (U^T L Vn), N^T N = I - B^T B, B = U^T L Vn (rho x nn).
+    // Strong columns c: sig[c]^2 > thr (A col c holds U_c); null columns: A col c == 0.
+    double smax2 = 0.0;
+    for (int c = 0; c < R; ++c) smax2 = fmax(smax2, sig[c] * sig[c]);
+    const int nn = R - rho;
+    if (nn > 0) {
+      // B (R x R buffer, only strong rows / null cols used): B[c][d] = sum_{i<R} U[i][c] Vn[i][d]
+      for (int e = lane; e < RR; e += 32) {
+        const int c = e / R, d = e - (e / R) * R;
+        double acc = 0.0;
+        const bool cs_ = amax != 0.0 && sig[c] * sig[c] > kNullRatio * smax2;
+        const bool dn = !(amax != 0.0 && sig[d] * sig[d] > kNullRatio * smax2);
+        if (cs_ && dn)
+          for (int i = 0; i < R; ++i) acc = fma(A[i * R + c], Vj[i * R + d], acc);
+        B[e] = acc;
+      }
+      __syncwarp();
+      // NtN over null columns packed into nn x nn (EA), eig -> TN = (NtN)^{-1/2} (nn x nn)
+      // map null index list into pq-free array: compute on the fly
+      for (int e = lane; e < nn * nn; e += 32) {
+        const int x = e / nn, y = e - (e / nn) * nn;
+        // x-th and y-th null columns
+        int dx = -1, dy = -1, cnt = 0;
+        for (int c = 0; c < R; ++c) {
+          const bool isnull = !(amax != 0.0 && sig[c] * sig[c] > kNullRatio * smax2);
+          if (isnull) {
+            if (cnt == x) dx = c;
+            if (cnt == y) dy = c;
+            ++cnt;
+          }
+        }
+        double acc = (x == y) ? 1.0 : 0.0;
+        for (int c = 0; c < R; ++c) acc -= B[c * R + dx] * B[c * R + dy];
+        EA[e] = acc;
+      }
+      __syncwarp();
+      dev::warp_jacobi_eig(EA, EE, nn, cs, pq, lane);
+      double emin = 1e308;
+      for (int i = 0; i < nn; ++i) emin = fmin(emin, EA[i * nn + i]);
+      if (!(emin > 1e-8)) flag = P2G_FLAG_DEGENERATE;
+      for (int e = lane; e < nn * nn; e += 32) {
+        const int x = e / nn, y = e - (e / nn) * nn;
+        double acc = 0.0;
+        for (int m = 0; m < nn; ++m) {
+          const double ev = fmax(EA[m * nn + m], 1e-300);
+          acc += EE[x * nn + m] * EE[y * nn + m] * rsqrt(ev);
+        }
+        TN[e] = acc;
+      }
+      __syncwarp();
+    }
+    // Q rows (lane = row), then m1_k = Q^T XV D through 32-row chunks.
+    for (int b = 0; b < I; b += 32) {
+      const int i = b + lane;
+      const int nr = min(32, I - b);
+      double xv[RP];
+      double q[RP];
+#pragma unroll
+      for (int r = 0; r < RP; ++r) q[r] = 0.0;
+      if (i < I) {
+        dev::csr_row_times<RP>(xv, a.X.ci, a.X.val, a.X.rp[r0 + i], a.X.rp[r0 + i + 1], a.V, R);
+        // strong part: sum_c U[i][c] Vj[:, c]
+        for (int c = 0; c < R; ++c) {
+          const bool strong_c = amax != 0.0 && sig[c] * sig[c] > kNullRatio * smax2;
+          if (!strong_c) continue;
+          const double u = A[i * R + c];
+#pragma unroll
+          for (int r = 0; r < RP; ++r)
+            if (r < R) q[r] = fma(u, Vj[r * R + c], q[r]);
+        }
+        if (nn > 0) {
+          // N[i][x] = (i<R ? Vn[i][x] : 0) - sum_c U[i][c] B[c][dx]; polar row = N[i] TN
+          double nrow[RP];
+          int cnt = 0;
+          for (int d = 0; d < R; ++d) {
+            const bool isnull = !(amax != 0.0 && sig[d] * sig[d] > kNullRatio * smax2);
+            if (!isnull) continue;
+            double v = (i < R) ? Vj[i * R + d] : 0.0;
+            for (int c = 0; c < R; ++c) v -= A[i * R + c] * B[c * R + d];
+            nrow[cnt < RP ? cnt : RP - 1] = v;
+            ++cnt;
+          }
+          int xi = 0;
+          for (int d = 0; d < R; ++d) {
+            const bool isnull = !(amax != 0.0 && sig[d] * sig[d] > kNullRatio * smax2);
+            if (!isnull) continue;
+            double pn = 0.0;
+            for (int y = 0; y < nn; ++y) pn = fma(nrow[y < RP ? y : RP - 1], TN[y * nn + xi], pn);
+#pragma unroll
+            for (int r = 0; r < RP; ++r)
+              if (r < R) q[r] = fma(pn, Vj[r * R + d], q[r]);
+            ++xi;
+          }
+        }
+      } else {
+#pragma unroll
+        for (int r = 0; r < RP; ++r) xv[r] = 0.0;
+      }
+#pragma unroll
+      for (int r = 0; r < RP; ++r) {
+        qch[lane * RP + r] = q[r];
+        xch[lane * RP + r] = (r < R) ? xv[r] * s[r] : 0.0;
+      }
+      __syncwarp();
+      double* qdst = a.Q + (r0 + b) * R;
+      for (int idx = lane; idx < nr * R; idx += 32) qdst[idx] = qch[(idx / R) * RP + (idx - (idx / R) * R)];
+      for (int e = lane; e < RR; e += 32) {
+        const int x = e / R, y = e - (e / R) * R;
+        double acc = M1[e];
+        for (int rr = 0; rr < nr; ++rr) acc = fma(qch[rr * RP + x], xch[rr * RP + y], acc);
+        M1[e] = acc;
+      }
+      __syncwarp();
+    }
+    if (lane == 0) a.flags[k] = flag;
+    __syncwarp();
+  }
+  __syncthreads();
+  if (wid == 0) {
+    for (int e = lane; e < RR; e += 32) {
+      double acc = 0.0;
+      for (int w = 0; w < WPB; ++w) acc += smem[RP * RP + w * AccSmem<RP>::kPerWarpDoubles + 2 * RP * RP + e];
+      m1_partials_acc[static_cast<std::int64_t>(blockIdx.x) * RR + e] = acc;
+    }
+  }
+}
+
+template <int RP>
+constexpr int k1_wpb() {
+  return RP <= 16 ? 8 : (RP <= 32 ? 4 : 2);
+}
+
+template <int RP>
+int launch_k1(p2g_ctx* c, const K1Args& a, int max_blocks, cudaStream_t s) {
+  constexpr int WPB = k1_wpb<RP>();
+  const std::size_t smem = sizeof(double) * (RP * RP + WPB * K1Smem<RP>::kPerWarpDoubles);
+  auto kern = k_procrustes<RP, WPB>;
+  P2G_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  int per_sm = 0;
+  P2G_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, WPB * 32, smem));
+  per_sm = std::max(per_sm, 1);
+  std::int64_t want = (a.X.K + WPB - 1) / WPB;
+  int blocks = static_cast<int>(std::min<std::int64_t>(want, static_cast<std::int64_t>(per_sm) * c->num_sms));
+  blocks = std::max(1, std::min(blocks, max_blocks));
+  kern<<<blocks, WPB * 32, smem, s>>>(a);
+  P2G_LAUNCHED(1);
+  return blocks;
+}
+
+template <int RP>
+constexpr int acc_wpb() {
+  return RP <= 16 ? 4 : (RP <= 32 ? 2 : 1);
+}
+
+template <int RP>
+int acc_blocks(const p2g_ctx* c) {
+  return std::max(1, c->num_sms * 2);
+}
+
+template <int RP>
+void launch_acc(p2g_ctx* c, const K1Args& a, double* m1p, cudaStream_t s) {
+  constexpr int WPB = acc_wpb<RP>();
+  const std::size_t smem = sizeof(double) * (RP * RP + WPB * AccSmem<RP>::kPerWarpDoubles);
+  auto kern = k_procrustes_accurate<RP, WPB>;
+  P2G_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  kern<<<acc_blocks<RP>(c), WPB * 32, smem, s>>>(a, m1p);
+  P2G_LAUNCHED(1);
+}
+
+}  // namespace
+
+#define P2G_RP_DISPATCH(R, CALL)                         \
+  do {                                                   \
+    if ((R) <= 2) {                                      \
+      constexpr int RP_ = 2;                             \
+      CALL;                                              \
+    } else if ((R) <= 4) {                               \
+      constexpr int RP_ = 4;                             \
+      CALL;                                              \
+    } else if ((R) <= 5) {                               \
+      constexpr int RP_ = 5;                             \
+      CALL;                                              \
+    } else if ((R) <= 8) {                               \
+      constexpr int RP_ = 8;                             \
+      CALL;                                              \
+    } else if ((R) <= 10) {                              \
+      constexpr int RP_ = 10;                            \
+      CALL;                                              \
+    } else if ((R) <= 16) {                              \
+      constexpr int RP_ = 16;                            \
+      CALL;                                              \
+    } else if ((R) <= 24) {                              \
+      constexpr int RP_ = 24;                            \
+      CALL;                                              \
+    } else if ((R) <= 32) {                              \
+      constexpr int RP_ = 32;                            \
+      CALL;                                              \
+    } else if ((R) <= 40) {                              \
+      constexpr int RP_ = 40;                            \
+      CALL;                                              \
+    } else {                                             \
+      throw InvalidArgument("rank above 40 unsupported"); \
+    }                                                    \
+  } while (0)
+
+int launch_procrustes(p2g_ctx* c, int R, const double* H, const double* V, const double* W, double* Q,
+                      std::int32_t* flags, double* m1_partials, int max_blocks, cudaStream_t s) {
+  K1Args a{};
+  a.X = ShardArgs{c->srp.get(), c->rp.get(), c->ci.get(), c->val.get(), c->k_end - c->k_begin, c->NR, c->nnz, c->J};
+  a.R = R;
+  a.H = H;
+  a.V = V;
+  a.W = W;
+  a.Q = Q;
+  a.flags = flags;
+  a.m1_partials = m1_partials;
+  a.counters = c->counters.get();
+  int blocks = 0;
+  P2G_RP_DISPATCH(R, blocks = launch_k1<RP_>(c, a, max_blocks, s));
+  return blocks;
+}
+
+int launch_procrustes_accurate(p2g_ctx* c, int R, const double* H, const double* V, const double* W, double* Q,
+                               std::int32_t* flags, double* m1_partials, cudaStream_t s) {
+  K1Args a{};
+  a.X = ShardArgs{c->srp.get(), c->rp.get(), c->ci.get(), c->val.get(), c->k_end - c->k_begin, c->NR, c->nnz, c->J};
+  a.R = R;
+  a.H = H;
+  a.V = V;
+  a.W = W;
+  a.Q = Q;
+  a.flags = flags;
+  a.max_rows = c->max_rows;
+  a.counters = c->counters.get();
+  int blocks = 0, wpb = 1;
+  P2G_RP_DISPATCH(R, (blocks = acc_blocks<RP_>(c), wpb = acc_wpb<RP_>()));
+  // Per-warp scratch slabs holding A (I_max x R) of the subject in flight.
+  c->acc_scratch.resize(static_cast<std::size_t>(blocks) * wpb * static_cast<std::size_t>(c->max_rows) * R);
+  a.scratch = c->acc_scratch.get();
+  P2G_RP_DISPATCH(R, launch_acc<RP_>(c, a, m1_partials, s));
+  return blocks;
+}
+
+int procrustes_accurate_blocks(p2g_ctx* c, int R) {
+  int blocks = 0;
+  P2G_RP_DISPATCH(R, blocks = acc_blocks<RP_>(c));
+  return blocks;
+}
+
+}  // namespace p2g

@@ -1,0 +1,967 @@
+// C-ABI implementation (include/p2g.h): device context, CSR upload and
+// sharding, the fused PARAFAC2-ALS loop (fit_parafac2, solver.hpp:251-321)
+// and the per-step parity hooks.
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <limits>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "p2g_ctx.hpp"
+
+namespace p2g {
+
+void partition_weighted(const std::uint64_t* w, std::int64_t n, std::int32_t n_chunks,
+                        std::vector<std::pair<std::int64_t, std::int64_t>>& out);
+
+// ---------------------------------------------------------------------------
+// NCCL, loaded lazily (dlopen) so a process that already has torch's NCCL
+// reuses it and a single-GPU context never touches NCCL.
+// ---------------------------------------------------------------------------
+struct NcclApi {
+  void* h = nullptr;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+static NcclApi& nccl_api() {
+  static NcclApi api;
+  if (!api.h) {
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) throw CudaError("NCCL unavailable: cannot dlopen libnccl.so.2");
+    api.GetUniqueId = reinterpret_cast<decltype(api.GetUniqueId)>(dlsym(h, "ncclGetUniqueId"));
+    api.CommInitRank = reinterpret_cast<decltype(api.CommInitRank)>(dlsym(h, "ncclCommInitRank"));
+    api.AllReduce = reinterpret_cast<decltype(api.AllReduce)>(dlsym(h, "ncclAllReduce"));
+    api.CommDestroy = reinterpret_cast<decltype(api.CommDestroy)>(dlsym(h, "ncclCommDestroy"));
+    api.GetErrorString = reinterpret_cast<decltype(api.GetErrorString)>(dlsym(h, "ncclGetErrorString"));
+    if (!api.GetUniqueId || !api.CommInitRank || !api.AllReduce || !api.CommDestroy)
+      throw CudaError("NCCL unavailable: missing symbols");
+    api.h = h;
+  }
+  return api;
+}
+
+struct NcclState {
+  ncclComm_t comm = nullptr;
+};
+
+static void nccl_check(ncclResult_t r, const char* what) {
+  if (r != ncclSuccess)
+    throw CudaError(std::string("NCCL ") + what + " failed: " +
+                    (nccl_api().GetErrorString ? nccl_api().GetErrorString(r) : "?"));
+}
+
+/// Sum-allreduce of fp64 partials in place (no-op on one rank).  The only
+/// collectives of an iteration: M1 (R x R), M2 (J x R), [gram(W), cross].
+static void allreduce(p2g_ctx* c, double* buf, std::size_t count) {
+  if (c->world <= 1 || count == 0) return;
+  nccl_check(nccl_api().AllReduce(buf, buf, count, ncclFloat64, ncclSum, c->nccl->comm, c->stream), "allreduce");
+}
+
+DBuf<double>& scratch_partials(p2g_ctx* c, std::size_t count) {
+  c->partials.resize(count);
+  return c->partials;
+}
+
+namespace {
+
+// ---- timing helpers --------------------------------------------------------
+struct Phase {
+  p2g_ctx* c;
+  std::string name;
+  std::size_t ev0 = 0;
+  Phase(p2g_ctx* ctx, const char* n) : c(ctx), name(n) {
+    if (!c->timing) return;
+    ev0 = next_event();
+    P2G_CUDA(cudaEventRecord(c->ev_pool[ev0], c->stream));
+  }
+  ~Phase() noexcept(false) {
+    if (!c->timing) return;
+    const std::size_t ev1 = next_event();
+    P2G_CUDA(cudaEventRecord(c->ev_pool[ev1], c->stream));
+    c->pending.push_back({name, {ev0, ev1}});
+  }
+  std::size_t next_event() {
+    if (c->ev_used == c->ev_pool.size()) {
+      cudaEvent_t e;
+      P2G_CUDA(cudaEventCreate(&e));
+      c->ev_pool.push_back(e);
+    }
+    return c->ev_used++;
+  }
+};
+
+void collect_timing(p2g_ctx* c) {
+  if (!c->timing) return;
+  for (auto& p : c->pending) {
+    float ms = 0.f;
+    P2G_CUDA(cudaEventElapsedTime(&ms, c->ev_pool[p.second.first], c->ev_pool[p.second.second]));
+    auto& slot = c->timer.acc[p.first];
+    slot.first += ms;
+    slot.second += 1;
+  }
+  c->pending.clear();
+  c->ev_used = 0;
+}
+
+void require_loaded(const p2g_ctx* c) {
+  if (!c) throw InvalidArgument("null context");
+  if (!c->loaded) throw InvalidArgument("no tensor loaded (call p2g_load_csr first)");
+}
+
+void set_device(const p2g_ctx* c) { P2G_CUDA(cudaSetDevice(c->device)); }
+
+std::int64_t Ks(const p2g_ctx* c) { return c->k_end - c->k_begin; }
+
+/// Host column-major (rows x cols) -> device row-major.
+void upload_colmajor(p2g_ctx* c, const double* host, std::int64_t rows, std::int64_t cols, double* dev) {
+  c->stage.resize(static_cast<std::size_t>(rows * cols));
+  P2G_CUDA(cudaMemcpyAsync(c->stage.get(), host, sizeof(double) * rows * cols, cudaMemcpyHostToDevice, c->stream));
+  launch_transpose(c->stage.get(), dev, rows, cols, c->stream);
+}
+
+/// Host column-major (K_total x R) -> device row-major shard rows.
+void upload_shard_rows(p2g_ctx* c, const double* host, std::int64_t total_rows, int R, double* dev) {
+  const std::int64_t n = Ks(c);
+  c->stage.resize(static_cast<std::size_t>(n * R));
+  for (int r = 0; r < R; ++r)
+    P2G_CUDA(cudaMemcpyAsync(c->stage.get() + static_cast<std::int64_t>(r) * n, host + r * total_rows + c->k_begin,
+                             sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
+  launch_transpose(c->stage.get(), dev, n, R, c->stream);
+}
+
+/// Device row-major (rows x cols) -> host column-major.
+void download_colmajor(p2g_ctx* c, const double* dev, std::int64_t rows, std::int64_t cols, double* host) {
+  std::vector<double> tmp(static_cast<std::size_t>(rows * cols));
+  P2G_CUDA(cudaMemcpyAsync(tmp.data(), dev, sizeof(double) * rows * cols, cudaMemcpyDeviceToHost, c->stream));
+  P2G_CUDA(cudaStreamSynchronize(c->stream));
+  for (std::int64_t i = 0; i < rows; ++i)
+    for (std::int64_t j = 0; j < cols; ++j) host[i + j * rows] = tmp[static_cast<std::size_t>(i * cols + j)];
+}
+
+void check_finite_host(const double* a, std::int64_t n, const char* what) {
+  for (std::int64_t i = 0; i < n; ++i)
+    if (!std::isfinite(a[i])) throw NumericalError(std::string(what) + ": non-finite entries");
+}
+
+/// Config validation of initialize() (solver.hpp:106-122).
+void validate_fit(const p2g_ctx* c, const p2g_fit_config* cfg) {
+  const int R = cfg->rank;
+  if (R < 1) throw InvalidArgument("rank must be at least 1");
+  if (!(cfg->tol > 0.0)) throw InvalidArgument("convergence tolerance must be positive");
+  if (cfg->max_iters < 1) throw InvalidArgument("iteration limit must be at least 1");
+  if (R > 40) throw InvalidArgument("rank above 40 unsupported on device");
+  if (c->J < R) throw DataError("rank exceeds variables: J = " + std::to_string(c->J) + " < rank " + std::to_string(R));
+  for (std::int64_t k = 0; k < c->K_total; ++k) {
+    const std::int64_t I = c->srp_host[static_cast<std::size_t>(k + 1)] - c->srp_host[static_cast<std::size_t>(k)];
+    if (I < R)
+      throw DataError("rank exceeds observations for subject " + std::to_string(k) + ": I_k = " + std::to_string(I) +
+                      " < rank " + std::to_string(R));
+  }
+  if (cfg->init != 0 && cfg->init != 2) throw InvalidArgument("init must be 0 (random) or 2 (explicit factors)");
+}
+
+void alloc_state(p2g_ctx* c, int R) {
+  const std::size_t RR = static_cast<std::size_t>(R) * R;
+  c->R = R;
+  c->H.resize(RR);
+  c->V.resize(static_cast<std::size_t>(c->J) * R);
+  c->W.resize(static_cast<std::size_t>(std::max<std::int64_t>(Ks(c), 1)) * R);
+  c->Q.resize(static_cast<std::size_t>(std::max<std::int64_t>(c->NR, 1)) * R);
+  c->gramW.resize(RR);
+  c->gramV.resize(RR);
+  c->gramH.resize(RR);
+  c->gvraw.resize(RR);
+  c->gwc.resize(RR + 1);
+  c->nH.resize(R);
+  c->nV.resize(R);
+  c->m1.resize(RR);
+  c->M2.resize(static_cast<std::size_t>(c->J) * R);
+  c->m3.resize(static_cast<std::size_t>(std::max<std::int64_t>(Ks(c), 1)) * R);
+  c->G1.resize(RR);
+  c->G2.resize(RR);
+  c->G3.resize(RR);
+  c->pinvbuf.resize(RR);
+  c->scal.resize(8);
+  c->flags.resize(static_cast<std::size_t>(std::max<std::int64_t>(Ks(c), 1)));
+  c->counters.resize(8);
+}
+
+constexpr int kMaxPartials = 148 * 8;
+
+/// gram(W) and the cross term over this shard, allreduced -> c->gwc.
+void gram_w_cross(p2g_ctx* c, const double* m3_or_null) {
+  const int R = c->R;
+  const std::size_t RR = static_cast<std::size_t>(R) * R;
+  DBuf<double>& part = scratch_partials(c, kMaxPartials * (RR + 1));
+  const int np = gram_partials(R, Ks(c), c->W.get(), m3_or_null, part.get(), kMaxPartials, c->stream);
+  reduce_partials(part.get(), np, static_cast<std::int64_t>(RR + 1), c->gwc.get(), c->stream);
+  allreduce(c, c->gwc.get(), RR + 1);
+}
+
+/// gram(V) (replicated, no collective) -> c->gramV.
+void gram_v(p2g_ctx* c, double* out) {
+  const int R = c->R;
+  const std::size_t RR = static_cast<std::size_t>(R) * R;
+  DBuf<double>& part = scratch_partials(c, kMaxPartials * (RR + 1));
+  const int np = gram_partials(R, c->J, c->V.get(), nullptr, part.get(), 148, c->stream);
+  // partial stride is RR+1; reduce the first RR entries of each via a strided copy
+  reduce_partials(part.get(), np, static_cast<std::int64_t>(RR + 1), c->gwc.get(), c->stream);
+  P2G_CUDA(cudaMemcpyAsync(out, c->gwc.get(), sizeof(double) * RR, cudaMemcpyDeviceToDevice, c->stream));
+}
+
+/// Initial state: H, V (J x R), W (shard) on device plus gram(W), gram(V).
+void init_state(p2g_ctx* c, const p2g_fit_config* cfg, const double* H0, const double* V0, const double* W0) {
+  const int R = cfg->rank;
+  alloc_state(c, R);
+  if (cfg->init == 2) {
+    if (!H0 || !V0 || !W0) throw InvalidArgument("explicit init needs H0, V0 and W0");
+    upload_colmajor(c, H0, R, R, c->H.get());
+    upload_colmajor(c, V0, c->J, R, c->V.get());
+    upload_shard_rows(c, W0, c->K_total, R, c->W.get());
+  } else {
+    // solver.hpp:124-132: H = I, S = ones, V = Rng(seed).uniform() r-outer j-inner.
+    std::vector<double> h(static_cast<std::size_t>(R) * R), v(static_cast<std::size_t>(c->J) * R);
+    if (p2g_initialize_random(cfg->seed, c->K_total, c->J, R, h.data(), nullptr, v.data()) != P2G_OK)
+      throw InvalidArgument(p2g_last_error());
+    upload_colmajor(c, h.data(), R, R, c->H.get());
+    upload_colmajor(c, v.data(), c->J, R, c->V.get());
+    launch_fill(c->W.get(), Ks(c) * R, 1.0, c->stream);
+  }
+  gram_v(c, c->gramV.get());
+  gram_w_cross(c, nullptr);
+  P2G_CUDA(cudaMemcpyAsync(c->gramW.get(), c->gwc.get(), sizeof(double) * R * R, cudaMemcpyDeviceToDevice, c->stream));
+  c->state_valid = true;
+}
+
+struct IterOut {
+  double fit, resid;
+};
+
+/// One PARAFAC2-ALS iteration on device (solver.hpp:274-306).
+IterOut iterate(p2g_ctx* c, bool nonneg, int iter) {
+  const int R = c->R;
+  const std::size_t RR = static_cast<std::size_t>(R) * R;
+  cudaStream_t s = c->stream;
+  P2G_CUDA(cudaMemsetAsync(c->counters.get(), 0, sizeof(std::int32_t) * 8, s));
+  int n1 = 0, n2 = 0;
+  {
+    DBuf<double>& part = scratch_partials(c, static_cast<std::size_t>(kMaxPartials + 4 * 148) * RR);
+    {
+      Phase ph(c, "procrustes");
+      n1 = launch_procrustes(c, R, c->H.get(), c->V.get(), c->W.get(), c->Q.get(), c->flags.get(), part.get(),
+                             kMaxPartials, s);
+    }
+    {
+      Phase ph(c, "procrustes_accurate");
+      n2 = launch_procrustes_accurate(c, R, c->H.get(), c->V.get(), c->W.get(), c->Q.get(), c->flags.get(),
+                                      part.get() + static_cast<std::size_t>(n1) * RR, s);
+    }
+    Phase ph(c, "m1_reduce");
+    reduce_partials(part.get(), n1 + n2, static_cast<std::int64_t>(RR), c->m1.get(), s);
+    allreduce(c, c->m1.get(), RR);
+  }
+  {
+    Phase ph(c, "solve_h");
+    launch_solve_h(R, c->m1.get(), c->gramW.get(), c->gramV.get(), c->H.get(), c->nH.get(), c->gramH.get(),
+                   c->G2.get(), s);
+  }
+  {
+    Phase ph(c, "mode2");
+    launch_mode2(c, R, c->Q.get(), c->H.get(), c->W.get(), c->nH.get(), c->M2.get(), s);
+    allreduce(c, c->M2.get(), static_cast<std::size_t>(c->J) * R);
+  }
+  {
+    Phase ph(c, "update_v");
+    if (nonneg) {
+      launch_nnls_rows(R, c->J, c->G2.get(), c->M2.get(), c->V.get(), 0, c->counters.get() + 1, s);
+    } else {
+      launch_pinv(R, c->G2.get(), c->pinvbuf.get(), s);
+      launch_rows_times(R, c->J, c->M2.get(), c->pinvbuf.get(), c->V.get(), s);
+    }
+    gram_v(c, c->gvraw.get());
+    launch_normalize_v(R, c->J, c->V.get(), c->gvraw.get(), c->gramV.get(), c->nV.get(), c->gramH.get(), c->G3.get(),
+                       s);
+  }
+  {
+    Phase ph(c, "mode3");
+    launch_mode3(c, R, c->Q.get(), c->H.get(), c->V.get(), c->m3.get(), s);
+  }
+  {
+    Phase ph(c, "update_w");
+    if (nonneg) {
+      launch_nnls_rows(R, Ks(c), c->G3.get(), c->m3.get(), c->W.get(), 0, c->counters.get() + 1, s);
+    } else {
+      launch_pinv(R, c->G3.get(), c->pinvbuf.get(), s);
+      launch_rows_times(R, Ks(c), c->m3.get(), c->pinvbuf.get(), c->W.get(), s);
+    }
+  }
+  {
+    Phase ph(c, "fit");
+    gram_w_cross(c, c->m3.get());
+    launch_fit(R, c->gwc.get(), c->gramH.get(), c->gramV.get(), c->norm_x, c->gramW.get(), c->scal.get(), s);
+  }
+  // One host sync per iteration: fit scalars + error counters.
+  P2G_CUDA(cudaMemcpyAsync(c->pinned, c->scal.get(), sizeof(double) * 4, cudaMemcpyDeviceToHost, s));
+  P2G_CUDA(cudaMemcpyAsync(c->pinned + 4, c->counters.get(), sizeof(std::int32_t) * 8, cudaMemcpyDeviceToHost, s));
+  P2G_CUDA(cudaStreamSynchronize(s));
+  collect_timing(c);
+  const std::int32_t* cnt = reinterpret_cast<const std::int32_t*>(c->pinned + 4);
+  if (cnt[2] > 0) throw NumericalError("svd operand: non-finite entries");
+  if (cnt[1] > 0) throw NumericalError("NNLS did not converge");
+  IterOut o{c->pinned[0], c->pinned[1]};
+  if (!std::isfinite(o.fit) || !std::isfinite(o.resid))
+    throw NumericalError("numerical divergence at iteration " + std::to_string(iter));
+  return o;
+}
+
+}  // namespace
+}  // namespace p2g
+
+using namespace p2g;
+
+// ---------------------------------------------------------------------------
+// Context
+// ---------------------------------------------------------------------------
+extern "C" int p2g_nccl_unique_id(char out_id[128]) {
+  return guarded([&] {
+    ncclUniqueId id;
+    nccl_check(nccl_api().GetUniqueId(&id), "get unique id");
+    static_assert(sizeof(ncclUniqueId) == 128, "unexpected NCCL id size");
+    std::memcpy(out_id, &id, 128);
+  });
+}
+
+extern "C" int p2g_create(int32_t device, int32_t rank, int32_t world, const char* nccl_id, p2g_ctx** out) {
+  return guarded([&] {
+    if (!out) throw InvalidArgument("null output");
+    if (world < 1 || rank < 0 || rank >= world) throw InvalidArgument("bad rank/world");
+    int ndev = 0;
+    cudaError_t e = cudaGetDeviceCount(&ndev);
+    if (e != cudaSuccess || ndev == 0) throw CudaError("no CUDA device available (the GPU path has no CPU fallback)");
+    if (device < 0 || device >= ndev) throw InvalidArgument("device ordinal out of range");
+    auto c = std::make_unique<p2g_ctx>();
+    c->device = device;
+    c->rank = rank;
+    c->world = world;
+    P2G_CUDA(cudaSetDevice(device));
+    cudaDeviceProp prop;
+    P2G_CUDA(cudaGetDeviceProperties(&prop, device));
+    if (prop.major < 10) throw CudaError("libp2g is built for sm_100a (B200); found sm_" + std::to_string(prop.major) + std::to_string(prop.minor));
+    c->num_sms = prop.multiProcessorCount;
+    P2G_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    P2G_CUDA(cudaMallocHost(&c->pinned, 64 * sizeof(double)));
+    if (world > 1) {
+      if (!nccl_id) throw InvalidArgument("world > 1 needs an NCCL unique id");
+      ncclUniqueId id;
+      std::memcpy(&id, nccl_id, 128);
+      c->nccl = new NcclState();
+      nccl_check(nccl_api().CommInitRank(&c->nccl->comm, world, id, rank), "comm init");
+    }
+    *out = c.release();
+  });
+}
+
+extern "C" int p2g_destroy(p2g_ctx* c) {
+  return guarded([&] {
+    if (!c) return;
+    cudaSetDevice(c->device);
+    if (c->nccl) {
+      if (c->nccl->comm) nccl_api().CommDestroy(c->nccl->comm);
+      delete c->nccl;
+    }
+    for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
+    if (c->pinned) cudaFreeHost(c->pinned);
+    if (c->stream) cudaStreamDestroy(c->stream);
+    delete c;
+  });
+}
+
+extern "C" int p2g_load_csr(p2g_ctx* c, int64_t K, int64_t J, const int64_t* srp, const int64_t* rp,
+                            const int32_t* ci, const double* val) {
+  return guarded([&] {
+    if (!c) throw InvalidArgument("null context");
+    set_device(c);
+    // IrregularTensor::from_slices (sparse.hpp:176-193) validation.
+    if (J <= 0) throw DataError("tensor must have at least one column");
+    if (K <= 0) throw DataError("tensor must have at least one slice");
+    if (!srp || !rp) throw InvalidArgument("null CSR arrays");
+    if (srp[0] != 0) throw DataError("subj_row_ptr must start at 0");
+    for (int64_t k = 0; k < K; ++k)
+      if (srp[k + 1] < srp[k]) throw DataError("subj_row_ptr must be non-decreasing");
+    const int64_t NRt = srp[K];
+    if (rp[0] != 0) throw DataError("row_ptr must start at 0");
+    for (int64_t r = 0; r < NRt; ++r)
+      if (rp[r + 1] < rp[r]) throw DataError("row_ptr must be non-decreasing");
+    const int64_t nnz_t = rp[NRt];
+    if (nnz_t > 0 && (!ci || !val)) throw InvalidArgument("null CSR arrays");
+    // Column range / ascending order within rows; non-zero values.
+    for (int64_t r = 0; r < NRt; ++r)
+      for (int64_t p = rp[r]; p < rp[r + 1]; ++p) {
+        if (ci[p] < 0 || ci[p] >= J) throw DataError("column index out of range");
+        if (p > rp[r] && ci[p] <= ci[p - 1]) throw DataError("column indices must be strictly ascending within a row");
+      }
+    // Shard by partition_weighted(nnz_k + I_k, world) (solver.hpp:263-267).
+    std::vector<std::uint64_t> w(static_cast<std::size_t>(K));
+    for (int64_t k = 0; k < K; ++k)
+      w[static_cast<std::size_t>(k)] =
+          static_cast<std::uint64_t>(rp[srp[k + 1]] - rp[srp[k]]) + static_cast<std::uint64_t>(srp[k + 1] - srp[k]);
+    std::vector<std::pair<std::int64_t, std::int64_t>> parts;
+    partition_weighted(w.data(), K, c->world, parts);
+    if (static_cast<int>(parts.size()) != c->world) throw DataError("fewer subjects than ranks");
+    c->K_total = K;
+    c->J = J;
+    c->k_begin = parts[static_cast<std::size_t>(c->rank)].first;
+    c->k_end = parts[static_cast<std::size_t>(c->rank)].second;
+    c->srp_host.assign(srp, srp + K + 1);
+    const int64_t row0 = srp[c->k_begin], row1 = srp[c->k_end];
+    const int64_t nz0 = rp[row0], nz1 = rp[row1];
+    c->NR = row1 - row0;
+    c->nnz = nz1 - nz0;
+    c->nnz_total = nnz_t;
+    c->max_rows = 0;
+    for (int64_t k = c->k_begin; k < c->k_end; ++k) c->max_rows = std::max<std::int64_t>(c->max_rows, srp[k + 1] - srp[k]);
+    std::vector<std::int64_t> srp_s(static_cast<std::size_t>(c->k_end - c->k_begin + 1));
+    for (int64_t k = c->k_begin; k <= c->k_end; ++k) srp_s[static_cast<std::size_t>(k - c->k_begin)] = srp[k] - row0;
+    std::vector<std::int64_t> rp_s(static_cast<std::size_t>(c->NR + 1));
+    for (int64_t r = row0; r <= row1; ++r) rp_s[static_cast<std::size_t>(r - row0)] = rp[r] - nz0;
+    c->srp.resize(srp_s.size());
+    c->rp.resize(rp_s.size());
+    c->ci.resize(static_cast<std::size_t>(std::max<int64_t>(c->nnz, 1)));
+    c->val.resize(static_cast<std::size_t>(std::max<int64_t>(c->nnz, 1)));
+    P2G_CUDA(cudaMemcpyAsync(c->srp.get(), srp_s.data(), sizeof(int64_t) * srp_s.size(), cudaMemcpyHostToDevice, c->stream));
+    P2G_CUDA(cudaMemcpyAsync(c->rp.get(), rp_s.data(), sizeof(int64_t) * rp_s.size(), cudaMemcpyHostToDevice, c->stream));
+    if (c->nnz > 0) {
+      P2G_CUDA(cudaMemcpyAsync(c->ci.get(), ci + nz0, sizeof(int32_t) * c->nnz, cudaMemcpyHostToDevice, c->stream));
+      P2G_CUDA(cudaMemcpyAsync(c->val.get(), val + nz0, sizeof(double) * c->nnz, cudaMemcpyHostToDevice, c->stream));
+    }
+    // ||X||_F^2 (sparse.hpp:219-223): slice order then entry order over all
+    // subjects; the full host tensor is available on every rank.
+    double acc = 0.0;
+    for (int64_t p = 0; p < nnz_t; ++p) acc += val[p] * val[p];
+    c->norm_x = acc;
+    P2G_CUDA(cudaStreamSynchronize(c->stream));
+    c->loaded = true;
+    c->state_valid = false;
+  });
+}
+
+extern "C" int p2g_shard_info(const p2g_ctx* c, int64_t* k_begin, int64_t* k_end, int64_t* n_rows, int64_t* nnz) {
+  return guarded([&] {
+    require_loaded(c);
+    if (k_begin) *k_begin = c->k_begin;
+    if (k_end) *k_end = c->k_end;
+    if (n_rows) *n_rows = c->NR;
+    if (nnz) *nnz = c->nnz;
+  });
+}
+
+// ---------------------------------------------------------------------------
+// Fused loop
+// ---------------------------------------------------------------------------
+extern "C" int p2g_fit(p2g_ctx* c, const p2g_fit_config* cfg, const double* H0, const double* V0, const double* W0,
+                       double* H_out, double* V_out, double* W_out, double* Q_out, int32_t* flags_out,
+                       double* fit_trace, double* resid_trace, double* ms_trace, p2g_fit_summary* summary) {
+  return guarded([&] {
+    require_loaded(c);
+    if (!cfg) throw InvalidArgument("null config");
+    set_device(c);
+    const auto t_start = std::chrono::steady_clock::now();
+    validate_fit(c, cfg);
+    if (!(c->norm_x > 0.0)) throw DataError("tensor has no non-zero entries");
+    init_state(c, cfg, H0, V0, W0);
+    double prev_fit = 0.0;
+    int iters = 0;
+    bool converged = false;
+    for (int it = 1; it <= cfg->max_iters; ++it) {
+      const auto t0 = std::chrono::steady_clock::now();
+      const IterOut o = iterate(c, cfg->nonneg != 0, it);
+      ++iters;
+      if (fit_trace) fit_trace[it - 1] = o.fit;
+      if (resid_trace) resid_trace[it - 1] = o.resid;
+      if (ms_trace)
+        ms_trace[it - 1] = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+      const double change = std::abs(o.fit - prev_fit) / std::max(prev_fit, std::numeric_limits<double>::epsilon());
+      prev_fit = o.fit;
+      if (change < cfg->tol) {
+        converged = true;
+        break;
+      }
+    }
+    const int R = cfg->rank;
+    if (H_out) download_colmajor(c, c->H.get(), R, R, H_out);
+    if (V_out) download_colmajor(c, c->V.get(), c->J, R, V_out);
+    if (W_out) download_colmajor(c, c->W.get(), Ks(c), R, W_out);
+    if (Q_out)
+      P2G_CUDA(cudaMemcpyAsync(Q_out, c->Q.get(), sizeof(double) * c->NR * R, cudaMemcpyDeviceToHost, c->stream));
+    if (flags_out)
+      P2G_CUDA(cudaMemcpyAsync(flags_out, c->flags.get(), sizeof(int32_t) * Ks(c), cudaMemcpyDeviceToHost, c->stream));
+    P2G_CUDA(cudaStreamSynchronize(c->stream));
+    if (summary) {
+      summary->iterations = iters;
+      summary->converged = converged ? 1 : 0;
+      summary->norm_x = c->norm_x;
+      summary->total_ms =
+          std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count();
+    }
+  });
+}
+
+extern "C" int p2g_bench_iterations(p2g_ctx* c, const p2g_fit_config* cfg, const double* H0, const double* V0,
+                                    const double* W0, int32_t reset, int32_t iters, double* ms_per_iter,
+                                    double* fit_trace) {
+  return guarded([&] {
+    require_loaded(c);
+    if (!cfg) throw InvalidArgument("null config");
+    set_device(c);
+    if (reset || !c->state_valid || c->R != cfg->rank) {
+      validate_fit(c, cfg);
+      if (!(c->norm_x > 0.0)) throw DataError("tensor has no non-zero entries");
+      init_state(c, cfg, H0, V0, W0);
+    }
+    c->timer.acc.clear();  // per-call kernel times (the timed steps only)
+    c->timing = true;
+    cudaEvent_t e0, e1;
+    P2G_CUDA(cudaEventCreate(&e0));
+    P2G_CUDA(cudaEventCreate(&e1));
+    try {
+      for (int it = 0; it < iters; ++it) {
+        P2G_CUDA(cudaEventRecord(e0, c->stream));
+        const IterOut o = iterate(c, cfg->nonneg != 0, it + 1);
+        P2G_CUDA(cudaEventRecord(e1, c->stream));
+        P2G_CUDA(cudaEventSynchronize(e1));
+        float ms = 0.f;
+        P2G_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+        double msd = ms;
+        if (c->world > 1) {  // max over ranks
+          c->scal.resize(8);
+          P2G_CUDA(cudaMemcpyAsync(c->scal.get() + 6, &msd, sizeof(double), cudaMemcpyHostToDevice, c->stream));
+          nccl_check(nccl_api().AllReduce(c->scal.get() + 6, c->scal.get() + 6, 1, ncclFloat64, ncclMax,
+                                          c->nccl->comm, c->stream),
+                     "allreduce max");
+          P2G_CUDA(cudaMemcpyAsync(&msd, c->scal.get() + 6, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+          P2G_CUDA(cudaStreamSynchronize(c->stream));
+        }
+        if (ms_per_iter) ms_per_iter[it] = msd;
+        if (fit_trace) fit_trace[it] = o.fit;
+      }
+    } catch (...) {
+      c->timing = false;
+      cudaEventDestroy(e0);
+      cudaEventDestroy(e1);
+      throw;
+    }
+    c->timing = false;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+  });
+}
+
+extern "C" int64_t p2g_launch_count(void) { return launch_counter().load(); }
+
+extern "C" int p2g_kernel_times(const p2g_ctx* c, int32_t max_entries, char* names, double* ms_per_launch,
+                                int64_t* launches, int32_t* n_out) {
+  return guarded([&] {
+    if (!c) throw InvalidArgument("null context");
+    int n = 0;
+    for (const auto& kv : c->timer.acc) {
+      if (n >= max_entries) break;
+      std::memset(names + 32 * n, 0, 32);
+      std::strncpy(names + 32 * n, kv.first.c_str(), 31);
+      ms_per_launch[n] = kv.second.second ? kv.second.first / kv.second.second : 0.0;
+      launches[n] = kv.second.second;
+      ++n;
+    }
+    *n_out = n;
+  });
+}
+
+// ---------------------------------------------------------------------------
+// Per-step hooks
+// ---------------------------------------------------------------------------
+extern "C" int p2g_procrustes(p2g_ctx* c, int32_t R, const double* H, const double* V, const double* W,
+                              double* Q_out, int32_t* flags_out, double* m1_out) {
+  return guarded([&] {
+    require_loaded(c);
+    set_device(c);
+    if (R < 1 || R > 40) throw InvalidArgument("rank out of range");
+    if (!H || !V || !W) throw InvalidArgument("null factor");
+    for (int64_t k = c->k_begin; k < c->k_end; ++k)
+      if (c->srp_host[static_cast<std::size_t>(k + 1)] - c->srp_host[static_cast<std::size_t>(k)] < R)
+        throw InvalidArgument("rank exceeds observations in procrustes step");
+    alloc_state(c, R);
+    upload_colmajor(c, H, R, R, c->H.get());
+    upload_colmajor(c, V, c->J, R, c->V.get());
+    upload_shard_rows(c, W, c->K_total, R, c->W.get());
+    const std::size_t RR = static_cast<std::size_t>(R) * R;
+    P2G_CUDA(cudaMemsetAsync(c->counters.get(), 0, sizeof(std::int32_t) * 8, c->stream));
+    DBuf<double>& part = scratch_partials(c, static_cast<std::size_t>(kMaxPartials + 4 * 148) * RR);
+    const int n1 = launch_procrustes(c, R, c->H.get(), c->V.get(), c->W.get(), c->Q.get(), c->flags.get(), part.get(),
+                                     kMaxPartials, c->stream);
+    const int n2 = launch_procrustes_accurate(c, R, c->H.get(), c->V.get(), c->W.get(), c->Q.get(), c->flags.get(),
+                                              part.get() + static_cast<std::size_t>(n1) * RR, c->stream);
+    reduce_partials(part.get(), n1 + n2, static_cast<std::int64_t>(RR), c->m1.get(), c->stream);
+    allreduce(c, c->m1.get(), RR);
+    std::int32_t cnt[8];
+    P2G_CUDA(cudaMemcpyAsync(cnt, c->counters.get(), sizeof(cnt), cudaMemcpyDeviceToHost, c->stream));
+    P2G_CUDA(cudaStreamSynchronize(c->stream));
+    if (cnt[2] > 0) throw NumericalError("svd operand: non-finite entries");
+    if (Q_out) P2G_CUDA(cudaMemcpy(Q_out, c->Q.get(), sizeof(double) * c->NR * R, cudaMemcpyDeviceToHost));
+    if (flags_out) P2G_CUDA(cudaMemcpy(flags_out, c->flags.get(), sizeof(int32_t) * Ks(c), cudaMemcpyDeviceToHost));
+    if (m1_out) download_colmajor(c, c->m1.get(), R, R, m1_out);
+    c->state_valid = false;
+  });
+}
+
+extern "C" int p2g_mttkrp_q(p2g_ctx* c, int32_t mode, int32_t R, const double* Q, const double* H, const double* V,
+                            const double* W, double* out) {
+  return guarded([&] {
+    require_loaded(c);
+    set_device(c);
+    if (mode < 1 || mode > 3) throw InvalidArgument("mttkrp: mode must be 1, 2 or 3");
+    if (R < 1 || R > 40) throw InvalidArgument("rank out of range");
+    if (!Q || !H || !V || !W || !out) throw InvalidArgument("null argument");
+    alloc_state(c, R);
+    P2G_CUDA(cudaMemcpyAsync(c->Q.get(), Q, sizeof(double) * c->NR * R, cudaMemcpyHostToDevice, c->stream));
+    upload_colmajor(c, H, R, R, c->H.get());
+    upload_colmajor(c, V, c->J, R, c->V.get());
+    upload_shard_rows(c, W, c->K_total, R, c->W.get());
+    const std::size_t RR = static_cast<std::size_t>(R) * R;
+    if (mode == 1) {
+      const int nb = 2 * c->num_sms;
+      DBuf<double>& part = scratch_partials(c, static_cast<std::size_t>(nb) * RR);
+      launch_mode1_q(c, R, c->Q.get(), c->V.get(), c->W.get(), part.get(), nb, c->stream);
+      reduce_partials(part.get(), nb, static_cast<std::int64_t>(RR), c->m1.get(), c->stream);
+      allreduce(c, c->m1.get(), RR);
+      download_colmajor(c, c->m1.get(), R, R, out);
+    } else if (mode == 2) {
+      launch_mode2(c, R, c->Q.get(), c->H.get(), c->W.get(), nullptr, c->M2.get(), c->stream);
+      allreduce(c, c->M2.get(), static_cast<std::size_t>(c->J) * R);
+      download_colmajor(c, c->M2.get(), c->J, R, out);
+    } else {
+      launch_mode3(c, R, c->Q.get(), c->H.get(), c->V.get(), c->m3.get(), c->stream);
+      download_colmajor(c, c->m3.get(), Ks(c), R, out);
+    }
+    c->state_valid = false;
+  });
+}
+
+namespace {
+/// Distinct sorted columns per shard subject (nnz_cols of each slice,
+/// sparse.hpp:96-98), from the device CSR.
+void shard_cols(p2g_ctx* c, std::vector<std::int64_t>& ptr, std::vector<std::int32_t>& cols) {
+  std::vector<std::int64_t> srp(static_cast<std::size_t>(Ks(c) + 1)), rp(static_cast<std::size_t>(c->NR + 1));
+  std::vector<std::int32_t> ci(static_cast<std::size_t>(c->nnz));
+  P2G_CUDA(cudaMemcpy(srp.data(), c->srp.get(), sizeof(std::int64_t) * srp.size(), cudaMemcpyDeviceToHost));
+  P2G_CUDA(cudaMemcpy(rp.data(), c->rp.get(), sizeof(std::int64_t) * rp.size(), cudaMemcpyDeviceToHost));
+  if (c->nnz) P2G_CUDA(cudaMemcpy(ci.data(), c->ci.get(), sizeof(std::int32_t) * ci.size(), cudaMemcpyDeviceToHost));
+  ptr.assign(static_cast<std::size_t>(Ks(c) + 1), 0);
+  cols.clear();
+  std::vector<std::int32_t> tmp;
+  for (std::int64_t k = 0; k < Ks(c); ++k) {
+    tmp.assign(ci.begin() + rp[static_cast<std::size_t>(srp[static_cast<std::size_t>(k)])],
+               ci.begin() + rp[static_cast<std::size_t>(srp[static_cast<std::size_t>(k + 1)])]);
+    std::sort(tmp.begin(), tmp.end());
+    tmp.erase(std::unique(tmp.begin(), tmp.end()), tmp.end());
+    cols.insert(cols.end(), tmp.begin(), tmp.end());
+    ptr[static_cast<std::size_t>(k + 1)] = static_cast<std::int64_t>(cols.size());
+  }
+}
+}  // namespace
+
+extern "C" int p2g_project(p2g_ctx* c, int32_t R, const double* Q, int64_t* ycol_ptr, int32_t* ycols, double* Y_out) {
+  return guarded([&] {
+    require_loaded(c);
+    set_device(c);
+    if (R < 1 || R > 40) throw InvalidArgument("rank out of range");
+    std::vector<std::int64_t> ptr;
+    std::vector<std::int32_t> cols;
+    shard_cols(c, ptr, cols);
+    if (ycol_ptr) std::memcpy(ycol_ptr, ptr.data(), sizeof(int64_t) * ptr.size());
+    if (!Y_out) return;
+    if (!Q || !ycols) throw InvalidArgument("null argument");
+    std::memcpy(ycols, cols.data(), sizeof(int32_t) * cols.size());
+    alloc_state(c, R);
+    DBuf<std::int64_t> dptr;
+    DBuf<std::int32_t> dcols;
+    DBuf<double> dY;
+    dptr.resize(ptr.size());
+    dcols.resize(std::max<std::size_t>(cols.size(), 1));
+    dY.resize(std::max<std::size_t>(cols.size() * R, 1));
+    P2G_CUDA(cudaMemcpyAsync(c->Q.get(), Q, sizeof(double) * c->NR * R, cudaMemcpyHostToDevice, c->stream));
+    P2G_CUDA(cudaMemcpyAsync(dptr.get(), ptr.data(), sizeof(std::int64_t) * ptr.size(), cudaMemcpyHostToDevice, c->stream));
+    if (!cols.empty())
+      P2G_CUDA(cudaMemcpyAsync(dcols.get(), cols.data(), sizeof(std::int32_t) * cols.size(), cudaMemcpyHostToDevice, c->stream));
+    launch_project(c, R, c->Q.get(), dptr.get(), dcols.get(), dY.get(), c->stream);
+    if (!cols.empty())
+      P2G_CUDA(cudaMemcpyAsync(Y_out, dY.get(), sizeof(double) * cols.size() * R, cudaMemcpyDeviceToHost, c->stream));
+    P2G_CUDA(cudaStreamSynchronize(c->stream));
+    c->state_valid = false;
+  });
+}
+
+namespace {
+
+struct PackedDev {
+  DBuf<std::int64_t> ptr, occ_ptr, occ;
+  DBuf<std::int32_t> cols;
+  DBuf<double> Y, H, V, W, out, part;
+};
+
+/// Shape checks of check_mttkrp_input / ProjectedSlices::from_packed
+/// (mttkrp.hpp:170-181, slices.hpp:43-67) and upload.
+void upload_packed(p2g_ctx* c, std::int64_t K, std::int64_t J, int R, const int64_t* ycol_ptr, const int32_t* ycols,
+                   const double* Y, PackedDev& d) {
+  if (R <= 0) throw InvalidArgument("slice rank must be positive");
+  if (R > 40) throw InvalidArgument("rank above 40 unsupported on device");
+  if (K < 0 || J < 0 || !ycol_ptr) throw InvalidArgument("bad packed slices");
+  if (ycol_ptr[0] != 0) throw InvalidArgument("ycol_ptr must start at 0");
+  for (std::int64_t k = 0; k < K; ++k) {
+    if (ycol_ptr[k + 1] < ycol_ptr[k]) throw InvalidArgument("packed block width differs from column list");
+    for (std::int64_t t = ycol_ptr[k]; t < ycol_ptr[k + 1]; ++t) {
+      if (ycols[t] < 0 || ycols[t] >= J) throw InvalidArgument("packed column index out of range");
+      if (t > ycol_ptr[k] && ycols[t] <= ycols[t - 1]) throw InvalidArgument("packed column indices must be ascending");
+    }
+  }
+  const std::int64_t nc = ycol_ptr[K];
+  d.ptr.resize(static_cast<std::size_t>(K + 1));
+  d.cols.resize(static_cast<std::size_t>(std::max<std::int64_t>(nc, 1)));
+  d.Y.resize(static_cast<std::size_t>(std::max<std::int64_t>(nc * R, 1)));
+  P2G_CUDA(cudaMemcpyAsync(d.ptr.get(), ycol_ptr, sizeof(int64_t) * (K + 1), cudaMemcpyHostToDevice, c->stream));
+  if (nc > 0) {
+    P2G_CUDA(cudaMemcpyAsync(d.cols.get(), ycols, sizeof(int32_t) * nc, cudaMemcpyHostToDevice, c->stream));
+    P2G_CUDA(cudaMemcpyAsync(d.Y.get(), Y, sizeof(double) * nc * R, cudaMemcpyHostToDevice, c->stream));
+  }
+  // per-column occurrence lists for the deterministic mode-2 kernel
+  std::vector<std::int64_t> cnt(static_cast<std::size_t>(J + 1), 0);
+  for (std::int64_t t = 0; t < nc; ++t) cnt[static_cast<std::size_t>(ycols[t]) + 1]++;
+  for (std::int64_t j = 0; j < J; ++j) cnt[static_cast<std::size_t>(j + 1)] += cnt[static_cast<std::size_t>(j)];
+  std::vector<std::int64_t> occ(static_cast<std::size_t>(2 * std::max<std::int64_t>(nc, 1)));
+  std::vector<std::int64_t> fill(cnt.begin(), cnt.end() - 1);
+  for (std::int64_t k = 0; k < K; ++k)
+    for (std::int64_t t = ycol_ptr[k]; t < ycol_ptr[k + 1]; ++t) {
+      const std::int64_t pos = fill[static_cast<std::size_t>(ycols[t])]++;
+      occ[static_cast<std::size_t>(2 * pos)] = t;
+      occ[static_cast<std::size_t>(2 * pos + 1)] = k;
+    }
+  d.occ_ptr.resize(cnt.size());
+  d.occ.resize(occ.size());
+  P2G_CUDA(cudaMemcpyAsync(d.occ_ptr.get(), cnt.data(), sizeof(std::int64_t) * cnt.size(), cudaMemcpyHostToDevice, c->stream));
+  P2G_CUDA(cudaMemcpyAsync(d.occ.get(), occ.data(), sizeof(std::int64_t) * occ.size(), cudaMemcpyHostToDevice, c->stream));
+  P2G_CUDA(cudaStreamSynchronize(c->stream));  // host vectors go out of scope
+}
+
+void packed_mode(p2g_ctx* c, int mode, std::int64_t K, std::int64_t J, int R, PackedDev& d, const double* dH,
+                 const double* dV, const double* dW, double* dout) {
+  const std::size_t RR = static_cast<std::size_t>(R) * R;
+  if (mode == 1) {
+    const int nb = packed_mode1_blocks(c->num_sms);
+    d.part.resize(static_cast<std::size_t>(nb) * RR);
+    launch_packed_mode13(1, K, J, R, d.ptr.get(), d.cols.get(), d.Y.get(), dH, dV, dW, d.part.get(), nb, c->stream);
+    reduce_partials(d.part.get(), nb, static_cast<std::int64_t>(RR), dout, c->stream);
+  } else if (mode == 2) {
+    launch_packed_mode2(K, J, R, d.ptr.get(), d.cols.get(), d.Y.get(), dH, dW, d.occ_ptr.get(), d.occ.get(), dout,
+                        c->stream);
+  } else {
+    const int nb = packed_mode1_blocks(c->num_sms);
+    launch_packed_mode13(3, K, J, R, d.ptr.get(), d.cols.get(), d.Y.get(), dH, dV, dW, dout, nb, c->stream);
+  }
+}
+
+}  // namespace
+
+extern "C" int p2g_mttkrp_packed(p2g_ctx* c, int32_t mode, int64_t K, int64_t J, int32_t R, const int64_t* ycol_ptr,
+                                 const int32_t* ycols, const double* Y, const double* H, const double* V,
+                                 const double* W, double* out) {
+  return guarded([&] {
+    if (!c) throw InvalidArgument("null context");
+    set_device(c);
+    if (mode < 1 || mode > 3) throw InvalidArgument("mttkrp: mode must be 1, 2 or 3");
+    if (!H || !V || !W || !out) throw InvalidArgument("null factor");
+    PackedDev d;
+    upload_packed(c, K, J, R, ycol_ptr, ycols, Y, d);
+    d.H.resize(static_cast<std::size_t>(R) * R);
+    d.V.resize(static_cast<std::size_t>(std::max<std::int64_t>(J, 1)) * R);
+    d.W.resize(static_cast<std::size_t>(std::max<std::int64_t>(K, 1)) * R);
+    upload_colmajor(c, H, R, R, d.H.get());
+    P2G_CUDA(cudaStreamSynchronize(c->stream));
+    upload_colmajor(c, V, J, R, d.V.get());
+    P2G_CUDA(cudaStreamSynchronize(c->stream));
+    upload_colmajor(c, W, K, R, d.W.get());
+    const std::int64_t rows = mode == 1 ? R : (mode == 2 ? J : K);
+    d.out.resize(static_cast<std::size_t>(std::max<std::int64_t>(rows, 1)) * R);
+    packed_mode(c, mode, K, J, R, d, d.H.get(), d.V.get(), d.W.get(), d.out.get());
+    download_colmajor(c, d.out.get(), rows, R, out);
+  });
+}
+
+extern "C" int p2g_cp_als_iteration(p2g_ctx* c, int64_t K, int64_t J, int32_t R, const int64_t* ycol_ptr,
+                                    const int32_t* ycols, const double* Y, double* H, double* V, double* W,
+                                    int32_t nonneg, int32_t normalize_w, double* lambda_out, double* m3_out) {
+  return guarded([&] {
+    if (!c) throw InvalidArgument("null context");
+    set_device(c);
+    if (!H || !V || !W) throw InvalidArgument("null factor");
+    PackedDev d;
+    upload_packed(c, K, J, R, ycol_ptr, ycols, Y, d);
+    const std::size_t RR = static_cast<std::size_t>(R) * R;
+    cudaStream_t s = c->stream;
+    DBuf<double> dH, dV, dW, m1, M2, m3, gW, gV, gH, G2, G3, nH, nV, gvraw, pinv, part, gwc;
+    DBuf<std::int32_t> err;
+    dH.resize(RR);
+    dV.resize(static_cast<std::size_t>(std::max<std::int64_t>(J, 1)) * R);
+    dW.resize(static_cast<std::size_t>(std::max<std::int64_t>(K, 1)) * R);
+    m1.resize(RR);
+    M2.resize(static_cast<std::size_t>(std::max<std::int64_t>(J, 1)) * R);
+    m3.resize(static_cast<std::size_t>(std::max<std::int64_t>(K, 1)) * R);
+    for (DBuf<double>* b : {&gW, &gV, &gH, &G2, &G3, &gvraw, &pinv}) b->resize(RR);
+    nH.resize(R);
+    nV.resize(R);
+    gwc.resize(RR + 1);
+    part.resize(static_cast<std::size_t>(kMaxPartials) * (RR + 1));
+    err.resize(1);
+    P2G_CUDA(cudaMemsetAsync(err.get(), 0, sizeof(std::int32_t), s));
+    check_finite_host(H, static_cast<std::int64_t>(RR), "gram operand");
+    check_finite_host(V, J * R, "gram operand");
+    check_finite_host(W, K * R, "gram operand");
+    upload_colmajor(c, H, R, R, dH.get());
+    P2G_CUDA(cudaStreamSynchronize(s));
+    upload_colmajor(c, V, J, R, dV.get());
+    P2G_CUDA(cudaStreamSynchronize(s));
+    upload_colmajor(c, W, K, R, dW.get());
+    // gram(W), gram(V) of the incoming factors
+    int np = gram_partials(R, K, dW.get(), nullptr, part.get(), kMaxPartials, s);
+    reduce_partials(part.get(), np, static_cast<std::int64_t>(RR + 1), gwc.get(), s);
+    P2G_CUDA(cudaMemcpyAsync(gW.get(), gwc.get(), sizeof(double) * RR, cudaMemcpyDeviceToDevice, s));
+    np = gram_partials(R, J, dV.get(), nullptr, part.get(), kMaxPartials, s);
+    reduce_partials(part.get(), np, static_cast<std::int64_t>(RR + 1), gwc.get(), s);
+    P2G_CUDA(cudaMemcpyAsync(gV.get(), gwc.get(), sizeof(double) * RR, cudaMemcpyDeviceToDevice, s));
+    // H step (cp.hpp:107-112)
+    packed_mode(c, 1, K, J, R, d, dH.get(), dV.get(), dW.get(), m1.get());
+    launch_solve_h(R, m1.get(), gW.get(), gV.get(), dH.get(), nH.get(), gH.get(), G2.get(), s);
+    // W' = W diag(nH) (cp.hpp:111)
+    {
+      std::vector<double> ones(static_cast<std::size_t>(R));
+      DBuf<double> inv;
+      inv.resize(R);
+      // scale W columns by nH: reuse k_scale_cols with reciprocal norms computed on host
+      std::vector<double> hnh(static_cast<std::size_t>(R));
+      P2G_CUDA(cudaMemcpyAsync(hnh.data(), nH.get(), sizeof(double) * R, cudaMemcpyDeviceToHost, s));
+      P2G_CUDA(cudaStreamSynchronize(s));
+      for (int r = 0; r < R; ++r) ones[static_cast<std::size_t>(r)] = 1.0 / hnh[static_cast<std::size_t>(r)];
+      P2G_CUDA(cudaMemcpyAsync(inv.get(), ones.data(), sizeof(double) * R, cudaMemcpyHostToDevice, s));
+      launch_scale_cols(R, K, dW.get(), inv.get(), s);
+      P2G_CUDA(cudaStreamSynchronize(s));
+    }
+    // V step (cp.hpp:115-123)
+    packed_mode(c, 2, K, J, R, d, dH.get(), dV.get(), dW.get(), M2.get());
+    if (nonneg) {
+      launch_nnls_rows(R, J, G2.get(), M2.get(), dV.get(), 0, err.get(), s);
+    } else {
+      launch_pinv(R, G2.get(), pinv.get(), s);
+      launch_rows_times(R, J, M2.get(), pinv.get(), dV.get(), s);
+    }
+    np = gram_partials(R, J, dV.get(), nullptr, part.get(), kMaxPartials, s);
+    reduce_partials(part.get(), np, static_cast<std::int64_t>(RR + 1), gwc.get(), s);
+    P2G_CUDA(cudaMemcpyAsync(gvraw.get(), gwc.get(), sizeof(double) * RR, cudaMemcpyDeviceToDevice, s));
+    launch_normalize_v(R, J, dV.get(), gvraw.get(), gV.get(), nV.get(), gH.get(), G3.get(), s);
+    // W step (cp.hpp:126-133)
+    packed_mode(c, 3, K, J, R, d, dH.get(), dV.get(), dW.get(), m3.get());
+    if (nonneg) {
+      launch_nnls_rows(R, K, G3.get(), m3.get(), dW.get(), 0, err.get(), s);
+    } else {
+      launch_pinv(R, G3.get(), pinv.get(), s);
+      launch_rows_times(R, K, m3.get(), pinv.get(), dW.get(), s);
+    }
+    std::int32_t herr = 0;
+    P2G_CUDA(cudaMemcpyAsync(&herr, err.get(), sizeof(herr), cudaMemcpyDeviceToHost, s));
+    P2G_CUDA(cudaStreamSynchronize(s));
+    if (herr) throw NumericalError("NNLS did not converge");
+    download_colmajor(c, dH.get(), R, R, H);
+    download_colmajor(c, dV.get(), J, R, V);
+    download_colmajor(c, dW.get(), K, R, W);
+    if (m3_out) download_colmajor(c, m3.get(), K, R, m3_out);
+    // lambda (cp.hpp:136-143), on host (R values)
+    for (int r = 0; r < R; ++r) {
+      double acc = 0.0;
+      for (int64_t k = 0; k < K; ++k) acc += W[k + r * K] * W[k + r * K];
+      const double nrm = std::sqrt(acc);
+      if (lambda_out) lambda_out[r] = normalize_w ? nrm : 1.0;
+      if (normalize_w && nrm > 0.0)
+        for (int64_t k = 0; k < K; ++k) W[k + r * K] /= nrm;
+    }
+  });
+}
+
+extern "C" int p2g_nnls_rowwise(p2g_ctx* c, const double* G, const double* B, int64_t n, int32_t R, int32_t max_iter,
+                                double* X) {
+  return guarded([&] {
+    if (!c) throw InvalidArgument("null context");
+    set_device(c);
+    if (R < 1 || R > 40) throw InvalidArgument("nnls_rowwise: G must be square with 1 <= R <= 40");
+    if (n < 0 || !G || (n > 0 && (!B || !X))) throw InvalidArgument("nnls_rowwise: bad arguments");
+    check_finite_host(G, static_cast<std::int64_t>(R) * R, "nonnegative solve normal matrix");
+    check_finite_host(B, n * R, "nonnegative solve right-hand side");
+    if (n == 0) return;
+    DBuf<double> dG, dB, dX;
+    DBuf<std::int32_t> err;
+    dG.resize(static_cast<std::size_t>(R) * R);
+    dB.resize(static_cast<std::size_t>(n) * R);
+    dX.resize(static_cast<std::size_t>(n) * R);
+    err.resize(1);
+    P2G_CUDA(cudaMemsetAsync(err.get(), 0, sizeof(std::int32_t), c->stream));
+    upload_colmajor(c, G, R, R, dG.get());
+    P2G_CUDA(cudaStreamSynchronize(c->stream));
+    upload_colmajor(c, B, n, R, dB.get());
+    launch_nnls_rows(R, n, dG.get(), dB.get(), dX.get(), max_iter, err.get(), c->stream);
+    std::int32_t herr = 0;
+    P2G_CUDA(cudaMemcpyAsync(&herr, err.get(), sizeof(herr), cudaMemcpyDeviceToHost, c->stream));
+    P2G_CUDA(cudaStreamSynchronize(c->stream));
+    if (herr) throw NumericalError("NNLS did not converge");
+    download_colmajor(c, dX.get(), n, R, X);
+  });
+}
+
+extern "C" int p2g_pinv_small(p2g_ctx* c, const double* G, int32_t n, double* out) {
+  return guarded([&] {
+    if (!c) throw InvalidArgument("null context");
+    set_device(c);
+    if (n < 1 || n > 40 || !G || !out) throw InvalidArgument("pinv_small: matrix must be square (1..40)");
+    check_finite_host(G, static_cast<std::int64_t>(n) * n, "pseudoinverse operand");
+    DBuf<double> dG, dO;
+    dG.resize(static_cast<std::size_t>(n) * n);
+    dO.resize(static_cast<std::size_t>(n) * n);
+    upload_colmajor(c, G, n, n, dG.get());
+    launch_pinv(n, dG.get(), dO.get(), c->stream);
+    download_colmajor(c, dO.get(), n, n, out);
+  });
+}
+
+extern "C" int p2g_gram(p2g_ctx* c, const double* A, int64_t rows, int32_t cols, double* out) {
+  return guarded([&] {
+    if (!c) throw InvalidArgument("null context");
+    set_device(c);
+    if (cols < 1 || cols > 40 || rows < 0 || !out || (rows > 0 && !A)) throw InvalidArgument("gram: bad arguments");
+    check_finite_host(A, rows * cols, "gram operand");
+    const std::size_t RR = static_cast<std::size_t>(cols) * cols;
+    DBuf<double> dA, part, res;
+    dA.resize(static_cast<std::size_t>(std::max<std::int64_t>(rows, 1)) * cols);
+    part.resize(static_cast<std::size_t>(kMaxPartials) * (RR + 1));
+    res.resize(RR + 1);
+    if (rows > 0) upload_colmajor(c, A, rows, cols, dA.get());
+    const int np = gram_partials(cols, rows, dA.get(), nullptr, part.get(), kMaxPartials, c->stream);
+    reduce_partials(part.get(), np, static_cast<std::int64_t>(RR + 1), res.get(), c->stream);
+    download_colmajor(c, res.get(), cols, cols, out);
+  });
+}

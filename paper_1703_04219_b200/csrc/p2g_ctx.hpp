@@ -1,0 +1,187 @@
+// Device context of libp2g (one per rank / GPU) and the launcher
+// declarations shared by the .cu translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdint>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "p2g_common.hpp"
+
+namespace p2g {
+
+#define P2G_CUDA(call)                                                                                   \
+  do {                                                                                                   \
+    cudaError_t e_ = (call);                                                                             \
+    if (e_ != cudaSuccess)                                                                               \
+      throw ::p2g::CudaError(std::string("CUDA error: ") + cudaGetErrorString(e_) + " at " + __FILE__ + \
+                             ":" + std::to_string(__LINE__));                                            \
+  } while (0)
+
+/// Process-wide count of kernels this library launched (bench gpu_launches).
+inline std::atomic<long long>& launch_counter() {
+  static std::atomic<long long> n{0};
+  return n;
+}
+
+/// Call right after each <<<>>> launch: error check + launch count.
+#define P2G_LAUNCHED(nkernels)                  \
+  do {                                          \
+    ::p2g::launch_counter() += (nkernels);      \
+    P2G_CUDA(cudaGetLastError());               \
+  } while (0)
+
+/// Owning device buffer.
+template <typename T>
+struct DBuf {
+  T* p = nullptr;
+  std::size_t n = 0;
+  DBuf() = default;
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  ~DBuf() { release(); }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  void resize(std::size_t count) {
+    if (count <= n && p) return;
+    release();
+    if (count == 0) return;
+    P2G_CUDA(cudaMalloc(&p, count * sizeof(T)));
+    n = count;
+  }
+  T* get() const { return p; }
+};
+
+/// Per-phase device timing collected by the fused loop (bench / profiling).
+struct PhaseTimer {
+  std::vector<std::string> names;
+  std::vector<cudaEvent_t> start, stop;
+  std::map<std::string, std::pair<double, std::int64_t>> acc;  // total ms, launches
+};
+
+/// Device arguments of the sparse shard (CSR rebased to the shard).
+struct ShardArgs {
+  const std::int64_t* srp;  // K_s + 1, rows (rebased)
+  const std::int64_t* rp;   // NR_s + 1, nnz offsets (rebased)
+  const std::int32_t* ci;
+  const double* val;
+  std::int64_t K;  // shard subjects
+  std::int64_t NR;
+  std::int64_t nnz;
+  std::int64_t J;
+};
+
+struct NcclState;  // opaque, defined in p2g_api.cu
+
+}  // namespace p2g
+
+struct p2g_ctx {
+  int device = 0;
+  int rank = 0, world = 1;
+  cudaStream_t stream = nullptr;
+  p2g::NcclState* nccl = nullptr;
+  int num_sms = 148;
+
+  // Shard of the sparse tensor.
+  std::int64_t K_total = 0, J = 0;
+  std::int64_t k_begin = 0, k_end = 0;
+  std::int64_t NR = 0, nnz = 0;  // shard rows / nnz
+  std::int64_t max_rows = 0;     // max I_k in the shard
+  std::int64_t min_rows_global = 0;
+  std::int64_t nnz_total = 0;
+  double norm_x = 0.0;  // ||X||_F^2 over ALL subjects (allreduced)
+  bool loaded = false;
+  p2g::DBuf<std::int64_t> srp, rp;
+  p2g::DBuf<std::int32_t> ci;
+  p2g::DBuf<double> val;
+
+  // Factor state (row-major on device).
+  int R = 0;
+  p2g::DBuf<double> H, V, W, Q;       // R*R, J*R, K_s*R, NR*R
+  p2g::DBuf<double> gramW, gramV;     // R*R each
+  p2g::DBuf<double> nH, nV;           // R each
+  p2g::DBuf<double> m1, M2, m3;       // R*R, J*R, K_s*R
+  p2g::DBuf<double> G1, G2, G3, gramH; // R*R
+  p2g::DBuf<double> gvraw, gwc;       // R*R, R*R+1
+  p2g::DBuf<double> stage;            // host<->device staging (col-major)
+  std::vector<std::int64_t> srp_host;  // full subj_row_ptr (validation, shard bookkeeping)
+  double* pinned = nullptr;           // small pinned host block for per-iteration scalars
+  p2g::DBuf<double> pinvbuf;          // R*R
+  p2g::DBuf<double> partials;         // scratch for per-block partials
+  p2g::DBuf<double> scal;             // small scalars (fit, cross, residual ...)
+  p2g::DBuf<std::int32_t> flags;      // K_s
+  p2g::DBuf<std::int32_t> fb_list;    // compacted fallback subject ids
+  p2g::DBuf<std::int32_t> counters;   // [0]=n_fallback, [1]=nnls error, ...
+  p2g::DBuf<double> acc_scratch;      // accurate Procrustes path slabs
+  bool state_valid = false;
+
+  // Timing.
+  bool timing = false;
+  p2g::PhaseTimer timer;
+  std::vector<cudaEvent_t> ev_pool;
+  std::size_t ev_used = 0;
+  std::vector<std::pair<std::string, std::pair<std::size_t, std::size_t>>> pending;  // name, (ev0, ev1)
+};
+
+namespace p2g {
+
+// ---- launchers (defined in the kernel translation units) ----
+// K1: Procrustes fast path fused with the mode-1 partial.  Writes Q rows of
+// fast subjects, flags (0 = fast, 2 = needs accurate path), and per-block
+// R x R m1 partials (count returned).
+int launch_procrustes(p2g_ctx* c, int R, const double* H, const double* V, const double* W, double* Q,
+                      std::int32_t* flags, double* m1_partials, int max_blocks, cudaStream_t s);
+// Accurate Jacobi-SVD path over the subjects flagged P2G_FLAG_ACCURATE;
+// writes one R x R m1 partial per block (count = procrustes_accurate_blocks).
+int launch_procrustes_accurate(p2g_ctx* c, int R, const double* H, const double* V, const double* W, double* Q,
+                               std::int32_t* flags, double* m1_partials, cudaStream_t s);
+int procrustes_accurate_blocks(p2g_ctx* c, int R);
+void launch_mode2(p2g_ctx* c, int R, const double* Q, const double* H, const double* W, const double* nH,
+                  double* M2, cudaStream_t s);
+void launch_mode3(p2g_ctx* c, int R, const double* Q, const double* H, const double* V, double* m3,
+                  cudaStream_t s);
+void launch_mode1_q(p2g_ctx* c, int R, const double* Q, const double* V, const double* W, double* m1_partials,
+                    int nblocks, cudaStream_t s);
+void launch_project(p2g_ctx* c, int R, const double* Q, const std::int64_t* ycol_ptr, const std::int32_t* ycols,
+                    double* Y, cudaStream_t s);
+int packed_mode1_blocks(int num_sms);
+// Packed-Y MTTKRP (boundary): mode 1 -> nblocks R x R partials in out; mode 3 -> K x R rows.
+void launch_packed_mode13(int mode, std::int64_t K, std::int64_t J, int R, const std::int64_t* ycol_ptr,
+                          const std::int32_t* ycols, const double* Y, const double* H, const double* V,
+                          const double* W, double* out, int nblocks, cudaStream_t s);
+// Packed-Y mode 2, deterministic via the per-column occurrence list (c, k) pairs.
+void launch_packed_mode2(std::int64_t K, std::int64_t J, int R, const std::int64_t* ycol_ptr,
+                         const std::int32_t* ycols, const double* Y, const double* H, const double* W,
+                         const std::int64_t* occ_ptr, const std::int64_t* occ, double* out, cudaStream_t s);
+
+// Dense helpers (k_dense.cu).
+int gram_partials(int R, std::int64_t n, const double* A, const double* B, double* partials, int max_blocks,
+                  cudaStream_t s);  // returns #partials; each partial R*R (+1 cross if B)
+void reduce_partials(const double* partials, int nparts, std::int64_t len, double* out, cudaStream_t s);
+void launch_nnls_rows(int R, std::int64_t n, const double* G, const double* B, double* X, int max_iter,
+                      std::int32_t* err, cudaStream_t s);
+void launch_rows_times(int R, std::int64_t n, const double* B, const double* P, double* X,
+                       cudaStream_t s);  // X = B * P (row-major rows)
+void launch_pinv(int n, const double* G, double* out, cudaStream_t s);
+// Replicated R x R steps of the CP iteration (cp.hpp:99-145):
+void launch_solve_h(int R, const double* m1, const double* gramW, const double* gramV, double* H, double* nH,
+                    double* gramH, double* G2, cudaStream_t s);  // H update + normalize + G2 for the V step
+void launch_normalize_v(int R, std::int64_t J, double* V, const double* gramV_raw, double* gramV, double* nV,
+                        const double* gramH, double* G3, cudaStream_t s);
+void launch_fit(int R, const double* gramW_cross, const double* gramH, const double* gramV, double norm_x,
+                double* gramW, double* scal, cudaStream_t s);
+// A[:, c] /= norms[c] for a row-major n x R matrix.
+void launch_scale_cols(int R, std::int64_t n, double* A, const double* norms, cudaStream_t s);
+void launch_transpose(const double* in, double* out, std::int64_t rows, std::int64_t cols, cudaStream_t s);
+void launch_fill_identity(double* A, int n, cudaStream_t s);
+void launch_fill(double* A, std::int64_t n, double v, cudaStream_t s);
+void launch_hadamard(const double* A, const double* B, double* C, int n, cudaStream_t s);
+
+}  // namespace p2g

@@ -1,0 +1,248 @@
+"""GPU parity: every kernel through the C ABI against the CPU oracle.
+
+Tolerances (north_star): per-step outputs (MTTKRPs, Q, factors) relative
+Frobenius error <= 1e-9 when teacher-forced with oracle state; fit trajectory
+|fit_gpu - fit_oracle| <= 1e-7 over 10 free-running iterations; integer
+bookkeeping (partition, flags/deficiency counts) bit-exact.
+"""
+import numpy as np
+import pytest
+
+from tests.helpers import oracle_from_csr, rel_err, rel_frob
+
+pytestmark = pytest.mark.gpu
+
+TOL_STEP = 1e-9
+TOL_FIT = 1e-7
+
+
+def proj(P):
+    return P["rank"], P["n_cols"], P["blocks"], P["cols"]
+
+
+# ---------------------------------------------------------------------------
+# Boundary kernels on packed projected slices (mttkrp.hpp, kernels.hpp)
+# ---------------------------------------------------------------------------
+def test_packed_mode_kats(ctx):  # test_mttkrp.cpp:36-101 through the C ABI
+    b, c = [np.array([[1.0, 0.0], [0.0, 2.0]])], [[0, 1]]
+    w = np.array([[3.0, 5.0]])
+    assert np.array_equal(ctx.mttkrp_packed(1, 2, 2, b, c, np.eye(2), np.ones((2, 2)), w), [[3, 5], [6, 10]])
+    assert np.array_equal(ctx.mttkrp_packed(2, 2, 2, b, c, np.eye(2), np.ones((2, 2)), w), [[3, 0], [0, 10]])
+    m = ctx.mttkrp_packed(2, 1, 3, [np.array([[4.0]]), np.array([[7.0]])], [[0], [2]], np.array([[1.0]]),
+                          np.ones((3, 1)), np.array([[1.0], [10.0]]))
+    assert m[0, 0] == 4 and m[1, 0] == 0 and m[2, 0] == 70
+    m = ctx.mttkrp_packed(3, 2, 2, b, c, np.eye(2), np.ones((2, 2)), np.ones((1, 2)))
+    assert m[0, 0] == 1 and m[0, 1] == 2
+    m = ctx.mttkrp_packed(3, 2, 2, b, c, np.array([[1.0, 2], [3, 4]]), np.ones((2, 2)), np.ones((1, 2)))
+    assert m[0, 0] == 7 and m[0, 1] == 10
+
+
+def test_packed_vs_oracle_random(ctx, oracle, p2g):  # test_mttkrp.cpp:139-156 + acceptance c1 style
+    o = oracle
+    rng = o.Rng(24)
+    for trial in range(40):
+        rank = 1 + rng.below(4)
+        n_cols = 2 + rng.below(12)
+        n_slices = 1 + rng.below(8)
+        density = 1.0 if trial % 3 == 0 else (0.5 if trial % 3 == 1 else 0.15)
+        P = o.random_projected(rng, rank, n_cols, n_slices, density)
+        h = o.random_matrix(rng, rank, rank)
+        v = o.random_matrix(rng, n_cols, rank)
+        w = o.random_matrix(rng, n_slices, rank)
+        for mode in (1, 2, 3):
+            gpu = ctx.mttkrp_packed(mode, *proj(P), h, v, w)
+            assert rel_frob(gpu, o.naive_mttkrp(*proj(P), h, v, w, mode)) < 1e-10
+            assert rel_frob(gpu, o.mttkrp(*proj(P), h, v, w, mode)) < 1e-13
+    # determinism (test_mttkrp.cpp:218-229) and shape checks (:235-247)
+    P = o.random_projected(o.Rng(27), 3, 10, 6, 0.5)
+    h, v, w = np.eye(3), np.ones((10, 3)), np.ones((6, 3))
+    for mode in (1, 2, 3):
+        assert np.array_equal(ctx.mttkrp_packed(mode, *proj(P), h, v, w), ctx.mttkrp_packed(mode, *proj(P), h, v, w))
+    with pytest.raises(p2g.InvalidArgument):
+        ctx.mttkrp_packed(0, *proj(P), h, v, w)
+    with pytest.raises(p2g.InvalidArgument):
+        ctx.mttkrp_packed(1, *proj(P), np.ones((3, 2)), v, w)
+    with pytest.raises(p2g.InvalidArgument):
+        ctx.mttkrp_packed(1, 2, 3, [np.ones((2, 2))], [[1, 1]], np.eye(2), np.ones((3, 2)), np.ones((1, 2)))
+
+
+def test_nnls_pinv_gram_vs_oracle(ctx, oracle, p2g):  # test_kernels.cpp:85-254
+    o = oracle
+    x = ctx.nnls_rowwise(np.eye(2), np.array([[1.0, -2.0]]))
+    assert abs(x[0, 0] - 1) < 1e-12 and x[0, 1] == 0.0
+    x = ctx.nnls_rowwise(np.eye(2), np.array([[3.0, 4.0]]))
+    assert abs(x[0, 0] - 3) < 1e-12 and abs(x[0, 1] - 4) < 1e-12
+    x = ctx.nnls_rowwise(np.array([[2.0, 1], [1, 2]]), np.array([[1.0, 1.0]]))
+    assert np.abs(x - 1 / 3).max() < 1e-12
+    with pytest.raises(p2g.NumericalError, match="NNLS did not converge"):
+        ctx.nnls_rowwise(np.eye(2), np.array([[3.0, 4.0]]), max_iter=1)
+    with pytest.raises(p2g.NumericalError):
+        ctx.nnls_rowwise(np.eye(2), np.array([[np.nan, 1.0]]))
+    rng = o.Rng(16)
+    for n in (1, 3, 5, 10, 17, 40):
+        f = o.random_matrix(rng, n + 2, n)
+        g = o.gram(f) + 0.01 * np.eye(n)
+        b = o.random_matrix(rng, 200, n, -2.0, 2.0)
+        assert rel_frob(ctx.nnls_rowwise(g, b), o.nnls_rowwise(g, b)) < 1e-9
+        assert rel_frob(ctx.pinv_small(g), o.pinv_small(g)) < 1e-9
+        assert np.array_equal(ctx.gram(f), ctx.gram(f).T)
+        assert rel_frob(ctx.gram(f), o.gram(f)) < 1e-14
+    assert np.abs(ctx.pinv_small(np.array([[4.0, 0], [0, 0]])) - np.array([[0.25, 0], [0, 0]])).max() < 1e-14
+    assert np.array_equal(ctx.gram(np.array([[1.0, 2], [3, 4]])), [[10, 14], [14, 20]])
+
+
+def test_cp_als_iteration_vs_oracle(ctx, oracle):  # cp.hpp:99-145
+    o = oracle
+    rng = o.Rng(32)
+    for trial in range(20):
+        rank = 1 + rng.below(4)
+        n_cols = 2 + rng.below(9)
+        n_slices = 1 + rng.below(8)
+        P = o.random_projected(rng, rank, n_cols, n_slices, 1.0 if trial % 2 == 0 else 0.4)
+        nonneg = trial % 2 == 0
+        lo = 0.0 if nonneg else -1.0
+        h = o.random_matrix(rng, rank, rank)
+        v = o.random_matrix(rng, n_cols, rank, lo, 1.0)
+        w = o.random_matrix(rng, n_slices, rank, lo, 1.0)
+        ref = o.cp_als_iteration(*proj(P), h, v, w, nonneg, trial % 4 == 1)
+        got = ctx.cp_als_iteration(*proj(P), h, v, w, nonneg, trial % 4 == 1)
+        for key in ("H", "V", "W", "m3", "lambda"):
+            assert rel_err(got[key], ref[key]) <= TOL_STEP, (trial, key)
+
+
+# ---------------------------------------------------------------------------
+# The fused-loop kernels on the BASELINE cfg1 workload, teacher-forced
+# ---------------------------------------------------------------------------
+@pytest.fixture(scope="module")
+def cfg1(p2g, oracle):
+    X = p2g.generate_baseline(1, 5)
+    H0, V0, W0 = p2g.init_factors(101, X.K, X.J, 5)
+    T = oracle_from_csr(oracle, X)
+    dumps = {}
+    for nonneg in (False, True):
+        dumps[nonneg] = oracle.fit_parafac2(T, 5, max_iters=10, tol=1e-300, nonneg=nonneg, threads=4, H0=H0, V0=V0,
+                                            W0=W0, dumps=True)
+    return X, T, (H0, V0, W0), dumps
+
+
+@pytest.mark.parametrize("nonneg", [False, True])
+def test_procrustes_teacher_forced(ctx, oracle, cfg1, nonneg):
+    X, T, _, dumps = cfg1
+    ctx.load(X)
+    for it, d in enumerate(dumps[nonneg]["dumps"]):
+        Q, flags, m1 = ctx.procrustes(d["H_in"], d["V_in"], d["W_in"])
+        oq = d["Q"]
+        # integer gate: rank-deficient subjects identical
+        ofl = np.array(d["flags"])
+        assert np.array_equal(np.isin(flags, (1, 3)), np.isin(ofl, (1, 3))), it
+        assert rel_err(Q, oq) <= TOL_STEP, it
+        assert rel_err(m1, d["m1"]) <= TOL_STEP, it
+        # every Q_k column-orthonormal (acceptance c3)
+        for k in range(0, X.K, 37):
+            qk = Q[X.subj_row_ptr[k]:X.subj_row_ptr[k + 1]]
+            assert np.linalg.norm(qk.T @ qk - np.eye(5)) < 1e-8
+
+
+@pytest.mark.parametrize("nonneg", [False, True])
+def test_mttkrp_q_and_project_teacher_forced(ctx, oracle, cfg1, nonneg):
+    X, T, _, dumps = cfg1
+    ctx.load(X)
+    for it, d in enumerate(dumps[nonneg]["dumps"][:4]):
+        Q = d["Q"]
+        P = oracle.project_slices(T, Q)
+        H, V, W = d["H"], d["V"], d["W"]
+        for mode in (1, 2, 3):
+            ref = oracle.mttkrp(*proj(P), H, V, W, mode)
+            got = ctx.mttkrp_q(mode, Q, H, V, W)
+            assert rel_err(got, ref) <= TOL_STEP, (it, mode)
+        ptr, cols, blocks = ctx.project(Q, 5)
+        for k in range(0, X.K, 11):
+            assert list(cols[ptr[k]:ptr[k + 1]]) == P["cols"][k]
+            assert rel_err(blocks[k], P["blocks"][k]) <= 1e-12
+
+
+@pytest.mark.parametrize("nonneg", [False, True])
+def test_fit_trajectory_cfg1(ctx, oracle, p2g, cfg1, nonneg):
+    X, T, (H0, V0, W0), dumps = cfg1
+    ctx.load(X)
+    ref = dumps[nonneg]
+    cfg = p2g.SolverConfig(rank=5, max_iters=10, tol=1e-300, nonneg=nonneg)
+    res = ctx.fit(cfg, H0, V0, W0)
+    assert res.iterations == 10 and not res.converged
+    assert np.abs(res.fit - np.array(ref["fit"])).max() <= TOL_FIT
+    assert abs(res.norm_x - T.frobenius_sq()) <= 1e-12 * res.norm_x
+    # factors after 10 free-running iterations (reported; step-gated above)
+    assert rel_err(res.H, ref["H"]) < 1e-6
+    assert rel_err(res.V, ref["V"]) < 1e-6
+    assert rel_err(res.W, ref["S"]) < 1e-6
+
+
+def test_fit_single_iteration_factors_exact(ctx, oracle, p2g, cfg1):
+    """One iteration from identical inputs: H, V, W, Q within 1e-9."""
+    X, T, (H0, V0, W0), dumps = cfg1
+    ctx.load(X)
+    for nonneg in (False, True):
+        d = dumps[nonneg]["dumps"][0]
+        res = ctx.fit(p2g.SolverConfig(rank=5, max_iters=1, tol=1e-300, nonneg=nonneg), H0, V0, W0)
+        assert rel_err(res.H, d["H"]) <= TOL_STEP
+        assert rel_err(res.V, d["V"]) <= TOL_STEP
+        assert rel_err(res.W, d["W"]) <= TOL_STEP
+        assert rel_err(res.Q, d["Q"]) <= TOL_STEP
+        assert abs(res.fit[0] - d["fit"]) <= 1e-12
+
+
+def test_reference_random_init_and_residual_identity(ctx, oracle, p2g):
+    """fit with the reference's own initialisation (init=random, seed) and the
+    efficient-residual identity (test_solver.cpp:256-280) on GPU outputs."""
+    o = oracle
+    rng = o.Rng(51)
+    for trial in range(4):
+        T = o.random_tensor(rng, 4, 6, 3, 7, 0.4 if trial % 2 else 1.0)
+        rank = 1 + rng.below(3)
+        X = p2g.CSRTensor(*T.to_csr())
+        ctx.load(X)
+        for iters in (1, 3, 8):
+            cfg = p2g.SolverConfig(rank=rank, max_iters=iters, tol=1e-300, nonneg=trial % 2 == 0, seed=trial)
+            res = ctx.fit(cfg)
+            ref = o.fit_parafac2(T, rank, max_iters=iters, tol=1e-300, nonneg=trial % 2 == 0, seed=trial)
+            assert np.abs(res.fit - np.array(ref["fit"])).max() <= TOL_FIT
+            direct = o.dense_residual(T, res.Q, res.H, res.W, res.V)
+            assert abs(res.residual_sq[-1] - direct) <= 1e-9 * max(1.0, direct)
+
+
+def test_error_semantics(ctx, oracle, p2g):  # test_solver.cpp:86-120, 300-319
+    o = oracle
+    T = o.random_tensor(o.Rng(42), 3, 4, 2, 3, 1.0)
+    ctx.load(p2g.CSRTensor(*T.to_csr()))
+    with pytest.raises(p2g.DataError, match="rank exceeds variables"):
+        ctx.fit(p2g.SolverConfig(rank=5))
+    with pytest.raises(p2g.DataError, match="rank exceeds observations"):
+        ctx.fit(p2g.SolverConfig(rank=4))
+    for bad in (p2g.SolverConfig(rank=0), p2g.SolverConfig(rank=2, tol=0.0), p2g.SolverConfig(rank=2, max_iters=0)):
+        with pytest.raises(p2g.InvalidArgument):
+            ctx.fit(bad)
+    T = o.Tensor.from_triplets(3, [(3, []), (2, [])])
+    ctx.load(p2g.CSRTensor(*T.to_csr()))
+    with pytest.raises(p2g.DataError, match="no non-zero entries"):
+        ctx.fit(p2g.SolverConfig(rank=1))
+    T = o.Tensor.from_triplets(2, [(2, [(0, 0, 1e200), (0, 1, 1e200), (1, 0, 1e200), (1, 1, 1e200)])])
+    ctx.load(p2g.CSRTensor(*T.to_csr()))
+    with pytest.raises(p2g.NumericalError):
+        ctx.fit(p2g.SolverConfig(rank=2, max_iters=10))
+    with pytest.raises(p2g.DataError):
+        ctx.load(p2g.CSRTensor(3, np.array([0]), np.array([0]), np.array([], np.int32), np.array([])))
+
+
+def test_cfg2_prefix_parity(ctx, oracle, p2g):
+    """First 20,000 subjects of BASELINE cfg2 (R=10): 3 free-running iterations."""
+    X = p2g.generate_baseline(2, 10, K=20000)
+    H0, V0, W0 = p2g.init_factors(102, X.K, X.J, 10)
+    T = oracle_from_csr(oracle, X)
+    ref = oracle.fit_parafac2(T, 10, max_iters=3, tol=1e-300, nonneg=True, threads=8, H0=H0, V0=V0, W0=W0,
+                              dumps=True)
+    ctx.load(X)
+    res = ctx.fit(p2g.SolverConfig(rank=10, max_iters=3, tol=1e-300, nonneg=True), H0, V0, W0)
+    assert np.abs(res.fit - np.array(ref["fit"])).max() <= TOL_FIT
+    d = ref["dumps"][0]
+    Q, flags, m1 = ctx.procrustes(d["H_in"], d["V_in"], d["W_in"])
+    assert rel_err(Q, d["Q"]) <= TOL_STEP and rel_err(m1, d["m1"]) <= TOL_STEP
