@@ -422,6 +422,15 @@ int elem_grid(std::int64_t n) {
 
 constexpr std::size_t kSmallSmem = sizeof(SmallWs);
 
+/// Opt the single-warp R x R kernels into > 48 KB of dynamic shared memory.
+void small_smem_optin() {
+  static bool done = false;
+  if (done) return;
+  P2G_CUDA(cudaFuncSetAttribute(k_pinv, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmallSmem)));
+  P2G_CUDA(cudaFuncSetAttribute(k_solve_h, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmallSmem)));
+  done = true;
+}
+
 template <int RP>
 void nnls_launch(int R, std::int64_t n, const double* G, const double* B, double* X, int cap, std::int32_t* err,
                  cudaStream_t s) {
@@ -476,12 +485,14 @@ void launch_rows_times(int R, std::int64_t n, const double* B, const double* P, 
 
 void launch_pinv(int n, const double* G, double* out, cudaStream_t s) {
   if (n > kMaxR) throw InvalidArgument("pinv: size above 40 unsupported on device");
+  small_smem_optin();
   k_pinv<<<1, 32, kSmallSmem, s>>>(n, G, out);
   P2G_LAUNCHED(1);
 }
 
 void launch_solve_h(int R, const double* m1, const double* gramW, const double* gramV, double* H, double* nH,
                     double* gramH, double* G2, cudaStream_t s) {
+  small_smem_optin();
   k_solve_h<<<1, 32, kSmallSmem, s>>>(R, m1, gramW, gramV, H, nH, gramH, G2);
   P2G_LAUNCHED(1);
 }
