@@ -92,7 +92,7 @@ struct NnlsSmem {
 template <int RP, int WPB>
 __global__ void __launch_bounds__(WPB * 32)
     k_nnls(int R, std::int64_t n, const double* __restrict__ G, const double* __restrict__ B, double* __restrict__ X,
-           int cap, std::int32_t* err) {
+           int cap, std::int32_t* err, const std::int32_t* __restrict__ rowlist, const std::int32_t* __restrict__ nlist) {
   extern __shared__ double smem[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   double* Gs = smem;
@@ -112,7 +112,9 @@ __global__ void __launch_bounds__(WPB * 32)
   for (int e = threadIdx.x; e < R * R; e += blockDim.x) Gs[e] = G[e];
   __syncthreads();
   const std::int64_t nwarps = static_cast<std::int64_t>(gridDim.x) * WPB;
-  for (std::int64_t row = static_cast<std::int64_t>(blockIdx.x) * WPB + wid; row < n; row += nwarps) {
+  const std::int64_t nrows = rowlist ? static_cast<std::int64_t>(*nlist) : n;
+  for (std::int64_t it = static_cast<std::int64_t>(blockIdx.x) * WPB + wid; it < nrows; it += nwarps) {
+    const std::int64_t row = rowlist ? static_cast<std::int64_t>(rowlist[it]) : it;
     for (int r = lane; r < R; r += 32) {
       const double v = B[row * R + r];
       b[r] = v;
@@ -433,7 +435,7 @@ void small_smem_optin() {
 
 template <int RP>
 void nnls_launch(int R, std::int64_t n, const double* G, const double* B, double* X, int cap, std::int32_t* err,
-                 cudaStream_t s) {
+                 const std::int32_t* rowlist, const std::int32_t* nlist, cudaStream_t s) {
   constexpr int WPB = RP <= 16 ? 8 : 4;
   const std::size_t per_warp = sizeof(double) * (NnlsSmem<RP>::kDoubles + (NnlsSmem<RP>::kInts + 1) / 2);
   const std::size_t smem = sizeof(double) * RP * RP + WPB * per_warp;
@@ -441,7 +443,27 @@ void nnls_launch(int R, std::int64_t n, const double* G, const double* B, double
   P2G_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   const std::int64_t want = (n + WPB - 1) / WPB;
   const int blocks = static_cast<int>(std::max<std::int64_t>(1, std::min<std::int64_t>(want, 148 * 8)));
-  kern<<<blocks, WPB * 32, smem, s>>>(R, n, G, B, X, cap, err);
+  kern<<<blocks, WPB * 32, smem, s>>>(R, n, G, B, X, cap, err, rowlist, nlist);
+}
+
+template <int RP>
+void nnls_warp(int R, std::int64_t n, const double* G, const double* B, double* X, int cap, std::int32_t* err,
+               const std::int32_t* rowlist, const std::int32_t* nlist, cudaStream_t s) {
+  nnls_launch<RP>(R, n, G, B, X, cap, err, rowlist, nlist, s);
+}
+
+void nnls_warp_any(int R, std::int64_t n, const double* G, const double* B, double* X, int cap, std::int32_t* err,
+                   const std::int32_t* rowlist, const std::int32_t* nlist, cudaStream_t s) {
+  if (R <= 8)
+    nnls_warp<8>(R, n, G, B, X, cap, err, rowlist, nlist, s);
+  else if (R <= 16)
+    nnls_warp<16>(R, n, G, B, X, cap, err, rowlist, nlist, s);
+  else if (R <= 32)
+    nnls_warp<32>(R, n, G, B, X, cap, err, rowlist, nlist, s);
+  else if (R <= 40)
+    nnls_warp<40>(R, n, G, B, X, cap, err, rowlist, nlist, s);
+  else
+    throw InvalidArgument("rank above 40 unsupported");
 }
 
 }  // namespace
@@ -461,19 +483,19 @@ void reduce_partials(const double* partials, int nparts, std::int64_t len, doubl
 }
 
 void launch_nnls_rows(int R, std::int64_t n, const double* G, const double* B, double* X, int max_iter,
-                      std::int32_t* err, cudaStream_t s) {
+                      std::int32_t* err, std::int32_t* work, cudaStream_t s) {
   if (n == 0) return;
   const int cap = max_iter > 0 ? max_iter : 30 * R;
-  if (R <= 8)
-    nnls_launch<8>(R, n, G, B, X, cap, err, s);
-  else if (R <= 16)
-    nnls_launch<16>(R, n, G, B, X, cap, err, s);
-  else if (R <= 32)
-    nnls_launch<32>(R, n, G, B, X, cap, err, s);
-  else if (R <= 40)
-    nnls_launch<40>(R, n, G, B, X, cap, err, s);
-  else
-    throw InvalidArgument("rank above 40 unsupported");
+  if (R <= kSmallRankMax && work) {
+    // thread per row; rows whose passive Cholesky meets a non-positive pivot
+    // are re-solved by the warp kernel with the pseudo-inverse (work[0] = count).
+    P2G_CUDA(cudaMemsetAsync(work, 0, sizeof(std::int32_t), s));
+    launch_nnls_thread(R, n, G, B, X, max_iter, err, work + 1, work, s);
+    nnls_warp_any(R, n, G, B, X, cap, err, work + 1, work, s);
+    P2G_LAUNCHED(1);
+    return;
+  }
+  nnls_warp_any(R, n, G, B, X, cap, err, nullptr, nullptr, s);
   P2G_LAUNCHED(1);
 }
 

@@ -42,6 +42,7 @@ struct K1Args {
   double* scratch;      // accurate path: per-warp I_max x R slabs
   std::int64_t max_rows;
   std::int32_t* counters;  // [2] = non-finite operand seen
+  const double* Ebuf;      // accurate path preconditioner (K x R x R) or null
 };
 
 template <int RP>
@@ -272,6 +273,21 @@ __global__ void __launch_bounds__(WPB * 32) k_procrustes_accurate(K1Args a, doub
       T[e] = s[i] * Hs[j * R + i];
     }
     __syncwarp();
+    // Preconditioner: eigenvectors E of A^T A from the fast path (small-R
+    // pipeline).  B = A E has nearly orthogonal columns, so the Hestenes
+    // sweeps below converge in 1-3 sweeps; V = E V' afterwards.
+    const double* Ek = a.Ebuf ? a.Ebuf + k * RR : nullptr;
+    if (Ek) {
+      for (int e = lane; e < RR; e += 32) {
+        const int i = e / R, j = e - (e / R) * R;
+        double acc = 0.0;
+        for (int c = 0; c < R; ++c) acc = fma(T[i * R + c], Ek[c * R + j], acc);
+        B[e] = acc;
+      }
+      __syncwarp();
+      for (int e = lane; e < RR; e += 32) T[e] = B[e];
+      __syncwarp();
+    }
     // A = XV T (solver.hpp:189-190, transposed)
     double amax = 0.0;
     bool finite = true;
@@ -349,6 +365,17 @@ __global__ void __launch_bounds__(WPB * 32) k_procrustes_accurate(K1Args a, doub
             __syncwarp();
           }
         if (!rotated) break;
+      }
+      if (Ek) {  // right singular vectors of A = E V'
+        for (int e = lane; e < RR; e += 32) {
+          const int i = e / R, j = e - (e / R) * R;
+          double acc = 0.0;
+          for (int c = 0; c < R; ++c) acc = fma(Ek[i * R + c], Vj[c * R + j], acc);
+          B[e] = acc;
+        }
+        __syncwarp();
+        for (int e = lane; e < RR; e += 32) Vj[e] = B[e];
+        __syncwarp();
       }
       // singular values (of the scaled A), U columns in place
       for (int c = 0; c < R; ++c) {
@@ -594,8 +621,9 @@ int launch_procrustes(p2g_ctx* c, int R, const double* H, const double* V, const
 }
 
 int launch_procrustes_accurate(p2g_ctx* c, int R, const double* H, const double* V, const double* W, double* Q,
-                               std::int32_t* flags, double* m1_partials, cudaStream_t s) {
+                               std::int32_t* flags, double* m1_partials, const double* Ebuf, cudaStream_t s) {
   K1Args a{};
+  a.Ebuf = Ebuf;
   a.X = ShardArgs{c->srp.get(), c->rp.get(), c->ci.get(), c->val.get(), c->k_end - c->k_begin, c->NR, c->nnz, c->J};
   a.R = R;
   a.H = H;

@@ -1,0 +1,763 @@
+// Small-rank (R <= 16) pipeline of the Procrustes step and the batched NNLS.
+//
+// The R x R dense work of the Procrustes step (eigendecomposition of the
+// Gram matrix, the polar factor) is inherently serial per subject.  A warp
+// cooperating on one 10 x 10 Jacobi spends most issue slots on index math,
+// shuffles and synchronisation (profiles/: ~28.8K warp instructions per
+// subject).  Here each thread owns one subject: the packed Gram matrix lives
+// in registers (static indices from fully unrolled rotations), the
+// eigenvectors in the thread's column of a [element][lane] shared-memory
+// array (conflict-free: all lanes touch the same element index).
+//
+// Split of K1 (procrustes_update, solver.hpp:173-193, + mode-1 partial):
+//   K1a  k_gram_c      warp per subject: C_k = (X_k V)^T (X_k V), packed lower
+//   K1b  k_polar_small thread per subject: G = H D C D H^T, Jacobi eig,
+//                      S = G^{-1/2}, m1_k = S H D C D, flags
+//   K1c  k_qrows       warp per subject: Q_k = X_k V D H^T S (rows, coalesced)
+// The accurate path (k_procrustes.cu) takes the flagged subjects.
+#include <algorithm>
+#include <utility>
+
+#include "dev_common.cuh"
+#include "p2g_ctx.hpp"
+
+namespace p2g {
+namespace {
+
+constexpr int LD = 33;  // [element][lane] stride (conflict-free both ways)
+
+__host__ __device__ constexpr int tri(int i, int j) { return i >= j ? i * (i + 1) / 2 + j : j * (j + 1) / 2 + i; }
+
+// ---------------------------------------------------------------------------
+// K1a: C_k = XV^T XV (packed lower triangle) for every subject.
+// ---------------------------------------------------------------------------
+template <int RP, int WPB>
+__global__ void __launch_bounds__(WPB * 32)
+    k_gram_c(ShardArgs X, int R, const double* __restrict__ V, double* __restrict__ Cbuf) {
+  __shared__ double chunk[WPB][32 * RP];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  double* ch = chunk[wid];
+  constexpr int NTP = RP * (RP + 1) / 2;
+  constexpr int kTri = (NTP + 31) / 32;
+  const int nt = R * (R + 1) / 2;
+  int ea[kTri], eb[kTri];
+#pragma unroll
+  for (int t = 0; t < kTri; ++t) {
+    const int e = lane + 32 * t;
+    int x = 0;
+    while ((x + 1) * (x + 2) / 2 <= e) ++x;
+    ea[t] = x;
+    eb[t] = e - x * (x + 1) / 2;
+  }
+  const std::int64_t nwarps = static_cast<std::int64_t>(gridDim.x) * WPB;
+  for (std::int64_t k = static_cast<std::int64_t>(blockIdx.x) * WPB + wid; k < X.K; k += nwarps) {
+    const std::int64_t r0 = X.srp[k];
+    const int I = static_cast<int>(X.srp[k + 1] - r0);
+    double cacc[kTri];
+#pragma unroll
+    for (int t = 0; t < kTri; ++t) cacc[t] = 0.0;
+    for (int b = 0; b < I; b += 32) {
+      const int i = b + lane;
+      const int nr = min(32, I - b);
+      double xv[RP];
+      if (i < I) {
+        dev::csr_row_times<RP>(xv, X.ci, X.val, X.rp[r0 + i], X.rp[r0 + i + 1], V, R);
+      } else {
+#pragma unroll
+        for (int r = 0; r < RP; ++r) xv[r] = 0.0;
+      }
+#pragma unroll
+      for (int r = 0; r < RP; ++r) ch[lane * RP + r] = xv[r];
+      __syncwarp();
+#pragma unroll
+      for (int t = 0; t < kTri; ++t) {
+        if (lane + 32 * t < nt) {
+          double acc = cacc[t];
+          for (int rr = 0; rr < nr; ++rr) acc = fma(ch[rr * RP + ea[t]], ch[rr * RP + eb[t]], acc);
+          cacc[t] = acc;
+        }
+      }
+      __syncwarp();
+    }
+#pragma unroll
+    for (int t = 0; t < kTri; ++t)
+      if (lane + 32 * t < nt) Cbuf[k * nt + lane + 32 * t] = cacc[t];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K1b: thread-per-subject polar factor.  Jacobi on G = H C' H^T with
+// C' = D C D (rotation form of the oracle / Numerical Recipes); the fast path
+// keeps the subject when lambda_min >= kFastRatio lambda_max, otherwise flags
+// it for the accurate path and hands it the eigenvectors as a preconditioner.
+//
+// Ordering: parallel (tournament) rounds.  In every round the MP/2 rotations
+// act on the fixed physical slot pairs (2i, 2i+1), so they are independent
+// instruction streams (ILP) with compile-time register indices; after each
+// round the register-resident G is permuted by the fixed tournament shift
+// sigma, which brings the next round's pairs into the same slots.  The round
+// loop itself is not unrolled, keeping the code inside the instruction cache
+// (a fully unrolled sweep stalled on "no_instructions", profiles/).
+// Eigenvectors stay in logical order in shared memory; their columns are
+// addressed through the runtime slot -> index map L(r, s).
+// ---------------------------------------------------------------------------
+constexpr double kFastRatio = 1e-6;
+constexpr int kMaxSweeps = 16;  // not converged -> accurate path
+
+/// Logical index held by physical slot s in round r (M players, M even).
+__host__ __device__ constexpr int rr_slot(int M, int r, int s) {
+  return s == 0 ? r : (s == 1 ? M - 1 : ((s & 1) == 0 ? (r + s / 2) % (M - 1) : (r - s / 2 + (M - 1)) % (M - 1)));
+}
+
+/// Physical slot holding logical index i at the start of a sweep (round 0).
+__host__ __device__ constexpr int rr_inv0(int M, int i) {
+  return i == 0 ? 0 : (i == M - 1 ? 1 : (i <= M / 2 - 1 ? 2 * i : 2 * (M - 1 - i) + 1));
+}
+
+/// Physical slot that slot s moves to between consecutive rounds.
+__host__ __device__ constexpr int rr_sigma(int M, int s) {
+  if (s == 1) return 1;
+  const int d = s == 0 ? 0 : ((s & 1) == 0 ? s / 2 : (M - 1) - s / 2);
+  const int d2 = (d - 1 + (M - 1)) % (M - 1);
+  return d2 == 0 ? 0 : (d2 <= M / 2 - 1 ? 2 * d2 : 2 * ((M - 1) - d2) + 1);
+}
+
+/// Cycle decomposition (compile time) of the packed-index permutation
+/// e = tri(x, y) -> tri(sigma x, sigma y).  cyc lists each cycle as
+/// e0, perm(e0), perm(perm(e0)), ...
+template <int MP>
+struct PermCycles {
+  static constexpr int NT = MP * (MP + 1) / 2;
+  int cyc[NT] = {};
+  int start[NT] = {};
+  int len[NT] = {};
+  int ncycles = 0;
+  constexpr PermCycles() {
+    int perm[NT] = {};
+    for (int x = 0; x < MP; ++x)
+      for (int y = 0; y <= x; ++y) perm[tri(x, y)] = tri(rr_sigma(MP, x), rr_sigma(MP, y));
+    bool seen[NT] = {};
+    int pos = 0;
+    for (int e0 = 0; e0 < NT; ++e0) {
+      if (seen[e0]) continue;
+      start[ncycles] = pos;
+      int e = e0, n = 0;
+      while (!seen[e]) {
+        seen[e] = true;
+        cyc[pos++] = e;
+        ++n;
+        e = perm[e];
+      }
+      len[ncycles++] = n;
+    }
+  }
+};
+
+template <int MP>
+struct PermTable {
+  static constexpr PermCycles<MP> value{};
+  /// index of the cycle containing flattened position t
+  static constexpr int cycle_of(int t) {
+    int c = 0;
+    while (c + 1 < value.ncycles && value.start[c + 1] <= t) ++c;
+    return c;
+  }
+};
+
+/// One step of the cycle walk at flattened position T.
+template <int MP, int T>
+__device__ __forceinline__ void perm_step(double (&g)[MP * (MP + 1) / 2], double& carry) {
+  constexpr int c = PermTable<MP>::cycle_of(T);
+  constexpr int s = PermTable<MP>::value.start[c];
+  constexpr int n = PermTable<MP>::value.len[c];
+  constexpr int e = PermTable<MP>::value.cyc[T];
+  constexpr int e0 = PermTable<MP>::value.cyc[s];
+  if constexpr (n == 1) {
+    // fixed point
+  } else if constexpr (T == s) {
+    carry = g[e];
+  } else {
+    const double tmp = g[e];
+    g[e] = carry;
+    carry = tmp;
+    if constexpr (T == s + n - 1) g[e0] = carry;
+  }
+}
+
+template <int MP, int... Ts>
+__device__ __forceinline__ void perm_steps(double (&g)[MP * (MP + 1) / 2], double& carry,
+                                           std::integer_sequence<int, Ts...>) {
+  (perm_step<MP, Ts>(g, carry), ...);
+}
+
+template <int MP>
+__device__ __forceinline__ void jacobi_round(double (&g)[MP * (MP + 1) / 2], double* E, int r) {
+  constexpr int H = MP / 2;
+  double cs[H], sn[H], tt[H], ap[H];
+#pragma unroll
+  for (int i = 0; i < H; ++i) {
+    const int p = 2 * i, q = 2 * i + 1;
+    const double apq = g[tri(q, p)];
+    const double app = g[tri(p, p)], aqq = g[tri(q, q)];
+    cs[i] = 1.0;
+    sn[i] = 0.0;
+    tt[i] = 0.0;
+    ap[i] = 0.0;
+    if (fabs(apq) > 1e-300 && fabs(apq) > 2.2e-18 * sqrt(fabs(app * aqq))) {
+      const double theta = (aqq - app) / (2.0 * apq);
+      const double t = (theta >= 0.0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(fma(theta, theta, 1.0)));
+      const double c = rsqrt(fma(t, t, 1.0));
+      cs[i] = c;
+      sn[i] = t * c;
+      tt[i] = t;
+      ap[i] = apq;
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < H; ++i) {
+    const int p = 2 * i, q = 2 * i + 1;
+    g[tri(p, p)] -= tt[i] * ap[i];
+    g[tri(q, q)] += tt[i] * ap[i];
+    if (sn[i] != 0.0) g[tri(q, p)] = 0.0;
+  }
+#pragma unroll
+  for (int i1 = 0; i1 < H; ++i1)
+#pragma unroll
+    for (int i2 = i1 + 1; i2 < H; ++i2) {
+      const int p1 = 2 * i1, q1 = p1 + 1, p2 = 2 * i2, q2 = p2 + 1;
+      const double c1 = cs[i1], s1 = sn[i1], c2 = cs[i2], s2 = sn[i2];
+      const double x11 = g[tri(p1, p2)], x12 = g[tri(p1, q2)], x21 = g[tri(q1, p2)], x22 = g[tri(q1, q2)];
+      const double y11 = c2 * x11 - s2 * x12, y12 = s2 * x11 + c2 * x12;
+      const double y21 = c2 * x21 - s2 * x22, y22 = s2 * x21 + c2 * x22;
+      g[tri(p1, p2)] = c1 * y11 - s1 * y21;
+      g[tri(q1, p2)] = s1 * y11 + c1 * y21;
+      g[tri(p1, q2)] = c1 * y12 - s1 * y22;
+      g[tri(q1, q2)] = s1 * y12 + c1 * y22;
+    }
+  // eigenvectors (logical order): columns a = L(r,2i), b = L(r,2i+1)
+#pragma unroll
+  for (int i = 0; i < H; ++i) {
+    if (sn[i] == 0.0) continue;
+    const int a = rr_slot(MP, r, 2 * i), b = rr_slot(MP, r, 2 * i + 1);
+    const double c = cs[i], s = sn[i];
+#pragma unroll
+    for (int k = 0; k < MP; ++k) {
+      const double ea = E[(k * MP + a) * LD], eb = E[(k * MP + b) * LD];
+      E[(k * MP + a) * LD] = c * ea - s * eb;
+      E[(k * MP + b) * LD] = s * ea + c * eb;
+    }
+  }
+  // physical permutation g_new[tri(sigma x, sigma y)] = g_old[tri(x, y)],
+  // applied along its cycles with a single carried register (all indices
+  // are template constants, so g stays in registers).
+  double carry = 0.0;
+  perm_steps<MP>(g, carry, std::make_integer_sequence<int, MP*(MP + 1) / 2>{});
+}
+
+template <int RP>
+struct PolarSmem {
+  static constexpr int MP = (RP + 1) & ~1;
+  static constexpr int kPerWarp = (MP * MP) * LD;  // E (then staging)
+};
+
+template <int RP, int WPB>
+__global__ void __launch_bounds__(WPB * 32)
+    k_polar_small(std::int64_t K, int R, const double* __restrict__ H, const double* __restrict__ W,
+                  const double* __restrict__ Cbuf, double* __restrict__ Sbuf, double* __restrict__ Ebuf,
+                  std::int32_t* __restrict__ flags, double* __restrict__ m1_partials) {
+  extern __shared__ double smem[];
+  constexpr int MP = PolarSmem<RP>::MP;
+  constexpr int NT = MP * (MP + 1) / 2;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  double* Hs = smem;                                   // R x R row-major
+  double* M1w = Hs + MP * MP;                          // WPB x (R x R) warp accumulators
+  double* Ew = M1w + WPB * MP * MP + wid * PolarSmem<RP>::kPerWarp;
+  double* E = Ew + lane;  // this thread's column: E[(i*MP + j)*LD]
+  const int nt = R * (R + 1) / 2;
+  for (int e = threadIdx.x; e < R * R; e += blockDim.x) Hs[e] = H[e];
+  for (int e = lane; e < MP * MP; e += 32) M1w[wid * MP * MP + e] = 0.0;
+  __syncthreads();
+
+  const std::int64_t nwarps = static_cast<std::int64_t>(gridDim.x) * WPB;
+  for (std::int64_t kb = (static_cast<std::int64_t>(blockIdx.x) * WPB + wid) * 32; kb < K; kb += nwarps * 32) {
+    const std::int64_t k = kb + lane;
+    const bool active = k < K;
+    double s[MP];
+#pragma unroll
+    for (int r = 0; r < MP; ++r) s[r] = (active && r < R) ? W[k * R + r] : 0.0;
+    // C' = D C D (logical, packed) into the E slots; Z = C' H^T into g-sized
+    // temporaries row by row; G = H Z written physically permuted (slot x
+    // holds logical rr_slot(MP, 0, x)).
+#pragma unroll
+    for (int a = 0; a < MP; ++a)
+#pragma unroll
+      for (int b = 0; b <= a; ++b)
+        E[tri(a, b) * LD] = (active && a < R) ? s[a] * Cbuf[k * nt + tri(a, b)] * s[b] : 0.0;
+    double g[NT];
+    {
+#pragma unroll
+      for (int i = 0; i < MP; ++i) {
+        double z[MP];  // row i of H C': z_b = sum_a H_ia C'_ab
+#pragma unroll
+        for (int b = 0; b < MP; ++b) {
+          double acc = 0.0;
+          if (i < R && b < R) {
+#pragma unroll
+            for (int a = 0; a < MP; ++a)
+              if (a < R) acc = fma(Hs[i * R + a], E[tri(a, b) * LD], acc);
+          }
+          z[b] = acc;
+        }
+#pragma unroll
+        for (int j = 0; j <= i; ++j) {
+          double acc = 0.0;
+#pragma unroll
+          for (int b = 0; b < MP; ++b)
+            if (j < R && b < R) acc = fma(z[b], Hs[j * R + b], acc);
+          // logical (i, j) lives in physical slots (pi i, pi j); padding: identity block
+          g[tri(rr_inv0(MP, i), rr_inv0(MP, j))] = (i < R) ? acc : (i == j ? 1.0 : 0.0);
+        }
+      }
+    }
+    double gmax = 0.0;
+    bool finite = true;
+#pragma unroll
+    for (int e = 0; e < NT; ++e) {
+      finite &= isfinite(g[e]);
+      gmax = fmax(gmax, fabs(g[e]));
+    }
+#pragma unroll
+    for (int i = 0; i < MP; ++i)
+#pragma unroll
+      for (int j = 0; j < MP; ++j) E[(i * MP + j) * LD] = i == j ? 1.0 : 0.0;
+    bool ok = active && finite && gmax > 0.0;
+    if (ok) {
+      bool converged = false;
+      for (int sweep = 0; sweep < kMaxSweeps; ++sweep) {
+        double off = 0.0, dia = 0.0;
+#pragma unroll
+        for (int i = 0; i < MP; ++i)
+#pragma unroll
+          for (int j = 0; j <= i; ++j) {
+            if (i == j)
+              dia = fma(g[tri(i, i)], g[tri(i, i)], dia);
+            else
+              off = fma(g[tri(i, j)], g[tri(i, j)], off);
+          }
+        if (off <= 1e-32 * dia) {
+          converged = true;
+          break;
+        }
+#pragma unroll 1
+        for (int r = 0; r < MP - 1; ++r) jacobi_round<MP>(g, E, r);
+      }
+      ok = converged;
+    }
+    // eigenvalues in logical order
+    double lam[MP];
+#pragma unroll
+    for (int x = 0; x < MP; ++x) lam[rr_slot(MP, 0, x)] = g[tri(x, x)];
+    if (ok) {
+      double lmax = 0.0, lmin = 1e308;
+#pragma unroll
+      for (int i = 0; i < MP; ++i)
+        if (i < R) {
+          lmax = fmax(lmax, lam[i]);
+          lmin = fmin(lmin, lam[i]);
+        }
+      ok = lmax > 0.0 && lmin >= kFastRatio * lmax;
+    }
+    if (active) flags[k] = ok ? P2G_FLAG_FULL_RANK : P2G_FLAG_ACCURATE;
+    if (active && !ok) {
+      // eigenvectors (identity if G was zero / non-finite) precondition the accurate path
+      const bool useE = finite && gmax > 0.0;
+      for (int i = 0; i < R; ++i)
+        for (int j = 0; j < R; ++j)
+          Ebuf[k * R * R + i * R + j] = useE ? E[(i * MP + j) * LD] : (i == j ? 1.0 : 0.0);
+    }
+    // S = E diag(lambda^-1/2) E^T (logical packed, into g)
+#pragma unroll
+    for (int m = 0; m < MP; ++m) lam[m] = (ok && m < R) ? rsqrt(lam[m]) : 0.0;
+#pragma unroll
+    for (int i = 0; i < MP; ++i)
+#pragma unroll
+      for (int j = 0; j <= i; ++j) {
+        double acc = 0.0;
+#pragma unroll
+        for (int m = 0; m < MP; ++m) acc = fma(E[(i * MP + m) * LD] * lam[m], E[(j * MP + m) * LD], acc);
+        g[tri(i, j)] = acc;
+      }
+    // m1_k = S (H C'), column by column; warp-summed into the warp accumulator.
+#pragma unroll
+    for (int a = 0; a < MP; ++a)
+#pragma unroll
+      for (int b = 0; b <= a; ++b)
+        E[tri(a, b) * LD] = (ok && a < R) ? s[a] * Cbuf[k * nt + tri(a, b)] * s[b] : 0.0;
+#pragma unroll 1
+    for (int j = 0; j < R; ++j) {
+      double y[MP];
+#pragma unroll
+      for (int c = 0; c < MP; ++c) {
+        double acc = 0.0;
+        if (c < R) {
+#pragma unroll
+          for (int a = 0; a < MP; ++a)
+            if (a < R) acc = fma(Hs[c * R + a], E[tri(a, j) * LD], acc);
+        }
+        y[c] = acc;
+      }
+#pragma unroll
+      for (int i = 0; i < MP; ++i) {
+        if (i >= R) continue;
+        double acc = 0.0;
+#pragma unroll
+        for (int c = 0; c < MP; ++c) acc = fma(g[tri(i, c)], y[c], acc);
+        acc = dev::warp_sum(acc);
+        if (lane == 0) M1w[wid * MP * MP + i * R + j] += acc;
+      }
+    }
+    // S out, staged through the (now free) E slots for coalesced stores.
+#pragma unroll
+    for (int e = 0; e < NT; ++e) E[e * LD] = g[e];
+    __syncwarp();
+    const std::int64_t nk = min(static_cast<std::int64_t>(32), K - kb);
+    for (std::int64_t idx = lane; idx < nk * nt; idx += 32) {
+      const int sub = static_cast<int>(idx / nt), e = static_cast<int>(idx - (idx / nt) * nt);
+      Sbuf[(kb + sub) * nt + e] = Ew[e * LD + sub];  // packed index is size independent
+    }
+    __syncwarp();
+  }
+  __syncthreads();
+  if (wid == 0)
+    for (int e = lane; e < R * R; e += 32) {
+      double acc = 0.0;
+      for (int w = 0; w < WPB; ++w) acc += M1w[w * MP * MP + e];
+      m1_partials[static_cast<std::int64_t>(blockIdx.x) * R * R + e] = acc;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K1c: Q_k rows = XV P, P = D H^T S (fast-path subjects only).
+// ---------------------------------------------------------------------------
+template <int RP, int WPB>
+__global__ void __launch_bounds__(WPB * 32)
+    k_qrows(ShardArgs X, int R, const double* __restrict__ H, const double* __restrict__ V,
+            const double* __restrict__ W, const double* __restrict__ Sbuf, const std::int32_t* __restrict__ flags,
+            double* __restrict__ Q) {
+  __shared__ double Hs[RP * RP];
+  __shared__ double Ps[WPB][RP * RP];
+  __shared__ double Ss[WPB][RP * RP];
+  __shared__ double chunk[WPB][32 * RP];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int e = threadIdx.x; e < R * R; e += blockDim.x) Hs[e] = H[e];
+  __syncthreads();
+  double* P = Ps[wid];
+  double* S = Ss[wid];
+  double* ch = chunk[wid];
+  const int nt = R * (R + 1) / 2;
+  const std::int64_t nwarps = static_cast<std::int64_t>(gridDim.x) * WPB;
+  for (std::int64_t k = static_cast<std::int64_t>(blockIdx.x) * WPB + wid; k < X.K; k += nwarps) {
+    if (flags[k] != P2G_FLAG_FULL_RANK) continue;
+    const std::int64_t r0 = X.srp[k];
+    const int I = static_cast<int>(X.srp[k + 1] - r0);
+    for (int e = lane; e < nt; e += 32) {
+      int x = 0;
+      while ((x + 1) * (x + 2) / 2 <= e) ++x;
+      const int y = e - x * (x + 1) / 2;
+      const double v = Sbuf[k * nt + e];
+      S[x * R + y] = v;
+      S[y * R + x] = v;
+    }
+    __syncwarp();
+    for (int e = lane; e < R * R; e += 32) {  // P = D H^T S
+      const int a = e / R, b = e - (e / R) * R;
+      double acc = 0.0;
+      for (int c = 0; c < R; ++c) acc = fma(Hs[c * R + a], S[c * R + b], acc);
+      P[e] = acc * W[k * R + a];
+    }
+    __syncwarp();
+    for (int b0 = 0; b0 < I; b0 += 32) {
+      const int i = b0 + lane;
+      const int nr = min(32, I - b0);
+      if (i < I) {
+        double xv[RP];
+        dev::csr_row_times<RP>(xv, X.ci, X.val, X.rp[r0 + i], X.rp[r0 + i + 1], V, R);
+#pragma unroll
+        for (int c = 0; c < RP; ++c) {
+          if (c < R) {
+            double q = 0.0;
+#pragma unroll
+            for (int r = 0; r < RP; ++r)
+              if (r < R) q = fma(xv[r], P[r * R + c], q);
+            ch[lane * RP + c] = q;
+          }
+        }
+      }
+      __syncwarp();
+      double* qdst = Q + (r0 + b0) * R;
+      for (int idx = lane; idx < nr * R; idx += 32) qdst[idx] = ch[(idx / R) * RP + (idx - (idx / R) * R)];
+      __syncwarp();
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Thread-per-row NNLS (kernels.hpp:115-185) for R <= 16: identical control
+// flow to nnls_single; passive solves by Cholesky in the thread's column of
+// a [element][lane] shared array, falling back to a flag for the warp path
+// when a pivot is not positive (the reference's pinv semantics).
+// ---------------------------------------------------------------------------
+template <int RP>
+struct NnlsThreadSmem {
+  static constexpr int NT = RP * (RP + 1) / 2;
+  static constexpr int kPerWarp = (NT + RP) * LD;  // L, sp
+};
+
+template <int RP, int WPB>
+__global__ void __launch_bounds__(WPB * 32)
+    k_nnls_thread(int R, std::int64_t n, const double* __restrict__ G, const double* __restrict__ B,
+                  double* __restrict__ X, int cap, std::int32_t* __restrict__ err, std::int32_t* __restrict__ redo,
+                  std::int32_t* __restrict__ n_redo) {
+  extern __shared__ double smem[];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  double* Gs = smem;
+  double* Lw = Gs + RP * RP + wid * NnlsThreadSmem<RP>::kPerWarp;
+  double* spw = Lw + NnlsThreadSmem<RP>::NT * LD;
+  for (int e = threadIdx.x; e < R * R; e += blockDim.x) Gs[e] = G[e];
+  __syncthreads();
+  auto L = [&](int i, int j) -> double& { return Lw[tri(i, j) * LD + lane]; };
+  auto SP = [&](int i) -> double& { return spw[i * LD + lane]; };
+  const std::int64_t stride = static_cast<std::int64_t>(gridDim.x) * blockDim.x;
+  for (std::int64_t row = static_cast<std::int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; row < n; row += stride) {
+    double b[RP], x[RP], w[RP];
+#pragma unroll
+    for (int r = 0; r < RP; ++r) {
+      b[r] = r < R ? B[row * R + r] : 0.0;
+      w[r] = b[r];
+      x[r] = 0.0;
+    }
+    unsigned passive = 0u;
+    int iters = 0;
+    bool failed = false, chol_fail = false;
+    while (true) {
+      double best = 1e-10;
+      int enter = -1;
+#pragma unroll
+      for (int r = 0; r < RP; ++r)
+        if (r < R && !((passive >> r) & 1u) && w[r] > best) {
+          best = w[r];
+          enter = r;
+        }
+      if (enter < 0) break;
+      passive |= 1u << enter;
+      while (true) {
+        if (++iters > cap) {
+          failed = true;
+          break;
+        }
+        int pset[RP];
+        int np = 0;
+#pragma unroll
+        for (int r = 0; r < RP; ++r)
+          if ((passive >> r) & 1u) pset[np++] = r;
+        // Cholesky of G_pp (lower, packed) in shared memory
+        for (int i = 0; i < np; ++i) {
+          for (int j = 0; j <= i; ++j) {
+            double acc = Gs[pset[i] * R + pset[j]];
+            for (int m = 0; m < j; ++m) acc -= L(i, m) * L(j, m);
+            if (i == j) {
+              if (!(acc > 0.0)) {
+                chol_fail = true;
+                break;
+              }
+              L(i, i) = sqrt(acc);
+            } else {
+              L(i, j) = acc / L(j, j);
+            }
+          }
+          if (chol_fail) break;
+        }
+        if (chol_fail) break;
+        for (int i = 0; i < np; ++i) {  // L y = b_p
+          double acc = 0.0;
+#pragma unroll
+          for (int r = 0; r < RP; ++r)
+            if (r == pset[i]) acc = b[r];
+          for (int m = 0; m < i; ++m) acc -= L(i, m) * SP(m);
+          SP(i) = acc / L(i, i);
+        }
+        for (int i = np - 1; i >= 0; --i) {  // L^T s = y
+          double acc = SP(i);
+          for (int m = i + 1; m < np; ++m) acc -= L(m, i) * SP(m);
+          SP(i) = acc / L(i, i);
+        }
+        bool allpos = true;
+        for (int a = 0; a < np; ++a) allpos &= SP(a) > 0.0;
+        double sv[RP];
+#pragma unroll
+        for (int r = 0; r < RP; ++r) sv[r] = 0.0;
+        for (int a = 0; a < np; ++a) {
+          const double v = SP(a);
+#pragma unroll
+          for (int r = 0; r < RP; ++r)
+            if (r == pset[a]) sv[r] = v;
+        }
+        if (allpos) {
+#pragma unroll
+          for (int r = 0; r < RP; ++r) x[r] = sv[r];
+          break;
+        }
+        double alpha = __longlong_as_double(0x7ff0000000000000ll);
+#pragma unroll
+        for (int r = 0; r < RP; ++r)
+          if (((passive >> r) & 1u) && sv[r] <= 0.0) {
+            const double denom = x[r] - sv[r];
+            alpha = fmin(alpha, denom > 0.0 ? x[r] / denom : 0.0);
+          }
+        double xm = 0.0;
+#pragma unroll
+        for (int r = 0; r < RP; ++r)
+          if ((passive >> r) & 1u) x[r] += alpha * (sv[r] - x[r]);
+#pragma unroll
+        for (int r = 0; r < RP; ++r) xm = fmax(xm, fabs(x[r]));
+        const double drop_tol = 1e-14 * fmax(1.0, xm);
+#pragma unroll
+        for (int r = 0; r < RP; ++r)
+          if (((passive >> r) & 1u) && x[r] <= drop_tol) {
+            x[r] = 0.0;
+            passive &= ~(1u << r);
+          }
+      }
+      if (failed || chol_fail) break;
+#pragma unroll
+      for (int r = 0; r < RP; ++r) {
+        if (r >= R) continue;
+        double acc = 0.0;
+#pragma unroll
+        for (int c = 0; c < RP; ++c)
+          if (c < R) acc = fma(Gs[r * R + c], x[c], acc);
+        w[r] = b[r] - acc;
+      }
+    }
+    if (chol_fail) {  // this row is re-solved by the warp kernel (pinv route)
+      redo[atomicAdd(n_redo, 1)] = static_cast<std::int32_t>(row);
+      continue;
+    }
+    if (failed) atomicAdd(err, 1);
+#pragma unroll
+    for (int r = 0; r < RP; ++r)
+      if (r < R) X[row * R + r] = x[r];
+  }
+}
+
+template <int RP>
+constexpr int gram_wpb() {
+  int w = 8;
+  while (w > 1 && w * 32 * RP * 8 > 40 * 1024) --w;
+  return w;
+}
+
+int grid_cap(std::int64_t work_warps, int wpb, int num_sms, int per_sm) {
+  const std::int64_t want = (work_warps + wpb - 1) / wpb;
+  return static_cast<int>(std::max<std::int64_t>(1, std::min<std::int64_t>(want, static_cast<std::int64_t>(num_sms) * per_sm)));
+}
+
+}  // namespace
+
+#define P2G_SMALL_DISPATCH(R, CALL)                       \
+  do {                                                    \
+    if ((R) <= 2) {                                       \
+      constexpr int RP_ = 2;                              \
+      CALL;                                               \
+    } else if ((R) <= 4) {                                \
+      constexpr int RP_ = 4;                              \
+      CALL;                                               \
+    } else if ((R) <= 5) {                                \
+      constexpr int RP_ = 5;                              \
+      CALL;                                               \
+    } else if ((R) <= 8) {                                \
+      constexpr int RP_ = 8;                              \
+      CALL;                                               \
+    } else if ((R) <= 10) {                               \
+      constexpr int RP_ = 10;                             \
+      CALL;                                               \
+    } else if ((R) <= 12) {                               \
+      constexpr int RP_ = 12;                             \
+      CALL;                                               \
+    } else if ((R) <= 16) {                               \
+      constexpr int RP_ = 16;                             \
+      CALL;                                               \
+    } else {                                              \
+      throw InvalidArgument("small-rank path needs R <= 16"); \
+    }                                                     \
+  } while (0)
+
+static ShardArgs shard_args_s(p2g_ctx* c) {
+  return ShardArgs{c->srp.get(), c->rp.get(), c->ci.get(), c->val.get(), c->k_end - c->k_begin, c->NR, c->nnz, c->J};
+}
+
+void launch_gram_c(p2g_ctx* c, int R, const double* V, double* Cbuf, cudaStream_t s) {
+  const ShardArgs X = shard_args_s(c);
+  P2G_SMALL_DISPATCH(R, ({
+                       constexpr int WPB = gram_wpb<RP_>();
+                       k_gram_c<RP_, WPB><<<grid_cap(X.K, WPB, c->num_sms, 16), WPB * 32, 0, s>>>(X, R, V, Cbuf);
+                     }));
+  P2G_LAUNCHED(1);
+}
+
+template <int RP>
+static int polar_launch(p2g_ctx* c, std::int64_t K, int R, const double* H, const double* W, const double* Cbuf,
+                        double* Sbuf, double* Ebuf, std::int32_t* flags, double* m1p, int max_blocks, cudaStream_t s) {
+  constexpr int WPB = RP <= 10 ? 4 : 2;
+  constexpr int MP = PolarSmem<RP>::MP;
+  const std::size_t smem = sizeof(double) * (MP * MP + WPB * MP * MP + WPB * PolarSmem<RP>::kPerWarp);
+  auto kern = k_polar_small<RP, WPB>;
+  P2G_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  int per_sm = 0;
+  P2G_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, WPB * 32, smem));
+  const int blocks = grid_cap((K + 31) / 32, WPB, c->num_sms, std::max(per_sm, 1));
+  const int nb = std::min(blocks, max_blocks);
+  kern<<<nb, WPB * 32, smem, s>>>(K, R, H, W, Cbuf, Sbuf, Ebuf, flags, m1p);
+  return nb;
+}
+
+int launch_polar_small(p2g_ctx* c, int R, const double* H, const double* W, const double* Cbuf, double* Sbuf,
+                       double* Ebuf, std::int32_t* flags, double* m1_partials, int max_blocks, cudaStream_t s) {
+  int nb = 0;
+  P2G_SMALL_DISPATCH(R, nb = polar_launch<RP_>(c, c->k_end - c->k_begin, R, H, W, Cbuf, Sbuf, Ebuf, flags,
+                                               m1_partials, max_blocks, s));
+  P2G_LAUNCHED(1);
+  return nb;
+}
+
+void launch_qrows(p2g_ctx* c, int R, const double* H, const double* V, const double* W, const double* Sbuf,
+                  const std::int32_t* flags, double* Q, cudaStream_t s) {
+  const ShardArgs X = shard_args_s(c);
+  P2G_SMALL_DISPATCH(R, ({
+                       constexpr int WPB = RP_ <= 10 ? 8 : 4;
+                       k_qrows<RP_, WPB><<<grid_cap(X.K, WPB, c->num_sms, 16), WPB * 32, 0, s>>>(X, R, H, V, W, Sbuf,
+                                                                                                 flags, Q);
+                     }));
+  P2G_LAUNCHED(1);
+}
+
+template <int RP>
+static void nnls_thread_launch(int R, std::int64_t n, const double* G, const double* B, double* X, int cap,
+                               std::int32_t* err, std::int32_t* redo, std::int32_t* n_redo, cudaStream_t s) {
+  constexpr int WPB = 4;
+  const std::size_t smem = sizeof(double) * (RP * RP + WPB * NnlsThreadSmem<RP>::kPerWarp);
+  auto kern = k_nnls_thread<RP, WPB>;
+  P2G_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  const int blocks = static_cast<int>(std::max<std::int64_t>(1, std::min<std::int64_t>((n + 127) / 128, 148 * 16)));
+  kern<<<blocks, WPB * 32, smem, s>>>(R, n, G, B, X, cap, err, redo, n_redo);
+}
+
+void launch_nnls_thread(int R, std::int64_t n, const double* G, const double* B, double* X, int max_iter,
+                        std::int32_t* err, std::int32_t* redo, std::int32_t* n_redo, cudaStream_t s) {
+  if (n == 0) return;
+  const int cap = max_iter > 0 ? max_iter : 30 * R;
+  P2G_SMALL_DISPATCH(R, nnls_thread_launch<RP_>(R, n, G, B, X, cap, err, redo, n_redo, s));
+  P2G_LAUNCHED(1);
+}
+
+}  // namespace p2g

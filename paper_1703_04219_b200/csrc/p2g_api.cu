@@ -196,9 +196,56 @@ void alloc_state(p2g_ctx* c, int R) {
   c->scal.resize(8);
   c->flags.resize(static_cast<std::size_t>(std::max<std::int64_t>(Ks(c), 1)));
   c->counters.resize(8);
+  c->redo.resize(static_cast<std::size_t>(std::max<std::int64_t>(c->J, Ks(c)) + 1));
+  if (R <= kSmallRankMax) {
+    const std::size_t ks = static_cast<std::size_t>(std::max<std::int64_t>(Ks(c), 1));
+    const std::size_t nt = static_cast<std::size_t>(R) * (R + 1) / 2;
+    c->Cbuf.resize(ks * nt);
+    c->Sbuf.resize(ks * nt);
+    c->Ebuf.resize(ks * RR);
+  }
 }
 
 constexpr int kMaxPartials = 148 * 8;
+
+/// Procrustes step over the shard (solver.hpp:279-284) fused with the
+/// mode-1 partials: writes Q, flags and per-block m1 partials into `part`;
+/// returns the number of partials.  R <= 16: K1a/K1b/K1c (k_small.cu);
+/// larger R: the warp-per-subject K1 (k_procrustes.cu).  Flagged subjects go
+/// through the accurate Jacobi-SVD path either way.
+int procrustes_step(p2g_ctx* c, double* part) {
+  const int R = c->R;
+  const std::size_t RR = static_cast<std::size_t>(R) * R;
+  cudaStream_t s = c->stream;
+  int n1 = 0, n2 = 0;
+  const double* E = nullptr;
+  if (R <= kSmallRankMax) {
+    {
+      Phase ph(c, "gram_c");
+      launch_gram_c(c, R, c->V.get(), c->Cbuf.get(), s);
+    }
+    {
+      Phase ph(c, "polar");
+      n1 = launch_polar_small(c, R, c->H.get(), c->W.get(), c->Cbuf.get(), c->Sbuf.get(), c->Ebuf.get(),
+                              c->flags.get(), part, kMaxPartials, s);
+    }
+    {
+      Phase ph(c, "qrows");
+      launch_qrows(c, R, c->H.get(), c->V.get(), c->W.get(), c->Sbuf.get(), c->flags.get(), c->Q.get(), s);
+    }
+    E = c->Ebuf.get();
+  } else {
+    Phase ph(c, "procrustes");
+    n1 = launch_procrustes(c, R, c->H.get(), c->V.get(), c->W.get(), c->Q.get(), c->flags.get(), part, kMaxPartials,
+                           s);
+  }
+  {
+    Phase ph(c, "procrustes_accurate");
+    n2 = launch_procrustes_accurate(c, R, c->H.get(), c->V.get(), c->W.get(), c->Q.get(), c->flags.get(),
+                                    part + static_cast<std::size_t>(n1) * RR, E, s);
+  }
+  return n1 + n2;
+}
 
 /// gram(W) and the cross term over this shard, allreduced -> c->gwc.
 void gram_w_cross(p2g_ctx* c, const double* m3_or_null) {
@@ -255,21 +302,11 @@ IterOut iterate(p2g_ctx* c, bool nonneg, int iter) {
   const std::size_t RR = static_cast<std::size_t>(R) * R;
   cudaStream_t s = c->stream;
   P2G_CUDA(cudaMemsetAsync(c->counters.get(), 0, sizeof(std::int32_t) * 8, s));
-  int n1 = 0, n2 = 0;
   {
     DBuf<double>& part = scratch_partials(c, static_cast<std::size_t>(kMaxPartials + 4 * 148) * RR);
-    {
-      Phase ph(c, "procrustes");
-      n1 = launch_procrustes(c, R, c->H.get(), c->V.get(), c->W.get(), c->Q.get(), c->flags.get(), part.get(),
-                             kMaxPartials, s);
-    }
-    {
-      Phase ph(c, "procrustes_accurate");
-      n2 = launch_procrustes_accurate(c, R, c->H.get(), c->V.get(), c->W.get(), c->Q.get(), c->flags.get(),
-                                      part.get() + static_cast<std::size_t>(n1) * RR, s);
-    }
+    const int np = procrustes_step(c, part.get());
     Phase ph(c, "m1_reduce");
-    reduce_partials(part.get(), n1 + n2, static_cast<std::int64_t>(RR), c->m1.get(), s);
+    reduce_partials(part.get(), np, static_cast<std::int64_t>(RR), c->m1.get(), s);
     allreduce(c, c->m1.get(), RR);
   }
   {
@@ -285,7 +322,7 @@ IterOut iterate(p2g_ctx* c, bool nonneg, int iter) {
   {
     Phase ph(c, "update_v");
     if (nonneg) {
-      launch_nnls_rows(R, c->J, c->G2.get(), c->M2.get(), c->V.get(), 0, c->counters.get() + 1, s);
+      launch_nnls_rows(R, c->J, c->G2.get(), c->M2.get(), c->V.get(), 0, c->counters.get() + 1, c->redo.get(), s);
     } else {
       launch_pinv(R, c->G2.get(), c->pinvbuf.get(), s);
       launch_rows_times(R, c->J, c->M2.get(), c->pinvbuf.get(), c->V.get(), s);
@@ -301,7 +338,7 @@ IterOut iterate(p2g_ctx* c, bool nonneg, int iter) {
   {
     Phase ph(c, "update_w");
     if (nonneg) {
-      launch_nnls_rows(R, Ks(c), c->G3.get(), c->m3.get(), c->W.get(), 0, c->counters.get() + 1, s);
+      launch_nnls_rows(R, Ks(c), c->G3.get(), c->m3.get(), c->W.get(), 0, c->counters.get() + 1, c->redo.get(), s);
     } else {
       launch_pinv(R, c->G3.get(), c->pinvbuf.get(), s);
       launch_rows_times(R, Ks(c), c->m3.get(), c->pinvbuf.get(), c->W.get(), s);
@@ -607,11 +644,8 @@ extern "C" int p2g_procrustes(p2g_ctx* c, int32_t R, const double* H, const doub
     const std::size_t RR = static_cast<std::size_t>(R) * R;
     P2G_CUDA(cudaMemsetAsync(c->counters.get(), 0, sizeof(std::int32_t) * 8, c->stream));
     DBuf<double>& part = scratch_partials(c, static_cast<std::size_t>(kMaxPartials + 4 * 148) * RR);
-    const int n1 = launch_procrustes(c, R, c->H.get(), c->V.get(), c->W.get(), c->Q.get(), c->flags.get(), part.get(),
-                                     kMaxPartials, c->stream);
-    const int n2 = launch_procrustes_accurate(c, R, c->H.get(), c->V.get(), c->W.get(), c->Q.get(), c->flags.get(),
-                                              part.get() + static_cast<std::size_t>(n1) * RR, c->stream);
-    reduce_partials(part.get(), n1 + n2, static_cast<std::int64_t>(RR), c->m1.get(), c->stream);
+    const int np = procrustes_step(c, part.get());
+    reduce_partials(part.get(), np, static_cast<std::int64_t>(RR), c->m1.get(), c->stream);
     allreduce(c, c->m1.get(), RR);
     std::int32_t cnt[8];
     P2G_CUDA(cudaMemcpyAsync(cnt, c->counters.get(), sizeof(cnt), cudaMemcpyDeviceToHost, c->stream));
@@ -818,7 +852,7 @@ extern "C" int p2g_cp_als_iteration(p2g_ctx* c, int64_t K, int64_t J, int32_t R,
     const std::size_t RR = static_cast<std::size_t>(R) * R;
     cudaStream_t s = c->stream;
     DBuf<double> dH, dV, dW, m1, M2, m3, gW, gV, gH, G2, G3, nH, nV, gvraw, pinv, part, gwc;
-    DBuf<std::int32_t> err;
+    DBuf<std::int32_t> err, work;
     dH.resize(RR);
     dV.resize(static_cast<std::size_t>(std::max<std::int64_t>(J, 1)) * R);
     dW.resize(static_cast<std::size_t>(std::max<std::int64_t>(K, 1)) * R);
@@ -867,7 +901,8 @@ extern "C" int p2g_cp_als_iteration(p2g_ctx* c, int64_t K, int64_t J, int32_t R,
     // V step (cp.hpp:115-123)
     packed_mode(c, 2, K, J, R, d, dH.get(), dV.get(), dW.get(), M2.get());
     if (nonneg) {
-      launch_nnls_rows(R, J, G2.get(), M2.get(), dV.get(), 0, err.get(), s);
+      work.resize(static_cast<std::size_t>(std::max<std::int64_t>(J, K)) + 1);
+      launch_nnls_rows(R, J, G2.get(), M2.get(), dV.get(), 0, err.get(), work.get(), s);
     } else {
       launch_pinv(R, G2.get(), pinv.get(), s);
       launch_rows_times(R, J, M2.get(), pinv.get(), dV.get(), s);
@@ -879,7 +914,8 @@ extern "C" int p2g_cp_als_iteration(p2g_ctx* c, int64_t K, int64_t J, int32_t R,
     // W step (cp.hpp:126-133)
     packed_mode(c, 3, K, J, R, d, dH.get(), dV.get(), dW.get(), m3.get());
     if (nonneg) {
-      launch_nnls_rows(R, K, G3.get(), m3.get(), dW.get(), 0, err.get(), s);
+      work.resize(static_cast<std::size_t>(std::max<std::int64_t>(J, K)) + 1);
+      launch_nnls_rows(R, K, G3.get(), m3.get(), dW.get(), 0, err.get(), work.get(), s);
     } else {
       launch_pinv(R, G3.get(), pinv.get(), s);
       launch_rows_times(R, K, m3.get(), pinv.get(), dW.get(), s);
@@ -924,7 +960,9 @@ extern "C" int p2g_nnls_rowwise(p2g_ctx* c, const double* G, const double* B, in
     upload_colmajor(c, G, R, R, dG.get());
     P2G_CUDA(cudaStreamSynchronize(c->stream));
     upload_colmajor(c, B, n, R, dB.get());
-    launch_nnls_rows(R, n, dG.get(), dB.get(), dX.get(), max_iter, err.get(), c->stream);
+    DBuf<std::int32_t> work;
+    work.resize(static_cast<std::size_t>(n) + 1);
+    launch_nnls_rows(R, n, dG.get(), dB.get(), dX.get(), max_iter, err.get(), work.get(), c->stream);
     std::int32_t herr = 0;
     P2G_CUDA(cudaMemcpyAsync(&herr, err.get(), sizeof(herr), cudaMemcpyDeviceToHost, c->stream));
     P2G_CUDA(cudaStreamSynchronize(c->stream));

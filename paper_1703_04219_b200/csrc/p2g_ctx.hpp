@@ -120,6 +120,9 @@ struct p2g_ctx {
   p2g::DBuf<std::int32_t> fb_list;    // compacted fallback subject ids
   p2g::DBuf<std::int32_t> counters;   // [0]=n_fallback, [1]=nnls error, ...
   p2g::DBuf<double> acc_scratch;      // accurate Procrustes path slabs
+  p2g::DBuf<double> Cbuf, Sbuf, Ebuf; // small-R pipeline: per-subject packed C, S; E of flagged subjects
+  p2g::DBuf<std::int32_t> redo;       // NNLS rows re-solved by the warp (pinv) kernel
+  p2g::DBuf<double> m2part;           // per-range J x R partials of the on-chip mode-2 kernel
   bool state_valid = false;
 
   // Timing.
@@ -141,8 +144,18 @@ int launch_procrustes(p2g_ctx* c, int R, const double* H, const double* V, const
 // Accurate Jacobi-SVD path over the subjects flagged P2G_FLAG_ACCURATE;
 // writes one R x R m1 partial per block (count = procrustes_accurate_blocks).
 int launch_procrustes_accurate(p2g_ctx* c, int R, const double* H, const double* V, const double* W, double* Q,
-                               std::int32_t* flags, double* m1_partials, cudaStream_t s);
+                               std::int32_t* flags, double* m1_partials, const double* Ebuf, cudaStream_t s);
 int procrustes_accurate_blocks(p2g_ctx* c, int R);
+
+// Small-rank pipeline (k_small.cu, R <= 16).
+constexpr int kSmallRankMax = 16;
+void launch_gram_c(p2g_ctx* c, int R, const double* V, double* Cbuf, cudaStream_t s);
+int launch_polar_small(p2g_ctx* c, int R, const double* H, const double* W, const double* Cbuf, double* Sbuf,
+                       double* Ebuf, std::int32_t* flags, double* m1_partials, int max_blocks, cudaStream_t s);
+void launch_qrows(p2g_ctx* c, int R, const double* H, const double* V, const double* W, const double* Sbuf,
+                  const std::int32_t* flags, double* Q, cudaStream_t s);
+void launch_nnls_thread(int R, std::int64_t n, const double* G, const double* B, double* X, int max_iter,
+                        std::int32_t* err, std::int32_t* redo, std::int32_t* n_redo, cudaStream_t s);
 void launch_mode2(p2g_ctx* c, int R, const double* Q, const double* H, const double* W, const double* nH,
                   double* M2, cudaStream_t s);
 void launch_mode3(p2g_ctx* c, int R, const double* Q, const double* H, const double* V, double* m3,
@@ -165,8 +178,9 @@ void launch_packed_mode2(std::int64_t K, std::int64_t J, int R, const std::int64
 int gram_partials(int R, std::int64_t n, const double* A, const double* B, double* partials, int max_blocks,
                   cudaStream_t s);  // returns #partials; each partial R*R (+1 cross if B)
 void reduce_partials(const double* partials, int nparts, std::int64_t len, double* out, cudaStream_t s);
+// work: n+1 ints of scratch (thread-per-row path for R <= 16) or null.
 void launch_nnls_rows(int R, std::int64_t n, const double* G, const double* B, double* X, int max_iter,
-                      std::int32_t* err, cudaStream_t s);
+                      std::int32_t* err, std::int32_t* work, cudaStream_t s);
 void launch_rows_times(int R, std::int64_t n, const double* B, const double* P, double* X,
                        cudaStream_t s);  // X = B * P (row-major rows)
 void launch_pinv(int n, const double* G, double* out, cudaStream_t s);
