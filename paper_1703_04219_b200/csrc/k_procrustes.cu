@@ -43,6 +43,8 @@ struct K1Args {
   std::int64_t max_rows;
   std::int32_t* counters;  // [2] = non-finite operand seen
   const double* Ebuf;      // accurate path preconditioner (K x R x R) or null
+  double* Shat;            // Q-free outputs (K x R x R) or null: Q = A Shat + L Chat
+  double* Chat;
 };
 
 template <int RP>
@@ -449,6 +451,58 @@ __global__ void __launch_bounds__(WPB * 32) k_procrustes_accurate(K1Args a, doub
       }
       __syncwarp();
     }
+    // Q-free form for the streaming kernels: Q = A Shat + L Chat with
+    //   Shat = sum_c V_c V_c^T / sigma_c - sum_c V_c / sigma_c (B TN Vn^T)_c
+    //   Chat = Vn TN Vn^T
+    // (strong c; sigma of the unscaled A = sig * amax).
+    if (a.Shat) {
+      double* Sh = a.Shat + k * RR;
+      double* Ch = a.Chat + k * RR;
+      for (int e = lane; e < RR; e += 32) {
+        const int i = e / R, j = e - (e / R) * R;
+        double sh = 0.0, chv = 0.0;
+        for (int c = 0; c < R; ++c) {
+          const bool strong_c = amax != 0.0 && sig[c] * sig[c] > kNullRatio * smax2;
+          if (!strong_c) continue;
+          double vj = Vj[j * R + c];
+          if (nn > 0) {  // subtract (B TN Vn^T)(c, j)
+            int x = 0;
+            for (int d = 0; d < R; ++d) {
+              const bool dn = !(amax != 0.0 && sig[d] * sig[d] > kNullRatio * smax2);
+              if (!dn) continue;
+              double btn = 0.0;  // (B TN)(c, x)
+              int y = 0;
+              for (int d2 = 0; d2 < R; ++d2) {
+                const bool dn2 = !(amax != 0.0 && sig[d2] * sig[d2] > kNullRatio * smax2);
+                if (!dn2) continue;
+                btn = fma(B[c * R + d2], TN[y * nn + x], btn);
+                ++y;
+              }
+              vj -= btn * Vj[j * R + d];
+              ++x;
+            }
+          }
+          sh = fma(Vj[i * R + c] / (sig[c] * amax), vj, sh);
+        }
+        if (nn > 0) {
+          int x = 0;
+          for (int d = 0; d < R; ++d) {
+            const bool dn = !(amax != 0.0 && sig[d] * sig[d] > kNullRatio * smax2);
+            if (!dn) continue;
+            int y = 0;
+            for (int d2 = 0; d2 < R; ++d2) {
+              const bool dn2 = !(amax != 0.0 && sig[d2] * sig[d2] > kNullRatio * smax2);
+              if (!dn2) continue;
+              chv = fma(Vj[i * R + d] * TN[x * nn + y], Vj[j * R + d2], chv);
+              ++y;
+            }
+            ++x;
+          }
+        }
+        Sh[e] = sh;
+        Ch[e] = chv;
+      }
+    }
     // Q rows (lane = row), then m1_k = Q^T XV D through 32-row chunks.
     for (int b = 0; b < I; b += 32) {
       const int i = b + lane;
@@ -503,7 +557,8 @@ __global__ void __launch_bounds__(WPB * 32) k_procrustes_accurate(K1Args a, doub
       }
       __syncwarp();
       double* qdst = a.Q + (r0 + b) * R;
-      for (int idx = lane; idx < nr * R; idx += 32) qdst[idx] = qch[(idx / R) * RP + (idx - (idx / R) * R)];
+      if (a.Q)
+        for (int idx = lane; idx < nr * R; idx += 32) qdst[idx] = qch[(idx / R) * RP + (idx - (idx / R) * R)];
       for (int e = lane; e < RR; e += 32) {
         const int x = e / R, y = e - (e / R) * R;
         double acc = M1[e];
@@ -621,9 +676,12 @@ int launch_procrustes(p2g_ctx* c, int R, const double* H, const double* V, const
 }
 
 int launch_procrustes_accurate(p2g_ctx* c, int R, const double* H, const double* V, const double* W, double* Q,
-                               std::int32_t* flags, double* m1_partials, const double* Ebuf, cudaStream_t s) {
+                               std::int32_t* flags, double* m1_partials, const double* Ebuf, double* Shat,
+                               double* Chat, cudaStream_t s) {
   K1Args a{};
   a.Ebuf = Ebuf;
+  a.Shat = Shat;
+  a.Chat = Chat;
   a.X = ShardArgs{c->srp.get(), c->rp.get(), c->ci.get(), c->val.get(), c->k_end - c->k_begin, c->NR, c->nnz, c->J};
   a.R = R;
   a.H = H;

@@ -437,13 +437,64 @@ __global__ void __launch_bounds__(WPB * 32)
 }
 
 // ---------------------------------------------------------------------------
-// K1c: Q_k rows = XV P, P = D H^T S (fast-path subjects only).
+// Q-free forms.  With P_k = D H^T S_k (S_k = G_k^{-1/2}, packed symmetric,
+// fast path) or P_k = D H^T Shat_k plus the completion term L Chat_k
+// (accurate / rank-deficient subjects, full R x R in Shat/Chat), the
+// Procrustes factor is Q_k = (X_k V) P_k + L Chat_k with V, H, W the factors
+// the Procrustes step used.  Mode 2 and mode 3 rebuild Q rows on the fly from
+// the CSR instead of reading a materialised Q (4 GB at cfg2), and mode 3 also
+// emits next iteration's Gram C = (X_k V_t)^T (X_k V_t).
 // ---------------------------------------------------------------------------
+
+/// Builds P = D H^T S for subject k in shared memory (R x R row-major) and
+/// returns whether the completion term applies (flagged subject).
+template <int RP>
+__device__ __forceinline__ bool build_p(int R, std::int64_t k, std::int32_t flag, const double* __restrict__ Sbuf,
+                                        const double* __restrict__ Shat, const double* Hs, const double* __restrict__ W,
+                                        double* S, double* P, int lane) {
+  const int RR = R * R;
+  const bool flagged = flag != P2G_FLAG_FULL_RANK;
+  if (!flagged) {
+    const int nt = R * (R + 1) / 2;
+    for (int e = lane; e < nt; e += 32) {
+      int x = 0;
+      while ((x + 1) * (x + 2) / 2 <= e) ++x;
+      const int y = e - x * (x + 1) / 2;
+      const double v = Sbuf[k * nt + e];
+      S[x * R + y] = v;
+      S[y * R + x] = v;
+    }
+  } else {
+    for (int e = lane; e < RR; e += 32) S[e] = Shat[k * RR + e];
+  }
+  __syncwarp();
+  for (int e = lane; e < RR; e += 32) {
+    const int a = e / R, b = e - (e / R) * R;
+    double acc = 0.0;
+    for (int c = 0; c < R; ++c) acc = fma(Hs[c * R + a], S[c * R + b], acc);
+    P[e] = acc * W[k * R + a];
+  }
+  __syncwarp();
+  return flagged;
+}
+
+/// Z = A * B (R x R, row-major smem), warp-cooperative.
+__device__ __forceinline__ void small_mm(int R, const double* A, const double* B, double* Z, int lane) {
+  for (int e = lane; e < R * R; e += 32) {
+    const int a = e / R, b = e - (e / R) * R;
+    double acc = 0.0;
+    for (int c = 0; c < R; ++c) acc = fma(A[a * R + c], B[c * R + b], acc);
+    Z[e] = acc;
+  }
+  __syncwarp();
+}
+
+/// Export: Q rows of every subject (p2g_fit Q_out, p2g_procrustes).
 template <int RP, int WPB>
 __global__ void __launch_bounds__(WPB * 32)
     k_qrows(ShardArgs X, int R, const double* __restrict__ H, const double* __restrict__ V,
-            const double* __restrict__ W, const double* __restrict__ Sbuf, const std::int32_t* __restrict__ flags,
-            double* __restrict__ Q) {
+            const double* __restrict__ W, const double* __restrict__ Sbuf, const double* __restrict__ Shat,
+            const double* __restrict__ Chat, const std::int32_t* __restrict__ flags, double* __restrict__ Q) {
   __shared__ double Hs[RP * RP];
   __shared__ double Ps[WPB][RP * RP];
   __shared__ double Ss[WPB][RP * RP];
@@ -454,28 +505,12 @@ __global__ void __launch_bounds__(WPB * 32)
   double* P = Ps[wid];
   double* S = Ss[wid];
   double* ch = chunk[wid];
-  const int nt = R * (R + 1) / 2;
   const std::int64_t nwarps = static_cast<std::int64_t>(gridDim.x) * WPB;
   for (std::int64_t k = static_cast<std::int64_t>(blockIdx.x) * WPB + wid; k < X.K; k += nwarps) {
-    if (flags[k] != P2G_FLAG_FULL_RANK) continue;
+    const std::int32_t flag = flags[k];
+    const bool flagged = build_p<RP>(R, k, flag, Sbuf, Shat, Hs, W, S, P, lane);
     const std::int64_t r0 = X.srp[k];
     const int I = static_cast<int>(X.srp[k + 1] - r0);
-    for (int e = lane; e < nt; e += 32) {
-      int x = 0;
-      while ((x + 1) * (x + 2) / 2 <= e) ++x;
-      const int y = e - x * (x + 1) / 2;
-      const double v = Sbuf[k * nt + e];
-      S[x * R + y] = v;
-      S[y * R + x] = v;
-    }
-    __syncwarp();
-    for (int e = lane; e < R * R; e += 32) {  // P = D H^T S
-      const int a = e / R, b = e - (e / R) * R;
-      double acc = 0.0;
-      for (int c = 0; c < R; ++c) acc = fma(Hs[c * R + a], S[c * R + b], acc);
-      P[e] = acc * W[k * R + a];
-    }
-    __syncwarp();
     for (int b0 = 0; b0 < I; b0 += 32) {
       const int i = b0 + lane;
       const int nr = min(32, I - b0);
@@ -485,7 +520,7 @@ __global__ void __launch_bounds__(WPB * 32)
 #pragma unroll
         for (int c = 0; c < RP; ++c) {
           if (c < R) {
-            double q = 0.0;
+            double q = (flagged && i < R) ? Chat[k * R * R + i * R + c] : 0.0;
 #pragma unroll
             for (int r = 0; r < RP; ++r)
               if (r < R) q = fma(xv[r], P[r * R + c], q);
@@ -498,6 +533,173 @@ __global__ void __launch_bounds__(WPB * 32)
       for (int idx = lane; idx < nr * R; idx += 32) qdst[idx] = ch[(idx / R) * RP + (idx - (idx / R) * R)];
       __syncwarp();
     }
+  }
+}
+
+/// mode 2 (mttkrp.hpp:111-138) in Q-free form: U' rows = Q rows H_t diag(W o nH)
+/// = xv Z (+ Chat_i HW), Z = P H_t diag(W o nH); scattered with L2 fp64 reductions.
+template <int RP, int WPB>
+__global__ void __launch_bounds__(WPB * 32)
+    k_mode2_qf(ShardArgs X, int R, const double* __restrict__ Hprev, const double* __restrict__ Vprev,
+               const double* __restrict__ Wprev, const double* __restrict__ Ht, const double* __restrict__ nH,
+               const double* __restrict__ Sbuf, const double* __restrict__ Shat, const double* __restrict__ Chat,
+               const std::int32_t* __restrict__ flags, double* __restrict__ M2) {
+  __shared__ double Hs[RP * RP];
+  __shared__ double Ws[WPB][4][RP * RP];  // S, P, HW, Z
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int e = threadIdx.x; e < R * R; e += blockDim.x) Hs[e] = Hprev[e];
+  __syncthreads();
+  double* S = Ws[wid][0];
+  double* P = Ws[wid][1];
+  double* HW = Ws[wid][2];
+  double* Z = Ws[wid][3];
+  const int RR = R * R;
+  const std::int64_t nwarps = static_cast<std::int64_t>(gridDim.x) * WPB;
+  for (std::int64_t k = static_cast<std::int64_t>(blockIdx.x) * WPB + wid; k < X.K; k += nwarps) {
+    const std::int32_t flag = flags[k];
+    const bool flagged = build_p<RP>(R, k, flag, Sbuf, Shat, Hs, Wprev, S, P, lane);
+    for (int e = lane; e < RR; e += 32) {
+      const int c = e - (e / R) * R;
+      HW[e] = Ht[e] * Wprev[k * R + c] * nH[c];
+    }
+    __syncwarp();
+    small_mm(R, P, HW, Z, lane);
+    if (flagged) small_mm(R, Chat + k * RR, HW, S, lane);  // S <- Chat HW (rows < R)
+    const std::int64_t r0 = X.srp[k];
+    const int I = static_cast<int>(X.srp[k + 1] - r0);
+    for (int i = lane; i < I; i += 32) {
+      double xv[RP];
+      const std::int64_t p0 = X.rp[r0 + i], p1 = X.rp[r0 + i + 1];
+      dev::csr_row_times<RP>(xv, X.ci, X.val, p0, p1, Vprev, R);
+      double u[RP];
+#pragma unroll
+      for (int c = 0; c < RP; ++c) {
+        double acc = (flagged && i < R && c < R) ? S[i * R + c] : 0.0;
+        if (c < R) {
+#pragma unroll
+          for (int a = 0; a < RP; ++a)
+            if (a < R) acc = fma(xv[a], Z[a * R + c], acc);
+        }
+        u[c] = acc;
+      }
+      for (std::int64_t p = p0; p < p1; ++p) {
+        const int j = __ldg(X.ci + p);
+        const double v = __ldg(X.val + p);
+        double* dst = M2 + static_cast<std::int64_t>(j) * R;
+#pragma unroll
+        for (int c = 0; c < RP; ++c)
+          if (c < R) atomicAdd(dst + c, v * u[c]);
+      }
+    }
+    __syncwarp();
+  }
+}
+
+/// mode 3 (mttkrp.hpp:143-166) in Q-free form, fused with next iteration's
+/// Gram: m3(k,c) = sum_i (xv_prev Z3 + Chat_i H_t)_c (xv_new)_c with
+/// Z3 = P H_t, and C_k = sum_i xv_new^T xv_new (packed lower) into Cnext.
+template <int RP, int WPB>
+__global__ void __launch_bounds__(WPB * 32)
+    k_mode3_qf(ShardArgs X, int R, const double* __restrict__ Hprev, const double* __restrict__ Vprev,
+               const double* __restrict__ Wprev, const double* __restrict__ Ht, const double* __restrict__ Vt,
+               const double* __restrict__ Sbuf, const double* __restrict__ Shat, const double* __restrict__ Chat,
+               const std::int32_t* __restrict__ flags, double* __restrict__ M3, double* __restrict__ Cnext) {
+  __shared__ double Hs[RP * RP];
+  __shared__ double Hts[RP * RP];
+  __shared__ double Ws[WPB][3][RP * RP];  // S, P, Z
+  __shared__ double chunk[WPB][32 * RP];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
+    Hs[e] = Hprev[e];
+    Hts[e] = Ht[e];
+  }
+  __syncthreads();
+  double* S = Ws[wid][0];
+  double* P = Ws[wid][1];
+  double* Z = Ws[wid][2];
+  double* ch = chunk[wid];
+  const int RR = R * R;
+  constexpr int NTP = RP * (RP + 1) / 2;
+  constexpr int kTri = (NTP + 31) / 32;
+  const int nt = R * (R + 1) / 2;
+  int ea[kTri], eb[kTri];
+#pragma unroll
+  for (int t = 0; t < kTri; ++t) {
+    const int e = lane + 32 * t;
+    int x = 0;
+    while ((x + 1) * (x + 2) / 2 <= e) ++x;
+    ea[t] = x;
+    eb[t] = e - x * (x + 1) / 2;
+  }
+  const std::int64_t nwarps = static_cast<std::int64_t>(gridDim.x) * WPB;
+  for (std::int64_t k = static_cast<std::int64_t>(blockIdx.x) * WPB + wid; k < X.K; k += nwarps) {
+    const std::int32_t flag = flags[k];
+    const bool flagged = build_p<RP>(R, k, flag, Sbuf, Shat, Hs, Wprev, S, P, lane);
+    small_mm(R, P, Hts, Z, lane);
+    if (flagged) small_mm(R, Chat + k * RR, Hts, S, lane);  // S <- Chat H_t
+    const std::int64_t r0 = X.srp[k];
+    const int I = static_cast<int>(X.srp[k + 1] - r0);
+    double part[RP];
+#pragma unroll
+    for (int c = 0; c < RP; ++c) part[c] = 0.0;
+    double cacc[kTri];
+#pragma unroll
+    for (int t = 0; t < kTri; ++t) cacc[t] = 0.0;
+    for (int b0 = 0; b0 < I; b0 += 32) {
+      const int i = b0 + lane;
+      const int nr = min(32, I - b0);
+      double xn[RP];
+      if (i < I) {
+        const std::int64_t p0 = X.rp[r0 + i], p1 = X.rp[r0 + i + 1];
+        double xp[RP];
+#pragma unroll
+        for (int r = 0; r < RP; ++r) {
+          xp[r] = 0.0;
+          xn[r] = 0.0;
+        }
+        for (std::int64_t p = p0; p < p1; ++p) {  // both gathers share the entry stream
+          const int j = __ldg(X.ci + p);
+          const double v = __ldg(X.val + p);
+          dev::axpy_row<RP>(xp, Vprev + static_cast<std::int64_t>(j) * R, v, R);
+          dev::axpy_row<RP>(xn, Vt + static_cast<std::int64_t>(j) * R, v, R);
+        }
+#pragma unroll
+        for (int c = 0; c < RP; ++c) {
+          if (c < R) {
+            double qh = (flagged && i < R) ? S[i * R + c] : 0.0;
+#pragma unroll
+            for (int a = 0; a < RP; ++a)
+              if (a < R) qh = fma(xp[a], Z[a * R + c], qh);
+            part[c] = fma(qh, xn[c], part[c]);
+          }
+        }
+      } else {
+#pragma unroll
+        for (int r = 0; r < RP; ++r) xn[r] = 0.0;
+      }
+#pragma unroll
+      for (int r = 0; r < RP; ++r) ch[lane * RP + r] = xn[r];
+      __syncwarp();
+#pragma unroll
+      for (int t = 0; t < kTri; ++t) {
+        if (lane + 32 * t < nt) {
+          double acc = cacc[t];
+          for (int rr = 0; rr < nr; ++rr) acc = fma(ch[rr * RP + ea[t]], ch[rr * RP + eb[t]], acc);
+          cacc[t] = acc;
+        }
+      }
+      __syncwarp();
+    }
+#pragma unroll
+    for (int c = 0; c < RP; ++c) {
+      if (c < R) {
+        const double t = dev::warp_sum(part[c]);
+        if (lane == 0) M3[k * R + c] = t;
+      }
+    }
+#pragma unroll
+    for (int t = 0; t < kTri; ++t)
+      if (lane + 32 * t < nt) Cnext[k * nt + lane + 32 * t] = cacc[t];
   }
 }
 
@@ -731,12 +933,37 @@ int launch_polar_small(p2g_ctx* c, int R, const double* H, const double* W, cons
 }
 
 void launch_qrows(p2g_ctx* c, int R, const double* H, const double* V, const double* W, const double* Sbuf,
-                  const std::int32_t* flags, double* Q, cudaStream_t s) {
+                  const double* Shat, const double* Chat, const std::int32_t* flags, double* Q, cudaStream_t s) {
   const ShardArgs X = shard_args_s(c);
   P2G_SMALL_DISPATCH(R, ({
                        constexpr int WPB = RP_ <= 10 ? 8 : 4;
-                       k_qrows<RP_, WPB><<<grid_cap(X.K, WPB, c->num_sms, 16), WPB * 32, 0, s>>>(X, R, H, V, W, Sbuf,
-                                                                                                 flags, Q);
+                       k_qrows<RP_, WPB><<<grid_cap(X.K, WPB, c->num_sms, 16), WPB * 32, 0, s>>>(
+                           X, R, H, V, W, Sbuf, Shat, Chat, flags, Q);
+                     }));
+  P2G_LAUNCHED(1);
+}
+
+void launch_mode2_qf(p2g_ctx* c, int R, const double* Hprev, const double* Vprev, const double* Wprev,
+                     const double* Ht, const double* nH, const double* Sbuf, const double* Shat, const double* Chat,
+                     const std::int32_t* flags, double* M2, cudaStream_t s) {
+  const ShardArgs X = shard_args_s(c);
+  P2G_CUDA(cudaMemsetAsync(M2, 0, sizeof(double) * c->J * R, s));
+  P2G_SMALL_DISPATCH(R, ({
+                       constexpr int WPB = RP_ <= 10 ? 8 : 4;
+                       k_mode2_qf<RP_, WPB><<<grid_cap(X.K, WPB, c->num_sms, 16), WPB * 32, 0, s>>>(
+                           X, R, Hprev, Vprev, Wprev, Ht, nH, Sbuf, Shat, Chat, flags, M2);
+                     }));
+  P2G_LAUNCHED(1);
+}
+
+void launch_mode3_qf(p2g_ctx* c, int R, const double* Hprev, const double* Vprev, const double* Wprev,
+                     const double* Ht, const double* Vt, const double* Sbuf, const double* Shat, const double* Chat,
+                     const std::int32_t* flags, double* M3, double* Cnext, cudaStream_t s) {
+  const ShardArgs X = shard_args_s(c);
+  P2G_SMALL_DISPATCH(R, ({
+                       constexpr int WPB = RP_ <= 10 ? 8 : 4;
+                       k_mode3_qf<RP_, WPB><<<grid_cap(X.K, WPB, c->num_sms, 16), WPB * 32, 0, s>>>(
+                           X, R, Hprev, Vprev, Wprev, Ht, Vt, Sbuf, Shat, Chat, flags, M3, Cnext);
                      }));
   P2G_LAUNCHED(1);
 }

@@ -197,73 +197,91 @@ void alloc_state(p2g_ctx* c, int R) {
   c->flags.resize(static_cast<std::size_t>(std::max<std::int64_t>(Ks(c), 1)));
   c->counters.resize(8);
   c->redo.resize(static_cast<std::size_t>(std::max<std::int64_t>(c->J, Ks(c)) + 1));
+  c->Hp.resize(RR);
+  c->Vp.resize(static_cast<std::size_t>(c->J) * R);
+  c->Wp.resize(static_cast<std::size_t>(std::max<std::int64_t>(Ks(c), 1)) * R);
   if (R <= kSmallRankMax) {
     const std::size_t ks = static_cast<std::size_t>(std::max<std::int64_t>(Ks(c), 1));
     const std::size_t nt = static_cast<std::size_t>(R) * (R + 1) / 2;
     c->Cbuf.resize(ks * nt);
     c->Sbuf.resize(ks * nt);
     c->Ebuf.resize(ks * RR);
+    c->Chat.resize(ks * RR);
   }
+}
+
+template <typename T>
+void swap_buf(DBuf<T>& a, DBuf<T>& b) {
+  std::swap(a.p, b.p);
+  std::swap(a.n, b.n);
 }
 
 constexpr int kMaxPartials = 148 * 8;
 
-/// Procrustes step over the shard (solver.hpp:279-284) fused with the
-/// mode-1 partials: writes Q, flags and per-block m1 partials into `part`;
-/// returns the number of partials.  R <= 16: K1a/K1b/K1c (k_small.cu);
-/// larger R: the warp-per-subject K1 (k_procrustes.cu).  Flagged subjects go
-/// through the accurate Jacobi-SVD path either way.
+bool small_rank(const p2g_ctx* c) { return c->R <= kSmallRankMax; }
+
+/// Procrustes step over the shard (solver.hpp:279-284) with the factors
+/// c->H, c->V, c->W, fused with the mode-1 partials (into `part`; returns
+/// their count).  R <= 16 (Q-free): Gram C (unless mode 3 already produced
+/// it), thread-per-subject polar factor -> S_k, accurate path -> Shat/Chat;
+/// Q is not materialised.  Larger R: the warp-per-subject K1 writes Q.
+/// Flagged subjects go through the accurate Jacobi-SVD path either way.
 int procrustes_step(p2g_ctx* c, double* part) {
   const int R = c->R;
   const std::size_t RR = static_cast<std::size_t>(R) * R;
   cudaStream_t s = c->stream;
   int n1 = 0, n2 = 0;
-  const double* E = nullptr;
-  if (R <= kSmallRankMax) {
-    {
+  if (small_rank(c)) {
+    if (!c->c_valid) {
       Phase ph(c, "gram_c");
       launch_gram_c(c, R, c->V.get(), c->Cbuf.get(), s);
+      c->c_valid = true;
     }
     {
       Phase ph(c, "polar");
       n1 = launch_polar_small(c, R, c->H.get(), c->W.get(), c->Cbuf.get(), c->Sbuf.get(), c->Ebuf.get(),
                               c->flags.get(), part, kMaxPartials, s);
     }
-    {
-      Phase ph(c, "qrows");
-      launch_qrows(c, R, c->H.get(), c->V.get(), c->W.get(), c->Sbuf.get(), c->flags.get(), c->Q.get(), s);
-    }
-    E = c->Ebuf.get();
+    Phase ph(c, "procrustes_accurate");
+    n2 = launch_procrustes_accurate(c, R, c->H.get(), c->V.get(), c->W.get(), nullptr, c->flags.get(),
+                                    part + static_cast<std::size_t>(n1) * RR, c->Ebuf.get(), c->Ebuf.get(),
+                                    c->Chat.get(), s);
   } else {
-    Phase ph(c, "procrustes");
-    n1 = launch_procrustes(c, R, c->H.get(), c->V.get(), c->W.get(), c->Q.get(), c->flags.get(), part, kMaxPartials,
-                           s);
-  }
-  {
+    {
+      Phase ph(c, "procrustes");
+      n1 = launch_procrustes(c, R, c->H.get(), c->V.get(), c->W.get(), c->Q.get(), c->flags.get(), part,
+                             kMaxPartials, s);
+    }
     Phase ph(c, "procrustes_accurate");
     n2 = launch_procrustes_accurate(c, R, c->H.get(), c->V.get(), c->W.get(), c->Q.get(), c->flags.get(),
-                                    part + static_cast<std::size_t>(n1) * RR, E, s);
+                                    part + static_cast<std::size_t>(n1) * RR, nullptr, nullptr, nullptr, s);
   }
   return n1 + n2;
 }
 
+/// Materialises Q of the last Procrustes step (factors Hp, Vp, Wp after an
+/// iteration, or H, V, W for the per-step hook) — export only.
+void export_q(p2g_ctx* c, const double* H, const double* V, const double* W) {
+  if (!small_rank(c)) return;  // large R: K1 already wrote Q
+  launch_qrows(c, c->R, H, V, W, c->Sbuf.get(), c->Ebuf.get(), c->Chat.get(), c->flags.get(), c->Q.get(), c->stream);
+}
+
 /// gram(W) and the cross term over this shard, allreduced -> c->gwc.
-void gram_w_cross(p2g_ctx* c, const double* m3_or_null) {
+void gram_w_cross(p2g_ctx* c, const double* W, const double* m3_or_null) {
   const int R = c->R;
   const std::size_t RR = static_cast<std::size_t>(R) * R;
   DBuf<double>& part = scratch_partials(c, kMaxPartials * (RR + 1));
-  const int np = gram_partials(R, Ks(c), c->W.get(), m3_or_null, part.get(), kMaxPartials, c->stream);
+  const int np = gram_partials(R, Ks(c), W, m3_or_null, part.get(), kMaxPartials, c->stream);
   reduce_partials(part.get(), np, static_cast<std::int64_t>(RR + 1), c->gwc.get(), c->stream);
   allreduce(c, c->gwc.get(), RR + 1);
 }
 
-/// gram(V) (replicated, no collective) -> c->gramV.
-void gram_v(p2g_ctx* c, double* out) {
+/// gram(V) (replicated, no collective) -> out.
+void gram_v(p2g_ctx* c, const double* V, double* out) {
   const int R = c->R;
   const std::size_t RR = static_cast<std::size_t>(R) * R;
   DBuf<double>& part = scratch_partials(c, kMaxPartials * (RR + 1));
-  const int np = gram_partials(R, c->J, c->V.get(), nullptr, part.get(), 148, c->stream);
-  // partial stride is RR+1; reduce the first RR entries of each via a strided copy
+  const int np = gram_partials(R, c->J, V, nullptr, part.get(), 148, c->stream);
   reduce_partials(part.get(), np, static_cast<std::int64_t>(RR + 1), c->gwc.get(), c->stream);
   P2G_CUDA(cudaMemcpyAsync(out, c->gwc.get(), sizeof(double) * RR, cudaMemcpyDeviceToDevice, c->stream));
 }
@@ -286,9 +304,10 @@ void init_state(p2g_ctx* c, const p2g_fit_config* cfg, const double* H0, const d
     upload_colmajor(c, v.data(), c->J, R, c->V.get());
     launch_fill(c->W.get(), Ks(c) * R, 1.0, c->stream);
   }
-  gram_v(c, c->gramV.get());
-  gram_w_cross(c, nullptr);
+  gram_v(c, c->V.get(), c->gramV.get());
+  gram_w_cross(c, c->W.get(), nullptr);
   P2G_CUDA(cudaMemcpyAsync(c->gramW.get(), c->gwc.get(), sizeof(double) * R * R, cudaMemcpyDeviceToDevice, c->stream));
+  c->c_valid = false;
   c->state_valid = true;
 }
 
@@ -296,11 +315,15 @@ struct IterOut {
   double fit, resid;
 };
 
-/// One PARAFAC2-ALS iteration on device (solver.hpp:274-306).
+/// One PARAFAC2-ALS iteration on device (solver.hpp:274-306).  Reads the
+/// t-1 factors from H, V, W and writes the t factors into Hp, Vp, Wp, then
+/// swaps, so afterwards Hp, Vp, Wp hold the factors this Procrustes step
+/// used (Q export).
 IterOut iterate(p2g_ctx* c, bool nonneg, int iter) {
   const int R = c->R;
   const std::size_t RR = static_cast<std::size_t>(R) * R;
   cudaStream_t s = c->stream;
+  const bool qf = small_rank(c);
   P2G_CUDA(cudaMemsetAsync(c->counters.get(), 0, sizeof(std::int32_t) * 8, s));
   {
     DBuf<double>& part = scratch_partials(c, static_cast<std::size_t>(kMaxPartials + 4 * 148) * RR);
@@ -310,45 +333,57 @@ IterOut iterate(p2g_ctx* c, bool nonneg, int iter) {
     allreduce(c, c->m1.get(), RR);
   }
   {
-    Phase ph(c, "solve_h");
-    launch_solve_h(R, c->m1.get(), c->gramW.get(), c->gramV.get(), c->H.get(), c->nH.get(), c->gramH.get(),
+    Phase ph(c, "solve_h");  // H_t -> Hp
+    launch_solve_h(R, c->m1.get(), c->gramW.get(), c->gramV.get(), c->Hp.get(), c->nH.get(), c->gramH.get(),
                    c->G2.get(), s);
   }
   {
     Phase ph(c, "mode2");
-    launch_mode2(c, R, c->Q.get(), c->H.get(), c->W.get(), c->nH.get(), c->M2.get(), s);
+    if (qf)
+      launch_mode2_qf(c, R, c->H.get(), c->V.get(), c->W.get(), c->Hp.get(), c->nH.get(), c->Sbuf.get(),
+                      c->Ebuf.get(), c->Chat.get(), c->flags.get(), c->M2.get(), s);
+    else
+      launch_mode2(c, R, c->Q.get(), c->Hp.get(), c->W.get(), c->nH.get(), c->M2.get(), s);
     allreduce(c, c->M2.get(), static_cast<std::size_t>(c->J) * R);
   }
   {
-    Phase ph(c, "update_v");
+    Phase ph(c, "update_v");  // V_t -> Vp
     if (nonneg) {
-      launch_nnls_rows(R, c->J, c->G2.get(), c->M2.get(), c->V.get(), 0, c->counters.get() + 1, c->redo.get(), s);
+      launch_nnls_rows(R, c->J, c->G2.get(), c->M2.get(), c->Vp.get(), 0, c->counters.get() + 1, c->redo.get(), s);
     } else {
       launch_pinv(R, c->G2.get(), c->pinvbuf.get(), s);
-      launch_rows_times(R, c->J, c->M2.get(), c->pinvbuf.get(), c->V.get(), s);
+      launch_rows_times(R, c->J, c->M2.get(), c->pinvbuf.get(), c->Vp.get(), s);
     }
-    gram_v(c, c->gvraw.get());
-    launch_normalize_v(R, c->J, c->V.get(), c->gvraw.get(), c->gramV.get(), c->nV.get(), c->gramH.get(), c->G3.get(),
-                       s);
+    gram_v(c, c->Vp.get(), c->gvraw.get());
+    launch_normalize_v(R, c->J, c->Vp.get(), c->gvraw.get(), c->gramV.get(), c->nV.get(), c->gramH.get(),
+                       c->G3.get(), s);
   }
   {
     Phase ph(c, "mode3");
-    launch_mode3(c, R, c->Q.get(), c->H.get(), c->V.get(), c->m3.get(), s);
+    if (qf)
+      launch_mode3_qf(c, R, c->H.get(), c->V.get(), c->W.get(), c->Hp.get(), c->Vp.get(), c->Sbuf.get(),
+                      c->Ebuf.get(), c->Chat.get(), c->flags.get(), c->m3.get(), c->Cbuf.get(), s);
+    else
+      launch_mode3(c, R, c->Q.get(), c->Hp.get(), c->Vp.get(), c->m3.get(), s);
   }
   {
-    Phase ph(c, "update_w");
+    Phase ph(c, "update_w");  // W_t -> Wp
     if (nonneg) {
-      launch_nnls_rows(R, Ks(c), c->G3.get(), c->m3.get(), c->W.get(), 0, c->counters.get() + 1, c->redo.get(), s);
+      launch_nnls_rows(R, Ks(c), c->G3.get(), c->m3.get(), c->Wp.get(), 0, c->counters.get() + 1, c->redo.get(), s);
     } else {
       launch_pinv(R, c->G3.get(), c->pinvbuf.get(), s);
-      launch_rows_times(R, Ks(c), c->m3.get(), c->pinvbuf.get(), c->W.get(), s);
+      launch_rows_times(R, Ks(c), c->m3.get(), c->pinvbuf.get(), c->Wp.get(), s);
     }
   }
   {
     Phase ph(c, "fit");
-    gram_w_cross(c, c->m3.get());
+    gram_w_cross(c, c->Wp.get(), c->m3.get());
     launch_fit(R, c->gwc.get(), c->gramH.get(), c->gramV.get(), c->norm_x, c->gramW.get(), c->scal.get(), s);
   }
+  swap_buf(c->H, c->Hp);
+  swap_buf(c->V, c->Vp);
+  swap_buf(c->W, c->Wp);
+  c->c_valid = qf;  // mode 3 produced the Gram for the new V
   // One host sync per iteration: fit scalars + error counters.
   P2G_CUDA(cudaMemcpyAsync(c->pinned, c->scal.get(), sizeof(double) * 4, cudaMemcpyDeviceToHost, s));
   P2G_CUDA(cudaMemcpyAsync(c->pinned + 4, c->counters.get(), sizeof(std::int32_t) * 8, cudaMemcpyDeviceToHost, s));
@@ -540,8 +575,10 @@ extern "C" int p2g_fit(p2g_ctx* c, const p2g_fit_config* cfg, const double* H0, 
     if (H_out) download_colmajor(c, c->H.get(), R, R, H_out);
     if (V_out) download_colmajor(c, c->V.get(), c->J, R, V_out);
     if (W_out) download_colmajor(c, c->W.get(), Ks(c), R, W_out);
-    if (Q_out)
+    if (Q_out) {
+      export_q(c, c->Hp.get(), c->Vp.get(), c->Wp.get());  // factors of the last Procrustes step
       P2G_CUDA(cudaMemcpyAsync(Q_out, c->Q.get(), sizeof(double) * c->NR * R, cudaMemcpyDeviceToHost, c->stream));
+    }
     if (flags_out)
       P2G_CUDA(cudaMemcpyAsync(flags_out, c->flags.get(), sizeof(int32_t) * Ks(c), cudaMemcpyDeviceToHost, c->stream));
     P2G_CUDA(cudaStreamSynchronize(c->stream));
@@ -641,6 +678,7 @@ extern "C" int p2g_procrustes(p2g_ctx* c, int32_t R, const double* H, const doub
     upload_colmajor(c, H, R, R, c->H.get());
     upload_colmajor(c, V, c->J, R, c->V.get());
     upload_shard_rows(c, W, c->K_total, R, c->W.get());
+    c->c_valid = false;
     const std::size_t RR = static_cast<std::size_t>(R) * R;
     P2G_CUDA(cudaMemsetAsync(c->counters.get(), 0, sizeof(std::int32_t) * 8, c->stream));
     DBuf<double>& part = scratch_partials(c, static_cast<std::size_t>(kMaxPartials + 4 * 148) * RR);
@@ -651,7 +689,11 @@ extern "C" int p2g_procrustes(p2g_ctx* c, int32_t R, const double* H, const doub
     P2G_CUDA(cudaMemcpyAsync(cnt, c->counters.get(), sizeof(cnt), cudaMemcpyDeviceToHost, c->stream));
     P2G_CUDA(cudaStreamSynchronize(c->stream));
     if (cnt[2] > 0) throw NumericalError("svd operand: non-finite entries");
-    if (Q_out) P2G_CUDA(cudaMemcpy(Q_out, c->Q.get(), sizeof(double) * c->NR * R, cudaMemcpyDeviceToHost));
+    if (Q_out) {
+      export_q(c, c->H.get(), c->V.get(), c->W.get());
+      P2G_CUDA(cudaMemcpyAsync(Q_out, c->Q.get(), sizeof(double) * c->NR * R, cudaMemcpyDeviceToHost, c->stream));
+      P2G_CUDA(cudaStreamSynchronize(c->stream));
+    }
     if (flags_out) P2G_CUDA(cudaMemcpy(flags_out, c->flags.get(), sizeof(int32_t) * Ks(c), cudaMemcpyDeviceToHost));
     if (m1_out) download_colmajor(c, c->m1.get(), R, R, m1_out);
     c->state_valid = false;
@@ -671,6 +713,7 @@ extern "C" int p2g_mttkrp_q(p2g_ctx* c, int32_t mode, int32_t R, const double* Q
     upload_colmajor(c, H, R, R, c->H.get());
     upload_colmajor(c, V, c->J, R, c->V.get());
     upload_shard_rows(c, W, c->K_total, R, c->W.get());
+    c->c_valid = false;
     const std::size_t RR = static_cast<std::size_t>(R) * R;
     if (mode == 1) {
       const int nb = 2 * c->num_sms;

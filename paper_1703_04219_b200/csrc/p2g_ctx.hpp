@@ -120,7 +120,10 @@ struct p2g_ctx {
   p2g::DBuf<std::int32_t> fb_list;    // compacted fallback subject ids
   p2g::DBuf<std::int32_t> counters;   // [0]=n_fallback, [1]=nnls error, ...
   p2g::DBuf<double> acc_scratch;      // accurate Procrustes path slabs
-  p2g::DBuf<double> Cbuf, Sbuf, Ebuf; // small-R pipeline: per-subject packed C, S; E of flagged subjects
+  p2g::DBuf<double> Cbuf, Sbuf, Ebuf; // small-R pipeline: per-subject packed C, S; E / Shat of flagged subjects
+  p2g::DBuf<double> Chat;             // completion term of flagged subjects (K_s x R x R)
+  p2g::DBuf<double> Hp, Vp, Wp;       // factors the last Procrustes step used (Q-free reconstruction)
+  bool c_valid = false;               // Cbuf holds Gram of X V for the current V
   p2g::DBuf<std::int32_t> redo;       // NNLS rows re-solved by the warp (pinv) kernel
   p2g::DBuf<double> m2part;           // per-range J x R partials of the on-chip mode-2 kernel
   bool state_valid = false;
@@ -144,7 +147,8 @@ int launch_procrustes(p2g_ctx* c, int R, const double* H, const double* V, const
 // Accurate Jacobi-SVD path over the subjects flagged P2G_FLAG_ACCURATE;
 // writes one R x R m1 partial per block (count = procrustes_accurate_blocks).
 int launch_procrustes_accurate(p2g_ctx* c, int R, const double* H, const double* V, const double* W, double* Q,
-                               std::int32_t* flags, double* m1_partials, const double* Ebuf, cudaStream_t s);
+                               std::int32_t* flags, double* m1_partials, const double* Ebuf, double* Shat,
+                               double* Chat, cudaStream_t s);
 int procrustes_accurate_blocks(p2g_ctx* c, int R);
 
 // Small-rank pipeline (k_small.cu, R <= 16).
@@ -153,7 +157,13 @@ void launch_gram_c(p2g_ctx* c, int R, const double* V, double* Cbuf, cudaStream_
 int launch_polar_small(p2g_ctx* c, int R, const double* H, const double* W, const double* Cbuf, double* Sbuf,
                        double* Ebuf, std::int32_t* flags, double* m1_partials, int max_blocks, cudaStream_t s);
 void launch_qrows(p2g_ctx* c, int R, const double* H, const double* V, const double* W, const double* Sbuf,
-                  const std::int32_t* flags, double* Q, cudaStream_t s);
+                  const double* Shat, const double* Chat, const std::int32_t* flags, double* Q, cudaStream_t s);
+void launch_mode2_qf(p2g_ctx* c, int R, const double* Hprev, const double* Vprev, const double* Wprev,
+                     const double* Ht, const double* nH, const double* Sbuf, const double* Shat, const double* Chat,
+                     const std::int32_t* flags, double* M2, cudaStream_t s);
+void launch_mode3_qf(p2g_ctx* c, int R, const double* Hprev, const double* Vprev, const double* Wprev,
+                     const double* Ht, const double* Vt, const double* Sbuf, const double* Shat, const double* Chat,
+                     const std::int32_t* flags, double* M3, double* Cnext, cudaStream_t s);
 void launch_nnls_thread(int R, std::int64_t n, const double* G, const double* B, double* X, int max_iter,
                         std::int32_t* err, std::int32_t* redo, std::int32_t* n_redo, cudaStream_t s);
 void launch_mode2(p2g_ctx* c, int R, const double* Q, const double* H, const double* W, const double* nH,
