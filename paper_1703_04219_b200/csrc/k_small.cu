@@ -16,6 +16,7 @@
 //   K1c  k_qrows       warp per subject: Q_k = X_k V D H^T S (rows, coalesced)
 // The accurate path (k_procrustes.cu) takes the flagged subjects.
 #include <algorithm>
+#include <cstdlib>
 #include <utility>
 
 #include "dev_common.cuh"
@@ -263,8 +264,8 @@ struct PolarSmem {
 template <int RP, int WPB>
 __global__ void __launch_bounds__(WPB * 32)
     k_polar_small(std::int64_t K, int R, const double* __restrict__ H, const double* __restrict__ W,
-                  const double* __restrict__ Cbuf, double* __restrict__ Sbuf, double* __restrict__ Ebuf,
-                  std::int32_t* __restrict__ flags, double* __restrict__ m1_partials) {
+                  const double* __restrict__ Cbuf, double* __restrict__ Sbuf, double* __restrict__ Ewarm, int /*warm*/,
+                  std::int32_t* __restrict__ flags, double* __restrict__ m1_partials, int* __restrict__ dbg) {
   extern __shared__ double smem[];
   constexpr int MP = PolarSmem<RP>::MP;
   constexpr int NT = MP * (MP + 1) / 2;
@@ -331,9 +332,10 @@ __global__ void __launch_bounds__(WPB * 32)
 #pragma unroll
       for (int j = 0; j < MP; ++j) E[(i * MP + j) * LD] = i == j ? 1.0 : 0.0;
     bool ok = active && finite && gmax > 0.0;
+    int sweeps = 0;
     if (ok) {
       bool converged = false;
-      for (int sweep = 0; sweep < kMaxSweeps; ++sweep) {
+      for (int sweep = 0; sweep < kMaxSweeps; ++sweep, ++sweeps) {
         double off = 0.0, dia = 0.0;
 #pragma unroll
         for (int i = 0; i < MP; ++i)
@@ -353,6 +355,16 @@ __global__ void __launch_bounds__(WPB * 32)
       }
       ok = converged;
     }
+    if (dbg) {  // sweep statistics: sum per subject, max, sum of per-warp max, warps
+      int wmax = sweeps;
+      for (int o = 16; o > 0; o >>= 1) wmax = max(wmax, __shfl_xor_sync(dev::kFull, wmax, o));
+      atomicAdd(dbg + 0, sweeps);
+      atomicMax(dbg + 1, sweeps);
+      if (lane == 0) {
+        atomicAdd(dbg + 2, wmax);
+        atomicAdd(dbg + 3, 1);
+      }
+    }
     // eigenvalues in logical order
     double lam[MP];
 #pragma unroll
@@ -368,13 +380,19 @@ __global__ void __launch_bounds__(WPB * 32)
       ok = lmax > 0.0 && lmin >= kFastRatio * lmax;
     }
     if (active) flags[k] = ok ? P2G_FLAG_FULL_RANK : P2G_FLAG_ACCURATE;
-    if (active && !ok) {
-      // eigenvectors (identity if G was zero / non-finite) precondition the accurate path
-      const bool useE = finite && gmax > 0.0;
-      for (int i = 0; i < R; ++i)
-        for (int j = 0; j < R; ++j)
-          Ebuf[k * R * R + i * R + j] = useE ? E[(i * MP + j) * LD] : (i == j ? 1.0 : 0.0);
+    // Eigenvectors (orthogonal in every case) -> Ewarm: the accurate path's
+    // preconditioner.  Coalesced via the [element][lane] layout.
+    __syncwarp();
+    {
+      const int RR = R * R;
+      const std::int64_t nk = min(static_cast<std::int64_t>(32), K - kb);
+      for (std::int64_t idx = lane; idx < nk * RR; idx += 32) {
+        const int sub = static_cast<int>(idx / RR), e = static_cast<int>(idx - (idx / RR) * RR);
+        const int i = e / R, j = e - (e / R) * R;
+        Ewarm[(kb + sub) * RR + e] = Ew[(i * MP + j) * LD + sub];
+      }
     }
+    __syncwarp();
     // S = E diag(lambda^-1/2) E^T (logical packed, into g)
 #pragma unroll
     for (int m = 0; m < MP; ++m) lam[m] = (ok && m < R) ? rsqrt(lam[m]) : 0.0;
@@ -909,7 +927,8 @@ void launch_gram_c(p2g_ctx* c, int R, const double* V, double* Cbuf, cudaStream_
 
 template <int RP>
 static int polar_launch(p2g_ctx* c, std::int64_t K, int R, const double* H, const double* W, const double* Cbuf,
-                        double* Sbuf, double* Ebuf, std::int32_t* flags, double* m1p, int max_blocks, cudaStream_t s) {
+                        double* Sbuf, double* Ewarm, int warm, std::int32_t* flags, double* m1p, int max_blocks,
+                        cudaStream_t s) {
   constexpr int WPB = RP <= 10 ? 4 : 2;
   constexpr int MP = PolarSmem<RP>::MP;
   const std::size_t smem = sizeof(double) * (MP * MP + WPB * MP * MP + WPB * PolarSmem<RP>::kPerWarp);
@@ -919,14 +938,16 @@ static int polar_launch(p2g_ctx* c, std::int64_t K, int R, const double* H, cons
   P2G_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, WPB * 32, smem));
   const int blocks = grid_cap((K + 31) / 32, WPB, c->num_sms, std::max(per_sm, 1));
   const int nb = std::min(blocks, max_blocks);
-  kern<<<nb, WPB * 32, smem, s>>>(K, R, H, W, Cbuf, Sbuf, Ebuf, flags, m1p);
+  kern<<<nb, WPB * 32, smem, s>>>(K, R, H, W, Cbuf, Sbuf, Ewarm, warm, flags, m1p,
+                                  std::getenv("P2G_DEBUG") ? c->counters.get() + 4 : nullptr);
   return nb;
 }
 
 int launch_polar_small(p2g_ctx* c, int R, const double* H, const double* W, const double* Cbuf, double* Sbuf,
-                       double* Ebuf, std::int32_t* flags, double* m1_partials, int max_blocks, cudaStream_t s) {
+                       double* Ewarm, int warm, std::int32_t* flags, double* m1_partials, int max_blocks,
+                       cudaStream_t s) {
   int nb = 0;
-  P2G_SMALL_DISPATCH(R, nb = polar_launch<RP_>(c, c->k_end - c->k_begin, R, H, W, Cbuf, Sbuf, Ebuf, flags,
+  P2G_SMALL_DISPATCH(R, nb = polar_launch<RP_>(c, c->k_end - c->k_begin, R, H, W, Cbuf, Sbuf, Ewarm, warm, flags,
                                                m1_partials, max_blocks, s));
   P2G_LAUNCHED(1);
   return nb;

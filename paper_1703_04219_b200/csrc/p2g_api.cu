@@ -7,6 +7,8 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <memory>
@@ -207,6 +209,7 @@ void alloc_state(p2g_ctx* c, int R) {
     c->Sbuf.resize(ks * nt);
     c->Ebuf.resize(ks * RR);
     c->Chat.resize(ks * RR);
+    c->Ewarm.resize(ks * RR);
   }
 }
 
@@ -239,12 +242,14 @@ int procrustes_step(p2g_ctx* c, double* part) {
     }
     {
       Phase ph(c, "polar");
-      n1 = launch_polar_small(c, R, c->H.get(), c->W.get(), c->Cbuf.get(), c->Sbuf.get(), c->Ebuf.get(),
-                              c->flags.get(), part, kMaxPartials, s);
+      n1 = launch_polar_small(c, R, c->H.get(), c->W.get(), c->Cbuf.get(), c->Sbuf.get(), c->Ewarm.get(),
+                              (c->ew_valid && std::getenv("P2G_WARM")) ? 1 : 0, c->flags.get(), part,
+                              kMaxPartials, s);
+      c->ew_valid = true;
     }
     Phase ph(c, "procrustes_accurate");
     n2 = launch_procrustes_accurate(c, R, c->H.get(), c->V.get(), c->W.get(), nullptr, c->flags.get(),
-                                    part + static_cast<std::size_t>(n1) * RR, c->Ebuf.get(), c->Ebuf.get(),
+                                    part + static_cast<std::size_t>(n1) * RR, c->Ewarm.get(), c->Ebuf.get(),
                                     c->Chat.get(), s);
   } else {
     {
@@ -308,6 +313,7 @@ void init_state(p2g_ctx* c, const p2g_fit_config* cfg, const double* H0, const d
   gram_w_cross(c, c->W.get(), nullptr);
   P2G_CUDA(cudaMemcpyAsync(c->gramW.get(), c->gwc.get(), sizeof(double) * R * R, cudaMemcpyDeviceToDevice, c->stream));
   c->c_valid = false;
+  c->ew_valid = false;
   c->state_valid = true;
 }
 
@@ -390,6 +396,10 @@ IterOut iterate(p2g_ctx* c, bool nonneg, int iter) {
   P2G_CUDA(cudaStreamSynchronize(s));
   collect_timing(c);
   const std::int32_t* cnt = reinterpret_cast<const std::int32_t*>(c->pinned + 4);
+  if (std::getenv("P2G_DEBUG") && cnt[7] > 0)
+    std::fprintf(stderr, "[p2g] iter %d polar sweeps: mean %.2f max %d mean-warp-max %.2f\n", iter,
+                 static_cast<double>(cnt[4]) / static_cast<double>(std::max<std::int64_t>(Ks(c), 1)), cnt[5],
+                 static_cast<double>(cnt[6]) / cnt[7]);
   if (cnt[2] > 0) throw NumericalError("svd operand: non-finite entries");
   if (cnt[1] > 0) throw NumericalError("NNLS did not converge");
   IterOut o{c->pinned[0], c->pinned[1]};
@@ -679,6 +689,7 @@ extern "C" int p2g_procrustes(p2g_ctx* c, int32_t R, const double* H, const doub
     upload_colmajor(c, V, c->J, R, c->V.get());
     upload_shard_rows(c, W, c->K_total, R, c->W.get());
     c->c_valid = false;
+    c->ew_valid = false;  // cold Jacobi start for a teacher-forced step
     const std::size_t RR = static_cast<std::size_t>(R) * R;
     P2G_CUDA(cudaMemsetAsync(c->counters.get(), 0, sizeof(std::int32_t) * 8, c->stream));
     DBuf<double>& part = scratch_partials(c, static_cast<std::size_t>(kMaxPartials + 4 * 148) * RR);

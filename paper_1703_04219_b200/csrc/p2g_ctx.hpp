@@ -122,6 +122,8 @@ struct p2g_ctx {
   p2g::DBuf<double> acc_scratch;      // accurate Procrustes path slabs
   p2g::DBuf<double> Cbuf, Sbuf, Ebuf; // small-R pipeline: per-subject packed C, S; E / Shat of flagged subjects
   p2g::DBuf<double> Chat;             // completion term of flagged subjects (K_s x R x R)
+  p2g::DBuf<double> Ewarm;            // per-subject Jacobi eigenvectors (warm start / preconditioner)
+  bool ew_valid = false;              // Ewarm holds eigenvectors from a previous Procrustes step
   p2g::DBuf<double> Hp, Vp, Wp;       // factors the last Procrustes step used (Q-free reconstruction)
   bool c_valid = false;               // Cbuf holds Gram of X V for the current V
   p2g::DBuf<std::int32_t> redo;       // NNLS rows re-solved by the warp (pinv) kernel
@@ -155,7 +157,8 @@ int procrustes_accurate_blocks(p2g_ctx* c, int R);
 constexpr int kSmallRankMax = 16;
 void launch_gram_c(p2g_ctx* c, int R, const double* V, double* Cbuf, cudaStream_t s);
 int launch_polar_small(p2g_ctx* c, int R, const double* H, const double* W, const double* Cbuf, double* Sbuf,
-                       double* Ebuf, std::int32_t* flags, double* m1_partials, int max_blocks, cudaStream_t s);
+                       double* Ewarm, int warm, std::int32_t* flags, double* m1_partials, int max_blocks,
+                       cudaStream_t s);
 void launch_qrows(p2g_ctx* c, int R, const double* H, const double* V, const double* W, const double* Sbuf,
                   const double* Shat, const double* Chat, const std::int32_t* flags, double* Q, cudaStream_t s);
 void launch_mode2_qf(p2g_ctx* c, int R, const double* Hprev, const double* Vprev, const double* Wprev,
