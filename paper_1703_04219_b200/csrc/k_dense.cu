@@ -483,14 +483,14 @@ void reduce_partials(const double* partials, int nparts, std::int64_t len, doubl
 }
 
 void launch_nnls_rows(int R, std::int64_t n, const double* G, const double* B, double* X, int max_iter,
-                      std::int32_t* err, std::int32_t* work, cudaStream_t s) {
+                      std::int32_t* err, std::int32_t* work, cudaStream_t s, unsigned* masks, int warm) {
   if (n == 0) return;
   const int cap = max_iter > 0 ? max_iter : 30 * R;
   if (R <= kSmallRankMax && work) {
     // thread per row; rows whose passive Cholesky meets a non-positive pivot
     // are re-solved by the warp kernel with the pseudo-inverse (work[0] = count).
     P2G_CUDA(cudaMemsetAsync(work, 0, sizeof(std::int32_t), s));
-    launch_nnls_thread(R, n, G, B, X, max_iter, err, work + 1, work, s);
+    launch_nnls_thread(R, n, G, B, X, max_iter, err, work + 1, work, masks, warm, s);
     nnls_warp_any(R, n, G, B, X, cap, err, work + 1, work, s);
     P2G_LAUNCHED(1);
     return;

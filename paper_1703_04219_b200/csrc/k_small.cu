@@ -737,7 +737,7 @@ template <int RP, int WPB>
 __global__ void __launch_bounds__(WPB * 32)
     k_nnls_thread(int R, std::int64_t n, const double* __restrict__ G, const double* __restrict__ B,
                   double* __restrict__ X, int cap, std::int32_t* __restrict__ err, std::int32_t* __restrict__ redo,
-                  std::int32_t* __restrict__ n_redo) {
+                  std::int32_t* __restrict__ n_redo, unsigned* __restrict__ masks, int warm) {
   extern __shared__ double smem[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   double* Gs = smem;
@@ -756,20 +756,27 @@ __global__ void __launch_bounds__(WPB * 32)
       w[r] = b[r];
       x[r] = 0.0;
     }
-    unsigned passive = 0u;
+    // Warm start (optional): begin from the row's previous passive set.  The
+    // optimum is unique (G positive definite), so only the path changes; an
+    // infeasible warm solve sheds its non-positive coordinates and retries,
+    // and an emptied set falls back to the reference's cold start.
+    unsigned passive = (masks && warm) ? (masks[row] & ((R >= 32) ? ~0u : ((1u << R) - 1u))) : 0u;
+    bool warm_phase = passive != 0u;
     int iters = 0;
     bool failed = false, chol_fail = false;
     while (true) {
-      double best = 1e-10;
-      int enter = -1;
+      if (!warm_phase) {
+        double best = 1e-10;
+        int enter = -1;
 #pragma unroll
-      for (int r = 0; r < RP; ++r)
-        if (r < R && !((passive >> r) & 1u) && w[r] > best) {
-          best = w[r];
-          enter = r;
-        }
-      if (enter < 0) break;
-      passive |= 1u << enter;
+        for (int r = 0; r < RP; ++r)
+          if (r < R && !((passive >> r) & 1u) && w[r] > best) {
+            best = w[r];
+            enter = r;
+          }
+        if (enter < 0) break;
+        passive |= 1u << enter;
+      }
       while (true) {
         if (++iters > cap) {
           failed = true;
@@ -827,6 +834,13 @@ __global__ void __launch_bounds__(WPB * 32)
           for (int r = 0; r < RP; ++r) x[r] = sv[r];
           break;
         }
+        if (warm_phase) {  // x = 0 here: drop the non-positive coordinates and re-solve
+#pragma unroll
+          for (int r = 0; r < RP; ++r)
+            if (((passive >> r) & 1u) && sv[r] <= 0.0) passive &= ~(1u << r);
+          if (passive == 0u) break;
+          continue;
+        }
         double alpha = __longlong_as_double(0x7ff0000000000000ll);
 #pragma unroll
         for (int r = 0; r < RP; ++r)
@@ -848,6 +862,7 @@ __global__ void __launch_bounds__(WPB * 32)
             passive &= ~(1u << r);
           }
       }
+      warm_phase = false;
       if (failed || chol_fail) break;
 #pragma unroll
       for (int r = 0; r < RP; ++r) {
@@ -864,6 +879,7 @@ __global__ void __launch_bounds__(WPB * 32)
       continue;
     }
     if (failed) atomicAdd(err, 1);
+    if (masks) masks[row] = passive;
 #pragma unroll
     for (int r = 0; r < RP; ++r)
       if (r < R) X[row * R + r] = x[r];
@@ -991,20 +1007,22 @@ void launch_mode3_qf(p2g_ctx* c, int R, const double* Hprev, const double* Vprev
 
 template <int RP>
 static void nnls_thread_launch(int R, std::int64_t n, const double* G, const double* B, double* X, int cap,
-                               std::int32_t* err, std::int32_t* redo, std::int32_t* n_redo, cudaStream_t s) {
+                               std::int32_t* err, std::int32_t* redo, std::int32_t* n_redo, unsigned* masks, int warm,
+                               cudaStream_t s) {
   constexpr int WPB = 4;
   const std::size_t smem = sizeof(double) * (RP * RP + WPB * NnlsThreadSmem<RP>::kPerWarp);
   auto kern = k_nnls_thread<RP, WPB>;
   P2G_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   const int blocks = static_cast<int>(std::max<std::int64_t>(1, std::min<std::int64_t>((n + 127) / 128, 148 * 16)));
-  kern<<<blocks, WPB * 32, smem, s>>>(R, n, G, B, X, cap, err, redo, n_redo);
+  kern<<<blocks, WPB * 32, smem, s>>>(R, n, G, B, X, cap, err, redo, n_redo, masks, warm);
 }
 
 void launch_nnls_thread(int R, std::int64_t n, const double* G, const double* B, double* X, int max_iter,
-                        std::int32_t* err, std::int32_t* redo, std::int32_t* n_redo, cudaStream_t s) {
+                        std::int32_t* err, std::int32_t* redo, std::int32_t* n_redo, unsigned* masks, int warm,
+                        cudaStream_t s) {
   if (n == 0) return;
   const int cap = max_iter > 0 ? max_iter : 30 * R;
-  P2G_SMALL_DISPATCH(R, nnls_thread_launch<RP_>(R, n, G, B, X, cap, err, redo, n_redo, s));
+  P2G_SMALL_DISPATCH(R, nnls_thread_launch<RP_>(R, n, G, B, X, cap, err, redo, n_redo, masks, warm, s));
   P2G_LAUNCHED(1);
 }
 

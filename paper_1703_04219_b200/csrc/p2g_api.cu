@@ -210,6 +210,8 @@ void alloc_state(p2g_ctx* c, int R) {
     c->Ebuf.resize(ks * RR);
     c->Chat.resize(ks * RR);
     c->Ewarm.resize(ks * RR);
+    c->mask_v.resize(static_cast<std::size_t>(std::max<std::int64_t>(c->J, 1)));
+    c->mask_w.resize(ks);
   }
 }
 
@@ -314,6 +316,7 @@ void init_state(p2g_ctx* c, const p2g_fit_config* cfg, const double* H0, const d
   P2G_CUDA(cudaMemcpyAsync(c->gramW.get(), c->gwc.get(), sizeof(double) * R * R, cudaMemcpyDeviceToDevice, c->stream));
   c->c_valid = false;
   c->ew_valid = false;
+  c->masks_valid = false;
   c->state_valid = true;
 }
 
@@ -355,7 +358,8 @@ IterOut iterate(p2g_ctx* c, bool nonneg, int iter) {
   {
     Phase ph(c, "update_v");  // V_t -> Vp
     if (nonneg) {
-      launch_nnls_rows(R, c->J, c->G2.get(), c->M2.get(), c->Vp.get(), 0, c->counters.get() + 1, c->redo.get(), s);
+      launch_nnls_rows(R, c->J, c->G2.get(), c->M2.get(), c->Vp.get(), 0, c->counters.get() + 1, c->redo.get(), s,
+                       c->mask_v.get(), c->masks_valid ? 1 : 0);
     } else {
       launch_pinv(R, c->G2.get(), c->pinvbuf.get(), s);
       launch_rows_times(R, c->J, c->M2.get(), c->pinvbuf.get(), c->Vp.get(), s);
@@ -375,7 +379,9 @@ IterOut iterate(p2g_ctx* c, bool nonneg, int iter) {
   {
     Phase ph(c, "update_w");  // W_t -> Wp
     if (nonneg) {
-      launch_nnls_rows(R, Ks(c), c->G3.get(), c->m3.get(), c->Wp.get(), 0, c->counters.get() + 1, c->redo.get(), s);
+      launch_nnls_rows(R, Ks(c), c->G3.get(), c->m3.get(), c->Wp.get(), 0, c->counters.get() + 1, c->redo.get(), s,
+                       c->mask_w.get(), c->masks_valid ? 1 : 0);
+      c->masks_valid = small_rank(c);
     } else {
       launch_pinv(R, c->G3.get(), c->pinvbuf.get(), s);
       launch_rows_times(R, Ks(c), c->m3.get(), c->pinvbuf.get(), c->Wp.get(), s);

@@ -128,6 +128,8 @@ struct p2g_ctx {
   bool c_valid = false;               // Cbuf holds Gram of X V for the current V
   p2g::DBuf<std::int32_t> redo;       // NNLS rows re-solved by the warp (pinv) kernel
   p2g::DBuf<double> m2part;           // per-range J x R partials of the on-chip mode-2 kernel
+  p2g::DBuf<unsigned> mask_v, mask_w; // NNLS passive sets of the previous iteration (warm start)
+  bool masks_valid = false;
   bool state_valid = false;
 
   // Timing.
@@ -168,7 +170,8 @@ void launch_mode3_qf(p2g_ctx* c, int R, const double* Hprev, const double* Vprev
                      const double* Ht, const double* Vt, const double* Sbuf, const double* Shat, const double* Chat,
                      const std::int32_t* flags, double* M3, double* Cnext, cudaStream_t s);
 void launch_nnls_thread(int R, std::int64_t n, const double* G, const double* B, double* X, int max_iter,
-                        std::int32_t* err, std::int32_t* redo, std::int32_t* n_redo, cudaStream_t s);
+                        std::int32_t* err, std::int32_t* redo, std::int32_t* n_redo, unsigned* masks, int warm,
+                        cudaStream_t s);
 void launch_mode2(p2g_ctx* c, int R, const double* Q, const double* H, const double* W, const double* nH,
                   double* M2, cudaStream_t s);
 void launch_mode3(p2g_ctx* c, int R, const double* Q, const double* H, const double* V, double* m3,
@@ -192,8 +195,11 @@ int gram_partials(int R, std::int64_t n, const double* A, const double* B, doubl
                   cudaStream_t s);  // returns #partials; each partial R*R (+1 cross if B)
 void reduce_partials(const double* partials, int nparts, std::int64_t len, double* out, cudaStream_t s);
 // work: n+1 ints of scratch (thread-per-row path for R <= 16) or null.
+// masks: n passive-set bit masks (R <= 16) carried across calls for the warm
+// start (warm != 0 uses them), or null.
 void launch_nnls_rows(int R, std::int64_t n, const double* G, const double* B, double* X, int max_iter,
-                      std::int32_t* err, std::int32_t* work, cudaStream_t s);
+                      std::int32_t* err, std::int32_t* work, cudaStream_t s, unsigned* masks = nullptr,
+                      int warm = 0);
 void launch_rows_times(int R, std::int64_t n, const double* B, const double* P, double* X,
                        cudaStream_t s);  // X = B * P (row-major rows)
 void launch_pinv(int n, const double* G, double* out, cudaStream_t s);
