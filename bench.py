@@ -101,22 +101,28 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def algorithmic_bytes(X, R, k_lo=0, k_hi=None):
-    """Per-launch compulsory HBM bytes of each fused-loop kernel:
-    CSR = 12 B/nnz + 8 B/row + 8 B/subject; Q rows 8R B; W rows 8R B."""
-    K = X.K
+def algorithmic_bytes(X, R):
+    """Per-launch compulsory HBM bytes of each loop kernel.
+    CSR = 12 B/nnz + 8 B/row + 8 B/subject; per-subject packed C/S = 8 R(R+1)/2 B;
+    E = 8 R^2 B; W rows 8 R B; V 8 J R B (L2-resident, counted once)."""
+    K, J = X.K, X.J
     nnz, nr = X.nnz, X.n_rows
+    nt = R * (R + 1) // 2
     csr = 12 * nnz + 8 * (nr + 1) + 8 * (K + 1)
     q = 8 * nr * R
     w = 8 * K * R
-    v = 8 * X.J * R
+    v = 8 * J * R
     return {
-        "procrustes": csr + q + w + v,           # K1: CSR + V, W_k in; Q out
-        "mode2": csr + q + w + v,                # CSR + Q + W in; M2 (J x R) out
-        "mode3": csr + q + w + v,                # CSR + Q + V in; m3 out
-        "update_w": 2 * w,                       # m3 in, W out (NNLS)
-        "fit": 2 * w,                            # W, m3 in (gram + cross)
-        "iteration": 3 * csr + 3 * q + 4 * w + 4 * v,  # SURVEY.md §8d B_iter
+        # small-R Q-free pipeline
+        "polar": 8 * K * (2 * nt + R + R * R),          # C, W in; S, E out
+        "mode2": csr + 8 * K * nt + w + v,              # CSR, S, W in (V L2); M2 out
+        "mode3": csr + 8 * K * nt + w + w + 8 * K * nt + 2 * v,  # CSR, S, W in; m3, next C out
+        "update_w": 2 * w,                              # m3 in, W out (NNLS)
+        "fit": 2 * w,                                   # W, m3 in (gram + cross)
+        # large-R (Q-based) pipeline
+        "procrustes": csr + q + w + v,                  # K1: CSR + V, W_k in; Q out
+        # SURVEY.md §8d north-star iteration bytes (Q-based formulation)
+        "iteration": 3 * csr + 3 * q + 4 * w + 4 * v,
     }
 
 
@@ -276,7 +282,7 @@ def main():
     # roofline of the dominant kernel (largest share of the step)
     peak, peak_kind = load_peaks()
     ab = algorithmic_bytes(X.subset(kb, ke) if world > 1 else X, R)
-    cand = {k: v for k, v in ktimes.items() if k in ("procrustes", "mode2", "mode3", "update_w")}
+    cand = {k: v for k, v in ktimes.items() if k in ("polar", "procrustes", "mode2", "mode3", "update_w")}
     dom = max(cand, key=lambda k: cand[k][0]) if cand else None
     roofline = None
     if dom:

@@ -14,10 +14,17 @@
 namespace p2g {
 
 namespace {
-thread_local std::string g_last_error;
+// Trivially destructible on purpose: a static object's destructor (e.g. the
+// drop-in headers' Device) may call into the ABI after the main thread's
+// thread_local objects have been destroyed at exit.
+thread_local char g_last_error[1024];
 }
 
-void set_last_error(const std::string& msg) { g_last_error = msg; }
+void set_last_error(const std::string& msg) {
+  const std::size_t n = std::min(msg.size(), sizeof(g_last_error) - 1);
+  std::memcpy(g_last_error, msg.data(), n);
+  g_last_error[n] = '\0';
+}
 
 /// parallel.hpp:51-79 (and partition_even :34-45 for zero total weight).
 void partition_weighted(const std::uint64_t* w, std::int64_t n, std::int32_t n_chunks,
@@ -47,7 +54,7 @@ void partition_weighted(const std::uint64_t* w, std::int64_t n, std::int32_t n_c
 
 using namespace p2g;
 
-extern "C" const char* p2g_last_error(void) { return g_last_error.c_str(); }
+extern "C" const char* p2g_last_error(void) { return g_last_error; }
 
 extern "C" const char* p2g_version(void) { return "p2g 0.1 (sm_100a, fp64)"; }
 
