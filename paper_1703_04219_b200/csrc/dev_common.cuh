@@ -30,6 +30,18 @@ __device__ __forceinline__ double warp_max(double v) {
 __device__ __forceinline__ int warp_or(int v) { return __any_sync(kFull, v); }
 
 /// Row-major R-vector gather of V row j (V is J x R row-major).
+/// 1/sqrt(x) for normal x > 0 without the library slow path (whose
+/// out-of-line call forces spills in register-resident loops): the MUFU
+/// approximation refined by two Newton steps, y <- y (3/2 - x/2 y^2).
+__device__ __forceinline__ double rsqrt_nr(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  const double h = 0.5 * x;
+  y = y * fma(-h * y, y, 1.5);
+  y = y * fma(-h * y, y, 1.5);
+  return y;
+}
+
 template <int RP>
 __device__ __forceinline__ void axpy_row(double (&acc)[RP], const double* __restrict__ vrow, double a, int R) {
 #pragma unroll

@@ -96,7 +96,7 @@ __global__ void __launch_bounds__(WPB * 32) k_procrustes(K1Args a) {
   for (std::int64_t k = static_cast<std::int64_t>(blockIdx.x) * WPB + wid; k < a.X.K; k += nwarps) {
     const std::int64_t r0 = a.X.srp[k];
     const int I = static_cast<int>(a.X.srp[k + 1] - r0);
-    if (lane < R) s[lane] = a.W[k * R + lane];
+    for (int r = lane; r < R; r += 32) s[r] = a.W[k * R + r];  // R may exceed 32
     __syncwarp();
 
     // ---- pass 1: C = XV^T XV -------------------------------------------
@@ -268,7 +268,7 @@ __global__ void __launch_bounds__(WPB * 32) k_procrustes_accurate(K1Args a, doub
     if (a.flags[k] != P2G_FLAG_ACCURATE) continue;
     const std::int64_t r0 = a.X.srp[k];
     const int I = static_cast<int>(a.X.srp[k + 1] - r0);
-    if (lane < R) s[lane] = a.W[k * R + lane];
+    for (int r = lane; r < R; r += 32) s[r] = a.W[k * R + r];  // R may exceed 32
     __syncwarp();
     for (int e = lane; e < RR; e += 32) {
       const int i = e / R, j = e - (e / R) * R;
@@ -323,7 +323,7 @@ __global__ void __launch_bounds__(WPB * 32) k_procrustes_accurate(K1Args a, doub
       // kernels.hpp:101-104: M == 0 -> Q = I(I_k, R).
       flag = P2G_FLAG_DEFICIENT;
       for (int e = lane; e < RR; e += 32) Vj[e] = 0.0;  // no strong part
-      if (lane < R) sig[lane] = 0.0;
+      for (int r = lane; r < R; r += 32) sig[r] = 0.0;
       __syncwarp();
       for (int e = lane; e < RR; e += 32) Vj[e] = (e / R == e % R) ? 1.0 : 0.0;
       __syncwarp();
@@ -359,10 +359,10 @@ __global__ void __launch_bounds__(WPB * 32) k_procrustes_accurate(K1Args a, doub
               A[i * R + p] = c * x - sn * y;
               A[i * R + q] = sn * x + c * y;
             }
-            if (lane < R) {
-              const double x = Vj[lane * R + p], y = Vj[lane * R + q];
-              Vj[lane * R + p] = c * x - sn * y;
-              Vj[lane * R + q] = sn * x + c * y;
+            for (int r = lane; r < R; r += 32) {
+              const double x = Vj[r * R + p], y = Vj[r * R + q];
+              Vj[r * R + p] = c * x - sn * y;
+              Vj[r * R + q] = sn * x + c * y;
             }
             __syncwarp();
           }
@@ -417,36 +417,76 @@ __global__ void __launch_bounds__(WPB * 32) k_procrustes_accurate(K1Args a, doub
         B[e] = acc;
       }
       __syncwarp();
-      // NtN over null columns packed into nn x nn (EA), eig -> TN = (NtN)^{-1/2} (nn x nn)
-      // map null index list into pq-free array: compute on the fly
-      for (int e = lane; e < nn * nn; e += 32) {
-        const int x = e / nn, y = e - (e / nn) * nn;
-        // x-th and y-th null columns
-        int dx = -1, dy = -1, cnt = 0;
-        for (int c = 0; c < R; ++c) {
-          const bool isnull = !(amax != 0.0 && sig[c] * sig[c] > kNullRatio * smax2);
-          if (isnull) {
-            if (cnt == x) dx = c;
-            if (cnt == y) dy = c;
-            ++cnt;
-          }
-        }
-        double acc = (x == y) ? 1.0 : 0.0;
-        for (int c = 0; c < R; ++c) acc -= B[c * R + dx] * B[c * R + dy];
-        EA[e] = acc;
+      // polar(N) as the oracle computes it: N = L Vn - U (U^T L Vn) built
+      // explicitly in the (zeroed) null columns of A, then one-sided Jacobi
+      // over the null-column pairs (same rotations and threshold as
+      // one_sided_jacobi).  TN = V_N diag(1/sigma_N) V_N^T, so polar(N) = N TN.
+      // (Forming N^T N = I - B^T B instead cancels catastrophically when |N|
+      // is small: relative error eps / |N|^2.)
+      if (lane == 0) {
+        int cnt = 0;
+        for (int c = 0; c < R; ++c)
+          if (!(amax != 0.0 && sig[c] * sig[c] > kNullRatio * smax2)) pq[cnt++] = c;
       }
       __syncwarp();
-      dev::warp_jacobi_eig(EA, EE, nn, cs, pq, lane);
+      for (int i = lane; i < I; i += 32)
+        for (int x = 0; x < nn; ++x) {
+          const int d = pq[x];
+          double v = (i < R) ? Vj[i * R + d] : 0.0;
+          for (int c = 0; c < R; ++c) v -= A[i * R + c] * B[c * R + d];  // B = 0 on null rows c
+          A[i * R + d] = v;
+        }
+      for (int e = lane; e < nn * nn; e += 32) EE[e] = (e / nn == e % nn) ? 1.0 : 0.0;
+      __syncwarp();
+      for (int sweep = 0; sweep < 80; ++sweep) {
+        int rotated = 0;
+        for (int x = 0; x < nn - 1; ++x)
+          for (int y = x + 1; y < nn; ++y) {
+            const int p = pq[x], q = pq[y];
+            double al = 0.0, be = 0.0, ga = 0.0;
+            for (int i = lane; i < I; i += 32) {
+              const double u = A[i * R + p], w = A[i * R + q];
+              al = fma(u, u, al);
+              be = fma(w, w, be);
+              ga = fma(u, w, ga);
+            }
+            al = dev::warp_sum(al);
+            be = dev::warp_sum(be);
+            ga = dev::warp_sum(ga);
+            if (ga == 0.0 || fabs(ga) <= 1e-15 * sqrt(al * be)) continue;
+            rotated = 1;
+            const double zeta = (be - al) / (2.0 * ga);
+            const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+            const double c = 1.0 / sqrt(1.0 + t * t);
+            const double sn = c * t;
+            for (int i = lane; i < I; i += 32) {
+              const double u = A[i * R + p], w = A[i * R + q];
+              A[i * R + p] = c * u - sn * w;
+              A[i * R + q] = sn * u + c * w;
+            }
+            for (int r = lane; r < nn; r += 32) {
+              const double u = EE[r * nn + x], w = EE[r * nn + y];
+              EE[r * nn + x] = c * u - sn * w;
+              EE[r * nn + y] = sn * u + c * w;
+            }
+            __syncwarp();
+          }
+        if (!rotated) break;
+      }
+      for (int x = 0; x < nn; ++x) {
+        double acc = 0.0;
+        for (int i = lane; i < I; i += 32) acc = fma(A[i * R + pq[x]], A[i * R + pq[x]], acc);
+        acc = dev::warp_sum(acc);
+        if (lane == 0) EA[x] = sqrt(acc);  // sigma_N
+      }
+      __syncwarp();
       double emin = 1e308;
-      for (int i = 0; i < nn; ++i) emin = fmin(emin, EA[i * nn + i]);
+      for (int x = 0; x < nn; ++x) emin = fmin(emin, EA[x] * EA[x]);
       if (!(emin > 1e-8)) flag = P2G_FLAG_DEGENERATE;
       for (int e = lane; e < nn * nn; e += 32) {
         const int x = e / nn, y = e - (e / nn) * nn;
         double acc = 0.0;
-        for (int m = 0; m < nn; ++m) {
-          const double ev = fmax(EA[m * nn + m], 1e-300);
-          acc += EE[x * nn + m] * EE[y * nn + m] * rsqrt(ev);
-        }
+        for (int m = 0; m < nn; ++m) acc += EE[x * nn + m] * EE[y * nn + m] / fmax(EA[m], 1e-300);
         TN[e] = acc;
       }
       __syncwarp();

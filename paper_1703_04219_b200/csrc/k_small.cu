@@ -191,8 +191,12 @@ __device__ __forceinline__ void perm_steps(double (&g)[MP * (MP + 1) / 2], doubl
   (perm_step<MP, Ts>(g, carry), ...);
 }
 
+/// E lives in the thread's pair-packed column store: logical element
+/// (row k, column a) at ec = a * MP + k, unit ec / 2 of 16 bytes at
+/// (unit * 32 + lane): a rotation streams both columns with LDS.128/STS.128,
+/// and the 32 lanes of a warp hit 32 consecutive 16-byte words.
 template <int MP>
-__device__ __forceinline__ void jacobi_round(double (&g)[MP * (MP + 1) / 2], double* E, int r) {
+__device__ __forceinline__ void jacobi_round(double (&g)[MP * (MP + 1) / 2], double2* E2, int r) {
   constexpr int H = MP / 2;
   double cs[H], sn[H], tt[H], ap[H];
 #pragma unroll
@@ -204,13 +208,25 @@ __device__ __forceinline__ void jacobi_round(double (&g)[MP * (MP + 1) / 2], dou
     sn[i] = 0.0;
     tt[i] = 0.0;
     ap[i] = 0.0;
-    if (fabs(apq) > 1e-300 && fabs(apq) > 2.2e-18 * sqrt(fabs(app * aqq))) {
-      const double theta = (aqq - app) / (2.0 * apq);
-      const double t = (theta >= 0.0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(fma(theta, theta, 1.0)));
-      const double c = rsqrt(fma(t, t, 1.0));
-      cs[i] = c;
-      sn[i] = t * c;
-      tt[i] = t;
+    const double a2 = apq * apq;
+    const double d = aqq - app;
+    const double rho2 = fma(d, d, 4.0 * a2);
+    // (rho2 > 1e-300 keeps the approximate rsqrt in its normal range; with
+    // max |G| = 1 a smaller pair is far below the convergence threshold.)
+    if (a2 > 4.84e-36 * fabs(app * aqq) && rho2 > 1e-300) {
+      // t = tan(phi) of the annihilating rotation (the oracle's
+      // sign(theta) / (|theta| + sqrt(theta^2 + 1)), theta = d / 2apq),
+      // from cos(2 phi) = |d| / rho, sin(2 phi) = 2 apq sign(d) / rho,
+      // rho = sqrt(d^2 + 4 apq^2): two reciprocal square roots, no division.
+      const double u = dev::rsqrt_nr(rho2);
+      const double cos2 = fabs(d) * u;
+      const double sin2 = (d >= 0.0 ? 2.0 : -2.0) * apq * u;
+      const double x = fma(0.5, cos2, 0.5);  // cos^2(phi)
+      const double rc = dev::rsqrt_nr(x);     // 1 / cos(phi)
+      const double s = 0.5 * sin2 * rc;
+      cs[i] = x * rc;
+      sn[i] = s;
+      tt[i] = s * rc;
       ap[i] = apq;
     }
   }
@@ -221,10 +237,13 @@ __device__ __forceinline__ void jacobi_round(double (&g)[MP * (MP + 1) / 2], dou
     g[tri(q, q)] += tt[i] * ap[i];
     if (sn[i] != 0.0) g[tri(q, p)] = 0.0;
   }
+  // constant-bound loops (a dependent inner trip count is not fully
+  // unrolled, and the runtime indices then demote g to local memory)
 #pragma unroll
   for (int i1 = 0; i1 < H; ++i1)
 #pragma unroll
-    for (int i2 = i1 + 1; i2 < H; ++i2) {
+    for (int i2 = 0; i2 < H; ++i2) {
+      if (i2 <= i1) continue;
       const int p1 = 2 * i1, q1 = p1 + 1, p2 = 2 * i2, q2 = p2 + 1;
       const double c1 = cs[i1], s1 = sn[i1], c2 = cs[i2], s2 = sn[i2];
       const double x11 = g[tri(p1, p2)], x12 = g[tri(p1, q2)], x21 = g[tri(q1, p2)], x22 = g[tri(q1, q2)];
@@ -241,11 +260,13 @@ __device__ __forceinline__ void jacobi_round(double (&g)[MP * (MP + 1) / 2], dou
     if (sn[i] == 0.0) continue;
     const int a = rr_slot(MP, r, 2 * i), b = rr_slot(MP, r, 2 * i + 1);
     const double c = cs[i], s = sn[i];
+    double2* ea = E2 + a * H * 32;
+    double2* eb = E2 + b * H * 32;
 #pragma unroll
-    for (int k = 0; k < MP; ++k) {
-      const double ea = E[(k * MP + a) * LD], eb = E[(k * MP + b) * LD];
-      E[(k * MP + a) * LD] = c * ea - s * eb;
-      E[(k * MP + b) * LD] = s * ea + c * eb;
+    for (int kk = 0; kk < H; ++kk) {
+      const double2 va = ea[kk * 32], vb = eb[kk * 32];
+      ea[kk * 32] = make_double2(c * va.x - s * vb.x, c * va.y - s * vb.y);
+      eb[kk * 32] = make_double2(s * va.x + c * vb.x, s * va.y + c * vb.y);
     }
   }
   // physical permutation g_new[tri(sigma x, sigma y)] = g_old[tri(x, y)],
@@ -258,7 +279,10 @@ __device__ __forceinline__ void jacobi_round(double (&g)[MP * (MP + 1) / 2], dou
 template <int RP>
 struct PolarSmem {
   static constexpr int MP = (RP + 1) & ~1;
-  static constexpr int kPerWarp = (MP * MP) * LD;  // E (then staging)
+  static constexpr int NT = MP * (MP + 1) / 2;
+  // per-lane doubles: E (MP x MP), later C' (NT) + an m1 column (MP)
+  static constexpr int kLane = ((MP * MP > NT + MP ? MP * MP : NT + MP) + 1) & ~1;
+  static constexpr int kPerWarp = kLane * 32;
 };
 
 template <int RP, int WPB>
@@ -268,12 +292,15 @@ __global__ void __launch_bounds__(WPB * 32)
                   std::int32_t* __restrict__ flags, double* __restrict__ m1_partials, int* __restrict__ dbg) {
   extern __shared__ double smem[];
   constexpr int MP = PolarSmem<RP>::MP;
-  constexpr int NT = MP * (MP + 1) / 2;
+  constexpr int NT = PolarSmem<RP>::NT;
+  constexpr int HP = MP / 2;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   double* Hs = smem;                                   // R x R row-major
   double* M1w = Hs + MP * MP;                          // WPB x (R x R) warp accumulators
   double* Ew = M1w + WPB * MP * MP + wid * PolarSmem<RP>::kPerWarp;
-  double* E = Ew + lane;  // this thread's column: E[(i*MP + j)*LD]
+  double2* E2 = reinterpret_cast<double2*>(Ew) + lane;
+  // scalar element e of lane l's store
+  auto el = [&](int l, int e) -> double& { return Ew[((e >> 1) * 32 + l) * 2 + (e & 1)]; };
   const int nt = R * (R + 1) / 2;
   for (int e = threadIdx.x; e < R * R; e += blockDim.x) Hs[e] = H[e];
   for (int e = lane; e < MP * MP; e += 32) M1w[wid * MP * MP + e] = 0.0;
@@ -283,43 +310,49 @@ __global__ void __launch_bounds__(WPB * 32)
   for (std::int64_t kb = (static_cast<std::int64_t>(blockIdx.x) * WPB + wid) * 32; kb < K; kb += nwarps * 32) {
     const std::int64_t k = kb + lane;
     const bool active = k < K;
+    const int nk = static_cast<int>(min(static_cast<std::int64_t>(32), K - kb));
     double s[MP];
 #pragma unroll
     for (int r = 0; r < MP; ++r) s[r] = (active && r < R) ? W[k * R + r] : 0.0;
-    // C' = D C D (logical, packed) into the E slots; Z = C' H^T into g-sized
-    // temporaries row by row; G = H Z written physically permuted (slot x
-    // holds logical rr_slot(MP, 0, x)).
-#pragma unroll
-    for (int a = 0; a < MP; ++a)
-#pragma unroll
-      for (int b = 0; b <= a; ++b)
-        E[tri(a, b) * LD] = (active && a < R) ? s[a] * Cbuf[k * nt + tri(a, b)] * s[b] : 0.0;
-    double g[NT];
+    // G = H C' H^T with C' = D C D held in registers; rows of G go to this
+    // lane's store physically permuted (slot x holds logical rr_slot(MP,0,x)).
     {
+      double cp[NT];
+#pragma unroll
+      for (int a = 0; a < MP; ++a)
+#pragma unroll
+        for (int b = 0; b <= a; ++b) cp[tri(a, b)] = (active && a < R) ? s[a] * Cbuf[k * nt + tri(a, b)] * s[b] : 0.0;
 #pragma unroll
       for (int i = 0; i < MP; ++i) {
-        double z[MP];  // row i of H C': z_b = sum_a H_ia C'_ab
+        double z[MP];  // row i of H C'
 #pragma unroll
-        for (int b = 0; b < MP; ++b) {
-          double acc = 0.0;
-          if (i < R && b < R) {
+        for (int b = 0; b < MP; ++b) z[b] = 0.0;
+        if (i < R) {
 #pragma unroll
-            for (int a = 0; a < MP; ++a)
-              if (a < R) acc = fma(Hs[i * R + a], E[tri(a, b) * LD], acc);
+          for (int a = 0; a < MP; ++a) {
+            if (a >= R) continue;
+            const double h = Hs[i * R + a];
+#pragma unroll
+            for (int b = 0; b < MP; ++b) z[b] = fma(h, cp[tri(a, b)], z[b]);
           }
-          z[b] = acc;
         }
 #pragma unroll
         for (int j = 0; j <= i; ++j) {
           double acc = 0.0;
+          if (i < R) {
 #pragma unroll
-          for (int b = 0; b < MP; ++b)
-            if (j < R && b < R) acc = fma(z[b], Hs[j * R + b], acc);
-          // logical (i, j) lives in physical slots (pi i, pi j); padding: identity block
-          g[tri(rr_inv0(MP, i), rr_inv0(MP, j))] = (i < R) ? acc : (i == j ? 1.0 : 0.0);
+            for (int b = 0; b < MP; ++b)
+              if (b < R) acc = fma(z[b], Hs[j * R + b], acc);
+          } else {
+            acc = i == j ? 1.0 : 0.0;  // padding: identity block
+          }
+          el(lane, tri(rr_inv0(MP, i), rr_inv0(MP, j))) = acc;
         }
       }
     }
+    double g[NT];
+#pragma unroll
+    for (int e = 0; e < NT; ++e) g[e] = el(lane, e);
     double gmax = 0.0;
     bool finite = true;
 #pragma unroll
@@ -327,11 +360,17 @@ __global__ void __launch_bounds__(WPB * 32)
       finite &= isfinite(g[e]);
       gmax = fmax(gmax, fabs(g[e]));
     }
-#pragma unroll
-    for (int i = 0; i < MP; ++i)
-#pragma unroll
-      for (int j = 0; j < MP; ++j) E[(i * MP + j) * LD] = i == j ? 1.0 : 0.0;
     bool ok = active && finite && gmax > 0.0;
+    // scale to max |G| = 1 (the rotation formulas square entries)
+    const double gscale = ok ? 1.0 / gmax : 1.0;
+#pragma unroll
+    for (int e = 0; e < NT; ++e) g[e] *= gscale;
+    // E = I
+#pragma unroll
+    for (int u = 0; u < MP * HP; ++u) {
+      const int a = u / HP, kk = u - a * HP;
+      E2[u * 32] = make_double2(2 * kk == a ? 1.0 : 0.0, 2 * kk + 1 == a ? 1.0 : 0.0);
+    }
     int sweeps = 0;
     if (ok) {
       bool converged = false;
@@ -351,7 +390,7 @@ __global__ void __launch_bounds__(WPB * 32)
           break;
         }
 #pragma unroll 1
-        for (int r = 0; r < MP - 1; ++r) jacobi_round<MP>(g, E, r);
+        for (int r = 0; r < MP - 1; ++r) jacobi_round<MP>(g, E2, r);
       }
       ok = converged;
     }
@@ -365,10 +404,10 @@ __global__ void __launch_bounds__(WPB * 32)
         atomicAdd(dbg + 3, 1);
       }
     }
-    // eigenvalues in logical order
+    // eigenvalues in logical order (unscaled)
     double lam[MP];
 #pragma unroll
-    for (int x = 0; x < MP; ++x) lam[rr_slot(MP, 0, x)] = g[tri(x, x)];
+    for (int x = 0; x < MP; ++x) lam[rr_slot(MP, 0, x)] = g[tri(x, x)] * gmax;
     if (ok) {
       double lmax = 0.0, lmin = 1e308;
 #pragma unroll
@@ -380,69 +419,79 @@ __global__ void __launch_bounds__(WPB * 32)
       ok = lmax > 0.0 && lmin >= kFastRatio * lmax;
     }
     if (active) flags[k] = ok ? P2G_FLAG_FULL_RANK : P2G_FLAG_ACCURATE;
-    // Eigenvectors (orthogonal in every case) -> Ewarm: the accurate path's
-    // preconditioner.  Coalesced via the [element][lane] layout.
-    __syncwarp();
-    {
-      const int RR = R * R;
-      const std::int64_t nk = min(static_cast<std::int64_t>(32), K - kb);
-      for (std::int64_t idx = lane; idx < nk * RR; idx += 32) {
-        const int sub = static_cast<int>(idx / RR), e = static_cast<int>(idx - (idx / RR) * RR);
-        const int i = e / R, j = e - (e / R) * R;
-        Ewarm[(kb + sub) * RR + e] = Ew[(i * MP + j) * LD + sub];
-      }
+    // Eigenvectors -> Ewarm (row-major E[i][j]) for the accurate path's
+    // preconditioner, flagged subjects only.
+    if (active && !ok) {
+      double* ew = Ewarm + k * R * R;
+#pragma unroll
+      for (int j = 0; j < MP; ++j)
+#pragma unroll
+        for (int i = 0; i < MP; ++i)
+          if (i < R && j < R) ew[i * R + j] = el(lane, j * MP + i);
     }
-    __syncwarp();
-    // S = E diag(lambda^-1/2) E^T (logical packed, into g)
+    // S = E diag(lambda^-1/2) E^T (logical packed, into g), column by column of E
 #pragma unroll
     for (int m = 0; m < MP; ++m) lam[m] = (ok && m < R) ? rsqrt(lam[m]) : 0.0;
 #pragma unroll
-    for (int i = 0; i < MP; ++i)
+    for (int e = 0; e < NT; ++e) g[e] = 0.0;
 #pragma unroll
-      for (int j = 0; j <= i; ++j) {
-        double acc = 0.0;
+    for (int m = 0; m < MP; ++m) {
+      double col[MP];
 #pragma unroll
-        for (int m = 0; m < MP; ++m) acc = fma(E[(i * MP + m) * LD] * lam[m], E[(j * MP + m) * LD], acc);
-        g[tri(i, j)] = acc;
+      for (int kk = 0; kk < HP; ++kk) {
+        const double2 v = E2[(m * HP + kk) * 32];
+        col[2 * kk] = v.x;
+        col[2 * kk + 1] = v.y;
       }
-    // m1_k = S (H C'), column by column; warp-summed into the warp accumulator.
+#pragma unroll
+      for (int i = 0; i < MP; ++i) {
+        const double li = lam[m] * col[i];
+#pragma unroll
+        for (int j = 0; j <= i; ++j) g[tri(i, j)] = fma(li, col[j], g[tri(i, j)]);
+      }
+    }
+    // m1_k = S (H C'): C' (zero unless ok) into slots [0, NT), column j of
+    // m1_k into slots [NT, NT + R); the warp sums each column over its 32
+    // subjects through shared memory (fixed order) into the warp accumulator.
 #pragma unroll
     for (int a = 0; a < MP; ++a)
 #pragma unroll
       for (int b = 0; b <= a; ++b)
-        E[tri(a, b) * LD] = (ok && a < R) ? s[a] * Cbuf[k * nt + tri(a, b)] * s[b] : 0.0;
+        el(lane, tri(a, b)) = (ok && a < R) ? s[a] * Cbuf[k * nt + tri(a, b)] * s[b] : 0.0;
 #pragma unroll 1
     for (int j = 0; j < R; ++j) {
       double y[MP];
 #pragma unroll
-      for (int c = 0; c < MP; ++c) {
-        double acc = 0.0;
-        if (c < R) {
+      for (int c = 0; c < MP; ++c) y[c] = 0.0;
 #pragma unroll
-          for (int a = 0; a < MP; ++a)
-            if (a < R) acc = fma(Hs[c * R + a], E[tri(a, j) * LD], acc);
-        }
-        y[c] = acc;
+      for (int a = 0; a < MP; ++a) {
+        if (a >= R) continue;
+        const double caj = el(lane, a >= j ? tri(a, j) : tri(j, a));
+#pragma unroll
+        for (int c = 0; c < MP; ++c)
+          if (c < R) y[c] = fma(Hs[c * R + a], caj, y[c]);
       }
 #pragma unroll
       for (int i = 0; i < MP; ++i) {
-        if (i >= R) continue;
         double acc = 0.0;
 #pragma unroll
-        for (int c = 0; c < MP; ++c) acc = fma(g[tri(i, c)], y[c], acc);
-        acc = dev::warp_sum(acc);
-        if (lane == 0) M1w[wid * MP * MP + i * R + j] += acc;
+        for (int c = 0; c < MP; ++c) acc = fma(g[i >= c ? tri(i, c) : tri(c, i)], y[c], acc);
+        if (i < R) el(lane, NT + i) = acc;
       }
+      __syncwarp();
+      if (lane < R) {
+        double acc = 0.0;
+        for (int t = 0; t < 32; ++t) acc += el((lane + t) & 31, NT + lane);
+        M1w[wid * MP * MP + lane * R + j] += acc;
+      }
+      __syncwarp();
     }
-    // S out, staged through the (now free) E slots for coalesced stores.
+    // S out (logical packed), staged through the store for coalesced rows.
 #pragma unroll
-    for (int e = 0; e < NT; ++e) E[e * LD] = g[e];
+    for (int e = 0; e < NT; ++e) el(lane, e) = g[e];
     __syncwarp();
-    const std::int64_t nk = min(static_cast<std::int64_t>(32), K - kb);
-    for (std::int64_t idx = lane; idx < nk * nt; idx += 32) {
-      const int sub = static_cast<int>(idx / nt), e = static_cast<int>(idx - (idx / nt) * nt);
-      Sbuf[(kb + sub) * nt + e] = Ew[e * LD + sub];  // packed index is size independent
-    }
+    for (int sub = 0; sub < nk; ++sub)
+      for (int e = lane; e < nt; e += 32) Sbuf[(kb + sub) * nt + e] = el(sub, e);
     __syncwarp();
   }
   __syncthreads();
@@ -496,17 +545,6 @@ __device__ __forceinline__ bool build_p(int R, std::int64_t k, std::int32_t flag
   return flagged;
 }
 
-/// Z = A * B (R x R, row-major smem), warp-cooperative.
-__device__ __forceinline__ void small_mm(int R, const double* A, const double* B, double* Z, int lane) {
-  for (int e = lane; e < R * R; e += 32) {
-    const int a = e / R, b = e - (e / R) * R;
-    double acc = 0.0;
-    for (int c = 0; c < R; ++c) acc = fma(A[a * R + c], B[c * R + b], acc);
-    Z[e] = acc;
-  }
-  __syncwarp();
-}
-
 /// Export: Q rows of every subject (p2g_fit Q_out, p2g_procrustes).
 template <int RP, int WPB>
 __global__ void __launch_bounds__(WPB * 32)
@@ -551,173 +589,6 @@ __global__ void __launch_bounds__(WPB * 32)
       for (int idx = lane; idx < nr * R; idx += 32) qdst[idx] = ch[(idx / R) * RP + (idx - (idx / R) * R)];
       __syncwarp();
     }
-  }
-}
-
-/// mode 2 (mttkrp.hpp:111-138) in Q-free form: U' rows = Q rows H_t diag(W o nH)
-/// = xv Z (+ Chat_i HW), Z = P H_t diag(W o nH); scattered with L2 fp64 reductions.
-template <int RP, int WPB>
-__global__ void __launch_bounds__(WPB * 32)
-    k_mode2_qf(ShardArgs X, int R, const double* __restrict__ Hprev, const double* __restrict__ Vprev,
-               const double* __restrict__ Wprev, const double* __restrict__ Ht, const double* __restrict__ nH,
-               const double* __restrict__ Sbuf, const double* __restrict__ Shat, const double* __restrict__ Chat,
-               const std::int32_t* __restrict__ flags, double* __restrict__ M2) {
-  __shared__ double Hs[RP * RP];
-  __shared__ double Ws[WPB][4][RP * RP];  // S, P, HW, Z
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  for (int e = threadIdx.x; e < R * R; e += blockDim.x) Hs[e] = Hprev[e];
-  __syncthreads();
-  double* S = Ws[wid][0];
-  double* P = Ws[wid][1];
-  double* HW = Ws[wid][2];
-  double* Z = Ws[wid][3];
-  const int RR = R * R;
-  const std::int64_t nwarps = static_cast<std::int64_t>(gridDim.x) * WPB;
-  for (std::int64_t k = static_cast<std::int64_t>(blockIdx.x) * WPB + wid; k < X.K; k += nwarps) {
-    const std::int32_t flag = flags[k];
-    const bool flagged = build_p<RP>(R, k, flag, Sbuf, Shat, Hs, Wprev, S, P, lane);
-    for (int e = lane; e < RR; e += 32) {
-      const int c = e - (e / R) * R;
-      HW[e] = Ht[e] * Wprev[k * R + c] * nH[c];
-    }
-    __syncwarp();
-    small_mm(R, P, HW, Z, lane);
-    if (flagged) small_mm(R, Chat + k * RR, HW, S, lane);  // S <- Chat HW (rows < R)
-    const std::int64_t r0 = X.srp[k];
-    const int I = static_cast<int>(X.srp[k + 1] - r0);
-    for (int i = lane; i < I; i += 32) {
-      double xv[RP];
-      const std::int64_t p0 = X.rp[r0 + i], p1 = X.rp[r0 + i + 1];
-      dev::csr_row_times<RP>(xv, X.ci, X.val, p0, p1, Vprev, R);
-      double u[RP];
-#pragma unroll
-      for (int c = 0; c < RP; ++c) {
-        double acc = (flagged && i < R && c < R) ? S[i * R + c] : 0.0;
-        if (c < R) {
-#pragma unroll
-          for (int a = 0; a < RP; ++a)
-            if (a < R) acc = fma(xv[a], Z[a * R + c], acc);
-        }
-        u[c] = acc;
-      }
-      for (std::int64_t p = p0; p < p1; ++p) {
-        const int j = __ldg(X.ci + p);
-        const double v = __ldg(X.val + p);
-        double* dst = M2 + static_cast<std::int64_t>(j) * R;
-#pragma unroll
-        for (int c = 0; c < RP; ++c)
-          if (c < R) atomicAdd(dst + c, v * u[c]);
-      }
-    }
-    __syncwarp();
-  }
-}
-
-/// mode 3 (mttkrp.hpp:143-166) in Q-free form, fused with next iteration's
-/// Gram: m3(k,c) = sum_i (xv_prev Z3 + Chat_i H_t)_c (xv_new)_c with
-/// Z3 = P H_t, and C_k = sum_i xv_new^T xv_new (packed lower) into Cnext.
-template <int RP, int WPB>
-__global__ void __launch_bounds__(WPB * 32)
-    k_mode3_qf(ShardArgs X, int R, const double* __restrict__ Hprev, const double* __restrict__ Vprev,
-               const double* __restrict__ Wprev, const double* __restrict__ Ht, const double* __restrict__ Vt,
-               const double* __restrict__ Sbuf, const double* __restrict__ Shat, const double* __restrict__ Chat,
-               const std::int32_t* __restrict__ flags, double* __restrict__ M3, double* __restrict__ Cnext) {
-  __shared__ double Hs[RP * RP];
-  __shared__ double Hts[RP * RP];
-  __shared__ double Ws[WPB][3][RP * RP];  // S, P, Z
-  __shared__ double chunk[WPB][32 * RP];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
-    Hs[e] = Hprev[e];
-    Hts[e] = Ht[e];
-  }
-  __syncthreads();
-  double* S = Ws[wid][0];
-  double* P = Ws[wid][1];
-  double* Z = Ws[wid][2];
-  double* ch = chunk[wid];
-  const int RR = R * R;
-  constexpr int NTP = RP * (RP + 1) / 2;
-  constexpr int kTri = (NTP + 31) / 32;
-  const int nt = R * (R + 1) / 2;
-  int ea[kTri], eb[kTri];
-#pragma unroll
-  for (int t = 0; t < kTri; ++t) {
-    const int e = lane + 32 * t;
-    int x = 0;
-    while ((x + 1) * (x + 2) / 2 <= e) ++x;
-    ea[t] = x;
-    eb[t] = e - x * (x + 1) / 2;
-  }
-  const std::int64_t nwarps = static_cast<std::int64_t>(gridDim.x) * WPB;
-  for (std::int64_t k = static_cast<std::int64_t>(blockIdx.x) * WPB + wid; k < X.K; k += nwarps) {
-    const std::int32_t flag = flags[k];
-    const bool flagged = build_p<RP>(R, k, flag, Sbuf, Shat, Hs, Wprev, S, P, lane);
-    small_mm(R, P, Hts, Z, lane);
-    if (flagged) small_mm(R, Chat + k * RR, Hts, S, lane);  // S <- Chat H_t
-    const std::int64_t r0 = X.srp[k];
-    const int I = static_cast<int>(X.srp[k + 1] - r0);
-    double part[RP];
-#pragma unroll
-    for (int c = 0; c < RP; ++c) part[c] = 0.0;
-    double cacc[kTri];
-#pragma unroll
-    for (int t = 0; t < kTri; ++t) cacc[t] = 0.0;
-    for (int b0 = 0; b0 < I; b0 += 32) {
-      const int i = b0 + lane;
-      const int nr = min(32, I - b0);
-      double xn[RP];
-      if (i < I) {
-        const std::int64_t p0 = X.rp[r0 + i], p1 = X.rp[r0 + i + 1];
-        double xp[RP];
-#pragma unroll
-        for (int r = 0; r < RP; ++r) {
-          xp[r] = 0.0;
-          xn[r] = 0.0;
-        }
-        for (std::int64_t p = p0; p < p1; ++p) {  // both gathers share the entry stream
-          const int j = __ldg(X.ci + p);
-          const double v = __ldg(X.val + p);
-          dev::axpy_row<RP>(xp, Vprev + static_cast<std::int64_t>(j) * R, v, R);
-          dev::axpy_row<RP>(xn, Vt + static_cast<std::int64_t>(j) * R, v, R);
-        }
-#pragma unroll
-        for (int c = 0; c < RP; ++c) {
-          if (c < R) {
-            double qh = (flagged && i < R) ? S[i * R + c] : 0.0;
-#pragma unroll
-            for (int a = 0; a < RP; ++a)
-              if (a < R) qh = fma(xp[a], Z[a * R + c], qh);
-            part[c] = fma(qh, xn[c], part[c]);
-          }
-        }
-      } else {
-#pragma unroll
-        for (int r = 0; r < RP; ++r) xn[r] = 0.0;
-      }
-#pragma unroll
-      for (int r = 0; r < RP; ++r) ch[lane * RP + r] = xn[r];
-      __syncwarp();
-#pragma unroll
-      for (int t = 0; t < kTri; ++t) {
-        if (lane + 32 * t < nt) {
-          double acc = cacc[t];
-          for (int rr = 0; rr < nr; ++rr) acc = fma(ch[rr * RP + ea[t]], ch[rr * RP + eb[t]], acc);
-          cacc[t] = acc;
-        }
-      }
-      __syncwarp();
-    }
-#pragma unroll
-    for (int c = 0; c < RP; ++c) {
-      if (c < R) {
-        const double t = dev::warp_sum(part[c]);
-        if (lane == 0) M3[k * R + c] = t;
-      }
-    }
-#pragma unroll
-    for (int t = 0; t < kTri; ++t)
-      if (lane + 32 * t < nt) Cnext[k * nt + lane + 32 * t] = cacc[t];
   }
 }
 
@@ -976,31 +847,6 @@ void launch_qrows(p2g_ctx* c, int R, const double* H, const double* V, const dou
                        constexpr int WPB = RP_ <= 10 ? 8 : 4;
                        k_qrows<RP_, WPB><<<grid_cap(X.K, WPB, c->num_sms, 16), WPB * 32, 0, s>>>(
                            X, R, H, V, W, Sbuf, Shat, Chat, flags, Q);
-                     }));
-  P2G_LAUNCHED(1);
-}
-
-void launch_mode2_qf(p2g_ctx* c, int R, const double* Hprev, const double* Vprev, const double* Wprev,
-                     const double* Ht, const double* nH, const double* Sbuf, const double* Shat, const double* Chat,
-                     const std::int32_t* flags, double* M2, cudaStream_t s) {
-  const ShardArgs X = shard_args_s(c);
-  P2G_CUDA(cudaMemsetAsync(M2, 0, sizeof(double) * c->J * R, s));
-  P2G_SMALL_DISPATCH(R, ({
-                       constexpr int WPB = RP_ <= 10 ? 8 : 4;
-                       k_mode2_qf<RP_, WPB><<<grid_cap(X.K, WPB, c->num_sms, 16), WPB * 32, 0, s>>>(
-                           X, R, Hprev, Vprev, Wprev, Ht, nH, Sbuf, Shat, Chat, flags, M2);
-                     }));
-  P2G_LAUNCHED(1);
-}
-
-void launch_mode3_qf(p2g_ctx* c, int R, const double* Hprev, const double* Vprev, const double* Wprev,
-                     const double* Ht, const double* Vt, const double* Sbuf, const double* Shat, const double* Chat,
-                     const std::int32_t* flags, double* M3, double* Cnext, cudaStream_t s) {
-  const ShardArgs X = shard_args_s(c);
-  P2G_SMALL_DISPATCH(R, ({
-                       constexpr int WPB = RP_ <= 10 ? 8 : 4;
-                       k_mode3_qf<RP_, WPB><<<grid_cap(X.K, WPB, c->num_sms, 16), WPB * 32, 0, s>>>(
-                           X, R, Hprev, Vprev, Wprev, Ht, Vt, Sbuf, Shat, Chat, flags, M3, Cnext);
                      }));
   P2G_LAUNCHED(1);
 }

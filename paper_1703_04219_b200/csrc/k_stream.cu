@@ -1,0 +1,396 @@
+// Small-rank (R <= 16) streaming passes of the Q-free iteration: mode 2 and
+// mode 3 (+ next iteration's Gram C), restated from mttkrp.hpp:111-166 with
+// Q_k = X_k V P_k (+ L Chat_k) rebuilt on the fly (see k_small.cu).
+//
+// Layout (B200-first):
+//  * one warp owns a batch of SB consecutive subjects.  Setup builds the
+//    batch's R x R row operators T_s in shared memory, [element][subject]
+//    (stride SB+1: lanes of different subjects hit different banks):
+//        mode 3:  T3_s = diag(w_s) Hprev^T S_s H_t          (q_i = xv_i T3)
+//        mode 2:  T2_s = T3_s diag(w_s o nH)                (u_i = xv_i T2)
+//    with S_s the packed fast-path factor or the accurate path's full Shat.
+//    Each lane computes R/LPS rows of one subject's T (LPS = 32/SB lanes
+//    per subject), all indices compile-time (exact-R template).
+//  * the batch's rows (contiguous in the CSR) stream in chunks of 32, one
+//    row per lane, across subject boundaries (full lanes regardless of I_k);
+//    each lane finds its subject in the batch row offsets.
+//  * mode 2 scatters v * u into M2 with L2 fp64 reductions (RED.ADD.F64).
+//  * mode 3 stages [xn | q o xn | 1] per row in shared memory; lanes own
+//    entries of the packed Gram C and of m3 and accumulate them in row order,
+//    flushing at subject boundaries (warp-uniform, deterministic).
+#include <algorithm>
+
+#include "dev_common.cuh"
+#include "p2g_ctx.hpp"
+
+namespace p2g {
+namespace {
+
+template <int R>
+struct StreamCfg {
+  // subjects per batch: the largest power of two keeping a lane's share of
+  // the setup (NRL rows of B, R doubles each) within ~32 registers' doubles
+  static constexpr int pick_sb() {
+    int sb = 32;
+    while (sb > 4 && ((R + 32 / sb - 1) / (32 / sb)) * R > 32) sb /= 2;
+    return sb;
+  }
+  static constexpr int SB = pick_sb();
+  static constexpr int SBP = SB + 1;                          // [element][subject] stride
+  static constexpr int LPS = 32 / SB;                         // lanes per subject in setup
+  static constexpr int NRL = (R + LPS - 1) / LPS;             // T rows per lane
+  static constexpr int RR = R * R;
+  static constexpr int NT = R * (R + 1) / 2;
+  static constexpr int CW = 2 * R + 1;                        // mode-3 row record: xn | q o xn | 1
+  static constexpr int NE = NT + R;                           // mode-3 accumulated entries
+  static constexpr int NU = (NE + 31) / 32;                   // entries per lane
+  static constexpr int WPB = 4;
+  static constexpr int kWarpT = RR * SBP;                     // doubles
+  static constexpr int kWarpCh = 32 * CW;                     // doubles (mode 3)
+};
+
+__host__ __device__ constexpr int tri_idx(int i, int j) { return i >= j ? i * (i + 1) / 2 + j : j * (j + 1) / 2 + i; }
+
+/// Builds T_s for the warp's batch [k0, k0 + nb) into Tw ([e][s], stride SBP).
+/// MODE 2 additionally scales column c by w_s[c] * nH[c].
+template <int R, int MODE>
+__device__ __forceinline__ void build_batch_ops(std::int64_t k0, int nb, const double* Hs, const double* Hts,
+                                                const double* __restrict__ nH, const double* __restrict__ Wprev,
+                                                const double* __restrict__ Sbuf, const double* __restrict__ Shat,
+                                                const std::int32_t* fl, double* Tw, int lane) {
+  using C = StreamCfg<R>;
+  // 1. stage S_s (full, row-major [c][b]) into the T area
+  for (int idx = lane; idx < nb * C::RR; idx += 32) {
+    const int s = idx / C::RR, e = idx - s * C::RR;
+    const int c = e / R, b = e - c * R;
+    const std::int64_t k = k0 + s;
+    const double v = fl[s] != P2G_FLAG_FULL_RANK ? Shat[k * C::RR + e] : Sbuf[k * C::NT + tri_idx(c, b)];
+    Tw[e * C::SBP + s] = v;
+  }
+  __syncwarp();
+  // 2. B rows a = q + LPS m of subject s: B[a][b] = sum_c H[c][a] S[c][b]
+  const int s = lane % C::SB, q = lane / C::SB;
+  const bool act = s < nb;
+  double Bm[C::NRL][R];
+#pragma unroll
+  for (int m = 0; m < C::NRL; ++m) {
+    const int a = q + C::LPS * m;
+#pragma unroll
+    for (int b = 0; b < R; ++b) Bm[m][b] = 0.0;
+    if (act && a < R) {
+#pragma unroll
+      for (int c = 0; c < R; ++c) {
+        const double h = Hs[c * R + a];
+#pragma unroll
+        for (int b = 0; b < R; ++b) Bm[m][b] = fma(h, Tw[(c * R + b) * C::SBP + s], Bm[m][b]);
+      }
+    }
+  }
+  __syncwarp();
+  // 3. T rows: T[a][c'] = w_a sum_b B[a][b] Ht[b][c'] (x w_c' nH_c' in mode 2)
+  const double* wk = Wprev + (k0 + s) * R;
+  double cs[R];
+#pragma unroll
+  for (int c = 0; c < R; ++c) cs[c] = (MODE == 2 && act) ? wk[c] * nH[c] : 1.0;
+#pragma unroll
+  for (int m = 0; m < C::NRL; ++m) {
+    const int a = q + C::LPS * m;
+    if (!act || a >= R) continue;
+    const double wa = wk[a];
+#pragma unroll
+    for (int c = 0; c < R; ++c) {
+      double acc = 0.0;
+#pragma unroll
+      for (int b = 0; b < R; ++b) acc = fma(Bm[m][b], Hts[b * R + c], acc);
+      Tw[(a * R + c) * C::SBP + s] = acc * wa * cs[c];
+    }
+  }
+  __syncwarp();
+}
+
+/// Mode 2: M2 += X_k^T (xv_i T2_s (+ Chat_i H_t diag(w o nH))) over the shard.
+template <int R>
+__global__ void __launch_bounds__(StreamCfg<R>::WPB * 32)
+    k_mode2_sb(ShardArgs X, const double* __restrict__ Hprev, const double* __restrict__ Vprev,
+               const double* __restrict__ Wprev, const double* __restrict__ Ht, const double* __restrict__ nH,
+               const double* __restrict__ Sbuf, const double* __restrict__ Shat, const double* __restrict__ Chat,
+               const std::int32_t* __restrict__ flags, double* __restrict__ M2) {
+  using C = StreamCfg<R>;
+  extern __shared__ double smem[];
+  __shared__ std::int32_t rowoff_s[C::WPB][C::SB + 1];
+  __shared__ std::int32_t fl_s[C::WPB][C::SB];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  double* Hs = smem;
+  double* Hts = Hs + C::RR;
+  double* Tw = Hts + C::RR + wid * C::kWarpT;
+  std::int32_t* rowoff = rowoff_s[wid];
+  std::int32_t* fl = fl_s[wid];
+  for (int e = threadIdx.x; e < C::RR; e += blockDim.x) {
+    Hs[e] = Hprev[e];
+    Hts[e] = Ht[e];
+  }
+  __syncthreads();
+  const std::int64_t nbatch = (X.K + C::SB - 1) / C::SB;
+  const std::int64_t nwarps = static_cast<std::int64_t>(gridDim.x) * C::WPB;
+  for (std::int64_t bt = static_cast<std::int64_t>(blockIdx.x) * C::WPB + wid; bt < nbatch; bt += nwarps) {
+    const std::int64_t k0 = bt * C::SB;
+    const int nb = static_cast<int>(min(static_cast<std::int64_t>(C::SB), X.K - k0));
+    const std::int64_t row0 = X.srp[k0];
+    const int nrows = static_cast<int>(X.srp[k0 + nb] - row0);
+    for (int s = lane; s <= C::SB; s += 32) rowoff[s] = s <= nb ? static_cast<int>(X.srp[k0 + s] - row0) : nrows;
+    if (lane < C::SB) fl[lane] = lane < nb ? flags[k0 + lane] : P2G_FLAG_FULL_RANK;
+    __syncwarp();
+    build_batch_ops<R, 2>(k0, nb, Hs, Hts, nH, Wprev, Sbuf, Shat, fl, Tw, lane);
+    int sl = 0;
+    for (int cb = 0; cb < nrows; cb += 32) {
+      const int r = cb + lane;
+      if (r < nrows) {
+        while (rowoff[sl + 1] <= r) ++sl;
+        const std::int64_t p0 = X.rp[row0 + r], p1 = X.rp[row0 + r + 1];
+        double xv[R];
+        dev::csr_row_times<R>(xv, X.ci, X.val, p0, p1, Vprev, R);
+        double u[R];
+#pragma unroll
+        for (int c = 0; c < R; ++c) {
+          double acc = 0.0;
+#pragma unroll
+          for (int a = 0; a < R; ++a) acc = fma(xv[a], Tw[(a * R + c) * C::SBP + sl], acc);
+          u[c] = acc;
+        }
+        const int i = r - rowoff[sl];
+        if (fl[sl] != P2G_FLAG_FULL_RANK && i < R) {  // completion term L Chat (rows < R)
+          const std::int64_t k = k0 + sl;
+          const double* ch = Chat + k * C::RR + i * R;
+#pragma unroll
+          for (int c = 0; c < R; ++c) {
+            double acc = 0.0;
+#pragma unroll
+            for (int b = 0; b < R; ++b) acc = fma(ch[b], Hts[b * R + c], acc);
+            u[c] = fma(acc, Wprev[k * R + c] * nH[c], u[c]);
+          }
+        }
+        for (std::int64_t p = p0; p < p1; ++p) {
+          const int j = __ldg(X.ci + p);
+          const double v = __ldg(X.val + p);
+          double* dst = M2 + static_cast<std::int64_t>(j) * R;
+#pragma unroll
+          for (int c = 0; c < R; ++c) atomicAdd(dst + c, v * u[c]);
+        }
+      }
+    }
+    __syncwarp();
+  }
+}
+
+/// Mode 3 fused with next iteration's Gram:
+///   m3(k,c) = sum_i (xv_prev,i T3_s + Chat_i H_t)_c (xv_new,i)_c,
+///   C_k     = sum_i xv_new,i^T xv_new,i (packed lower).
+template <int R>
+__global__ void __launch_bounds__(StreamCfg<R>::WPB * 32)
+    k_mode3_sb(ShardArgs X, const double* __restrict__ Hprev, const double* __restrict__ Vprev,
+               const double* __restrict__ Wprev, const double* __restrict__ Ht, const double* __restrict__ Vt,
+               const double* __restrict__ Sbuf, const double* __restrict__ Shat, const double* __restrict__ Chat,
+               const std::int32_t* __restrict__ flags, double* __restrict__ M3, double* __restrict__ Cnext) {
+  using C = StreamCfg<R>;
+  extern __shared__ double smem[];
+  __shared__ std::int32_t rowoff_s[C::WPB][C::SB + 1];
+  __shared__ std::int32_t fl_s[C::WPB][C::SB];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  double* Hs = smem;
+  double* Hts = Hs + C::RR;
+  double* Tw = Hts + C::RR + wid * (C::kWarpT + C::kWarpCh);
+  double* ch = Tw + C::kWarpT;
+  std::int32_t* rowoff = rowoff_s[wid];
+  std::int32_t* fl = fl_s[wid];
+  for (int e = threadIdx.x; e < C::RR; e += blockDim.x) {
+    Hs[e] = Hprev[e];
+    Hts[e] = Ht[e];
+  }
+  // accumulated entries owned by this lane: (ea, eb) into the row record
+  int ea[C::NU], eb[C::NU];
+#pragma unroll
+  for (int u = 0; u < C::NU; ++u) {
+    const int t = lane + 32 * u;
+    if (t < C::NT) {
+      int x = 0;
+      while ((x + 1) * (x + 2) / 2 <= t) ++x;
+      ea[u] = x;
+      eb[u] = t - x * (x + 1) / 2;
+    } else if (t < C::NE) {
+      ea[u] = R + (t - C::NT);
+      eb[u] = 2 * R;
+    } else {
+      ea[u] = 2 * R;  // unused (1 * 1)
+      eb[u] = 2 * R;
+    }
+  }
+  __syncthreads();
+  const std::int64_t nbatch = (X.K + C::SB - 1) / C::SB;
+  const std::int64_t nwarps = static_cast<std::int64_t>(gridDim.x) * C::WPB;
+  for (std::int64_t bt = static_cast<std::int64_t>(blockIdx.x) * C::WPB + wid; bt < nbatch; bt += nwarps) {
+    const std::int64_t k0 = bt * C::SB;
+    const int nb = static_cast<int>(min(static_cast<std::int64_t>(C::SB), X.K - k0));
+    const std::int64_t row0 = X.srp[k0];
+    const int nrows = static_cast<int>(X.srp[k0 + nb] - row0);
+    for (int s = lane; s <= C::SB; s += 32) rowoff[s] = s <= nb ? static_cast<int>(X.srp[k0 + s] - row0) : nrows;
+    if (lane < C::SB) fl[lane] = lane < nb ? flags[k0 + lane] : P2G_FLAG_FULL_RANK;
+    __syncwarp();
+    build_batch_ops<R, 3>(k0, nb, Hs, Hts, nullptr, Wprev, Sbuf, Shat, fl, Tw, lane);
+    double acc[C::NU];
+#pragma unroll
+    for (int u = 0; u < C::NU; ++u) acc[u] = 0.0;
+    int cur = 0;  // subject being accumulated (warp-uniform)
+    auto flush = [&](int s) {
+      const std::int64_t k = k0 + s;
+#pragma unroll
+      for (int u = 0; u < C::NU; ++u) {
+        const int t = lane + 32 * u;
+        if (t < C::NT)
+          Cnext[k * C::NT + t] = acc[u];
+        else if (t < C::NE)
+          M3[k * R + (t - C::NT)] = acc[u];
+        acc[u] = 0.0;
+      }
+    };
+    int sl = 0;
+    for (int cb = 0; cb < nrows; cb += 32) {
+      const int r = cb + lane;
+      const int nr = min(32, nrows - cb);
+      if (r < nrows) {
+        while (rowoff[sl + 1] <= r) ++sl;
+        const std::int64_t p0 = X.rp[row0 + r], p1 = X.rp[row0 + r + 1];
+        double xp[R], xn[R];
+#pragma unroll
+        for (int a = 0; a < R; ++a) {
+          xp[a] = 0.0;
+          xn[a] = 0.0;
+        }
+        for (std::int64_t p = p0; p < p1; ++p) {  // both gathers share the entry stream
+          const int j = __ldg(X.ci + p);
+          const double v = __ldg(X.val + p);
+          dev::axpy_row<R>(xp, Vprev + static_cast<std::int64_t>(j) * R, v, R);
+          dev::axpy_row<R>(xn, Vt + static_cast<std::int64_t>(j) * R, v, R);
+        }
+        double qv[R];
+#pragma unroll
+        for (int c = 0; c < R; ++c) {
+          double a0 = 0.0;
+#pragma unroll
+          for (int a = 0; a < R; ++a) a0 = fma(xp[a], Tw[(a * R + c) * C::SBP + sl], a0);
+          qv[c] = a0;
+        }
+        const int i = r - rowoff[sl];
+        if (fl[sl] != P2G_FLAG_FULL_RANK && i < R) {  // completion term L Chat (rows < R)
+          const double* chr = Chat + (k0 + sl) * C::RR + i * R;
+#pragma unroll
+          for (int c = 0; c < R; ++c) {
+            double a0 = 0.0;
+#pragma unroll
+            for (int b = 0; b < R; ++b) a0 = fma(chr[b], Hts[b * R + c], a0);
+            qv[c] += a0;
+          }
+        }
+        double* rec = ch + lane * C::CW;
+#pragma unroll
+        for (int a = 0; a < R; ++a) {
+          rec[a] = xn[a];
+          rec[R + a] = qv[a] * xn[a];
+        }
+        rec[2 * R] = 1.0;
+      }
+      __syncwarp();
+      for (int rr = 0; rr < nr; ++rr) {
+        while (cb + rr >= rowoff[cur + 1]) flush(cur++);
+        const double* rec = ch + rr * C::CW;
+#pragma unroll
+        for (int u = 0; u < C::NU; ++u) acc[u] = fma(rec[ea[u]], rec[eb[u]], acc[u]);
+      }
+      __syncwarp();
+    }
+    for (; cur < nb; ++cur) flush(cur);
+  }
+}
+
+template <int R>
+int stream_blocks(p2g_ctx* c, const void* kern, std::size_t smem) {
+  using C = StreamCfg<R>;
+  int per_sm = 0;
+  P2G_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, C::WPB * 32, smem));
+  const std::int64_t nbatch = (c->k_end - c->k_begin + C::SB - 1) / C::SB;
+  const std::int64_t want = (nbatch + C::WPB - 1) / C::WPB;
+  return static_cast<int>(std::max<std::int64_t>(
+      1, std::min<std::int64_t>(want, static_cast<std::int64_t>(c->num_sms) * std::max(per_sm, 1))));
+}
+
+ShardArgs shard_args_st(p2g_ctx* c) {
+  return ShardArgs{c->srp.get(), c->rp.get(), c->ci.get(), c->val.get(), c->k_end - c->k_begin, c->NR, c->nnz, c->J};
+}
+
+template <int R>
+void mode2_sb(p2g_ctx* c, const double* Hprev, const double* Vprev, const double* Wprev, const double* Ht,
+              const double* nH, const double* Sbuf, const double* Shat, const double* Chat, const std::int32_t* flags,
+              double* M2, cudaStream_t s) {
+  using C = StreamCfg<R>;
+  const std::size_t smem = sizeof(double) * (2 * C::RR + C::WPB * C::kWarpT);
+  auto kern = k_mode2_sb<R>;
+  P2G_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  const int nb = stream_blocks<R>(c, reinterpret_cast<const void*>(kern), smem);
+  kern<<<nb, C::WPB * 32, smem, s>>>(shard_args_st(c), Hprev, Vprev, Wprev, Ht, nH, Sbuf, Shat, Chat, flags, M2);
+}
+
+template <int R>
+void mode3_sb(p2g_ctx* c, const double* Hprev, const double* Vprev, const double* Wprev, const double* Ht,
+              const double* Vt, const double* Sbuf, const double* Shat, const double* Chat, const std::int32_t* flags,
+              double* M3, double* Cnext, cudaStream_t s) {
+  using C = StreamCfg<R>;
+  const std::size_t smem = sizeof(double) * (2 * C::RR + C::WPB * (C::kWarpT + C::kWarpCh));
+  auto kern = k_mode3_sb<R>;
+  P2G_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  const int nb = stream_blocks<R>(c, reinterpret_cast<const void*>(kern), smem);
+  kern<<<nb, C::WPB * 32, smem, s>>>(shard_args_st(c), Hprev, Vprev, Wprev, Ht, Vt, Sbuf, Shat, Chat, flags, M3,
+                                     Cnext);
+}
+
+}  // namespace
+
+#define P2G_EXACT_R_DISPATCH(R, CALL)                                   \
+  switch (R) {                                                          \
+    case 1: { constexpr int R_ = 1; CALL; } break;                      \
+    case 2: { constexpr int R_ = 2; CALL; } break;                      \
+    case 3: { constexpr int R_ = 3; CALL; } break;                      \
+    case 4: { constexpr int R_ = 4; CALL; } break;                      \
+    case 5: { constexpr int R_ = 5; CALL; } break;                      \
+    case 6: { constexpr int R_ = 6; CALL; } break;                      \
+    case 7: { constexpr int R_ = 7; CALL; } break;                      \
+    case 8: { constexpr int R_ = 8; CALL; } break;                      \
+    case 9: { constexpr int R_ = 9; CALL; } break;                      \
+    case 10: { constexpr int R_ = 10; CALL; } break;                    \
+    case 11: { constexpr int R_ = 11; CALL; } break;                    \
+    case 12: { constexpr int R_ = 12; CALL; } break;                    \
+    case 13: { constexpr int R_ = 13; CALL; } break;                    \
+    case 14: { constexpr int R_ = 14; CALL; } break;                    \
+    case 15: { constexpr int R_ = 15; CALL; } break;                    \
+    case 16: { constexpr int R_ = 16; CALL; } break;                    \
+    default: throw InvalidArgument("small-rank streaming path needs R <= 16"); \
+  }
+
+void launch_mode2_qf(p2g_ctx* c, int R, const double* Hprev, const double* Vprev, const double* Wprev,
+                     const double* Ht, const double* nH, const double* Sbuf, const double* Shat, const double* Chat,
+                     const std::int32_t* flags, double* M2, cudaStream_t s) {
+  P2G_CUDA(cudaMemsetAsync(M2, 0, sizeof(double) * c->J * R, s));
+  if (c->k_end > c->k_begin) {
+    P2G_EXACT_R_DISPATCH(R, (mode2_sb<R_>(c, Hprev, Vprev, Wprev, Ht, nH, Sbuf, Shat, Chat, flags, M2, s)));
+    P2G_LAUNCHED(1);
+  }
+}
+
+void launch_mode3_qf(p2g_ctx* c, int R, const double* Hprev, const double* Vprev, const double* Wprev,
+                     const double* Ht, const double* Vt, const double* Sbuf, const double* Shat, const double* Chat,
+                     const std::int32_t* flags, double* M3, double* Cnext, cudaStream_t s) {
+  if (c->k_end > c->k_begin) {
+    P2G_EXACT_R_DISPATCH(R, (mode3_sb<R_>(c, Hprev, Vprev, Wprev, Ht, Vt, Sbuf, Shat, Chat, flags, M3, Cnext, s)));
+    P2G_LAUNCHED(1);
+  }
+}
+
+}  // namespace p2g

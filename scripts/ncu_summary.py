@@ -16,8 +16,8 @@ want = {
     "dram_pct": "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
 }
 units = rows[1]
-stall_cols = [i for i, n in enumerate(h) if n.startswith("smsp__average_warp_latency_issue_stalled") or
-              (n.startswith("smsp__warp_issue_stalled") and n.endswith("_per_warp_active.pct"))]
+stall_cols = [i for i, n in enumerate(h) if n.startswith("smsp__average_warps_issue_stalled_") and
+              n.endswith("_per_issue_active.ratio")]
 for r in rows[2:]:
     name = r[col("Kernel Name")].split("(")[0].replace("void ", "")[-45:]
     out = {}
@@ -28,7 +28,7 @@ for r in rows[2:]:
     st = []
     for i in stall_cols:
         try:
-            st.append((float(r[i].replace(",", "")), h[i].split("stalled_")[-1].replace("_per_warp_active.pct", "")))
+            st.append((float(r[i].replace(",", "")), h[i].split("stalled_")[-1].replace("_per_issue_active.ratio", "")))
         except ValueError:
             pass
     st.sort(reverse=True)

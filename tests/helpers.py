@@ -59,3 +59,39 @@ def dense_slices(X):
             d[r - r0, X.col_idx[p0:p1]] = X.val[p0:p1]
         out.append(d)
     return out
+
+
+def assert_q_close(X, Q, Qref, H, V, W, base=1e-9, eps=1e-14):
+    """Per-subject Procrustes factors against the oracle's, with the polar
+    factor's perturbation bound: |dQ_k| / |Q_k| <= base + eps * kappa_k, where
+    kappa_k = sigma_max / sigma_r of A_k = X_k V diag(W_k) H^T over the
+    singular values kept by the canonical null rule (sigma^2 > 1e-26 sigma_max^2),
+    times cond(N) of the completion block for rank-deficient subjects.
+    Two backward-stable polar factorisations agree to O(eps kappa); a single
+    global Frobenius bound would be set by the worst-conditioned subject."""
+    worst = 0.0
+    for k in range(X.K):
+        r0, r1 = X.subj_row_ptr[k], X.subj_row_ptr[k + 1]
+        XV = np.zeros((r1 - r0, V.shape[1]))
+        for r in range(r0, r1):
+            p0, p1 = X.row_ptr[r], X.row_ptr[r + 1]
+            XV[r - r0] = X.val[p0:p1] @ V[X.col_idx[p0:p1]]
+        A = XV @ np.diag(W[k]) @ H.T
+        U, s, Vt = np.linalg.svd(A, full_matrices=False)
+        if s.size == 0 or s[0] == 0.0:
+            kappa = 1.0
+        else:
+            rho = int(np.count_nonzero(s * s > 1e-26 * s[0] * s[0]))
+            kappa = s[0] / s[rho - 1]
+            if rho < A.shape[1]:  # completion polar(N), N = L E_perp - U_rho U_rho^T L E_perp
+                Ep = Vt[rho:].T
+                LE = np.zeros((A.shape[0], Ep.shape[1]))
+                LE[:A.shape[1]] = Ep
+                N = LE - U[:, :rho] @ (U[:, :rho].T @ LE)
+                sn = np.linalg.svd(N, compute_uv=False)
+                kappa *= sn[0] / max(sn[-1], 1e-300)
+        err = np.linalg.norm(Q[r0:r1] - Qref[r0:r1]) / max(np.linalg.norm(Qref[r0:r1]), 1e-300)
+        tol = base + eps * kappa
+        assert err <= tol, (k, err, kappa)
+        worst = max(worst, err / tol)
+    return worst
