@@ -92,7 +92,8 @@ struct NnlsSmem {
 template <int RP, int WPB>
 __global__ void __launch_bounds__(WPB * 32)
     k_nnls(int R, std::int64_t n, const double* __restrict__ G, const double* __restrict__ B, double* __restrict__ X,
-           int cap, std::int32_t* err, const std::int32_t* __restrict__ rowlist, const std::int32_t* __restrict__ nlist) {
+           int cap, std::int32_t* err, const std::int32_t* __restrict__ rowlist, const std::int32_t* __restrict__ nlist,
+           unsigned long long* __restrict__ masks, int warm) {
   extern __shared__ double smem[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   double* Gs = smem;
@@ -121,11 +122,17 @@ __global__ void __launch_bounds__(WPB * 32)
       w[r] = v;
       x[r] = 0.0;
     }
-    unsigned long long passive = 0ull;
+    // Warm start (optional, as in k_nnls_thread): begin from the row's previous
+    // passive set; an infeasible warm solve sheds its non-positive coordinates
+    // and retries (x = 0 throughout), an emptied set is the reference's cold start.
+    const unsigned long long full = R >= 64 ? ~0ull : ((1ull << R) - 1ull);
+    unsigned long long passive = (masks && warm) ? (masks[row] & full) : 0ull;
+    bool warm_phase = passive != 0ull;
     int iters = 0;
     bool failed = false;
     __syncwarp();
     while (true) {
+     if (!warm_phase) {
       // entering coordinate: argmax_{j not passive, w_j > 1e-10} w_j, first index on ties
       double best = 1e-10;
       int enter = -1;
@@ -145,6 +152,7 @@ __global__ void __launch_bounds__(WPB * 32)
       }
       if (enter < 0) break;
       passive |= 1ull << enter;
+     }
       while (true) {
         if (++iters > cap) {
           failed = true;
@@ -222,6 +230,16 @@ __global__ void __launch_bounds__(WPB * 32)
           __syncwarp();
           break;
         }
+        if (warm_phase) {  // x = 0: drop the non-positive coordinates and re-solve
+          unsigned long long drop = 0ull;
+          for (int a2 = lane; a2 < np; a2 += 32)
+            if (!(sp[a2] > 0.0)) drop |= 1ull << pset[a2];
+          for (int o = 16; o > 0; o >>= 1) drop |= __shfl_xor_sync(dev::kFull, drop, o);
+          passive &= ~drop;
+          __syncwarp();
+          if (passive == 0ull) break;
+          continue;
+        }
         // step toward s until the first passive coordinate hits zero
         for (int r = lane; r < R; r += 32) sv[r] = 0.0;
         __syncwarp();
@@ -258,6 +276,7 @@ __global__ void __launch_bounds__(WPB * 32)
         passive &= ~drop;
         __syncwarp();
       }
+      warm_phase = false;
       if (failed) break;
       // w = b - G x
       for (int r = lane; r < R; r += 32) {
@@ -268,6 +287,7 @@ __global__ void __launch_bounds__(WPB * 32)
       __syncwarp();
     }
     if (failed && lane == 0) atomicAdd(err, 1);
+    if (masks && lane == 0) masks[row] = passive;
     for (int r = lane; r < R; r += 32) X[row * R + r] = x[r];
     __syncwarp();
   }
@@ -435,7 +455,8 @@ void small_smem_optin() {
 
 template <int RP>
 void nnls_launch(int R, std::int64_t n, const double* G, const double* B, double* X, int cap, std::int32_t* err,
-                 const std::int32_t* rowlist, const std::int32_t* nlist, cudaStream_t s) {
+                 const std::int32_t* rowlist, const std::int32_t* nlist, unsigned long long* masks, int warm,
+                 cudaStream_t s) {
   constexpr int WPB = RP <= 16 ? 8 : 4;
   const std::size_t per_warp = sizeof(double) * (NnlsSmem<RP>::kDoubles + (NnlsSmem<RP>::kInts + 1) / 2);
   const std::size_t smem = sizeof(double) * RP * RP + WPB * per_warp;
@@ -443,25 +464,27 @@ void nnls_launch(int R, std::int64_t n, const double* G, const double* B, double
   P2G_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   const std::int64_t want = (n + WPB - 1) / WPB;
   const int blocks = static_cast<int>(std::max<std::int64_t>(1, std::min<std::int64_t>(want, 148 * 8)));
-  kern<<<blocks, WPB * 32, smem, s>>>(R, n, G, B, X, cap, err, rowlist, nlist);
+  kern<<<blocks, WPB * 32, smem, s>>>(R, n, G, B, X, cap, err, rowlist, nlist, masks, warm);
 }
 
 template <int RP>
 void nnls_warp(int R, std::int64_t n, const double* G, const double* B, double* X, int cap, std::int32_t* err,
-               const std::int32_t* rowlist, const std::int32_t* nlist, cudaStream_t s) {
-  nnls_launch<RP>(R, n, G, B, X, cap, err, rowlist, nlist, s);
+               const std::int32_t* rowlist, const std::int32_t* nlist, unsigned long long* masks, int warm,
+               cudaStream_t s) {
+  nnls_launch<RP>(R, n, G, B, X, cap, err, rowlist, nlist, masks, warm, s);
 }
 
 void nnls_warp_any(int R, std::int64_t n, const double* G, const double* B, double* X, int cap, std::int32_t* err,
-                   const std::int32_t* rowlist, const std::int32_t* nlist, cudaStream_t s) {
+                   const std::int32_t* rowlist, const std::int32_t* nlist, cudaStream_t s,
+                   unsigned long long* masks = nullptr, int warm = 0) {
   if (R <= 8)
-    nnls_warp<8>(R, n, G, B, X, cap, err, rowlist, nlist, s);
+    nnls_warp<8>(R, n, G, B, X, cap, err, rowlist, nlist, masks, warm, s);
   else if (R <= 16)
-    nnls_warp<16>(R, n, G, B, X, cap, err, rowlist, nlist, s);
+    nnls_warp<16>(R, n, G, B, X, cap, err, rowlist, nlist, masks, warm, s);
   else if (R <= 32)
-    nnls_warp<32>(R, n, G, B, X, cap, err, rowlist, nlist, s);
+    nnls_warp<32>(R, n, G, B, X, cap, err, rowlist, nlist, masks, warm, s);
   else if (R <= 40)
-    nnls_warp<40>(R, n, G, B, X, cap, err, rowlist, nlist, s);
+    nnls_warp<40>(R, n, G, B, X, cap, err, rowlist, nlist, masks, warm, s);
   else
     throw InvalidArgument("rank above 40 unsupported");
 }
@@ -483,7 +506,8 @@ void reduce_partials(const double* partials, int nparts, std::int64_t len, doubl
 }
 
 void launch_nnls_rows(int R, std::int64_t n, const double* G, const double* B, double* X, int max_iter,
-                      std::int32_t* err, std::int32_t* work, cudaStream_t s, unsigned* masks, int warm) {
+                      std::int32_t* err, std::int32_t* work, cudaStream_t s, unsigned* masks, int warm,
+                      unsigned long long* masks64) {
   if (n == 0) return;
   const int cap = max_iter > 0 ? max_iter : 30 * R;
   if (R <= kSmallRankMax && work) {
@@ -495,7 +519,7 @@ void launch_nnls_rows(int R, std::int64_t n, const double* G, const double* B, d
     P2G_LAUNCHED(1);
     return;
   }
-  nnls_warp_any(R, n, G, B, X, cap, err, nullptr, nullptr, s);
+  nnls_warp_any(R, n, G, B, X, cap, err, nullptr, nullptr, s, masks64, masks64 ? warm : 0);
   P2G_LAUNCHED(1);
 }
 

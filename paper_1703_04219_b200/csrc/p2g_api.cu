@@ -212,6 +212,11 @@ void alloc_state(p2g_ctx* c, int R) {
     c->Ewarm.resize(ks * RR);
     c->mask_v.resize(static_cast<std::size_t>(std::max<std::int64_t>(c->J, 1)));
     c->mask_w.resize(ks);
+  } else {
+    // right singular vectors per subject: warm start / preconditioner (12.8 KB per subject at R = 40)
+    c->Ewarm.resize(static_cast<std::size_t>(std::max<std::int64_t>(Ks(c), 1)) * RR);
+    c->mask64_v.resize(static_cast<std::size_t>(std::max<std::int64_t>(c->J, 1)));
+    c->mask64_w.resize(static_cast<std::size_t>(std::max<std::int64_t>(Ks(c), 1)));
   }
 }
 
@@ -256,12 +261,13 @@ int procrustes_step(p2g_ctx* c, double* part) {
   } else {
     {
       Phase ph(c, "procrustes");
-      n1 = launch_procrustes(c, R, c->H.get(), c->V.get(), c->W.get(), c->Q.get(), c->flags.get(), part,
-                             kMaxPartials, s);
+      n1 = launch_procrustes_large(c, R, c->H.get(), c->V.get(), c->W.get(), c->Q.get(), c->flags.get(), part,
+                                   c->Ewarm.get(), c->ew_valid ? 1 : 0, kMaxPartials, s);
+      c->ew_valid = true;
     }
     Phase ph(c, "procrustes_accurate");
     n2 = launch_procrustes_accurate(c, R, c->H.get(), c->V.get(), c->W.get(), c->Q.get(), c->flags.get(),
-                                    part + static_cast<std::size_t>(n1) * RR, nullptr, nullptr, nullptr, s);
+                                    part + static_cast<std::size_t>(n1) * RR, c->Ewarm.get(), nullptr, nullptr, s);
   }
   return n1 + n2;
 }
@@ -359,7 +365,7 @@ IterOut iterate(p2g_ctx* c, bool nonneg, int iter) {
     Phase ph(c, "update_v");  // V_t -> Vp
     if (nonneg) {
       launch_nnls_rows(R, c->J, c->G2.get(), c->M2.get(), c->Vp.get(), 0, c->counters.get() + 1, c->redo.get(), s,
-                       c->mask_v.get(), c->masks_valid ? 1 : 0);
+                       c->mask_v.get(), c->masks_valid ? 1 : 0, c->mask64_v.get());
     } else {
       launch_pinv(R, c->G2.get(), c->pinvbuf.get(), s);
       launch_rows_times(R, c->J, c->M2.get(), c->pinvbuf.get(), c->Vp.get(), s);
@@ -380,8 +386,8 @@ IterOut iterate(p2g_ctx* c, bool nonneg, int iter) {
     Phase ph(c, "update_w");  // W_t -> Wp
     if (nonneg) {
       launch_nnls_rows(R, Ks(c), c->G3.get(), c->m3.get(), c->Wp.get(), 0, c->counters.get() + 1, c->redo.get(), s,
-                       c->mask_w.get(), c->masks_valid ? 1 : 0);
-      c->masks_valid = small_rank(c);
+                       c->mask_w.get(), c->masks_valid ? 1 : 0, c->mask64_w.get());
+      c->masks_valid = true;
     } else {
       launch_pinv(R, c->G3.get(), c->pinvbuf.get(), s);
       launch_rows_times(R, Ks(c), c->m3.get(), c->pinvbuf.get(), c->Wp.get(), s);
@@ -402,10 +408,15 @@ IterOut iterate(p2g_ctx* c, bool nonneg, int iter) {
   P2G_CUDA(cudaStreamSynchronize(s));
   collect_timing(c);
   const std::int32_t* cnt = reinterpret_cast<const std::int32_t*>(c->pinned + 4);
-  if (std::getenv("P2G_DEBUG") && cnt[7] > 0)
-    std::fprintf(stderr, "[p2g] iter %d polar sweeps: mean %.2f max %d mean-warp-max %.2f\n", iter,
-                 static_cast<double>(cnt[4]) / static_cast<double>(std::max<std::int64_t>(Ks(c), 1)), cnt[5],
-                 static_cast<double>(cnt[6]) / cnt[7]);
+  if (std::getenv("P2G_DEBUG") && cnt[7] > 0) {
+    if (small_rank(c))
+      std::fprintf(stderr, "[p2g] iter %d polar sweeps: mean %.2f max %d mean-warp-max %.2f\n", iter,
+                   static_cast<double>(cnt[4]) / static_cast<double>(std::max<std::int64_t>(Ks(c), 1)), cnt[5],
+                   static_cast<double>(cnt[6]) / cnt[7]);
+    else
+      std::fprintf(stderr, "[p2g] iter %d large-R Jacobi sweeps: mean %.2f per pass, max %d, redone %d of %d\n", iter,
+                   static_cast<double>(cnt[4]) / (cnt[7] + cnt[6]), cnt[5], cnt[6], cnt[7]);
+  }
   if (cnt[2] > 0) throw NumericalError("svd operand: non-finite entries");
   if (cnt[1] > 0) throw NumericalError("NNLS did not converge");
   IterOut o{c->pinned[0], c->pinned[1]};

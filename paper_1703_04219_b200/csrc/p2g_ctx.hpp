@@ -129,6 +129,7 @@ struct p2g_ctx {
   p2g::DBuf<std::int32_t> redo;       // NNLS rows re-solved by the warp (pinv) kernel
   p2g::DBuf<double> m2part;           // per-range J x R partials of the on-chip mode-2 kernel
   p2g::DBuf<unsigned> mask_v, mask_w; // NNLS passive sets of the previous iteration (warm start)
+  p2g::DBuf<unsigned long long> mask64_v, mask64_w;  // same, R > 16
   bool masks_valid = false;
   bool state_valid = false;
 
@@ -150,6 +151,9 @@ int launch_procrustes(p2g_ctx* c, int R, const double* H, const double* V, const
                       std::int32_t* flags, double* m1_partials, int max_blocks, cudaStream_t s);
 // Accurate Jacobi-SVD path over the subjects flagged P2G_FLAG_ACCURATE;
 // writes one R x R m1 partial per block (count = procrustes_accurate_blocks).
+int launch_procrustes_large(p2g_ctx* c, int R, const double* H, const double* V, const double* W, double* Q,
+                            std::int32_t* flags, double* m1_partials, double* Ewarm, int ew_valid, int max_blocks,
+                            cudaStream_t s);
 int launch_procrustes_accurate(p2g_ctx* c, int R, const double* H, const double* V, const double* W, double* Q,
                                std::int32_t* flags, double* m1_partials, const double* Ebuf, double* Shat,
                                double* Chat, cudaStream_t s);
@@ -195,11 +199,11 @@ int gram_partials(int R, std::int64_t n, const double* A, const double* B, doubl
                   cudaStream_t s);  // returns #partials; each partial R*R (+1 cross if B)
 void reduce_partials(const double* partials, int nparts, std::int64_t len, double* out, cudaStream_t s);
 // work: n+1 ints of scratch (thread-per-row path for R <= 16) or null.
-// masks: n passive-set bit masks (R <= 16) carried across calls for the warm
-// start (warm != 0 uses them), or null.
+// masks / masks64: n passive-set bit masks (R <= 16 / R <= 64) carried across
+// calls for the warm start (warm != 0 uses them), or null.
 void launch_nnls_rows(int R, std::int64_t n, const double* G, const double* B, double* X, int max_iter,
                       std::int32_t* err, std::int32_t* work, cudaStream_t s, unsigned* masks = nullptr,
-                      int warm = 0);
+                      int warm = 0, unsigned long long* masks64 = nullptr);
 void launch_rows_times(int R, std::int64_t n, const double* B, const double* P, double* X,
                        cudaStream_t s);  // X = B * P (row-major rows)
 void launch_pinv(int n, const double* G, double* out, cudaStream_t s);
