@@ -65,6 +65,68 @@ __device__ __forceinline__ void csr_row_times(double (&acc)[RP], const int32_t* 
   }
 }
 
+/// acc[u] += X_row(u) . V for U rows at once, V1 only (NV = 1) or also
+/// acc2[u] += X_row(u) . V2 (NV = 2): the t-th entry of every row is loaded
+/// together, so a lane keeps U independent ci -> V dependency chains in
+/// flight (the streaming kernels are bound by this gather latency).  V rows
+/// are read as 16-byte vectors when R is even.  Same per-row accumulation
+/// order as csr_row_times (entries ascending).
+template <int R, int U, int NV>
+__device__ __forceinline__ void csr_rows_times(double (&acc)[U][R], double (&acc2)[U][R],
+                                               const int32_t* __restrict__ ci, const double* __restrict__ val,
+                                               const int64_t (&p0)[U], const int64_t (&p1)[U],
+                                               const double* __restrict__ V1, const double* __restrict__ V2) {
+#pragma unroll
+  for (int u = 0; u < U; ++u)
+#pragma unroll
+    for (int a = 0; a < R; ++a) {
+      acc[u][a] = 0.0;
+      if (NV == 2) acc2[u][a] = 0.0;
+    }
+  int64_t p[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) p[u] = p0[u];
+  while (true) {
+    bool act[U], any = false;
+    int j[U];
+    double v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      act[u] = p[u] < p1[u];
+      any |= act[u];
+      j[u] = act[u] ? __ldg(ci + p[u]) : 0;
+      v[u] = act[u] ? __ldg(val + p[u]) : 0.0;
+    }
+    if (!any) break;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (!act[u]) continue;
+      const double* r1 = V1 + static_cast<int64_t>(j[u]) * R;
+      const double* r2 = V2 + static_cast<int64_t>(j[u]) * R;
+      if constexpr (R % 2 == 0) {
+#pragma unroll
+        for (int a = 0; a < R; a += 2) {
+          const double2 x = __ldg(reinterpret_cast<const double2*>(r1 + a));
+          acc[u][a] = fma(v[u], x.x, acc[u][a]);
+          acc[u][a + 1] = fma(v[u], x.y, acc[u][a + 1]);
+          if (NV == 2) {
+            const double2 y = __ldg(reinterpret_cast<const double2*>(r2 + a));
+            acc2[u][a] = fma(v[u], y.x, acc2[u][a]);
+            acc2[u][a + 1] = fma(v[u], y.y, acc2[u][a + 1]);
+          }
+        }
+      } else {
+#pragma unroll
+        for (int a = 0; a < R; ++a) {
+          acc[u][a] = fma(v[u], __ldg(r1 + a), acc[u][a]);
+          if (NV == 2) acc2[u][a] = fma(v[u], __ldg(r2 + a), acc2[u][a]);
+        }
+      }
+      ++p[u];
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Warp-cooperative small dense algebra on shared memory (row-major, ld = n).
 // ---------------------------------------------------------------------------

@@ -14,7 +14,8 @@
 //  * the batch's rows (contiguous in the CSR) stream in chunks of 32, one
 //    row per lane, across subject boundaries (full lanes regardless of I_k);
 //    each lane finds its subject in the batch row offsets.
-//  * mode 2 scatters v * u into M2 with L2 fp64 reductions (RED.ADD.F64).
+//  * mode 2 writes the row factors u_i (coalesced); M2 = X^T U is read out
+//    from the CSC copy without atomics (k_csc.cu).
 //  * mode 3 stages [xn | q o xn | 1] per row in shared memory; lanes own
 //    entries of the packed Gram C and of m3 and accumulate them in row order,
 //    flushing at subject boundaries (warp-uniform, deterministic).
@@ -46,7 +47,9 @@ struct StreamCfg {
   static constexpr int NU = (NE + 31) / 32;                   // entries per lane
   static constexpr int WPB = 4;
   static constexpr int kWarpT = RR * SBP;                     // doubles
-  static constexpr int kWarpCh = 32 * CW;                     // doubles (mode 3)
+  static constexpr int UM2 = 4;                               // rows per lane in flight (mode 2)
+  static constexpr int UM3 = 2;                               // rows per lane in flight (mode 3)
+  static constexpr int kWarpCh = 32 * UM3 * CW;               // doubles (mode 3 row records)
 };
 
 __host__ __device__ constexpr int tri_idx(int i, int j) { return i >= j ? i * (i + 1) / 2 + j : j * (j + 1) / 2 + i; }
@@ -108,13 +111,14 @@ __device__ __forceinline__ void build_batch_ops(std::int64_t k0, int nb, const d
   __syncwarp();
 }
 
-/// Mode 2: M2 += X_k^T (xv_i T2_s (+ Chat_i H_t diag(w o nH))) over the shard.
+/// Mode 2 row factors: u_i = xv_i T2_s (+ Chat_i H_t diag(w o nH)) -> U (NR x R);
+/// M2 = X^T U follows from the CSC pass (k_csc.cu).
 template <int R>
 __global__ void __launch_bounds__(StreamCfg<R>::WPB * 32)
     k_mode2_sb(ShardArgs X, const double* __restrict__ Hprev, const double* __restrict__ Vprev,
                const double* __restrict__ Wprev, const double* __restrict__ Ht, const double* __restrict__ nH,
                const double* __restrict__ Sbuf, const double* __restrict__ Shat, const double* __restrict__ Chat,
-               const std::int32_t* __restrict__ flags, double* __restrict__ M2) {
+               const std::int32_t* __restrict__ flags, double* __restrict__ U) {
   using C = StreamCfg<R>;
   extern __shared__ double smem[];
   __shared__ std::int32_t rowoff_s[C::WPB][C::SB + 1];
@@ -142,40 +146,51 @@ __global__ void __launch_bounds__(StreamCfg<R>::WPB * 32)
     __syncwarp();
     build_batch_ops<R, 2>(k0, nb, Hs, Hts, nH, Wprev, Sbuf, Shat, fl, Tw, lane);
     int sl = 0;
-    for (int cb = 0; cb < nrows; cb += 32) {
-      const int r = cb + lane;
-      if (r < nrows) {
-        while (rowoff[sl + 1] <= r) ++sl;
-        const std::int64_t p0 = X.rp[row0 + r], p1 = X.rp[row0 + r + 1];
-        double xv[R];
-        dev::csr_row_times<R>(xv, X.ci, X.val, p0, p1, Vprev, R);
-        double u[R];
+    constexpr int UR = C::UM2;
+    for (int cb = 0; cb < nrows; cb += 32 * UR) {
+      std::int64_t p0[UR], p1[UR];
+      int su[UR];
+#pragma unroll
+      for (int u = 0; u < UR; ++u) {
+        const int r = cb + lane + 32 * u;
+        p0[u] = p1[u] = 0;
+        su[u] = -1;
+        if (r < nrows) {
+          while (rowoff[sl + 1] <= r) ++sl;
+          su[u] = sl;
+          p0[u] = X.rp[row0 + r];
+          p1[u] = X.rp[row0 + r + 1];
+        }
+      }
+      double xv[UR][R];
+      dev::csr_rows_times<R, UR, 1>(xv, xv, X.ci, X.val, p0, p1, Vprev, Vprev);
+#pragma unroll
+      for (int u = 0; u < UR; ++u) {
+        const int s_ = su[u];
+        if (s_ < 0) continue;
+        double uv[R];
 #pragma unroll
         for (int c = 0; c < R; ++c) {
           double acc = 0.0;
 #pragma unroll
-          for (int a = 0; a < R; ++a) acc = fma(xv[a], Tw[(a * R + c) * C::SBP + sl], acc);
-          u[c] = acc;
+          for (int a = 0; a < R; ++a) acc = fma(xv[u][a], Tw[(a * R + c) * C::SBP + s_], acc);
+          uv[c] = acc;
         }
-        const int i = r - rowoff[sl];
-        if (fl[sl] != P2G_FLAG_FULL_RANK && i < R) {  // completion term L Chat (rows < R)
-          const std::int64_t k = k0 + sl;
-          const double* ch = Chat + k * C::RR + i * R;
+        const int i = cb + lane + 32 * u - rowoff[s_];
+        if (fl[s_] != P2G_FLAG_FULL_RANK && i < R) {  // completion term L Chat (rows < R)
+          const std::int64_t k = k0 + s_;
+          const double* chr = Chat + k * C::RR + i * R;
 #pragma unroll
           for (int c = 0; c < R; ++c) {
             double acc = 0.0;
 #pragma unroll
-            for (int b = 0; b < R; ++b) acc = fma(ch[b], Hts[b * R + c], acc);
-            u[c] = fma(acc, Wprev[k * R + c] * nH[c], u[c]);
+            for (int b = 0; b < R; ++b) acc = fma(chr[b], Hts[b * R + c], acc);
+            uv[c] = fma(acc, Wprev[k * R + c] * nH[c], uv[c]);
           }
         }
-        for (std::int64_t p = p0; p < p1; ++p) {
-          const int j = __ldg(X.ci + p);
-          const double v = __ldg(X.val + p);
-          double* dst = M2 + static_cast<std::int64_t>(j) * R;
+        double* urow = U + (row0 + cb + lane + 32 * u) * R;  // consecutive lanes, consecutive rows
 #pragma unroll
-          for (int c = 0; c < R; ++c) atomicAdd(dst + c, v * u[c]);
-        }
+        for (int c = 0; c < R; ++c) urow[c] = uv[c];
       }
     }
     __syncwarp();
@@ -253,35 +268,40 @@ __global__ void __launch_bounds__(StreamCfg<R>::WPB * 32)
       }
     };
     int sl = 0;
-    for (int cb = 0; cb < nrows; cb += 32) {
-      const int r = cb + lane;
-      const int nr = min(32, nrows - cb);
-      if (r < nrows) {
-        while (rowoff[sl + 1] <= r) ++sl;
-        const std::int64_t p0 = X.rp[row0 + r], p1 = X.rp[row0 + r + 1];
-        double xp[R], xn[R];
+    constexpr int UR = C::UM3;
+    for (int cb = 0; cb < nrows; cb += 32 * UR) {
+      const int nr = min(32 * UR, nrows - cb);
+      std::int64_t p0[UR], p1[UR];
+      int su[UR];
 #pragma unroll
-        for (int a = 0; a < R; ++a) {
-          xp[a] = 0.0;
-          xn[a] = 0.0;
+      for (int u = 0; u < UR; ++u) {
+        const int r = cb + lane + 32 * u;
+        p0[u] = p1[u] = 0;
+        su[u] = -1;
+        if (r < nrows) {
+          while (rowoff[sl + 1] <= r) ++sl;
+          su[u] = sl;
+          p0[u] = X.rp[row0 + r];
+          p1[u] = X.rp[row0 + r + 1];
         }
-        for (std::int64_t p = p0; p < p1; ++p) {  // both gathers share the entry stream
-          const int j = __ldg(X.ci + p);
-          const double v = __ldg(X.val + p);
-          dev::axpy_row<R>(xp, Vprev + static_cast<std::int64_t>(j) * R, v, R);
-          dev::axpy_row<R>(xn, Vt + static_cast<std::int64_t>(j) * R, v, R);
-        }
+      }
+      double xp[UR][R], xn[UR][R];  // both gathers share the entry stream
+      dev::csr_rows_times<R, UR, 2>(xp, xn, X.ci, X.val, p0, p1, Vprev, Vt);
+#pragma unroll
+      for (int u = 0; u < UR; ++u) {
+        const int s_ = su[u];
+        if (s_ < 0) continue;
         double qv[R];
 #pragma unroll
         for (int c = 0; c < R; ++c) {
           double a0 = 0.0;
 #pragma unroll
-          for (int a = 0; a < R; ++a) a0 = fma(xp[a], Tw[(a * R + c) * C::SBP + sl], a0);
+          for (int a = 0; a < R; ++a) a0 = fma(xp[u][a], Tw[(a * R + c) * C::SBP + s_], a0);
           qv[c] = a0;
         }
-        const int i = r - rowoff[sl];
-        if (fl[sl] != P2G_FLAG_FULL_RANK && i < R) {  // completion term L Chat (rows < R)
-          const double* chr = Chat + (k0 + sl) * C::RR + i * R;
+        const int i = cb + lane + 32 * u - rowoff[s_];
+        if (fl[s_] != P2G_FLAG_FULL_RANK && i < R) {  // completion term L Chat (rows < R)
+          const double* chr = Chat + (k0 + s_) * C::RR + i * R;
 #pragma unroll
           for (int c = 0; c < R; ++c) {
             double a0 = 0.0;
@@ -290,11 +310,11 @@ __global__ void __launch_bounds__(StreamCfg<R>::WPB * 32)
             qv[c] += a0;
           }
         }
-        double* rec = ch + lane * C::CW;
+        double* rec = ch + (lane + 32 * u) * C::CW;
 #pragma unroll
         for (int a = 0; a < R; ++a) {
-          rec[a] = xn[a];
-          rec[R + a] = qv[a] * xn[a];
+          rec[a] = xn[u][a];
+          rec[R + a] = qv[a] * xn[u][a];
         }
         rec[2 * R] = 1.0;
       }
@@ -329,13 +349,13 @@ ShardArgs shard_args_st(p2g_ctx* c) {
 template <int R>
 void mode2_sb(p2g_ctx* c, const double* Hprev, const double* Vprev, const double* Wprev, const double* Ht,
               const double* nH, const double* Sbuf, const double* Shat, const double* Chat, const std::int32_t* flags,
-              double* M2, cudaStream_t s) {
+              double* U, cudaStream_t s) {
   using C = StreamCfg<R>;
   const std::size_t smem = sizeof(double) * (2 * C::RR + C::WPB * C::kWarpT);
   auto kern = k_mode2_sb<R>;
   P2G_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   const int nb = stream_blocks<R>(c, reinterpret_cast<const void*>(kern), smem);
-  kern<<<nb, C::WPB * 32, smem, s>>>(shard_args_st(c), Hprev, Vprev, Wprev, Ht, nH, Sbuf, Shat, Chat, flags, M2);
+  kern<<<nb, C::WPB * 32, smem, s>>>(shard_args_st(c), Hprev, Vprev, Wprev, Ht, nH, Sbuf, Shat, Chat, flags, U);
 }
 
 template <int R>
@@ -376,10 +396,9 @@ void mode3_sb(p2g_ctx* c, const double* Hprev, const double* Vprev, const double
 
 void launch_mode2_qf(p2g_ctx* c, int R, const double* Hprev, const double* Vprev, const double* Wprev,
                      const double* Ht, const double* nH, const double* Sbuf, const double* Shat, const double* Chat,
-                     const std::int32_t* flags, double* M2, cudaStream_t s) {
-  P2G_CUDA(cudaMemsetAsync(M2, 0, sizeof(double) * c->J * R, s));
+                     const std::int32_t* flags, double* U, cudaStream_t s) {
   if (c->k_end > c->k_begin) {
-    P2G_EXACT_R_DISPATCH(R, (mode2_sb<R_>(c, Hprev, Vprev, Wprev, Ht, nH, Sbuf, Shat, Chat, flags, M2, s)));
+    P2G_EXACT_R_DISPATCH(R, (mode2_sb<R_>(c, Hprev, Vprev, Wprev, Ht, nH, Sbuf, Shat, Chat, flags, U, s)));
     P2G_LAUNCHED(1);
   }
 }

@@ -215,6 +215,7 @@ void alloc_state(p2g_ctx* c, int R) {
   } else {
     // right singular vectors per subject: warm start / preconditioner (12.8 KB per subject at R = 40)
     c->Ewarm.resize(static_cast<std::size_t>(std::max<std::int64_t>(Ks(c), 1)) * RR);
+    c->Ubuf.resize(static_cast<std::size_t>(std::max<std::int64_t>(c->NR, 1)) * R);
     c->mask64_v.resize(static_cast<std::size_t>(std::max<std::int64_t>(c->J, 1)));
     c->mask64_w.resize(static_cast<std::size_t>(std::max<std::int64_t>(Ks(c), 1)));
   }
@@ -354,11 +355,15 @@ IterOut iterate(p2g_ctx* c, bool nonneg, int iter) {
   }
   {
     Phase ph(c, "mode2");
+    // row factors U (small R: into the Q buffer, unused until export), then
+    // M2 = X^T U from the CSC copy (atomics-free, deterministic)
+    double* U = qf ? c->Q.get() : c->Ubuf.get();
     if (qf)
       launch_mode2_qf(c, R, c->H.get(), c->V.get(), c->W.get(), c->Hp.get(), c->nH.get(), c->Sbuf.get(),
-                      c->Ebuf.get(), c->Chat.get(), c->flags.get(), c->M2.get(), s);
+                      c->Ebuf.get(), c->Chat.get(), c->flags.get(), U, s);
     else
-      launch_mode2(c, R, c->Q.get(), c->Hp.get(), c->W.get(), c->nH.get(), c->M2.get(), s);
+      launch_urows_large(c, R, c->Q.get(), c->Hp.get(), c->W.get(), c->nH.get(), U, s);
+    launch_csc_mode2(c, R, U, c->M2.get(), s);
     allreduce(c, c->M2.get(), static_cast<std::size_t>(c->J) * R);
   }
   {
@@ -551,6 +556,7 @@ extern "C" int p2g_load_csr(p2g_ctx* c, int64_t K, int64_t J, const int64_t* srp
     for (int64_t p = 0; p < nnz_t; ++p) acc += val[p] * val[p];
     c->norm_x = acc;
     P2G_CUDA(cudaStreamSynchronize(c->stream));
+    build_csc(c);
     c->loaded = true;
     c->state_valid = false;
   });

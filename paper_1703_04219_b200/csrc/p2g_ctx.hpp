@@ -128,6 +128,11 @@ struct p2g_ctx {
   bool c_valid = false;               // Cbuf holds Gram of X V for the current V
   p2g::DBuf<std::int32_t> redo;       // NNLS rows re-solved by the warp (pinv) kernel
   p2g::DBuf<double> m2part;           // per-range J x R partials of the on-chip mode-2 kernel
+  // column-major copy of the shard for the atomics-free mode-2 pass (k_csc.cu)
+  p2g::DBuf<std::int64_t> col_ptr, seg_ptr, seg_beg, seg_end;
+  p2g::DBuf<std::int32_t> csc_row;
+  p2g::DBuf<double> csc_val, seg_part, Ubuf;
+  std::int64_t nseg = 0;
   p2g::DBuf<unsigned> mask_v, mask_w; // NNLS passive sets of the previous iteration (warm start)
   p2g::DBuf<unsigned long long> mask64_v, mask64_w;  // same, R > 16
   bool masks_valid = false;
@@ -151,6 +156,10 @@ int launch_procrustes(p2g_ctx* c, int R, const double* H, const double* V, const
                       std::int32_t* flags, double* m1_partials, int max_blocks, cudaStream_t s);
 // Accurate Jacobi-SVD path over the subjects flagged P2G_FLAG_ACCURATE;
 // writes one R x R m1 partial per block (count = procrustes_accurate_blocks).
+void build_csc(p2g_ctx* c);
+void launch_csc_mode2(p2g_ctx* c, int R, const double* U, double* M2, cudaStream_t s);
+void launch_urows_large(p2g_ctx* c, int R, const double* Q, const double* H, const double* W, const double* nH,
+                        double* U, cudaStream_t s);
 int launch_procrustes_large(p2g_ctx* c, int R, const double* H, const double* V, const double* W, double* Q,
                             std::int32_t* flags, double* m1_partials, double* Ewarm, int ew_valid, int max_blocks,
                             cudaStream_t s);
