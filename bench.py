@@ -102,25 +102,30 @@ class ClockSampler:
 
 
 def algorithmic_bytes(X, R):
-    """Per-launch compulsory HBM bytes of each loop kernel.
-    CSR = 12 B/nnz + 8 B/row + 8 B/subject; per-subject packed C/S = 8 R(R+1)/2 B;
-    E = 8 R^2 B; W rows 8 R B; V 8 J R B (L2-resident, counted once)."""
+    """Per-launch compulsory HBM bytes of each loop phase, for
+    the kernels as designed.  CSR = 12 B/nnz + 8 B/row + 8 B/subject; CSC copy
+    = 12 B/nnz + 8 B/column; per-subject packed C/S = 8 R(R+1)/2 B; E = 8 R^2 B;
+    W rows 8 R B; U / Q rows 8 R B; V 8 J R B (L2-resident, counted once)."""
     K, J = X.K, X.J
     nnz, nr = X.nnz, X.n_rows
     nt = R * (R + 1) // 2
     csr = 12 * nnz + 8 * (nr + 1) + 8 * (K + 1)
+    csc = 12 * nnz + 8 * (J + 1)
     q = 8 * nr * R
     w = 8 * K * R
     v = 8 * J * R
+    gather_u = 8 * nnz * R  # M2 = X^T U: one U row per entry
     return {
         # small-R Q-free pipeline
-        "polar": 8 * K * (2 * nt + R + R * R),          # C, W in; S, E out
-        "mode2": csr + 8 * K * nt + w + v,              # CSR, S, W in (V L2); M2 out
+        "polar": 8 * K * (2 * nt + R),                  # C, W in; S out
+        "mode2": csr + 8 * K * nt + w + v + q + csc + gather_u,  # rows: CSR, S, W in, U out; CSC + U rows in
         "mode3": csr + 8 * K * nt + w + w + 8 * K * nt + 2 * v,  # CSR, S, W in; m3, next C out
         "update_w": 2 * w,                              # m3 in, W out (NNLS)
         "fit": 2 * w,                                   # W, m3 in (gram + cross)
-        # large-R (Q-based) pipeline
-        "procrustes": csr + q + w + v,                  # K1: CSR + V, W_k in; Q out
+        # large-R pipeline: Procrustes writes Q and E (warm start) ...
+        "procrustes": csr + q + w + v + 2 * 8 * K * R * R,
+        # ... mode 2 = Q in, U out, CSC + U rows in
+        "mode2_large": 2 * q + csc + gather_u,
         # SURVEY.md §8d north-star iteration bytes (Q-based formulation)
         "iteration": 3 * csr + 3 * q + 4 * w + 4 * v,
     }
@@ -287,7 +292,8 @@ def main():
     roofline = None
     if dom:
         t_launch = cand[dom][0] * 1e-3
-        achieved = ab[dom] / t_launch / 1e9
+        akey = "mode2_large" if (dom == "mode2" and R > 16) else dom
+        achieved = ab[akey] / t_launch / 1e9
         traffic = None
         tpath = os.path.join(ROOT, "profiles", "traffic_r01.json")
         if os.path.exists(tpath):
@@ -297,7 +303,7 @@ def main():
                 traffic = None
         roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
                     "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
-                    "algorithmic_bytes_per_launch": ab[dom], "ms_per_launch": cand[dom][0],
+                    "algorithmic_bytes_per_launch": ab[akey], "ms_per_launch": cand[dom][0],
                     "share_of_step": sum(v[0] * v[1] for k, v in ktimes.items() if k == dom) /
                                      max(sum(v[0] * v[1] for v in ktimes.values()), 1e-12)}
     iter_gbs = ab["iteration"] / (ms_step * 1e-3) / 1e9
