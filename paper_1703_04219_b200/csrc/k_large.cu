@@ -60,8 +60,8 @@ struct LgSmem {
   static constexpr int LDM = RP + 1;
   static constexpr int kMat = RP * LDM;
   // Hs, E, T (then Z), M, Vp, M1acc, work (E V' product)
-  static constexpr int kDoubles = 7 * kMat + 4 * RP + 8;
-  static constexpr int kInts = RP + 8;
+  static constexpr int kDoubles = 7 * kMat + 5 * RP + 8;
+  static constexpr int kInts = RP + 8 + (RP / 2) * (RP / 2 + 1) / 4 + 2;  // pairs + uint16 block table
 };
 
 __device__ __forceinline__ double block_sum(double v, double* red) {
@@ -75,11 +75,11 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
   return t;
 }
 
-template <int RP>
+template <int RP, bool EXACT>
 __global__ void __launch_bounds__(kLgThreads, 2) k_procrustes_large(LgArgs a) {
   extern __shared__ double smem[];
   const int tid = threadIdx.x;
-  const int R = a.R;
+  const int R = EXACT ? RP : a.R;  // exact-R instances fold the index arithmetic
   const int RR = R * R;
   constexpr int LDM = LgSmem<RP>::LDM;  // odd leading dimension: column walks are bank-conflict free
   constexpr int kMat = LgSmem<RP>::kMat;
@@ -93,9 +93,11 @@ __global__ void __launch_bounds__(kLgThreads, 2) k_procrustes_large(LgArgs a) {
   double* w = Wk + kMat;   // W_k (RP)
   double* sig = w + RP;    // sigma (RP)
   double* rc = sig + RP;   // rotation c (RP/2)
-  double* rs = rc + RP;    // rotation s (RP/2)
-  double* red = rs + RP;   // 4 warp partials + flags
+  double* rs = rc + RP;   // rotation s (RP/2)
+  double* rt = rs + RP;    // diagonal shift t M_pq (RP/2)
+  double* red = rt + RP;   // 4 warp partials + flags
   int* rp = reinterpret_cast<int*>(red + 8);  // rotation pairs (RP ints: p, q)
+  std::uint16_t* blk = reinterpret_cast<std::uint16_t*>(rp + RP);  // (i1 << 8 | i2), i1 <= i2 < RP/2
 
   for (int e = tid; e < RR; e += kLgThreads) {
     Hs[(e / R) * LDM + e % R] = a.H[e];
@@ -106,6 +108,15 @@ __global__ void __launch_bounds__(kLgThreads, 2) k_procrustes_large(LgArgs a) {
   double* Xs = Bs + a.max_rows * R;
   const int m = (R + 1) & ~1;  // players incl. one dummy for odd R
   const int half = m / 2;
+  const int nblk = half * (half + 1) / 2;
+  for (int it = tid; it < nblk; it += kLgThreads) {  // block-pair table, row-major upper triangle
+    int i1 = 0, r = it;
+    while (r >= half - i1) {
+      r -= half - i1;
+      ++i1;
+    }
+    blk[it] = static_cast<std::uint16_t>((i1 << 8) | (i1 + r));
+  }
 
   constexpr int NW = kLgThreads / 32;
   constexpr int NP = (RP + NW - 1) / NW;  // rows p of M owned by a warp in the M/F build
@@ -243,60 +254,86 @@ __global__ void __launch_bounds__(kLgThreads, 2) k_procrustes_large(LgArgs a) {
               p = q;
               q = t;
             }
-            double c = 1.0, s = 0.0;
+            double c = 1.0, s = 0.0, tt = 0.0, ga = 0.0;
             if (q < R) {
-              const double al = M[p * LDM + p], be = M[q * LDM + q], ga = M[p * LDM + q];
+              const double al = M[p * LDM + p], be = M[q * LDM + q];
+              ga = M[p * LDM + q];
               // one_sided_jacobi's rotation with (alpha, beta, gamma) = (M_pp, M_qq, M_pq);
               // skip tolerance 4e-15 instead of 1e-15: two-sided updates leave
               // O(eps) noise in the scaled off-diagonal.
               if (al > tiny && be > tiny && !(ga == 0.0 || fabs(ga) <= kTolL * sqrt(al * be))) {
                 const double zeta = (be - al) / (2.0 * ga);
-                const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-                c = 1.0 / sqrt(1.0 + t * t);
-                s = c * t;
+                tt = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+                c = 1.0 / sqrt(1.0 + tt * tt);
+                s = c * tt;
               }
             } else {
               q = -1;
             }
             rc[tid] = c;
             rs[tid] = s;
+            rt[tid] = tt * ga;  // diagonal shift t * M_pq
             rp[2 * tid] = p;
             rp[2 * tid + 1] = q;
           }
           __syncthreads();
-          // columns: M <- M J, V' <- V' J (warp per pair, lanes along the column)
-          for (int pr = wid; pr < half; pr += NW) {
-            const int p = rp[2 * pr], q = rp[2 * pr + 1];
-            const double s = rs[pr];
-            if (q < 0 || s == 0.0) continue;
-            const double c = rc[pr];
-            for (int kk = lane; kk < R; kk += 32) {
-              const double mp = M[kk * LDM + p], mq = M[kk * LDM + q];
-              M[kk * LDM + p] = c * mp - s * mq;
-              M[kk * LDM + q] = s * mp + c * mq;
-              const double vp = Vp[kk * LDM + p], vq = Vp[kk * LDM + q];
-              Vp[kk * LDM + p] = c * vp - s * vq;
-              Vp[kk * LDM + q] = s * vp + c * vq;
+          // M <- J^T M J, 2 x 2 block by 2 x 2 block: the round's rotations are
+          // disjoint, so block (pair i1, pair i2) only needs its own four entries
+          // (J_1^T X J_2); rotated diagonal blocks take the exact Jacobi update
+          // diag(M_pp - t M_pq, M_qq + t M_pq), off-diagonal 0.
+          for (int it = tid; it < nblk; it += kLgThreads) {
+            const int i1 = blk[it] >> 8, i2 = blk[it] & 0xff;
+            const int p1 = rp[2 * i1], q1 = rp[2 * i1 + 1], p2 = rp[2 * i2], q2 = rp[2 * i2 + 1];
+            const double s1 = rs[i1], s2 = rs[i2];
+            if (s1 == 0.0 && s2 == 0.0) continue;
+            if (q1 < 0 || q2 < 0) {
+              // odd R: the dummy pair's real index still sees the other pair's
+              // rotation (a 1 x 2 block); the dummy itself never rotates
+              if (q1 < 0 && q2 < 0) continue;
+              const int a = q1 < 0 ? p1 : p2;                 // index of the dummy pair
+              const int u = q1 < 0 ? p2 : p1, v = q1 < 0 ? q2 : q1;  // the rotating pair
+              const double cc = q1 < 0 ? rc[i2] : rc[i1], ss = q1 < 0 ? s2 : s1;
+              const double xu = M[a * LDM + u], xv = M[a * LDM + v];
+              const double nu = cc * xu - ss * xv, nv = ss * xu + cc * xv;
+              M[a * LDM + u] = nu;
+              M[u * LDM + a] = nu;
+              M[a * LDM + v] = nv;
+              M[v * LDM + a] = nv;
+              continue;
             }
+            if (i1 == i2) {
+              const double d = rt[i1];
+              M[p1 * LDM + p1] -= d;
+              M[q1 * LDM + q1] += d;
+              M[p1 * LDM + q1] = 0.0;
+              M[q1 * LDM + p1] = 0.0;
+              continue;
+            }
+            const double c1 = rc[i1], c2 = rc[i2];
+            const double x11 = M[p1 * LDM + p2], x12 = M[p1 * LDM + q2], x21 = M[q1 * LDM + p2], x22 = M[q1 * LDM + q2];
+            const double y11 = c2 * x11 - s2 * x12, y12 = s2 * x11 + c2 * x12;
+            const double y21 = c2 * x21 - s2 * x22, y22 = s2 * x21 + c2 * x22;
+            const double z11 = c1 * y11 - s1 * y21, z21 = s1 * y11 + c1 * y21;
+            const double z12 = c1 * y12 - s1 * y22, z22 = s1 * y12 + c1 * y22;
+            M[p1 * LDM + p2] = z11;
+            M[p2 * LDM + p1] = z11;
+            M[p1 * LDM + q2] = z12;
+            M[q2 * LDM + p1] = z12;
+            M[q1 * LDM + p2] = z21;
+            M[p2 * LDM + q1] = z21;
+            M[q1 * LDM + q2] = z22;
+            M[q2 * LDM + q1] = z22;
           }
-          __syncthreads();
-          // rows: M <- J^T M, then the annihilated pair set to zero
-          for (int pr = wid; pr < half; pr += NW) {
+          // V' <- V' J (columns p, q of each rotated pair)
+          for (int it = tid; it < half * R; it += kLgThreads) {
+            const int pr = it / R, kk = it - (it / R) * R;
             const int p = rp[2 * pr], q = rp[2 * pr + 1];
             const double s = rs[pr];
             if (q < 0 || s == 0.0) continue;
             const double c = rc[pr];
-            for (int kk = lane; kk < R; kk += 32) {
-              const double mp = M[p * LDM + kk], mq = M[q * LDM + kk];
-              M[p * LDM + kk] = c * mp - s * mq;
-              M[q * LDM + kk] = s * mp + c * mq;
-            }
-            __syncwarp();
-            if (lane == 0) {
-              M[p * LDM + q] = 0.0;
-              M[q * LDM + p] = 0.0;
-            }
-            __syncwarp();
+            const double vp = Vp[kk * LDM + p], vq = Vp[kk * LDM + q];
+            Vp[kk * LDM + p] = c * vp - s * vq;
+            Vp[kk * LDM + q] = s * vp + c * vq;
           }
           __syncthreads();
         }
@@ -337,13 +374,13 @@ __global__ void __launch_bounds__(kLgThreads, 2) k_procrustes_large(LgArgs a) {
       // (sigma_min^2 < 1e-6 sigma_max^2, the fast-path bound of the small-R
       // pipeline): redo with the fresh E, which makes B nearly orthogonal.
       if (pass == 0 && off > 0.25 && smin2 < 1e-6 * smax2) continue;
-      for (int j = tid; j < R; j += kLgThreads) sig[j] = sqrt(M[j * LDM + j]);
+      for (int j = tid; j < R; j += kLgThreads) sig[j] = 1.0 / sqrt(M[j * LDM + j]);  // 1 / sigma
       __syncthreads();
       // Z = V' Sigma^-1 V_A^T (so q_i = b_i Z), into T
       for (int i = wid; i < R; i += NW)
         for (int j = lane; j < R; j += 32) {
           double acc = 0.0;
-          for (int c = 0; c < R; ++c) acc = fma(Vp[i * LDM + c] / sig[c], E[j * LDM + c], acc);
+          for (int c = 0; c < R; ++c) acc = fma(Vp[i * LDM + c] * sig[c], E[j * LDM + c], acc);
           T[i * LDM + j] = acc;
         }
       __syncthreads();
@@ -381,10 +418,10 @@ __global__ void __launch_bounds__(kLgThreads, 2) k_procrustes_large(LgArgs a) {
     a.m1_partials[static_cast<std::int64_t>(blockIdx.x) * RR + e] = M1[(e / R) * LDM + e % R];
 }
 
-template <int RP>
+template <int RP, bool EXACT>
 int launch_large(p2g_ctx* c, LgArgs a, int max_blocks, cudaStream_t s) {
   const std::size_t smem = sizeof(double) * LgSmem<RP>::kDoubles + sizeof(int) * LgSmem<RP>::kInts;
-  auto kern = k_procrustes_large<RP>;
+  auto kern = k_procrustes_large<RP, EXACT>;
   P2G_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   int per_sm = 0;
   P2G_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kLgThreads, smem));
@@ -419,12 +456,18 @@ int launch_procrustes_large(p2g_ctx* c, int R, const double* H, const double* V,
   a.dbg = std::getenv("P2G_DEBUG") ? c->counters.get() + 4 : nullptr;
   if (a.X.K == 0) return 0;
   int blocks = 0;
-  if (R <= 24)
-    blocks = launch_large<24>(c, a, max_blocks, s);
+  if (R == 24)
+    blocks = launch_large<24, true>(c, a, max_blocks, s);
+  else if (R == 32)
+    blocks = launch_large<32, true>(c, a, max_blocks, s);
+  else if (R == 40)
+    blocks = launch_large<40, true>(c, a, max_blocks, s);
+  else if (R <= 24)
+    blocks = launch_large<24, false>(c, a, max_blocks, s);
   else if (R <= 32)
-    blocks = launch_large<32>(c, a, max_blocks, s);
+    blocks = launch_large<32, false>(c, a, max_blocks, s);
   else if (R <= 40)
-    blocks = launch_large<40>(c, a, max_blocks, s);
+    blocks = launch_large<40, false>(c, a, max_blocks, s);
   else
     throw InvalidArgument("rank above 40 unsupported");
   P2G_LAUNCHED(1);

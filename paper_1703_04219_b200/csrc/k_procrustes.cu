@@ -21,6 +21,9 @@
 // canonical rank-deficiency rule D5 (oracle/p2_oracle.hpp canonical_polar).
 #include <algorithm>
 
+#include <cub/device/device_select.cuh>
+#include <thrust/iterator/counting_iterator.h>
+
 #include "dev_common.cuh"
 #include "p2g_ctx.hpp"
 
@@ -43,6 +46,8 @@ struct K1Args {
   std::int64_t max_rows;
   std::int32_t* counters;  // [2] = non-finite operand seen
   const double* Ebuf;      // accurate path preconditioner (K x R x R) or null
+  const std::int32_t* list;   // accurate path: flagged subjects, ascending (device), or null
+  const std::int32_t* nlist;  // its length (device)
   double* Shat;            // Q-free outputs (K x R x R) or null: Q = A Shat + L Chat
   double* Chat;
 };
@@ -264,7 +269,15 @@ __global__ void __launch_bounds__(WPB * 32) k_procrustes_accurate(K1Args a, doub
   const std::int64_t nwarps = static_cast<std::int64_t>(gridDim.x) * WPB;
   double* A = a.scratch + gw * a.max_rows * R;  // I x R row-major
 
-  for (std::int64_t k = gw; k < a.X.K; k += nwarps) {
+  // Flagged subjects come as a compacted, ascending list; warp gw takes the
+  // contiguous share [gw L / W, (gw + 1) L / W): equal counts per warp and a
+  // schedule independent of timing (the m1 partials stay deterministic).
+  const std::int64_t L = a.list ? static_cast<std::int64_t>(*a.nlist) : a.X.K;
+  const std::int64_t it0 = a.list ? gw * L / nwarps : gw;
+  const std::int64_t it1 = a.list ? (gw + 1) * L / nwarps : a.X.K;
+  const std::int64_t istep = a.list ? 1 : nwarps;
+  for (std::int64_t it = it0; it < it1; it += istep) {
+    const std::int64_t k = a.list ? static_cast<std::int64_t>(a.list[it]) : it;
     if (a.flags[k] != P2G_FLAG_ACCURATE) continue;
     const std::int64_t r0 = a.X.srp[k];
     const int I = static_cast<int>(a.X.srp[k + 1] - r0);
@@ -642,6 +655,33 @@ int launch_k1(p2g_ctx* c, const K1Args& a, int max_blocks, cudaStream_t s) {
   return blocks;
 }
 
+__global__ void k_flag_bytes(std::int64_t K, const std::int32_t* __restrict__ flags, unsigned char* __restrict__ out) {
+  for (std::int64_t k = static_cast<std::int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; k < K;
+       k += static_cast<std::int64_t>(gridDim.x) * blockDim.x)
+    out[k] = flags[k] == P2G_FLAG_ACCURATE ? 1 : 0;
+}
+
+/// Ascending list of the subjects flagged for the accurate path (stable select).
+void compact_flagged(p2g_ctx* c, const std::int32_t* flags, cudaStream_t s) {
+  const std::int64_t K = c->k_end - c->k_begin;
+  c->acc_list.resize(static_cast<std::size_t>(std::max<std::int64_t>(K, 1)) + 1);
+  c->acc_bytes.resize(static_cast<std::size_t>(std::max<std::int64_t>(K, 1)));
+  std::int32_t* nsel = c->acc_list.get() + std::max<std::int64_t>(K, 1);
+  if (K == 0) {
+    P2G_CUDA(cudaMemsetAsync(nsel, 0, sizeof(std::int32_t), s));
+    return;
+  }
+  const int blocks = static_cast<int>(std::min<std::int64_t>((K + 255) / 256, 148 * 16));
+  k_flag_bytes<<<blocks, 256, 0, s>>>(K, flags, c->acc_bytes.get());
+  thrust::counting_iterator<std::int32_t> idx(0);
+  std::size_t tbytes = 0;
+  P2G_CUDA(cub::DeviceSelect::Flagged(nullptr, tbytes, idx, c->acc_bytes.get(), c->acc_list.get(), nsel,
+                                      static_cast<int>(K), s));
+  c->acc_temp.resize(tbytes);
+  P2G_CUDA(cub::DeviceSelect::Flagged(c->acc_temp.get(), tbytes, idx, c->acc_bytes.get(), c->acc_list.get(), nsel,
+                                      static_cast<int>(K), s));
+}
+
 template <int RP>
 constexpr int acc_wpb() {
   return RP <= 16 ? 4 : (RP <= 32 ? 2 : 1);
@@ -731,6 +771,10 @@ int launch_procrustes_accurate(p2g_ctx* c, int R, const double* H, const double*
   a.flags = flags;
   a.max_rows = c->max_rows;
   a.counters = c->counters.get();
+  compact_flagged(c, flags, s);
+  P2G_LAUNCHED(2);
+  a.list = c->acc_list.get();
+  a.nlist = c->acc_list.get() + std::max<std::int64_t>(c->k_end - c->k_begin, 1);
   int blocks = 0, wpb = 1;
   P2G_RP_DISPATCH(R, (blocks = acc_blocks<RP_>(c), wpb = acc_wpb<RP_>()));
   // Per-warp scratch slabs holding A (I_max x R) of the subject in flight.

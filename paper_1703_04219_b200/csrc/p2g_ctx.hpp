@@ -120,6 +120,8 @@ struct p2g_ctx {
   p2g::DBuf<std::int32_t> fb_list;    // compacted fallback subject ids
   p2g::DBuf<std::int32_t> counters;   // [0]=n_fallback, [1]=nnls error, ...
   p2g::DBuf<double> acc_scratch;      // accurate Procrustes path slabs
+  p2g::DBuf<std::int32_t> acc_list;   // flagged subjects (ascending) + count
+  p2g::DBuf<unsigned char> acc_bytes, acc_temp;
   p2g::DBuf<double> Cbuf, Sbuf, Ebuf; // small-R pipeline: per-subject packed C, S; E / Shat of flagged subjects
   p2g::DBuf<double> Chat;             // completion term of flagged subjects (K_s x R x R)
   p2g::DBuf<double> Ewarm;            // per-subject Jacobi eigenvectors (warm start / preconditioner)
