@@ -84,8 +84,11 @@ __global__ void k_reduce_partials(const double* __restrict__ partials, int npart
 // ---------------------------------------------------------------------------
 template <int RP>
 struct NnlsSmem {
-  // L, PA, PE, PO (RP*RP each) + b, x, w, s, sp (RP each) + cs (RP+2) ; ints: pset RP, pq RP+2
-  static constexpr int kDoubles = 4 * RP * RP + 5 * RP + RP + 2;
+  // L (RP*RP) + b, x, w, s, sp (RP each) + cs (RP+2) ; ints: pset RP, pq RP+2.
+  // The pseudo-inverse fallback's three RP*RP work matrices live in a global
+  // per-warp slab (rarely touched, L1/L2): keeping them in shared memory
+  // capped the kernel at 4 warps per SM at R = 40.
+  static constexpr int kDoubles = RP * RP + 5 * RP + RP + 2;
   static constexpr int kInts = 2 * RP + 2;
 };
 
@@ -93,16 +96,16 @@ template <int RP, int WPB>
 __global__ void __launch_bounds__(WPB * 32)
     k_nnls(int R, std::int64_t n, const double* __restrict__ G, const double* __restrict__ B, double* __restrict__ X,
            int cap, std::int32_t* err, const std::int32_t* __restrict__ rowlist, const std::int32_t* __restrict__ nlist,
-           unsigned long long* __restrict__ masks, int warm) {
+           unsigned long long* __restrict__ masks, int warm, double* __restrict__ pinv_slab) {
   extern __shared__ double smem[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   double* Gs = smem;
   double* base = Gs + RP * RP + wid * (NnlsSmem<RP>::kDoubles + (NnlsSmem<RP>::kInts + 1) / 2);
   double* L = base;
-  double* PA = L + RP * RP;
+  double* PA = pinv_slab + (static_cast<std::int64_t>(blockIdx.x) * WPB + wid) * 3 * RP * RP;
   double* PE = PA + RP * RP;
   double* PO = PE + RP * RP;
-  double* b = PO + RP * RP;
+  double* b = L + RP * RP;
   double* x = b + RP;
   double* w = x + RP;
   double* sv = w + RP;
@@ -463,8 +466,12 @@ void nnls_launch(int R, std::int64_t n, const double* G, const double* B, double
   auto kern = k_nnls<RP, WPB>;
   P2G_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   const std::int64_t want = (n + WPB - 1) / WPB;
-  const int blocks = static_cast<int>(std::max<std::int64_t>(1, std::min<std::int64_t>(want, 148 * 8)));
-  kern<<<blocks, WPB * 32, smem, s>>>(R, n, G, B, X, cap, err, rowlist, nlist, masks, warm);
+  const int blocks = static_cast<int>(std::max<std::int64_t>(1, std::min<std::int64_t>(want, 148 * 16)));
+  // pinv fallback workspace: one process drives one device, so a
+  // process-wide slab grown on demand is enough
+  static DBuf<double> slab;
+  slab.resize(static_cast<std::size_t>(blocks) * WPB * 3 * RP * RP);
+  kern<<<blocks, WPB * 32, smem, s>>>(R, n, G, B, X, cap, err, rowlist, nlist, masks, warm, slab.get());
 }
 
 template <int RP>

@@ -15,12 +15,16 @@
 namespace p2g {
 namespace {
 
+/// Leading dimension of staged rows: odd, so 32 lanes reading their own rows
+/// hit distinct banks (an even stride such as 40 is a 16-way conflict).
+template <int RP>
+constexpr int CLD = RP | 1;
+
 template <int RP>
 __device__ __forceinline__ void stage_rows(double* chunk, const double* __restrict__ src, int nr, int R, int lane) {
-  for (int idx = lane; idx < nr * R; idx += 32) {
-    const int row = idx / R;
-    chunk[row * RP + (idx - row * R)] = __ldg(src + idx);
-  }
+  // rows at the odd stride CLD<RP> (conflict-free when lanes walk their own row)
+  for (int row = 0; row < nr; ++row)
+    for (int c = lane; c < R; c += 32) chunk[row * CLD<RP> + c] = __ldg(src + row * R + c);
   __syncwarp();
 }
 
@@ -33,7 +37,7 @@ __global__ void __launch_bounds__(WPB * 32)
     k_mode2(ShardArgs X, int R, const double* __restrict__ Q, const double* __restrict__ H,
             const double* __restrict__ W, const double* __restrict__ nH, double* __restrict__ M2) {
   __shared__ double HWs[WPB][RP * RP];
-  __shared__ double chunk[WPB][32 * RP];
+  __shared__ double chunk[WPB][32 * CLD<RP>];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   double* HW = HWs[wid];
   double* ch = chunk[wid];
@@ -58,7 +62,7 @@ __global__ void __launch_bounds__(WPB * 32)
           if (c < R) {
 #pragma unroll
             for (int a = 0; a < RP; ++a)
-              if (a < R) acc = fma(ch[lane * RP + a], HW[a * R + c], acc);
+              if (a < R) acc = fma(ch[lane * CLD<RP> + a], HW[a * R + c], acc);
           }
           u[c] = acc;
         }
@@ -99,7 +103,7 @@ __global__ void __launch_bounds__(512)
   const int cg = min(rg, R - c0);  // columns of this group
   const std::int64_t J = X.J;
   double* acc = sm;                               // J * rg
-  double* HW = acc + J * rg + wid * (RP * RP + 32 * RP);
+  double* HW = acc + J * rg + wid * (RP * RP + 32 * CLD<RP>);
   double* ch = HW + RP * RP;
   for (std::int64_t e = threadIdx.x; e < J * rg; e += blockDim.x) acc[e] = 0.0;
   __syncthreads();
@@ -123,7 +127,7 @@ __global__ void __launch_bounds__(512)
           if (c < cg) {
 #pragma unroll
             for (int a = 0; a < RP; ++a)
-              if (a < R) s = fma(ch[lane * RP + a], HW[a * cg + c], s);
+              if (a < R) s = fma(ch[lane * CLD<RP> + a], HW[a * cg + c], s);
           }
           u[c] = s;
         }
@@ -157,7 +161,7 @@ __global__ void __launch_bounds__(WPB * 32)
     k_mode3(ShardArgs X, int R, const double* __restrict__ Q, const double* __restrict__ H,
             const double* __restrict__ V, double* __restrict__ M3) {
   __shared__ double Hs[RP * RP];
-  __shared__ double chunk[WPB][32 * RP];
+  __shared__ double chunk[WPB][32 * CLD<RP>];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   for (int e = threadIdx.x; e < R * R; e += blockDim.x) Hs[e] = H[e];
   __syncthreads();
@@ -181,7 +185,7 @@ __global__ void __launch_bounds__(WPB * 32)
             double qh = 0.0;
 #pragma unroll
             for (int a = 0; a < RP; ++a)
-              if (a < R) qh = fma(ch[lane * RP + a], Hs[a * R + c], qh);
+              if (a < R) qh = fma(ch[lane * CLD<RP> + a], Hs[a * R + c], qh);
             part[c] = fma(qh, xv[c], part[c]);
           }
         }
@@ -199,6 +203,81 @@ __global__ void __launch_bounds__(WPB * 32)
 }
 
 // ---------------------------------------------------------------------------
+// mode 3 for R > 16: lane per output column (c = lane, lane + 32).  The row
+// loop keeps no R-vector per thread (the row-per-lane form spills ~6 KB per
+// thread at R = 40, which ncu shows as 48 GB of local-memory DRAM traffic
+// per 100K subjects): q_i is staged in shared memory and read as a
+// broadcast, H columns are read at stride 1 across lanes, and the V-row
+// gather is coalesced across lanes.  Two rows are in flight per iteration.
+// ---------------------------------------------------------------------------
+template <int WPB>
+__global__ void __launch_bounds__(WPB * 32)
+    k_mode3_cols(ShardArgs X, int R, const double* __restrict__ Q, const double* __restrict__ H,
+                 const double* __restrict__ V, double* __restrict__ M3) {
+  constexpr int kMaxR = 64;
+  __shared__ double Hs[kMaxR * kMaxR];
+  __shared__ double qs[WPB][2][kMaxR];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int e = threadIdx.x; e < R * R; e += blockDim.x) Hs[e] = H[e];
+  __syncthreads();
+  const int c0 = lane, c1 = lane + 32;
+  const bool ok0 = c0 < R, ok1 = c1 < R;
+  const std::int64_t nwarps = static_cast<std::int64_t>(gridDim.x) * WPB;
+  for (std::int64_t k = static_cast<std::int64_t>(blockIdx.x) * WPB + wid; k < X.K; k += nwarps) {
+    const std::int64_t r0 = X.srp[k], r1 = X.srp[k + 1];
+    double part0 = 0.0, part1 = 0.0;
+    for (std::int64_t i = r0; i < r1; i += 2) {
+      const bool two = i + 1 < r1;
+      // stage q rows i, i + 1
+      for (int a = lane; a < R; a += 32) {
+        qs[wid][0][a] = Q[i * R + a];
+        qs[wid][1][a] = two ? Q[(i + 1) * R + a] : 0.0;
+      }
+      // X rows i, i + 1 times V, my columns
+      double x00 = 0.0, x01 = 0.0, x10 = 0.0, x11 = 0.0;
+      const std::int64_t pa0 = X.rp[i], pa1 = X.rp[i + 1];
+      const std::int64_t pb1 = two ? X.rp[i + 2] : pa1;
+      std::int64_t pa = pa0, pb = pa1;
+      while (pa < pa1 || pb < pb1) {
+        if (pa < pa1) {
+          const int j = __ldg(X.ci + pa);
+          const double v = __ldg(X.val + pa);
+          const double* vr = V + static_cast<std::int64_t>(j) * R;
+          if (ok0) x00 = fma(v, __ldg(vr + c0), x00);
+          if (ok1) x01 = fma(v, __ldg(vr + c1), x01);
+          ++pa;
+        }
+        if (pb < pb1) {
+          const int j = __ldg(X.ci + pb);
+          const double v = __ldg(X.val + pb);
+          const double* vr = V + static_cast<std::int64_t>(j) * R;
+          if (ok0) x10 = fma(v, __ldg(vr + c0), x10);
+          if (ok1) x11 = fma(v, __ldg(vr + c1), x11);
+          ++pb;
+        }
+      }
+      __syncwarp();
+      double h00 = 0.0, h01 = 0.0, h10 = 0.0, h11 = 0.0;  // (q_i H)_c
+      for (int a = 0; a < R; ++a) {
+        const double qa = qs[wid][0][a], qb = qs[wid][1][a];
+        const double ha0 = ok0 ? Hs[a * R + c0] : 0.0, ha1 = ok1 ? Hs[a * R + c1] : 0.0;
+        h00 = fma(qa, ha0, h00);
+        h01 = fma(qa, ha1, h01);
+        h10 = fma(qb, ha0, h10);
+        h11 = fma(qb, ha1, h11);
+      }
+      part0 = fma(h00, x00, part0);
+      part1 = fma(h01, x01, part1);
+      part0 = fma(h10, x10, part0);
+      part1 = fma(h11, x11, part1);
+      __syncwarp();
+    }
+    if (ok0) M3[k * R + c0] = part0;
+    if (ok1) M3[k * R + c1] = part1;
+  }
+}
+
+// ---------------------------------------------------------------------------
 // mode 1 from a given Q (the p2g_mttkrp_q hook; the fused loop gets M1 from
 // K1): m1 += Q_k^T (XV o W_k) through 32-row chunks.
 // ---------------------------------------------------------------------------
@@ -206,8 +285,8 @@ template <int RP, int WPB>
 __global__ void __launch_bounds__(WPB * 32)
     k_mode1_q(ShardArgs X, int R, const double* __restrict__ Q, const double* __restrict__ V,
               const double* __restrict__ W, double* __restrict__ partials) {
-  __shared__ double qch[WPB][32 * RP];
-  __shared__ double xch[WPB][32 * RP];
+  __shared__ double qch[WPB][32 * CLD<RP>];
+  __shared__ double xch[WPB][32 * CLD<RP>];
   __shared__ double acc_s[WPB][RP * RP];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int RR = R * R;
@@ -225,13 +304,13 @@ __global__ void __launch_bounds__(WPB * 32)
         dev::csr_row_times<RP>(xv, X.ci, X.val, X.rp[r0 + b0 + lane], X.rp[r0 + b0 + lane + 1], V, R);
 #pragma unroll
         for (int c = 0; c < RP; ++c)
-          if (c < R) xch[wid][lane * RP + c] = xv[c] * W[k * R + c];
+          if (c < R) xch[wid][lane * CLD<RP> + c] = xv[c] * W[k * R + c];
       }
       __syncwarp();
       for (int e = lane; e < RR; e += 32) {
         const int x = e / R, y = e - (e / R) * R;
         double acc = acc_s[wid][e];
-        for (int rr = 0; rr < nr; ++rr) acc = fma(qch[wid][rr * RP + x], xch[wid][rr * RP + y], acc);
+        for (int rr = 0; rr < nr; ++rr) acc = fma(qch[wid][rr * CLD<RP> + x], xch[wid][rr * CLD<RP> + y], acc);
         acc_s[wid][e] = acc;
       }
       __syncwarp();
@@ -457,7 +536,7 @@ void launch_mode2(p2g_ctx* c, int R, const double* Q, const double* H, const dou
   }
   P2G_CUDA(cudaMemsetAsync(M2, 0, sizeof(double) * c->J * R, s));
   P2G_RP_DISPATCH2(R, ({
-                     constexpr int WPB = fit_wpb(RP_ * RP_ + 32 * RP_, 0);
+                     constexpr int WPB = fit_wpb(RP_ * RP_ + 32 * CLD<RP_>, 0);
                      k_mode2<RP_, WPB><<<grid_for(X.K, WPB, c->num_sms), WPB * 32, 0, s>>>(X, R, Q, H, W, nH, M2);
                    }));
   P2G_LAUNCHED(1);
@@ -466,8 +545,14 @@ void launch_mode2(p2g_ctx* c, int R, const double* Q, const double* H, const dou
 void launch_mode3(p2g_ctx* c, int R, const double* Q, const double* H, const double* V, double* m3,
                   cudaStream_t s) {
   const ShardArgs X = shard_args(c);
+  if (R > 16) {  // the row-per-lane form spills above R = 16
+    constexpr int WPB = 4;  // Hs 32 KB + 4 KB q staging
+    k_mode3_cols<WPB><<<grid_for(X.K, WPB, c->num_sms, 12), WPB * 32, 0, s>>>(X, R, Q, H, V, m3);
+    P2G_LAUNCHED(1);
+    return;
+  }
   P2G_RP_DISPATCH2(R, ({
-                     constexpr int WPB = fit_wpb(32 * RP_, RP_ * RP_);
+                     constexpr int WPB = fit_wpb(32 * CLD<RP_>, RP_ * RP_);
                      k_mode3<RP_, WPB><<<grid_for(X.K, WPB, c->num_sms), WPB * 32, 0, s>>>(X, R, Q, H, V, m3);
                    }));
   P2G_LAUNCHED(1);
@@ -477,7 +562,7 @@ void launch_mode1_q(p2g_ctx* c, int R, const double* Q, const double* V, const d
                     int nblocks, cudaStream_t s) {
   const ShardArgs X = shard_args(c);
   P2G_RP_DISPATCH2(R, ({
-                     constexpr int WPB = fit_wpb(64 * RP_ + RP_ * RP_, 0);
+                     constexpr int WPB = fit_wpb(64 * CLD<RP_> + RP_ * RP_, 0);
                      k_mode1_q<RP_, WPB><<<nblocks, WPB * 32, 0, s>>>(X, R, Q, V, W, partials);
                    }));
   P2G_LAUNCHED(1);
