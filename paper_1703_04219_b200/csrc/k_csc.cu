@@ -5,16 +5,23 @@
 // reductions costs one L2 request per (entry, column) pair: 630M requests per
 // iteration at cfg2, where ncu shows L1/L2 at 77%/64% of their request
 // throughput (profiles/).  Instead, each row's u_i is written once (the
-// streaming kernels produce it coalesced), and M2 is read out column by
-// column from a CSC copy of the shard built at load time:
+// streaming kernels produce it coalesced), and M2 is read out from a
+// column-major copy of the shard built at load time:
 //   M2[j, :] = sum_{(i, v) in column j} v * U[i, :]
-// Columns are cut into segments of at most kSeg entries (hot Zipf columns of
-// cfg5 stay balanced); one CTA sums a segment, and a second pass adds a
-// column's segment partials in order: deterministic, no atomics.
+// The copy is ordered by (row block, column), row blocks of 2^17 rows: the
+// segments in flight share one or two row blocks of U (10 MB at R = 10,
+// 42 MB at R = 40), so the random U-row gathers hit L2 instead of DRAM.
+// A segment is a run of one (row block, column) cut at kSeg entries (Zipf
+// columns of cfg5 stay balanced); one thread sums a segment, and a second
+// pass adds each column's segment partials in row-block order:
+// deterministic, no atomics.
 #include <algorithm>
 #include <vector>
 
 #include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+#include <cub/device/device_select.cuh>
+#include <thrust/iterator/counting_iterator.h>
 
 #include "dev_common.cuh"
 #include "p2g_ctx.hpp"
@@ -22,8 +29,8 @@
 namespace p2g {
 namespace {
 
-constexpr std::int64_t kSeg = 4096;
-constexpr int kSpThreads = 128;
+constexpr std::int64_t kSeg = 256;  // entries per segment (one thread)
+constexpr int kRowBlockBits = 17;   // row blocks of 2^17 rows
 
 __global__ void k_row_expand(std::int64_t NR, const std::int64_t* __restrict__ rp, std::int32_t* __restrict__ row_of) {
   for (std::int64_t r = static_cast<std::int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; r < NR;
@@ -47,20 +54,55 @@ __global__ void k_csc_gather(std::int64_t n, const std::int32_t* __restrict__ pe
   }
 }
 
-/// col_ptr[j] = first position of key >= j in the sorted keys (binary search).
-__global__ void k_col_ptr(std::int64_t J, std::int64_t n, const std::int32_t* __restrict__ keys,
-                          std::int64_t* __restrict__ col_ptr) {
+__global__ void k_block_keys(std::int64_t n, std::int64_t J, const std::int32_t* __restrict__ row_of,
+                             const std::int32_t* __restrict__ ci, std::uint64_t* __restrict__ keys) {
+  for (std::int64_t p = static_cast<std::int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; p < n;
+       p += static_cast<std::int64_t>(gridDim.x) * blockDim.x)
+    keys[p] = static_cast<std::uint64_t>(row_of[p] >> kRowBlockBits) * static_cast<std::uint64_t>(J) +
+              static_cast<std::uint64_t>(ci[p]);
+}
+
+/// run_start[q] candidates: q where the (block, column) key changes, else 0 (max-scanned).
+__global__ void k_run_marks(std::int64_t n, const std::uint64_t* __restrict__ keys, std::int64_t* __restrict__ mark) {
+  for (std::int64_t q = static_cast<std::int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; q < n;
+       q += static_cast<std::int64_t>(gridDim.x) * blockDim.x)
+    mark[q] = (q == 0 || keys[q] != keys[q - 1]) ? q : 0;
+}
+
+/// Segment heads: a new run, or every kSeg entries inside a run.
+__global__ void k_seg_heads(std::int64_t n, const std::int64_t* __restrict__ run_start, unsigned char* __restrict__ head) {
+  for (std::int64_t q = static_cast<std::int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; q < n;
+       q += static_cast<std::int64_t>(gridDim.x) * blockDim.x)
+    head[q] = ((q - run_start[q]) % kSeg) == 0 ? 1 : 0;
+}
+
+/// Per segment: column-major key col * nblk + block (for the per-column lists).
+__global__ void k_seg_colkeys(std::int64_t nseg, std::int64_t J, std::int64_t nblk, const std::int64_t* __restrict__ seg_beg,
+                              const std::uint64_t* __restrict__ keys, std::uint64_t* __restrict__ ckey,
+                              std::int32_t* __restrict__ ids) {
+  for (std::int64_t s = static_cast<std::int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; s < nseg;
+       s += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
+    const std::uint64_t k = keys[seg_beg[s]];
+    const std::uint64_t blk = k / static_cast<std::uint64_t>(J), col = k - blk * static_cast<std::uint64_t>(J);
+    ckey[s] = col * static_cast<std::uint64_t>(nblk) + blk;
+    ids[s] = static_cast<std::int32_t>(s);
+  }
+}
+
+/// ptr[j] = first position whose key / nblk >= j (binary search over sorted keys).
+__global__ void k_key_ptr(std::int64_t J, std::int64_t n, std::int64_t div, const std::uint64_t* __restrict__ keys,
+                          std::int64_t* __restrict__ ptr) {
   for (std::int64_t j = static_cast<std::int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; j <= J;
        j += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
     std::int64_t lo = 0, hi = n;
     while (lo < hi) {
       const std::int64_t mid = (lo + hi) >> 1;
-      if (keys[mid] < j)
+      if (static_cast<std::int64_t>(keys[mid] / static_cast<std::uint64_t>(div)) < j)
         lo = mid + 1;
       else
         hi = mid;
     }
-    col_ptr[j] = lo;
+    ptr[j] = lo;
   }
 }
 
@@ -68,21 +110,21 @@ int grid_for(std::int64_t n, int threads) {
   return static_cast<int>(std::max<std::int64_t>(1, std::min<std::int64_t>((n + threads - 1) / threads, 148 * 32)));
 }
 
-/// One CTA per segment: partial[s, :] = sum over the segment's entries of v * U[row, :].
+/// Thread per segment: partial[s, :] = sum over the segment's entries of v * U[row, :].
+/// Consecutive threads hold consecutive segments of the same row block.
 template <int RP>
-__global__ void __launch_bounds__(kSpThreads) k_seg_spmm(int R, std::int64_t nseg, const std::int64_t* __restrict__ seg_beg,
-                                                         const std::int64_t* __restrict__ seg_end,
-                                                         const std::int32_t* __restrict__ crow,
-                                                         const double* __restrict__ cval, const double* __restrict__ U,
-                                                         double* __restrict__ partial) {
-  extern __shared__ double red[];  // kSpThreads x (RP + 1)
-  const int tid = threadIdx.x;
-  for (std::int64_t s = blockIdx.x; s < nseg; s += gridDim.x) {
+__global__ void __launch_bounds__(128) k_seg_spmm(int R, std::int64_t nseg, std::int64_t n,
+                                                  const std::int64_t* __restrict__ seg_beg,
+                                                  const std::int32_t* __restrict__ crow,
+                                                  const double* __restrict__ cval, const double* __restrict__ U,
+                                                  double* __restrict__ partial) {
+  for (std::int64_t s = static_cast<std::int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; s < nseg;
+       s += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
     double acc[RP];
 #pragma unroll
     for (int c = 0; c < RP; ++c) acc[c] = 0.0;
-    const std::int64_t q1 = seg_end[s];
-    for (std::int64_t q = seg_beg[s] + tid; q < q1; q += kSpThreads) {
+    const std::int64_t q1 = s + 1 < nseg ? seg_beg[s + 1] : n;
+    for (std::int64_t q = seg_beg[s]; q < q1; ++q) {
       const double v = cval[q];
       const double* u = U + static_cast<std::int64_t>(crow[q]) * R;
       if constexpr (RP % 2 == 0) {
@@ -101,27 +143,23 @@ __global__ void __launch_bounds__(kSpThreads) k_seg_spmm(int R, std::int64_t nse
       for (int c = 0; c < RP; ++c)
         if (c < R) acc[c] = fma(v, __ldg(u + c), acc[c]);
     }
+    double* out = partial + s * R;
 #pragma unroll
-    for (int c = 0; c < RP; ++c) red[tid * (RP + 1) + c] = acc[c];
-    __syncthreads();
-    for (int c = tid; c < R; c += kSpThreads) {
-      double t = 0.0;
-      for (int i = 0; i < kSpThreads; ++i) t += red[i * (RP + 1) + c];
-      partial[s * R + c] = t;
-    }
-    __syncthreads();
+    for (int c = 0; c < RP; ++c)
+      if (c < R) out[c] = acc[c];
   }
 }
 
-/// M2[j, c] = sum of column j's segment partials, in segment order.
+/// M2[j, c] = sum of column j's segment partials, in row-block order.
 __global__ void k_seg_reduce(int R, std::int64_t J, const std::int64_t* __restrict__ seg_ptr,
-                             const double* __restrict__ partial, double* __restrict__ M2) {
+                             const std::int32_t* __restrict__ seg_ids, const double* __restrict__ partial,
+                             double* __restrict__ M2) {
   for (std::int64_t e = static_cast<std::int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < J * R;
        e += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
     const std::int64_t j = e / R;
     const int c = static_cast<int>(e - j * R);
     double t = 0.0;
-    for (std::int64_t s = seg_ptr[j]; s < seg_ptr[j + 1]; ++s) t += partial[s * R + c];
+    for (std::int64_t q = seg_ptr[j]; q < seg_ptr[j + 1]; ++q) t += partial[static_cast<std::int64_t>(seg_ids[q]) * R + c];
     M2[e] = t;
   }
 }
@@ -161,66 +199,90 @@ __global__ void __launch_bounds__(WPB * 32)
 void build_csc(p2g_ctx* c) {
   cudaStream_t s = c->stream;
   const std::int64_t n = c->nnz, J = c->J;
-  c->col_ptr.resize(static_cast<std::size_t>(J + 1));
-  c->csc_row.resize(static_cast<std::size_t>(std::max<std::int64_t>(n, 1)));
-  c->csc_val.resize(static_cast<std::size_t>(std::max<std::int64_t>(n, 1)));
   if (n > static_cast<std::int64_t>(0x7fffffff) || c->NR > static_cast<std::int64_t>(0x7fffffff))
     throw InvalidArgument("shard too large for 32-bit CSC indices");
-  std::vector<std::int64_t> cp(static_cast<std::size_t>(J + 1), 0);
-  if (n > 0) {
-    DBuf<std::int32_t> row_of, keys, iota, perm;
-    row_of.resize(static_cast<std::size_t>(n));
-    keys.resize(static_cast<std::size_t>(n));
-    iota.resize(static_cast<std::size_t>(n));
-    perm.resize(static_cast<std::size_t>(n));
-    k_row_expand<<<grid_for(c->NR, 256), 256, 0, s>>>(c->NR, c->rp.get(), row_of.get());
-    k_iota<<<grid_for(n, 256), 256, 0, s>>>(n, iota.get());
-    int bits = 1;
-    while ((std::int64_t{1} << bits) < J) ++bits;
-    std::size_t tbytes = 0;
-    P2G_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tbytes, c->ci.get(), keys.get(), iota.get(), perm.get(),
-                                             static_cast<int>(n), 0, bits, s));
-    DBuf<unsigned char> temp;
-    temp.resize(tbytes);
-    // LSD radix sort: stable, so entries of a column keep CSR (row-ascending) order
-    P2G_CUDA(cub::DeviceRadixSort::SortPairs(temp.get(), tbytes, c->ci.get(), keys.get(), iota.get(), perm.get(),
-                                             static_cast<int>(n), 0, bits, s));
-    k_csc_gather<<<grid_for(n, 256), 256, 0, s>>>(n, perm.get(), row_of.get(), c->val.get(), c->csc_row.get(),
-                                                  c->csc_val.get());
-    k_col_ptr<<<grid_for(J + 1, 256), 256, 0, s>>>(J, n, keys.get(), c->col_ptr.get());
-    P2G_CUDA(cudaMemcpyAsync(cp.data(), c->col_ptr.get(), sizeof(std::int64_t) * (J + 1), cudaMemcpyDeviceToHost, s));
+  const std::int64_t nblk = (c->NR >> kRowBlockBits) + 1;
+  c->csc_row.resize(static_cast<std::size_t>(std::max<std::int64_t>(n, 1)));
+  c->csc_val.resize(static_cast<std::size_t>(std::max<std::int64_t>(n, 1)));
+  c->seg_ptr.resize(static_cast<std::size_t>(J + 1));
+  c->nseg = 0;
+  if (n == 0) {
+    P2G_CUDA(cudaMemsetAsync(c->seg_ptr.get(), 0, sizeof(std::int64_t) * (J + 1), s));
     P2G_CUDA(cudaStreamSynchronize(s));
+    return;
   }
-  // segment table (host; J entries)
-  std::vector<std::int64_t> sp(static_cast<std::size_t>(J + 1), 0), sb, se;
-  for (std::int64_t j = 0; j < J; ++j) {
-    const std::int64_t a = cp[static_cast<std::size_t>(j)], b = cp[static_cast<std::size_t>(j + 1)];
-    for (std::int64_t q = a; q < b; q += kSeg) {
-      sb.push_back(q);
-      se.push_back(std::min(b, q + kSeg));
-    }
-    sp[static_cast<std::size_t>(j + 1)] = static_cast<std::int64_t>(sb.size());
-  }
-  c->nseg = static_cast<std::int64_t>(sb.size());
-  c->seg_ptr.resize(sp.size());
-  c->seg_beg.resize(std::max<std::size_t>(sb.size(), 1));
-  c->seg_end.resize(std::max<std::size_t>(se.size(), 1));
-  P2G_CUDA(cudaMemcpyAsync(c->seg_ptr.get(), sp.data(), sizeof(std::int64_t) * sp.size(), cudaMemcpyHostToDevice, s));
-  if (!sb.empty()) {
-    P2G_CUDA(cudaMemcpyAsync(c->seg_beg.get(), sb.data(), sizeof(std::int64_t) * sb.size(), cudaMemcpyHostToDevice, s));
-    P2G_CUDA(cudaMemcpyAsync(c->seg_end.get(), se.data(), sizeof(std::int64_t) * se.size(), cudaMemcpyHostToDevice, s));
-  }
+  DBuf<std::int32_t> row_of, iota, perm;
+  DBuf<std::uint64_t> keys, skeys;
+  row_of.resize(static_cast<std::size_t>(n));
+  iota.resize(static_cast<std::size_t>(n));
+  perm.resize(static_cast<std::size_t>(n));
+  keys.resize(static_cast<std::size_t>(n));
+  skeys.resize(static_cast<std::size_t>(n));
+  k_row_expand<<<grid_for(c->NR, 256), 256, 0, s>>>(c->NR, c->rp.get(), row_of.get());
+  k_iota<<<grid_for(n, 256), 256, 0, s>>>(n, iota.get());
+  k_block_keys<<<grid_for(n, 256), 256, 0, s>>>(n, J, row_of.get(), c->ci.get(), keys.get());
+  int bits = 1;
+  while ((std::uint64_t{1} << bits) < static_cast<std::uint64_t>(nblk * J)) ++bits;
+  DBuf<unsigned char> temp;
+  std::size_t tbytes = 0;
+  P2G_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tbytes, keys.get(), skeys.get(), iota.get(), perm.get(),
+                                           static_cast<int>(n), 0, bits, s));
+  temp.resize(tbytes);
+  // LSD radix sort: stable, so a (row block, column) run keeps CSR (row-ascending) order
+  P2G_CUDA(cub::DeviceRadixSort::SortPairs(temp.get(), tbytes, keys.get(), skeys.get(), iota.get(), perm.get(),
+                                           static_cast<int>(n), 0, bits, s));
+  k_csc_gather<<<grid_for(n, 256), 256, 0, s>>>(n, perm.get(), row_of.get(), c->val.get(), c->csc_row.get(),
+                                                c->csc_val.get());
+  // segment heads: run starts (max-scan of change positions), split every kSeg
+  DBuf<std::int64_t> mark, runstart;
+  mark.resize(static_cast<std::size_t>(n));
+  runstart.resize(static_cast<std::size_t>(n));
+  k_run_marks<<<grid_for(n, 256), 256, 0, s>>>(n, skeys.get(), mark.get());
+  tbytes = 0;
+  P2G_CUDA(cub::DeviceScan::InclusiveScan(nullptr, tbytes, mark.get(), runstart.get(), cub::Max(), static_cast<int>(n), s));
+  temp.resize(tbytes);
+  P2G_CUDA(cub::DeviceScan::InclusiveScan(temp.get(), tbytes, mark.get(), runstart.get(), cub::Max(), static_cast<int>(n), s));
+  DBuf<unsigned char> head;
+  head.resize(static_cast<std::size_t>(n));
+  k_seg_heads<<<grid_for(n, 256), 256, 0, s>>>(n, runstart.get(), head.get());
+  c->seg_beg.resize(static_cast<std::size_t>(n));
+  DBuf<std::int64_t> nsel;
+  nsel.resize(1);
+  thrust::counting_iterator<std::int64_t> idx(0);
+  tbytes = 0;
+  P2G_CUDA(cub::DeviceSelect::Flagged(nullptr, tbytes, idx, head.get(), c->seg_beg.get(), nsel.get(),
+                                      static_cast<int>(n), s));
+  temp.resize(tbytes);
+  P2G_CUDA(cub::DeviceSelect::Flagged(temp.get(), tbytes, idx, head.get(), c->seg_beg.get(), nsel.get(),
+                                      static_cast<int>(n), s));
+  std::int64_t nseg = 0;
+  P2G_CUDA(cudaMemcpyAsync(&nseg, nsel.get(), sizeof(std::int64_t), cudaMemcpyDeviceToHost, s));
+  P2G_CUDA(cudaStreamSynchronize(s));
+  c->nseg = nseg;
+  // per-column segment lists in row-block order: sort segment ids by col * nblk + block
+  DBuf<std::uint64_t> ck, sck;
+  DBuf<std::int32_t> ids;
+  ck.resize(static_cast<std::size_t>(nseg));
+  sck.resize(static_cast<std::size_t>(nseg));
+  ids.resize(static_cast<std::size_t>(nseg));
+  c->seg_ids.resize(static_cast<std::size_t>(nseg));
+  k_seg_colkeys<<<grid_for(nseg, 256), 256, 0, s>>>(nseg, J, nblk, c->seg_beg.get(), skeys.get(), ck.get(), ids.get());
+  int cbits = 1;
+  while ((std::uint64_t{1} << cbits) < static_cast<std::uint64_t>(nblk * J)) ++cbits;
+  tbytes = 0;
+  P2G_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tbytes, ck.get(), sck.get(), ids.get(), c->seg_ids.get(),
+                                           static_cast<int>(nseg), 0, cbits, s));
+  temp.resize(tbytes);
+  P2G_CUDA(cub::DeviceRadixSort::SortPairs(temp.get(), tbytes, ck.get(), sck.get(), ids.get(), c->seg_ids.get(),
+                                           static_cast<int>(nseg), 0, cbits, s));
+  k_key_ptr<<<grid_for(J + 1, 256), 256, 0, s>>>(J, nseg, nblk, sck.get(), c->seg_ptr.get());
   P2G_CUDA(cudaStreamSynchronize(s));
 }
 
 template <int RP>
 static void seg_spmm(p2g_ctx* c, int R, const double* U, cudaStream_t s) {
-  const std::size_t smem = sizeof(double) * kSpThreads * (RP + 1);
-  auto kern = k_seg_spmm<RP>;
-  P2G_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-  const int blocks = static_cast<int>(std::max<std::int64_t>(1, std::min<std::int64_t>(c->nseg, 148 * 16)));
-  kern<<<blocks, kSpThreads, smem, s>>>(R, c->nseg, c->seg_beg.get(), c->seg_end.get(), c->csc_row.get(),
-                                        c->csc_val.get(), U, c->seg_part.get());
+  k_seg_spmm<RP><<<grid_for(c->nseg, 128), 128, 0, s>>>(R, c->nseg, c->nnz, c->seg_beg.get(), c->csc_row.get(),
+                                                        c->csc_val.get(), U, c->seg_part.get());
 }
 
 void launch_csc_mode2(p2g_ctx* c, int R, const double* U, double* M2, cudaStream_t s) {
@@ -250,7 +312,7 @@ void launch_csc_mode2(p2g_ctx* c, int R, const double* U, double* M2, cudaStream
       throw InvalidArgument("rank above 40 unsupported");
     P2G_LAUNCHED(1);
   }
-  k_seg_reduce<<<grid_for(c->J * R, 256), 256, 0, s>>>(R, c->J, c->seg_ptr.get(), c->seg_part.get(), M2);
+  k_seg_reduce<<<grid_for(c->J * R, 256), 256, 0, s>>>(R, c->J, c->seg_ptr.get(), c->seg_ids.get(), c->seg_part.get(), M2);
   P2G_LAUNCHED(1);
 }
 

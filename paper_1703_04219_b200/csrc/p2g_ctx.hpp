@@ -132,7 +132,7 @@ struct p2g_ctx {
   p2g::DBuf<double> m2part;           // per-range J x R partials of the on-chip mode-2 kernel
   // column-major copy of the shard for the atomics-free mode-2 pass (k_csc.cu)
   p2g::DBuf<std::int64_t> col_ptr, seg_ptr, seg_beg, seg_end;
-  p2g::DBuf<std::int32_t> csc_row;
+  p2g::DBuf<std::int32_t> csc_row, seg_ids;
   p2g::DBuf<double> csc_val, seg_part, Ubuf;
   std::int64_t nseg = 0;
   p2g::DBuf<unsigned> mask_v, mask_w; // NNLS passive sets of the previous iteration (warm start)
