@@ -278,3 +278,34 @@ def test_large_rank_prefix_parity(ctx, oracle, p2g, cfg_id, R, K):
     last = ref["dumps"][-1]
     for key, got in (("H", res.H), ("V", res.V), ("W", res.W)):
         assert rel_err(got, last[key]) <= TOL_STEP, key
+
+
+def test_cfg5_small_rank_prefix_parity(ctx, oracle, p2g):
+    """cfg5's Zipf-hot columns (split CSC segments) through the R <= 16 pipeline."""
+    R = 10
+    X = p2g.generate_baseline(5, R, K=3000)
+    H0, V0, W0 = p2g.init_factors(int(p2g.baseline_spec(5, R).seed), X.K, X.J, R)
+    T = oracle_from_csr(oracle, X)
+    ref = oracle.fit_parafac2(T, R, max_iters=3, tol=1e-300, nonneg=True, threads=8, H0=H0, V0=V0, W0=W0,
+                              dumps=True)
+    ctx.load(X)
+    res = ctx.fit(p2g.SolverConfig(rank=R, max_iters=3, tol=1e-300, nonneg=True), H0, V0, W0)
+    assert np.abs(res.fit - np.array(ref["fit"])).max() <= TOL_FIT
+    last = ref["dumps"][-1]
+    for key, got in (("H", res.H), ("V", res.V), ("W", res.W)):
+        assert rel_err(got, last[key]) <= TOL_STEP, key
+
+
+@pytest.mark.parametrize("R", [10, 40])
+def test_fit_bitwise_deterministic(ctx, p2g, R):
+    """Fixed-order reductions everywhere (CSC mode 2, partial sums, NNLS): two
+    fits from the same inputs agree bit for bit."""
+    X = p2g.generate_baseline(3 if R > 16 else 2, R, K=4000)
+    H0, V0, W0 = p2g.init_factors(7, X.K, X.J, R)
+    ctx.load(X)
+    cfg = p2g.SolverConfig(rank=R, max_iters=4, tol=1e-300, nonneg=True)
+    a = ctx.fit(cfg, H0, V0, W0)
+    b = ctx.fit(cfg, H0, V0, W0)
+    assert np.array_equal(a.fit, b.fit)
+    for x, y in ((a.H, b.H), (a.V, b.V), (a.W, b.W), (a.Q, b.Q)):
+        assert np.array_equal(x, y)
