@@ -65,6 +65,14 @@ __device__ __forceinline__ void csr_row_times(double (&acc)[RP], const int32_t* 
   }
 }
 
+/// D += A B on the fp64 tensor cores (DMMA m8n8k4, row.col): the warp holds
+/// A[lane/4][lane%4], B[lane%4][lane/4] and D[lane/4][2(lane%4) + {0,1}].
+__device__ __forceinline__ void dmma884(double (&d)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(d[0]), "+d"(d[1])
+               : "d"(a), "d"(b));
+}
+
 /// acc[u] += X_row(u) . V for U rows at once, V1 only (NV = 1) or also
 /// acc2[u] += X_row(u) . V2 (NV = 2): the t-th entry of every row is loaded
 /// together, so a lane keeps U independent ci -> V dependency chains in

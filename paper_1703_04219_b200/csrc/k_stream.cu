@@ -16,9 +16,11 @@
 //    each lane finds its subject in the batch row offsets.
 //  * mode 2 writes the row factors u_i (coalesced); M2 = X^T U is read out
 //    from the CSC copy without atomics (k_csc.cu).
-//  * mode 3 stages [xn | q o xn | 1] per row in shared memory; lanes own
-//    entries of the packed Gram C and of m3 and accumulate them in row order,
-//    flushing at subject boundaries (warp-uniform, deterministic).
+//  * mode 3 stages the xn and q rows in shared memory and accumulates the
+//    next iteration's Gram C = Xn^T Xn and m3 = diag(Q^T Xn) on the fp64
+//    tensor cores (DMMA m8n8k4, 4-row k-steps per subject segment, rows of
+//    other subjects masked to zero), flushing at subject boundaries
+//    (warp-uniform control, fixed order: deterministic).
 #include <algorithm>
 
 #include "dev_common.cuh"
@@ -42,14 +44,13 @@ struct StreamCfg {
   static constexpr int NRL = (R + LPS - 1) / LPS;             // T rows per lane
   static constexpr int RR = R * R;
   static constexpr int NT = R * (R + 1) / 2;
-  static constexpr int CW = 2 * R + 1;                        // mode-3 row record: xn | q o xn | 1
-  static constexpr int NE = NT + R;                           // mode-3 accumulated entries
-  static constexpr int NU = (NE + 31) / 32;                   // entries per lane
   static constexpr int WPB = 4;
   static constexpr int kWarpT = RR * SBP;                     // doubles
   static constexpr int UM2 = 4;                               // rows per lane in flight (mode 2)
   static constexpr int UM3 = 2;                               // rows per lane in flight (mode 3)
-  static constexpr int kWarpCh = 32 * UM3 * CW;               // doubles (mode 3 row records)
+  static constexpr int NB = (R + 7) / 8;                      // 8 x 8 tensor tiles per side (mode 3)
+  static constexpr int XS = NB == 1 ? 12 : 20;                // staged row stride: conflict-free fragments
+  static constexpr int kWarpCh = 2 * 32 * UM3 * XS;           // doubles (mode 3: xn and q rows)
 };
 
 __host__ __device__ constexpr int tri_idx(int i, int j) { return i >= j ? i * (i + 1) / 2 + j : j * (j + 1) / 2 + i; }
@@ -221,24 +222,6 @@ __global__ void __launch_bounds__(StreamCfg<R>::WPB * 32)
     Hs[e] = Hprev[e];
     Hts[e] = Ht[e];
   }
-  // accumulated entries owned by this lane: (ea, eb) into the row record
-  int ea[C::NU], eb[C::NU];
-#pragma unroll
-  for (int u = 0; u < C::NU; ++u) {
-    const int t = lane + 32 * u;
-    if (t < C::NT) {
-      int x = 0;
-      while ((x + 1) * (x + 2) / 2 <= t) ++x;
-      ea[u] = x;
-      eb[u] = t - x * (x + 1) / 2;
-    } else if (t < C::NE) {
-      ea[u] = R + (t - C::NT);
-      eb[u] = 2 * R;
-    } else {
-      ea[u] = 2 * R;  // unused (1 * 1)
-      eb[u] = 2 * R;
-    }
-  }
   __syncthreads();
   const std::int64_t nbatch = (X.K + C::SB - 1) / C::SB;
   const std::int64_t nwarps = static_cast<std::int64_t>(gridDim.x) * C::WPB;
@@ -251,21 +234,33 @@ __global__ void __launch_bounds__(StreamCfg<R>::WPB * 32)
     if (lane < C::SB) fl[lane] = lane < nb ? flags[k0 + lane] : P2G_FLAG_FULL_RANK;
     __syncwarp();
     build_batch_ops<R, 3>(k0, nb, Hs, Hts, nullptr, Wprev, Sbuf, Shat, fl, Tw, lane);
-    double acc[C::NU];
-#pragma unroll
-    for (int u = 0; u < C::NU; ++u) acc[u] = 0.0;
+    // fp64 tensor-core accumulators (DMMA m8n8k4, fragment: c0 = C[lane/4][2(lane%4)],
+    // c1 = C[lane/4][2(lane%4)+1]): Gram tiles (0,0), (1,0), (1,1) of Xn^T Xn and the
+    // diagonal tiles of Q^T Xn (m3 = its diagonal)
+    double g00[2] = {0.0, 0.0}, g10[2] = {0.0, 0.0}, g11[2] = {0.0, 0.0};
+    double d00[2] = {0.0, 0.0}, d11[2] = {0.0, 0.0};
     int cur = 0;  // subject being accumulated (warp-uniform)
+    const int fm = lane >> 2, fn = 2 * (lane & 3);
     auto flush = [&](int s) {
       const std::int64_t k = k0 + s;
-#pragma unroll
-      for (int u = 0; u < C::NU; ++u) {
-        const int t = lane + 32 * u;
-        if (t < C::NT)
-          Cnext[k * C::NT + t] = acc[u];
-        else if (t < C::NE)
-          M3[k * R + (t - C::NT)] = acc[u];
-        acc[u] = 0.0;
+      double* cn = Cnext + k * C::NT;
+      auto put = [&](int a, int b, double v) {
+        if (a < R && b <= a) cn[a * (a + 1) / 2 + b] = v;
+      };
+      put(fm, fn, g00[0]);
+      put(fm, fn + 1, g00[1]);
+      if (fm == fn && fm < R) M3[k * R + fm] = d00[0];
+      if (fm == fn + 1 && fm < R) M3[k * R + fm] = d00[1];
+      if constexpr (C::NB == 2) {
+        put(8 + fm, fn, g10[0]);
+        put(8 + fm, fn + 1, g10[1]);
+        put(8 + fm, 8 + fn, g11[0]);
+        put(8 + fm, 8 + fn + 1, g11[1]);
+        if (fm == fn && 8 + fm < R) M3[k * R + 8 + fm] = d11[0];
+        if (fm == fn + 1 && 8 + fm < R) M3[k * R + 8 + fm] = d11[1];
       }
+      g00[0] = g00[1] = g10[0] = g10[1] = g11[0] = g11[1] = 0.0;
+      d00[0] = d00[1] = d11[0] = d11[1] = 0.0;
     };
     int sl = 0;
     constexpr int UR = C::UM3;
@@ -310,20 +305,50 @@ __global__ void __launch_bounds__(StreamCfg<R>::WPB * 32)
             qv[c] += a0;
           }
         }
-        double* rec = ch + (lane + 32 * u) * C::CW;
+        double* xs = ch + (lane + 32 * u) * C::XS;
+        double* qs = xs + 32 * UR * C::XS;
 #pragma unroll
-        for (int a = 0; a < R; ++a) {
-          rec[a] = xn[u][a];
-          rec[R + a] = qv[a] * xn[u][a];
+        for (int a = 0; a < 8 * C::NB; ++a) {
+          xs[a] = a < R ? xn[u][a] : 0.0;
+          qs[a] = a < R ? qv[a] : 0.0;
         }
-        rec[2 * R] = 1.0;
       }
-      __syncwarp();
-      for (int rr = 0; rr < nr; ++rr) {
-        while (cb + rr >= rowoff[cur + 1]) flush(cur++);
-        const double* rec = ch + rr * C::CW;
 #pragma unroll
-        for (int u = 0; u < C::NU; ++u) acc[u] = fma(rec[ea[u]], rec[eb[u]], acc[u]);
+      for (int u = 0; u < UR; ++u)
+        if (su[u] < 0) {  // past the batch: zero rows accumulate nothing
+          double* xs = ch + (lane + 32 * u) * C::XS;
+          double* qs = xs + 32 * UR * C::XS;
+#pragma unroll
+          for (int a = 0; a < 8 * C::NB; ++a) xs[a] = qs[a] = 0.0;
+        }
+      __syncwarp();
+      // per subject segment [ss, se) of the chunk: 4-row k-steps on the tensor
+      // cores, rows outside the segment enter as zeros (warp-uniform control)
+      int ss = 0;
+      while (ss < nr) {
+        const int end = rowoff[cur + 1] - cb;
+        if (end <= ss) {  // subject closed at or before this point
+          flush(cur++);
+          continue;
+        }
+        const int se = min(end, nr);
+        for (int k4 = ss & ~3; k4 < se; k4 += 4) {
+          const int r = k4 + (lane & 3);
+          const bool in = r >= ss && r < se;
+          const double* xr = ch + r * C::XS;
+          const double* qr = xr + 32 * UR * C::XS;
+          const double x0 = in ? xr[fm] : 0.0, q0 = in ? qr[fm] : 0.0;
+          dev::dmma884(g00, x0, x0);
+          dev::dmma884(d00, q0, x0);
+          if constexpr (C::NB == 2) {
+            const double x1 = in ? xr[8 + fm] : 0.0, q1 = in ? qr[8 + fm] : 0.0;
+            dev::dmma884(g10, x1, x0);
+            dev::dmma884(g11, x1, x1);
+            dev::dmma884(d11, q1, x1);
+          }
+        }
+        if (end <= nr) flush(cur++);
+        ss = se;
       }
       __syncwarp();
     }
