@@ -36,7 +36,7 @@ namespace {
 
 constexpr int kLgThreads = 128;
 constexpr int kLgMaxSweeps = 40;
-constexpr double kTolL = 4e-15;   // two-sided skip tolerance (scaled off-diagonal)
+constexpr double kTolL = 1e-12;   // two-sided skip tolerance (scaled off-diagonal)
 constexpr double kTinyL = 1e-24;  // M_pp below this x max diag: near-null column (covers D5's 1e-26)
 
 struct LgArgs {
