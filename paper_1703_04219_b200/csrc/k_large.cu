@@ -418,6 +418,392 @@ __global__ void __launch_bounds__(kLgThreads, 2) k_procrustes_large(LgArgs a) {
     a.m1_partials[static_cast<std::int64_t>(blockIdx.x) * RR + e] = M1[(e / R) * LDM + e % R];
 }
 
+// ---------------------------------------------------------------------------
+// Warp-per-subject variant (default).  Same algorithm as k_procrustes_large;
+// a CTA-wide Jacobi round costs two barriers and leaves most threads idle, so
+// here one warp owns a subject: M and V' live in the warp's shared memory,
+// the row slabs (B, X~), T/Z, F, E and the warp's M1 partial in a per-warp
+// global slab (L1/L2 resident), and M = B^T B, F = B^T X~ run on the fp64
+// tensor cores (DMMA m8n8k4 over 4-row k-steps of the slab).
+// ---------------------------------------------------------------------------
+template <int RP>
+struct LgWarp {
+  static constexpr int LDM = RP + 1;
+  static constexpr int kMat = RP * LDM;
+  static constexpr int NBLK = (RP / 2) * (RP / 2 + 1) / 2;
+  static constexpr int kBlkD = (NBLK + 3) / 4;            // uint16 table in doubles
+  static constexpr int kWarpD = 2 * kMat + 4 * RP;         // M, V', w, 1/sigma, (c, s, t), pairs
+  static constexpr int pick_wpb() {
+    int w = 16;
+    while (w > 1 && (kMat + kBlkD + w * kWarpD) * 8 > 225 * 1024) --w;
+    return w;
+  }
+  static constexpr int WPB = pick_wpb();
+  static constexpr std::size_t kSmem = sizeof(double) * (kMat + kBlkD + WPB * kWarpD);
+  static constexpr int NB = RP / 8;  // 8-wide tensor tiles (RP multiple of 8)
+};
+
+template <int RP, bool EXACT>
+__global__ void __launch_bounds__(LgWarp<RP>::WPB * 32, 1) k_procrustes_large_w(LgArgs a) {
+  using L = LgWarp<RP>;
+  constexpr int LDM = L::LDM, NB = L::NB, WPB = L::WPB;
+  extern __shared__ double smem[];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int R = EXACT ? RP : a.R;
+  const int RR = R * R;
+  double* Hs = smem;
+  std::uint16_t* blk = reinterpret_cast<std::uint16_t*>(Hs + L::kMat);
+  double* M = Hs + L::kMat + L::kBlkD + wid * L::kWarpD;
+  double* Vp = M + L::kMat;
+  double* w = Vp + L::kMat;
+  double* isg = w + RP;      // 1 / sigma
+  double* rc = isg + RP;     // rotation c, s, t M_pq (RP/2 each)
+  double* rs = rc + RP / 2;
+  double* rt = rs + RP / 2;
+  int* rp = reinterpret_cast<int*>(rt + RP / 2);  // pairs (RP ints)
+  for (int e = threadIdx.x; e < RR; e += blockDim.x) Hs[(e / R) * LDM + e % R] = a.H[e];
+  const int m = (R + 1) & ~1, half = m / 2, nblk = half * (half + 1) / 2;
+  for (int it = threadIdx.x; it < nblk; it += blockDim.x) {
+    int i1 = 0, r = it;
+    while (r >= half - i1) {
+      r -= half - i1;
+      ++i1;
+    }
+    blk[it] = static_cast<std::uint16_t>((i1 << 8) | (i1 + r));
+  }
+  __syncthreads();
+  const std::int64_t gw = static_cast<std::int64_t>(blockIdx.x) * WPB + wid;
+  const std::int64_t nwarps = static_cast<std::int64_t>(gridDim.x) * WPB;
+  double* slab = a.slab + gw * (2 * a.max_rows * R + 5 * RR);
+  double* Bs = slab;                  // I x R rows of B
+  double* Xs = Bs + a.max_rows * R;   // I x R rows of X~ = XV D
+  double* Ts = Xs + a.max_rows * R;   // T, later Z (R x R)
+  double* Fs = Ts + RR;               // F = B^T X~
+  double* Es = Fs + RR;               // E (R x R)
+  double* Ns = Es + RR;               // E V' scratch
+  double* M1 = Ns + RR;               // this warp's m1 partial
+  for (int e = lane; e < RR; e += 32) M1[e] = 0.0;
+  const int fm = lane >> 2, fk = lane & 3, fn = 2 * (lane & 3);
+  for (std::int64_t k = gw; k < a.X.K; k += nwarps) {
+    const std::int64_t r0 = a.X.srp[k];
+    const int I = static_cast<int>(a.X.srp[k + 1] - r0);
+    for (int r = lane; r < R; r += 32) w[r] = a.W[k * R + r];
+    double* Ek = a.Ewarm + k * RR;
+    for (int e = lane; e < RR; e += 32) Es[e] = a.ew_valid ? Ek[e] : ((e / R == e % R) ? 1.0 : 0.0);
+    __syncwarp();
+    int flag = P2G_FLAG_FULL_RANK;
+    for (int pass = 0; pass < 2; ++pass) {
+      // T = D H^T E (lanes along columns j)
+      for (int j = lane; j < R; j += 32)
+        for (int i = 0; i < R; ++i) {
+          double acc = 0.0;
+          for (int c = 0; c < R; ++c) acc = fma(Hs[c * LDM + i], Es[c * R + j], acc);
+          Ts[i * R + j] = acc * w[i];
+        }
+      __syncwarp();
+      // rows: b_i = xv_i T, x~_i = xv_i o w
+      for (int i = lane; i < I; i += 32) {
+        double xv[RP];
+        dev::csr_row_times<RP>(xv, a.X.ci, a.X.val, a.X.rp[r0 + i], a.X.rp[r0 + i + 1], a.V, R);
+        double* brow = Bs + static_cast<std::int64_t>(i) * R;
+        for (int j = 0; j < R; ++j) {
+          double acc = 0.0;
+#pragma unroll
+          for (int c = 0; c < RP; ++c)
+            if (c < R) acc = fma(xv[c], Ts[c * R + j], acc);
+          brow[j] = acc;
+        }
+        if (pass == 0) {
+          double* xrow = Xs + static_cast<std::int64_t>(i) * R;
+#pragma unroll
+          for (int c = 0; c < RP; ++c)
+            if (c < R) xrow[c] = xv[c] * w[c];
+        }
+      }
+      __syncwarp();
+      // M = B^T B (lower tiles) on the tensor cores, into shared memory
+      bool finite = true;
+      {
+        double acc[NB * (NB + 1) / 2][2];
+#pragma unroll
+        for (int t = 0; t < NB * (NB + 1) / 2; ++t) acc[t][0] = acc[t][1] = 0.0;
+        for (int k4 = 0; k4 < I; k4 += 4) {
+          const int r = k4 + fk;
+          double f[NB];
+#pragma unroll
+          for (int b = 0; b < NB; ++b) {
+            const int col = 8 * b + fm;
+            f[b] = (r < I && col < R) ? Bs[static_cast<std::int64_t>(r) * R + col] : 0.0;
+          }
+          int t = 0;
+#pragma unroll
+          for (int bi = 0; bi < NB; ++bi)
+#pragma unroll
+            for (int bj = 0; bj <= bi; ++bj) dev::dmma884(acc[t++], f[bi], f[bj]);
+        }
+        int t = 0;
+#pragma unroll
+        for (int bi = 0; bi < NB; ++bi)
+#pragma unroll
+          for (int bj = 0; bj <= bi; ++bj, ++t) {
+            const int i = 8 * bi + fm;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const int j = 8 * bj + fn + h;
+              if (i < R && j < R) {
+                M[i * LDM + j] = acc[t][h];
+                M[j * LDM + i] = acc[t][h];
+                finite &= isfinite(acc[t][h]);
+              }
+            }
+          }
+      }
+      // F = B^T X~ (all tiles) into the slab
+      {
+#pragma unroll 1
+        for (int bi = 0; bi < NB; ++bi) {
+          double acc[NB][2];
+#pragma unroll
+          for (int bj = 0; bj < NB; ++bj) acc[bj][0] = acc[bj][1] = 0.0;
+          for (int k4 = 0; k4 < I; k4 += 4) {
+            const int r = k4 + fk;
+            const int ci = 8 * bi + fm;
+            const double fa = (r < I && ci < R) ? Bs[static_cast<std::int64_t>(r) * R + ci] : 0.0;
+#pragma unroll
+            for (int bj = 0; bj < NB; ++bj) {
+              const int cj = 8 * bj + fm;
+              const double fb = (r < I && cj < R) ? Xs[static_cast<std::int64_t>(r) * R + cj] : 0.0;
+              dev::dmma884(acc[bj], fa, fb);
+            }
+          }
+#pragma unroll
+          for (int bj = 0; bj < NB; ++bj) {
+            const int i = 8 * bi + fm;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const int j = 8 * bj + fn + h;
+              if (i < R && j < R) {
+                Fs[i * R + j] = acc[bj][h];
+                finite &= isfinite(acc[bj][h]);
+              }
+            }
+          }
+        }
+      }
+      finite = __all_sync(dev::kFull, finite);
+      __syncwarp();
+      if (!finite) {  // the accurate path re-checks the operand; no preconditioner from here
+        for (int e = lane; e < RR; e += 32) Es[e] = (e / R == e % R) ? 1.0 : 0.0;
+        __syncwarp();
+        flag = P2G_FLAG_ACCURATE;
+        break;
+      }
+      // scaled off-diagonal mass, V' = I
+      double off = 0.0;
+      for (int p = 0; p < R; ++p)
+        for (int q = lane; q < R; q += 32) {
+          const double d = M[p * LDM + p] * M[q * LDM + q];
+          if (p != q && d > 0.0) off += M[p * LDM + q] * M[p * LDM + q] / d;
+          Vp[p * LDM + q] = p == q ? 1.0 : 0.0;
+        }
+      off = dev::warp_sum(off);
+      __syncwarp();
+      bool converged = false;
+      int sweeps = 0;
+      for (int sweep = 0; sweep < kLgMaxSweeps; ++sweep, ++sweeps) {
+        double dmax = 0.0;
+        for (int j = 0; j < R; ++j) dmax = fmax(dmax, M[j * LDM + j]);
+        const double tiny = kTinyL * dmax;
+        bool need = false;
+        for (int p = 0; p < R; ++p)
+          for (int q = lane; q < R; q += 32) {
+            if (q <= p) continue;
+            const double al = M[p * LDM + p], be = M[q * LDM + q], ga = M[p * LDM + q];
+            if (al > tiny && be > tiny && !(ga == 0.0 || fabs(ga) <= kTolL * sqrt(al * be))) need = true;
+          }
+        if (!__any_sync(dev::kFull, need)) {
+          converged = true;
+          break;
+        }
+        for (int round = 0; round < m - 1; ++round) {
+          if (lane < half) {
+            int p, q;
+            if (lane == 0) {
+              p = round;
+              q = m - 1;
+            } else {
+              p = (round + lane) % (m - 1);
+              q = (round - lane + (m - 1)) % (m - 1);
+            }
+            if (p > q) {
+              const int t = p;
+              p = q;
+              q = t;
+            }
+            double c = 1.0, sn = 0.0, tt = 0.0, ga = 0.0;
+            if (q < R) {
+              const double al = M[p * LDM + p], be = M[q * LDM + q];
+              ga = M[p * LDM + q];
+              if (al > tiny && be > tiny && !(ga == 0.0 || fabs(ga) <= kTolL * sqrt(al * be))) {
+                const double zeta = (be - al) / (2.0 * ga);
+                tt = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+                c = 1.0 / sqrt(1.0 + tt * tt);
+                sn = c * tt;
+              }
+            } else {
+              q = -1;
+            }
+            rc[lane] = c;
+            rs[lane] = sn;
+            rt[lane] = tt * ga;
+            rp[2 * lane] = p;
+            rp[2 * lane + 1] = q;
+          }
+          __syncwarp();
+          for (int it = lane; it < nblk; it += 32) {
+            const int i1 = blk[it] >> 8, i2 = blk[it] & 0xff;
+            const int p1 = rp[2 * i1], q1 = rp[2 * i1 + 1], p2 = rp[2 * i2], q2 = rp[2 * i2 + 1];
+            const double s1 = rs[i1], s2 = rs[i2];
+            if (s1 == 0.0 && s2 == 0.0) continue;
+            if (q1 < 0 || q2 < 0) {  // odd R: 1 x 2 block against the dummy pair's index
+              if (q1 < 0 && q2 < 0) continue;
+              const int aa = q1 < 0 ? p1 : p2;
+              const int u = q1 < 0 ? p2 : p1, v = q1 < 0 ? q2 : q1;
+              const double cc = q1 < 0 ? rc[i2] : rc[i1], ss = q1 < 0 ? s2 : s1;
+              const double xu = M[aa * LDM + u], xv = M[aa * LDM + v];
+              const double nu = cc * xu - ss * xv, nv = ss * xu + cc * xv;
+              M[aa * LDM + u] = nu;
+              M[u * LDM + aa] = nu;
+              M[aa * LDM + v] = nv;
+              M[v * LDM + aa] = nv;
+              continue;
+            }
+            if (i1 == i2) {
+              const double d = rt[i1];
+              M[p1 * LDM + p1] -= d;
+              M[q1 * LDM + q1] += d;
+              M[p1 * LDM + q1] = 0.0;
+              M[q1 * LDM + p1] = 0.0;
+              continue;
+            }
+            const double c1 = rc[i1], c2 = rc[i2];
+            const double x11 = M[p1 * LDM + p2], x12 = M[p1 * LDM + q2], x21 = M[q1 * LDM + p2], x22 = M[q1 * LDM + q2];
+            const double y11 = c2 * x11 - s2 * x12, y12 = s2 * x11 + c2 * x12;
+            const double y21 = c2 * x21 - s2 * x22, y22 = s2 * x21 + c2 * x22;
+            const double z11 = c1 * y11 - s1 * y21, z21 = s1 * y11 + c1 * y21;
+            const double z12 = c1 * y12 - s1 * y22, z22 = s1 * y12 + c1 * y22;
+            M[p1 * LDM + p2] = z11;
+            M[p2 * LDM + p1] = z11;
+            M[p1 * LDM + q2] = z12;
+            M[q2 * LDM + p1] = z12;
+            M[q1 * LDM + p2] = z21;
+            M[p2 * LDM + q1] = z21;
+            M[q1 * LDM + q2] = z22;
+            M[q2 * LDM + q1] = z22;
+          }
+          // V' <- V' J: lanes along the rows, pairs in turn
+          for (int pr = 0; pr < half; ++pr) {
+            const int p = rp[2 * pr], q = rp[2 * pr + 1];
+            const double sn = rs[pr];
+            if (q < 0 || sn == 0.0) continue;
+            const double c = rc[pr];
+            for (int kk = lane; kk < R; kk += 32) {
+              const double vp = Vp[kk * LDM + p], vq = Vp[kk * LDM + q];
+              Vp[kk * LDM + p] = c * vp - sn * vq;
+              Vp[kk * LDM + q] = sn * vp + c * vq;
+            }
+          }
+          __syncwarp();
+        }
+      }
+      if (a.dbg && lane == 0) {
+        atomicAdd(a.dbg + 0, sweeps);
+        atomicMax(a.dbg + 1, sweeps);
+        if (pass == 0) atomicAdd(a.dbg + 3, 1);
+        if (pass == 1) atomicAdd(a.dbg + 2, 1);
+      }
+      // E <- E V' (lanes along columns)
+      for (int j = lane; j < R; j += 32)
+        for (int i = 0; i < R; ++i) {
+          double acc = 0.0;
+          for (int c = 0; c < R; ++c) acc = fma(Es[i * R + c], Vp[c * LDM + j], acc);
+          Ns[i * R + j] = acc;
+        }
+      __syncwarp();
+      for (int e = lane; e < RR; e += 32) Es[e] = Ns[e];
+      __syncwarp();
+      if (!converged) {
+        flag = P2G_FLAG_ACCURATE;
+        break;
+      }
+      double smax2 = 0.0, smin2 = 1e308;
+      for (int j = 0; j < R; ++j) {
+        smax2 = fmax(smax2, M[j * LDM + j]);
+        smin2 = fmin(smin2, M[j * LDM + j]);
+      }
+      if (!(smax2 > 0.0) || !(smin2 > kTinyL * smax2)) {
+        flag = P2G_FLAG_ACCURATE;
+        break;
+      }
+      if (pass == 0 && off > 0.25 && smin2 < 1e-6 * smax2) continue;
+      for (int j = lane; j < R; j += 32) isg[j] = 1.0 / sqrt(M[j * LDM + j]);
+      __syncwarp();
+      // Z = V' Sigma^-1 V_A^T into Ts; m1 += Z^T F
+      for (int j = lane; j < R; j += 32)
+        for (int i = 0; i < R; ++i) {
+          double acc = 0.0;
+          for (int c = 0; c < R; ++c) acc = fma(Vp[i * LDM + c] * isg[c], Es[j * R + c], acc);
+          Ts[i * R + j] = acc;
+        }
+      __syncwarp();
+      for (int j = lane; j < R; j += 32)
+        for (int i = 0; i < R; ++i) {
+          double acc = 0.0;
+          for (int c = 0; c < R; ++c) acc = fma(Ts[c * R + i], Fs[c * R + j], acc);
+          M1[i * R + j] += acc;
+        }
+      // Q rows = b_i Z
+      for (int i = lane; i < I; i += 32) {
+        const double* brow = Bs + static_cast<std::int64_t>(i) * R;
+        double b[RP];
+#pragma unroll
+        for (int c = 0; c < RP; ++c) b[c] = c < R ? brow[c] : 0.0;
+        double* qrow = a.Q + (r0 + i) * R;
+        for (int j = 0; j < R; ++j) {
+          double acc = 0.0;
+#pragma unroll
+          for (int c = 0; c < RP; ++c)
+            if (c < R) acc = fma(b[c], Ts[c * R + j], acc);
+          qrow[j] = acc;
+        }
+      }
+      __syncwarp();
+      break;
+    }
+    for (int e = lane; e < RR; e += 32) Ek[e] = Es[e];
+    if (lane == 0) a.flags[k] = flag;
+    __syncwarp();
+  }
+  for (int e = lane; e < RR; e += 32) a.m1_partials[gw * RR + e] = M1[e];
+}
+
+template <int RP, bool EXACT>
+int launch_large_w(p2g_ctx* c, LgArgs a, int max_partials, cudaStream_t s) {
+  using L = LgWarp<RP>;
+  auto kern = k_procrustes_large_w<RP, EXACT>;
+  P2G_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(L::kSmem)));
+  const std::int64_t K = a.X.K;
+  const int blocks = static_cast<int>(std::max<std::int64_t>(
+      1, std::min<std::int64_t>({(K + L::WPB - 1) / L::WPB, static_cast<std::int64_t>(c->num_sms),
+                                 static_cast<std::int64_t>(max_partials / L::WPB)})));
+  const std::size_t per_warp = 2 * static_cast<std::size_t>(std::max<std::int64_t>(a.max_rows, 1)) * a.R +
+                               5 * static_cast<std::size_t>(a.R) * a.R;
+  c->acc_scratch.resize(static_cast<std::size_t>(blocks) * L::WPB * per_warp);
+  a.slab = c->acc_scratch.get();
+  kern<<<blocks, L::WPB * 32, L::kSmem, s>>>(a);
+  return blocks * L::WPB;  // one m1 partial per warp
+}
+
 template <int RP, bool EXACT>
 int launch_large(p2g_ctx* c, LgArgs a, int max_blocks, cudaStream_t s) {
   const std::size_t smem = sizeof(double) * LgSmem<RP>::kDoubles + sizeof(int) * LgSmem<RP>::kInts;
@@ -456,6 +842,24 @@ int launch_procrustes_large(p2g_ctx* c, int R, const double* H, const double* V,
   a.dbg = std::getenv("P2G_DEBUG") ? c->counters.get() + 4 : nullptr;
   if (a.X.K == 0) return 0;
   int blocks = 0;
+  if (!std::getenv("P2G_LARGE_CTA")) {  // default: warp per subject
+    if (R == 24)
+      blocks = launch_large_w<24, true>(c, a, max_blocks, s);
+    else if (R == 32)
+      blocks = launch_large_w<32, true>(c, a, max_blocks, s);
+    else if (R == 40)
+      blocks = launch_large_w<40, true>(c, a, max_blocks, s);
+    else if (R <= 24)
+      blocks = launch_large_w<24, false>(c, a, max_blocks, s);
+    else if (R <= 32)
+      blocks = launch_large_w<32, false>(c, a, max_blocks, s);
+    else if (R <= 40)
+      blocks = launch_large_w<40, false>(c, a, max_blocks, s);
+    else
+      throw InvalidArgument("rank above 40 unsupported");
+    P2G_LAUNCHED(1);
+    return blocks;
+  }
   if (R == 24)
     blocks = launch_large<24, true>(c, a, max_blocks, s);
   else if (R == 32)
