@@ -38,6 +38,21 @@ CONFIG_NAME = {1: "cfg1 tiny (K=1000, J=500, R=5)", 2: "cfg2 paper-scale (K=1M, 
 METRIC = "spartan_als_nnz_per_s"
 
 
+def load_fp64_peak():
+    """Measured DFMA peak (scripts/fp64_peak.cu, profiles/fp64_peak_r01.json)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "fp64_peak_r01.json")) as f:
+            return float(json.load(f)["dfma_tflops"]), "measured (scripts/fp64_peak.cu)"
+    except Exception:
+        return 37.0, "fallback"
+
+
+def iteration_flops(X, R):
+    """SURVEY.md 8(d) F_iter: 6 nnz R + 12 sum(I_k) R^2 + 11 K R^3 (XV twice and X^T U';
+    six I_k x R x R products; eig ~9R^3 + 2R^3 for the inverse square root)."""
+    return 6.0 * X.nnz * R + 12.0 * X.n_rows * R * R + 11.0 * X.K * R ** 3
+
+
 def load_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -342,6 +357,12 @@ def main():
                "d2h_bytes_per_step": d2h // e2e_iters, "iterations_per_call": e2e_iters, "sec_per_call": dt,
                "fit_final": float(res.fit[-1])}
 
+    # FP64 view of the step (the per-subject R x R work is FP64-issue bound)
+    fpk, fpk_kind = load_fp64_peak()
+    flops = iteration_flops(X, R)
+    fp_tf = flops / (ms_step * 1e-3) / 1e12
+    fp64 = {"bound": "fp64", "achieved": fp_tf, "peak": fpk, "unit": "TFLOP/s", "frac": fp_tf / fpk,
+            "flops_per_iter": flops, "peak_kind": fpk_kind, "model": "SURVEY.md 8(d) F_iter"}
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(X, R, cfg_id)
@@ -357,7 +378,7 @@ def main():
                        "l2": "inputs larger than L2 (CSR+Q >> 126 MB)", "parallelism": f"subject-shard x{world}"},
             "ms_per_iter_all": [float(x) for x in ms], "fit_trace": [float(x) for x in fits],
             "iteration_gbs_algorithmic": iter_gbs, "iteration_hbm_frac": iter_gbs / peak,
-            "roofline": roofline, "kernel_ms_per_launch": {k: v[0] for k, v in ktimes.items()},
+            "roofline": roofline, "roofline_fp64": fp64, "kernel_ms_per_launch": {k: v[0] for k, v in ktimes.items()},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches), "wall_s_timed": wall,
             "clocks": clk.summary(), "gen_s": t_gen,
         }
