@@ -19,6 +19,8 @@
 #include <cstdlib>
 #include <utility>
 
+#include <cub/device/device_radix_sort.cuh>
+
 #include "dev_common.cuh"
 #include "p2g_ctx.hpp"
 
@@ -289,7 +291,8 @@ template <int RP, int WPB>
 __global__ void __launch_bounds__(WPB * 32)
     k_polar_small(std::int64_t K, int R, const double* __restrict__ H, const double* __restrict__ W,
                   const double* __restrict__ Cbuf, double* __restrict__ Sbuf, double* __restrict__ Ewarm, int /*warm*/,
-                  std::int32_t* __restrict__ flags, double* __restrict__ m1_partials, int* __restrict__ dbg) {
+                  std::int32_t* __restrict__ flags, double* __restrict__ m1_partials, int* __restrict__ dbg,
+                  const std::int32_t* __restrict__ perm, std::uint8_t* __restrict__ sweeps_out) {
   extern __shared__ double smem[];
   constexpr int MP = PolarSmem<RP>::MP;
   constexpr int NT = PolarSmem<RP>::NT;
@@ -308,8 +311,11 @@ __global__ void __launch_bounds__(WPB * 32)
 
   const std::int64_t nwarps = static_cast<std::int64_t>(gridDim.x) * WPB;
   for (std::int64_t kb = (static_cast<std::int64_t>(blockIdx.x) * WPB + wid) * 32; kb < K; kb += nwarps * 32) {
-    const std::int64_t k = kb + lane;
-    const bool active = k < K;
+    // subjects in the order of the previous step's sweep counts (perm), so a
+    // warp's 32 subjects need similar numbers of sweeps (the warp runs until
+    // its slowest lane converges)
+    const bool active = kb + lane < K;
+    const std::int64_t k = active ? (perm ? static_cast<std::int64_t>(perm[kb + lane]) : kb + lane) : K;
     const int nk = static_cast<int>(min(static_cast<std::int64_t>(32), K - kb));
     double s[MP];
 #pragma unroll
@@ -394,6 +400,7 @@ __global__ void __launch_bounds__(WPB * 32)
       }
       ok = converged;
     }
+    if (active && sweeps_out) sweeps_out[k] = static_cast<std::uint8_t>(sweeps);
     if (dbg) {  // sweep statistics: sum per subject, max, sum of per-warp max, warps
       int wmax = sweeps;
       for (int o = 16; o > 0; o >>= 1) wmax = max(wmax, __shfl_xor_sync(dev::kFull, wmax, o));
@@ -490,8 +497,10 @@ __global__ void __launch_bounds__(WPB * 32)
 #pragma unroll
     for (int e = 0; e < NT; ++e) el(lane, e) = g[e];
     __syncwarp();
-    for (int sub = 0; sub < nk; ++sub)
-      for (int e = lane; e < nt; e += 32) Sbuf[(kb + sub) * nt + e] = el(sub, e);
+    for (int sub = 0; sub < nk; ++sub) {
+      const std::int64_t ks = __shfl_sync(dev::kFull, k, sub);
+      for (int e = lane; e < nt; e += 32) Sbuf[ks * nt + e] = el(sub, e);
+    }
     __syncwarp();
   }
   __syncthreads();
@@ -764,6 +773,16 @@ constexpr int gram_wpb() {
   return w;
 }
 
+__global__ void k_iota32(std::int64_t n, std::int32_t* __restrict__ out) {
+  for (std::int64_t i = static_cast<std::int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<std::int64_t>(gridDim.x) * blockDim.x)
+    out[i] = static_cast<std::int32_t>(i);
+}
+
+void fill_iota(std::int32_t* out, std::int64_t n, cudaStream_t s) {
+  k_iota32<<<static_cast<int>(std::min<std::int64_t>((n + 255) / 256, 148 * 16)), 256, 0, s>>>(n, out);
+}
+
 int grid_cap(std::int64_t work_warps, int wpb, int num_sms, int per_sm) {
   const std::int64_t want = (work_warps + wpb - 1) / wpb;
   return static_cast<int>(std::max<std::int64_t>(1, std::min<std::int64_t>(want, static_cast<std::int64_t>(num_sms) * per_sm)));
@@ -815,7 +834,7 @@ void launch_gram_c(p2g_ctx* c, int R, const double* V, double* Cbuf, cudaStream_
 template <int RP>
 static int polar_launch(p2g_ctx* c, std::int64_t K, int R, const double* H, const double* W, const double* Cbuf,
                         double* Sbuf, double* Ewarm, int warm, std::int32_t* flags, double* m1p, int max_blocks,
-                        cudaStream_t s) {
+                        const std::int32_t* perm, std::uint8_t* sweeps_out, cudaStream_t s) {
   constexpr int WPB = RP <= 10 ? 4 : 2;
   constexpr int MP = PolarSmem<RP>::MP;
   const std::size_t smem = sizeof(double) * (MP * MP + WPB * MP * MP + WPB * PolarSmem<RP>::kPerWarp);
@@ -826,16 +845,35 @@ static int polar_launch(p2g_ctx* c, std::int64_t K, int R, const double* H, cons
   const int blocks = grid_cap((K + 31) / 32, WPB, c->num_sms, std::max(per_sm, 1));
   const int nb = std::min(blocks, max_blocks);
   kern<<<nb, WPB * 32, smem, s>>>(K, R, H, W, Cbuf, Sbuf, Ewarm, warm, flags, m1p,
-                                  std::getenv("P2G_DEBUG") ? c->counters.get() + 4 : nullptr);
+                                  std::getenv("P2G_DEBUG") ? c->counters.get() + 4 : nullptr, perm, sweeps_out);
   return nb;
 }
 
 int launch_polar_small(p2g_ctx* c, int R, const double* H, const double* W, const double* Cbuf, double* Sbuf,
                        double* Ewarm, int warm, std::int32_t* flags, double* m1_partials, int max_blocks,
                        cudaStream_t s) {
+  const std::int64_t K = c->k_end - c->k_begin;
+  // order subjects by the previous step's sweep counts (stable, 5-bit keys)
+  c->polar_sweeps.resize(static_cast<std::size_t>(std::max<std::int64_t>(K, 1)));
+  const std::int32_t* perm = nullptr;
+  if (c->polar_sweeps_valid && K > 0 && !std::getenv("P2G_POLAR_NOSORT")) {
+    c->polar_perm.resize(static_cast<std::size_t>(2 * K));
+    c->polar_keys.resize(static_cast<std::size_t>(K));
+    std::int32_t* iota = c->polar_perm.get() + K;
+    fill_iota(iota, K, s);
+    std::size_t tbytes = 0;
+    P2G_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tbytes, c->polar_sweeps.get(), c->polar_keys.get(), iota,
+                                             c->polar_perm.get(), static_cast<int>(K), 0, 5, s));
+    c->polar_temp.resize(tbytes);
+    P2G_CUDA(cub::DeviceRadixSort::SortPairs(c->polar_temp.get(), tbytes, c->polar_sweeps.get(), c->polar_keys.get(),
+                                             iota, c->polar_perm.get(), static_cast<int>(K), 0, 5, s));
+    P2G_LAUNCHED(2);
+    perm = c->polar_perm.get();
+  }
   int nb = 0;
-  P2G_SMALL_DISPATCH(R, nb = polar_launch<RP_>(c, c->k_end - c->k_begin, R, H, W, Cbuf, Sbuf, Ewarm, warm, flags,
-                                               m1_partials, max_blocks, s));
+  P2G_SMALL_DISPATCH(R, nb = polar_launch<RP_>(c, K, R, H, W, Cbuf, Sbuf, Ewarm, warm, flags, m1_partials, max_blocks,
+                                               perm, c->polar_sweeps.get(), s));
+  c->polar_sweeps_valid = true;
   P2G_LAUNCHED(1);
   return nb;
 }

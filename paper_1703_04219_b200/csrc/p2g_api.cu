@@ -324,6 +324,7 @@ void init_state(p2g_ctx* c, const p2g_fit_config* cfg, const double* H0, const d
   c->c_valid = false;
   c->ew_valid = false;
   c->masks_valid = false;
+  c->polar_sweeps_valid = false;
   c->state_valid = true;
 }
 

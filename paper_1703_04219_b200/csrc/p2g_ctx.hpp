@@ -137,6 +137,10 @@ struct p2g_ctx {
   std::int64_t nseg = 0;
   p2g::DBuf<unsigned> mask_v, mask_w; // NNLS passive sets of the previous iteration (warm start)
   p2g::DBuf<unsigned long long> mask64_v, mask64_w;  // same, R > 16
+  p2g::DBuf<std::uint8_t> polar_sweeps, polar_keys;  // per-subject Jacobi sweeps of the last polar step
+  p2g::DBuf<std::int32_t> polar_perm;                // subjects sorted by those counts (+ iota scratch)
+  p2g::DBuf<unsigned char> polar_temp;
+  bool polar_sweeps_valid = false;
   bool masks_valid = false;
   bool state_valid = false;
 
