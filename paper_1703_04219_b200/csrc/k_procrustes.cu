@@ -346,40 +346,61 @@ __global__ void __launch_bounds__(WPB * 32) k_procrustes_accurate(K1Args a, doub
         for (int c = 0; c < R; ++c) A[i * R + c] *= inv;
       for (int e = lane; e < RR; e += 32) Vj[e] = (e / R == e % R) ? 1.0 : 0.0;
       __syncwarp();
-      // Hestenes sweeps (same rotation formulas as oracle one_sided_jacobi).
-      for (int sweep = 0; sweep < 80; ++sweep) {
-        int rotated = 0;
-        for (int p = 0; p < R - 1; ++p)
-          for (int q = p + 1; q < R; ++q) {
-            double al = 0.0, be = 0.0, ga = 0.0;
-            for (int i = lane; i < I; i += 32) {
-              const double x = A[i * R + p], y = A[i * R + q];
-              al = fma(x, x, al);
-              be = fma(y, y, be);
-              ga = fma(x, y, ga);
-            }
-            al = dev::warp_sum(al);
-            be = dev::warp_sum(be);
-            ga = dev::warp_sum(ga);
-            if (ga == 0.0 || fabs(ga) <= 1e-15 * sqrt(al * be)) continue;
-            rotated = 1;
-            const double zeta = (be - al) / (2.0 * ga);
-            const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-            const double c = 1.0 / sqrt(1.0 + t * t);
-            const double sn = c * t;
-            for (int i = lane; i < I; i += 32) {
-              const double x = A[i * R + p], y = A[i * R + q];
-              A[i * R + p] = c * x - sn * y;
-              A[i * R + q] = sn * x + c * y;
-            }
-            for (int r = lane; r < R; r += 32) {
-              const double x = Vj[r * R + p], y = Vj[r * R + q];
-              Vj[r * R + p] = c * x - sn * y;
-              Vj[r * R + q] = sn * x + c * y;
+      // Hestenes sweeps (same rotation formulas and skip rule as the oracle's
+      // one_sided_jacobi), round-robin ordering: the R/2 disjoint column pairs of
+      // a round go to R/2 lanes, each lane forming its (alpha, beta, gamma) over
+      // the rows and rotating its own two columns of A and V.  A round reads
+      // whole rows of A (coalesced) and needs no cross-lane reductions.
+      {
+        const int mm = (R + 1) & ~1, hh = mm / 2;
+        for (int sweep = 0; sweep < 80; ++sweep) {
+          bool rot = false;
+          for (int round = 0; round < mm - 1; ++round) {
+            if (lane < hh) {
+              int p, q;
+              if (lane == 0) {
+                p = round;
+                q = mm - 1;
+              } else {
+                p = (round + lane) % (mm - 1);
+                q = (round - lane + (mm - 1)) % (mm - 1);
+              }
+              if (p > q) {
+                const int t = p;
+                p = q;
+                q = t;
+              }
+              if (q < R) {
+                double al = 0.0, be = 0.0, ga = 0.0;
+                for (int i = 0; i < I; ++i) {
+                  const double x = A[i * R + p], y = A[i * R + q];
+                  al = fma(x, x, al);
+                  be = fma(y, y, be);
+                  ga = fma(x, y, ga);
+                }
+                if (!(ga == 0.0 || fabs(ga) <= 1e-15 * sqrt(al * be))) {
+                  rot = true;
+                  const double zeta = (be - al) / (2.0 * ga);
+                  const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+                  const double c = 1.0 / sqrt(1.0 + t * t);
+                  const double sn = c * t;
+                  for (int i = 0; i < I; ++i) {
+                    const double x = A[i * R + p], y = A[i * R + q];
+                    A[i * R + p] = c * x - sn * y;
+                    A[i * R + q] = sn * x + c * y;
+                  }
+                  for (int r = 0; r < R; ++r) {
+                    const double x = Vj[r * R + p], y = Vj[r * R + q];
+                    Vj[r * R + p] = c * x - sn * y;
+                    Vj[r * R + q] = sn * x + c * y;
+                  }
+                }
+              }
             }
             __syncwarp();
           }
-        if (!rotated) break;
+          if (!__any_sync(dev::kFull, rot)) break;
+        }
       }
       if (Ek) {  // right singular vectors of A = E V'
         for (int e = lane; e < RR; e += 32) {
