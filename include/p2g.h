@@ -218,6 +218,51 @@ int p2g_nnls_rowwise(p2g_ctx* ctx, const double* G, const double* B, int64_t n, 
 int p2g_pinv_small(p2g_ctx* ctx, const double* G, int32_t n, double* out);
 int p2g_gram(p2g_ctx* ctx, const double* A, int64_t rows, int32_t cols, double* out);
 
+/* ---------------------------------------------------------------------------
+ * Ingest and export (host side).  No GPU needed.
+ * ------------------------------------------------------------------------- */
+
+/* A parsed/loaded host CSR tensor owned by the library. */
+typedef struct p2g_csr p2g_csr;
+
+/* parse_coordinate_stream / parse_coordinate_file (io.hpp:100-177): '#'
+ * comments and blank lines skipped, "K J" header, entries "k i j v" (0-based),
+ * duplicates summed, zero sums dropped, all-zero rows removed (counted in
+ * filtered_rows), empty subjects rejected.  Errors are P2G_EDATA with the
+ * reference's messages ("... at line N").  threads 0 = all host threads. */
+int p2g_coo_parse(const char* text, int64_t len, int32_t threads, p2g_csr** out);
+int p2g_coo_read(const char* path, int32_t threads, p2g_csr** out);
+int p2g_csr_info(const p2g_csr* t, int64_t* K, int64_t* J, int64_t* n_rows, int64_t* nnz, int64_t* filtered_rows);
+int p2g_csr_copy(const p2g_csr* t, int64_t* subj_row_ptr, int64_t* row_ptr, int32_t* col_idx, double* val);
+void p2g_csr_free(p2g_csr* t);
+
+/* write_coordinate_file (io.hpp:179-204): canonical order (subject, column,
+ * row), "%.17g" values, optional "# comment" lines first. */
+int p2g_coo_write(const char* path, int64_t K, int64_t J, const int64_t* subj_row_ptr, const int64_t* row_ptr,
+                  const int32_t* col_idx, const double* val, const char* const* comments, int32_t n_comments);
+
+/* Binary CSR cache ("P2GCSR01" + K, J, NR, nnz + the four arrays): reloads a
+ * parsed tensor at storage speed. */
+int p2g_csr_cache_write(const char* path, int64_t K, int64_t J, const int64_t* subj_row_ptr, const int64_t* row_ptr,
+                        const int32_t* col_idx, const double* val);
+int p2g_csr_cache_read(const char* path, p2g_csr** out);
+
+/* write_matrix_file / read_matrix_file (io.hpp:206-268).  Column-major data.
+ * read: pass colmajor = NULL to query rows/cols. */
+int p2g_matrix_write(const char* path, int64_t rows, int64_t cols, const double* colmajor, const char* title);
+int p2g_matrix_read(const char* path, int64_t* rows, int64_t* cols, double* colmajor, int64_t capacity);
+int p2g_matrix_parse(const char* text, int64_t len, int64_t* rows, int64_t* cols, double* colmajor, int64_t capacity);
+
+/* write_factors (io.hpp:270-305): V.txt, S.txt, H.txt, U_<k>.txt with
+ * U_k = Q_k H (assemble_U, solver.hpp:238-243), manifest.json.  H, V, S
+ * column-major; Q packed row-major (sum I_k) x R; metadata_json is embedded
+ * as "config" (may be NULL). */
+int p2g_write_factors(const char* dir, int64_t K, int64_t J, int32_t R, const int64_t* subj_row_ptr, const double* H,
+                      const double* V, const double* S, const double* Q, const char* metadata_json);
+
+/* write_trace_tsv (io.hpp:307-315): "iter\tresidual_sq\tfit". */
+int p2g_write_trace(const char* path, int32_t n, const int32_t* iters, const double* residual_sq, const double* fit);
+
 #ifdef __cplusplus
 }
 #endif

@@ -10,3 +10,4 @@
 #include "slices.hpp"
 #include "solver.hpp"
 #include "sparse.hpp"
+#include "io.hpp"

@@ -121,6 +121,20 @@ _SIGS = {
     "p2g_nnls_rowwise": (ctypes.c_int, [_P, _P, _P, _I64, _I32, _I32, _P]),
     "p2g_pinv_small": (ctypes.c_int, [_P, _P, _I32, _P]),
     "p2g_gram": (ctypes.c_int, [_P, _P, _I64, _I32, _P]),
+    # ingest / export (host side)
+    "p2g_coo_parse": (ctypes.c_int, [ctypes.c_char_p, _I64, _I32, _P]),
+    "p2g_coo_read": (ctypes.c_int, [ctypes.c_char_p, _I32, _P]),
+    "p2g_csr_info": (ctypes.c_int, [_P, _P, _P, _P, _P, _P]),
+    "p2g_csr_copy": (ctypes.c_int, [_P, _P, _P, _P, _P]),
+    "p2g_csr_free": (None, [_P]),
+    "p2g_coo_write": (ctypes.c_int, [ctypes.c_char_p, _I64, _I64, _P, _P, _P, _P, _P, _I32]),
+    "p2g_csr_cache_write": (ctypes.c_int, [ctypes.c_char_p, _I64, _I64, _P, _P, _P, _P]),
+    "p2g_csr_cache_read": (ctypes.c_int, [ctypes.c_char_p, _P]),
+    "p2g_matrix_write": (ctypes.c_int, [ctypes.c_char_p, _I64, _I64, _P, ctypes.c_char_p]),
+    "p2g_matrix_read": (ctypes.c_int, [ctypes.c_char_p, _P, _P, _P, _I64]),
+    "p2g_matrix_parse": (ctypes.c_int, [ctypes.c_char_p, _I64, _P, _P, _P, _I64]),
+    "p2g_write_factors": (ctypes.c_int, [ctypes.c_char_p, _I64, _I64, _I32, _P, _P, _P, _P, _P, ctypes.c_char_p]),
+    "p2g_write_trace": (ctypes.c_int, [ctypes.c_char_p, _I32, _P, _P, _P]),
 }
 
 
@@ -215,6 +229,120 @@ class CSRTensor:
 
     def frobenius_sq(self) -> float:
         return float(np.dot(self.val, self.val))
+
+    def write_coordinate(self, path: str, comments: Sequence[str] = ()) -> None:
+        """write_coordinate_file (io.hpp:179-204): canonical order, %.17g values."""
+        arr = (ctypes.c_char_p * max(len(comments), 1))(*[c.encode() for c in comments])
+        _check(load_library().p2g_coo_write(os.fsencode(path), self.K, self.J, _ptr(self.subj_row_ptr),
+                                            _ptr(self.row_ptr), _ptr(self.col_idx), _ptr(self.val),
+                                            ctypes.cast(arr, ctypes.c_void_p), len(comments)))
+
+    def write_cache(self, path: str) -> None:
+        """Binary CSR cache (reloads at storage speed)."""
+        _check(load_library().p2g_csr_cache_write(os.fsencode(path), self.K, self.J, _ptr(self.subj_row_ptr),
+                                                  _ptr(self.row_ptr), _ptr(self.col_idx), _ptr(self.val)))
+
+
+def _take_csr(handle) -> "CSRTensor":
+    lib = load_library()
+    try:
+        K, J, nr, nz, filt = (ctypes.c_int64() for _ in range(5))
+        _check(lib.p2g_csr_info(handle, ctypes.byref(K), ctypes.byref(J), ctypes.byref(nr), ctypes.byref(nz),
+                                ctypes.byref(filt)))
+        srp = np.empty(K.value + 1, np.int64)
+        rp = np.empty(nr.value + 1, np.int64)
+        ci = np.empty(nz.value, np.int32)
+        val = np.empty(nz.value, np.float64)
+        _check(lib.p2g_csr_copy(handle, _ptr(srp), _ptr(rp), _ptr(ci), _ptr(val)))
+    finally:
+        lib.p2g_csr_free(handle)
+    t = CSRTensor(J.value, srp, rp, ci, val)
+    t.filtered_rows = filt.value
+    return t
+
+
+def parse_coordinate(text, threads: int = 0) -> "CSRTensor":
+    """parse_coordinate_stream (io.hpp:100-171) on a string/bytes; the result
+    carries .filtered_rows (all-zero rows removed)."""
+    data = text.encode() if isinstance(text, str) else bytes(text)
+    h = ctypes.c_void_p()
+    _check(load_library().p2g_coo_parse(data, len(data), threads, ctypes.byref(h)))
+    return _take_csr(h)
+
+
+def read_coordinate(path: str, threads: int = 0) -> "CSRTensor":
+    """parse_coordinate_file (io.hpp:173-177)."""
+    h = ctypes.c_void_p()
+    _check(load_library().p2g_coo_read(os.fsencode(path), threads, ctypes.byref(h)))
+    return _take_csr(h)
+
+
+def read_cache(path: str) -> "CSRTensor":
+    h = ctypes.c_void_p()
+    _check(load_library().p2g_csr_cache_read(os.fsencode(path), ctypes.byref(h)))
+    return _take_csr(h)
+
+
+def write_matrix(path: str, M, title: str) -> None:
+    """write_matrix_file (io.hpp:262-268)."""
+    M = _f64(M)
+    _check(load_library().p2g_matrix_write(os.fsencode(path), M.shape[0], M.shape[1], _ptr(M), title.encode()))
+
+
+def _matrix_from(reader, *args) -> np.ndarray:
+    rows, cols = ctypes.c_int64(), ctypes.c_int64()
+    _check(reader(*args, ctypes.byref(rows), ctypes.byref(cols), None, 0))
+    M = np.empty((rows.value, cols.value), order="F")
+    _check(reader(*args, ctypes.byref(rows), ctypes.byref(cols), _ptr(M), M.size))
+    return M
+
+
+def read_matrix(path: str) -> np.ndarray:
+    """read_matrix_file (io.hpp:256-260)."""
+    return _matrix_from(load_library().p2g_matrix_read, os.fsencode(path))
+
+
+def parse_matrix(text: str) -> np.ndarray:
+    """read_matrix_stream (io.hpp:218-254) on a string."""
+    data = text.encode()
+    return _matrix_from(load_library().p2g_matrix_parse, data, len(data))
+
+
+def write_factors(out_dir: str, X: "CSRTensor", H, V, S, Q, metadata: Optional[dict] = None) -> None:
+    """write_factors (io.hpp:270-305): V, S, H, U_k = Q_k H, manifest.json.
+    Q is the packed row-major (sum I_k) x R array (Context.fit's Q)."""
+    import json as _json
+    R = np.asarray(H).shape[0]
+    H, V, S = _f64(H), _f64(V), _f64(S)
+    Q = np.ascontiguousarray(Q, dtype=np.float64)
+    meta = _json.dumps(metadata) if metadata else None
+    _check(load_library().p2g_write_factors(os.fsencode(out_dir), X.K, X.J, R, _ptr(X.subj_row_ptr), _ptr(H),
+                                            _ptr(V), _ptr(S), _ptr(Q), meta.encode() if meta else None))
+
+
+def write_trace(path: str, iters, residual_sq, fit) -> None:
+    """write_trace_tsv (io.hpp:307-315): deterministic fields only."""
+    it = np.ascontiguousarray(iters, dtype=np.int32)
+    rs = np.ascontiguousarray(residual_sq, dtype=np.float64)
+    ft = np.ascontiguousarray(fit, dtype=np.float64)
+    _check(load_library().p2g_write_trace(os.fsencode(path), len(it), _ptr(it), _ptr(rs), _ptr(ft)))
+
+
+def format_value(v: float) -> str:
+    """io.hpp:55-60: 17 significant digits (round-trips exactly)."""
+    return "%.17g" % v
+
+
+def rank_components(S, subject: int, top_n: int):
+    """io.hpp:317-333: components of subject k by decreasing diag(S_k), ties
+    toward the lower index."""
+    S = np.asarray(S)
+    if subject < 0 or subject >= S.shape[0]:
+        raise DataError(f"subject index out of range: {subject}")
+    if top_n < 0 or top_n > S.shape[1]:
+        raise InvalidArgument("top_n must be between 0 and the rank")
+    order = sorted(range(S.shape[1]), key=lambda r: -S[subject, r])  # stable: ties keep index order
+    return [(r, float(S[subject, r])) for r in order[:top_n]]
 
 
 @dataclass

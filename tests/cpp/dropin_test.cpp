@@ -5,6 +5,7 @@
 #include <cmath>
 #include <cstdio>
 #include <functional>
+#include <sstream>
 #include <string>
 
 #include "parafac2/parafac2.hpp"
@@ -76,6 +77,43 @@ static double dense_residual(const IrregularTensor& x, const Parafac2Factors& f)
 }
 
 int main() {
+  // test_io.cpp:55-163, 212-222, 276-293 — ingest/export through io.hpp
+  {
+    auto parse = [](const std::string& t) {
+      std::istringstream in(t);
+      return parse_coordinate_stream(in);
+    };
+    ParsedTensor p = parse("2 3\n0 0 1 2.5\n1 0 0 1.0\n");
+    CHECK(p.tensor.n_slices() == 2 && p.tensor.slice(0).dense()(0, 1) == 2.5 && p.filtered_rows == 0);
+    CHECK(parse("1 3\n0 5 1 2.0\n").filtered_rows == 5);
+    bool msg_ok = false;
+    try {
+      parse("1 3\n0 0 5 1.0\n");
+    } catch (const DataError& e) {
+      msg_ok = std::string(e.what()).find("column index out of range at line 2") != std::string::npos;
+    }
+    CHECK(msg_ok);
+    CHECK(throws<DataError>([&] { parse(""); }));
+    auto t = IrregularTensor::from_slices(
+        3, {SparseSlice::from_triplets(2, 3, {{1, 2, 2.5}, {0, 0, 1.5}}), SparseSlice::from_triplets(1, 3, {{0, 1, -3.0}})});
+    std::ostringstream ser;
+    write_coordinate_stream(ser, t, {"demo"});
+    CHECK(ser.str() == "# demo\n2 3\n0 0 0 1.5\n0 1 2 2.5\n1 0 1 -3\n");
+    Matrix m = Matrix::FromRows(2, 2, {1.5, -3.0, 0.25, 100.0});
+    std::ostringstream ms;
+    write_matrix_stream(ms, m, "demo");
+    CHECK(ms.str() == "# demo\n2 2\n1.5 -3\n0.25 100\n");
+    std::istringstream mi(ms.str());
+    CHECK(read_matrix_stream(mi) == m);
+    FitTrace tr;
+    IterationStats a, b;
+    a.iter = 1, a.residual_sq = 2.5, a.fit = 0.5, a.ms_procrustes = 123.0;
+    b.iter = 2, b.residual_sq = 1.25, b.fit = 0.75;
+    tr.iterations = {a, b};
+    std::ostringstream ts;
+    write_trace_tsv(ts, tr);
+    CHECK(ts.str() == "iter\tresidual_sq\tfit\n1\t2.5\t0.5\n2\t1.25\t0.75\n");
+  }
   // test_mttkrp.cpp:36-101 — mode KATs
   {
     Matrix y = Matrix::FromRows(2, 2, {1, 0, 0, 2});
