@@ -303,30 +303,47 @@ void check_csr(std::int64_t K, std::int64_t J, const std::int64_t* srp, const st
   if (srp[K] > 0 && rp[srp[K]] > 0 && (!ci || !val)) throw InvalidArgument("invalid CSR tensor");
 }
 
-/// Canonical serialisation (io.hpp:179-195): subject ascending, then column,
-/// then row; values at 17 significant digits.
-void write_coordinate(std::ostream& out, std::int64_t K, std::int64_t J, const std::int64_t* srp,
-                      const std::int64_t* rp, const std::int32_t* ci, const double* val,
-                      const std::vector<std::string>& comments) {
-  for (const std::string& c : comments) out << "# " << c << '\n';
-  out << K << ' ' << J << '\n';
-  std::vector<std::int64_t> order;
-  for (std::int64_t k = 0; k < K; ++k) {
-    const std::int64_t r0 = srp[k], r1 = srp[k + 1];
+/// Canonical text of subjects [k0, k1) (io.hpp:179-195): subject ascending,
+/// then column, then row; values at 17 significant digits.
+void format_subjects(std::int64_t k0, std::int64_t k1, const std::int64_t* srp, const std::int64_t* rp,
+                     const std::int32_t* ci, const double* val, std::string& out) {
+  std::vector<std::int64_t> order, row_of;
+  char buf[96];
+  for (std::int64_t k = k0; k < k1; ++k) {
+    const std::int64_t r0 = srp[k], r1 = srp[k + 1], q0 = rp[r0];
     order.clear();
-    for (std::int64_t q = rp[r0]; q < rp[r1]; ++q) order.push_back(q);
-    // row of each entry: rows are contiguous ranges of q
-    std::vector<std::int64_t> row_of(order.size());
+    row_of.assign(static_cast<std::size_t>(rp[r1] - q0), 0);
     for (std::int64_t r = r0; r < r1; ++r)
-      for (std::int64_t q = rp[r]; q < rp[r + 1]; ++q) row_of[static_cast<std::size_t>(q - rp[r0])] = r - r0;
-    std::stable_sort(order.begin(), order.end(), [&](std::int64_t a, std::int64_t b) {
-      const std::int32_t ca = ci[a], cb = ci[b];
-      if (ca != cb) return ca < cb;
-      return row_of[static_cast<std::size_t>(a - rp[r0])] < row_of[static_cast<std::size_t>(b - rp[r0])];
+      for (std::int64_t q = rp[r]; q < rp[r + 1]; ++q) {
+        order.push_back(q);
+        row_of[static_cast<std::size_t>(q - q0)] = r - r0;
+      }
+    // rows ascend in CSR order, so a stable sort by column yields (column, row)
+    std::stable_sort(order.begin(), order.end(), [&](std::int64_t a, std::int64_t b) { return ci[a] < ci[b]; });
+    for (std::int64_t q : order) {
+      const int n = std::snprintf(buf, sizeof(buf), "%lld %lld %d %.17g\n", static_cast<long long>(k),
+                                  static_cast<long long>(row_of[static_cast<std::size_t>(q - q0)]), ci[q], val[q]);
+      out.append(buf, static_cast<std::size_t>(n));
+    }
+  }
+}
+
+void write_coordinate(std::FILE* f, std::int64_t K, std::int64_t J, const std::int64_t* srp, const std::int64_t* rp,
+                      const std::int32_t* ci, const double* val, const std::vector<std::string>& comments) {
+  std::string head;
+  for (const std::string& c : comments) head += "# " + c + "\n";
+  head += std::to_string(K) + " " + std::to_string(J) + "\n";
+  std::fwrite(head.data(), 1, head.size(), f);
+  // formatted in parallel by subject ranges, written in order
+  const int nt = pick_threads(0, static_cast<std::size_t>(rp[srp[K]]) * 24);
+  const std::int64_t step = std::max<std::int64_t>(1, std::min<std::int64_t>(K, 4096));
+  for (std::int64_t kb = 0; kb < K; kb += step * nt) {
+    std::vector<std::string> parts(static_cast<std::size_t>(nt));
+    run_parallel(nt, [&](int t) {
+      const std::int64_t a = std::min(K, kb + step * t), b = std::min(K, a + step);
+      format_subjects(a, b, srp, rp, ci, val, parts[static_cast<std::size_t>(t)]);
     });
-    for (std::int64_t q : order)
-      out << k << ' ' << row_of[static_cast<std::size_t>(q - rp[r0])] << ' ' << ci[q] << ' ' << format_value(val[q])
-          << '\n';
+    for (const std::string& p : parts) std::fwrite(p.data(), 1, p.size(), f);
   }
 }
 
@@ -419,9 +436,16 @@ extern "C" int p2g_coo_parse(const char* text, int64_t len, int32_t threads, p2g
 extern "C" int p2g_coo_read(const char* path, int32_t threads, p2g_csr** out) {
   return guarded([&] {
     if (!path || !out) throw InvalidArgument("null argument");
-    std::ifstream in(path, std::ios::binary);
-    if (!in) throw DataError(std::string("cannot open input file: ") + path);
-    std::string data((std::istreambuf_iterator<char>(in)), std::istreambuf_iterator<char>());
+    std::FILE* f = std::fopen(path, "rb");
+    if (!f) throw DataError(std::string("cannot open input file: ") + path);
+    std::vector<char> data;
+    std::fseek(f, 0, SEEK_END);
+    const long n = std::ftell(f);
+    std::fseek(f, 0, SEEK_SET);
+    data.resize(static_cast<std::size_t>(std::max(n, 0L)));
+    const std::size_t got = n > 0 ? std::fread(data.data(), 1, data.size(), f) : 0;
+    std::fclose(f);
+    if (got != data.size()) throw DataError(std::string("failed reading input file: ") + path);
     *out = parse_buffer(data.data(), data.size(), threads).release();
   });
 }
@@ -457,10 +481,11 @@ extern "C" int p2g_coo_write(const char* path, int64_t K, int64_t J, const int64
     check_csr(K, J, srp, rp, ci, val);
     std::vector<std::string> cm;
     for (int32_t c = 0; c < n_comments; ++c) cm.emplace_back(comments[c]);
-    std::ofstream out(path);
-    if (!out) throw DataError(std::string("cannot open output file: ") + path);
-    write_coordinate(out, K, J, srp, rp, ci, val, cm);
-    if (!out) throw DataError(std::string("failed writing output file: ") + path);
+    std::FILE* f = std::fopen(path, "wb");
+    if (!f) throw DataError(std::string("cannot open output file: ") + path);
+    write_coordinate(f, K, J, srp, rp, ci, val, cm);
+    const bool bad = std::ferror(f) != 0;
+    if (std::fclose(f) != 0 || bad) throw DataError(std::string("failed writing output file: ") + path);
   });
 }
 
