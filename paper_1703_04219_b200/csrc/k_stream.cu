@@ -47,7 +47,7 @@ struct StreamCfg {
   static constexpr int WPB = 4;
   static constexpr int kWarpT = RR * SBP;                     // doubles
   static constexpr int UM2 = 4;                               // rows per lane in flight (mode 2)
-  static constexpr int UM3 = 2;                               // rows per lane in flight (mode 3)
+  static constexpr int UM3 = 1;                               // rows per lane in flight (mode 3)
   static constexpr int NB = (R + 7) / 8;                      // 8 x 8 tensor tiles per side (mode 3)
   static constexpr int XS = NB == 1 ? 12 : 20;                // staged row stride: conflict-free fragments
   static constexpr int kWarpCh = 2 * 32 * UM3 * XS;           // doubles (mode 3: xn and q rows)
