@@ -5,6 +5,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <thread>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -493,6 +494,36 @@ extern "C" int p2g_destroy(p2g_ctx* c) {
   });
 }
 
+namespace p2g {
+namespace {
+/// Host threads for an O(n) pass: fixed by n (not by timing), so chunked
+/// reductions are reproducible on a given machine.
+int host_threads(std::int64_t n) {
+  const int hw = static_cast<int>(std::max(1u, std::thread::hardware_concurrency()));
+  return static_cast<int>(std::max<std::int64_t>(1, std::min<std::int64_t>(std::min(hw, 32), n / (1 << 20) + 1)));
+}
+template <typename Fn>
+void run_host_parallel(int n, Fn&& fn) {
+  if (n == 1) {
+    fn(0);
+    return;
+  }
+  std::vector<std::thread> ts;
+  for (int t = 0; t < n; ++t) ts.emplace_back([&fn, t] { fn(t); });
+  for (auto& th : ts) th.join();
+}
+__global__ void k_rebase(std::int64_t* a, std::int64_t n, std::int64_t off) {
+  for (std::int64_t i = static_cast<std::int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<std::int64_t>(gridDim.x) * blockDim.x)
+    a[i] -= off;
+}
+void launch_rebase(std::int64_t* a, std::int64_t n, std::int64_t off, cudaStream_t s) {
+  if (off == 0 || n == 0) return;
+  k_rebase<<<static_cast<int>(std::min<std::int64_t>((n + 255) / 256, 148 * 16)), 256, 0, s>>>(a, n, off);
+}
+}  // namespace
+}  // namespace p2g
+
 extern "C" int p2g_load_csr(p2g_ctx* c, int64_t K, int64_t J, const int64_t* srp, const int64_t* rp,
                             const int32_t* ci, const double* val) {
   return guarded([&] {
@@ -507,16 +538,39 @@ extern "C" int p2g_load_csr(p2g_ctx* c, int64_t K, int64_t J, const int64_t* srp
       if (srp[k + 1] < srp[k]) throw DataError("subj_row_ptr must be non-decreasing");
     const int64_t NRt = srp[K];
     if (rp[0] != 0) throw DataError("row_ptr must start at 0");
-    for (int64_t r = 0; r < NRt; ++r)
-      if (rp[r + 1] < rp[r]) throw DataError("row_ptr must be non-decreasing");
+    // Row pointers first (over all rows, as the serial check), then column
+    // range / ascending order within rows: both in parallel over fixed row
+    // ranges, the first failing range reports.
+    const int nthr = host_threads(NRt);
+    std::vector<int> bad(static_cast<std::size_t>(nthr), 0);
+    run_host_parallel(nthr, [&](int t) {
+      for (int64_t r = NRt * t / nthr; r < NRt * (t + 1) / nthr; ++r)
+        if (rp[r + 1] < rp[r]) {
+          bad[static_cast<std::size_t>(t)] = 1;
+          break;
+        }
+    });
+    for (int b : bad)
+      if (b) throw DataError("row_ptr must be non-decreasing");
     const int64_t nnz_t = rp[NRt];
     if (nnz_t > 0 && (!ci || !val)) throw InvalidArgument("null CSR arrays");
-    // Column range / ascending order within rows; non-zero values.
-    for (int64_t r = 0; r < NRt; ++r)
-      for (int64_t p = rp[r]; p < rp[r + 1]; ++p) {
-        if (ci[p] < 0 || ci[p] >= J) throw DataError("column index out of range");
-        if (p > rp[r] && ci[p] <= ci[p - 1]) throw DataError("column indices must be strictly ascending within a row");
-      }
+    run_host_parallel(nthr, [&](int t) {
+      for (int64_t r = NRt * t / nthr; r < NRt * (t + 1) / nthr && !bad[static_cast<std::size_t>(t)]; ++r)
+        for (int64_t p = rp[r]; p < rp[r + 1]; ++p) {
+          if (ci[p] < 0 || ci[p] >= J) {
+            bad[static_cast<std::size_t>(t)] = 2;
+            break;
+          }
+          if (p > rp[r] && ci[p] <= ci[p - 1]) {
+            bad[static_cast<std::size_t>(t)] = 3;
+            break;
+          }
+        }
+    });
+    for (int b : bad) {
+      if (b == 2) throw DataError("column index out of range");
+      if (b == 3) throw DataError("column indices must be strictly ascending within a row");
+    }
     // Shard by partition_weighted(nnz_k + I_k, world) (solver.hpp:263-267).
     std::vector<std::uint64_t> w(static_cast<std::size_t>(K));
     for (int64_t k = 0; k < K; ++k)
@@ -537,25 +591,36 @@ extern "C" int p2g_load_csr(p2g_ctx* c, int64_t K, int64_t J, const int64_t* srp
     c->nnz_total = nnz_t;
     c->max_rows = 0;
     for (int64_t k = c->k_begin; k < c->k_end; ++k) c->max_rows = std::max<std::int64_t>(c->max_rows, srp[k + 1] - srp[k]);
-    std::vector<std::int64_t> srp_s(static_cast<std::size_t>(c->k_end - c->k_begin + 1));
-    for (int64_t k = c->k_begin; k <= c->k_end; ++k) srp_s[static_cast<std::size_t>(k - c->k_begin)] = srp[k] - row0;
-    std::vector<std::int64_t> rp_s(static_cast<std::size_t>(c->NR + 1));
-    for (int64_t r = row0; r <= row1; ++r) rp_s[static_cast<std::size_t>(r - row0)] = rp[r] - nz0;
-    c->srp.resize(srp_s.size());
-    c->rp.resize(rp_s.size());
+    // Upload the shard as is and rebase row pointers on the device (the
+    // caller's buffers are read once; pinned ones copy at link speed).
+    c->srp.resize(static_cast<std::size_t>(c->k_end - c->k_begin + 1));
+    c->rp.resize(static_cast<std::size_t>(c->NR + 1));
     c->ci.resize(static_cast<std::size_t>(std::max<int64_t>(c->nnz, 1)));
     c->val.resize(static_cast<std::size_t>(std::max<int64_t>(c->nnz, 1)));
-    P2G_CUDA(cudaMemcpyAsync(c->srp.get(), srp_s.data(), sizeof(int64_t) * srp_s.size(), cudaMemcpyHostToDevice, c->stream));
-    P2G_CUDA(cudaMemcpyAsync(c->rp.get(), rp_s.data(), sizeof(int64_t) * rp_s.size(), cudaMemcpyHostToDevice, c->stream));
+    P2G_CUDA(cudaMemcpyAsync(c->srp.get(), srp + c->k_begin, sizeof(int64_t) * (c->k_end - c->k_begin + 1),
+                             cudaMemcpyHostToDevice, c->stream));
+    P2G_CUDA(cudaMemcpyAsync(c->rp.get(), rp + row0, sizeof(int64_t) * (c->NR + 1), cudaMemcpyHostToDevice, c->stream));
+    launch_rebase(c->srp.get(), c->k_end - c->k_begin + 1, row0, c->stream);
+    launch_rebase(c->rp.get(), c->NR + 1, nz0, c->stream);
     if (c->nnz > 0) {
       P2G_CUDA(cudaMemcpyAsync(c->ci.get(), ci + nz0, sizeof(int32_t) * c->nnz, cudaMemcpyHostToDevice, c->stream));
       P2G_CUDA(cudaMemcpyAsync(c->val.get(), val + nz0, sizeof(double) * c->nnz, cudaMemcpyHostToDevice, c->stream));
     }
     // ||X||_F^2 (sparse.hpp:219-223): slice order then entry order over all
     // subjects; the full host tensor is available on every rank.
-    double acc = 0.0;
-    for (int64_t p = 0; p < nnz_t; ++p) acc += val[p] * val[p];
-    c->norm_x = acc;
+    // fixed chunks summed in order: deterministic for a given thread count
+    {
+      const int nt = host_threads(nnz_t);
+      std::vector<double> part(static_cast<std::size_t>(nt), 0.0);
+      run_host_parallel(nt, [&](int t) {
+        double a = 0.0;
+        for (int64_t p = nnz_t * t / nt; p < nnz_t * (t + 1) / nt; ++p) a += val[p] * val[p];
+        part[static_cast<std::size_t>(t)] = a;
+      });
+      double acc = 0.0;
+      for (double v : part) acc += v;
+      c->norm_x = acc;
+    }
     P2G_CUDA(cudaStreamSynchronize(c->stream));
     build_csc(c);
     c->loaded = true;
