@@ -146,11 +146,12 @@ void upload_shard_rows(p2g_ctx* c, const double* host, std::int64_t total_rows, 
 
 /// Device row-major (rows x cols) -> host column-major.
 void download_colmajor(p2g_ctx* c, const double* dev, std::int64_t rows, std::int64_t cols, double* host) {
-  std::vector<double> tmp(static_cast<std::size_t>(rows * cols));
-  P2G_CUDA(cudaMemcpyAsync(tmp.data(), dev, sizeof(double) * rows * cols, cudaMemcpyDeviceToHost, c->stream));
+  // transpose on the device (row-major rows x cols viewed as column-major
+  // cols x rows), then one copy straight into the caller's buffer
+  c->stage.resize(static_cast<std::size_t>(std::max<std::int64_t>(rows * cols, 1)));
+  launch_transpose(dev, c->stage.get(), cols, rows, c->stream);
+  P2G_CUDA(cudaMemcpyAsync(host, c->stage.get(), sizeof(double) * rows * cols, cudaMemcpyDeviceToHost, c->stream));
   P2G_CUDA(cudaStreamSynchronize(c->stream));
-  for (std::int64_t i = 0; i < rows; ++i)
-    for (std::int64_t j = 0; j < cols; ++j) host[i + j * rows] = tmp[static_cast<std::size_t>(i * cols + j)];
 }
 
 void check_finite_host(const double* a, std::int64_t n, const char* what) {
