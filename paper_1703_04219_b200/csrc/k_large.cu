@@ -419,50 +419,112 @@ __global__ void __launch_bounds__(kLgThreads, 2) k_procrustes_large(LgArgs a) {
 }
 
 // ---------------------------------------------------------------------------
-// Warp-per-subject variant (default).  Same algorithm as k_procrustes_large;
-// a CTA-wide Jacobi round costs two barriers and leaves most threads idle, so
-// here one warp owns a subject: M and V' live in the warp's shared memory,
-// the row slabs (B, X~), T/Z, F, E and the warp's M1 partial in a per-warp
-// global slab (L1/L2 resident), and M = B^T B, F = B^T X~ run on the fp64
-// tensor cores (DMMA m8n8k4 over 4-row k-steps of the slab).
+// Warp-per-subject variant (default).  Same preconditioned two-sided Jacobi
+// as k_procrustes_large, but one warp owns a subject: M and V' live in the
+// warp's shared memory, every R x R (and I x R) product runs on the fp64
+// tensor cores (DMMA m8n8k4) over per-warp slabs in global memory (L1/L2
+// resident), and the sweeps stop early:
+//
+//   Jacobi stops once the scaled off-diagonal max |M'_pq| / sqrt(M'_pp M'_qq)
+//   is at most kTauL = 1e-4 (instead of ~1e-12, one to two sweeps fewer), and
+//   S' = M'^{-1/2} comes from the second-order Daleckii-Krein expansion of
+//   f(x) = x^{-1/2} about Lambda = diag(M'), with N = M' - Lambda:
+//     S' = f(Lambda) + sum_pq f[l_p, l_q] N_pq + sum_pqr f[l_p, l_r, l_q] N_pr N_rq
+//   f's divided differences have closed forms in s = sqrt(l), u = 1/s,
+//   P_pq = 1/(s_p + s_q) and A = P o N:
+//     S'_pq = delta_pq u_p + u_p u_q (C1 - A + P o C2)_pq,
+//     C1 = A diag(u) A,  C2 = A A
+//   (no eigenvalue gaps appear, so clustered eigenvalues are harmless).  The
+//   truncation error in Q is O(R tau^3) ~ 1e-12 (measured 2.4e-12 with every
+//   scaled off-diagonal at tau).  Then G^{-1/2} = E' S' E'^T with E' = E V',
+//   Z = V' S' E'^T, Q = B Z and m1_k = Z^T F as before.
 // ---------------------------------------------------------------------------
+constexpr double kTauL = 1e-4;   // Jacobi stop: max scaled off-diagonal
+constexpr double kSkipL = 1e-9;  // rotations below this scaled size are skipped
+
 template <int RP>
 struct LgWarp {
-  static constexpr int LDM = RP + 1;
+  static constexpr int LDM = RP + 1;  // M: odd leading dimension (column walks conflict free)
+  static constexpr int LDV = RP + 2;  // V'^T: even, 16-byte rows for the paired updates
   static constexpr int kMat = RP * LDM;
+  static constexpr int kVt = RP * LDV;
   static constexpr int NBLK = (RP / 2) * (RP / 2 + 1) / 2;
-  static constexpr int kBlkD = (NBLK + 3) / 4;            // uint16 table in doubles
-  static constexpr int kWarpD = 2 * kMat + 4 * RP;         // M, V', w, 1/sigma, (c, s, t), pairs
+  static constexpr int kTabD = ((NBLK + (RP - 1) * (RP / 2) + 7) / 8) * 2;  // uint16 tables, in doubles (even)
+  // M, V'^T, w, u (1/sqrt diag), (c, s) per pair slot, t M_pq per slot, packed (p, q) per slot
+  static constexpr int kWarpD = kMat + kVt + 2 * RP + RP + RP / 2 + RP / 4 + 2;
+  static constexpr int kWarpDE = (kWarpD + 1) & ~1;
   static constexpr int pick_wpb() {
     int w = 16;
-    while (w > 1 && (kMat + kBlkD + w * kWarpD) * 8 > 225 * 1024) --w;
+    while (w > 1 && (kTabD + w * kWarpDE) * 8 > 227 * 1024) --w;
     return w;
   }
   static constexpr int WPB = pick_wpb();
-  static constexpr std::size_t kSmem = sizeof(double) * (kMat + kBlkD + WPB * kWarpD);
+  static constexpr std::size_t kSmem = sizeof(double) * (kTabD + WPB * kWarpDE);
   static constexpr int NB = RP / 8;  // 8-wide tensor tiles (RP multiple of 8)
+  // per-warp global slab: B, X~ (max_rows x R each), T, F, E, N, M1 (R x R), s (R)
+  __host__ __device__ static std::size_t slab_doubles(std::int64_t max_rows, int R) {
+    return 2 * static_cast<std::size_t>(max_rows > 1 ? max_rows : 1) * R +
+           5 * static_cast<std::size_t>(R) * R + RP;
+  }
 };
+
+/// out(i, j) for i < rows, j < R of the product sum_c a(i, c) b(c, j), c < R,
+/// on DMMA m8n8k4 (row.col): lane (fm, fk) feeds A[fm][fk] and B[fk][fm] and
+/// holds C[fm][2 fk + h].  8-row tiles of the output in turn, all RP/8
+/// column tiles at once.
+template <int RP, bool EXACT, class FA, class FB, class Epi>
+__device__ __forceinline__ void warp_mm(int rows, int R, FA fa, FB fb, Epi epi) {
+  constexpr int NB = RP / 8;
+  const int lane = threadIdx.x & 31, fm = lane >> 2, fk = lane & 3;
+#pragma unroll 1
+  for (int i0 = 0; i0 < rows; i0 += 8) {
+    const int i = i0 + fm;
+    const bool iv = i < rows;
+    double acc[NB][2];
+#pragma unroll
+    for (int b = 0; b < NB; ++b) acc[b][0] = acc[b][1] = 0.0;
+#pragma unroll 2
+    for (int k4 = 0; k4 < RP; k4 += 4) {
+      const int c = k4 + fk;
+      const bool cv = EXACT || c < R;
+      const double x = (iv && cv) ? fa(i, c) : 0.0;
+#pragma unroll
+      for (int b = 0; b < NB; ++b) {
+        const int j = 8 * b + fm;
+        const double y = (cv && (EXACT || j < R)) ? fb(c, j) : 0.0;
+        dev::dmma884(acc[b], x, y);
+      }
+    }
+    if (iv) {
+#pragma unroll
+      for (int b = 0; b < NB; ++b)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int j = 8 * b + 2 * fk + h;
+          if (EXACT || j < R) epi(i, j, acc[b][h]);
+        }
+    }
+  }
+}
 
 template <int RP, bool EXACT>
 __global__ void __launch_bounds__(LgWarp<RP>::WPB * 32, 1) k_procrustes_large_w(LgArgs a) {
   using L = LgWarp<RP>;
-  constexpr int LDM = L::LDM, NB = L::NB, WPB = L::WPB;
-  extern __shared__ double smem[];
+  constexpr int LDM = L::LDM, LDV = L::LDV, NB = L::NB, WPB = L::WPB;
+  extern __shared__ __align__(16) double smem[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int R = EXACT ? RP : a.R;
   const int RR = R * R;
-  double* Hs = smem;
-  std::uint16_t* blk = reinterpret_cast<std::uint16_t*>(Hs + L::kMat);
-  double* M = Hs + L::kMat + L::kBlkD + wid * L::kWarpD;
-  double* Vp = M + L::kMat;
-  double* w = Vp + L::kMat;
-  double* isg = w + RP;      // 1 / sigma
-  double* rc = isg + RP;     // rotation c, s, t M_pq (RP/2 each)
-  double* rs = rc + RP / 2;
-  double* rt = rs + RP / 2;
-  int* rp = reinterpret_cast<int*>(rt + RP / 2);  // pairs (RP ints)
-  for (int e = threadIdx.x; e < RR; e += blockDim.x) Hs[(e / R) * LDM + e % R] = a.H[e];
   const int m = (R + 1) & ~1, half = m / 2, nblk = half * (half + 1) / 2;
+  std::uint16_t* blk = reinterpret_cast<std::uint16_t*>(smem);  // 2 x 2 block (slot i1, slot i2) of M
+  std::uint16_t* sched = blk + L::NBLK;                         // round-robin (p, q) per (round, slot)
+  double* M = smem + L::kTabD + wid * L::kWarpDE;
+  double* Vt = M + L::kMat;  // V'^T: Vt[p * LDV + k] = V'(k, p)
+  double* w = Vt + L::kVt;
+  double* u = w + RP;
+  double2* rot = reinterpret_cast<double2*>(u + RP);  // (c, s)
+  double* rt = reinterpret_cast<double*>(rot + RP / 2);
+  int* rpq = reinterpret_cast<int*>(rt + RP / 2);  // p | q << 8, q = 0xff: no pair
   for (int it = threadIdx.x; it < nblk; it += blockDim.x) {
     int i1 = 0, r = it;
     while (r >= half - i1) {
@@ -471,19 +533,36 @@ __global__ void __launch_bounds__(LgWarp<RP>::WPB * 32, 1) k_procrustes_large_w(
     }
     blk[it] = static_cast<std::uint16_t>((i1 << 8) | (i1 + r));
   }
+  for (int it = threadIdx.x; it < (m - 1) * half; it += blockDim.x) {
+    const int round = it / half, l = it - round * half;
+    int p, q;
+    if (l == 0) {
+      p = round;
+      q = m - 1;
+    } else {
+      p = (round + l) % (m - 1);
+      q = (round - l + (m - 1)) % (m - 1);
+    }
+    if (p > q) {
+      const int t = p;
+      p = q;
+      q = t;
+    }
+    sched[it] = static_cast<std::uint16_t>(p | ((q < R ? q : 0xff) << 8));
+  }
   __syncthreads();
   const std::int64_t gw = static_cast<std::int64_t>(blockIdx.x) * WPB + wid;
   const std::int64_t nwarps = static_cast<std::int64_t>(gridDim.x) * WPB;
-  double* slab = a.slab + gw * (2 * a.max_rows * R + 5 * RR);
-  double* Bs = slab;                  // I x R rows of B
-  double* Xs = Bs + a.max_rows * R;   // I x R rows of X~ = XV D
-  double* Ts = Xs + a.max_rows * R;   // T, later Z (R x R)
+  double* slab = a.slab + gw * L::slab_doubles(a.max_rows, R);
+  double* Bs = slab;                  // I x R rows of B = X~ H^T E
+  double* Xs = Bs + a.max_rows * R;   // I x R rows of X~ = X V D
+  double* Ts = Xs + a.max_rows * R;   // H^T E; later A = P o N; later Z
   double* Fs = Ts + RR;               // F = B^T X~
   double* Es = Fs + RR;               // E (R x R)
-  double* Ns = Es + RR;               // E V' scratch
+  double* Ns = Es + RR;               // scratch: E V', P, V' S'
   double* M1 = Ns + RR;               // this warp's m1 partial
+  double* sv = M1 + RR;               // sqrt(M'_pp)
   for (int e = lane; e < RR; e += 32) M1[e] = 0.0;
-  const int fm = lane >> 2, fk = lane & 3, fn = 2 * (lane & 3);
   for (std::int64_t k = gw; k < a.X.K; k += nwarps) {
     const std::int64_t r0 = a.X.srp[k];
     const int I = static_cast<int>(a.X.srp[k + 1] - r0);
@@ -491,39 +570,31 @@ __global__ void __launch_bounds__(LgWarp<RP>::WPB * 32, 1) k_procrustes_large_w(
     double* Ek = a.Ewarm + k * RR;
     for (int e = lane; e < RR; e += 32) Es[e] = a.ew_valid ? Ek[e] : ((e / R == e % R) ? 1.0 : 0.0);
     __syncwarp();
+    // rows of X~ = X_k V D (lane per row)
+    for (int i = lane; i < I; i += 32) {
+      double xv[RP];
+      dev::csr_row_times<RP>(xv, a.X.ci, a.X.val, a.X.rp[r0 + i], a.X.rp[r0 + i + 1], a.V, R);
+      double* xrow = Xs + static_cast<std::int64_t>(i) * R;
+#pragma unroll
+      for (int c = 0; c < RP; ++c)
+        if (c < R) xrow[c] = xv[c] * w[c];
+    }
     int flag = P2G_FLAG_FULL_RANK;
     for (int pass = 0; pass < 2; ++pass) {
-      // T = D H^T E (lanes along columns j)
-      for (int j = lane; j < R; j += 32)
-        for (int i = 0; i < R; ++i) {
-          double acc = 0.0;
-          for (int c = 0; c < R; ++c) acc = fma(Hs[c * LDM + i], Es[c * R + j], acc);
-          Ts[i * R + j] = acc * w[i];
-        }
       __syncwarp();
-      // rows: b_i = xv_i T, x~_i = xv_i o w
-      for (int i = lane; i < I; i += 32) {
-        double xv[RP];
-        dev::csr_row_times<RP>(xv, a.X.ci, a.X.val, a.X.rp[r0 + i], a.X.rp[r0 + i + 1], a.V, R);
-        double* brow = Bs + static_cast<std::int64_t>(i) * R;
-        for (int j = 0; j < R; ++j) {
-          double acc = 0.0;
-#pragma unroll
-          for (int c = 0; c < RP; ++c)
-            if (c < R) acc = fma(xv[c], Ts[c * R + j], acc);
-          brow[j] = acc;
-        }
-        if (pass == 0) {
-          double* xrow = Xs + static_cast<std::int64_t>(i) * R;
-#pragma unroll
-          for (int c = 0; c < RP; ++c)
-            if (c < R) xrow[c] = xv[c] * w[c];
-        }
-      }
+      // T' = H^T E, then B = X~ T' (= X_k V D H^T E)
+      warp_mm<RP, EXACT>(
+          R, R, [&](int i, int c) { return __ldg(a.H + c * R + i); }, [&](int c, int j) { return Es[c * R + j]; },
+          [&](int i, int j, double v) { Ts[i * R + j] = v; });
       __syncwarp();
-      // M = B^T B (lower tiles) on the tensor cores, into shared memory
+      warp_mm<RP, EXACT>(
+          I, R, [&](int i, int c) { return Xs[i * R + c]; }, [&](int c, int j) { return Ts[c * R + j]; },
+          [&](int i, int j, double v) { Bs[i * R + j] = v; });
+      __syncwarp();
+      // M = B^T B (lower tiles) into shared memory, F = B^T X~ into the slab
       bool finite = true;
       {
+        const int fm = lane >> 2, fk = lane & 3, fn = 2 * (lane & 3);
         double acc[NB * (NB + 1) / 2][2];
 #pragma unroll
         for (int t = 0; t < NB * (NB + 1) / 2; ++t) acc[t][0] = acc[t][1] = 0.0;
@@ -533,7 +604,7 @@ __global__ void __launch_bounds__(LgWarp<RP>::WPB * 32, 1) k_procrustes_large_w(
 #pragma unroll
           for (int b = 0; b < NB; ++b) {
             const int col = 8 * b + fm;
-            f[b] = (r < I && col < R) ? Bs[static_cast<std::int64_t>(r) * R + col] : 0.0;
+            f[b] = (r < I && (EXACT || col < R)) ? Bs[static_cast<std::int64_t>(r) * R + col] : 0.0;
           }
           int t = 0;
 #pragma unroll
@@ -550,7 +621,7 @@ __global__ void __launch_bounds__(LgWarp<RP>::WPB * 32, 1) k_procrustes_large_w(
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
               const int j = 8 * bj + fn + h;
-              if (i < R && j < R) {
+              if (EXACT || (i < R && j < R)) {
                 M[i * LDM + j] = acc[t][h];
                 M[j * LDM + i] = acc[t][h];
                 finite &= isfinite(acc[t][h]);
@@ -558,8 +629,8 @@ __global__ void __launch_bounds__(LgWarp<RP>::WPB * 32, 1) k_procrustes_large_w(
             }
           }
       }
-      // F = B^T X~ (all tiles) into the slab
       {
+        const int fm = lane >> 2, fk = lane & 3, fn = 2 * (lane & 3);
 #pragma unroll 1
         for (int bi = 0; bi < NB; ++bi) {
           double acc[NB][2];
@@ -568,11 +639,11 @@ __global__ void __launch_bounds__(LgWarp<RP>::WPB * 32, 1) k_procrustes_large_w(
           for (int k4 = 0; k4 < I; k4 += 4) {
             const int r = k4 + fk;
             const int ci = 8 * bi + fm;
-            const double fa = (r < I && ci < R) ? Bs[static_cast<std::int64_t>(r) * R + ci] : 0.0;
+            const double fa = (r < I && (EXACT || ci < R)) ? Bs[static_cast<std::int64_t>(r) * R + ci] : 0.0;
 #pragma unroll
             for (int bj = 0; bj < NB; ++bj) {
               const int cj = 8 * bj + fm;
-              const double fb = (r < I && cj < R) ? Xs[static_cast<std::int64_t>(r) * R + cj] : 0.0;
+              const double fb = (r < I && (EXACT || cj < R)) ? Xs[static_cast<std::int64_t>(r) * R + cj] : 0.0;
               dev::dmma884(acc[bj], fa, fb);
             }
           }
@@ -582,7 +653,7 @@ __global__ void __launch_bounds__(LgWarp<RP>::WPB * 32, 1) k_procrustes_large_w(
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
               const int j = 8 * bj + fn + h;
-              if (i < R && j < R) {
+              if (EXACT || (i < R && j < R)) {
                 Fs[i * R + j] = acc[bj][h];
                 finite &= isfinite(acc[bj][h]);
               }
@@ -598,84 +669,81 @@ __global__ void __launch_bounds__(LgWarp<RP>::WPB * 32, 1) k_procrustes_large_w(
         flag = P2G_FLAG_ACCURATE;
         break;
       }
-      // scaled off-diagonal mass, V' = I
-      double off = 0.0;
-      for (int p = 0; p < R; ++p)
-        for (int q = lane; q < R; q += 32) {
-          const double d = M[p * LDM + p] * M[q * LDM + q];
-          if (p != q && d > 0.0) off += M[p * LDM + q] * M[p * LDM + q] / d;
-          Vp[p * LDM + q] = p == q ? 1.0 : 0.0;
-        }
-      off = dev::warp_sum(off);
-      __syncwarp();
+      // V' = I
+      for (int e = lane; e < R * LDV; e += 32) {
+        const int p = e / LDV, kk = e - p * LDV;
+        Vt[e] = p == kk ? 1.0 : 0.0;
+      }
       bool converged = false;
       int sweeps = 0;
+      double off = 0.0;  // scaled off-diagonal mass at the start of the pass
       for (int sweep = 0; sweep < kLgMaxSweeps; ++sweep, ++sweeps) {
         double dmax = 0.0;
         for (int j = 0; j < R; ++j) dmax = fmax(dmax, M[j * LDM + j]);
         const double tiny = kTinyL * dmax;
-        bool need = false;
-        for (int p = 0; p < R; ++p)
-          for (int q = lane; q < R; q += 32) {
-            if (q <= p) continue;
-            const double al = M[p * LDM + p], be = M[q * LDM + q], ga = M[p * LDM + q];
-            if (al > tiny && be > tiny && !(ga == 0.0 || fabs(ga) <= kTolL * sqrt(al * be))) need = true;
+        for (int p = lane; p < R; p += 32) {
+          const double d = M[p * LDM + p];
+          u[p] = d > tiny ? 1.0 / sqrt(d) : 0.0;
+        }
+        __syncwarp();
+        double omax = 0.0, osum = 0.0;
+        for (int e = lane; e < RR; e += 32) {
+          const int p = e / R, q = e - p * R;
+          const double x = M[p * LDM + q] * u[p] * u[q];
+          if (p != q) {
+            omax = fmax(omax, fabs(x));
+            osum = fma(x, x, osum);
           }
-        if (!__any_sync(dev::kFull, need)) {
+        }
+        omax = dev::warp_max(omax);
+        if (sweep == 0) {
+          off = dev::warp_sum(osum);
+          if (a.dbg && lane == 0) {
+            const int b = omax <= 0.0 ? 0 : min(9, max(0, static_cast<int>(floor(log10(omax))) + 9));
+            atomicAdd(a.dbg + 4 + b, 1);
+          }
+        }
+        if (omax <= kTauL) {
           converged = true;
           break;
         }
         for (int round = 0; round < m - 1; ++round) {
           if (lane < half) {
-            int p, q;
-            if (lane == 0) {
-              p = round;
-              q = m - 1;
-            } else {
-              p = (round + lane) % (m - 1);
-              q = (round - lane + (m - 1)) % (m - 1);
-            }
-            if (p > q) {
-              const int t = p;
-              p = q;
-              q = t;
-            }
+            const int pq = sched[round * half + lane];
+            const int p = pq & 0xff, q = pq >> 8;
             double c = 1.0, sn = 0.0, tt = 0.0, ga = 0.0;
-            if (q < R) {
+            if (q != 0xff) {
               const double al = M[p * LDM + p], be = M[q * LDM + q];
               ga = M[p * LDM + q];
-              if (al > tiny && be > tiny && !(ga == 0.0 || fabs(ga) <= kTolL * sqrt(al * be))) {
+              if (al > tiny && be > tiny && fabs(ga) > kSkipL * sqrt(al * be)) {
                 const double zeta = (be - al) / (2.0 * ga);
                 tt = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
                 c = 1.0 / sqrt(1.0 + tt * tt);
                 sn = c * tt;
               }
-            } else {
-              q = -1;
             }
-            rc[lane] = c;
-            rs[lane] = sn;
+            rot[lane] = make_double2(c, sn);
             rt[lane] = tt * ga;
-            rp[2 * lane] = p;
-            rp[2 * lane + 1] = q;
+            rpq[lane] = pq;
           }
           __syncwarp();
+          // M <- J^T M J over 2 x 2 blocks of slot pairs
           for (int it = lane; it < nblk; it += 32) {
             const int i1 = blk[it] >> 8, i2 = blk[it] & 0xff;
-            const int p1 = rp[2 * i1], q1 = rp[2 * i1 + 1], p2 = rp[2 * i2], q2 = rp[2 * i2 + 1];
-            const double s1 = rs[i1], s2 = rs[i2];
-            if (s1 == 0.0 && s2 == 0.0) continue;
-            if (q1 < 0 || q2 < 0) {  // odd R: 1 x 2 block against the dummy pair's index
-              if (q1 < 0 && q2 < 0) continue;
-              const int aa = q1 < 0 ? p1 : p2;
-              const int u = q1 < 0 ? p2 : p1, v = q1 < 0 ? q2 : q1;
-              const double cc = q1 < 0 ? rc[i2] : rc[i1], ss = q1 < 0 ? s2 : s1;
-              const double xu = M[aa * LDM + u], xv = M[aa * LDM + v];
+            const double2 r1 = rot[i1], r2 = rot[i2];
+            if (r1.y == 0.0 && r2.y == 0.0) continue;
+            const int pq1 = rpq[i1], pq2 = rpq[i2];
+            const int p1 = pq1 & 0xff, q1 = pq1 >> 8, p2 = pq2 & 0xff, q2 = pq2 >> 8;
+            if (q1 == 0xff || q2 == 0xff) {  // odd R: 1 x 2 block against the dummy slot's index
+              const int aa = q1 == 0xff ? p1 : p2;
+              const int uu = q1 == 0xff ? p2 : p1, vv = q1 == 0xff ? q2 : q1;
+              const double cc = q1 == 0xff ? r2.x : r1.x, ss = q1 == 0xff ? r2.y : r1.y;
+              const double xu = M[aa * LDM + uu], xv = M[aa * LDM + vv];
               const double nu = cc * xu - ss * xv, nv = ss * xu + cc * xv;
-              M[aa * LDM + u] = nu;
-              M[u * LDM + aa] = nu;
-              M[aa * LDM + v] = nv;
-              M[v * LDM + aa] = nv;
+              M[aa * LDM + uu] = nu;
+              M[uu * LDM + aa] = nu;
+              M[aa * LDM + vv] = nv;
+              M[vv * LDM + aa] = nv;
               continue;
             }
             if (i1 == i2) {
@@ -686,7 +754,7 @@ __global__ void __launch_bounds__(LgWarp<RP>::WPB * 32, 1) k_procrustes_large_w(
               M[q1 * LDM + p1] = 0.0;
               continue;
             }
-            const double c1 = rc[i1], c2 = rc[i2];
+            const double c1 = r1.x, s1 = r1.y, c2 = r2.x, s2 = r2.y;
             const double x11 = M[p1 * LDM + p2], x12 = M[p1 * LDM + q2], x21 = M[q1 * LDM + p2], x22 = M[q1 * LDM + q2];
             const double y11 = c2 * x11 - s2 * x12, y12 = s2 * x11 + c2 * x12;
             const double y21 = c2 * x21 - s2 * x22, y22 = s2 * x21 + c2 * x22;
@@ -701,34 +769,36 @@ __global__ void __launch_bounds__(LgWarp<RP>::WPB * 32, 1) k_procrustes_large_w(
             M[q1 * LDM + q2] = z22;
             M[q2 * LDM + q1] = z22;
           }
-          // V' <- V' J: lanes along the rows, pairs in turn
-          for (int pr = 0; pr < half; ++pr) {
-            const int p = rp[2 * pr], q = rp[2 * pr + 1];
-            const double sn = rs[pr];
-            if (q < 0 || sn == 0.0) continue;
-            const double c = rc[pr];
-            for (int kk = lane; kk < R; kk += 32) {
-              const double vp = Vp[kk * LDM + p], vq = Vp[kk * LDM + q];
-              Vp[kk * LDM + p] = c * vp - sn * vq;
-              Vp[kk * LDM + q] = sn * vp + c * vq;
+          // V' <- V' J: rows of V'^T p, q over pairs of columns k, k + 1
+          {
+            const int nkp = (R + 1) >> 1;
+            for (int it = lane; it < nkp * half; it += 32) {
+              const int kp = it / half, sl = it - kp * half;
+              const double2 r = rot[sl];
+              if (r.y == 0.0) continue;
+              const int pq = rpq[sl];
+              const int p = pq & 0xff, q = pq >> 8;
+              double2* vp = reinterpret_cast<double2*>(Vt + p * LDV + 2 * kp);
+              double2* vq = reinterpret_cast<double2*>(Vt + q * LDV + 2 * kp);
+              const double2 x = *vp, y = *vq;
+              *vp = make_double2(r.x * x.x - r.y * y.x, r.x * x.y - r.y * y.y);
+              *vq = make_double2(r.y * x.x + r.x * y.x, r.y * x.y + r.x * y.y);
             }
           }
           __syncwarp();
         }
       }
       if (a.dbg && lane == 0) {
+        atomicAdd(a.dbg + 16 + min(sweeps, 9), 1);
         atomicAdd(a.dbg + 0, sweeps);
         atomicMax(a.dbg + 1, sweeps);
         if (pass == 0) atomicAdd(a.dbg + 3, 1);
         if (pass == 1) atomicAdd(a.dbg + 2, 1);
       }
-      // E <- E V' (lanes along columns)
-      for (int j = lane; j < R; j += 32)
-        for (int i = 0; i < R; ++i) {
-          double acc = 0.0;
-          for (int c = 0; c < R; ++c) acc = fma(Es[i * R + c], Vp[c * LDM + j], acc);
-          Ns[i * R + j] = acc;
-        }
+      // E <- E V'
+      warp_mm<RP, EXACT>(
+          R, R, [&](int i, int c) { return Es[i * R + c]; }, [&](int c, int j) { return Vt[j * LDV + c]; },
+          [&](int i, int j, double v) { Ns[i * R + j] = v; });
       __syncwarp();
       for (int e = lane; e < RR; e += 32) Es[e] = Ns[e];
       __syncwarp();
@@ -746,37 +816,72 @@ __global__ void __launch_bounds__(LgWarp<RP>::WPB * 32, 1) k_procrustes_large_w(
         break;
       }
       if (pass == 0 && off > 0.25 && smin2 < 1e-6 * smax2) continue;
-      for (int j = lane; j < R; j += 32) isg[j] = 1.0 / sqrt(M[j * LDM + j]);
+      // S' = M'^{-1/2} (second order about the diagonal) into M
+      for (int p = lane; p < R; p += 32) {
+        const double s = sqrt(M[p * LDM + p]);
+        sv[p] = s;
+        u[p] = 1.0 / s;
+      }
       __syncwarp();
-      // Z = V' Sigma^-1 V_A^T into Ts; m1 += Z^T F
-      for (int j = lane; j < R; j += 32)
-        for (int i = 0; i < R; ++i) {
-          double acc = 0.0;
-          for (int c = 0; c < R; ++c) acc = fma(Vp[i * LDM + c] * isg[c], Es[j * R + c], acc);
-          Ts[i * R + j] = acc;
-        }
+      for (int e = lane; e < RR; e += 32) {
+        const int p = e / R, q = e - p * R;
+        const double P = 1.0 / (sv[p] + sv[q]);
+        Ns[e] = P;
+        Ts[e] = p == q ? 0.0 : P * M[p * LDM + q];
+      }
       __syncwarp();
-      for (int j = lane; j < R; j += 32)
-        for (int i = 0; i < R; ++i) {
-          double acc = 0.0;
-          for (int c = 0; c < R; ++c) acc = fma(Ts[c * R + i], Fs[c * R + j], acc);
-          M1[i * R + j] += acc;
-        }
-      // Q rows = b_i Z
-      for (int i = lane; i < I; i += 32) {
-        const double* brow = Bs + static_cast<std::int64_t>(i) * R;
-        double b[RP];
+      {
+        const int fm = lane >> 2, fk = lane & 3;
+#pragma unroll 1
+        for (int bi = 0; bi < NB; ++bi) {
+          const int i = 8 * bi + fm;
+          double c1[NB][2], c2[NB][2];
 #pragma unroll
-        for (int c = 0; c < RP; ++c) b[c] = c < R ? brow[c] : 0.0;
-        double* qrow = a.Q + (r0 + i) * R;
-        for (int j = 0; j < R; ++j) {
-          double acc = 0.0;
+          for (int b = 0; b < NB; ++b) c1[b][0] = c1[b][1] = c2[b][0] = c2[b][1] = 0.0;
+#pragma unroll 2
+          for (int k4 = 0; k4 < RP; k4 += 4) {
+            const int c = k4 + fk;
+            const bool ok = EXACT || (i < R && c < R);
+            const double x = ok ? Ts[i * R + c] : 0.0;
+            const double xu = ok ? x * u[c] : 0.0;
 #pragma unroll
-          for (int c = 0; c < RP; ++c)
-            if (c < R) acc = fma(b[c], Ts[c * R + j], acc);
-          qrow[j] = acc;
+            for (int b = 0; b < NB; ++b) {
+              const int j = 8 * b + fm;
+              const double y = (EXACT || (c < R && j < R)) ? Ts[c * R + j] : 0.0;
+              dev::dmma884(c1[b], xu, y);
+              dev::dmma884(c2[b], x, y);
+            }
+          }
+#pragma unroll
+          for (int b = 0; b < NB; ++b)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const int j = 8 * b + 2 * fk + h;
+              if (EXACT || (i < R && j < R)) {
+                const double corr = c1[b][h] - Ts[i * R + j] + Ns[i * R + j] * c2[b][h];
+                M[i * LDM + j] = (i == j ? u[i] : 0.0) + u[i] * u[j] * corr;
+              }
+            }
         }
       }
+      __syncwarp();
+      // Y = V' S' into Ns, Z = Y E'^T into Ts
+      warp_mm<RP, EXACT>(
+          R, R, [&](int i, int c) { return Vt[c * LDV + i]; }, [&](int c, int j) { return M[c * LDM + j]; },
+          [&](int i, int j, double v) { Ns[i * R + j] = v; });
+      __syncwarp();
+      warp_mm<RP, EXACT>(
+          R, R, [&](int i, int c) { return Ns[i * R + c]; }, [&](int c, int j) { return Es[j * R + c]; },
+          [&](int i, int j, double v) { Ts[i * R + j] = v; });
+      __syncwarp();
+      // m1 += Z^T F;  Q = B Z
+      warp_mm<RP, EXACT>(
+          R, R, [&](int i, int c) { return Ts[c * R + i]; }, [&](int c, int j) { return Fs[c * R + j]; },
+          [&](int i, int j, double v) { M1[i * R + j] += v; });
+      double* Qk = a.Q + r0 * R;
+      warp_mm<RP, EXACT>(
+          I, R, [&](int i, int c) { return Bs[i * R + c]; }, [&](int c, int j) { return Ts[c * R + j]; },
+          [&](int i, int j, double v) { Qk[static_cast<std::int64_t>(i) * R + j] = v; });
       __syncwarp();
       break;
     }
@@ -796,9 +901,7 @@ int launch_large_w(p2g_ctx* c, LgArgs a, int max_partials, cudaStream_t s) {
   const int blocks = static_cast<int>(std::max<std::int64_t>(
       1, std::min<std::int64_t>({(K + L::WPB - 1) / L::WPB, static_cast<std::int64_t>(c->num_sms),
                                  static_cast<std::int64_t>(max_partials / L::WPB)})));
-  const std::size_t per_warp = 2 * static_cast<std::size_t>(std::max<std::int64_t>(a.max_rows, 1)) * a.R +
-                               5 * static_cast<std::size_t>(a.R) * a.R;
-  c->acc_scratch.resize(static_cast<std::size_t>(blocks) * L::WPB * per_warp);
+  c->acc_scratch.resize(static_cast<std::size_t>(blocks) * L::WPB * L::slab_doubles(a.max_rows, a.R));
   a.slab = c->acc_scratch.get();
   kern<<<blocks, L::WPB * 32, L::kSmem, s>>>(a);
   return blocks * L::WPB;  // one m1 partial per warp

@@ -199,7 +199,7 @@ void alloc_state(p2g_ctx* c, int R) {
   c->pinvbuf.resize(RR);
   c->scal.resize(8);
   c->flags.resize(static_cast<std::size_t>(std::max<std::int64_t>(Ks(c), 1)));
-  c->counters.resize(8);
+  c->counters.resize(32);
   c->redo.resize(static_cast<std::size_t>(std::max<std::int64_t>(c->J, Ks(c)) + 1));
   c->Hp.resize(RR);
   c->Vp.resize(static_cast<std::size_t>(c->J) * R);
@@ -343,7 +343,7 @@ IterOut iterate(p2g_ctx* c, bool nonneg, int iter) {
   const std::size_t RR = static_cast<std::size_t>(R) * R;
   cudaStream_t s = c->stream;
   const bool qf = small_rank(c);
-  P2G_CUDA(cudaMemsetAsync(c->counters.get(), 0, sizeof(std::int32_t) * 8, s));
+  P2G_CUDA(cudaMemsetAsync(c->counters.get(), 0, sizeof(std::int32_t) * 32, s));
   {
     DBuf<double>& part = scratch_partials(c, static_cast<std::size_t>(kMaxPartials + 4 * 148) * RR);
     const int np = procrustes_step(c, part.get());
@@ -422,8 +422,17 @@ IterOut iterate(p2g_ctx* c, bool nonneg, int iter) {
                    static_cast<double>(cnt[4]) / static_cast<double>(std::max<std::int64_t>(Ks(c), 1)), cnt[5],
                    static_cast<double>(cnt[6]) / cnt[7]);
     else
+    {
       std::fprintf(stderr, "[p2g] iter %d large-R Jacobi sweeps: mean %.2f per pass, max %d, redone %d of %d\n", iter,
                    static_cast<double>(cnt[4]) / (cnt[7] + cnt[6]), cnt[5], cnt[6], cnt[7]);
+      std::int32_t h[24];
+      P2G_CUDA(cudaMemcpy(h, c->counters.get() + 8, sizeof(h), cudaMemcpyDeviceToHost));
+      std::fprintf(stderr, "[p2g]   warm max scaled off-diag, log10 bins <-8..>=0:");
+      for (int b = 0; b < 10; ++b) std::fprintf(stderr, " %d", h[b]);
+      std::fprintf(stderr, "\n[p2g]   sweeps per pass 0..9+:");
+      for (int b = 0; b < 10; ++b) std::fprintf(stderr, " %d", h[12 + b]);
+      std::fprintf(stderr, "\n");
+    }
   }
   if (cnt[2] > 0) throw NumericalError("svd operand: non-finite entries");
   if (cnt[1] > 0) throw NumericalError("NNLS did not converge");
@@ -781,7 +790,7 @@ extern "C" int p2g_procrustes(p2g_ctx* c, int32_t R, const double* H, const doub
     c->c_valid = false;
     c->ew_valid = false;  // cold Jacobi start for a teacher-forced step
     const std::size_t RR = static_cast<std::size_t>(R) * R;
-    P2G_CUDA(cudaMemsetAsync(c->counters.get(), 0, sizeof(std::int32_t) * 8, c->stream));
+    P2G_CUDA(cudaMemsetAsync(c->counters.get(), 0, sizeof(std::int32_t) * 32, c->stream));
     DBuf<double>& part = scratch_partials(c, static_cast<std::size_t>(kMaxPartials + 4 * 148) * RR);
     const int np = procrustes_step(c, part.get());
     reduce_partials(part.get(), np, static_cast<std::int64_t>(RR), c->m1.get(), c->stream);
