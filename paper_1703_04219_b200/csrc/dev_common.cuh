@@ -42,6 +42,16 @@ __device__ __forceinline__ double rsqrt_nr(double x) {
   return y;
 }
 
+/// 1/x for normal x without the IEEE division sequence: the MUFU
+/// approximation refined by two Newton steps, y <- y (2 - x y).
+__device__ __forceinline__ double rcp_nr(double x) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  y = y * fma(-x, y, 2.0);
+  y = y * fma(-x, y, 2.0);
+  return y;
+}
+
 template <int RP>
 __device__ __forceinline__ void axpy_row(double (&acc)[RP], const double* __restrict__ vrow, double a, int R) {
 #pragma unroll

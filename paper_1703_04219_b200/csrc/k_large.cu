@@ -440,7 +440,7 @@ __global__ void __launch_bounds__(kLgThreads, 2) k_procrustes_large(LgArgs a) {
 //   Z = V' S' E'^T, Q = B Z and m1_k = Z^T F as before.
 // ---------------------------------------------------------------------------
 constexpr double kTauL = 1e-4;   // Jacobi stop: max scaled off-diagonal
-constexpr double kSkipL = 1e-9;  // rotations below this scaled size are skipped
+constexpr double kSkipL = 1e-6;  // rotations below this scaled size are skipped (threshold Jacobi)
 
 template <int RP>
 struct LgWarp {
@@ -450,8 +450,8 @@ struct LgWarp {
   static constexpr int kVt = RP * LDV;
   static constexpr int NBLK = (RP / 2) * (RP / 2 + 1) / 2;
   static constexpr int kTabD = ((NBLK + (RP - 1) * (RP / 2) + 7) / 8) * 2;  // uint16 tables, in doubles (even)
-  // M, V'^T, w, u (1/sqrt diag), (c, s) per pair slot, t M_pq per slot, packed (p, q) per slot
-  static constexpr int kWarpD = kMat + kVt + 2 * RP + RP + RP / 2 + RP / 4 + 2;
+  // M, V'^T, w, u (1/sqrt diag), (c, s) per pair slot, t M_pq per slot, int4 offsets per slot
+  static constexpr int kWarpD = kMat + kVt + 2 * RP + RP + RP / 2 + RP;
   static constexpr int kWarpDE = (kWarpD + 1) & ~1;
   static constexpr int pick_wpb() {
     int w = 16;
@@ -524,7 +524,7 @@ __global__ void __launch_bounds__(LgWarp<RP>::WPB * 32, 1) k_procrustes_large_w(
   double* u = w + RP;
   double2* rot = reinterpret_cast<double2*>(u + RP);  // (c, s)
   double* rt = reinterpret_cast<double*>(rot + RP / 2);
-  int* rpq = reinterpret_cast<int*>(rt + RP / 2);  // p | q << 8, q = 0xff: no pair
+  int4* ofs = reinterpret_cast<int4*>(rt + RP / 2);  // per slot: p LDM, q LDM, p, q (q < 0: no pair)
   for (int it = threadIdx.x; it < nblk; it += blockDim.x) {
     int i1 = 0, r = it;
     while (r >= half - i1) {
@@ -543,14 +543,31 @@ __global__ void __launch_bounds__(LgWarp<RP>::WPB * 32, 1) k_procrustes_large_w(
       p = (round + l) % (m - 1);
       q = (round - l + (m - 1)) % (m - 1);
     }
-    if (p > q) {
-      const int t = p;
-      p = q;
-      q = t;
-    }
+    // no p < q swap: slots l of a round then touch the consecutive indices
+    // round + l and round - l, so the lanes of a block row hit consecutive
+    // shared-memory words (conflict-free); the rotation is symmetric in p, q
     sched[it] = static_cast<std::uint16_t>(p | ((q < R ? q : 0xff) << 8));
   }
   __syncthreads();
+  // this lane's share of every round: 2 x 2 blocks (slot i1 | i2 << 8) of M
+  // and (slot | column offset << 8) items of V'^T, fixed for the whole kernel
+  constexpr int kLaneBlk = (L::NBLK + 31) / 32;
+  constexpr int kLaneVit = ((RP / 2) * (RP / 2) + 31) / 32;
+  int lblk[kLaneBlk], lvit[kLaneVit];
+#pragma unroll
+  for (int j = 0; j < kLaneBlk; ++j) {
+    const int it = lane + 32 * j;
+    lblk[j] = it < nblk ? ((blk[it] >> 8) | ((blk[it] & 0xff) << 8)) : -1;
+  }
+  {
+    const int nkp = (R + 1) >> 1;
+#pragma unroll
+    for (int j = 0; j < kLaneVit; ++j) {
+      const int it = lane + 32 * j;
+      const int sl = it / nkp, kp = it - sl * nkp;  // consecutive lanes: consecutive 16-byte units of a row
+      lvit[j] = it < nkp * half ? (sl | ((2 * kp) << 8)) : -1;
+    }
+  }
   const std::int64_t gw = static_cast<std::int64_t>(blockIdx.x) * WPB + wid;
   const std::int64_t nwarps = static_cast<std::int64_t>(gridDim.x) * WPB;
   double* slab = a.slab + gw * L::slab_doubles(a.max_rows, R);
@@ -715,75 +732,82 @@ __global__ void __launch_bounds__(LgWarp<RP>::WPB * 32, 1) k_procrustes_large_w(
             if (q != 0xff) {
               const double al = M[p * LDM + p], be = M[q * LDM + q];
               ga = M[p * LDM + q];
-              if (al > tiny && be > tiny && fabs(ga) > kSkipL * sqrt(al * be)) {
-                const double zeta = (be - al) / (2.0 * ga);
-                tt = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-                c = 1.0 / sqrt(1.0 + tt * tt);
+              if (al > tiny && be > tiny && ga * ga > (kSkipL * kSkipL) * (al * be)) {
+                // t = sign(zeta) / (|zeta| + sqrt(1 + zeta^2)), zeta = (be - al) / (2 ga),
+                // without divisions: t = sign(d) 2ga / (|d| + sqrt(d^2 + 4ga^2))
+                const double d = be - al, g2 = 2.0 * ga;
+                const double h = fma(d, d, g2 * g2);
+                const double rh = h * dev::rsqrt_nr(h);
+                tt = (d >= 0.0 ? g2 : -g2) * dev::rcp_nr(fabs(d) + rh);
+                c = dev::rsqrt_nr(fma(tt, tt, 1.0));
                 sn = c * tt;
               }
             }
             rot[lane] = make_double2(c, sn);
             rt[lane] = tt * ga;
-            rpq[lane] = pq;
+            ofs[lane] = q != 0xff ? make_int4(p * LDM, q * LDM, p, q) : make_int4(p * LDM, -1, p, -1);
           }
           __syncwarp();
-          // M <- J^T M J over 2 x 2 blocks of slot pairs
-          for (int it = lane; it < nblk; it += 32) {
-            const int i1 = blk[it] >> 8, i2 = blk[it] & 0xff;
+          // M <- J^T M J over this lane's 2 x 2 blocks of slot pairs
+#pragma unroll
+          for (int j = 0; j < kLaneBlk; ++j) {
+            const int b = lblk[j];
+            if (b < 0) continue;
+            const int i1 = b & 0xff, i2 = b >> 8;
             const double2 r1 = rot[i1], r2 = rot[i2];
             if (r1.y == 0.0 && r2.y == 0.0) continue;
-            const int pq1 = rpq[i1], pq2 = rpq[i2];
-            const int p1 = pq1 & 0xff, q1 = pq1 >> 8, p2 = pq2 & 0xff, q2 = pq2 >> 8;
-            if (q1 == 0xff || q2 == 0xff) {  // odd R: 1 x 2 block against the dummy slot's index
-              const int aa = q1 == 0xff ? p1 : p2;
-              const int uu = q1 == 0xff ? p2 : p1, vv = q1 == 0xff ? q2 : q1;
-              const double cc = q1 == 0xff ? r2.x : r1.x, ss = q1 == 0xff ? r2.y : r1.y;
-              const double xu = M[aa * LDM + uu], xv = M[aa * LDM + vv];
+            const int4 o1 = ofs[i1], o2 = ofs[i2];
+            if (!EXACT && (o1.w < 0 || o2.w < 0)) {  // odd R: 1 x 2 block against the dummy slot's index
+              const bool d1 = o1.w < 0;
+              const int ar = d1 ? o1.x : o2.x, ac = d1 ? o1.z : o2.z;  // the single index (row / column offsets)
+              const int ur = d1 ? o2.x : o1.x, uc = d1 ? o2.z : o1.z;
+              const int vr = d1 ? o2.y : o1.y, vc = d1 ? o2.w : o1.w;
+              const double cc = d1 ? r2.x : r1.x, ss = d1 ? r2.y : r1.y;
+              const double xu = M[ar + uc], xv = M[ar + vc];
               const double nu = cc * xu - ss * xv, nv = ss * xu + cc * xv;
-              M[aa * LDM + uu] = nu;
-              M[uu * LDM + aa] = nu;
-              M[aa * LDM + vv] = nv;
-              M[vv * LDM + aa] = nv;
+              M[ar + uc] = nu;
+              M[ur + ac] = nu;
+              M[ar + vc] = nv;
+              M[vr + ac] = nv;
               continue;
             }
             if (i1 == i2) {
               const double d = rt[i1];
-              M[p1 * LDM + p1] -= d;
-              M[q1 * LDM + q1] += d;
-              M[p1 * LDM + q1] = 0.0;
-              M[q1 * LDM + p1] = 0.0;
+              M[o1.x + o1.z] -= d;
+              M[o1.y + o1.w] += d;
+              M[o1.x + o1.w] = 0.0;
+              M[o1.y + o1.z] = 0.0;
               continue;
             }
             const double c1 = r1.x, s1 = r1.y, c2 = r2.x, s2 = r2.y;
-            const double x11 = M[p1 * LDM + p2], x12 = M[p1 * LDM + q2], x21 = M[q1 * LDM + p2], x22 = M[q1 * LDM + q2];
+            const double x11 = M[o1.x + o2.z], x12 = M[o1.x + o2.w], x21 = M[o1.y + o2.z], x22 = M[o1.y + o2.w];
             const double y11 = c2 * x11 - s2 * x12, y12 = s2 * x11 + c2 * x12;
             const double y21 = c2 * x21 - s2 * x22, y22 = s2 * x21 + c2 * x22;
             const double z11 = c1 * y11 - s1 * y21, z21 = s1 * y11 + c1 * y21;
             const double z12 = c1 * y12 - s1 * y22, z22 = s1 * y12 + c1 * y22;
-            M[p1 * LDM + p2] = z11;
-            M[p2 * LDM + p1] = z11;
-            M[p1 * LDM + q2] = z12;
-            M[q2 * LDM + p1] = z12;
-            M[q1 * LDM + p2] = z21;
-            M[p2 * LDM + q1] = z21;
-            M[q1 * LDM + q2] = z22;
-            M[q2 * LDM + q1] = z22;
+            M[o1.x + o2.z] = z11;
+            M[o2.x + o1.z] = z11;
+            M[o1.x + o2.w] = z12;
+            M[o2.y + o1.z] = z12;
+            M[o1.y + o2.z] = z21;
+            M[o2.x + o1.w] = z21;
+            M[o1.y + o2.w] = z22;
+            M[o2.y + o1.w] = z22;
           }
-          // V' <- V' J: rows of V'^T p, q over pairs of columns k, k + 1
-          {
-            const int nkp = (R + 1) >> 1;
-            for (int it = lane; it < nkp * half; it += 32) {
-              const int kp = it / half, sl = it - kp * half;
-              const double2 r = rot[sl];
-              if (r.y == 0.0) continue;
-              const int pq = rpq[sl];
-              const int p = pq & 0xff, q = pq >> 8;
-              double2* vp = reinterpret_cast<double2*>(Vt + p * LDV + 2 * kp);
-              double2* vq = reinterpret_cast<double2*>(Vt + q * LDV + 2 * kp);
-              const double2 x = *vp, y = *vq;
-              *vp = make_double2(r.x * x.x - r.y * y.x, r.x * x.y - r.y * y.y);
-              *vq = make_double2(r.y * x.x + r.x * y.x, r.y * x.y + r.x * y.y);
-            }
+          // V' <- V' J: rows p, q of V'^T (offset p LDV = p LDM + p) over this lane's column pairs
+#pragma unroll
+          for (int j = 0; j < kLaneVit; ++j) {
+            const int v = lvit[j];
+            if (v < 0) continue;
+            const int sl = v & 0xff, kc = v >> 8;
+            const double2 r = rot[sl];
+            if (r.y == 0.0) continue;
+            const int4 o = ofs[sl];
+            double2* vp = reinterpret_cast<double2*>(Vt + (o.x + o.z + kc));
+            double2* vq = reinterpret_cast<double2*>(Vt + (o.y + o.w + kc));
+            const double2 x = *vp, y = *vq;
+            *vp = make_double2(r.x * x.x - r.y * y.x, r.x * x.y - r.y * y.y);
+            *vq = make_double2(r.y * x.x + r.x * y.x, r.y * x.y + r.x * y.y);
           }
           __syncwarp();
         }
