@@ -164,33 +164,57 @@ __global__ void k_seg_reduce(int R, std::int64_t J, const std::int64_t* __restri
   }
 }
 
-/// U rows of the large-R path: u_i = q_i H diag(w_k o nH), warp per subject.
+/// U = Q_k H diag(W_k o nH) row factors for R > 16 on the fp64 tensor cores:
+/// warp per subject, HW_k (R x R, zero-padded to RP) in the warp's shared
+/// memory, 8-row tiles of Q_k as DMMA A fragments straight from HBM, U rows
+/// stored from the C fragments (16-byte pairs).
 template <int RP, int WPB>
 __global__ void __launch_bounds__(WPB * 32)
     k_urows(ShardArgs X, int R, const double* __restrict__ Q, const double* __restrict__ H,
             const double* __restrict__ W, const double* __restrict__ nH, double* __restrict__ U) {
+  constexpr int NB = RP / 8;
   extern __shared__ double sm[];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  double* HW = sm + wid * RP * (RP + 1);  // R x R, ld RP + 1
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, fm = lane >> 2, fk = lane & 3;
+  double* HW = sm + wid * RP * RP;  // RP x RP row-major
+  const bool even = (R & 1) == 0;
   const std::int64_t nwarps = static_cast<std::int64_t>(gridDim.x) * WPB;
   for (std::int64_t k = static_cast<std::int64_t>(blockIdx.x) * WPB + wid; k < X.K; k += nwarps) {
-    for (int a = 0; a < R; ++a)
-      for (int c = lane; c < R; c += 32) HW[a * (RP + 1) + c] = H[a * R + c] * W[k * R + c] * nH[c];
     __syncwarp();
-    const std::int64_t r0 = X.srp[k], r1 = X.srp[k + 1];
-    for (std::int64_t i = r0 + lane; i < r1; i += 32) {
-      double q[RP];
-#pragma unroll
-      for (int a = 0; a < RP; ++a) q[a] = a < R ? Q[i * R + a] : 0.0;
-      for (int c = 0; c < R; ++c) {
-        double acc = 0.0;
-#pragma unroll
-        for (int a = 0; a < RP; ++a)
-          if (a < R) acc = fma(q[a], HW[a * (RP + 1) + c], acc);
-        U[i * R + c] = acc;
-      }
+    for (int e = lane; e < RP * RP; e += 32) {
+      const int a = e / RP, c = e - a * RP;
+      HW[e] = (a < R && c < R) ? H[a * R + c] * W[k * R + c] * nH[c] : 0.0;
     }
     __syncwarp();
+    const std::int64_t r0 = X.srp[k];
+    const int I = static_cast<int>(X.srp[k + 1] - r0);
+    for (int i0 = 0; i0 < I; i0 += 8) {
+      const int i = i0 + fm;
+      const bool iv = i < I;
+      const double* qrow = Q + (r0 + i) * R;
+      double acc[NB][2];
+#pragma unroll
+      for (int b = 0; b < NB; ++b) acc[b][0] = acc[b][1] = 0.0;
+#pragma unroll
+      for (int k4 = 0; k4 < RP; k4 += 4) {
+        const int c = k4 + fk;
+        const double x = (iv && c < R) ? __ldg(qrow + c) : 0.0;
+#pragma unroll
+        for (int b = 0; b < NB; ++b) dev::dmma884(acc[b], x, HW[c * RP + 8 * b + fm]);
+      }
+      if (iv) {
+        double* urow = U + (r0 + i) * R;
+#pragma unroll
+        for (int b = 0; b < NB; ++b) {
+          const int c = 8 * b + 2 * fk;
+          if (even) {
+            if (c < R) *reinterpret_cast<double2*>(urow + c) = make_double2(acc[b][0], acc[b][1]);
+          } else {
+            if (c < R) urow[c] = acc[b][0];
+            if (c + 1 < R) urow[c + 1] = acc[b][1];
+          }
+        }
+      }
+    }
   }
 }
 
@@ -319,8 +343,8 @@ void launch_csc_mode2(p2g_ctx* c, int R, const double* U, double* M2, cudaStream
 template <int RP>
 static void urows(p2g_ctx* c, int R, const double* Q, const double* H, const double* W, const double* nH, double* U,
                   cudaStream_t s) {
-  constexpr int WPB = 4;
-  const std::size_t smem = sizeof(double) * WPB * RP * (RP + 1);
+  constexpr int WPB = 8;
+  const std::size_t smem = sizeof(double) * WPB * RP * RP;
   auto kern = k_urows<RP, WPB>;
   P2G_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   const ShardArgs X{c->srp.get(), c->rp.get(), c->ci.get(), c->val.get(), c->k_end - c->k_begin, c->NR, c->nnz, c->J};

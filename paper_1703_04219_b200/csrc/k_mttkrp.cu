@@ -278,6 +278,94 @@ __global__ void __launch_bounds__(WPB * 32)
 }
 
 // ---------------------------------------------------------------------------
+// mode 3 for R > 16 on the fp64 tensor cores: per subject, 8-row tiles of
+// P = Q_k H (DMMA m8n8k4: Q fragments straight from HBM, H from shared
+// memory) meet the matching fragment of X_k V, which each lane gathers for
+// its own row (lane (fm, fk) holds row fm, columns 8b + 2fk + {0, 1} in the
+// C layout); the column sums over rows are a 3-step shuffle over fm.
+// Per subject: Q read once (coalesced 32-byte sectors), CSR streamed once,
+// V rows from L2.
+// ---------------------------------------------------------------------------
+template <int RP, int WPB>
+__global__ void __launch_bounds__(WPB * 32)
+    k_mode3_mma(ShardArgs X, int R, const double* __restrict__ Q, const double* __restrict__ H,
+                const double* __restrict__ V, double* __restrict__ M3) {
+  constexpr int NB = RP / 8;
+  __shared__ double Hs[RP * RP];  // H zero-padded to RP x RP, row-major
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, fm = lane >> 2, fk = lane & 3;
+  for (int e = threadIdx.x; e < RP * RP; e += blockDim.x) {
+    const int a = e / RP, c = e - a * RP;
+    Hs[e] = (a < R && c < R) ? H[a * R + c] : 0.0;
+  }
+  __syncthreads();
+  const bool even = (R & 1) == 0;
+  const std::int64_t nwarps = static_cast<std::int64_t>(gridDim.x) * WPB;
+  for (std::int64_t k = static_cast<std::int64_t>(blockIdx.x) * WPB + wid; k < X.K; k += nwarps) {
+    const std::int64_t r0 = X.srp[k];
+    const int I = static_cast<int>(X.srp[k + 1] - r0);
+    double m3p[NB][2];
+#pragma unroll
+    for (int b = 0; b < NB; ++b) m3p[b][0] = m3p[b][1] = 0.0;
+    for (int i0 = 0; i0 < I; i0 += 8) {
+      const int i = i0 + fm;
+      const bool iv = i < I;
+      const double* qrow = Q + (r0 + i) * R;
+      double acc[NB][2];
+#pragma unroll
+      for (int b = 0; b < NB; ++b) acc[b][0] = acc[b][1] = 0.0;
+#pragma unroll
+      for (int k4 = 0; k4 < RP; k4 += 4) {
+        const int c = k4 + fk;
+        const double x = (iv && c < R) ? __ldg(qrow + c) : 0.0;
+#pragma unroll
+        for (int b = 0; b < NB; ++b) dev::dmma884(acc[b], x, Hs[c * RP + 8 * b + fm]);
+      }
+      double xv[NB][2];
+#pragma unroll
+      for (int b = 0; b < NB; ++b) xv[b][0] = xv[b][1] = 0.0;
+      if (iv) {
+        const std::int64_t p0 = X.rp[r0 + i], p1 = X.rp[r0 + i + 1];
+#pragma unroll 2
+        for (std::int64_t p = p0; p < p1; ++p) {
+          const double v = __ldg(X.val + p);
+          const double* vr = V + static_cast<std::int64_t>(__ldg(X.ci + p)) * R;
+#pragma unroll
+          for (int b = 0; b < NB; ++b) {
+            const int c = 8 * b + 2 * fk;
+            if (even) {
+              if (c < R) {
+                const double2 y = __ldg(reinterpret_cast<const double2*>(vr + c));
+                xv[b][0] = fma(v, y.x, xv[b][0]);
+                xv[b][1] = fma(v, y.y, xv[b][1]);
+              }
+            } else {
+              if (c < R) xv[b][0] = fma(v, __ldg(vr + c), xv[b][0]);
+              if (c + 1 < R) xv[b][1] = fma(v, __ldg(vr + c + 1), xv[b][1]);
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int b = 0; b < NB; ++b) {
+        m3p[b][0] = fma(acc[b][0], xv[b][0], m3p[b][0]);
+        m3p[b][1] = fma(acc[b][1], xv[b][1], m3p[b][1]);
+      }
+    }
+#pragma unroll
+    for (int b = 0; b < NB; ++b)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        double t = m3p[b][h];
+        t += __shfl_xor_sync(dev::kFull, t, 4);
+        t += __shfl_xor_sync(dev::kFull, t, 8);
+        t += __shfl_xor_sync(dev::kFull, t, 16);
+        const int c = 8 * b + 2 * fk + h;
+        if (fm == 0 && c < R) M3[k * R + c] = t;
+      }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // mode 1 from a given Q (the p2g_mttkrp_q hook; the fused loop gets M1 from
 // K1): m1 += Q_k^T (XV o W_k) through 32-row chunks.
 // ---------------------------------------------------------------------------
@@ -546,8 +634,15 @@ void launch_mode3(p2g_ctx* c, int R, const double* Q, const double* H, const dou
                   cudaStream_t s) {
   const ShardArgs X = shard_args(c);
   if (R > 16) {  // the row-per-lane form spills above R = 16
-    constexpr int WPB = 4;  // Hs 32 KB + 4 KB q staging
-    k_mode3_cols<WPB><<<grid_for(X.K, WPB, c->num_sms, 12), WPB * 32, 0, s>>>(X, R, Q, H, V, m3);
+    constexpr int WPB = 8;
+    if (R <= 24)
+      k_mode3_mma<24, WPB><<<grid_for(X.K, WPB, c->num_sms, 4), WPB * 32, 0, s>>>(X, R, Q, H, V, m3);
+    else if (R <= 32)
+      k_mode3_mma<32, WPB><<<grid_for(X.K, WPB, c->num_sms, 4), WPB * 32, 0, s>>>(X, R, Q, H, V, m3);
+    else if (R <= 40)
+      k_mode3_mma<40, WPB><<<grid_for(X.K, WPB, c->num_sms, 4), WPB * 32, 0, s>>>(X, R, Q, H, V, m3);
+    else
+      k_mode3_cols<4><<<grid_for(X.K, 4, c->num_sms, 12), 4 * 32, 0, s>>>(X, R, Q, H, V, m3);
     P2G_LAUNCHED(1);
     return;
   }
