@@ -82,6 +82,44 @@ __global__ void k_reduce_partials(const double* __restrict__ partials, int npart
 // reference's pinv_small(G_pp) b_p when G_pp is positive definite); a
 // non-positive pivot falls back to the eigen pseudo-inverse.
 // ---------------------------------------------------------------------------
+constexpr int kNnlsFastN0 = 12;  // largest zero set the fast warm path solves
+
+/// G^{-1} for the NNLS fast warm path: Gauss-Jordan without pivoting on the
+/// SPD Gram (one warp); out[R * R] = 1 when every pivot was positive and
+/// finite, else 0 (the fast path is then off for this launch).
+template <int RP>
+__global__ void k_ginv(int R, const double* __restrict__ G, double* __restrict__ out) {
+  __shared__ double A[RP][2 * RP + 1];
+  __shared__ double f[RP];
+  const int lane = threadIdx.x;
+  for (int e = lane; e < R * 2 * R; e += 32) {
+    const int i = e / (2 * R), j = e - i * 2 * R;
+    A[i][j] = j < R ? G[i * R + j] : (j - R == i ? 1.0 : 0.0);
+  }
+  __syncwarp();
+  bool ok = true;
+  for (int k = 0; k < R && ok; ++k) {
+    const double piv = A[k][k];
+    ok = piv > 0.0 && isfinite(piv);
+    if (!ok) break;
+    const double ip = 1.0 / piv;
+    __syncwarp();
+    for (int j = lane; j < 2 * R; j += 32) A[k][j] *= ip;
+    for (int i = lane; i < R; i += 32) f[i] = i == k ? 0.0 : A[i][k];
+    __syncwarp();
+    for (int e = lane; e < R * 2 * R; e += 32) {
+      const int i = e / (2 * R), j = e - i * 2 * R;
+      if (i != k) A[i][j] = fma(-f[i], A[k][j], A[i][j]);
+    }
+    __syncwarp();
+  }
+  for (int e = lane; e < R * R; e += 32) {
+    const int i = e / R, j = e - i * R;
+    out[e] = 0.5 * (A[i][R + j] + A[j][R + i]);
+  }
+  if (lane == 0) out[R * R] = ok ? 1.0 : 0.0;
+}
+
 template <int RP>
 struct NnlsSmem {
   // L (RP*RP) + b, x, w, s, sp (RP each) + cs (RP+2) ; ints: pset RP, pq RP+2.
@@ -96,11 +134,13 @@ template <int RP, int WPB>
 __global__ void __launch_bounds__(WPB * 32)
     k_nnls(int R, std::int64_t n, const double* __restrict__ G, const double* __restrict__ B, double* __restrict__ X,
            int cap, std::int32_t* err, const std::int32_t* __restrict__ rowlist, const std::int32_t* __restrict__ nlist,
-           unsigned long long* __restrict__ masks, int warm, double* __restrict__ pinv_slab) {
+           unsigned long long* __restrict__ masks, int warm, double* __restrict__ pinv_slab,
+           const double* __restrict__ ginv) {
   extern __shared__ double smem[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   double* Gs = smem;
-  double* base = Gs + RP * RP + wid * (NnlsSmem<RP>::kDoubles + (NnlsSmem<RP>::kInts + 1) / 2);
+  double* Gi = Gs + RP * RP;  // G^{-1} (fast warm path), when ginv is valid
+  double* base = Gi + RP * RP + wid * (NnlsSmem<RP>::kDoubles + (NnlsSmem<RP>::kInts + 1) / 2);
   double* L = base;
   double* PA = pinv_slab + (static_cast<std::int64_t>(blockIdx.x) * WPB + wid) * 3 * RP * RP;
   double* PE = PA + RP * RP;
@@ -114,6 +154,9 @@ __global__ void __launch_bounds__(WPB * 32)
   int* pset = reinterpret_cast<int*>(cs + RP + 2);
   int* pq = pset + RP;
   for (int e = threadIdx.x; e < R * R; e += blockDim.x) Gs[e] = G[e];
+  const bool fast = ginv && warm && masks && ginv[R * R] == 1.0;
+  if (fast)
+    for (int e = threadIdx.x; e < R * R; e += blockDim.x) Gi[e] = ginv[e];
   __syncthreads();
   const std::int64_t nwarps = static_cast<std::int64_t>(gridDim.x) * WPB;
   const std::int64_t nrows = rowlist ? static_cast<std::int64_t>(*nlist) : n;
@@ -134,6 +177,89 @@ __global__ void __launch_bounds__(WPB * 32)
     int iters = 0;
     bool failed = false;
     __syncwarp();
+    // Fast warm path: G is shared by every row, so with G^{-1} precomputed the
+    // passive solve G_PP s = b_P is a Schur complement on the zero set N,
+    //   s = (Gi_PP - Gi_PN Gi_NN^{-1} Gi_NP) b_P,
+    // an |N| x |N| Cholesky instead of a |P| x |P| one.  Accepted only at the
+    // reference's optimum (s > 0 on P, no entering coordinate w_j > 1e-10 off
+    // P: nnls_single's KKT test); otherwise the row takes the general path.
+    if (fast && warm_phase) {
+      const unsigned long long nmask = full & ~passive;
+      const int n0 = __popcll(nmask);
+      if (n0 <= kNnlsFastN0) {
+        for (int r = lane; r < R; r += 32)
+          if ((nmask >> r) & 1ull) pq[__popcll(nmask & ((1ull << r) - 1ull))] = r;
+        for (int r = lane; r < R; r += 32) {  // t = Gi[:, P] b_P
+          double acc = 0.0;
+          for (int c = 0; c < R; ++c)
+            if ((passive >> c) & 1ull) acc = fma(Gi[r * R + c], b[c], acc);
+          sp[r] = acc;
+        }
+        __syncwarp();
+        int ok = 1;
+        if (n0 > 0) {
+          if (lane == 0) {  // Gi_NN z = t_N by Cholesky on one lane (n0 <= kNnlsFastN0)
+            for (int i = 0; i < n0 && ok; ++i)
+              for (int j = 0; j <= i; ++j) {
+                double acc = Gi[pq[i] * R + pq[j]];
+                for (int c = 0; c < j; ++c) acc = fma(-L[i * n0 + c], L[j * n0 + c], acc);
+                if (i == j) {
+                  if (!(acc > 0.0) || !isfinite(acc)) {
+                    ok = 0;
+                    break;
+                  }
+                  L[i * n0 + i] = sqrt(acc);
+                } else {
+                  L[i * n0 + j] = acc / L[j * n0 + j];
+                }
+              }
+            if (ok) {
+              for (int i = 0; i < n0; ++i) {
+                double acc = sp[pq[i]];
+                for (int c = 0; c < i; ++c) acc = fma(-L[i * n0 + c], sv[c], acc);
+                sv[i] = acc / L[i * n0 + i];
+              }
+              for (int i = n0 - 1; i >= 0; --i) {
+                double acc = sv[i];
+                for (int c = i + 1; c < n0; ++c) acc = fma(-L[c * n0 + i], sv[c], acc);
+                sv[i] = acc / L[i * n0 + i];
+              }
+            }
+          }
+          ok = __shfl_sync(dev::kFull, ok, 0);
+          __syncwarp();
+        }
+        if (ok) {
+          for (int r = lane; r < R; r += 32) {
+            double acc = 0.0;
+            if ((passive >> r) & 1ull) {
+              acc = sp[r];
+              for (int a2 = 0; a2 < n0; ++a2) acc = fma(-Gi[r * R + pq[a2]], sv[a2], acc);
+            }
+            x[r] = acc;
+          }
+          __syncwarp();
+          bool good = true;
+          for (int r = lane; r < R; r += 32) {
+            if ((passive >> r) & 1ull) {
+              good = good && x[r] > 0.0 && isfinite(x[r]);
+            } else {
+              double acc = 0.0;
+              for (int c = 0; c < R; ++c) acc = fma(Gs[r * R + c], x[c], acc);
+              good = good && !(b[r] - acc > 1e-10);
+            }
+          }
+          if (__all_sync(dev::kFull, good)) {
+            if (lane == 0) masks[row] = passive;
+            for (int r = lane; r < R; r += 32) X[row * R + r] = x[r];
+            __syncwarp();
+            continue;
+          }
+          for (int r = lane; r < R; r += 32) x[r] = 0.0;
+          __syncwarp();
+        }
+      }
+    }
     while (true) {
      if (!warm_phase) {
       // entering coordinate: argmax_{j not passive, w_j > 1e-10} w_j, first index on ties
@@ -462,7 +588,7 @@ void nnls_launch(int R, std::int64_t n, const double* G, const double* B, double
                  cudaStream_t s) {
   constexpr int WPB = RP <= 16 ? 8 : 4;
   const std::size_t per_warp = sizeof(double) * (NnlsSmem<RP>::kDoubles + (NnlsSmem<RP>::kInts + 1) / 2);
-  const std::size_t smem = sizeof(double) * RP * RP + WPB * per_warp;
+  const std::size_t smem = sizeof(double) * 2 * RP * RP + WPB * per_warp;
   auto kern = k_nnls<RP, WPB>;
   P2G_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   const std::int64_t want = (n + WPB - 1) / WPB;
@@ -471,7 +597,14 @@ void nnls_launch(int R, std::int64_t n, const double* G, const double* B, double
   // process-wide slab grown on demand is enough
   static DBuf<double> slab;
   slab.resize(static_cast<std::size_t>(blocks) * WPB * 3 * RP * RP);
-  kern<<<blocks, WPB * 32, smem, s>>>(R, n, G, B, X, cap, err, rowlist, nlist, masks, warm, slab.get());
+  static DBuf<double> ginv;
+  const bool fast = masks && warm && !rowlist;
+  if (fast) {
+    ginv.resize(static_cast<std::size_t>(RP) * RP + 1);
+    k_ginv<RP><<<1, 32, 0, s>>>(R, G, ginv.get());
+  }
+  kern<<<blocks, WPB * 32, smem, s>>>(R, n, G, B, X, cap, err, rowlist, nlist, masks, warm, slab.get(),
+                                      fast ? ginv.get() : nullptr);
 }
 
 template <int RP>
