@@ -439,6 +439,8 @@ __global__ void __launch_bounds__(kLgThreads, 2) k_procrustes_large(LgArgs a) {
 //   scaled off-diagonal at tau).  Then G^{-1/2} = E' S' E'^T with E' = E V',
 //   Z = V' S' E'^T, Q = B Z and m1_k = Z^T F as before.
 // ---------------------------------------------------------------------------
+// During the sweeps M is kept in its upper triangle only (M[min * LDM + max]):
+// half the shared-memory stores of a full symmetric update.
 constexpr double kTauL = 1e-4;   // Jacobi stop: max scaled off-diagonal
 constexpr double kSkipL = 1e-6;  // rotations below this scaled size are skipped (threshold Jacobi)
 
@@ -706,7 +708,7 @@ __global__ void __launch_bounds__(LgWarp<RP>::WPB * 32, 1) k_procrustes_large_w(
         double omax = 0.0, osum = 0.0;
         for (int e = lane; e < RR; e += 32) {
           const int p = e / R, q = e - p * R;
-          const double x = M[p * LDM + q] * u[p] * u[q];
+          const double x = M[p < q ? p * LDM + q : q * LDM + p] * u[p] * u[q];
           if (p != q) {
             omax = fmax(omax, fabs(x));
             osum = fma(x, x, osum);
@@ -731,7 +733,7 @@ __global__ void __launch_bounds__(LgWarp<RP>::WPB * 32, 1) k_procrustes_large_w(
             double c = 1.0, sn = 0.0, tt = 0.0, ga = 0.0;
             if (q != 0xff) {
               const double al = M[p * LDM + p], be = M[q * LDM + q];
-              ga = M[p * LDM + q];
+              ga = M[p < q ? p * LDM + q : q * LDM + p];
               if (al > tiny && be > tiny && ga * ga > (kSkipL * kSkipL) * (al * be)) {
                 // t = sign(zeta) / (|zeta| + sqrt(1 + zeta^2)), zeta = (be - al) / (2 ga),
                 // without divisions: t = sign(d) 2ga / (|d| + sqrt(d^2 + 4ga^2))
@@ -763,36 +765,34 @@ __global__ void __launch_bounds__(LgWarp<RP>::WPB * 32, 1) k_procrustes_large_w(
               const int ur = d1 ? o2.x : o1.x, uc = d1 ? o2.z : o1.z;
               const int vr = d1 ? o2.y : o1.y, vc = d1 ? o2.w : o1.w;
               const double cc = d1 ? r2.x : r1.x, ss = d1 ? r2.y : r1.y;
-              const double xu = M[ar + uc], xv = M[ar + vc];
-              const double nu = cc * xu - ss * xv, nv = ss * xu + cc * xv;
-              M[ar + uc] = nu;
-              M[ur + ac] = nu;
-              M[ar + vc] = nv;
-              M[vr + ac] = nv;
+              const int au = ac < uc ? ar + uc : ur + ac, av = ac < vc ? ar + vc : vr + ac;
+              const double xu = M[au], xv = M[av];
+              M[au] = cc * xu - ss * xv;
+              M[av] = ss * xu + cc * xv;
               continue;
             }
             if (i1 == i2) {
               const double d = rt[i1];
               M[o1.x + o1.z] -= d;
               M[o1.y + o1.w] += d;
-              M[o1.x + o1.w] = 0.0;
-              M[o1.y + o1.z] = 0.0;
+              M[o1.z < o1.w ? o1.x + o1.w : o1.y + o1.z] = 0.0;
               continue;
             }
             const double c1 = r1.x, s1 = r1.y, c2 = r2.x, s2 = r2.y;
-            const double x11 = M[o1.x + o2.z], x12 = M[o1.x + o2.w], x21 = M[o1.y + o2.z], x22 = M[o1.y + o2.w];
+            // upper-triangle (canonical) addresses: row index < column index
+            const int e11 = o1.z < o2.z ? o1.x + o2.z : o2.x + o1.z;
+            const int e12 = o1.z < o2.w ? o1.x + o2.w : o2.y + o1.z;
+            const int e21 = o1.w < o2.z ? o1.y + o2.z : o2.x + o1.w;
+            const int e22 = o1.w < o2.w ? o1.y + o2.w : o2.y + o1.w;
+            const double x11 = M[e11], x12 = M[e12], x21 = M[e21], x22 = M[e22];
             const double y11 = c2 * x11 - s2 * x12, y12 = s2 * x11 + c2 * x12;
             const double y21 = c2 * x21 - s2 * x22, y22 = s2 * x21 + c2 * x22;
             const double z11 = c1 * y11 - s1 * y21, z21 = s1 * y11 + c1 * y21;
             const double z12 = c1 * y12 - s1 * y22, z22 = s1 * y12 + c1 * y22;
-            M[o1.x + o2.z] = z11;
-            M[o2.x + o1.z] = z11;
-            M[o1.x + o2.w] = z12;
-            M[o2.y + o1.z] = z12;
-            M[o1.y + o2.z] = z21;
-            M[o2.x + o1.w] = z21;
-            M[o1.y + o2.w] = z22;
-            M[o2.y + o1.w] = z22;
+            M[e11] = z11;
+            M[e12] = z12;
+            M[e21] = z21;
+            M[e22] = z22;
           }
           // V' <- V' J: rows p, q of V'^T (offset p LDV = p LDM + p) over this lane's column pairs
 #pragma unroll
@@ -851,7 +851,7 @@ __global__ void __launch_bounds__(LgWarp<RP>::WPB * 32, 1) k_procrustes_large_w(
         const int p = e / R, q = e - p * R;
         const double P = 1.0 / (sv[p] + sv[q]);
         Ns[e] = P;
-        Ts[e] = p == q ? 0.0 : P * M[p * LDM + q];
+        Ts[e] = p == q ? 0.0 : P * M[p < q ? p * LDM + q : q * LDM + p];
       }
       __syncwarp();
       {
