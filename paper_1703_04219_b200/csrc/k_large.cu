@@ -452,8 +452,8 @@ struct LgWarp {
   static constexpr int kVt = RP * LDV;
   static constexpr int NBLK = (RP / 2) * (RP / 2 + 1) / 2;
   static constexpr int kTabD = ((NBLK + (RP - 1) * (RP / 2) + 7) / 8) * 2;  // uint16 tables, in doubles (even)
-  // M, V'^T, w, u (1/sqrt diag), (c, s) per pair slot, t M_pq per slot, int4 offsets per slot
-  static constexpr int kWarpD = kMat + kVt + 2 * RP + RP + RP / 2 + RP;
+  // M, V'^T, w, u (1/sqrt diag), then per pair slot and double-buffered: (c, s), t M_pq, int4 offsets
+  static constexpr int kWarpD = kMat + kVt + 2 * RP + 2 * (RP + RP / 2 + RP);
   static constexpr int kWarpDE = (kWarpD + 1) & ~1;
   static constexpr int pick_wpb() {
     int w = 16;
@@ -524,9 +524,11 @@ __global__ void __launch_bounds__(LgWarp<RP>::WPB * 32, 1) k_procrustes_large_w(
   double* Vt = M + L::kMat;  // V'^T: Vt[p * LDV + k] = V'(k, p)
   double* w = Vt + L::kVt;
   double* u = w + RP;
-  double2* rot = reinterpret_cast<double2*>(u + RP);  // (c, s)
-  double* rt = reinterpret_cast<double*>(rot + RP / 2);
-  int4* ofs = reinterpret_cast<int4*>(rt + RP / 2);  // per slot: p LDM, q LDM, p, q (q < 0: no pair)
+  // per slot, double-buffered by round parity: (c, s), t M_pq, and the offsets
+  // (p LDM, q LDM, p, q; q < 0: no pair)
+  double2* rotb = reinterpret_cast<double2*>(u + RP);
+  double* rtb = reinterpret_cast<double*>(rotb + RP);
+  int4* ofsb = reinterpret_cast<int4*>(rtb + RP);
   for (int it = threadIdx.x; it < nblk; it += blockDim.x) {
     int i1 = 0, r = it;
     while (r >= half - i1) {
@@ -726,30 +728,48 @@ __global__ void __launch_bounds__(LgWarp<RP>::WPB * 32, 1) k_procrustes_large_w(
           converged = true;
           break;
         }
-        for (int round = 0; round < m - 1; ++round) {
+        // Rotation parameters of one round's slot (lanes < half store them).
+        // Split into the shared-memory loads and a pure-ALU tail, so that the
+        // tail of round r + 1 can be scheduled among round r's V' updates.
+        struct PIn {
+          double al, be, ga;
+          int p, q;
+        };
+        auto param_load = [&](int round) {
+          PIn in;
+          const int pq = sched[round * half + (lane < half ? lane : 0)];
+          in.p = pq & 0xff;
+          in.q = pq >> 8;
+          const int qq = in.q != 0xff ? in.q : in.p;
+          in.al = M[in.p * LDM + in.p];
+          in.be = M[qq * LDM + qq];
+          in.ga = in.q != 0xff ? M[in.p < qq ? in.p * LDM + qq : qq * LDM + in.p] : 0.0;
+          return in;
+        };
+        auto param_store = [&](const PIn& in, int buf) {
+          const bool on = in.q != 0xff && in.al > tiny && in.be > tiny &&
+                          in.ga * in.ga > (kSkipL * kSkipL) * (in.al * in.be);
+          // t = sign(zeta) / (|zeta| + sqrt(1 + zeta^2)), zeta = (be - al) / (2 ga),
+          // without divisions: t = sign(d) 2ga / (|d| + sqrt(d^2 + 4ga^2))
+          const double d = in.be - in.al, g2 = 2.0 * in.ga;
+          const double h = on ? fma(d, d, g2 * g2) : 1.0;
+          const double rh = h * dev::rsqrt_nr(h);
+          const double tt = on ? (d >= 0.0 ? g2 : -g2) * dev::rcp_nr(fabs(d) + rh) : 0.0;
+          const double c = on ? dev::rsqrt_nr(fma(tt, tt, 1.0)) : 1.0;
           if (lane < half) {
-            const int pq = sched[round * half + lane];
-            const int p = pq & 0xff, q = pq >> 8;
-            double c = 1.0, sn = 0.0, tt = 0.0, ga = 0.0;
-            if (q != 0xff) {
-              const double al = M[p * LDM + p], be = M[q * LDM + q];
-              ga = M[p < q ? p * LDM + q : q * LDM + p];
-              if (al > tiny && be > tiny && ga * ga > (kSkipL * kSkipL) * (al * be)) {
-                // t = sign(zeta) / (|zeta| + sqrt(1 + zeta^2)), zeta = (be - al) / (2 ga),
-                // without divisions: t = sign(d) 2ga / (|d| + sqrt(d^2 + 4ga^2))
-                const double d = be - al, g2 = 2.0 * ga;
-                const double h = fma(d, d, g2 * g2);
-                const double rh = h * dev::rsqrt_nr(h);
-                tt = (d >= 0.0 ? g2 : -g2) * dev::rcp_nr(fabs(d) + rh);
-                c = dev::rsqrt_nr(fma(tt, tt, 1.0));
-                sn = c * tt;
-              }
-            }
-            rot[lane] = make_double2(c, sn);
-            rt[lane] = tt * ga;
-            ofs[lane] = q != 0xff ? make_int4(p * LDM, q * LDM, p, q) : make_int4(p * LDM, -1, p, -1);
+            rotb[buf * (RP / 2) + lane] = make_double2(c, c * tt);
+            rtb[buf * (RP / 2) + lane] = tt * in.ga;
+            ofsb[buf * (RP / 2) + lane] = in.q != 0xff ? make_int4(in.p * LDM, in.q * LDM, in.p, in.q)
+                                                      : make_int4(in.p * LDM, -1, in.p, -1);
           }
-          __syncwarp();
+        };
+        param_store(param_load(0), 0);
+        __syncwarp();
+        for (int round = 0; round < m - 1; ++round) {
+          const int buf = round & 1;
+          const double2* rot = rotb + buf * (RP / 2);
+          const double* rt = rtb + buf * (RP / 2);
+          const int4* ofs = ofsb + buf * (RP / 2);
           // M <- J^T M J over this lane's 2 x 2 blocks of slot pairs
 #pragma unroll
           for (int j = 0; j < kLaneBlk; ++j) {
@@ -794,21 +814,28 @@ __global__ void __launch_bounds__(LgWarp<RP>::WPB * 32, 1) k_procrustes_large_w(
             M[e21] = z21;
             M[e22] = z22;
           }
-          // V' <- V' J: rows p, q of V'^T (offset p LDV = p LDM + p) over this lane's column pairs
+          __syncwarp();
+          // next round's parameter loads (M is final for this round) ...
+          const PIn nxt = param_load(round + 1 < m - 1 ? round + 1 : 0);
+          // ... V' <- V' J: rows p, q of V'^T (offset p LDV = p LDM + p) over this
+          // lane's column pairs, branch-free so the parameter tail interleaves ...
 #pragma unroll
           for (int j = 0; j < kLaneVit; ++j) {
             const int v = lvit[j];
-            if (v < 0) continue;
-            const int sl = v & 0xff, kc = v >> 8;
-            const double2 r = rot[sl];
-            if (r.y == 0.0) continue;
-            const int4 o = ofs[sl];
-            double2* vp = reinterpret_cast<double2*>(Vt + (o.x + o.z + kc));
-            double2* vq = reinterpret_cast<double2*>(Vt + (o.y + o.w + kc));
+            const int sl = v & 0xff, kc = (v >> 8) & 0xff;
+            const double2 r = rot[v < 0 ? 0 : sl];
+            const int4 o = ofs[v < 0 ? 0 : sl];
+            const bool on = v >= 0 && r.y != 0.0;
+            double2* vp = reinterpret_cast<double2*>(Vt + (on ? o.x + o.z + kc : 0));
+            double2* vq = reinterpret_cast<double2*>(Vt + (on ? o.y + o.w + kc : 0));
             const double2 x = *vp, y = *vq;
-            *vp = make_double2(r.x * x.x - r.y * y.x, r.x * x.y - r.y * y.y);
-            *vq = make_double2(r.y * x.x + r.x * y.x, r.y * x.y + r.x * y.y);
+            if (on) {
+              *vp = make_double2(r.x * x.x - r.y * y.x, r.x * x.y - r.y * y.y);
+              *vq = make_double2(r.y * x.x + r.x * y.x, r.y * x.y + r.x * y.y);
+            }
           }
+          // ... and the parameters into the other buffer
+          param_store(nxt, buf ^ 1);
           __syncwarp();
         }
       }
