@@ -340,6 +340,7 @@ def main():
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         ctx.load(Xp)
+        t_load = time.perf_counter() - t0
         res = ctx.fit(p2g.SolverConfig(rank=R, max_iters=e2e_iters, tol=1e-300, nonneg=True), H0, V0, W0,
                       want_q=False)
         torch.cuda.synchronize()
@@ -355,6 +356,7 @@ def main():
         d2h = res.H.nbytes + res.V.nbytes + res.W.nbytes + 8 * 2 * e2e_iters
         e2e = {"value": X.nnz * e2e_iters / dt, "unit": "nnz/s", "h2d_bytes_per_step": h2d // e2e_iters,
                "d2h_bytes_per_step": d2h // e2e_iters, "iterations_per_call": e2e_iters, "sec_per_call": dt,
+               "load_s": t_load, "fit_s": dt - t_load,
                "fit_final": float(res.fit[-1])}
 
     # FP64 view of the step (the per-subject R x R work is FP64-issue bound)

@@ -154,7 +154,7 @@ __global__ void __launch_bounds__(WPB * 32)
   int* pset = reinterpret_cast<int*>(cs + RP + 2);
   int* pq = pset + RP;
   for (int e = threadIdx.x; e < R * R; e += blockDim.x) Gs[e] = G[e];
-  const bool fast = ginv && warm && masks && ginv[R * R] == 1.0;
+  const bool fast = ginv && ginv[R * R] == 1.0;
   if (fast)
     for (int e = threadIdx.x; e < R * R; e += blockDim.x) Gi[e] = ginv[e];
   __syncthreads();
@@ -173,6 +173,17 @@ __global__ void __launch_bounds__(WPB * 32)
     // and retries (x = 0 throughout), an emptied set is the reference's cold start.
     const unsigned long long full = R >= 64 ? ~0ull : ((1ull << R) - 1ull);
     unsigned long long passive = (masks && warm) ? (masks[row] & full) : 0ull;
+    if (fast && !(masks && warm)) {
+      // cold row: start from the support of the unconstrained solution G^{-1} b
+      // (any starting passive set reaches the same unique NNLS optimum; an
+      // infeasible start sheds coordinates and falls back to the cold path)
+      for (int r = lane; r < R; r += 32) {
+        double acc = 0.0;
+        for (int c = 0; c < R; ++c) acc = fma(Gi[r * R + c], b[c], acc);
+        if (acc > 0.0) passive |= 1ull << r;
+      }
+      for (int o = 16; o > 0; o >>= 1) passive |= __shfl_xor_sync(dev::kFull, passive, o);
+    }
     bool warm_phase = passive != 0ull;
     int iters = 0;
     bool failed = false;
@@ -183,7 +194,7 @@ __global__ void __launch_bounds__(WPB * 32)
     // an |N| x |N| Cholesky instead of a |P| x |P| one.  Accepted only at the
     // reference's optimum (s > 0 on P, no entering coordinate w_j > 1e-10 off
     // P: nnls_single's KKT test); otherwise the row takes the general path.
-    if (fast && warm_phase) {
+    if (fast && warm_phase && masks) {
       const unsigned long long nmask = full & ~passive;
       const int n0 = __popcll(nmask);
       if (n0 <= kNnlsFastN0) {
@@ -598,7 +609,7 @@ void nnls_launch(int R, std::int64_t n, const double* G, const double* B, double
   static DBuf<double> slab;
   slab.resize(static_cast<std::size_t>(blocks) * WPB * 3 * RP * RP);
   static DBuf<double> ginv;
-  const bool fast = masks && warm && !rowlist;
+  const bool fast = !rowlist && RP > 16;
   if (fast) {
     ginv.resize(static_cast<std::size_t>(RP) * RP + 1);
     k_ginv<RP><<<1, 32, 0, s>>>(R, G, ginv.get());
