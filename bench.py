@@ -335,13 +335,21 @@ def main():
             pin[name] = t
         Xp = p2g.CSRTensor(X.J, pin["subj_row_ptr"].numpy(), pin["row_ptr"].numpy(), pin["col_idx"].numpy(),
                            pin["val"].numpy())
+        # initial factors from pinned host memory too (column-major views)
+        pinned_f = []
+        for a in (H0, V0, W0):
+            t = torch.empty(a.size, dtype=torch.float64, pin_memory=True)
+            v = t.numpy().reshape(a.shape[::-1]).T
+            v[...] = a
+            pinned_f.append((t, v))
+        H0p, V0p, W0p = (v for _, v in pinned_f)
         e2e_iters = args.steps
         barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         ctx.load(Xp)
         t_load = time.perf_counter() - t0
-        res = ctx.fit(p2g.SolverConfig(rank=R, max_iters=e2e_iters, tol=1e-300, nonneg=True), H0, V0, W0,
+        res = ctx.fit(p2g.SolverConfig(rank=R, max_iters=e2e_iters, tol=1e-300, nonneg=True), H0p, V0p, W0p,
                       want_q=False)
         torch.cuda.synchronize()
         dt = time.perf_counter() - t0

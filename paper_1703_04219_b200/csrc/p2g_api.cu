@@ -531,6 +531,53 @@ void launch_rebase(std::int64_t* a, std::int64_t n, std::int64_t off, cudaStream
   if (off == 0 || n == 0) return;
   k_rebase<<<static_cast<int>(std::min<std::int64_t>((n + 255) / 256, 148 * 16)), 256, 0, s>>>(a, n, off);
 }
+
+// Device-side checks of a single-rank load (the host loops of
+// IrregularTensor::from_slices, sparse.hpp:176-193, read 0.7 GB of host
+// memory at cfg2): the first failing row in row order wins, as on the host.
+__global__ void k_check_rowptr(const std::int64_t* __restrict__ rp, std::int64_t NR,
+                               unsigned long long* __restrict__ bad) {
+  for (std::int64_t r = static_cast<std::int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; r < NR;
+       r += static_cast<std::int64_t>(gridDim.x) * blockDim.x)
+    if (rp[r + 1] < rp[r]) atomicMin(bad, static_cast<unsigned long long>(r));
+}
+/// bad = 4 * row + {2: column out of range, 3: not strictly ascending}, the
+/// first failing entry of the first failing row (host loop order).
+__global__ void k_check_cols(const std::int64_t* __restrict__ rp, const std::int32_t* __restrict__ ci,
+                             std::int64_t NR, std::int64_t J, unsigned long long* __restrict__ bad) {
+  for (std::int64_t r = static_cast<std::int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; r < NR;
+       r += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
+    const std::int64_t p0 = rp[r], p1 = rp[r + 1];
+    for (std::int64_t p = p0; p < p1; ++p) {
+      const std::int32_t j = ci[p];
+      int t = 0;
+      if (j < 0 || j >= J)
+        t = 2;
+      else if (p > p0 && j <= ci[p - 1])
+        t = 3;
+      if (t) {
+        atomicMin(bad, static_cast<unsigned long long>(r) * 4ull + static_cast<unsigned long long>(t));
+        break;
+      }
+    }
+  }
+}
+/// ||X||_F^2 partials: block b sums the fixed chunk [b n / B, (b + 1) n / B)
+/// with a fixed tree (deterministic); the host adds the B partials in order.
+constexpr int kNormBlocks = 1024;
+__global__ void __launch_bounds__(256) k_sumsq(const double* __restrict__ v, std::int64_t n, double* __restrict__ out) {
+  __shared__ double red[256];
+  const std::int64_t b0 = n * blockIdx.x / gridDim.x, b1 = n * (blockIdx.x + 1) / gridDim.x;
+  double a = 0.0;
+  for (std::int64_t p = b0 + threadIdx.x; p < b1; p += blockDim.x) a = fma(v[p], v[p], a);
+  red[threadIdx.x] = a;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if (static_cast<int>(threadIdx.x) < o) red[threadIdx.x] += red[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[blockIdx.x] = red[0];
+}
 }  // namespace
 }  // namespace p2g
 
@@ -539,6 +586,13 @@ extern "C" int p2g_load_csr(p2g_ctx* c, int64_t K, int64_t J, const int64_t* srp
   return guarded([&] {
     if (!c) throw InvalidArgument("null context");
     set_device(c);
+    const bool tim = std::getenv("P2G_TIMING") != nullptr;
+    const auto tl0 = std::chrono::steady_clock::now();
+    auto lap = [&](const char* what) {
+      if (tim)
+        std::fprintf(stderr, "[p2g] load %-12s %8.2f ms\n", what,
+                     std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tl0).count());
+    };
     // IrregularTensor::from_slices (sparse.hpp:176-193) validation.
     if (J <= 0) throw DataError("tensor must have at least one column");
     if (K <= 0) throw DataError("tensor must have at least one slice");
@@ -548,6 +602,10 @@ extern "C" int p2g_load_csr(p2g_ctx* c, int64_t K, int64_t J, const int64_t* srp
       if (srp[k + 1] < srp[k]) throw DataError("subj_row_ptr must be non-decreasing");
     const int64_t NRt = srp[K];
     if (rp[0] != 0) throw DataError("row_ptr must start at 0");
+    // One rank holds the whole tensor: the row-pointer / column checks and
+    // ||X||^2 run on the device after the upload (same errors, same order).
+    const bool dev_checks = c->world == 1;
+    if (!dev_checks) {
     // Row pointers first (over all rows, as the serial check), then column
     // range / ascending order within rows: both in parallel over fixed row
     // ranges, the first failing range reports.
@@ -562,8 +620,7 @@ extern "C" int p2g_load_csr(p2g_ctx* c, int64_t K, int64_t J, const int64_t* srp
     });
     for (int b : bad)
       if (b) throw DataError("row_ptr must be non-decreasing");
-    const int64_t nnz_t = rp[NRt];
-    if (nnz_t > 0 && (!ci || !val)) throw InvalidArgument("null CSR arrays");
+    if (rp[NRt] > 0 && (!ci || !val)) throw InvalidArgument("null CSR arrays");
     run_host_parallel(nthr, [&](int t) {
       for (int64_t r = NRt * t / nthr; r < NRt * (t + 1) / nthr && !bad[static_cast<std::size_t>(t)]; ++r)
         for (int64_t p = rp[r]; p < rp[r + 1]; ++p) {
@@ -581,13 +638,24 @@ extern "C" int p2g_load_csr(p2g_ctx* c, int64_t K, int64_t J, const int64_t* srp
       if (b == 2) throw DataError("column index out of range");
       if (b == 3) throw DataError("column indices must be strictly ascending within a row");
     }
-    // Shard by partition_weighted(nnz_k + I_k, world) (solver.hpp:263-267).
-    std::vector<std::uint64_t> w(static_cast<std::size_t>(K));
-    for (int64_t k = 0; k < K; ++k)
-      w[static_cast<std::size_t>(k)] =
-          static_cast<std::uint64_t>(rp[srp[k + 1]] - rp[srp[k]]) + static_cast<std::uint64_t>(srp[k + 1] - srp[k]);
+    }
+    lap("validated");
+    const int64_t nnz_t = rp[NRt];
+    if (nnz_t < 0) throw DataError("row_ptr must be non-decreasing");  // rp[0] = 0 > rp[NR]
+    if (nnz_t > 0 && (!ci || !val)) throw InvalidArgument("null CSR arrays");
+    c->loaded = false;  // the device checks below may still reject the tensor
+    // Shard by partition_weighted(nnz_k + I_k, world) (solver.hpp:263-267);
+    // one rank takes [0, K) (partition_weighted's single chunk).
     std::vector<std::pair<std::int64_t, std::int64_t>> parts;
-    partition_weighted(w.data(), K, c->world, parts);
+    if (c->world == 1) {
+      parts.emplace_back(0, K);
+    } else {
+      std::vector<std::uint64_t> w(static_cast<std::size_t>(K));
+      for (int64_t k = 0; k < K; ++k)
+        w[static_cast<std::size_t>(k)] =
+            static_cast<std::uint64_t>(rp[srp[k + 1]] - rp[srp[k]]) + static_cast<std::uint64_t>(srp[k + 1] - srp[k]);
+      partition_weighted(w.data(), K, c->world, parts);
+    }
     if (static_cast<int>(parts.size()) != c->world) throw DataError("fewer subjects than ranks");
     c->K_total = K;
     c->J = J;
@@ -616,6 +684,33 @@ extern "C" int p2g_load_csr(p2g_ctx* c, int64_t K, int64_t J, const int64_t* srp
       P2G_CUDA(cudaMemcpyAsync(c->ci.get(), ci + nz0, sizeof(int32_t) * c->nnz, cudaMemcpyHostToDevice, c->stream));
       P2G_CUDA(cudaMemcpyAsync(c->val.get(), val + nz0, sizeof(double) * c->nnz, cudaMemcpyHostToDevice, c->stream));
     }
+    lap("h2d issued");
+    if (dev_checks) {
+      DBuf<unsigned long long> bad;
+      bad.resize(2);
+      DBuf<double> part;
+      part.resize(kNormBlocks);
+      P2G_CUDA(cudaMemsetAsync(bad.get(), 0xff, sizeof(unsigned long long) * 2, c->stream));
+      const int g = static_cast<int>(std::max<std::int64_t>(1, std::min<std::int64_t>((NRt + 255) / 256, 148 * 8)));
+      k_check_rowptr<<<g, 256, 0, c->stream>>>(c->rp.get(), NRt, bad.get());
+      k_sumsq<<<kNormBlocks, 256, 0, c->stream>>>(c->val.get(), nnz_t, part.get());
+      unsigned long long hb[2];
+      std::vector<double> hp(kNormBlocks);
+      P2G_CUDA(cudaMemcpyAsync(hb, bad.get(), sizeof(hb), cudaMemcpyDeviceToHost, c->stream));
+      P2G_CUDA(cudaStreamSynchronize(c->stream));
+      if (hb[0] != ~0ull) throw DataError("row_ptr must be non-decreasing");
+      k_check_cols<<<g, 256, 0, c->stream>>>(c->rp.get(), c->ci.get(), NRt, J, bad.get() + 1);
+      P2G_CUDA(cudaMemcpyAsync(hb + 1, bad.get() + 1, sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->stream));
+      P2G_CUDA(cudaMemcpyAsync(hp.data(), part.get(), sizeof(double) * kNormBlocks, cudaMemcpyDeviceToHost, c->stream));
+      P2G_CUDA(cudaStreamSynchronize(c->stream));
+      if (hb[1] != ~0ull) {
+        if ((hb[1] & 3ull) == 2ull) throw DataError("column index out of range");
+        throw DataError("column indices must be strictly ascending within a row");
+      }
+      double acc = 0.0;
+      for (double v : hp) acc += v;
+      c->norm_x = acc;
+    } else {
     // ||X||_F^2 (sparse.hpp:219-223): slice order then entry order over all
     // subjects; the full host tensor is available on every rank.
     // fixed chunks summed in order: deterministic for a given thread count
@@ -631,8 +726,12 @@ extern "C" int p2g_load_csr(p2g_ctx* c, int64_t K, int64_t J, const int64_t* srp
       for (double v : part) acc += v;
       c->norm_x = acc;
     }
+    }
+    lap("norm");
     P2G_CUDA(cudaStreamSynchronize(c->stream));
+    lap("h2d done");
     build_csc(c);
+    lap("csc built");
     c->loaded = true;
     c->state_valid = false;
   });
@@ -662,6 +761,11 @@ extern "C" int p2g_fit(p2g_ctx* c, const p2g_fit_config* cfg, const double* H0, 
     validate_fit(c, cfg);
     if (!(c->norm_x > 0.0)) throw DataError("tensor has no non-zero entries");
     init_state(c, cfg, H0, V0, W0);
+    if (std::getenv("P2G_TIMING")) {
+      P2G_CUDA(cudaStreamSynchronize(c->stream));
+      std::fprintf(stderr, "[p2g] fit init_state %8.2f ms\n",
+                   std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count());
+    }
     double prev_fit = 0.0;
     int iters = 0;
     bool converged = false;
@@ -691,6 +795,9 @@ extern "C" int p2g_fit(p2g_ctx* c, const p2g_fit_config* cfg, const double* H0, 
     if (flags_out)
       P2G_CUDA(cudaMemcpyAsync(flags_out, c->flags.get(), sizeof(int32_t) * Ks(c), cudaMemcpyDeviceToHost, c->stream));
     P2G_CUDA(cudaStreamSynchronize(c->stream));
+    if (std::getenv("P2G_TIMING"))
+      std::fprintf(stderr, "[p2g] fit total      %8.2f ms (%d iterations)\n",
+                   std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count(), iters);
     if (summary) {
       summary->iterations = iters;
       summary->converged = converged ? 1 : 0;

@@ -309,3 +309,31 @@ def test_fit_bitwise_deterministic(ctx, p2g, R):
     assert np.array_equal(a.fit, b.fit)
     for x, y in ((a.H, b.H), (a.V, b.V), (a.W, b.W), (a.Q, b.Q)):
         assert np.array_equal(x, y)
+
+
+def test_load_validation_errors(ctx, p2g):
+    """IrregularTensor::from_slices checks (sparse.hpp:176-193), run on the
+    device for a single-rank load: same messages, first failing row wins, and
+    a rejected tensor leaves the context reloadable."""
+    good = dict(srp=np.array([0, 2, 3]), rp=np.array([0, 2, 3, 5]), ci=np.array([0, 2, 1, 0, 3], np.int32),
+                val=np.ones(5))
+
+    def load(**kw):
+        d = dict(good)
+        d.update(kw)
+        ctx.load(p2g.CSRTensor(4, d["srp"], d["rp"], d["ci"], d["val"]))
+
+    load()
+    with pytest.raises(p2g.DataError, match="row_ptr must be non-decreasing"):
+        load(rp=np.array([0, 2, 1, 5]))
+    with pytest.raises(p2g.DataError, match="column index out of range"):
+        load(ci=np.array([0, 2, 1, 0, 4], np.int32))
+    with pytest.raises(p2g.DataError, match="strictly ascending"):
+        load(ci=np.array([0, 2, 1, 3, 3], np.int32))
+    with pytest.raises(p2g.DataError, match="strictly ascending"):  # row 0 before row 2's range error
+        load(ci=np.array([2, 0, 1, 0, 9], np.int32))
+    with pytest.raises(p2g.DataError, match="column index out of range"):  # row 0 before row 2's order error
+        load(ci=np.array([0, 7, 1, 3, 3], np.int32))
+    load()
+    res = ctx.fit(p2g.SolverConfig(rank=1, max_iters=2, tol=1e-300))
+    assert np.all(np.isfinite(res.fit))
