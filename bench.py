@@ -343,6 +343,11 @@ def main():
             v[...] = a
             pinned_f.append((t, v))
         H0p, V0p, W0p = (v for _, v in pinned_f)
+        kb_, ke_, _, _ = ctx.shard_info()
+        outs = []
+        for shp in ((R, R), (X.J, R), (ke_ - kb_, R)):
+            t = torch.empty(shp[0] * shp[1], dtype=torch.float64, pin_memory=True)
+            outs.append((t, t.numpy().reshape(shp[::-1]).T))
         e2e_iters = args.steps
         barrier()
         torch.cuda.synchronize()
@@ -350,7 +355,7 @@ def main():
         ctx.load(Xp)
         t_load = time.perf_counter() - t0
         res = ctx.fit(p2g.SolverConfig(rank=R, max_iters=e2e_iters, tol=1e-300, nonneg=True), H0p, V0p, W0p,
-                      want_q=False)
+                      want_q=False, out=tuple(v for _, v in outs))
         torch.cuda.synchronize()
         dt = time.perf_counter() - t0
         if world > 1:

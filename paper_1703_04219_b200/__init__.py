@@ -493,8 +493,10 @@ class Context:
         return _FitConfig(int(cfg.rank), int(cfg.max_iters), float(cfg.tol), 1 if cfg.nonneg else 0,
                           2 if explicit else 0, int(cfg.seed) & ((1 << 64) - 1))
 
-    def fit(self, cfg: SolverConfig, H0=None, V0=None, W0=None, want_q: bool = True) -> FitResult:
-        """fit_parafac2 (solver.hpp:251-321) on this rank's shard."""
+    def fit(self, cfg: SolverConfig, H0=None, V0=None, W0=None, want_q: bool = True, out=None) -> FitResult:
+        """fit_parafac2 (solver.hpp:251-321) on this rank's shard.  `out` may
+        supply the (H, V, W) result arrays (column-major float64, e.g. views of
+        pinned host memory)."""
         X = self.tensor
         if X is None:
             raise InvalidArgument("no tensor loaded")
@@ -506,9 +508,15 @@ class Context:
             W0 = _f64(W0, (X.K, R))
         kb, ke, nr, _ = self.shard_info()
         Rv = max(R, 1)
-        H = np.empty((Rv, Rv), order="F")
-        V = np.empty((X.J, Rv), order="F")
-        W = np.empty((ke - kb, Rv), order="F")
+        if out is not None:
+            H, V, W = out
+            for a, shp in ((H, (Rv, Rv)), (V, (X.J, Rv)), (W, (ke - kb, Rv))):
+                if a.shape != shp or a.dtype != np.float64 or not a.flags.f_contiguous:
+                    raise InvalidArgument(f"out array must be column-major float64 of shape {shp}")
+        else:
+            H = np.empty((Rv, Rv), order="F")
+            V = np.empty((X.J, Rv), order="F")
+            W = np.empty((ke - kb, Rv), order="F")
         Q = np.empty((nr, Rv)) if want_q else None
         flags = np.empty(ke - kb, np.int32)
         n = max(int(cfg.max_iters), 1)

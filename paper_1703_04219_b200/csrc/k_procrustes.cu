@@ -232,8 +232,15 @@ __global__ void __launch_bounds__(WPB * 32) k_procrustes(K1Args a) {
 // ---------------------------------------------------------------------------
 template <int RP>
 struct AccSmem {
-  // per warp: T, Vj, M1, B, Es(eig A), Ee(eig E), TN + qchunk(32*RP) + xchunk(32*RP) + s, sig, cs, pq, idx
-  static constexpr int kPerWarpDoubles = 7 * RP * RP + 64 * RP + 3 * RP + 2 * (RP + 2) + RP;
+  // Shared memory per warp holds only what the Hestenes sweeps touch: Vj plus
+  // s, sig, cs, pq, idx.  The other R x R work matrices (T, M1, B, Es, Ee, TN)
+  // and the row chunks live in the warp's global slab next to A (L1/L2): with
+  // all seven in shared memory (112 KB at R = 40) one warp ran per SM.
+  static constexpr int kPerWarpDoubles = RP * RP + 3 * RP + 2 * (RP + 2) + RP;
+  __host__ __device__ static constexpr std::size_t slab(std::int64_t max_rows, int R) {
+    return 6 * static_cast<std::size_t>(RP) * RP + 64 * static_cast<std::size_t>(RP) +
+           static_cast<std::size_t>(max_rows > 1 ? max_rows : 1) * R;
+  }
 };
 
 template <int RP, int WPB>
@@ -245,16 +252,20 @@ __global__ void __launch_bounds__(WPB * 32) k_procrustes_accurate(K1Args a, doub
   const int RR = R * R;
   double* Hs = smem;
   double* base = smem + RP * RP + wid * AccSmem<RP>::kPerWarpDoubles;
-  double* T = base;
-  double* Vj = T + RP * RP;
-  double* M1 = Vj + RP * RP;
+  const std::int64_t gw = static_cast<std::int64_t>(blockIdx.x) * WPB + wid;
+  const std::int64_t nwarps = static_cast<std::int64_t>(gridDim.x) * WPB;
+  double* slab = a.scratch + gw * AccSmem<RP>::slab(a.max_rows, R);
+  double* T = slab;
+  double* M1 = T + RP * RP;
   double* B = M1 + RP * RP;
   double* EA = B + RP * RP;
   double* EE = EA + RP * RP;
   double* TN = EE + RP * RP;
   double* qch = TN + RP * RP;
   double* xch = qch + 32 * RP;
-  double* s = xch + 32 * RP;
+  double* A = xch + 32 * RP;  // I x R row-major
+  double* Vj = base;
+  double* s = Vj + RP * RP;
   double* sig = s + RP;
   double* cs = sig + RP;
   int* pq = reinterpret_cast<int*>(cs + RP + 2);
@@ -265,9 +276,6 @@ __global__ void __launch_bounds__(WPB * 32) k_procrustes_accurate(K1Args a, doub
   for (int e = lane; e < RR; e += 32) M1[e] = 0.0;
   __syncthreads();
 
-  const std::int64_t gw = static_cast<std::int64_t>(blockIdx.x) * WPB + wid;
-  const std::int64_t nwarps = static_cast<std::int64_t>(gridDim.x) * WPB;
-  double* A = a.scratch + gw * a.max_rows * R;  // I x R row-major
 
   // Flagged subjects come as a compacted, ascending list; warp gw takes the
   // contiguous share [gw L / W, (gw + 1) L / W): equal counts per warp and a
@@ -648,7 +656,9 @@ __global__ void __launch_bounds__(WPB * 32) k_procrustes_accurate(K1Args a, doub
   if (wid == 0) {
     for (int e = lane; e < RR; e += 32) {
       double acc = 0.0;
-      for (int w = 0; w < WPB; ++w) acc += smem[RP * RP + w * AccSmem<RP>::kPerWarpDoubles + 2 * RP * RP + e];
+      for (int w = 0; w < WPB; ++w)
+        acc += a.scratch[(static_cast<std::int64_t>(blockIdx.x) * WPB + w) * AccSmem<RP>::slab(a.max_rows, R) +
+                         RP * RP + e];
       m1_partials_acc[static_cast<std::int64_t>(blockIdx.x) * RR + e] = acc;
     }
   }
@@ -705,7 +715,7 @@ void compact_flagged(p2g_ctx* c, const std::int32_t* flags, cudaStream_t s) {
 
 template <int RP>
 constexpr int acc_wpb() {
-  return RP <= 16 ? 4 : (RP <= 32 ? 2 : 1);
+  return 4;
 }
 
 template <int RP>
@@ -798,8 +808,11 @@ int launch_procrustes_accurate(p2g_ctx* c, int R, const double* H, const double*
   a.nlist = c->acc_list.get() + std::max<std::int64_t>(c->k_end - c->k_begin, 1);
   int blocks = 0, wpb = 1;
   P2G_RP_DISPATCH(R, (blocks = acc_blocks<RP_>(c), wpb = acc_wpb<RP_>()));
-  // Per-warp scratch slabs holding A (I_max x R) of the subject in flight.
-  c->acc_scratch.resize(static_cast<std::size_t>(blocks) * wpb * static_cast<std::size_t>(c->max_rows) * R);
+  // Per-warp global slabs: A (I_max x R) of the subject in flight and the
+  // R x R work matrices (AccSmem).
+  std::size_t per_warp = 0;
+  P2G_RP_DISPATCH(R, per_warp = AccSmem<RP_>::slab(c->max_rows, R));
+  c->acc_scratch.resize(static_cast<std::size_t>(blocks) * wpb * per_warp);
   a.scratch = c->acc_scratch.get();
   P2G_RP_DISPATCH(R, launch_acc<RP_>(c, a, m1_partials, s));
   return blocks;
