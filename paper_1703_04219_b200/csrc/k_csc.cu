@@ -30,7 +30,7 @@ namespace p2g {
 namespace {
 
 constexpr std::int64_t kSeg = 256;  // entries per segment (one thread)
-constexpr int kRowBlockBits = 17;   // row blocks of 2^17 rows
+constexpr int kRowBlockBits = 16;   // row blocks of 2^16 rows (U block 21 MB at R = 40)
 
 __global__ void k_row_expand(std::int64_t NR, const std::int64_t* __restrict__ rp, std::int32_t* __restrict__ row_of) {
   for (std::int64_t r = static_cast<std::int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; r < NR;

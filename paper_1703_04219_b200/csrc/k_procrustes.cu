@@ -719,8 +719,8 @@ constexpr int acc_wpb() {
 }
 
 template <int RP>
-int acc_blocks(const p2g_ctx* c) {
-  return std::max(1, c->num_sms * 2);
+int acc_blocks(const p2g_ctx* c) {  // 4-warp CTAs: 8 warps/SM at R > 16 (254 registers), 16 below
+  return std::max(1, c->num_sms * (RP <= 16 ? 4 : 2));
 }
 
 template <int RP>
