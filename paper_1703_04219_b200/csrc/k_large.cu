@@ -426,7 +426,7 @@ __global__ void __launch_bounds__(kLgThreads, 2) k_procrustes_large(LgArgs a) {
 // resident), and the sweeps stop early:
 //
 //   Jacobi stops once the scaled off-diagonal max |M'_pq| / sqrt(M'_pp M'_qq)
-//   is at most kTauL = 3e-4 (instead of ~1e-12, one to two sweeps fewer), and
+//   is at most kTauL = 1e-4 (instead of ~1e-12, one to two sweeps fewer), and
 //   S' = M'^{-1/2} comes from the second-order Daleckii-Krein expansion of
 //   f(x) = x^{-1/2} about Lambda = diag(M'), with N = M' - Lambda:
 //     S' = f(Lambda) + sum_pq f[l_p, l_q] N_pq + sum_pqr f[l_p, l_r, l_q] N_pr N_rq
@@ -435,13 +435,13 @@ __global__ void __launch_bounds__(kLgThreads, 2) k_procrustes_large(LgArgs a) {
 //     S'_pq = delta_pq u_p + u_p u_q (C1 - A + P o C2)_pq,
 //     C1 = A diag(u) A,  C2 = A A
 //   (no eigenvalue gaps appear, so clustered eigenvalues are harmless).  The
-//   truncation error in Q is O(R tau^3): measured 8e-11 at tau = 3e-4 (2.4e-12 at 1e-4) with every
+//   truncation error in Q is O(R tau^3): measured 2.4e-12 at tau = 1e-4 (8e-11 at 3e-4) with every
 //   scaled off-diagonal at tau).  Then G^{-1/2} = E' S' E'^T with E' = E V',
 //   Z = V' S' E'^T, Q = B Z and m1_k = Z^T F as before.
 // ---------------------------------------------------------------------------
 // During the sweeps M is kept in its upper triangle only (M[min * LDM + max]):
 // half the shared-memory stores of a full symmetric update.
-constexpr double kTauL = 3e-4;   // Jacobi stop: max scaled off-diagonal (truncation error <= 8e-11 measured)
+constexpr double kTauL = 1e-4;   // Jacobi stop: max scaled off-diagonal (truncation error <= 3e-12 measured)
 constexpr double kSkipL = 1e-6;  // rotations below this scaled size are skipped (threshold Jacobi)
 
 template <int RP>
