@@ -16,6 +16,7 @@
 // pass adds each column's segment partials in row-block order:
 // deterministic, no atomics.
 #include <algorithm>
+#include <cstring>
 #include <vector>
 
 #include <cub/device/device_radix_sort.cuh>
@@ -221,86 +222,113 @@ __global__ void __launch_bounds__(WPB * 32)
 }  // namespace
 
 void build_csc(p2g_ctx* c) {
-  cudaStream_t s = c->stream;
+  sync_csc(c);
   const std::int64_t n = c->nnz, J = c->J;
   if (n > static_cast<std::int64_t>(0x7fffffff) || c->NR > static_cast<std::int64_t>(0x7fffffff))
     throw InvalidArgument("shard too large for 32-bit CSC indices");
+  if (!c->side) {
+    P2G_CUDA(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
+    P2G_CUDA(cudaEventCreateWithFlags(&c->ev_upload, cudaEventDisableTiming));
+    P2G_CUDA(cudaEventCreateWithFlags(&c->ev_csc, cudaEventDisableTiming));
+  }
+  // phase A on the side stream, behind everything the load queued so far
+  P2G_CUDA(cudaEventRecord(c->ev_upload, c->stream));
+  P2G_CUDA(cudaStreamWaitEvent(c->side, c->ev_upload, 0));
+  cudaStream_t s = c->side;
   const std::int64_t nblk = (c->NR >> kRowBlockBits) + 1;
   c->csc_row.resize(static_cast<std::size_t>(std::max<std::int64_t>(n, 1)));
   c->csc_val.resize(static_cast<std::size_t>(std::max<std::int64_t>(n, 1)));
   c->seg_ptr.resize(static_cast<std::size_t>(J + 1));
   c->nseg = 0;
   if (n == 0) {
-    P2G_CUDA(cudaMemsetAsync(c->seg_ptr.get(), 0, sizeof(std::int64_t) * (J + 1), s));
-    P2G_CUDA(cudaStreamSynchronize(s));
+    P2G_CUDA(cudaMemsetAsync(c->seg_ptr.get(), 0, sizeof(std::int64_t) * (J + 1), c->stream));
+    P2G_CUDA(cudaStreamSynchronize(c->stream));
     return;
   }
-  DBuf<std::int32_t> row_of, iota, perm;
-  DBuf<std::uint64_t> keys, skeys;
-  row_of.resize(static_cast<std::size_t>(n));
-  iota.resize(static_cast<std::size_t>(n));
-  perm.resize(static_cast<std::size_t>(n));
-  keys.resize(static_cast<std::size_t>(n));
-  skeys.resize(static_cast<std::size_t>(n));
-  k_row_expand<<<grid_for(c->NR, 256), 256, 0, s>>>(c->NR, c->rp.get(), row_of.get());
-  k_iota<<<grid_for(n, 256), 256, 0, s>>>(n, iota.get());
-  k_block_keys<<<grid_for(n, 256), 256, 0, s>>>(n, J, row_of.get(), c->ci.get(), keys.get());
+  c->csc_rowof.resize(static_cast<std::size_t>(n));
+  c->csc_iota.resize(static_cast<std::size_t>(n));
+  c->csc_perm.resize(static_cast<std::size_t>(n));
+  c->csc_keys.resize(static_cast<std::size_t>(n));
+  c->csc_skeys.resize(static_cast<std::size_t>(n));
+  std::int32_t* row_of = c->csc_rowof.get();
+  std::int32_t* iota = c->csc_iota.get();
+  std::int32_t* perm = c->csc_perm.get();
+  std::uint64_t* keys = c->csc_keys.get();
+  std::uint64_t* skeys = c->csc_skeys.get();
+  k_row_expand<<<grid_for(c->NR, 256), 256, 0, s>>>(c->NR, c->rp.get(), row_of);
+  k_iota<<<grid_for(n, 256), 256, 0, s>>>(n, iota);
+  k_block_keys<<<grid_for(n, 256), 256, 0, s>>>(n, J, row_of, c->ci.get(), keys);
   int bits = 1;
   while ((std::uint64_t{1} << bits) < static_cast<std::uint64_t>(nblk * J)) ++bits;
-  DBuf<unsigned char> temp;
-  std::size_t tbytes = 0;
-  P2G_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tbytes, keys.get(), skeys.get(), iota.get(), perm.get(),
-                                           static_cast<int>(n), 0, bits, s));
-  temp.resize(tbytes);
-  // LSD radix sort: stable, so a (row block, column) run keeps CSR (row-ascending) order
-  P2G_CUDA(cub::DeviceRadixSort::SortPairs(temp.get(), tbytes, keys.get(), skeys.get(), iota.get(), perm.get(),
-                                           static_cast<int>(n), 0, bits, s));
-  k_csc_gather<<<grid_for(n, 256), 256, 0, s>>>(n, perm.get(), row_of.get(), c->val.get(), c->csc_row.get(),
-                                                c->csc_val.get());
-  // segment heads: run starts (max-scan of change positions), split every kSeg
-  DBuf<std::int64_t> mark, runstart;
-  mark.resize(static_cast<std::size_t>(n));
-  runstart.resize(static_cast<std::size_t>(n));
-  k_run_marks<<<grid_for(n, 256), 256, 0, s>>>(n, skeys.get(), mark.get());
-  tbytes = 0;
-  P2G_CUDA(cub::DeviceScan::InclusiveScan(nullptr, tbytes, mark.get(), runstart.get(), cub::Max(), static_cast<int>(n), s));
-  temp.resize(tbytes);
-  P2G_CUDA(cub::DeviceScan::InclusiveScan(temp.get(), tbytes, mark.get(), runstart.get(), cub::Max(), static_cast<int>(n), s));
-  DBuf<unsigned char> head;
-  head.resize(static_cast<std::size_t>(n));
-  k_seg_heads<<<grid_for(n, 256), 256, 0, s>>>(n, runstart.get(), head.get());
+  std::size_t tbytes = 0, tb2 = 0, tb3 = 0;
+  P2G_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tbytes, keys, skeys, iota, perm, static_cast<int>(n), 0, bits, s));
+  c->csc_mark.resize(static_cast<std::size_t>(n));
+  c->csc_runstart.resize(static_cast<std::size_t>(n));
+  P2G_CUDA(cub::DeviceScan::InclusiveScan(nullptr, tb2, c->csc_mark.get(), c->csc_runstart.get(), cub::Max(),
+                                          static_cast<int>(n), s));
+  c->csc_head.resize(static_cast<std::size_t>(n));
   c->seg_beg.resize(static_cast<std::size_t>(n));
-  DBuf<std::int64_t> nsel;
-  nsel.resize(1);
+  c->csc_nsel.resize(1);
   thrust::counting_iterator<std::int64_t> idx(0);
-  tbytes = 0;
-  P2G_CUDA(cub::DeviceSelect::Flagged(nullptr, tbytes, idx, head.get(), c->seg_beg.get(), nsel.get(),
+  P2G_CUDA(cub::DeviceSelect::Flagged(nullptr, tb3, idx, c->csc_head.get(), c->seg_beg.get(), c->csc_nsel.get(),
                                       static_cast<int>(n), s));
-  temp.resize(tbytes);
-  P2G_CUDA(cub::DeviceSelect::Flagged(temp.get(), tbytes, idx, head.get(), c->seg_beg.get(), nsel.get(),
-                                      static_cast<int>(n), s));
+  // one temp allocation for the three passes (no frees, which would sync the device)
+  c->csc_temp.resize(std::max({tbytes, tb2, tb3}));
+  tbytes = c->csc_temp.n;
+  // LSD radix sort: stable, so a (row block, column) run keeps CSR (row-ascending) order
+  P2G_CUDA(cub::DeviceRadixSort::SortPairs(c->csc_temp.get(), tbytes, keys, skeys, iota, perm, static_cast<int>(n), 0,
+                                           bits, s));
+  k_csc_gather<<<grid_for(n, 256), 256, 0, s>>>(n, perm, row_of, c->val.get(), c->csc_row.get(), c->csc_val.get());
+  // segment heads: run starts (max-scan of change positions), split every kSeg
+  k_run_marks<<<grid_for(n, 256), 256, 0, s>>>(n, skeys, c->csc_mark.get());
+  tb2 = c->csc_temp.n;
+  P2G_CUDA(cub::DeviceScan::InclusiveScan(c->csc_temp.get(), tb2, c->csc_mark.get(), c->csc_runstart.get(),
+                                          cub::Max(), static_cast<int>(n), s));
+  k_seg_heads<<<grid_for(n, 256), 256, 0, s>>>(n, c->csc_runstart.get(), c->csc_head.get());
+  tb3 = c->csc_temp.n;
+  P2G_CUDA(cub::DeviceSelect::Flagged(c->csc_temp.get(), tb3, idx, c->csc_head.get(), c->seg_beg.get(),
+                                      c->csc_nsel.get(), static_cast<int>(n), s));
+  P2G_CUDA(cudaMemcpyAsync(c->pinned + 60, c->csc_nsel.get(), sizeof(std::int64_t), cudaMemcpyDeviceToHost, s));
+  c->csc_pending = true;
+}
+
+/// Phase B of the CSC build (per-column segment lists in row-block order:
+/// segment ids sorted by col * nblk + block), then the main stream waits for it.
+void ensure_csc(p2g_ctx* c) {
+  if (!c->csc_pending) return;
+  cudaStream_t s = c->side;
+  P2G_CUDA(cudaStreamSynchronize(s));  // phase A done: the segment count is on the host
   std::int64_t nseg = 0;
-  P2G_CUDA(cudaMemcpyAsync(&nseg, nsel.get(), sizeof(std::int64_t), cudaMemcpyDeviceToHost, s));
-  P2G_CUDA(cudaStreamSynchronize(s));
+  std::memcpy(&nseg, c->pinned + 60, sizeof(nseg));
   c->nseg = nseg;
-  // per-column segment lists in row-block order: sort segment ids by col * nblk + block
-  DBuf<std::uint64_t> ck, sck;
-  DBuf<std::int32_t> ids;
-  ck.resize(static_cast<std::size_t>(nseg));
-  sck.resize(static_cast<std::size_t>(nseg));
-  ids.resize(static_cast<std::size_t>(nseg));
+  const std::int64_t J = c->J;
+  const std::int64_t nblk = (c->NR >> kRowBlockBits) + 1;
+  c->csc_ck.resize(static_cast<std::size_t>(nseg));
+  c->csc_sck.resize(static_cast<std::size_t>(nseg));
+  c->csc_ids.resize(static_cast<std::size_t>(nseg));
   c->seg_ids.resize(static_cast<std::size_t>(nseg));
-  k_seg_colkeys<<<grid_for(nseg, 256), 256, 0, s>>>(nseg, J, nblk, c->seg_beg.get(), skeys.get(), ck.get(), ids.get());
+  k_seg_colkeys<<<grid_for(nseg, 256), 256, 0, s>>>(nseg, J, nblk, c->seg_beg.get(), c->csc_skeys.get(),
+                                                    c->csc_ck.get(), c->csc_ids.get());
   int cbits = 1;
   while ((std::uint64_t{1} << cbits) < static_cast<std::uint64_t>(nblk * J)) ++cbits;
-  tbytes = 0;
-  P2G_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tbytes, ck.get(), sck.get(), ids.get(), c->seg_ids.get(),
-                                           static_cast<int>(nseg), 0, cbits, s));
-  temp.resize(tbytes);
-  P2G_CUDA(cub::DeviceRadixSort::SortPairs(temp.get(), tbytes, ck.get(), sck.get(), ids.get(), c->seg_ids.get(),
-                                           static_cast<int>(nseg), 0, cbits, s));
-  k_key_ptr<<<grid_for(J + 1, 256), 256, 0, s>>>(J, nseg, nblk, sck.get(), c->seg_ptr.get());
-  P2G_CUDA(cudaStreamSynchronize(s));
+  std::size_t tbytes = 0;
+  P2G_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tbytes, c->csc_ck.get(), c->csc_sck.get(), c->csc_ids.get(),
+                                           c->seg_ids.get(), static_cast<int>(nseg), 0, cbits, s));
+  c->csc_temp.resize(tbytes);
+  tbytes = c->csc_temp.n;
+  P2G_CUDA(cub::DeviceRadixSort::SortPairs(c->csc_temp.get(), tbytes, c->csc_ck.get(), c->csc_sck.get(),
+                                           c->csc_ids.get(), c->seg_ids.get(), static_cast<int>(nseg), 0, cbits, s));
+  k_key_ptr<<<grid_for(J + 1, 256), 256, 0, s>>>(J, nseg, nblk, c->csc_sck.get(), c->seg_ptr.get());
+  P2G_CUDA(cudaEventRecord(c->ev_csc, s));
+  P2G_CUDA(cudaStreamWaitEvent(c->stream, c->ev_csc, 0));
+  c->csc_pending = false;
+}
+
+/// Completes any pending build and waits for the side stream (before the
+/// shard buffers it reads are replaced, and at teardown).
+void sync_csc(p2g_ctx* c) {
+  ensure_csc(c);
+  if (c->side) P2G_CUDA(cudaStreamSynchronize(c->side));
 }
 
 template <int RP>
@@ -310,6 +338,7 @@ static void seg_spmm(p2g_ctx* c, int R, const double* U, cudaStream_t s) {
 }
 
 void launch_csc_mode2(p2g_ctx* c, int R, const double* U, double* M2, cudaStream_t s) {
+  ensure_csc(c);
   c->seg_part.resize(static_cast<std::size_t>(std::max<std::int64_t>(c->nseg, 1)) * R);
   if (c->nseg > 0) {
     if (R <= 2)

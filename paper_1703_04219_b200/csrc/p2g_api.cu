@@ -497,6 +497,12 @@ extern "C" int p2g_destroy(p2g_ctx* c) {
       if (c->nccl->comm) nccl_api().CommDestroy(c->nccl->comm);
       delete c->nccl;
     }
+    if (c->side) {
+      cudaStreamSynchronize(c->side);
+      cudaStreamDestroy(c->side);
+      cudaEventDestroy(c->ev_upload);
+      cudaEventDestroy(c->ev_csc);
+    }
     for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
     if (c->pinned) cudaFreeHost(c->pinned);
     if (c->stream) cudaStreamDestroy(c->stream);
@@ -643,6 +649,7 @@ extern "C" int p2g_load_csr(p2g_ctx* c, int64_t K, int64_t J, const int64_t* srp
     const int64_t nnz_t = rp[NRt];
     if (nnz_t < 0) throw DataError("row_ptr must be non-decreasing");  // rp[0] = 0 > rp[NR]
     if (nnz_t > 0 && (!ci || !val)) throw InvalidArgument("null CSR arrays");
+    sync_csc(c);        // a previous load's CSC build may still read the shard buffers
     c->loaded = false;  // the device checks below may still reject the tensor
     // Shard by partition_weighted(nnz_k + I_k, world) (solver.hpp:263-267);
     // one rank takes [0, K) (partition_weighted's single chunk).

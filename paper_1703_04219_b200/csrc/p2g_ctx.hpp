@@ -135,6 +135,16 @@ struct p2g_ctx {
   p2g::DBuf<std::int32_t> csc_row, seg_ids;
   p2g::DBuf<double> csc_val, seg_part, Ubuf;
   std::int64_t nseg = 0;
+  // The CSC build runs on `side` behind the load's upload (phase A: the big
+  // sort, overlapping the first Procrustes step) and is finished at its first
+  // use (phase B needs the segment count on the host): build_csc / ensure_csc.
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_upload = nullptr, ev_csc = nullptr;
+  bool csc_pending = false;
+  p2g::DBuf<std::int32_t> csc_rowof, csc_iota, csc_perm, csc_ids;
+  p2g::DBuf<std::uint64_t> csc_keys, csc_skeys, csc_ck, csc_sck;
+  p2g::DBuf<std::int64_t> csc_mark, csc_runstart, csc_nsel;
+  p2g::DBuf<unsigned char> csc_head, csc_temp;
   p2g::DBuf<unsigned> mask_v, mask_w; // NNLS passive sets of the previous iteration (warm start)
   p2g::DBuf<unsigned long long> mask64_v, mask64_w;  // same, R > 16
   p2g::DBuf<std::uint8_t> polar_sweeps, polar_keys;  // per-subject Jacobi sweeps of the last polar step
@@ -163,6 +173,8 @@ int launch_procrustes(p2g_ctx* c, int R, const double* H, const double* V, const
 // Accurate Jacobi-SVD path over the subjects flagged P2G_FLAG_ACCURATE;
 // writes one R x R m1 partial per block (count = procrustes_accurate_blocks).
 void build_csc(p2g_ctx* c);
+void ensure_csc(p2g_ctx* c);
+void sync_csc(p2g_ctx* c);
 void launch_csc_mode2(p2g_ctx* c, int R, const double* U, double* M2, cudaStream_t s);
 void launch_urows_large(p2g_ctx* c, int R, const double* Q, const double* H, const double* W, const double* nH,
                         double* U, cudaStream_t s);
