@@ -470,6 +470,13 @@ struct LgWarp {
   }
 };
 
+/// Logical index held by physical position x (pair slot x / 2, p side for even
+/// x, q side for odd x) in round 0 of the round-robin of sched below; after a
+/// round every position moves along one fixed cycle (see the V' rows below).
+__host__ __device__ constexpr int rr_l0(int m, int x) {
+  return (x & 1) ? ((x >> 1) == 0 ? m - 1 : m - 1 - (x >> 1)) : (x >> 1);
+}
+
 /// out(i, j) for i < rows, j < R of the product sum_c a(i, c) b(c, j), c < R,
 /// on DMMA m8n8k4 (row.col): lane (fm, fk) feeds A[fm][fk] and B[fk][fm] and
 /// holds C[fm][2 fk + h].  8-row tiles of the output in turn, all RP/8
@@ -556,7 +563,11 @@ __global__ void __launch_bounds__(LgWarp<RP>::WPB * 32, 1) k_procrustes_large_w(
   // this lane's share of every round: 2 x 2 blocks (slot i1 | i2 << 8) of M
   // and (slot | column offset << 8) items of V'^T, fixed for the whole kernel
   constexpr int kLaneBlk = (L::NBLK + 31) / 32;
-  constexpr int kLaneVit = ((RP / 2) * (RP / 2) + 31) / 32;
+  // V' rows 0..31 of an exact-R subject live in registers (one row per lane,
+  // below); only rows 32..R-1 (R = 40) stay as shared-memory items
+  constexpr int kRegRows = EXACT ? (RP < 32 ? RP : 32) : 0;
+  constexpr int kSmemKp = RP / 2 - kRegRows / 2;  // column pairs of V'^T still in shared memory
+  constexpr int kLaneVit = kSmemKp > 0 ? (kSmemKp * (RP / 2) + 31) / 32 : 1;
   int lblk[kLaneBlk], lvit[kLaneVit];
 #pragma unroll
   for (int j = 0; j < kLaneBlk; ++j) {
@@ -564,12 +575,13 @@ __global__ void __launch_bounds__(LgWarp<RP>::WPB * 32, 1) k_procrustes_large_w(
     lblk[j] = it < nblk ? ((blk[it] >> 8) | ((blk[it] & 0xff) << 8)) : -1;
   }
   {
-    const int nkp = (R + 1) >> 1;
+    const int kp0 = kRegRows / 2;
+    const int nkp = ((R + 1) >> 1) - kp0;
 #pragma unroll
     for (int j = 0; j < kLaneVit; ++j) {
       const int it = lane + 32 * j;
-      const int sl = it / nkp, kp = it - sl * nkp;  // consecutive lanes: consecutive 16-byte units of a row
-      lvit[j] = it < nkp * half ? (sl | ((2 * kp) << 8)) : -1;
+      const int sl = nkp > 0 ? it / nkp : 0, kp = kp0 + (nkp > 0 ? it - sl * nkp : 0);  // consecutive lanes: consecutive 16-byte units
+      lvit[j] = (nkp > 0 && it < nkp * half) ? (sl | ((2 * kp) << 8)) : -1;
     }
   }
   const std::int64_t gw = static_cast<std::int64_t>(blockIdx.x) * WPB + wid;
@@ -690,11 +702,14 @@ __global__ void __launch_bounds__(LgWarp<RP>::WPB * 32, 1) k_procrustes_large_w(
         flag = P2G_FLAG_ACCURATE;
         break;
       }
-      // V' = I
+      // V' = I; row `lane` of V' also in registers, in round-0 physical order
       for (int e = lane; e < R * LDV; e += 32) {
         const int p = e / LDV, kk = e - p * LDV;
         Vt[e] = p == kk ? 1.0 : 0.0;
       }
+      double vreg[kRegRows > 0 ? RP : 1];
+#pragma unroll
+      for (int x = 0; x < (kRegRows > 0 ? RP : 1); ++x) vreg[x] = rr_l0(RP, x) == lane ? 1.0 : 0.0;
       bool converged = false;
       int sweeps = 0;
       double off = 0.0;  // scaled off-diagonal mass at the start of the pass
@@ -817,10 +832,31 @@ __global__ void __launch_bounds__(LgWarp<RP>::WPB * 32, 1) k_procrustes_large_w(
           __syncwarp();
           // next round's parameter loads (M is final for this round) ...
           const PIn nxt = param_load(round + 1 < m - 1 ? round + 1 : 0);
-          // ... V' <- V' J: rows p, q of V'^T (offset p LDV = p LDM + p) over this
-          // lane's column pairs, branch-free so the parameter tail interleaves ...
+          // ... V' <- V' J.  Register rows: slot i's pair sits at positions
+          // (2i, 2i+1); afterwards every position moves one step along the
+          // fixed cycle 0 <- 2 <- ... <- RP-2 <- RP-1 <- RP-3 <- ... <- 3 <- 0
+          // (position 1, index RP-1, stays), which is how the round-robin's
+          // pairs advance, so the next round's pairs are again (2i, 2i+1) ...
+          if constexpr (kRegRows > 0) {
 #pragma unroll
-          for (int j = 0; j < kLaneVit; ++j) {
+            for (int i = 0; i < RP / 2; ++i) {
+              const double2 r = rot[i];
+              const double x0 = vreg[2 * i], y0 = vreg[2 * i + 1];
+              vreg[2 * i] = r.x * x0 - r.y * y0;
+              vreg[2 * i + 1] = r.y * x0 + r.x * y0;
+            }
+            const double t0 = vreg[0];
+#pragma unroll
+            for (int l = 0; l < RP / 2 - 1; ++l) vreg[2 * l] = vreg[2 * l + 2];
+            vreg[RP - 2] = vreg[RP - 1];
+#pragma unroll
+            for (int l = RP / 2 - 1; l >= 2; --l) vreg[2 * l + 1] = vreg[2 * l - 1];
+            vreg[3] = t0;
+          }
+          // ... shared-memory rows: p, q of V'^T (offset p LDV = p LDM + p) over
+          // this lane's column pairs, branch-free so the parameter tail interleaves ...
+#pragma unroll
+          for (int j = 0; j < (kSmemKp > 0 ? kLaneVit : 0); ++j) {
             const int v = lvit[j];
             const int sl = v & 0xff, kc = (v >> 8) & 0xff;
             const double2 r = rot[v < 0 ? 0 : sl];
@@ -838,6 +874,14 @@ __global__ void __launch_bounds__(LgWarp<RP>::WPB * 32, 1) k_procrustes_large_w(
           param_store(nxt, buf ^ 1);
           __syncwarp();
         }
+      }
+      // register rows back (whole sweeps bring positions back to round-0 order)
+      if constexpr (kRegRows > 0) {
+        if (lane < R) {
+#pragma unroll
+          for (int x = 0; x < RP; ++x) Vt[rr_l0(RP, x) * LDV + lane] = vreg[x];
+        }
+        __syncwarp();
       }
       if (a.dbg && lane == 0) {
         atomicAdd(a.dbg + 16 + min(sweeps, 9), 1);
