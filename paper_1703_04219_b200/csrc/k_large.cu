@@ -6,22 +6,21 @@
 // column pairs of length I_k, and unpreconditioned A needs ~10 sweeps: far
 // too slow, and the Gram route (eig of A^T A) squares the condition number.
 //
-// B200 design: one 128-thread CTA per subject, persistent.
+// B200 design: one warp per subject, persistent (k_procrustes_large_w below).
 //   E    = right singular vectors of A from the previous Procrustes step
 //          (Ewarm, K x R x R in HBM; identity on the first step)
-//   B    = A E = X_k V T,  T = D H^T E   (thread per row, rows to a slab)
-//   M    = B^T B,  F = B^T (X_k V D)     (thread-owned entries over the slab)
-//   two-sided Jacobi on M with the oracle's rotation and skip rule
-//   (|M_pq| <= 1e-15 sqrt(M_pp M_qq)): in exact arithmetic this is the
-//   one-sided Jacobi of B.  With E from the previous step the columns of B
-//   are nearly orthogonal (scaled off-diagonal of M small), the case in which
-//   two-sided Jacobi on M has the relative accuracy of one-sided Jacobi on B
-//   (Demmel-Veselic); when they are not (first step, or factors moved), E is
-//   refreshed from this solve and the subject is redone once if it is also
-//   ill-conditioned (sigma_min^2 < 1e-6 sigma_max^2; otherwise the Gram
-//   route's eps kappa^2 error is below 1e-10, as in the small-R fast path).
-//   sigma_j^2 = M'_jj,  V_A = E V',  Q = B V' Sigma^-1 V_A^T = B Z,
-//   m1_k = Q^T X_k V D = Z^T F.
+//   X~   = X_k V D (lane per row),  B = A E = X~ (H^T E)      (DMMA)
+//   M    = B^T B,  F = B^T X~                                   (DMMA)
+//   two-sided Jacobi on M with the oracle's rotation: in exact arithmetic
+//   the one-sided Jacobi of B.  With E from the previous step the columns of
+//   B are nearly orthogonal, the case in which two-sided Jacobi on M has the
+//   relative accuracy of one-sided Jacobi on B (Demmel-Veselic); when they
+//   are not (first step, or factors moved), E is refreshed from this solve
+//   and the subject is redone once if it is also ill-conditioned
+//   (sigma_min^2 < 1e-6 sigma_max^2; otherwise the Gram route's eps kappa^2
+//   error is below 1e-10, as in the small-R fast path).  The sweeps stop at a
+//   scaled off-diagonal of 1e-4 and M'^{-1/2} gets a second-order correction
+//   (below).  V_A = E V',  Q = B V' S' V_A^T = B Z,  m1_k = Q^T X~ = Z^T F.
 // Rank-deficient (canonical rule D5), non-finite or non-converged subjects
 // are flagged P2G_FLAG_ACCURATE and finished by k_procrustes_accurate, which
 // takes V_A (stored in Ewarm) as its preconditioner.
@@ -34,9 +33,7 @@
 namespace p2g {
 namespace {
 
-constexpr int kLgThreads = 128;
 constexpr int kLgMaxSweeps = 40;
-constexpr double kTolL = 1e-12;   // two-sided skip tolerance (scaled off-diagonal)
 constexpr double kTinyL = 1e-24;  // M_pp below this x max diag: near-null column (covers D5's 1e-26)
 
 struct LgArgs {
@@ -55,373 +52,10 @@ struct LgArgs {
   int* dbg;  // optional: [0] sweeps, [1] max sweeps, [2] redone subjects, [3] subjects
 };
 
-template <int RP>
-struct LgSmem {
-  static constexpr int LDM = RP + 1;
-  static constexpr int kMat = RP * LDM;
-  // Hs, E, T (then Z), M, Vp, M1acc, work (E V' product)
-  static constexpr int kDoubles = 7 * kMat + 5 * RP + 8;
-  static constexpr int kInts = RP + 8 + (RP / 2) * (RP / 2 + 1) / 4 + 2;  // pairs + uint16 block table
-};
-
-__device__ __forceinline__ double block_sum(double v, double* red) {
-  v = dev::warp_sum(v);
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  __syncthreads();
-  if (lane == 0) red[wid] = v;
-  __syncthreads();
-  double t = 0.0;
-  for (int w = 0; w < kLgThreads / 32; ++w) t += red[w];
-  return t;
-}
-
-template <int RP, bool EXACT>
-__global__ void __launch_bounds__(kLgThreads, 2) k_procrustes_large(LgArgs a) {
-  extern __shared__ double smem[];
-  const int tid = threadIdx.x;
-  const int R = EXACT ? RP : a.R;  // exact-R instances fold the index arithmetic
-  const int RR = R * R;
-  constexpr int LDM = LgSmem<RP>::LDM;  // odd leading dimension: column walks are bank-conflict free
-  constexpr int kMat = LgSmem<RP>::kMat;
-  double* Hs = smem;
-  double* E = Hs + kMat;
-  double* T = E + kMat;  // T, later Z
-  double* M = T + kMat;
-  double* Vp = M + kMat;
-  double* M1 = Vp + kMat;
-  double* Wk = M1 + kMat;  // E V' product
-  double* w = Wk + kMat;   // W_k (RP)
-  double* sig = w + RP;    // sigma (RP)
-  double* rc = sig + RP;   // rotation c (RP/2)
-  double* rs = rc + RP;   // rotation s (RP/2)
-  double* rt = rs + RP;    // diagonal shift t M_pq (RP/2)
-  double* red = rt + RP;   // 4 warp partials + flags
-  int* rp = reinterpret_cast<int*>(red + 8);  // rotation pairs (RP ints: p, q)
-  std::uint16_t* blk = reinterpret_cast<std::uint16_t*>(rp + RP);  // (i1 << 8 | i2), i1 <= i2 < RP/2
-
-  for (int e = tid; e < RR; e += kLgThreads) {
-    Hs[(e / R) * LDM + e % R] = a.H[e];
-    M1[(e / R) * LDM + e % R] = 0.0;
-  }
-  __syncthreads();
-  double* Bs = a.slab + static_cast<std::int64_t>(blockIdx.x) * 2 * a.max_rows * R;
-  double* Xs = Bs + a.max_rows * R;
-  const int m = (R + 1) & ~1;  // players incl. one dummy for odd R
-  const int half = m / 2;
-  const int nblk = half * (half + 1) / 2;
-  for (int it = tid; it < nblk; it += kLgThreads) {  // block-pair table, row-major upper triangle
-    int i1 = 0, r = it;
-    while (r >= half - i1) {
-      r -= half - i1;
-      ++i1;
-    }
-    blk[it] = static_cast<std::uint16_t>((i1 << 8) | (i1 + r));
-  }
-
-  constexpr int NW = kLgThreads / 32;
-  constexpr int NP = (RP + NW - 1) / NW;  // rows p of M owned by a warp in the M/F build
-  const int lane = tid & 31, wid = tid >> 5;
-  for (std::int64_t k = blockIdx.x; k < a.X.K; k += gridDim.x) {
-    const std::int64_t r0 = a.X.srp[k];
-    const int I = static_cast<int>(a.X.srp[k + 1] - r0);
-    for (int r = tid; r < R; r += kLgThreads) w[r] = a.W[k * R + r];
-    double* Ek = a.Ewarm + k * RR;
-    for (int i = wid; i < R; i += NW)
-      for (int j = lane; j < R; j += 32) E[i * LDM + j] = a.ew_valid ? Ek[i * R + j] : (i == j ? 1.0 : 0.0);
-    __syncthreads();
-    int flag = P2G_FLAG_FULL_RANK;
-    for (int pass = 0; pass < 2; ++pass) {
-      // T = D H^T E
-      for (int i = wid; i < R; i += NW)
-        for (int j = lane; j < R; j += 32) {
-          double acc = 0.0;
-          for (int c = 0; c < R; ++c) acc = fma(Hs[c * LDM + i], E[c * LDM + j], acc);
-          T[i * LDM + j] = acc * w[i];
-        }
-      __syncthreads();
-      // Pass A: b_i = xv_i T (slab), x~_i = xv_i o w (slab, first pass only)
-      for (int i = tid; i < I; i += kLgThreads) {
-        double xv[RP];
-        dev::csr_row_times<RP>(xv, a.X.ci, a.X.val, a.X.rp[r0 + i], a.X.rp[r0 + i + 1], a.V, R);
-        double* brow = Bs + static_cast<std::int64_t>(i) * R;
-        for (int j = 0; j < R; ++j) {
-          double acc = 0.0;
-#pragma unroll
-          for (int c = 0; c < RP; ++c)
-            if (c < R) acc = fma(xv[c], T[c * LDM + j], acc);
-          brow[j] = acc;
-        }
-        if (pass == 0) {
-          double* xrow = Xs + static_cast<std::int64_t>(i) * R;
-#pragma unroll
-          for (int c = 0; c < RP; ++c)
-            if (c < R) xrow[c] = xv[c] * w[c];
-        }
-      }
-      __syncthreads();
-      // M = B^T B, F = B^T X~: warp owns rows p = wid + NW pp, lanes own columns
-      // q = lane, lane + 32 (coalesced slab rows, broadcast b_ip).
-      bool finite = true;
-      {
-        double mm[NP][2], ff[NP][2];
-#pragma unroll
-        for (int pp = 0; pp < NP; ++pp) mm[pp][0] = mm[pp][1] = ff[pp][0] = ff[pp][1] = 0.0;
-        const bool q1ok = lane + 32 < R;
-        for (int i = 0; i < I; ++i) {
-          const double* brow = Bs + static_cast<std::int64_t>(i) * R;
-          const double* xrow = Xs + static_cast<std::int64_t>(i) * R;
-          const double b0 = lane < R ? brow[lane] : 0.0, x0 = lane < R ? xrow[lane] : 0.0;
-          const double b1 = q1ok ? brow[lane + 32] : 0.0, x1 = q1ok ? xrow[lane + 32] : 0.0;
-#pragma unroll
-          for (int pp = 0; pp < NP; ++pp) {
-            const int pr = wid + NW * pp;
-            if (pr < R) {
-              const double bp = brow[pr];
-              mm[pp][0] = fma(bp, b0, mm[pp][0]);
-              ff[pp][0] = fma(bp, x0, ff[pp][0]);
-              mm[pp][1] = fma(bp, b1, mm[pp][1]);
-              ff[pp][1] = fma(bp, x1, ff[pp][1]);
-            }
-          }
-        }
-#pragma unroll
-        for (int pp = 0; pp < NP; ++pp) {
-          const int pr = wid + NW * pp;
-          if (pr >= R) continue;
-          if (lane < R) {
-            M[pr * LDM + lane] = mm[pp][0];
-            Wk[pr * LDM + lane] = ff[pp][0];  // F
-            finite &= isfinite(mm[pp][0]) && isfinite(ff[pp][0]);
-          }
-          if (q1ok) {
-            M[pr * LDM + lane + 32] = mm[pp][1];
-            Wk[pr * LDM + lane + 32] = ff[pp][1];
-            finite &= isfinite(mm[pp][1]) && isfinite(ff[pp][1]);
-          }
-        }
-      }
-      finite = __syncthreads_and(finite);
-      if (!finite) {  // the accurate path re-checks the operand; no preconditioner from here
-        for (int i = wid; i < R; i += NW)
-          for (int j = lane; j < R; j += 32) E[i * LDM + j] = i == j ? 1.0 : 0.0;
-        __syncthreads();
-        flag = P2G_FLAG_ACCURATE;
-        break;
-      }
-      // scaled off-diagonal mass ||D^-1 M D^-1 - I||_F^2
-      double off = 0.0;
-      for (int p = wid; p < R; p += NW)
-        for (int q = lane; q < R; q += 32) {
-          const double d = M[p * LDM + p] * M[q * LDM + q];
-          if (p != q && d > 0.0) off += M[p * LDM + q] * M[p * LDM + q] / d;
-          Vp[p * LDM + q] = p == q ? 1.0 : 0.0;
-        }
-      off = block_sum(off, red);
-      // Two-sided Jacobi on M (round-robin ordering; rotations of a round are disjoint).
-      // Columns with M_pp <= kTinyL max_j M_jj (sigma below 1e-12 sigma_max) are
-      // not rotated: their off-diagonals sit at the rounding floor of the large
-      // entries; such subjects go to the accurate path below.
-      bool converged = false;
-      int sweeps = 0;
-      double dmax = 0.0;
-      for (int sweep = 0; sweep < kLgMaxSweeps; ++sweep, ++sweeps) {
-        dmax = 0.0;
-        for (int j = 0; j < R; ++j) dmax = fmax(dmax, M[j * LDM + j]);
-        const double tiny = kTinyL * dmax;
-        bool need = false;
-        for (int p = wid; p < R; p += NW)
-          for (int q = lane; q < R; q += 32) {
-            if (q <= p) continue;
-            const double al = M[p * LDM + p], be = M[q * LDM + q], ga = M[p * LDM + q];
-            if (al > tiny && be > tiny && !(ga == 0.0 || fabs(ga) <= kTolL * sqrt(al * be))) need = true;
-          }
-        if (!__syncthreads_or(need)) {
-          converged = true;
-          break;
-        }
-        for (int round = 0; round < m - 1; ++round) {
-          if (tid < half) {
-            int p, q;
-            if (tid == 0) {
-              p = round;
-              q = m - 1;
-            } else {
-              p = (round + tid) % (m - 1);
-              q = (round - tid + (m - 1)) % (m - 1);
-            }
-            if (p > q) {
-              const int t = p;
-              p = q;
-              q = t;
-            }
-            double c = 1.0, s = 0.0, tt = 0.0, ga = 0.0;
-            if (q < R) {
-              const double al = M[p * LDM + p], be = M[q * LDM + q];
-              ga = M[p * LDM + q];
-              // one_sided_jacobi's rotation with (alpha, beta, gamma) = (M_pp, M_qq, M_pq);
-              // skip tolerance 4e-15 instead of 1e-15: two-sided updates leave
-              // O(eps) noise in the scaled off-diagonal.
-              if (al > tiny && be > tiny && !(ga == 0.0 || fabs(ga) <= kTolL * sqrt(al * be))) {
-                const double zeta = (be - al) / (2.0 * ga);
-                tt = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-                c = 1.0 / sqrt(1.0 + tt * tt);
-                s = c * tt;
-              }
-            } else {
-              q = -1;
-            }
-            rc[tid] = c;
-            rs[tid] = s;
-            rt[tid] = tt * ga;  // diagonal shift t * M_pq
-            rp[2 * tid] = p;
-            rp[2 * tid + 1] = q;
-          }
-          __syncthreads();
-          // M <- J^T M J, 2 x 2 block by 2 x 2 block: the round's rotations are
-          // disjoint, so block (pair i1, pair i2) only needs its own four entries
-          // (J_1^T X J_2); rotated diagonal blocks take the exact Jacobi update
-          // diag(M_pp - t M_pq, M_qq + t M_pq), off-diagonal 0.
-          for (int it = tid; it < nblk; it += kLgThreads) {
-            const int i1 = blk[it] >> 8, i2 = blk[it] & 0xff;
-            const int p1 = rp[2 * i1], q1 = rp[2 * i1 + 1], p2 = rp[2 * i2], q2 = rp[2 * i2 + 1];
-            const double s1 = rs[i1], s2 = rs[i2];
-            if (s1 == 0.0 && s2 == 0.0) continue;
-            if (q1 < 0 || q2 < 0) {
-              // odd R: the dummy pair's real index still sees the other pair's
-              // rotation (a 1 x 2 block); the dummy itself never rotates
-              if (q1 < 0 && q2 < 0) continue;
-              const int a = q1 < 0 ? p1 : p2;                 // index of the dummy pair
-              const int u = q1 < 0 ? p2 : p1, v = q1 < 0 ? q2 : q1;  // the rotating pair
-              const double cc = q1 < 0 ? rc[i2] : rc[i1], ss = q1 < 0 ? s2 : s1;
-              const double xu = M[a * LDM + u], xv = M[a * LDM + v];
-              const double nu = cc * xu - ss * xv, nv = ss * xu + cc * xv;
-              M[a * LDM + u] = nu;
-              M[u * LDM + a] = nu;
-              M[a * LDM + v] = nv;
-              M[v * LDM + a] = nv;
-              continue;
-            }
-            if (i1 == i2) {
-              const double d = rt[i1];
-              M[p1 * LDM + p1] -= d;
-              M[q1 * LDM + q1] += d;
-              M[p1 * LDM + q1] = 0.0;
-              M[q1 * LDM + p1] = 0.0;
-              continue;
-            }
-            const double c1 = rc[i1], c2 = rc[i2];
-            const double x11 = M[p1 * LDM + p2], x12 = M[p1 * LDM + q2], x21 = M[q1 * LDM + p2], x22 = M[q1 * LDM + q2];
-            const double y11 = c2 * x11 - s2 * x12, y12 = s2 * x11 + c2 * x12;
-            const double y21 = c2 * x21 - s2 * x22, y22 = s2 * x21 + c2 * x22;
-            const double z11 = c1 * y11 - s1 * y21, z21 = s1 * y11 + c1 * y21;
-            const double z12 = c1 * y12 - s1 * y22, z22 = s1 * y12 + c1 * y22;
-            M[p1 * LDM + p2] = z11;
-            M[p2 * LDM + p1] = z11;
-            M[p1 * LDM + q2] = z12;
-            M[q2 * LDM + p1] = z12;
-            M[q1 * LDM + p2] = z21;
-            M[p2 * LDM + q1] = z21;
-            M[q1 * LDM + q2] = z22;
-            M[q2 * LDM + q1] = z22;
-          }
-          // V' <- V' J (columns p, q of each rotated pair)
-          for (int it = tid; it < half * R; it += kLgThreads) {
-            const int pr = it / R, kk = it - (it / R) * R;
-            const int p = rp[2 * pr], q = rp[2 * pr + 1];
-            const double s = rs[pr];
-            if (q < 0 || s == 0.0) continue;
-            const double c = rc[pr];
-            const double vp = Vp[kk * LDM + p], vq = Vp[kk * LDM + q];
-            Vp[kk * LDM + p] = c * vp - s * vq;
-            Vp[kk * LDM + q] = s * vp + c * vq;
-          }
-          __syncthreads();
-        }
-      }
-      if (a.dbg && tid == 0) {
-        atomicAdd(a.dbg + 0, sweeps);
-        atomicMax(a.dbg + 1, sweeps);
-        if (pass == 0) atomicAdd(a.dbg + 3, 1);
-        if (pass == 1) atomicAdd(a.dbg + 2, 1);
-      }
-      // E <- E V' (right singular vectors of A)
-      for (int i = wid; i < R; i += NW)
-        for (int j = lane; j < R; j += 32) {
-          double acc = 0.0;
-          for (int c = 0; c < R; ++c) acc = fma(E[i * LDM + c], Vp[c * LDM + j], acc);
-          T[i * LDM + j] = acc;  // T no longer needed this pass
-        }
-      __syncthreads();
-      for (int i = wid; i < R; i += NW)
-        for (int j = lane; j < R; j += 32) E[i * LDM + j] = T[i * LDM + j];
-      __syncthreads();
-      if (!converged) {
-        flag = P2G_FLAG_ACCURATE;
-        break;
-      }
-      // sigma; near-null columns (incl. the canonical rule D5) -> accurate path
-      double smax2 = 0.0, smin2 = 1e308;
-      for (int j = 0; j < R; ++j) {
-        smax2 = fmax(smax2, M[j * LDM + j]);
-        smin2 = fmin(smin2, M[j * LDM + j]);
-      }
-      if (!(smax2 > 0.0) || !(smin2 > kTinyL * smax2)) {
-        flag = P2G_FLAG_ACCURATE;
-        break;
-      }
-      // B was not nearly column-orthogonal (||D^-1 M D^-1 - I||_F > 1/2) and A is
-      // ill-conditioned enough for the squared condition number to matter
-      // (sigma_min^2 < 1e-6 sigma_max^2, the fast-path bound of the small-R
-      // pipeline): redo with the fresh E, which makes B nearly orthogonal.
-      if (pass == 0 && off > 0.25 && smin2 < 1e-6 * smax2) continue;
-      for (int j = tid; j < R; j += kLgThreads) sig[j] = 1.0 / sqrt(M[j * LDM + j]);  // 1 / sigma
-      __syncthreads();
-      // Z = V' Sigma^-1 V_A^T (so q_i = b_i Z), into T
-      for (int i = wid; i < R; i += NW)
-        for (int j = lane; j < R; j += 32) {
-          double acc = 0.0;
-          for (int c = 0; c < R; ++c) acc = fma(Vp[i * LDM + c] * sig[c], E[j * LDM + c], acc);
-          T[i * LDM + j] = acc;
-        }
-      __syncthreads();
-      // m1_k = Z^T F
-      for (int i = wid; i < R; i += NW)
-        for (int j = lane; j < R; j += 32) {
-          double acc = 0.0;
-          for (int c = 0; c < R; ++c) acc = fma(T[c * LDM + i], Wk[c * LDM + j], acc);
-          M1[i * LDM + j] += acc;
-        }
-      // Q rows = b_i Z
-      for (int i = tid; i < I; i += kLgThreads) {
-        const double* brow = Bs + static_cast<std::int64_t>(i) * R;
-        double b[RP];
-#pragma unroll
-        for (int c = 0; c < RP; ++c) b[c] = c < R ? brow[c] : 0.0;
-        double* qrow = a.Q + (r0 + i) * R;
-        for (int j = 0; j < R; ++j) {
-          double acc = 0.0;
-#pragma unroll
-          for (int c = 0; c < RP; ++c)
-            if (c < R) acc = fma(b[c], T[c * LDM + j], acc);
-          qrow[j] = acc;
-        }
-      }
-      break;
-    }
-    // V_A -> Ewarm (next step's E, and the accurate path's preconditioner)
-    for (int i = wid; i < R; i += NW)
-      for (int j = lane; j < R; j += 32) Ek[i * R + j] = E[i * LDM + j];
-    if (tid == 0) a.flags[k] = flag;
-    __syncthreads();
-  }
-  for (int e = tid; e < RR; e += kLgThreads)
-    a.m1_partials[static_cast<std::int64_t>(blockIdx.x) * RR + e] = M1[(e / R) * LDM + e % R];
-}
-
 // ---------------------------------------------------------------------------
-// Warp-per-subject variant (default).  Same preconditioned two-sided Jacobi
-// as k_procrustes_large, but one warp owns a subject: M and V' live in the
-// warp's shared memory, every R x R (and I x R) product runs on the fp64
+// One warp owns a subject: M and V' live in the warp's shared memory (V'
+// rows 0..31 in registers during the sweeps), every R x R (and I x R)
+// product runs on the fp64
 // tensor cores (DMMA m8n8k4) over per-warp slabs in global memory (L1/L2
 // resident), and the sweeps stop early:
 //
@@ -1002,24 +636,6 @@ int launch_large_w(p2g_ctx* c, LgArgs a, int max_partials, cudaStream_t s) {
   return blocks * L::WPB;  // one m1 partial per warp
 }
 
-template <int RP, bool EXACT>
-int launch_large(p2g_ctx* c, LgArgs a, int max_blocks, cudaStream_t s) {
-  const std::size_t smem = sizeof(double) * LgSmem<RP>::kDoubles + sizeof(int) * LgSmem<RP>::kInts;
-  auto kern = k_procrustes_large<RP, EXACT>;
-  P2G_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-  int per_sm = 0;
-  P2G_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kLgThreads, smem));
-  const std::int64_t K = a.X.K;
-  const int blocks = static_cast<int>(std::max<std::int64_t>(
-      1, std::min<std::int64_t>({K, static_cast<std::int64_t>(c->num_sms) * std::max(per_sm, 1),
-                                 static_cast<std::int64_t>(max_blocks)})));
-  c->acc_scratch.resize(static_cast<std::size_t>(blocks) * 2 * static_cast<std::size_t>(std::max<std::int64_t>(a.max_rows, 1)) *
-                        a.R);
-  a.slab = c->acc_scratch.get();
-  kern<<<blocks, kLgThreads, smem, s>>>(a);
-  return blocks;
-}
-
 }  // namespace
 
 int launch_procrustes_large(p2g_ctx* c, int R, const double* H, const double* V, const double* W, double* Q,
@@ -1040,36 +656,18 @@ int launch_procrustes_large(p2g_ctx* c, int R, const double* H, const double* V,
   a.dbg = std::getenv("P2G_DEBUG") ? c->counters.get() + 4 : nullptr;
   if (a.X.K == 0) return 0;
   int blocks = 0;
-  if (!std::getenv("P2G_LARGE_CTA")) {  // default: warp per subject
-    if (R == 24)
-      blocks = launch_large_w<24, true>(c, a, max_blocks, s);
-    else if (R == 32)
-      blocks = launch_large_w<32, true>(c, a, max_blocks, s);
-    else if (R == 40)
-      blocks = launch_large_w<40, true>(c, a, max_blocks, s);
-    else if (R <= 24)
-      blocks = launch_large_w<24, false>(c, a, max_blocks, s);
-    else if (R <= 32)
-      blocks = launch_large_w<32, false>(c, a, max_blocks, s);
-    else if (R <= 40)
-      blocks = launch_large_w<40, false>(c, a, max_blocks, s);
-    else
-      throw InvalidArgument("rank above 40 unsupported");
-    P2G_LAUNCHED(1);
-    return blocks;
-  }
   if (R == 24)
-    blocks = launch_large<24, true>(c, a, max_blocks, s);
+    blocks = launch_large_w<24, true>(c, a, max_blocks, s);
   else if (R == 32)
-    blocks = launch_large<32, true>(c, a, max_blocks, s);
+    blocks = launch_large_w<32, true>(c, a, max_blocks, s);
   else if (R == 40)
-    blocks = launch_large<40, true>(c, a, max_blocks, s);
+    blocks = launch_large_w<40, true>(c, a, max_blocks, s);
   else if (R <= 24)
-    blocks = launch_large<24, false>(c, a, max_blocks, s);
+    blocks = launch_large_w<24, false>(c, a, max_blocks, s);
   else if (R <= 32)
-    blocks = launch_large<32, false>(c, a, max_blocks, s);
+    blocks = launch_large_w<32, false>(c, a, max_blocks, s);
   else if (R <= 40)
-    blocks = launch_large<40, false>(c, a, max_blocks, s);
+    blocks = launch_large_w<40, false>(c, a, max_blocks, s);
   else
     throw InvalidArgument("rank above 40 unsupported");
   P2G_LAUNCHED(1);

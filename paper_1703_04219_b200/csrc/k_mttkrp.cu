@@ -203,81 +203,6 @@ __global__ void __launch_bounds__(WPB * 32)
 }
 
 // ---------------------------------------------------------------------------
-// mode 3 for R > 16: lane per output column (c = lane, lane + 32).  The row
-// loop keeps no R-vector per thread (the row-per-lane form spills ~6 KB per
-// thread at R = 40, which ncu shows as 48 GB of local-memory DRAM traffic
-// per 100K subjects): q_i is staged in shared memory and read as a
-// broadcast, H columns are read at stride 1 across lanes, and the V-row
-// gather is coalesced across lanes.  Two rows are in flight per iteration.
-// ---------------------------------------------------------------------------
-template <int WPB>
-__global__ void __launch_bounds__(WPB * 32)
-    k_mode3_cols(ShardArgs X, int R, const double* __restrict__ Q, const double* __restrict__ H,
-                 const double* __restrict__ V, double* __restrict__ M3) {
-  constexpr int kMaxR = 64;
-  __shared__ double Hs[kMaxR * kMaxR];
-  __shared__ double qs[WPB][2][kMaxR];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  for (int e = threadIdx.x; e < R * R; e += blockDim.x) Hs[e] = H[e];
-  __syncthreads();
-  const int c0 = lane, c1 = lane + 32;
-  const bool ok0 = c0 < R, ok1 = c1 < R;
-  const std::int64_t nwarps = static_cast<std::int64_t>(gridDim.x) * WPB;
-  for (std::int64_t k = static_cast<std::int64_t>(blockIdx.x) * WPB + wid; k < X.K; k += nwarps) {
-    const std::int64_t r0 = X.srp[k], r1 = X.srp[k + 1];
-    double part0 = 0.0, part1 = 0.0;
-    for (std::int64_t i = r0; i < r1; i += 2) {
-      const bool two = i + 1 < r1;
-      // stage q rows i, i + 1
-      for (int a = lane; a < R; a += 32) {
-        qs[wid][0][a] = Q[i * R + a];
-        qs[wid][1][a] = two ? Q[(i + 1) * R + a] : 0.0;
-      }
-      // X rows i, i + 1 times V, my columns
-      double x00 = 0.0, x01 = 0.0, x10 = 0.0, x11 = 0.0;
-      const std::int64_t pa0 = X.rp[i], pa1 = X.rp[i + 1];
-      const std::int64_t pb1 = two ? X.rp[i + 2] : pa1;
-      std::int64_t pa = pa0, pb = pa1;
-      while (pa < pa1 || pb < pb1) {
-        if (pa < pa1) {
-          const int j = __ldg(X.ci + pa);
-          const double v = __ldg(X.val + pa);
-          const double* vr = V + static_cast<std::int64_t>(j) * R;
-          if (ok0) x00 = fma(v, __ldg(vr + c0), x00);
-          if (ok1) x01 = fma(v, __ldg(vr + c1), x01);
-          ++pa;
-        }
-        if (pb < pb1) {
-          const int j = __ldg(X.ci + pb);
-          const double v = __ldg(X.val + pb);
-          const double* vr = V + static_cast<std::int64_t>(j) * R;
-          if (ok0) x10 = fma(v, __ldg(vr + c0), x10);
-          if (ok1) x11 = fma(v, __ldg(vr + c1), x11);
-          ++pb;
-        }
-      }
-      __syncwarp();
-      double h00 = 0.0, h01 = 0.0, h10 = 0.0, h11 = 0.0;  // (q_i H)_c
-      for (int a = 0; a < R; ++a) {
-        const double qa = qs[wid][0][a], qb = qs[wid][1][a];
-        const double ha0 = ok0 ? Hs[a * R + c0] : 0.0, ha1 = ok1 ? Hs[a * R + c1] : 0.0;
-        h00 = fma(qa, ha0, h00);
-        h01 = fma(qa, ha1, h01);
-        h10 = fma(qb, ha0, h10);
-        h11 = fma(qb, ha1, h11);
-      }
-      part0 = fma(h00, x00, part0);
-      part1 = fma(h01, x01, part1);
-      part0 = fma(h10, x10, part0);
-      part1 = fma(h11, x11, part1);
-      __syncwarp();
-    }
-    if (ok0) M3[k * R + c0] = part0;
-    if (ok1) M3[k * R + c1] = part1;
-  }
-}
-
-// ---------------------------------------------------------------------------
 // mode 3 for R > 16 on the fp64 tensor cores: per subject, 8-row tiles of
 // P = Q_k H (DMMA m8n8k4: Q fragments straight from HBM, H from shared
 // memory) meet the matching fragment of X_k V, which each lane gathers for
@@ -642,7 +567,7 @@ void launch_mode3(p2g_ctx* c, int R, const double* Q, const double* H, const dou
     else if (R <= 40)
       k_mode3_mma<40, WPB><<<grid_for(X.K, WPB, c->num_sms, 4), WPB * 32, 0, s>>>(X, R, Q, H, V, m3);
     else
-      k_mode3_cols<4><<<grid_for(X.K, 4, c->num_sms, 12), 4 * 32, 0, s>>>(X, R, Q, H, V, m3);
+      throw InvalidArgument("rank above 40 unsupported");
     P2G_LAUNCHED(1);
     return;
   }
