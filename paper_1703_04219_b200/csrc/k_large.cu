@@ -76,7 +76,7 @@ struct LgArgs {
 // During the sweeps M is kept in its upper triangle only (M[min * LDM + max]):
 // half the shared-memory stores of a full symmetric update.
 constexpr double kTauL = 1e-4;   // Jacobi stop: max scaled off-diagonal (truncation error <= 3e-12 measured)
-constexpr double kSkipL = 1e-6;  // rotations below this scaled size are skipped (threshold Jacobi)
+constexpr double kSkipL = 1e-5;  // rotations below this scaled size are skipped (threshold Jacobi; the second-order correction covers them)
 
 template <int RP>
 struct LgWarp {
