@@ -50,6 +50,7 @@ struct LgArgs {
   double* slab;  // per CTA: 2 x max_rows x R (B rows, X~ rows)
   std::int64_t max_rows;
   int* dbg;  // optional: [0] sweeps, [1] max sweeps, [2] redone subjects, [3] subjects
+  const double* XV;  // optional: X V rows (NR x R) from the previous mode-3 pass
 };
 
 // ---------------------------------------------------------------------------
@@ -237,7 +238,12 @@ __global__ void __launch_bounds__(LgWarp<RP>::WPB * 32, 1) k_procrustes_large_w(
     double* Ek = a.Ewarm + k * RR;
     for (int e = lane; e < RR; e += 32) Es[e] = a.ew_valid ? Ek[e] : ((e / R == e % R) ? 1.0 : 0.0);
     __syncwarp();
-    // rows of X~ = X_k V D (lane per row)
+    // rows of X~ = X_k V D: from the previous mode-3 pass's X V rows when
+    // available (a coalesced copy), else gathered (lane per row)
+    if (a.XV) {
+      const double* xs = a.XV + r0 * R;
+      for (int e = lane; e < I * R; e += 32) Xs[e] = xs[e] * w[e % R];
+    } else
     for (int i = lane; i < I; i += 32) {
       double xv[RP];
       dev::csr_row_times<RP>(xv, a.X.ci, a.X.val, a.X.rp[r0 + i], a.X.rp[r0 + i + 1], a.V, R);
@@ -640,8 +646,9 @@ int launch_large_w(p2g_ctx* c, LgArgs a, int max_partials, cudaStream_t s) {
 
 int launch_procrustes_large(p2g_ctx* c, int R, const double* H, const double* V, const double* W, double* Q,
                             std::int32_t* flags, double* m1_partials, double* Ewarm, int ew_valid, int max_blocks,
-                            cudaStream_t s) {
+                            cudaStream_t s, const double* XV_in) {
   LgArgs a{};
+  a.XV = XV_in;
   a.X = ShardArgs{c->srp.get(), c->rp.get(), c->ci.get(), c->val.get(), c->k_end - c->k_begin, c->NR, c->nnz, c->J};
   a.R = R;
   a.H = H;

@@ -214,7 +214,7 @@ __global__ void __launch_bounds__(WPB * 32)
 template <int RP, int WPB>
 __global__ void __launch_bounds__(WPB * 32)
     k_mode3_mma(ShardArgs X, int R, const double* __restrict__ Q, const double* __restrict__ H,
-                const double* __restrict__ V, double* __restrict__ M3) {
+                const double* __restrict__ V, double* __restrict__ M3, double* __restrict__ XV) {
   constexpr int NB = RP / 8;
   __shared__ double Hs[RP * RP];  // H zero-padded to RP x RP, row-major
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, fm = lane >> 2, fk = lane & 3;
@@ -267,6 +267,19 @@ __global__ void __launch_bounds__(WPB * 32)
               if (c < R) xv[b][0] = fma(v, __ldg(vr + c), xv[b][0]);
               if (c + 1 < R) xv[b][1] = fma(v, __ldg(vr + c + 1), xv[b][1]);
             }
+          }
+        }
+      }
+      if (XV && iv) {  // X_k V rows for the next Procrustes step (it would re-gather them)
+        double* xr = XV + (r0 + i) * R;
+#pragma unroll
+        for (int b = 0; b < NB; ++b) {
+          const int c = 8 * b + 2 * fk;
+          if (even) {
+            if (c < R) *reinterpret_cast<double2*>(xr + c) = make_double2(xv[b][0], xv[b][1]);
+          } else {
+            if (c < R) xr[c] = xv[b][0];
+            if (c + 1 < R) xr[c + 1] = xv[b][1];
           }
         }
       }
@@ -556,16 +569,16 @@ void launch_mode2(p2g_ctx* c, int R, const double* Q, const double* H, const dou
 }
 
 void launch_mode3(p2g_ctx* c, int R, const double* Q, const double* H, const double* V, double* m3,
-                  cudaStream_t s) {
+                  cudaStream_t s, double* XV_out) {
   const ShardArgs X = shard_args(c);
   if (R > 16) {  // the row-per-lane form spills above R = 16
     constexpr int WPB = 8;
     if (R <= 24)
-      k_mode3_mma<24, WPB><<<grid_for(X.K, WPB, c->num_sms, 4), WPB * 32, 0, s>>>(X, R, Q, H, V, m3);
+      k_mode3_mma<24, WPB><<<grid_for(X.K, WPB, c->num_sms, 4), WPB * 32, 0, s>>>(X, R, Q, H, V, m3, XV_out);
     else if (R <= 32)
-      k_mode3_mma<32, WPB><<<grid_for(X.K, WPB, c->num_sms, 4), WPB * 32, 0, s>>>(X, R, Q, H, V, m3);
+      k_mode3_mma<32, WPB><<<grid_for(X.K, WPB, c->num_sms, 4), WPB * 32, 0, s>>>(X, R, Q, H, V, m3, XV_out);
     else if (R <= 40)
-      k_mode3_mma<40, WPB><<<grid_for(X.K, WPB, c->num_sms, 4), WPB * 32, 0, s>>>(X, R, Q, H, V, m3);
+      k_mode3_mma<40, WPB><<<grid_for(X.K, WPB, c->num_sms, 4), WPB * 32, 0, s>>>(X, R, Q, H, V, m3, XV_out);
     else
       throw InvalidArgument("rank above 40 unsupported");
     P2G_LAUNCHED(1);

@@ -264,8 +264,10 @@ int procrustes_step(p2g_ctx* c, double* part) {
   } else {
     {
       Phase ph(c, "procrustes");
+      // c_valid: the last mode-3 pass left X V (current V) in Ubuf
       n1 = launch_procrustes_large(c, R, c->H.get(), c->V.get(), c->W.get(), c->Q.get(), c->flags.get(), part,
-                                   c->Ewarm.get(), c->ew_valid ? 1 : 0, kMaxPartials, s);
+                                   c->Ewarm.get(), c->ew_valid ? 1 : 0, kMaxPartials, s,
+                                   c->c_valid ? c->Ubuf.get() : nullptr);
       c->ew_valid = true;
     }
     Phase ph(c, "procrustes_accurate");
@@ -388,7 +390,7 @@ IterOut iterate(p2g_ctx* c, bool nonneg, int iter) {
       launch_mode3_qf(c, R, c->H.get(), c->V.get(), c->W.get(), c->Hp.get(), c->Vp.get(), c->Sbuf.get(),
                       c->Ebuf.get(), c->Chat.get(), c->flags.get(), c->m3.get(), c->Cbuf.get(), s);
     else
-      launch_mode3(c, R, c->Q.get(), c->Hp.get(), c->Vp.get(), c->m3.get(), s);
+      launch_mode3(c, R, c->Q.get(), c->Hp.get(), c->Vp.get(), c->m3.get(), s, c->Ubuf.get());  // U is dead here
   }
   {
     Phase ph(c, "update_w");  // W_t -> Wp
@@ -409,7 +411,7 @@ IterOut iterate(p2g_ctx* c, bool nonneg, int iter) {
   swap_buf(c->H, c->Hp);
   swap_buf(c->V, c->Vp);
   swap_buf(c->W, c->Wp);
-  c->c_valid = qf;  // mode 3 produced the Gram for the new V
+  c->c_valid = true;  // mode 3 produced the Gram (R <= 16) or X V rows (R > 16) for the new V
   // One host sync per iteration: fit scalars + error counters.
   P2G_CUDA(cudaMemcpyAsync(c->pinned, c->scal.get(), sizeof(double) * 4, cudaMemcpyDeviceToHost, s));
   P2G_CUDA(cudaMemcpyAsync(c->pinned + 4, c->counters.get(), sizeof(std::int32_t) * 8, cudaMemcpyDeviceToHost, s));

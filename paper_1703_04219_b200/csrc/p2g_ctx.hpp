@@ -180,7 +180,7 @@ void launch_urows_large(p2g_ctx* c, int R, const double* Q, const double* H, con
                         double* U, cudaStream_t s);
 int launch_procrustes_large(p2g_ctx* c, int R, const double* H, const double* V, const double* W, double* Q,
                             std::int32_t* flags, double* m1_partials, double* Ewarm, int ew_valid, int max_blocks,
-                            cudaStream_t s);
+                            cudaStream_t s, const double* XV_in = nullptr);
 int launch_procrustes_accurate(p2g_ctx* c, int R, const double* H, const double* V, const double* W, double* Q,
                                std::int32_t* flags, double* m1_partials, const double* Ebuf, double* Shat,
                                double* Chat, cudaStream_t s);
@@ -206,7 +206,7 @@ void launch_nnls_thread(int R, std::int64_t n, const double* G, const double* B,
 void launch_mode2(p2g_ctx* c, int R, const double* Q, const double* H, const double* W, const double* nH,
                   double* M2, cudaStream_t s);
 void launch_mode3(p2g_ctx* c, int R, const double* Q, const double* H, const double* V, double* m3,
-                  cudaStream_t s);
+                  cudaStream_t s, double* XV_out = nullptr);
 void launch_mode1_q(p2g_ctx* c, int R, const double* Q, const double* V, const double* W, double* m1_partials,
                     int nblocks, cudaStream_t s);
 void launch_project(p2g_ctx* c, int R, const double* Q, const std::int64_t* ycol_ptr, const std::int32_t* ycols,
