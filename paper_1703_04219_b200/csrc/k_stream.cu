@@ -119,7 +119,7 @@ __global__ void __launch_bounds__(StreamCfg<R>::WPB * 32)
     k_mode2_sb(ShardArgs X, const double* __restrict__ Hprev, const double* __restrict__ Vprev,
                const double* __restrict__ Wprev, const double* __restrict__ Ht, const double* __restrict__ nH,
                const double* __restrict__ Sbuf, const double* __restrict__ Shat, const double* __restrict__ Chat,
-               const std::int32_t* __restrict__ flags, double* __restrict__ U) {
+               const std::int32_t* __restrict__ flags, double* __restrict__ U, const double* __restrict__ XV) {
   using C = StreamCfg<R>;
   extern __shared__ double smem[];
   __shared__ std::int32_t rowoff_s[C::WPB][C::SB + 1];
@@ -164,7 +164,16 @@ __global__ void __launch_bounds__(StreamCfg<R>::WPB * 32)
         }
       }
       double xv[UR][R];
-      dev::csr_rows_times<R, UR, 1>(xv, xv, X.ci, X.val, p0, p1, Vprev, Vprev);
+      if (XV) {  // X V_prev rows left by the previous mode-3 pass (a streaming read, no V gathers)
+#pragma unroll
+        for (int u = 0; u < UR; ++u) {
+          const double* xr = XV + (row0 + cb + lane + 32 * u) * R;
+#pragma unroll
+          for (int a = 0; a < R; ++a) xv[u][a] = su[u] >= 0 ? xr[a] : 0.0;
+        }
+      } else {
+        dev::csr_rows_times<R, UR, 1>(xv, xv, X.ci, X.val, p0, p1, Vprev, Vprev);
+      }
 #pragma unroll
       for (int u = 0; u < UR; ++u) {
         const int s_ = su[u];
@@ -206,7 +215,8 @@ __global__ void __launch_bounds__(StreamCfg<R>::WPB * 32)
     k_mode3_sb(ShardArgs X, const double* __restrict__ Hprev, const double* __restrict__ Vprev,
                const double* __restrict__ Wprev, const double* __restrict__ Ht, const double* __restrict__ Vt,
                const double* __restrict__ Sbuf, const double* __restrict__ Shat, const double* __restrict__ Chat,
-               const std::int32_t* __restrict__ flags, double* __restrict__ M3, double* __restrict__ Cnext) {
+               const std::int32_t* __restrict__ flags, double* __restrict__ M3, double* __restrict__ Cnext,
+               double* __restrict__ XV, int xv_in) {
   using C = StreamCfg<R>;
   extern __shared__ double smem[];
   __shared__ std::int32_t rowoff_s[C::WPB][C::SB + 1];
@@ -281,7 +291,26 @@ __global__ void __launch_bounds__(StreamCfg<R>::WPB * 32)
         }
       }
       double xp[UR][R], xn[UR][R];  // both gathers share the entry stream
-      dev::csr_rows_times<R, UR, 2>(xp, xn, X.ci, X.val, p0, p1, Vprev, Vt);
+      if (xv_in) {  // X V_prev rows from the previous pass; only V_t is gathered
+#pragma unroll
+        for (int u = 0; u < UR; ++u) {
+          const double* xr = XV + (row0 + cb + lane + 32 * u) * R;
+#pragma unroll
+          for (int a = 0; a < R; ++a) xp[u][a] = su[u] >= 0 ? xr[a] : 0.0;
+        }
+        dev::csr_rows_times<R, UR, 1>(xn, xn, X.ci, X.val, p0, p1, Vt, Vt);
+      } else {
+        dev::csr_rows_times<R, UR, 2>(xp, xn, X.ci, X.val, p0, p1, Vprev, Vt);
+      }
+      if (XV) {  // X V_t rows for the next iteration (each lane rewrites its own rows)
+#pragma unroll
+        for (int u = 0; u < UR; ++u) {
+          if (su[u] < 0) continue;
+          double* xr = XV + (row0 + cb + lane + 32 * u) * R;
+#pragma unroll
+          for (int a = 0; a < R; ++a) xr[a] = xn[u][a];
+        }
+      }
 #pragma unroll
       for (int u = 0; u < UR; ++u) {
         const int s_ = su[u];
@@ -374,26 +403,26 @@ ShardArgs shard_args_st(p2g_ctx* c) {
 template <int R>
 void mode2_sb(p2g_ctx* c, const double* Hprev, const double* Vprev, const double* Wprev, const double* Ht,
               const double* nH, const double* Sbuf, const double* Shat, const double* Chat, const std::int32_t* flags,
-              double* U, cudaStream_t s) {
+              double* U, cudaStream_t s, const double* XV) {
   using C = StreamCfg<R>;
   const std::size_t smem = sizeof(double) * (2 * C::RR + C::WPB * C::kWarpT);
   auto kern = k_mode2_sb<R>;
   P2G_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   const int nb = stream_blocks<R>(c, reinterpret_cast<const void*>(kern), smem);
-  kern<<<nb, C::WPB * 32, smem, s>>>(shard_args_st(c), Hprev, Vprev, Wprev, Ht, nH, Sbuf, Shat, Chat, flags, U);
+  kern<<<nb, C::WPB * 32, smem, s>>>(shard_args_st(c), Hprev, Vprev, Wprev, Ht, nH, Sbuf, Shat, Chat, flags, U, XV);
 }
 
 template <int R>
 void mode3_sb(p2g_ctx* c, const double* Hprev, const double* Vprev, const double* Wprev, const double* Ht,
               const double* Vt, const double* Sbuf, const double* Shat, const double* Chat, const std::int32_t* flags,
-              double* M3, double* Cnext, cudaStream_t s) {
+              double* M3, double* Cnext, cudaStream_t s, double* XV, int xv_in) {
   using C = StreamCfg<R>;
   const std::size_t smem = sizeof(double) * (2 * C::RR + C::WPB * (C::kWarpT + C::kWarpCh));
   auto kern = k_mode3_sb<R>;
   P2G_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   const int nb = stream_blocks<R>(c, reinterpret_cast<const void*>(kern), smem);
   kern<<<nb, C::WPB * 32, smem, s>>>(shard_args_st(c), Hprev, Vprev, Wprev, Ht, Vt, Sbuf, Shat, Chat, flags, M3,
-                                     Cnext);
+                                     Cnext, XV, xv_in);
 }
 
 }  // namespace
@@ -421,18 +450,20 @@ void mode3_sb(p2g_ctx* c, const double* Hprev, const double* Vprev, const double
 
 void launch_mode2_qf(p2g_ctx* c, int R, const double* Hprev, const double* Vprev, const double* Wprev,
                      const double* Ht, const double* nH, const double* Sbuf, const double* Shat, const double* Chat,
-                     const std::int32_t* flags, double* U, cudaStream_t s) {
+                     const std::int32_t* flags, double* U, cudaStream_t s, const double* XV) {
   if (c->k_end > c->k_begin) {
-    P2G_EXACT_R_DISPATCH(R, (mode2_sb<R_>(c, Hprev, Vprev, Wprev, Ht, nH, Sbuf, Shat, Chat, flags, U, s)));
+    P2G_EXACT_R_DISPATCH(R, (mode2_sb<R_>(c, Hprev, Vprev, Wprev, Ht, nH, Sbuf, Shat, Chat, flags, U, s, XV)));
     P2G_LAUNCHED(1);
   }
 }
 
 void launch_mode3_qf(p2g_ctx* c, int R, const double* Hprev, const double* Vprev, const double* Wprev,
                      const double* Ht, const double* Vt, const double* Sbuf, const double* Shat, const double* Chat,
-                     const std::int32_t* flags, double* M3, double* Cnext, cudaStream_t s) {
+                     const std::int32_t* flags, double* M3, double* Cnext, cudaStream_t s, double* XV,
+                     int xv_in) {
   if (c->k_end > c->k_begin) {
-    P2G_EXACT_R_DISPATCH(R, (mode3_sb<R_>(c, Hprev, Vprev, Wprev, Ht, Vt, Sbuf, Shat, Chat, flags, M3, Cnext, s)));
+    P2G_EXACT_R_DISPATCH(R, (mode3_sb<R_>(c, Hprev, Vprev, Wprev, Ht, Vt, Sbuf, Shat, Chat, flags, M3, Cnext, s, XV,
+                                          xv_in)));
     P2G_LAUNCHED(1);
   }
 }

@@ -212,6 +212,7 @@ void alloc_state(p2g_ctx* c, int R) {
     c->Ebuf.resize(ks * RR);
     c->Chat.resize(ks * RR);
     c->Ewarm.resize(ks * RR);
+    c->Ubuf.resize(static_cast<std::size_t>(std::max<std::int64_t>(c->NR, 1)) * R);  // X V rows between passes
     c->mask_v.resize(static_cast<std::size_t>(std::max<std::int64_t>(c->J, 1)));
     c->mask_w.resize(ks);
   } else {
@@ -326,6 +327,7 @@ void init_state(p2g_ctx* c, const p2g_fit_config* cfg, const double* H0, const d
   gram_w_cross(c, c->W.get(), nullptr);
   P2G_CUDA(cudaMemcpyAsync(c->gramW.get(), c->gwc.get(), sizeof(double) * R * R, cudaMemcpyDeviceToDevice, c->stream));
   c->c_valid = false;
+  c->xv_valid = false;
   c->ew_valid = false;
   c->masks_valid = false;
   c->polar_sweeps_valid = false;
@@ -365,7 +367,7 @@ IterOut iterate(p2g_ctx* c, bool nonneg, int iter) {
     double* U = qf ? c->Q.get() : c->Ubuf.get();
     if (qf)
       launch_mode2_qf(c, R, c->H.get(), c->V.get(), c->W.get(), c->Hp.get(), c->nH.get(), c->Sbuf.get(),
-                      c->Ebuf.get(), c->Chat.get(), c->flags.get(), U, s);
+                      c->Ebuf.get(), c->Chat.get(), c->flags.get(), U, s, c->xv_valid ? c->Ubuf.get() : nullptr);
     else
       launch_urows_large(c, R, c->Q.get(), c->Hp.get(), c->W.get(), c->nH.get(), U, s);
     launch_csc_mode2(c, R, U, c->M2.get(), s);
@@ -388,7 +390,8 @@ IterOut iterate(p2g_ctx* c, bool nonneg, int iter) {
     Phase ph(c, "mode3");
     if (qf)
       launch_mode3_qf(c, R, c->H.get(), c->V.get(), c->W.get(), c->Hp.get(), c->Vp.get(), c->Sbuf.get(),
-                      c->Ebuf.get(), c->Chat.get(), c->flags.get(), c->m3.get(), c->Cbuf.get(), s);
+                      c->Ebuf.get(), c->Chat.get(), c->flags.get(), c->m3.get(), c->Cbuf.get(), s, c->Ubuf.get(),
+                      c->xv_valid ? 1 : 0);
     else
       launch_mode3(c, R, c->Q.get(), c->Hp.get(), c->Vp.get(), c->m3.get(), s, c->Ubuf.get());  // U is dead here
   }
@@ -412,6 +415,7 @@ IterOut iterate(p2g_ctx* c, bool nonneg, int iter) {
   swap_buf(c->V, c->Vp);
   swap_buf(c->W, c->Wp);
   c->c_valid = true;  // mode 3 produced the Gram (R <= 16) or X V rows (R > 16) for the new V
+  c->xv_valid = qf;   // and, for R <= 16, the X V rows in Ubuf
   // One host sync per iteration: fit scalars + error counters.
   P2G_CUDA(cudaMemcpyAsync(c->pinned, c->scal.get(), sizeof(double) * 4, cudaMemcpyDeviceToHost, s));
   P2G_CUDA(cudaMemcpyAsync(c->pinned + 4, c->counters.get(), sizeof(std::int32_t) * 8, cudaMemcpyDeviceToHost, s));
@@ -904,6 +908,7 @@ extern "C" int p2g_procrustes(p2g_ctx* c, int32_t R, const double* H, const doub
     upload_colmajor(c, V, c->J, R, c->V.get());
     upload_shard_rows(c, W, c->K_total, R, c->W.get());
     c->c_valid = false;
+  c->xv_valid = false;
     c->ew_valid = false;  // cold Jacobi start for a teacher-forced step
     const std::size_t RR = static_cast<std::size_t>(R) * R;
     P2G_CUDA(cudaMemsetAsync(c->counters.get(), 0, sizeof(std::int32_t) * 32, c->stream));
@@ -940,6 +945,7 @@ extern "C" int p2g_mttkrp_q(p2g_ctx* c, int32_t mode, int32_t R, const double* Q
     upload_colmajor(c, V, c->J, R, c->V.get());
     upload_shard_rows(c, W, c->K_total, R, c->W.get());
     c->c_valid = false;
+  c->xv_valid = false;
     const std::size_t RR = static_cast<std::size_t>(R) * R;
     if (mode == 1) {
       const int nb = 2 * c->num_sms;

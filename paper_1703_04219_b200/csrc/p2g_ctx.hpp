@@ -128,6 +128,7 @@ struct p2g_ctx {
   bool ew_valid = false;              // Ewarm holds eigenvectors from a previous Procrustes step
   p2g::DBuf<double> Hp, Vp, Wp;       // factors the last Procrustes step used (Q-free reconstruction)
   bool c_valid = false;               // Cbuf holds Gram of X V for the current V
+  bool xv_valid = false;              // R <= 16: Ubuf holds the X V rows of the current V (last mode-3 pass)
   p2g::DBuf<std::int32_t> redo;       // NNLS rows re-solved by the warp (pinv) kernel
   p2g::DBuf<double> m2part;           // per-range J x R partials of the on-chip mode-2 kernel
   // column-major copy of the shard for the atomics-free mode-2 pass (k_csc.cu)
@@ -196,10 +197,11 @@ void launch_qrows(p2g_ctx* c, int R, const double* H, const double* V, const dou
                   const double* Shat, const double* Chat, const std::int32_t* flags, double* Q, cudaStream_t s);
 void launch_mode2_qf(p2g_ctx* c, int R, const double* Hprev, const double* Vprev, const double* Wprev,
                      const double* Ht, const double* nH, const double* Sbuf, const double* Shat, const double* Chat,
-                     const std::int32_t* flags, double* M2, cudaStream_t s);
+                     const std::int32_t* flags, double* M2, cudaStream_t s, const double* XV = nullptr);
 void launch_mode3_qf(p2g_ctx* c, int R, const double* Hprev, const double* Vprev, const double* Wprev,
                      const double* Ht, const double* Vt, const double* Sbuf, const double* Shat, const double* Chat,
-                     const std::int32_t* flags, double* M3, double* Cnext, cudaStream_t s);
+                     const std::int32_t* flags, double* M3, double* Cnext, cudaStream_t s, double* XV = nullptr,
+                     int xv_in = 0);
 void launch_nnls_thread(int R, std::int64_t n, const double* G, const double* B, double* X, int max_iter,
                         std::int32_t* err, std::int32_t* redo, std::int32_t* n_redo, unsigned* masks, int warm,
                         cudaStream_t s);
