@@ -63,13 +63,35 @@ __device__ __forceinline__ void build_batch_ops(std::int64_t k0, int nb, const d
                                                 const double* __restrict__ Sbuf, const double* __restrict__ Shat,
                                                 const std::int32_t* fl, double* Tw, int lane) {
   using C = StreamCfg<R>;
-  // 1. stage S_s (full, row-major [c][b]) into the T area
-  for (int idx = lane; idx < nb * C::RR; idx += 32) {
+  // 1. stage S_s (full, row-major [c][b]) into the T area: every load of
+  //    the batch issued before any store (one dependent load at a time left
+  //    the setup latency-bound)
+  if constexpr (MODE == 2) {  // (mode 2: the plain loop measured faster; register budget)
+    for (int idx = lane; idx < nb * C::RR; idx += 32) {
+      const int s = idx / C::RR, e = idx - s * C::RR;
+      const int c = e / R, b = e - c * R;
+      const std::int64_t k = k0 + s;
+      Tw[e * C::SBP + s] = fl[s] != P2G_FLAG_FULL_RANK ? Shat[k * C::RR + e] : Sbuf[k * C::NT + tri_idx(c, b)];
+    }
+  } else {
+  constexpr int NIT = (C::SB * C::RR + 31) / 32;
+  double vv[NIT];
+#pragma unroll
+  for (int j = 0; j < NIT; ++j) {
+    const int idx = lane + 32 * j;
     const int s = idx / C::RR, e = idx - s * C::RR;
     const int c = e / R, b = e - c * R;
     const std::int64_t k = k0 + s;
-    const double v = fl[s] != P2G_FLAG_FULL_RANK ? Shat[k * C::RR + e] : Sbuf[k * C::NT + tri_idx(c, b)];
-    Tw[e * C::SBP + s] = v;
+    vv[j] = idx < nb * C::RR
+                ? (fl[s] != P2G_FLAG_FULL_RANK ? Shat[k * C::RR + e] : Sbuf[k * C::NT + tri_idx(c, b)])
+                : 0.0;
+  }
+#pragma unroll
+  for (int j = 0; j < NIT; ++j) {
+    const int idx = lane + 32 * j;
+    const int s = idx / C::RR, e = idx - s * C::RR;
+    if (idx < nb * C::RR) Tw[e * C::SBP + s] = vv[j];
+  }
   }
   __syncwarp();
   // 2. B rows a = q + LPS m of subject s: B[a][b] = sum_c H[c][a] S[c][b]
