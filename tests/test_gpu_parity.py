@@ -337,3 +337,25 @@ def test_load_validation_errors(ctx, p2g):
     load()
     res = ctx.fit(p2g.SolverConfig(rank=1, max_iters=2, tol=1e-300))
     assert np.all(np.isfinite(res.fit))
+
+
+@pytest.mark.parametrize("R", [10, 40])
+def test_state_reuse_across_calls(ctx, p2g, R):
+    """The fused loop carries state between passes (mode 3 leaves X V rows and,
+    for R <= 16, the next Gram C for the following iteration; Jacobi warm
+    starts; NNLS passive sets).  Per-step hooks and reloads in between must
+    invalidate it: a fit after them equals a fit on a fresh context, bit for bit."""
+    X = p2g.generate_baseline(3 if R > 16 else 2, R, K=3000)
+    H0, V0, W0 = p2g.init_factors(11, X.K, X.J, R)
+    cfg = p2g.SolverConfig(rank=R, max_iters=3, tol=1e-300, nonneg=True)
+    ctx.load(X)
+    a = ctx.fit(cfg, H0, V0, W0)
+    Q, _, _ = ctx.procrustes(a.H, a.V, a.W)       # teacher-forced step: overwrites Q, flags, Ewarm
+    ctx.mttkrp_q(3, Q, a.H, a.V, a.W)             # mode-3 hook: overwrites m3
+    b = ctx.fit(cfg, H0, V0, W0)
+    ctx.load(X)                                   # reload: new CSC build, state dropped
+    c = ctx.fit(cfg, H0, V0, W0)
+    for r in (b, c):
+        assert np.array_equal(a.fit, r.fit)
+        for x, y in ((a.H, r.H), (a.V, r.V), (a.W, r.W)):
+            assert np.array_equal(x, y)
