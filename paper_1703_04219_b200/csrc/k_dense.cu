@@ -656,6 +656,16 @@ void reduce_partials(const double* partials, int nparts, std::int64_t len, doubl
   P2G_LAUNCHED(1);
 }
 
+/// G^{-1} of an R <= 16 Gram into a process-wide buffer (out[R*R] = validity),
+/// for the thread-per-row NNLS's cold start.
+const double* launch_ginv_small(int R, const double* G, cudaStream_t s) {
+  static DBuf<double> buf;
+  buf.resize(16 * 16 + 1);
+  k_ginv<16><<<1, 32, 0, s>>>(R, G, buf.get());
+  P2G_LAUNCHED(1);
+  return buf.get();
+}
+
 void launch_nnls_rows(int R, std::int64_t n, const double* G, const double* B, double* X, int max_iter,
                       std::int32_t* err, std::int32_t* work, cudaStream_t s, unsigned* masks, int warm,
                       unsigned long long* masks64) {
@@ -665,7 +675,8 @@ void launch_nnls_rows(int R, std::int64_t n, const double* G, const double* B, d
     // thread per row; rows whose passive Cholesky meets a non-positive pivot
     // are re-solved by the warp kernel with the pseudo-inverse (work[0] = count).
     P2G_CUDA(cudaMemsetAsync(work, 0, sizeof(std::int32_t), s));
-    launch_nnls_thread(R, n, G, B, X, max_iter, err, work + 1, work, masks, warm, s);
+    const double* gi = (masks && !warm) ? launch_ginv_small(R, G, s) : nullptr;  // cold rows: G^{-1} b support
+    launch_nnls_thread(R, n, G, B, X, max_iter, err, work + 1, work, masks, warm, s, gi);
     nnls_warp_any(R, n, G, B, X, cap, err, work + 1, work, s);
     P2G_LAUNCHED(1);
     return;

@@ -617,13 +617,18 @@ template <int RP, int WPB>
 __global__ void __launch_bounds__(WPB * 32)
     k_nnls_thread(int R, std::int64_t n, const double* __restrict__ G, const double* __restrict__ B,
                   double* __restrict__ X, int cap, std::int32_t* __restrict__ err, std::int32_t* __restrict__ redo,
-                  std::int32_t* __restrict__ n_redo, unsigned* __restrict__ masks, int warm) {
+                  std::int32_t* __restrict__ n_redo, unsigned* __restrict__ masks, int warm,
+                  const double* __restrict__ ginv) {
   extern __shared__ double smem[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   double* Gs = smem;
-  double* Lw = Gs + RP * RP + wid * NnlsThreadSmem<RP>::kPerWarp;
+  double* Gi = Gs + RP * RP;  // G^{-1} (cold start), RP x RP
+  double* Lw = Gi + RP * RP + wid * NnlsThreadSmem<RP>::kPerWarp;
   double* spw = Lw + NnlsThreadSmem<RP>::NT * LD;
   for (int e = threadIdx.x; e < R * R; e += blockDim.x) Gs[e] = G[e];
+  const bool cold_gi = ginv && !(masks && warm) && ginv[R * R] == 1.0;
+  if (cold_gi)  // k_ginv<16> wrote R x R row-major (stride R), validity at [R * R]
+    for (int e = threadIdx.x; e < R * R; e += blockDim.x) Gi[e] = ginv[e];
   __syncthreads();
   auto L = [&](int i, int j) -> double& { return Lw[tri(i, j) * LD + lane]; };
   auto SP = [&](int i) -> double& { return spw[i * LD + lane]; };
@@ -641,6 +646,17 @@ __global__ void __launch_bounds__(WPB * 32)
     // infeasible warm solve sheds its non-positive coordinates and retries,
     // and an emptied set falls back to the reference's cold start.
     unsigned passive = (masks && warm) ? (masks[row] & ((R >= 32) ? ~0u : ((1u << R) - 1u))) : 0u;
+    if (cold_gi) {  // cold row: start from the support of G^{-1} b (same unique optimum)
+#pragma unroll
+      for (int r = 0; r < RP; ++r) {
+        if (r >= R) continue;
+        double acc = 0.0;
+#pragma unroll
+        for (int c = 0; c < RP; ++c)
+          if (c < R) acc = fma(Gi[r * R + c], b[c], acc);
+        if (acc > 0.0) passive |= 1u << r;
+      }
+    }
     bool warm_phase = passive != 0u;
     int iters = 0;
     bool failed = false, chol_fail = false;
@@ -892,21 +908,21 @@ void launch_qrows(p2g_ctx* c, int R, const double* H, const double* V, const dou
 template <int RP>
 static void nnls_thread_launch(int R, std::int64_t n, const double* G, const double* B, double* X, int cap,
                                std::int32_t* err, std::int32_t* redo, std::int32_t* n_redo, unsigned* masks, int warm,
-                               cudaStream_t s) {
+                               cudaStream_t s, const double* ginv) {
   constexpr int WPB = 4;
-  const std::size_t smem = sizeof(double) * (RP * RP + WPB * NnlsThreadSmem<RP>::kPerWarp);
+  const std::size_t smem = sizeof(double) * (2 * RP * RP + WPB * NnlsThreadSmem<RP>::kPerWarp);
   auto kern = k_nnls_thread<RP, WPB>;
   P2G_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   const int blocks = static_cast<int>(std::max<std::int64_t>(1, std::min<std::int64_t>((n + 127) / 128, 148 * 16)));
-  kern<<<blocks, WPB * 32, smem, s>>>(R, n, G, B, X, cap, err, redo, n_redo, masks, warm);
+  kern<<<blocks, WPB * 32, smem, s>>>(R, n, G, B, X, cap, err, redo, n_redo, masks, warm, ginv);
 }
 
 void launch_nnls_thread(int R, std::int64_t n, const double* G, const double* B, double* X, int max_iter,
                         std::int32_t* err, std::int32_t* redo, std::int32_t* n_redo, unsigned* masks, int warm,
-                        cudaStream_t s) {
+                        cudaStream_t s, const double* ginv) {
   if (n == 0) return;
   const int cap = max_iter > 0 ? max_iter : 30 * R;
-  P2G_SMALL_DISPATCH(R, nnls_thread_launch<RP_>(R, n, G, B, X, cap, err, redo, n_redo, masks, warm, s));
+  P2G_SMALL_DISPATCH(R, nnls_thread_launch<RP_>(R, n, G, B, X, cap, err, redo, n_redo, masks, warm, s, ginv));
   P2G_LAUNCHED(1);
 }
 

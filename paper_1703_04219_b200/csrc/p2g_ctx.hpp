@@ -204,7 +204,7 @@ void launch_mode3_qf(p2g_ctx* c, int R, const double* Hprev, const double* Vprev
                      int xv_in = 0);
 void launch_nnls_thread(int R, std::int64_t n, const double* G, const double* B, double* X, int max_iter,
                         std::int32_t* err, std::int32_t* redo, std::int32_t* n_redo, unsigned* masks, int warm,
-                        cudaStream_t s);
+                        cudaStream_t s, const double* ginv = nullptr);
 void launch_mode2(p2g_ctx* c, int R, const double* Q, const double* H, const double* W, const double* nH,
                   double* M2, cudaStream_t s);
 void launch_mode3(p2g_ctx* c, int R, const double* Q, const double* H, const double* V, double* m3,
