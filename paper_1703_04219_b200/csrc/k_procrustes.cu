@@ -355,54 +355,71 @@ __global__ void __launch_bounds__(WPB * 32) k_procrustes_accurate(K1Args a, doub
       for (int e = lane; e < RR; e += 32) Vj[e] = (e / R == e % R) ? 1.0 : 0.0;
       __syncwarp();
       // Hestenes sweeps (same rotation formulas and skip rule as the oracle's
-      // one_sided_jacobi), round-robin ordering: the R/2 disjoint column pairs of
-      // a round go to R/2 lanes, each lane forming its (alpha, beta, gamma) over
-      // the rows and rotating its own two columns of A and V.  A round reads
-      // whole rows of A (coalesced) and needs no cross-lane reductions.
+      // one_sided_jacobi), round-robin ordering: the R/2 disjoint column pairs
+      // of a round go to groups of g = 32 / (R/2) lanes (g = 1 at R = 40, 6 at
+      // R = 10: the small ranks used to leave 27 of 32 lanes idle); a group
+      // splits the rows, sums its (alpha, beta, gamma) partials in a fixed
+      // lane order (every lane of the group gets the same bits) and rotates
+      // its rows of the pair's two columns of A and V.
       {
         const int mm = (R + 1) & ~1, hh = mm / 2;
+        const int g = RP > 16 ? 1 : 32 / hh;  // compile-time 1 above R = 16 (unit-stride row loops)
+        const int pr = lane / g, sub = lane - pr * g;
+        const bool act = pr < hh;
+        const int base = act ? pr * g : 0;
         for (int sweep = 0; sweep < 80; ++sweep) {
           bool rot = false;
           for (int round = 0; round < mm - 1; ++round) {
-            if (lane < hh) {
-              int p, q;
-              if (lane == 0) {
+            int p = 0, q = mm;
+            if (act) {
+              if (pr == 0) {
                 p = round;
                 q = mm - 1;
               } else {
-                p = (round + lane) % (mm - 1);
-                q = (round - lane + (mm - 1)) % (mm - 1);
+                p = (round + pr) % (mm - 1);
+                q = (round - pr + (mm - 1)) % (mm - 1);
               }
               if (p > q) {
                 const int t = p;
                 p = q;
                 q = t;
               }
-              if (q < R) {
-                double al = 0.0, be = 0.0, ga = 0.0;
-                for (int i = 0; i < I; ++i) {
-                  const double x = A[i * R + p], y = A[i * R + q];
-                  al = fma(x, x, al);
-                  be = fma(y, y, be);
-                  ga = fma(x, y, ga);
-                }
-                if (!(ga == 0.0 || fabs(ga) <= 1e-15 * sqrt(al * be))) {
-                  rot = true;
-                  const double zeta = (be - al) / (2.0 * ga);
-                  const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-                  const double c = 1.0 / sqrt(1.0 + t * t);
-                  const double sn = c * t;
-                  for (int i = 0; i < I; ++i) {
-                    const double x = A[i * R + p], y = A[i * R + q];
-                    A[i * R + p] = c * x - sn * y;
-                    A[i * R + q] = sn * x + c * y;
-                  }
-                  for (int r = 0; r < R; ++r) {
-                    const double x = Vj[r * R + p], y = Vj[r * R + q];
-                    Vj[r * R + p] = c * x - sn * y;
-                    Vj[r * R + q] = sn * x + c * y;
-                  }
-                }
+            }
+            const bool valid = act && q < R;
+            double al = 0.0, be = 0.0, ga = 0.0;
+            if (valid)
+              for (int i = sub; i < I; i += g) {
+                const double x = A[i * R + p], y = A[i * R + q];
+                al = fma(x, x, al);
+                be = fma(y, y, be);
+                ga = fma(x, y, ga);
+              }
+            if (g > 1) {
+              double sa = 0.0, sb = 0.0, sg = 0.0;
+              for (int j = 0; j < g; ++j) {
+                sa += __shfl_sync(dev::kFull, al, base + j);
+                sb += __shfl_sync(dev::kFull, be, base + j);
+                sg += __shfl_sync(dev::kFull, ga, base + j);
+              }
+              al = sa;
+              be = sb;
+              ga = sg;
+            }
+            if (valid && !(ga == 0.0 || fabs(ga) <= 1e-15 * sqrt(al * be))) {
+              rot = true;
+              const double zeta = (be - al) / (2.0 * ga);
+              const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+              const double c = 1.0 / sqrt(1.0 + t * t);
+              const double sn = c * t;
+              for (int i = sub; i < I; i += g) {
+                const double x = A[i * R + p], y = A[i * R + q];
+                A[i * R + p] = c * x - sn * y;
+                A[i * R + q] = sn * x + c * y;
+              }
+              for (int r = sub; r < R; r += g) {
+                const double x = Vj[r * R + p], y = Vj[r * R + q];
+                Vj[r * R + p] = c * x - sn * y;
+                Vj[r * R + q] = sn * x + c * y;
               }
             }
             __syncwarp();
