@@ -85,7 +85,7 @@ struct LgWarp {
   static constexpr int LDV = RP + 2;  // V'^T: even, 16-byte rows for the paired updates
   static constexpr int kMat = RP * LDM;
   static constexpr int kVt = RP * LDV;
-  static constexpr int NBLK = (RP / 2) * (RP / 2 + 1) / 2;
+  static constexpr int NBLK = (RP / 2) * (RP / 2 - 1) / 2;  // off-diagonal 2 x 2 blocks (slot i1 < i2)
   static constexpr int kTabD = ((NBLK + (RP - 1) * (RP / 2) + 7) / 8) * 2;  // uint16 tables, in doubles (even)
   // M, V'^T, w, u (1/sqrt diag), then per pair slot and double-buffered: (c, s), t M_pq, int4 offsets
   static constexpr int kWarpD = kMat + kVt + 2 * RP + 2 * (RP + RP / 2 + RP);
@@ -159,7 +159,7 @@ __global__ void __launch_bounds__(LgWarp<RP>::WPB * 32, 1) k_procrustes_large_w(
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int R = EXACT ? RP : a.R;
   const int RR = R * R;
-  const int m = (R + 1) & ~1, half = m / 2, nblk = half * (half + 1) / 2;
+  const int m = (R + 1) & ~1, half = m / 2, nblk = half * (half - 1) / 2;
   std::uint16_t* blk = reinterpret_cast<std::uint16_t*>(smem);  // 2 x 2 block (slot i1, slot i2) of M
   std::uint16_t* sched = blk + L::NBLK;                         // round-robin (p, q) per (round, slot)
   double* M = smem + L::kTabD + wid * L::kWarpDE;
@@ -171,13 +171,13 @@ __global__ void __launch_bounds__(LgWarp<RP>::WPB * 32, 1) k_procrustes_large_w(
   double2* rotb = reinterpret_cast<double2*>(u + RP);
   double* rtb = reinterpret_cast<double*>(rotb + RP);
   int4* ofsb = reinterpret_cast<int4*>(rtb + RP);
-  for (int it = threadIdx.x; it < nblk; it += blockDim.x) {
+  for (int it = threadIdx.x; it < nblk; it += blockDim.x) {  // (the slots' own 2 x 2 blocks: param_store)
     int i1 = 0, r = it;
-    while (r >= half - i1) {
-      r -= half - i1;
+    while (r >= half - 1 - i1) {
+      r -= half - 1 - i1;
       ++i1;
     }
-    blk[it] = static_cast<std::uint16_t>((i1 << 8) | (i1 + r));
+    blk[it] = static_cast<std::uint16_t>((i1 << 8) | (i1 + 1 + r));
   }
   for (int it = threadIdx.x; it < (m - 1) * half; it += blockDim.x) {
     const int round = it / half, l = it - round * half;
@@ -401,7 +401,7 @@ __global__ void __launch_bounds__(LgWarp<RP>::WPB * 32, 1) k_procrustes_large_w(
           in.ga = in.q != 0xff ? M[in.p < qq ? in.p * LDM + qq : qq * LDM + in.p] : 0.0;
           return in;
         };
-        auto param_store = [&](const PIn& in, int buf) {
+        auto param_store = [&](const PIn& in, int buf, bool diag) {
           const bool on = in.q != 0xff && in.al > tiny && in.be > tiny &&
                           in.ga * in.ga > (kSkipL * kSkipL) * (in.al * in.be);
           // t = sign(zeta) / (|zeta| + sqrt(1 + zeta^2)), zeta = (be - al) / (2 ga),
@@ -412,18 +412,27 @@ __global__ void __launch_bounds__(LgWarp<RP>::WPB * 32, 1) k_procrustes_large_w(
           const double tt = on ? (d >= 0.0 ? g2 : -g2) * dev::rcp_nr(fabs(d) + rh) : 0.0;
           const double c = on ? dev::rsqrt_nr(fma(tt, tt, 1.0)) : 1.0;
           if (lane < half) {
+            // the slot's own 2 x 2 block (M_pp, M_qq, M_pq) is updated here, by
+            // the lane that holds its old values: no other block of the round
+            // touches these entries, and the next parameter load follows the
+            // round's block updates
+            if (on && diag) {  // (not for the wrapped-around load of the sweep's last round)
+              const double dt = __dmul_rn(tt, in.ga);
+              M[in.p * LDM + in.p] = in.al - dt;
+              M[in.q * LDM + in.q] = in.be + dt;
+              M[in.p < in.q ? in.p * LDM + in.q : in.q * LDM + in.p] = 0.0;
+            }
             rotb[buf * (RP / 2) + lane] = make_double2(c, c * tt);
             rtb[buf * (RP / 2) + lane] = tt * in.ga;
             ofsb[buf * (RP / 2) + lane] = in.q != 0xff ? make_int4(in.p * LDM, in.q * LDM, in.p, in.q)
                                                       : make_int4(in.p * LDM, -1, in.p, -1);
           }
         };
-        param_store(param_load(0), 0);
+        param_store(param_load(0), 0, true);
         __syncwarp();
         for (int round = 0; round < m - 1; ++round) {
           const int buf = round & 1;
           const double2* rot = rotb + buf * (RP / 2);
-          const double* rt = rtb + buf * (RP / 2);
           const int4* ofs = ofsb + buf * (RP / 2);
           // M <- J^T M J over this lane's 2 x 2 blocks of slot pairs
 #pragma unroll
@@ -444,13 +453,6 @@ __global__ void __launch_bounds__(LgWarp<RP>::WPB * 32, 1) k_procrustes_large_w(
               const double xu = M[au], xv = M[av];
               M[au] = cc * xu - ss * xv;
               M[av] = ss * xu + cc * xv;
-              continue;
-            }
-            if (i1 == i2) {
-              const double d = rt[i1];
-              M[o1.x + o1.z] -= d;
-              M[o1.y + o1.w] += d;
-              M[o1.z < o1.w ? o1.x + o1.w : o1.y + o1.z] = 0.0;
               continue;
             }
             const double c1 = r1.x, s1 = r1.y, c2 = r2.x, s2 = r2.y;
@@ -511,7 +513,7 @@ __global__ void __launch_bounds__(LgWarp<RP>::WPB * 32, 1) k_procrustes_large_w(
             }
           }
           // ... and the parameters into the other buffer
-          param_store(nxt, buf ^ 1);
+          param_store(nxt, buf ^ 1, round + 1 < m - 1);
           __syncwarp();
         }
       }

@@ -1,4 +1,4 @@
-CFG=4 K=100000 ITERS=4 timeout 600 ncu --set full --clock-control none --import-source on -k regex:"k_procrustes_large_w" -s 3 -c 1 -o /tmp/prof83 python scripts/prof_large.py > gpurun_out/ncu83.log 2>&1; echo "ncu rc=$?"
+CFG=4 K=100000 ITERS=4 timeout 600 ncu -f --set full --clock-control none --import-source on -k regex:"k_procrustes_large_w" -s 3 -c 1 -o /tmp/prof83 python scripts/prof_large.py > gpurun_out/ncu83.log 2>&1; echo "ncu rc=$?"
 python scripts/ncu_summary.py /tmp/prof83.ncu-rep > gpurun_out/full83.txt 2>&1
 python scripts/ncu_lines.py /tmp/prof83.ncu-rep k_procrustes_large_w 400 > gpurun_out/lines83.txt 2>&1
 ncu -i /tmp/prof83.ncu-rep --page raw --csv 2>/dev/null | python -c "
