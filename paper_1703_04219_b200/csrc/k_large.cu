@@ -240,9 +240,22 @@ __global__ void __launch_bounds__(LgWarp<RP>::WPB * 32, 1) k_procrustes_large_w(
     __syncwarp();
     // rows of X~ = X_k V D: from the previous mode-3 pass's X V rows when
     // available (a coalesced copy), else gathered (lane per row)
-    if (a.XV) {
+    if (a.XV) {  // 8 loads in flight per lane before the stores (they would alias)
       const double* xs = a.XV + r0 * R;
-      for (int e = lane; e < I * R; e += 32) Xs[e] = xs[e] * w[e % R];
+      const int n = I * R;
+      for (int e0 = 0; e0 < n; e0 += 256) {
+        double t[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int e = e0 + lane + 32 * u;
+          t[u] = e < n ? __ldg(xs + e) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int e = e0 + lane + 32 * u;
+          if (e < n) Xs[e] = t[u] * w[e % R];
+        }
+      }
     } else
     for (int i = lane; i < I; i += 32) {
       double xv[RP];
