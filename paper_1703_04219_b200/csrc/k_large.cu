@@ -112,6 +112,24 @@ __host__ __device__ constexpr int rr_l0(int m, int x) {
   return (x & 1) ? ((x >> 1) == 0 ? m - 1 : m - 1 - (x >> 1)) : (x >> 1);
 }
 
+/// dst[e] = src[e], e < n, by a warp: 8 loads in flight per lane ahead of
+/// the stores (global to global: the compiler cannot reorder them itself).
+__device__ __forceinline__ void warp_copy(double* dst, const double* src, int n, int lane) {
+  for (int e0 = 0; e0 < n; e0 += 256) {
+    double t[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int e = e0 + lane + 32 * u;
+      t[u] = e < n ? src[e] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int e = e0 + lane + 32 * u;
+      if (e < n) dst[e] = t[u];
+    }
+  }
+}
+
 /// out(i, j) for i < rows, j < R of the product sum_c a(i, c) b(c, j), c < R,
 /// on DMMA m8n8k4 (row.col): lane (fm, fk) feeds A[fm][fk] and B[fk][fm] and
 /// holds C[fm][2 fk + h].  8-row tiles of the output in turn, all RP/8
@@ -236,7 +254,10 @@ __global__ void __launch_bounds__(LgWarp<RP>::WPB * 32, 1) k_procrustes_large_w(
     const int I = static_cast<int>(a.X.srp[k + 1] - r0);
     for (int r = lane; r < R; r += 32) w[r] = a.W[k * R + r];
     double* Ek = a.Ewarm + k * RR;
-    for (int e = lane; e < RR; e += 32) Es[e] = a.ew_valid ? Ek[e] : ((e / R == e % R) ? 1.0 : 0.0);
+    if (a.ew_valid)
+      warp_copy(Es, Ek, RR, lane);
+    else
+      for (int e = lane; e < RR; e += 32) Es[e] = (e / R == e % R) ? 1.0 : 0.0;
     __syncwarp();
     // rows of X~ = X_k V D: from the previous mode-3 pass's X V rows when
     // available (a coalesced copy), else gathered (lane per row)
@@ -550,7 +571,7 @@ __global__ void __launch_bounds__(LgWarp<RP>::WPB * 32, 1) k_procrustes_large_w(
           R, R, [&](int i, int c) { return Es[i * R + c]; }, [&](int c, int j) { return Vt[j * LDV + c]; },
           [&](int i, int j, double v) { Ns[i * R + j] = v; });
       __syncwarp();
-      for (int e = lane; e < RR; e += 32) Es[e] = Ns[e];
+      warp_copy(Es, Ns, RR, lane);
       __syncwarp();
       if (!converged) {
         flag = P2G_FLAG_ACCURATE;
@@ -635,7 +656,7 @@ __global__ void __launch_bounds__(LgWarp<RP>::WPB * 32, 1) k_procrustes_large_w(
       __syncwarp();
       break;
     }
-    for (int e = lane; e < RR; e += 32) Ek[e] = Es[e];
+    warp_copy(Ek, Es, RR, lane);
     if (lane == 0) a.flags[k] = flag;
     __syncwarp();
   }
