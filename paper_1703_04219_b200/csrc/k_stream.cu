@@ -66,12 +66,14 @@ __device__ __forceinline__ void build_batch_ops(std::int64_t k0, int nb, const d
   // 1. stage S_s (full, row-major [c][b]) into the T area: every load of
   //    the batch issued before any store (one dependent load at a time left
   //    the setup latency-bound)
-  if constexpr (MODE == 2) {  // (mode 2: the plain loop measured faster; register budget)
+  if constexpr (MODE == 2) {  // (mode 2: the batched form below costs a CTA per SM in registers)
+#pragma unroll 4
     for (int idx = lane; idx < nb * C::RR; idx += 32) {
       const int s = idx / C::RR, e = idx - s * C::RR;
       const int c = e / R, b = e - c * R;
       const std::int64_t k = k0 + s;
-      Tw[e * C::SBP + s] = fl[s] != P2G_FLAG_FULL_RANK ? Shat[k * C::RR + e] : Sbuf[k * C::NT + tri_idx(c, b)];
+      Tw[e * C::SBP + s] =
+          fl[s] != P2G_FLAG_FULL_RANK ? __ldg(Shat + k * C::RR + e) : __ldg(Sbuf + k * C::NT + tri_idx(c, b));
     }
   } else {
   constexpr int NIT = (C::SB * C::RR + 31) / 32;
