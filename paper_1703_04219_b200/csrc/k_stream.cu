@@ -183,8 +183,10 @@ __global__ void __launch_bounds__(StreamCfg<R>::WPB * 32)
         if (r < nrows) {
           while (rowoff[sl + 1] <= r) ++sl;
           su[u] = sl;
-          p0[u] = X.rp[row0 + r];
-          p1[u] = X.rp[row0 + r + 1];
+          if (!XV) {  // the row extents are only needed to gather
+            p0[u] = __ldg(X.rp + row0 + r);
+            p1[u] = __ldg(X.rp + row0 + r + 1);
+          }
         }
       }
       double xv[UR][R];
@@ -193,7 +195,7 @@ __global__ void __launch_bounds__(StreamCfg<R>::WPB * 32)
         for (int u = 0; u < UR; ++u) {
           const double* xr = XV + (row0 + cb + lane + 32 * u) * R;
 #pragma unroll
-          for (int a = 0; a < R; ++a) xv[u][a] = su[u] >= 0 ? xr[a] : 0.0;
+          for (int a = 0; a < R; ++a) xv[u][a] = su[u] >= 0 ? __ldg(xr + a) : 0.0;
         }
       } else {
         dev::csr_rows_times<R, UR, 1>(xv, xv, X.ci, X.val, p0, p1, Vprev, Vprev);
@@ -310,8 +312,8 @@ __global__ void __launch_bounds__(StreamCfg<R>::WPB * 32)
         if (r < nrows) {
           while (rowoff[sl + 1] <= r) ++sl;
           su[u] = sl;
-          p0[u] = X.rp[row0 + r];
-          p1[u] = X.rp[row0 + r + 1];
+          p0[u] = __ldg(X.rp + row0 + r);
+          p1[u] = __ldg(X.rp + row0 + r + 1);
         }
       }
       double xp[UR][R], xn[UR][R];  // both gathers share the entry stream
