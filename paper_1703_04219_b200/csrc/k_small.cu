@@ -264,11 +264,19 @@ __device__ __forceinline__ void jacobi_round(double (&g)[MP * (MP + 1) / 2], dou
     const double c = cs[i], s = sn[i];
     double2* ea = E2 + a * H * 32;
     double2* eb = E2 + b * H * 32;
+    // both columns loaded before any store (the compiler cannot tell that
+    // columns a and b do not overlap and would otherwise serialise each
+    // load behind the previous store)
+    double2 va[H], vb[H];
 #pragma unroll
     for (int kk = 0; kk < H; ++kk) {
-      const double2 va = ea[kk * 32], vb = eb[kk * 32];
-      ea[kk * 32] = make_double2(c * va.x - s * vb.x, c * va.y - s * vb.y);
-      eb[kk * 32] = make_double2(s * va.x + c * vb.x, s * va.y + c * vb.y);
+      va[kk] = ea[kk * 32];
+      vb[kk] = eb[kk * 32];
+    }
+#pragma unroll
+    for (int kk = 0; kk < H; ++kk) {
+      ea[kk * 32] = make_double2(c * va[kk].x - s * vb[kk].x, c * va[kk].y - s * vb[kk].y);
+      eb[kk * 32] = make_double2(s * va[kk].x + c * vb[kk].x, s * va[kk].y + c * vb[kk].y);
     }
   }
   // physical permutation g_new[tri(sigma x, sigma y)] = g_old[tri(x, y)],
