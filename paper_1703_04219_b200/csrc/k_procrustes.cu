@@ -411,10 +411,25 @@ __global__ void __launch_bounds__(WPB * 32) k_procrustes_accurate(K1Args a, doub
               const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
               const double c = 1.0 / sqrt(1.0 + t * t);
               const double sn = c * t;
-              for (int i = sub; i < I; i += g) {
-                const double x = A[i * R + p], y = A[i * R + q];
-                A[i * R + p] = c * x - sn * y;
-                A[i * R + q] = sn * x + c * y;
+              // R > 16: 8 rows' loads ahead of their stores (possible aliasing
+              // keeps them in order otherwise); R <= 16 keeps its register budget
+              constexpr int UB = RP > 16 ? 8 : 1;
+              for (int i0 = sub; i0 < I; i0 += UB * g) {
+                double x[UB], y[UB];
+#pragma unroll
+                for (int u = 0; u < UB; ++u) {
+                  const int i = i0 + u * g;
+                  x[u] = i < I ? A[i * R + p] : 0.0;
+                  y[u] = i < I ? A[i * R + q] : 0.0;
+                }
+#pragma unroll
+                for (int u = 0; u < UB; ++u) {
+                  const int i = i0 + u * g;
+                  if (i < I) {
+                    A[i * R + p] = c * x[u] - sn * y[u];
+                    A[i * R + q] = sn * x[u] + c * y[u];
+                  }
+                }
               }
               for (int r = sub; r < R; r += g) {
                 const double x = Vj[r * R + p], y = Vj[r * R + q];
