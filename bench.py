@@ -130,17 +130,21 @@ def algorithmic_bytes(X, R):
     w = 8 * K * R
     v = 8 * J * R
     gather_u = 8 * nnz * R  # M2 = X^T U: one U row per entry
+    xv = q  # X V rows (NR x R) left by mode 3 for the next iteration's passes
     return {
-        # small-R Q-free pipeline
+        # small-R Q-free pipeline (steady state: the X V rows of the previous
+        # mode-3 pass replace mode 2's CSR pass and mode 3's V_{t-1} gathers)
         "polar": 8 * K * (2 * nt + R),                  # C, W in; S out
-        "mode2": csr + 8 * K * nt + w + v + q + csc + gather_u,  # rows: CSR, S, W in, U out; CSC + U rows in
-        "mode3": csr + 8 * K * nt + w + w + 8 * K * nt + 2 * v,  # CSR, S, W in; m3, next C out
+        "mode2": xv + 8 * K * nt + w + q + csc + gather_u,  # X V rows, S, W in, U out; CSC + U rows in
+        "mode3": csr + xv + xv + 8 * K * nt + w + w + 8 * K * nt + v,  # CSR, X V in and out, S, W in; m3, next C out
         "update_w": 2 * w,                              # m3 in, W out (NNLS)
         "fit": 2 * w,                                   # W, m3 in (gram + cross)
-        # large-R pipeline: Procrustes writes Q and E (warm start) ...
-        "procrustes": csr + q + w + v + 2 * 8 * K * R * R,
+        # large-R pipeline: Procrustes reads the X V rows, writes Q, E in/out (warm start) ...
+        "procrustes": xv + q + w + 2 * 8 * K * R * R,
         # ... mode 2 = Q in, U out, CSC + U rows in
         "mode2_large": 2 * q + csc + gather_u,
+        # ... mode 3 = Q and the CSR in, X V rows and m3 out
+        "mode3_large": q + csr + xv + w + v,
         # SURVEY.md §8d north-star iteration bytes (Q-based formulation)
         "iteration": 3 * csr + 3 * q + 4 * w + 4 * v,
     }
@@ -307,7 +311,7 @@ def main():
     roofline = None
     if dom:
         t_launch = cand[dom][0] * 1e-3
-        akey = "mode2_large" if (dom == "mode2" and R > 16) else dom
+        akey = (dom + "_large") if (dom in ("mode2", "mode3") and R > 16) else dom
         achieved = ab[akey] / t_launch / 1e9
         traffic = None
         tpath = os.path.join(ROOT, "profiles", "traffic_r01.json")
