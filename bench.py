@@ -4,18 +4,22 @@
 
 A "step" is one full PARAFAC2-ALS outer iteration (Procrustes + MTTKRP modes
 1-3 + H/V/W updates + fit, solver.hpp:274-318) over the whole synthetic
-workload.  Default workload: BASELINE.json configs[1] ("cfg2": K=1M
-subjects, J=5000, R=10, ~63M nnz, fp64), generated on the host (seeded,
-SURVEY.md §8d); inputs are far larger than L2 (CSR 1.2 GB + Q 4 GB vs
-126 MB), so no L2 flush is needed between steps.
+workload.  Default workload: BASELINE.json configs[3] ("cfg4": K=1M
+subjects, J=5000, R=40, ~500M nnz, fp64) -- the north star's named config and
+the largest that fits one GPU -- generated on the host (seeded, SURVEY.md
+§8d); inputs are far larger than L2 (CSR 6.2 GB + Q 18.7 GB vs 126 MB), so
+no L2 flush is needed between steps.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2] [--impl b200|reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 4] [--impl b200|reference]
 
 Under torchrun (N>1) each rank owns the subjects partition_weighted gives it
-(weak per-rank share of one fixed workload -> "scaling": "strong").
+(a per-rank share of one fixed workload -> "scaling": "strong").
 ``--impl reference`` times the reference algorithm's CPU implementation (the
-oracle port; the reference itself cannot be compiled here) on
-the host cores, rank 0 only.
+oracle port, built -O3 -march=native on the box; the reference itself cannot
+be compiled here) on the host cores, rank 0 only.  The CPU legs
+(``--impl reference`` and the ``cpu_baseline`` of the default run) generate
+their inputs with the oracle's own restatement of the BASELINE generator and
+never load libp2g.
 """
 import argparse
 import json
@@ -150,6 +154,21 @@ def algorithmic_bytes(X, R):
     }
 
 
+
+def procrustes_flops(K, n_rows, R):
+    """Algorithmic FP64 flops of one Procrustes launch (the per-subject dense
+    R x R work of SURVEY.md 8(d)'s F_iter): four I_k x R x R products
+    (B = X~ T, M = B^T B, F = B^T X~, Q = B Z: 8 sum(I_k) R^2) plus the
+    symmetric eigensolve and inverse square root (9 R^3 + 2 R^3 per subject)."""
+    return 8.0 * n_rows * R * R + 11.0 * K * R ** 3
+
+
+def polar_flops(K, R):
+    """k_polar_small (R <= 16): the R x R eigensolve + inverse square root and
+    the m1 partial per subject (11 R^3 + 2 R^3)."""
+    return 13.0 * K * R ** 3
+
+
 def setup_dist():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -163,80 +182,159 @@ def setup_dist():
     return world, rank, local
 
 
-def cpu_baseline(X, R, cfg_id, target_s=12.0, threads=None):
-    """Oracle (CPU restatement of the reference, kind "port") on a bounded
-    prefix of the same workload, all host threads."""
-    import paper_1703_04219_b200 as p2g
-    from tests.helpers import load_oracle, oracle_from_csr
+def workload_config(cfg_id, R, K, J, nnz, rows, world):
+    """The `config` object both arms print (identical for the same workload)."""
+    return {"workload": CONFIG_NAME[cfg_id], "config_id": cfg_id, "rank": R, "K": int(K), "J": int(J),
+            "nnz": int(nnz), "rows": int(rows), "nonneg": True, "fp": "f64",
+            "l2": "inputs larger than L2 (CSR+Q >> 126 MB), no flush",
+            "parallelism": f"subject-shard x{world}"}
 
-    o = load_oracle()
-    threads = threads or (os.cpu_count() or 1)
-    probe = min(X.K, 2000)
-    Xs = X.subset(0, probe)
-    H0, V0, W0 = p2g.init_factors(102, Xs.K, Xs.J, R)
+
+# ---------------------------------------------------------------------------
+# CPU legs: the oracle (a restatement of the reference's CPU path; the
+# reference itself cannot be compiled, SURVEY.md F2).  They import the oracle
+# module only -- never libp2g -- and generate their inputs with the oracle's
+# restatement of the BASELINE generator (oracle/baseline_gen.hpp).
+# ---------------------------------------------------------------------------
+def load_cpu_oracle():
+    """The oracle built -O3 -march=native on THIS host (make -C oracle native);
+    falls back to the portable -march=x86-64-v3 test build if that fails."""
+    native = os.path.join(ROOT, "oracle", "_build_native")
+    build = "native"
+    try:
+        subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "oracle"), "native"], check=True,
+                       stdout=subprocess.DEVNULL, stderr=subprocess.PIPE, timeout=600)
+        path = native
+    except Exception:
+        path, build = os.path.join(ROOT, "oracle", "_build"), "portable"
+    if path not in sys.path:
+        sys.path.insert(0, path)
+    import p2oracle  # noqa: E402
+
+    return p2oracle, ("-O3 -march=native" if build == "native" else "-O3 -march=x86-64-v3")
+
+
+def oracle_sample(o, cfg_id, R, n_subjects, threads):
+    """The first n_subjects of config cfg_id as an oracle Tensor, and the D2
+    initial factors of the FULL workload restricted to those subjects."""
+    spec = o.baseline_spec(cfg_id, R)
+    J, srp, rp, ci, v = o.baseline_generate(cfg_id, R, n_subjects, threads)
+    T = o.Tensor.from_csr(J, srp, rp, ci, v)
+    H0, V0, W0 = o.baseline_init(spec["seed"], spec["K"], J, R, n_subjects)
+    return T, H0, V0, W0, int(rp[-1]), int(srp[-1])
+
+
+def cpu_iteration_rate(o, cfg_id, R, threads, target_s, warmup, steps):
+    """Times `steps` oracle ALS iterations (after `warmup`, one fit) on a
+    subject prefix sized so one iteration takes about target_s.  Step time is
+    the reference's own per-phase timers (solver.hpp:278-297: procrustes +
+    project + cp).  One part of an iteration does not scale with the number
+    of subjects: the V solve over J rows (nnls_rowwise, cp.hpp:117-121; the
+    oracle times it as ms_v_update).  The full-workload iteration time is
+    therefore estimated as t_V + (nnz_full / nnz_sample) (t_step - t_V)."""
+    spec = o.baseline_spec(cfg_id, R)
+    K = spec["K"]
+    probe = min(K, 400 if R > 16 else 4000)
+    T, H0, V0, W0, _, _ = oracle_sample(o, cfg_id, R, probe, threads)
+    r = o.fit_parafac2(T, R, max_iters=2, tol=1e-300, nonneg=True, threads=threads, H0=H0, V0=V0, W0=W0)
+    step = r["ms_procrustes"][1] + r["ms_project"][1] + r["ms_cp"][1]
+    fixed = r["ms_v_update"][1]
+    per_subject = max(step - fixed, 1e-3) * 1e-3 / probe
+    n = int(min(K, max(probe, (target_s - fixed * 1e-3) / per_subject)))
+    T, H0, V0, W0, nnz, rows = oracle_sample(o, cfg_id, R, n, threads)
     t0 = time.perf_counter()
-    o.fit_parafac2(oracle_from_csr(o, Xs), R, max_iters=1, tol=1e-300, nonneg=True, threads=threads, H0=H0, V0=V0,
-                   W0=W0)
-    dt = max(time.perf_counter() - t0, 1e-3)
-    per_subject = dt / probe
-    n = int(min(X.K, max(probe, target_s / 3.0 / per_subject)))
-    Xs = X.subset(0, n)
-    H0, V0, W0 = p2g.init_factors(102, Xs.K, Xs.J, R)
-    T = oracle_from_csr(o, Xs)
-    iters = 3
-    t0 = time.perf_counter()
-    r = o.fit_parafac2(T, R, max_iters=iters, tol=1e-300, nonneg=True, threads=threads, H0=H0, V0=V0, W0=W0)
-    dt = time.perf_counter() - t0
-    sec_iter = dt / iters
-    return {"value": Xs.nnz / sec_iter, "unit": "nnz/s", "cores": threads, "kind": "port",
-            "sample": f"first {n} of {X.K} subjects of {CONFIG_NAME[cfg_id].split(' (')[0]} "
-                      f"({Xs.nnz} nnz), {iters} ALS iterations, oracle/p2_oracle.hpp -O3, {threads} threads",
-            "sec_per_iter_sample": sec_iter, "est_sec_per_iter_full": sec_iter * X.nnz / Xs.nnz,
-            "fit": r["fit"]}
+    r = o.fit_parafac2(T, R, max_iters=warmup + steps, tol=1e-300, nonneg=True, threads=threads, H0=H0, V0=V0,
+                       W0=W0)
+    wall = time.perf_counter() - t0
+    sl = slice(warmup, warmup + steps)
+    ph = {k: [float(x) for x in r[k][sl]] for k in ("ms_procrustes", "ms_project", "ms_cp", "ms_v_update")}
+    ms_steps = [a + b + c for a, b, c in zip(ph["ms_procrustes"], ph["ms_project"], ph["ms_cp"])]
+    ms = float(np.mean(ms_steps))
+    ms_fixed = float(np.mean(ph["ms_v_update"]))
+    return {"n_subjects": n, "nnz": nnz, "rows": rows, "ms_per_iter": ms, "nnz_per_s": nnz / (ms * 1e-3),
+            "ms_per_iter_all": ms_steps, "phase_ms_mean": {k: float(np.mean(v)) for k, v in ph.items()},
+            "ms_v_update": ms_fixed, "wall_s_fit": wall, "iterations_in_fit": warmup + steps,
+            "fit": [float(x) for x in r["fit"]]}
+
+
+def full_estimate(m, full_nnz):
+    """Full-workload seconds per iteration from a prefix sample (see
+    cpu_iteration_rate)."""
+    fixed = m["ms_v_update"] * 1e-3
+    return fixed + (m["ms_per_iter"] * 1e-3 - fixed) * full_nnz / max(m["nnz"], 1)
+
+
+def cpu_baseline(cfg_id, R, full_nnz, full_K, target_s=6.0):
+    """`cpu_baseline` of the default (N=1) line: the oracle port on a bounded
+    prefix of the same workload, all host threads, 1 warm-up + 2 timed
+    iterations, extrapolated to the full workload (cpu_iteration_rate)."""
+    o, flags = load_cpu_oracle()
+    threads = os.cpu_count() or 1
+    m = cpu_iteration_rate(o, cfg_id, R, threads, target_s, warmup=1, steps=2)
+    t_full = full_estimate(m, full_nnz)
+    return {"value": full_nnz / t_full, "unit": "nnz/s", "cores": threads, "kind": "port",
+            "sample": (f"first {m['n_subjects']} of {full_K} subjects of {CONFIG_NAME[cfg_id].split(' (')[0]} "
+                       f"({m['nnz']} nnz), iterations 2-3 of a fit from the same initial factors; "
+                       f"oracle/p2_oracle.hpp {flags}, {threads} threads; time = the reference's per-phase timers; "
+                       f"value = full nnz / (t_V + nnz_full/nnz_sample (t_iter - t_V)), t_V the J-row V solve"),
+            "sec_per_iter_sample": m["ms_per_iter"] * 1e-3, "sample_value": m["nnz_per_s"],
+            "phase_ms_mean": m["phase_ms_mean"], "est_sec_per_iter_full": t_full, "cpu_model": cpu_model()}
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
 
 
 def run_reference(args):
-    world, rank, _ = (int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")), 0)
+    world, rank = int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    import paper_1703_04219_b200 as p2g
-
+    o, flags = load_cpu_oracle()
     cfg_id = args.config
     R = args.rank or CONFIG_RANK[cfg_id]
-    X = p2g.generate_baseline(cfg_id, R)
-    from tests.helpers import load_oracle, oracle_from_csr
-
-    o = load_oracle()
     threads = os.cpu_count() or 1
-    # bounded sample: a prefix sized for ~args.ref_seconds of CPU per step
-    probe = min(X.K, 2000)
-    Xs = X.subset(0, probe)
-    H0, V0, W0 = p2g.init_factors(102, Xs.K, Xs.J, R)
-    t0 = time.perf_counter()
-    o.fit_parafac2(oracle_from_csr(o, Xs), R, max_iters=1, tol=1e-300, threads=threads, H0=H0, V0=V0, W0=W0)
-    per_subject = max(time.perf_counter() - t0, 1e-3) / probe
-    n = int(min(X.K, max(probe, args.ref_seconds / per_subject)))
-    Xs = X.subset(0, n)
-    H0, V0, W0 = p2g.init_factors(102, Xs.K, Xs.J, R)
-    T = oracle_from_csr(o, Xs)
-    o.fit_parafac2(T, R, max_iters=max(args.warmup, 1), tol=1e-300, threads=threads, H0=H0, V0=V0, W0=W0)
-    t0 = time.perf_counter()
-    o.fit_parafac2(T, R, max_iters=args.steps, tol=1e-300, threads=threads, H0=H0, V0=V0, W0=W0)
-    dt = time.perf_counter() - t0
-    ms = dt / args.steps * 1e3
-    value = Xs.nnz / (dt / args.steps)
-    sample = (f"first {n} of {X.K} subjects of {CONFIG_NAME[cfg_id]} ({Xs.nnz} nnz) per step; "
-              f"oracle port of the reference CPU path, {threads} threads")
+    # the full workload's shape for the config line (same config as the GPU arm)
+    J, srp, rp, _, _ = o.baseline_generate(cfg_id, R, 0, threads)
+    K, rows, nnz = len(srp) - 1, int(srp[-1]), int(rp[-1])
+    del srp, rp
+    # each step: one oracle ALS iteration over a bounded prefix, sized so the
+    # whole --steps K --warmup W run takes a few minutes
+    per_step = min(args.ref_seconds, 150.0 / max(args.steps + args.warmup, 1))
+    m = cpu_iteration_rate(o, cfg_id, R, threads, per_step, warmup=max(args.warmup, 0), steps=args.steps)
+    t_full = full_estimate(m, nnz)
+    value = nnz / t_full
+    sample = (f"first {m['n_subjects']} of {K} subjects ({m['nnz']} nnz) per step, "
+              f"{args.warmup} warm-up + {args.steps} timed iterations of one fit; oracle port of the reference CPU "
+              f"path (oracle/p2_oracle.hpp {flags}), {threads} threads; step time = the reference's per-phase "
+              f"timers (solver.hpp:278-297); value = full nnz / (t_V + nnz_full/nnz_sample (t_iter - t_V)), "
+              f"t_V the J-row V solve")
     line = {"metric": METRIC, "value": value, "unit": "nnz/s", "impl": "reference", "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": CONFIG_NAME[cfg_id], "config_id": cfg_id, "rank": R, "K": X.K, "J": X.J,
-                       "nnz": X.nnz, "sample_subjects": n, "sample_nnz": Xs.nnz},
-            "cpu_baseline": {"value": value, "unit": "nnz/s", "cores": threads, "kind": "port", "sample": sample},
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_full * 1e3,
+            "sec_per_iter": t_full, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded generator, SURVEY.md 8d)",
+            "config": workload_config(cfg_id, R, K, J, nnz, rows, world),
+            "cpu_baseline": {"value": value, "unit": "nnz/s", "cores": threads, "kind": "port", "sample": sample,
+                             "cpu_model": cpu_model()},
             "e2e": {"value": value, "unit": "nnz/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-            "gpu_launches": 0}
+            "phase_ms_mean": m["phase_ms_mean"], "ms_per_iter_all": m["ms_per_iter_all"],
+            "wall_s_fit": m["wall_s_fit"], "sample_ms_per_iter": m["ms_per_iter"], "sample_value": m["nnz_per_s"],
+            "ms_v_update": m["ms_v_update"], "gpu_launches": 0}
     print(json.dumps(line), flush=True)
     return 0
+
+
+def pinned_like(torch, a):
+    t = torch.empty(a.shape, dtype={np.int64: torch.int64, np.int32: torch.int32, np.float64: torch.float64}[
+        a.dtype.type], pin_memory=True)
+    t.numpy()[...] = a
+    return t
 
 
 def main():
@@ -244,7 +342,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--config", type=int, default=4)
     ap.add_argument("--rank", type=int, default=0)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -286,7 +384,6 @@ def main():
 
     # warm-up (untimed), then exactly K timed steps
     ctx.bench_iterations(cfg, max(args.warmup, 1), H0, V0, W0, reset=True)
-    ctx.kernel_times()  # (reset below via reset=True on the timed run's state)
     barrier()
     import torch
 
@@ -303,43 +400,55 @@ def main():
     value = X.nnz / (ms_step * 1e-3)
     ktimes = ctx.kernel_times()
 
-    # roofline of the dominant kernel (largest share of the step)
+    # roofline of the dominant kernel (largest share of the step), against
+    # the bound that applies to it: FP64 for the per-subject R x R Procrustes
+    # work, HBM for the streaming passes
     peak, peak_kind = load_peaks()
-    ab = algorithmic_bytes(X.subset(kb, ke) if world > 1 else X, R)
+    fpk, fpk_kind = load_fp64_peak()
+    Xs = X.subset(kb, ke) if world > 1 else X
+    ab = algorithmic_bytes(Xs, R)
     cand = {k: v for k, v in ktimes.items() if k in ("polar", "procrustes", "mode2", "mode3", "update_w")}
     dom = max(cand, key=lambda k: cand[k][0]) if cand else None
     roofline = None
     if dom:
         t_launch = cand[dom][0] * 1e-3
         akey = (dom + "_large") if (dom in ("mode2", "mode3") and R > 16) else dom
-        achieved = ab[akey] / t_launch / 1e9
         traffic = None
-        tpath = os.path.join(ROOT, "profiles", "traffic_r01.json")
-        if os.path.exists(tpath):
-            try:
-                traffic = json.load(open(tpath)).get(f"cfg{cfg_id}", {}).get(dom)
-            except Exception:
-                traffic = None
-        roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
-                    "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
-                    "algorithmic_bytes_per_launch": ab[akey], "ms_per_launch": cand[dom][0],
-                    "share_of_step": sum(v[0] * v[1] for k, v in ktimes.items() if k == dom) /
-                                     max(sum(v[0] * v[1] for v in ktimes.values()), 1e-12)}
+        for tname in ("traffic_r02.json", "traffic_r01.json"):
+            tpath = os.path.join(ROOT, "profiles", tname)
+            if traffic is None and os.path.exists(tpath):
+                try:
+                    traffic = json.load(open(tpath)).get(f"cfg{cfg_id}", {}).get(dom)
+                except Exception:
+                    traffic = None
+        share = sum(v[0] * v[1] for k, v in ktimes.items() if k == dom) / \
+            max(sum(v[0] * v[1] for v in ktimes.values()), 1e-12)
+        hbm_view = {"achieved": ab[akey] / t_launch / 1e9, "peak": peak, "unit": "GB/s",
+                    "frac": ab[akey] / t_launch / 1e9 / peak, "algorithmic_bytes_per_launch": ab[akey]}
+        if dom in ("procrustes", "polar"):
+            fl = procrustes_flops(Xs.K, Xs.n_rows, R) if dom == "procrustes" else polar_flops(Xs.K, R)
+            ach = fl / t_launch / 1e12
+            roofline = {"bound": "fp64", "kernel": dom, "achieved": ach, "peak": fpk, "unit": "TFLOP/s",
+                        "frac": ach / fpk, "traffic": traffic, "peak_kind": fpk_kind,
+                        "algorithmic_flops_per_launch": fl,
+                        "flop_model": ("8 sum(I_k) R^2 + 11 K R^3" if dom == "procrustes" else "13 K R^3"),
+                        "ms_per_launch": cand[dom][0], "share_of_step": share, "hbm_view": hbm_view,
+                        "note": "fp64 has no tcgen05 kind (SURVEY F8); peak = measured DFMA rate"}
+        else:
+            roofline = {"bound": "hbm", "kernel": dom, "achieved": hbm_view["achieved"], "peak": peak,
+                        "unit": "GB/s", "frac": hbm_view["frac"], "traffic": traffic, "peak_kind": peak_kind,
+                        "algorithmic_bytes_per_launch": ab[akey], "ms_per_launch": cand[dom][0],
+                        "share_of_step": share}
     iter_gbs = ab["iteration"] / (ms_step * 1e-3) / 1e9
 
-    # end-to-end through the public API: pinned host CSR -> load_csr -> fit -> factors back
+    # end-to-end through the public API, every byte the reference's
+    # fit_parafac2 hands back included: pinned host CSR -> load -> fit ->
+    # H, V, W and every Q_k back to pinned host memory
     e2e = None
     if not args.no_e2e:
-        pin = {}
-        for name in ("subj_row_ptr", "row_ptr", "col_idx", "val"):
-            a = getattr(X, name)
-            t = torch.empty(a.shape, dtype={np.int64: torch.int64, np.int32: torch.int32,
-                                            np.float64: torch.float64}[a.dtype.type], pin_memory=True)
-            t.numpy()[...] = a
-            pin[name] = t
+        pin = {name: pinned_like(torch, getattr(X, name)) for name in ("subj_row_ptr", "row_ptr", "col_idx", "val")}
         Xp = p2g.CSRTensor(X.J, pin["subj_row_ptr"].numpy(), pin["row_ptr"].numpy(), pin["col_idx"].numpy(),
                            pin["val"].numpy())
-        # initial factors from pinned host memory too (column-major views)
         pinned_f = []
         for a in (H0, V0, W0):
             t = torch.empty(a.size, dtype=torch.float64, pin_memory=True)
@@ -347,11 +456,12 @@ def main():
             v[...] = a
             pinned_f.append((t, v))
         H0p, V0p, W0p = (v for _, v in pinned_f)
-        kb_, ke_, _, _ = ctx.shard_info()
         outs = []
-        for shp in ((R, R), (X.J, R), (ke_ - kb_, R)):
+        for shp in ((R, R), (X.J, R), (ke - kb, R)):
             t = torch.empty(shp[0] * shp[1], dtype=torch.float64, pin_memory=True)
             outs.append((t, t.numpy().reshape(shp[::-1]).T))
+        qt = torch.empty(nr * R, dtype=torch.float64, pin_memory=True)
+        qv = qt.numpy().reshape(nr, R)
         e2e_iters = args.steps
         barrier()
         torch.cuda.synchronize()
@@ -359,7 +469,7 @@ def main():
         ctx.load(Xp)
         t_load = time.perf_counter() - t0
         res = ctx.fit(p2g.SolverConfig(rank=R, max_iters=e2e_iters, tol=1e-300, nonneg=True), H0p, V0p, W0p,
-                      want_q=False, out=tuple(v for _, v in outs))
+                      out=tuple(v for _, v in outs), q_out=qv)
         torch.cuda.synchronize()
         dt = time.perf_counter() - t0
         if world > 1:
@@ -370,21 +480,22 @@ def main():
             dt = float(tt.item())
         h2d = (X.subj_row_ptr.nbytes + X.row_ptr.nbytes + X.col_idx.nbytes + X.val.nbytes + H0.nbytes + V0.nbytes
                + W0.nbytes)
-        d2h = res.H.nbytes + res.V.nbytes + res.W.nbytes + 8 * 2 * e2e_iters
+        d2h = res.H.nbytes + res.V.nbytes + res.W.nbytes + qv.nbytes + res.flags.nbytes + 8 * 3 * e2e_iters
         e2e = {"value": X.nnz * e2e_iters / dt, "unit": "nnz/s", "h2d_bytes_per_step": h2d // e2e_iters,
                "d2h_bytes_per_step": d2h // e2e_iters, "iterations_per_call": e2e_iters, "sec_per_call": dt,
-               "load_s": t_load, "fit_s": dt - t_load,
+               "load_s": t_load, "fit_s": dt - t_load, "q_bytes": qv.nbytes,
+               "what": "load(pinned CSR) + fit_parafac2 with every Q_k, H, V, W returned to pinned host memory",
                "fit_final": float(res.fit[-1])}
+        del pin, Xp, qt, qv, outs
 
-    # FP64 view of the step (the per-subject R x R work is FP64-issue bound)
-    fpk, fpk_kind = load_fp64_peak()
+    # FP64 view of the whole step (SURVEY.md 8(d) F_iter)
     flops = iteration_flops(X, R)
     fp_tf = flops / (ms_step * 1e-3) / 1e12
     fp64 = {"bound": "fp64", "achieved": fp_tf, "peak": fpk, "unit": "TFLOP/s", "frac": fp_tf / fpk,
             "flops_per_iter": flops, "peak_kind": fpk_kind, "model": "SURVEY.md 8(d) F_iter"}
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(X, R, cfg_id)
+        cpu = cpu_baseline(cfg_id, R, X.nnz, X.K)
 
     if rank == 0:
         line = {
@@ -392,12 +503,11 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms_step, "sec_per_iter": ms_step * 1e-3,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded generator, SURVEY.md 8d; inputs > L2, no flush needed)",
-            "config": {"workload": CONFIG_NAME[cfg_id], "config_id": cfg_id, "rank": R, "K": X.K, "J": X.J,
-                       "nnz": X.nnz, "rows": X.n_rows, "nonneg": True, "iterations_timed": args.steps,
-                       "l2": "inputs larger than L2 (CSR+Q >> 126 MB)", "parallelism": f"subject-shard x{world}"},
+            "config": workload_config(cfg_id, R, X.K, X.J, X.nnz, X.n_rows, world),
             "ms_per_iter_all": [float(x) for x in ms], "fit_trace": [float(x) for x in fits],
             "iteration_gbs_algorithmic": iter_gbs, "iteration_hbm_frac": iter_gbs / peak,
-            "roofline": roofline, "roofline_fp64": fp64, "kernel_ms_per_launch": {k: v[0] for k, v in ktimes.items()},
+            "roofline": roofline, "roofline_fp64_step": fp64,
+            "kernel_ms_per_launch": {k: v[0] for k, v in ktimes.items()},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches), "wall_s_timed": wall,
             "clocks": clk.summary(), "gen_s": t_gen,
         }

@@ -125,6 +125,31 @@ int p2g_load_csr(p2g_ctx* ctx, int64_t K, int64_t J, const int64_t* subj_row_ptr
 /* This rank's subject range [k_begin, k_end) and its row / nnz counts. */
 int p2g_shard_info(const p2g_ctx* ctx, int64_t* k_begin, int64_t* k_end, int64_t* n_rows, int64_t* nnz);
 
+/* Shard-local load: a rank passes only its own subjects [k_begin, k_end) of
+ * a K-subject tensor, with subj_row_ptr[k_end-k_begin+1] and row_ptr rebased
+ * to the shard (both start at 0).  The ranges must tile [0, K) in rank order
+ * (bit-exact shards: p2g_partition_weighted over nnz_k + I_k, the weights of
+ * solver.hpp:263-267).  Checks, ||X||^2 and the verdict are collective:
+ * every rank returns the same status.  Afterwards W0 / W arguments are this
+ * rank's rows only ((k_end-k_begin) x R).  Replaces the per-rank slice of
+ * IrregularTensor construction (sparse.hpp:176-215). */
+int p2g_load_shard(p2g_ctx* ctx, int64_t K, int64_t J, int64_t k_begin, int64_t k_end, const int64_t* subj_row_ptr,
+                   const int64_t* row_ptr, const int32_t* col_idx, const double* val);
+
+/* Host-staged collective, used instead of NCCL: fn reduces `count` doubles
+ * in place across all ranks (op 0 = sum, 1 = max) and returns 0 on success.
+ * A context created with world > 1 and nccl_id == NULL must set one before
+ * loading.  (The reference reduces thread partials with merge_tree,
+ * parallel.hpp:115-124; this is the cross-process analogue's seam.) */
+typedef int (*p2g_host_allreduce_fn)(double* buf, int64_t count, int32_t op, void* user);
+int p2g_set_host_collective(p2g_ctx* ctx, p2g_host_allreduce_fn fn, void* user);
+
+/* Fault injection (tests): kind 1 makes this rank's W-NNLS report a failure
+ * at the given iteration (1-based); kind 0 clears.  The error is agreed over
+ * all ranks in the iteration's last collective, so every rank raises
+ * NumericalError("NNLS did not converge") (kernels.hpp:137) together. */
+int p2g_inject_fault(p2g_ctx* ctx, int32_t kind, int32_t iteration);
+
 /* ------------------------------------------------------------------------
  * The fused PARAFAC2-ALS loop — replaces fit_parafac2 (solver.hpp:251-321).
  * ------------------------------------------------------------------------ */
@@ -134,7 +159,9 @@ typedef struct {
   double tol;         /* > 0; relative fit change stop          (solver.hpp:53) */
   int32_t nonneg;     /* NNLS on V and W                        (solver.hpp:54) */
   int32_t init;       /* 0: random V from seed, H=I, W=ones (solver.hpp:124-132);
-                         2: explicit H0/V0/W0 (D2).  (eye init: not on GPU.) */
+                         1: eye: V = |top-R eigenvectors of sum_k X_k^T X_k|,
+                            H=I, W=ones (solver.hpp:133-164), on the device;
+                         2: explicit H0/V0/W0 (D2). */
   uint64_t seed;      /*                                        (solver.hpp:56) */
 } p2g_fit_config;
 
@@ -153,6 +180,27 @@ typedef struct {
 int p2g_fit(p2g_ctx* ctx, const p2g_fit_config* cfg, const double* H0, const double* V0, const double* W0,
             double* H_out, double* V_out, double* W_out, double* Q_out, int32_t* flags_out, double* fit_trace,
             double* resid_trace, double* ms_trace, p2g_fit_summary* summary);
+
+/* initialize(..., Init::eye) (solver.hpp:133-164) on the loaded tensor: V_out
+ * (J x R, column-major) = entry-wise |leading R eigenvectors| of the column
+ * Gram matrix sum_k X_k^T X_k over non-zero column pairs.  Same validation
+ * as initialize() (rank, J >= R, I_k >= R). */
+int p2g_initialize_eye(p2g_ctx* ctx, int32_t R, double* V_out);
+
+/* IterationStats of the last p2g_fit (solver.hpp:70-77): per iteration
+ * {ms_procrustes, ms_project, ms_cp} from CUDA events on the context's
+ * stream.  ms_procrustes includes the fused mode-1 partial; ms_project is 0
+ * (the loop is Q-based and never forms Y_k). */
+int p2g_fit_phase_ms(const p2g_ctx* ctx, int32_t max_iters, double* out /* 3 * max_iters */, int32_t* n_out);
+
+/* fit_parafac2 with per-iteration dumps of the loop kernels' own outputs
+ * (parity tests): for iteration t (0-based) the mode-1/2/3 MTTKRPs
+ * m1 (R x R), m2 (J x R), m3 (shard K x R) of cp.hpp:108,116,127 and the
+ * updated H, V, W, all column-major at offset t * size.  Any may be NULL.
+ * Stops like p2g_fit; *n_iters = iterations run. */
+int p2g_fit_dumps(p2g_ctx* ctx, const p2g_fit_config* cfg, const double* H0, const double* V0, const double* W0,
+                  double* m1, double* m2, double* m3, double* H, double* V, double* W, double* fit_trace,
+                  int32_t* n_iters);
 
 /* Device-resident variant for benchmarking: runs `iters` iterations from the
  * state left by the previous call (or from explicit factors when reset != 0),
@@ -213,6 +261,43 @@ int p2g_cp_als_iteration(p2g_ctx* ctx, int64_t K, int64_t J, int32_t R, const in
  * x G x^T - 2 x b^T; max_iter 0 -> 30 R.  Column-major G (R x R), B, X. */
 int p2g_nnls_rowwise(p2g_ctx* ctx, const double* G, const double* B, int64_t n, int32_t R, int32_t max_iter,
                      double* X);
+
+/* naive_mttkrp (mttkrp.hpp:198-235) on the device: the dense mode-n
+ * unfolding and the full Khatri-Rao product materialised in HBM, then one
+ * DGEMM.  Same arguments and shape checks as p2g_mttkrp_packed.  The
+ * baseline the slice-wise kernels beat. */
+int p2g_naive_mttkrp(p2g_ctx* ctx, int32_t mode, int64_t K, int64_t J, int32_t R, const int64_t* ycol_ptr,
+                     const int32_t* ycols, const double* Y, const double* H, const double* V, const double* W,
+                     double* out);
+/* naive_mttkrp_bytes (mttkrp.hpp:241-253); 0 for a bad mode. */
+uint64_t p2g_naive_mttkrp_bytes(int64_t K, int64_t J, int64_t R, int32_t mode);
+
+/* bench_mttkrp (bench.hpp:90-215) on the device over the loaded tensor:
+ * Y_k = Q_k^T X_k with seeded random orthonormal Q_k (generator.hpp:36-47,
+ * stream substream_seed(seed, k+1)) and seeded uniform H, V, W; `reps`
+ * timed sweeps (CUDA events, medians; one untimed warm-up sweep each) of the
+ * specialized kernels, then of the naive kernel per mode unless its
+ * materialisation exceeds budget_bytes (0 = free device memory - 2 GiB),
+ * which marks the cell out-of-memory as the reference does. */
+typedef struct {
+  int64_t K, J;
+  int32_t R;
+  int64_t nnz;
+  int32_t reps;
+  uint64_t budget_bytes;
+  double specialized_ms[3];    /* median per mode */
+  double naive_ms[3];          /* median per mode, -1 when out of memory */
+  uint64_t naive_bytes[3];     /* materialisation bytes per mode */
+  int32_t naive_oom[3];
+  double specialized_sweep_ms; /* median of the 3-mode sweeps */
+  double naive_sweep_ms;       /* 0 when any naive mode was skipped */
+  int32_t naive_sweep_oom;
+  double speedup;              /* naive / specialized sweep, 0 if unknown */
+  uint64_t specialized_device_bytes; /* device bytes the specialized path holds */
+  double checksum_specialized, checksum_naive; /* sums of the outputs (anti-elision) */
+} p2g_bench_report;
+int p2g_bench_mttkrp(p2g_ctx* ctx, int32_t R, int32_t reps, uint64_t budget_bytes, uint64_t seed,
+                     p2g_bench_report* report);
 
 /* pinv_small (kernels.hpp:68-87) and gram (kernels.hpp:57-63) on device. */
 int p2g_pinv_small(p2g_ctx* ctx, const double* G, int32_t n, double* out);

@@ -33,9 +33,9 @@ struct IterationStats {
   int iter = 0;
   double residual_sq = 0;
   double fit = 0;
-  double ms_procrustes = 0;  // the GPU loop is timed as a whole: ms_cp holds the iteration
-  double ms_project = 0;
-  double ms_cp = 0;
+  double ms_procrustes = 0;  // device-timed (CUDA events): Procrustes + fused mode-1 partial
+  double ms_project = 0;     // 0: the device loop is Q-based and never forms Y_k
+  double ms_cp = 0;          // MTTKRP modes 2-3, H/V/W updates, fit scalars
 };
 
 struct FitTrace {
@@ -64,8 +64,8 @@ inline std::vector<Matrix> unpack_q(const IrregularTensor& X, const std::vector<
 }
 }  // namespace detail
 
-/// solver.hpp:104-166 (random initialisation; eye init is not on the GPU
-/// path: std::invalid_argument).
+/// solver.hpp:104-166 (random initialisation on the host, eye initialisation
+/// on the device: p2g_initialize_eye).
 inline Parafac2Factors initialize(const IrregularTensor& X, const SolverConfig& cfg) {
   const Index R = cfg.rank;
   if (R < 1) throw std::invalid_argument("rank must be at least 1");
@@ -77,7 +77,6 @@ inline Parafac2Factors initialize(const IrregularTensor& X, const SolverConfig& 
     if (X.slice(k).n_rows() < R)
       throw DataError("rank exceeds observations for subject " + std::to_string(k) + ": I_k = " +
                       std::to_string(X.slice(k).n_rows()) + " < rank " + std::to_string(R));
-  if (cfg.init != SolverConfig::Init::random) throw std::invalid_argument("eye initialisation is not supported on the GPU");
   Parafac2Factors f;
   f.rank = R;
   f.H = Matrix(R, R);
@@ -85,6 +84,11 @@ inline Parafac2Factors initialize(const IrregularTensor& X, const SolverConfig& 
   f.V = Matrix(X.n_cols(), R);
   check(p2g_initialize_random(cfg.seed, X.n_slices(), X.n_cols(), static_cast<int32_t>(R), f.H.data(), f.S.data(),
                               f.V.data()));
+  if (cfg.init == SolverConfig::Init::eye) {
+    p2g_ctx* ctx = Device::get().ctx();
+    detail::load(ctx, X);
+    check(p2g_initialize_eye(ctx, static_cast<int32_t>(R), f.V.data()));
+  }
   return f;
 }
 
@@ -165,15 +169,25 @@ inline std::pair<Parafac2Factors, FitTrace> fit_parafac2(const IrregularTensor& 
   std::vector<double> Qp(static_cast<std::size_t>(X.to_csr().subj_row_ptr.back() * R));
   auto run = [&](int iters, bool explicit_init, std::vector<double>& fit, std::vector<double>& res,
                  std::vector<double>& ms, p2g_fit_summary& sum) {
-    p2g_fit_config c{static_cast<int32_t>(R), iters, config.tol, config.nonneg ? 1 : 0, explicit_init ? 2 : 0,
-                     config.seed};
+    // initialize() above already produced the reference's initial state
+    // (random or eye): the loop always starts from it
+    (void)explicit_init;
+    p2g_fit_config c{static_cast<int32_t>(R), iters, config.tol, config.nonneg ? 1 : 0, 2, config.seed};
     fit.assign(static_cast<std::size_t>(iters), 0.0);
     res.assign(static_cast<std::size_t>(iters), 0.0);
     ms.assign(static_cast<std::size_t>(iters), 0.0);
     Matrix H = state.H, V = state.V, S = state.S;
-    check(p2g_fit(ctx, &c, explicit_init ? H.data() : nullptr, explicit_init ? V.data() : nullptr,
-                  explicit_init ? S.data() : nullptr, state.H.data(), state.V.data(), state.S.data(), Qp.data(),
+    check(p2g_fit(ctx, &c, H.data(), V.data(), S.data(), state.H.data(), state.V.data(), state.S.data(), Qp.data(),
                   nullptr, fit.data(), res.data(), ms.data(), &sum));
+    phases.assign(static_cast<std::size_t>(3 * iters), 0.0);
+    int32_t np = 0;
+    check(p2g_fit_phase_ms(ctx, iters, phases.data(), &np));
+  };
+  std::vector<double> phases;
+  auto stats = [&](IterationStats& st, int i) {  // IterationStats timers (solver.hpp:278-297), device-timed
+    st.ms_procrustes = phases[static_cast<std::size_t>(3 * i)];
+    st.ms_project = phases[static_cast<std::size_t>(3 * i + 1)];
+    st.ms_cp = phases[static_cast<std::size_t>(3 * i + 2)];
   };
   std::vector<double> fit, res, ms;
   p2g_fit_summary sum{};
@@ -184,19 +198,19 @@ inline std::pair<Parafac2Factors, FitTrace> fit_parafac2(const IrregularTensor& 
       st.iter = i + 1;
       st.fit = fit[static_cast<std::size_t>(i)];
       st.residual_sq = res[static_cast<std::size_t>(i)];
-      st.ms_cp = ms[static_cast<std::size_t>(i)];
+      stats(st, i);
       trace.iterations.push_back(st);
     }
     trace.converged = sum.converged != 0;
   } else {
     double prev = 0.0;
     for (int it = 1; it <= config.max_iters; ++it) {
-      run(1, it > 1, fit, res, ms, sum);
+      run(1, true, fit, res, ms, sum);
       IterationStats st;
       st.iter = it;
       st.fit = fit[0];
       st.residual_sq = res[0];
-      st.ms_cp = ms[0];
+      stats(st, 0);
       trace.iterations.push_back(st);
       state.Q = detail::unpack_q(X, Qp, R);
       observer(state, st);

@@ -1090,9 +1090,16 @@ struct CpStepDump {
   Vec norm_h, norm_v;
 };
 
+inline double ms_since(std::chrono::steady_clock::time_point t0);
+
 /// cp.hpp:99-145 — H, V, W in fixed order.
+/// (Oracle-only diagnostic `ms_v_update`: wall time of the V solve, the
+/// step whose cost scales with J rather than with the number of subjects;
+/// bench.py uses it to extrapolate a subject-prefix sample to the full
+/// workload.)
 inline CpFactors cp_als_iteration(const ProjectedSlices& Y, CpFactors f, const CpOptions& opts = {},
-                                  Mat* mode3_out = nullptr, CpStepDump* dump = nullptr) {
+                                  Mat* mode3_out = nullptr, CpStepDump* dump = nullptr,
+                                  double* ms_v_update = nullptr) {
   detail::check_cp_shapes(Y, f);
   const Index R = Y.rank();
   {
@@ -1108,7 +1115,9 @@ inline CpFactors cp_als_iteration(const ProjectedSlices& Y, CpFactors f, const C
   {
     const Mat m2 = mttkrp_mode2(Y, f.H, f.W, opts.threads);
     const Mat G = hadamard(gram(f.W), gram(f.H));
+    const auto tv = std::chrono::steady_clock::now();
     f.V = opts.nonneg ? nnls_rowwise(G, m2, opts.threads) : matmul(m2, pinv_small(G));
+    if (ms_v_update) *ms_v_update = ms_since(tv);
     const Vec nv = detail::normalize_columns_into(f.V, f.W);
     if (dump) {
       dump->m2 = m2;
@@ -1161,6 +1170,7 @@ struct IterationStats {
   double residual_sq = 0;
   double fit = 0;
   double ms_procrustes = 0, ms_project = 0, ms_cp = 0;
+  double ms_v_update = 0;  // oracle-only: the J-row V solve inside ms_cp
   // Oracle-only diagnostics: rank-deficient Procrustes targets (D5 rule).
   std::int64_t n_deficient = 0;
   std::int64_t n_degenerate = 0;
@@ -1470,7 +1480,7 @@ inline std::pair<Parafac2Factors, FitTrace> fit_parafac2(const IrregularTensor& 
     st.ms_project = ms_since(t0);
     t0 = std::chrono::steady_clock::now();
     Mat m3;
-    cp = cp_als_iteration(Y, std::move(cp), opts, &m3, dumps ? &dump.cp : nullptr);
+    cp = cp_als_iteration(Y, std::move(cp), opts, &m3, dumps ? &dump.cp : nullptr, &st.ms_v_update);
     state.H = cp.H;
     state.V = cp.V;
     state.S = cp.W;

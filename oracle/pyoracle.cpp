@@ -6,6 +6,7 @@
 #include <pybind11/pybind11.h>
 #include <pybind11/stl.h>
 
+#include "baseline_gen.hpp"
 #include "p2_oracle.hpp"
 
 namespace py = pybind11;
@@ -184,6 +185,51 @@ PYBIND11_MODULE(p2oracle, m) {
       .def("normal", &Rng::normal)
       .def("below", &Rng::below);
   m.def("substream_seed", &substream_seed);
+  // BASELINE workload, oracle side: (J, subj_row_ptr, row_ptr, col_idx, val) of the first
+  // K subjects of config `config_id` at rank R (K <= 0: all), and the D2 initial factors.
+  m.def(
+      "baseline_generate",
+      [](int config_id, int R, std::int64_t K, int threads) {
+        const baseline::Spec s = baseline::config(config_id, R);
+        baseline::Csr c;
+        {
+          py::gil_scoped_release rel;
+          c = baseline::generate(s, K, threads);
+        }
+        return py::make_tuple(c.J, py::array_t<std::int64_t>(c.subj_row_ptr.size(), c.subj_row_ptr.data()),
+                              py::array_t<std::int64_t>(c.row_ptr.size(), c.row_ptr.data()),
+                              py::array_t<std::int32_t>(c.col_idx.size(), c.col_idx.data()),
+                              py::array_t<double>(c.val.size(), c.val.data()));
+      },
+      py::arg("config_id"), py::arg("R"), py::arg("K") = 0, py::arg("threads") = 1);
+  m.def(
+      "baseline_spec",
+      [](int config_id, int R) {
+        const baseline::Spec s = baseline::config(config_id, R);
+        py::dict d;
+        d["K"] = s.K;
+        d["J"] = s.J;
+        d["seed"] = s.seed;
+        return d;
+      },
+      py::arg("config_id"), py::arg("R"));
+  m.def(
+      "baseline_init",
+      [](std::uint64_t seed, std::int64_t K, std::int64_t J, int R, std::int64_t K_use) {
+        std::vector<double> H, V, W;
+        baseline::init_factors(seed, K, K_use, J, R, H, V, W);
+        if (K_use <= 0 || K_use > K) K_use = K;
+        // column-major buffers -> (rows, cols) arrays
+        auto colmajor = [](const std::vector<double>& a, std::int64_t rows, std::int64_t cols) {
+          py::array_t<double> out({rows, cols});
+          auto w = out.mutable_unchecked<2>();
+          for (std::int64_t c = 0; c < cols; ++c)
+            for (std::int64_t r = 0; r < rows; ++r) w(r, c) = a[static_cast<std::size_t>(c * rows + r)];
+          return out;
+        };
+        return py::make_tuple(colmajor(H, R, R), colmajor(V, J, R), colmajor(W, K_use, R));
+      },
+      py::arg("seed"), py::arg("K"), py::arg("J"), py::arg("R"), py::arg("K_use") = 0);
 
   m.def("partition_even", &partition_even);
   m.def("partition_weighted", &partition_weighted);
@@ -401,7 +447,7 @@ PYBIND11_MODULE(p2oracle, m) {
         r["H"] = from_mat(f.H);
         r["S"] = from_mat(f.S);
         r["V"] = from_mat(f.V);
-        std::vector<double> fits, res2, msp, msj, msc;
+        std::vector<double> fits, res2, msp, msj, msc, msv;
         std::vector<std::int64_t> ndef, ndeg;
         std::vector<double> minrat;
         for (const auto& s : tr.iterations) {
@@ -410,6 +456,7 @@ PYBIND11_MODULE(p2oracle, m) {
           msp.push_back(s.ms_procrustes);
           msj.push_back(s.ms_project);
           msc.push_back(s.ms_cp);
+          msv.push_back(s.ms_v_update);
           ndef.push_back(s.n_deficient);
           ndeg.push_back(s.n_degenerate);
           minrat.push_back(s.min_lambda_ratio);
@@ -419,6 +466,7 @@ PYBIND11_MODULE(p2oracle, m) {
         r["ms_procrustes"] = msp;
         r["ms_project"] = msj;
         r["ms_cp"] = msc;
+        r["ms_v_update"] = msv;
         r["n_deficient"] = ndef;
         r["n_degenerate"] = ndeg;
         r["min_lambda_ratio"] = minrat;

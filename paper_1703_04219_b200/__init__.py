@@ -82,6 +82,17 @@ class _FitConfig(ctypes.Structure):
     ]
 
 
+class _BenchReport(ctypes.Structure):
+    _fields_ = [("K", ctypes.c_int64), ("J", ctypes.c_int64), ("R", ctypes.c_int32), ("nnz", ctypes.c_int64),
+                ("reps", ctypes.c_int32), ("budget_bytes", ctypes.c_uint64),
+                ("specialized_ms", ctypes.c_double * 3), ("naive_ms", ctypes.c_double * 3),
+                ("naive_bytes", ctypes.c_uint64 * 3), ("naive_oom", ctypes.c_int32 * 3),
+                ("specialized_sweep_ms", ctypes.c_double), ("naive_sweep_ms", ctypes.c_double),
+                ("naive_sweep_oom", ctypes.c_int32), ("speedup", ctypes.c_double),
+                ("specialized_device_bytes", ctypes.c_uint64), ("checksum_specialized", ctypes.c_double),
+                ("checksum_naive", ctypes.c_double)]
+
+
 class _FitSummary(ctypes.Structure):
     _fields_ = [
         ("iterations", ctypes.c_int32), ("converged", ctypes.c_int32),
@@ -121,6 +132,15 @@ _SIGS = {
     "p2g_nnls_rowwise": (ctypes.c_int, [_P, _P, _P, _I64, _I32, _I32, _P]),
     "p2g_pinv_small": (ctypes.c_int, [_P, _P, _I32, _P]),
     "p2g_gram": (ctypes.c_int, [_P, _P, _I64, _I32, _P]),
+    "p2g_load_shard": (ctypes.c_int, [_P, _I64, _I64, _I64, _I64, _P, _P, _P, _P]),
+    "p2g_set_host_collective": (ctypes.c_int, [_P, _P, _P]),
+    "p2g_inject_fault": (ctypes.c_int, [_P, _I32, _I32]),
+    "p2g_fit_phase_ms": (ctypes.c_int, [_P, _I32, _P, _P]),
+    "p2g_initialize_eye": (ctypes.c_int, [_P, _I32, _P]),
+    "p2g_naive_mttkrp": (ctypes.c_int, [_P, _I32, _I64, _I64, _I32, _P, _P, _P, _P, _P, _P, _P]),
+    "p2g_naive_mttkrp_bytes": (ctypes.c_uint64, [_I64, _I64, _I64, _I32]),
+    "p2g_bench_mttkrp": (ctypes.c_int, [_P, _I32, _I32, _U64, _U64, _P]),
+    "p2g_fit_dumps": (ctypes.c_int, [_P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
     # ingest / export (host side)
     "p2g_coo_parse": (ctypes.c_int, [ctypes.c_char_p, _I64, _I32, _P]),
     "p2g_coo_read": (ctypes.c_int, [ctypes.c_char_p, _I32, _P]),
@@ -353,7 +373,7 @@ class SolverConfig:
     max_iters: int = 200
     tol: float = 1e-8
     nonneg: bool = True
-    init: str = "random"   # "random" (solver.hpp:128-132) or "explicit" (D2)
+    init: str = "random"   # "random" (solver.hpp:128-132), "eye" (solver.hpp:133-164) or explicit factors (D2)
     seed: int = 0
     threads: int = 1
 
@@ -387,6 +407,11 @@ def partition_weighted(weights: Sequence[int], n_chunks: int):
     n = ctypes.c_int32()
     _check(lib.p2g_partition_weighted(_ptr(w), len(w), n_chunks, _ptr(out), ctypes.byref(n)))
     return [(int(out[2 * i]), int(out[2 * i + 1])) for i in range(n.value)]
+
+
+def naive_mttkrp_bytes(K: int, J: int, R: int, mode: int) -> int:
+    """naive_mttkrp_bytes (mttkrp.hpp:241-253)."""
+    return int(load_library().p2g_naive_mttkrp_bytes(K, J, R, mode))
 
 
 def baseline_spec(config_id: int, R: int) -> GenSpec:
@@ -448,6 +473,11 @@ def nccl_unique_id() -> bytes:
 # ---------------------------------------------------------------------------
 # Device context
 # ---------------------------------------------------------------------------
+# int fn(double* buf, int64_t count, int32_t op, void* user): host-staged allreduce
+HOST_ALLREDUCE = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.POINTER(ctypes.c_double), ctypes.c_int64, ctypes.c_int32,
+                                  ctypes.c_void_p)
+
+
 class Context:
     """One GPU (rank).  Mirrors the reference's free functions as methods."""
 
@@ -458,6 +488,8 @@ class Context:
         _check(self._lib.p2g_create(device, rank, world, idbuf, ctypes.byref(self._h)))
         self.rank, self.world = rank, world
         self.tensor: Optional[CSRTensor] = None
+        self._w_rows = 0  # rows of W0 / W arguments: K (full load) or the shard's subjects (load_shard)
+        self._coll = None
 
     def close(self):
         if self._h:
@@ -481,6 +513,93 @@ class Context:
         _check(self._lib.p2g_load_csr(self._h, X.K, X.J, _ptr(X.subj_row_ptr), _ptr(X.row_ptr),
                                       _ptr(X.col_idx), _ptr(X.val)))
         self.tensor = X
+        self._w_rows = X.K
+
+    def load_shard(self, K: int, k_begin: int, k_end: int, shard: CSRTensor) -> None:
+        """This rank's subjects [k_begin, k_end) only (`shard` rebased to the
+        shard, e.g. X.subset(k_begin, k_end)); collective over the ranks."""
+        _check(self._lib.p2g_load_shard(self._h, int(K), shard.J, int(k_begin), int(k_end),
+                                        _ptr(shard.subj_row_ptr), _ptr(shard.row_ptr), _ptr(shard.col_idx),
+                                        _ptr(shard.val)))
+        self.tensor = shard
+        self._w_rows = shard.K
+
+    def set_host_collective(self, fn) -> None:
+        """fn(buf: np.ndarray (float64, modified in place), op: 0 sum | 1 max)
+        reduces over all ranks; replaces NCCL for this context."""
+        def _cb(ptr, count, op, user):
+            try:
+                fn(np.ctypeslib.as_array(ptr, shape=(count,)), int(op))
+                return 0
+            except Exception:  # noqa: BLE001 - reported as a status to the library
+                return 1
+        self._coll = HOST_ALLREDUCE(_cb)
+        _check(self._lib.p2g_set_host_collective(self._h, ctypes.cast(self._coll, ctypes.c_void_p), None))
+
+    def inject_fault(self, kind: int, iteration: int) -> None:
+        _check(self._lib.p2g_inject_fault(self._h, kind, iteration))
+
+    def naive_mttkrp(self, mode: int, rank: int, J: int, blocks, cols, H, V, W):
+        """naive_mttkrp (mttkrp.hpp:208-235) on the device."""
+        K = len(blocks)
+        ptr, cl, Y = _pack_projected(rank, blocks, cols)
+        rows = {1: rank, 2: J, 3: K}.get(mode, 1)
+        out = np.empty((rows, rank), order="F")
+        _check(self._lib.p2g_naive_mttkrp(self._h, mode, K, J, rank, _ptr(ptr), _ptr(cl), _ptr(Y),
+                                          _ptr(_f64(H, (rank, rank))), _ptr(_f64(V, (J, rank))),
+                                          _ptr(_f64(W, (K, rank))), _ptr(out)))
+        return out
+
+    def bench_mttkrp(self, R: int, reps: int = 3, budget_bytes: int = 0, seed: int = 0) -> dict:
+        """bench_mttkrp (bench.hpp:90-215) on the device over the loaded tensor."""
+        r = _BenchReport()
+        _check(self._lib.p2g_bench_mttkrp(self._h, R, reps, budget_bytes, seed, ctypes.byref(r)))
+        cells = []
+        for m in range(3):
+            cells.append({"kernel": "specialized", "mode": m + 1, "median_ms": r.specialized_ms[m], "oom": False})
+        cells.append({"kernel": "specialized", "mode": 0, "median_ms": r.specialized_sweep_ms, "oom": False})
+        for m in range(3):
+            cells.append({"kernel": "naive", "mode": m + 1, "median_ms": r.naive_ms[m], "oom": bool(r.naive_oom[m]),
+                          "bytes_needed": int(r.naive_bytes[m])})
+        cells.append({"kernel": "naive", "mode": 0, "median_ms": r.naive_sweep_ms, "oom": bool(r.naive_sweep_oom)})
+        return {"subjects": r.K, "cols": r.J, "rank": r.R, "nnz": r.nnz, "reps": r.reps,
+                "budget_bytes": int(r.budget_bytes), "cells": cells, "specialized_sweep_ms": r.specialized_sweep_ms,
+                "naive_sweep_ms": r.naive_sweep_ms, "naive_oom": bool(r.naive_sweep_oom), "speedup": r.speedup,
+                "specialized_device_bytes": int(r.specialized_device_bytes),
+                "checksum_specialized": r.checksum_specialized, "checksum_naive": r.checksum_naive}
+
+    def initialize_eye(self, R: int) -> np.ndarray:
+        """initialize(..., Init::eye) V (solver.hpp:133-164), J x R."""
+        V = np.empty((self.tensor.J, R), order="F")
+        _check(self._lib.p2g_initialize_eye(self._h, R, _ptr(V)))
+        return V
+
+    def fit_phase_ms(self, max_iters: int = 100000) -> np.ndarray:
+        """(iterations x 3) ms_procrustes, ms_project, ms_cp of the last fit."""
+        out = np.zeros(3 * max(max_iters, 1))
+        n = ctypes.c_int32()
+        _check(self._lib.p2g_fit_phase_ms(self._h, max_iters, _ptr(out), ctypes.byref(n)))
+        return out[:3 * n.value].reshape(n.value, 3)
+
+    def fit_dumps(self, cfg: "SolverConfig", H0, V0, W0):
+        """Per-iteration outputs of the loop kernels: list of dicts with m1, m2,
+        m3, H, V, W (column-major arrays) and fit."""
+        X = self.tensor
+        R = int(cfg.rank)
+        H0, V0, W0 = _f64(H0, (R, R)), _f64(V0, (X.J, R)), _f64(W0, (self._w_rows, R))
+        kb, ke, _, _ = self.shard_info()
+        n = max(int(cfg.max_iters), 1)
+        Ks = ke - kb
+        m1, H = np.zeros((n, R, R)), np.zeros((n, R, R))
+        m2, V = np.zeros((n, R, X.J)), np.zeros((n, R, X.J))
+        m3, W = np.zeros((n, R, Ks)), np.zeros((n, R, Ks))
+        fits = np.zeros(n)
+        it = ctypes.c_int32()
+        c = self._cfg(cfg, True)
+        _check(self._lib.p2g_fit_dumps(self._h, ctypes.byref(c), _ptr(H0), _ptr(V0), _ptr(W0), _ptr(m1), _ptr(m2),
+                                       _ptr(m3), _ptr(H), _ptr(V), _ptr(W), _ptr(fits), ctypes.byref(it)))
+        return [{"m1": m1[t].T, "m2": m2[t].T, "m3": m3[t].T, "H": H[t].T, "V": V[t].T, "W": W[t].T,
+                 "fit": float(fits[t])} for t in range(it.value)]
 
     def shard_info(self):
         kb, ke, nr, nz = (ctypes.c_int64() for _ in range(4))
@@ -490,13 +609,22 @@ class Context:
 
     # -- fused loop -----------------------------------------------------------
     def _cfg(self, cfg: SolverConfig, explicit: bool) -> _FitConfig:
+        if explicit:
+            init = 2
+        elif cfg.init == "eye":
+            init = 1
+        elif cfg.init == "random":
+            init = 0
+        else:
+            raise InvalidArgument(f"unknown init {cfg.init!r}")
         return _FitConfig(int(cfg.rank), int(cfg.max_iters), float(cfg.tol), 1 if cfg.nonneg else 0,
-                          2 if explicit else 0, int(cfg.seed) & ((1 << 64) - 1))
+                          init, int(cfg.seed) & ((1 << 64) - 1))
 
-    def fit(self, cfg: SolverConfig, H0=None, V0=None, W0=None, want_q: bool = True, out=None) -> FitResult:
+    def fit(self, cfg: SolverConfig, H0=None, V0=None, W0=None, want_q: bool = True, out=None,
+            q_out=None) -> FitResult:
         """fit_parafac2 (solver.hpp:251-321) on this rank's shard.  `out` may
         supply the (H, V, W) result arrays (column-major float64, e.g. views of
-        pinned host memory)."""
+        pinned host memory) and `q_out` the packed row-major (rows x R) Q."""
         X = self.tensor
         if X is None:
             raise InvalidArgument("no tensor loaded")
@@ -505,7 +633,7 @@ class Context:
         if explicit:
             H0 = _f64(H0, (R, R))
             V0 = _f64(V0, (X.J, R))
-            W0 = _f64(W0, (X.K, R))
+            W0 = _f64(W0, (self._w_rows, R))
         kb, ke, nr, _ = self.shard_info()
         Rv = max(R, 1)
         if out is not None:
@@ -517,7 +645,12 @@ class Context:
             H = np.empty((Rv, Rv), order="F")
             V = np.empty((X.J, Rv), order="F")
             W = np.empty((ke - kb, Rv), order="F")
-        Q = np.empty((nr, Rv)) if want_q else None
+        if q_out is not None:
+            if q_out.shape != (nr, Rv) or q_out.dtype != np.float64 or not q_out.flags.c_contiguous:
+                raise InvalidArgument(f"q_out must be row-major float64 of shape {(nr, Rv)}")
+            Q = q_out
+        else:
+            Q = np.empty((nr, Rv)) if want_q else None
         flags = np.empty(ke - kb, np.int32)
         n = max(int(cfg.max_iters), 1)
         fits, res, ms = np.zeros(n), np.zeros(n), np.zeros(n)
@@ -535,7 +668,7 @@ class Context:
         R = int(cfg.rank)
         explicit = H0 is not None
         if explicit:
-            H0, V0, W0 = _f64(H0, (R, R)), _f64(V0, (X.J, R)), _f64(W0, (X.K, R))
+            H0, V0, W0 = _f64(H0, (R, R)), _f64(V0, (X.J, R)), _f64(W0, (self._w_rows, R))
         ms = np.zeros(max(iters, 1))
         fits = np.zeros(max(iters, 1))
         c = self._cfg(cfg, explicit)
@@ -568,7 +701,7 @@ class Context:
         flags = np.empty(ke - kb, np.int32)
         m1 = np.empty((R, R), order="F")
         _check(self._lib.p2g_procrustes(self._h, R, _ptr(_f64(H, (R, R))), _ptr(_f64(V, (X.J, R))),
-                                        _ptr(_f64(W, (X.K, R))), _ptr(Q), _ptr(flags), _ptr(m1)))
+                                        _ptr(_f64(W, (self._w_rows, R))), _ptr(Q), _ptr(flags), _ptr(m1)))
         return Q, flags, m1
 
     def mttkrp_q(self, mode: int, Q, H, V, W):
@@ -579,7 +712,7 @@ class Context:
         out = np.empty((rows, R), order="F")
         Qc = np.ascontiguousarray(np.asarray(Q, dtype=np.float64).reshape(nr, R))
         _check(self._lib.p2g_mttkrp_q(self._h, mode, R, _ptr(Qc), _ptr(_f64(H, (R, R))),
-                                      _ptr(_f64(V, (X.J, R))), _ptr(_f64(W, (X.K, R))), _ptr(out)))
+                                      _ptr(_f64(V, (X.J, R))), _ptr(_f64(W, (self._w_rows, R))), _ptr(out)))
         return out
 
     def project(self, Q, R: int):

@@ -65,11 +65,44 @@ static void nccl_check(ncclResult_t r, const char* what) {
                     (nccl_api().GetErrorString ? nccl_api().GetErrorString(r) : "?"));
 }
 
-/// Sum-allreduce of fp64 partials in place (no-op on one rank).  The only
-/// collectives of an iteration: M1 (R x R), M2 (J x R), [gram(W), cross].
-static void allreduce(p2g_ctx* c, double* buf, std::size_t count) {
+/// Allreduce of fp64 values in device memory, in place (no-op on one rank);
+/// op 0 = sum, 1 = max.  NCCL on the context's stream, or the host-staged
+/// collective when one is set (p2g_set_host_collective).  The collectives of
+/// an iteration: M1 (R x R), M2 (J x R), [gram(W), cross, error flags].
+static void allreduce_op(p2g_ctx* c, double* buf, std::size_t count, int op) {
   if (c->world <= 1 || count == 0) return;
-  nccl_check(nccl_api().AllReduce(buf, buf, count, ncclFloat64, ncclSum, c->nccl->comm, c->stream), "allreduce");
+  if (c->host_coll) {
+    if (c->coll_pinned_n < count) {
+      if (c->coll_pinned) P2G_CUDA(cudaFreeHost(c->coll_pinned));
+      c->coll_pinned = nullptr;
+      c->coll_pinned_n = 0;
+      P2G_CUDA(cudaMallocHost(&c->coll_pinned, count * sizeof(double)));
+      c->coll_pinned_n = count;
+    }
+    P2G_CUDA(cudaMemcpyAsync(c->coll_pinned, buf, count * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    P2G_CUDA(cudaStreamSynchronize(c->stream));
+    if (c->host_coll(c->coll_pinned, static_cast<int64_t>(count), op, c->host_coll_user) != 0)
+      throw CudaError("host collective failed");
+    P2G_CUDA(cudaMemcpyAsync(buf, c->coll_pinned, count * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    return;
+  }
+  if (!c->nccl) throw InvalidArgument("world > 1 without NCCL: set a host collective first");
+  nccl_check(nccl_api().AllReduce(buf, buf, count, ncclFloat64, op == 1 ? ncclMax : ncclSum, c->nccl->comm,
+                                  c->stream),
+             "allreduce");
+}
+
+static void allreduce(p2g_ctx* c, double* buf, std::size_t count) { allreduce_op(c, buf, count, 0); }
+
+/// Allreduce of host values through the device path (one-time setup values:
+/// ||X||^2, validation verdicts).
+static void allreduce_host(p2g_ctx* c, double* host, std::size_t count, int op) {
+  if (c->world <= 1 || count == 0) return;
+  c->scal.resize(std::max<std::size_t>(8, count));
+  P2G_CUDA(cudaMemcpyAsync(c->scal.get(), host, count * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+  allreduce_op(c, c->scal.get(), count, op);
+  P2G_CUDA(cudaMemcpyAsync(host, c->scal.get(), count * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  P2G_CUDA(cudaStreamSynchronize(c->stream));
 }
 
 DBuf<double>& scratch_partials(p2g_ctx* c, std::size_t count) {
@@ -137,9 +170,11 @@ void upload_colmajor(p2g_ctx* c, const double* host, std::int64_t rows, std::int
 /// Host column-major (K_total x R) -> device row-major shard rows.
 void upload_shard_rows(p2g_ctx* c, const double* host, std::int64_t total_rows, int R, double* dev) {
   const std::int64_t n = Ks(c);
+  // after p2g_load_shard the caller passes this rank's rows only
+  const std::int64_t rows = c->shard_local ? n : total_rows, off = c->shard_local ? 0 : c->k_begin;
   c->stage.resize(static_cast<std::size_t>(n * R));
   for (int r = 0; r < R; ++r)
-    P2G_CUDA(cudaMemcpyAsync(c->stage.get() + static_cast<std::int64_t>(r) * n, host + r * total_rows + c->k_begin,
+    P2G_CUDA(cudaMemcpyAsync(c->stage.get() + static_cast<std::int64_t>(r) * n, host + r * rows + off,
                              sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
   launch_transpose(c->stage.get(), dev, n, R, c->stream);
 }
@@ -159,21 +194,40 @@ void check_finite_host(const double* a, std::int64_t n, const char* what) {
     if (!std::isfinite(a[i])) throw NumericalError(std::string(what) + ": non-finite entries");
 }
 
-/// Config validation of initialize() (solver.hpp:106-122).
-void validate_fit(const p2g_ctx* c, const p2g_fit_config* cfg) {
+/// First shard subject with I_k < R as (global index, I_k), or (-1, 0).
+std::pair<std::int64_t, std::int64_t> first_short_subject(const p2g_ctx* c, int R) {
+  for (std::int64_t k = 0; k + 1 < static_cast<std::int64_t>(c->srp_host.size()); ++k) {
+    const std::int64_t I = c->srp_host[static_cast<std::size_t>(k + 1)] - c->srp_host[static_cast<std::size_t>(k)];
+    if (I < R) return {c->k_begin + k, I};
+  }
+  return {-1, 0};
+}
+
+/// Config validation of initialize() (solver.hpp:106-122).  The I_k >= R
+/// check runs on each rank's shard; with several ranks the first failing
+/// subject over all ranks is agreed collectively, so every rank throws the
+/// same error (none is left waiting in a later collective).
+void validate_fit(p2g_ctx* c, const p2g_fit_config* cfg) {
   const int R = cfg->rank;
   if (R < 1) throw InvalidArgument("rank must be at least 1");
   if (!(cfg->tol > 0.0)) throw InvalidArgument("convergence tolerance must be positive");
   if (cfg->max_iters < 1) throw InvalidArgument("iteration limit must be at least 1");
   if (R > 40) throw InvalidArgument("rank above 40 unsupported on device");
   if (c->J < R) throw DataError("rank exceeds variables: J = " + std::to_string(c->J) + " < rank " + std::to_string(R));
-  for (std::int64_t k = 0; k < c->K_total; ++k) {
-    const std::int64_t I = c->srp_host[static_cast<std::size_t>(k + 1)] - c->srp_host[static_cast<std::size_t>(k)];
-    if (I < R)
-      throw DataError("rank exceeds observations for subject " + std::to_string(k) + ": I_k = " + std::to_string(I) +
-                      " < rank " + std::to_string(R));
+  if (cfg->init < 0 || cfg->init > 2) throw InvalidArgument("init must be 0 (random), 1 (eye) or 2 (explicit factors)");
+  auto [k, I] = first_short_subject(c, R);
+  if (c->world > 1) {  // max of (K - k): the smallest failing global index wins
+    double v[2] = {k >= 0 ? static_cast<double>(c->K_total - k) : 0.0, 0.0};
+    allreduce_host(c, v, 1, 1);
+    const std::int64_t kk = v[0] > 0.0 ? c->K_total - static_cast<std::int64_t>(v[0]) : -1;
+    double iv[1] = {kk >= 0 && kk == k ? static_cast<double>(I) : 0.0};
+    allreduce_host(c, iv, 1, 0);  // only the owning rank contributes I_k
+    k = kk;
+    I = static_cast<std::int64_t>(iv[0]);
   }
-  if (cfg->init != 0 && cfg->init != 2) throw InvalidArgument("init must be 0 (random) or 2 (explicit factors)");
+  if (k >= 0)
+    throw DataError("rank exceeds observations for subject " + std::to_string(k) + ": I_k = " + std::to_string(I) +
+                    " < rank " + std::to_string(R));
 }
 
 void alloc_state(p2g_ctx* c, int R) {
@@ -187,7 +241,7 @@ void alloc_state(p2g_ctx* c, int R) {
   c->gramV.resize(RR);
   c->gramH.resize(RR);
   c->gvraw.resize(RR);
-  c->gwc.resize(RR + 1);
+  c->gwc.resize(RR + 3);
   c->nH.resize(R);
   c->nV.resize(R);
   c->m1.resize(RR);
@@ -231,6 +285,13 @@ void swap_buf(DBuf<T>& a, DBuf<T>& b) {
 }
 
 constexpr int kMaxPartials = 148 * 8;
+
+/// m1 partials of one Procrustes step: up to kMaxPartials from the polar /
+/// large-R kernel plus one per block of the accurate path, whose grid is
+/// 4 x (or 2 x) the device's SM count.
+std::size_t procrustes_partials(const p2g_ctx* c) {
+  return static_cast<std::size_t>(kMaxPartials) + 4 * static_cast<std::size_t>(std::max(c->num_sms, 148));
+}
 
 bool small_rank(const p2g_ctx* c) { return c->R <= kSmallRankMax; }
 
@@ -285,14 +346,44 @@ void export_q(p2g_ctx* c, const double* H, const double* V, const double* W) {
   launch_qrows(c, c->R, H, V, W, c->Sbuf.get(), c->Ebuf.get(), c->Chat.get(), c->flags.get(), c->Q.get(), c->stream);
 }
 
-/// gram(W) and the cross term over this shard, allreduced -> c->gwc.
-void gram_w_cross(p2g_ctx* c, const double* W, const double* m3_or_null) {
+/// Rank-local error counters <-> the two doubles after [gram(W), cross], so
+/// that the iteration's last allreduce also agrees on the errors: a rank
+/// whose W-NNLS failed (or whose Procrustes operand was non-finite) makes
+/// every rank throw, instead of throwing alone and leaving the others in the
+/// next collective.  `inject` adds a fault (p2g_inject_fault).
+__global__ void k_err_pack(std::int32_t* counters, double* tail, int inject) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    if (inject) counters[1] += 1;
+    tail[0] = static_cast<double>(counters[1]);
+    tail[1] = static_cast<double>(counters[2]);
+  }
+}
+__global__ void k_err_unpack(std::int32_t* counters, const double* tail) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    counters[1] = static_cast<std::int32_t>(tail[0]);
+    counters[2] = static_cast<std::int32_t>(tail[1]);
+  }
+}
+
+/// gram(W) and the cross term over this shard, allreduced -> c->gwc; with
+/// `errors`, also the error counters (k_err_pack).
+void gram_w_cross(p2g_ctx* c, const double* W, const double* m3_or_null, bool errors = false, int inject = 0) {
   const int R = c->R;
   const std::size_t RR = static_cast<std::size_t>(R) * R;
   DBuf<double>& part = scratch_partials(c, kMaxPartials * (RR + 1));
   const int np = gram_partials(R, Ks(c), W, m3_or_null, part.get(), kMaxPartials, c->stream);
   reduce_partials(part.get(), np, static_cast<std::int64_t>(RR + 1), c->gwc.get(), c->stream);
-  allreduce(c, c->gwc.get(), RR + 1);
+  if (!errors) {
+    allreduce(c, c->gwc.get(), RR + 1);
+    return;
+  }
+  k_err_pack<<<1, 32, 0, c->stream>>>(c->counters.get(), c->gwc.get() + RR + 1, inject);
+  P2G_LAUNCHED(1);
+  allreduce(c, c->gwc.get(), RR + 3);
+  if (c->world > 1) {
+    k_err_unpack<<<1, 32, 0, c->stream>>>(c->counters.get(), c->gwc.get() + RR + 1);
+    P2G_LAUNCHED(1);
+  }
 }
 
 /// gram(V) (replicated, no collective) -> out.
@@ -314,6 +405,18 @@ void init_state(p2g_ctx* c, const p2g_fit_config* cfg, const double* H0, const d
     upload_colmajor(c, H0, R, R, c->H.get());
     upload_colmajor(c, V0, c->J, R, c->V.get());
     upload_shard_rows(c, W0, c->K_total, R, c->W.get());
+  } else if (cfg->init == 1) {
+    // solver.hpp:133-164: H = I, S = ones, V = |leading eigenvectors of sum_k X_k^T X_k|
+    std::vector<double> h(static_cast<std::size_t>(R) * R, 0.0);
+    for (int r = 0; r < R; ++r) h[static_cast<std::size_t>(r) * R + r] = 1.0;
+    upload_colmajor(c, h.data(), R, R, c->H.get());
+    DBuf<double> C;
+    C.resize(static_cast<std::size_t>(c->J) * static_cast<std::size_t>(c->J));
+    build_column_gram(c, C.get());
+    allreduce(c, C.get(), static_cast<std::size_t>(c->J) * static_cast<std::size_t>(c->J));
+    eye_vectors(c, C.get(), R, c->V.get());
+    launch_fill(c->W.get(), Ks(c) * R, 1.0, c->stream);
+    P2G_CUDA(cudaStreamSynchronize(c->stream));
   } else {
     // solver.hpp:124-132: H = I, S = ones, V = Rng(seed).uniform() r-outer j-inner.
     std::vector<double> h(static_cast<std::size_t>(R) * R), v(static_cast<std::size_t>(c->J) * R);
@@ -332,6 +435,7 @@ void init_state(p2g_ctx* c, const p2g_fit_config* cfg, const double* H0, const d
   c->masks_valid = false;
   c->polar_sweeps_valid = false;
   c->state_valid = true;
+  c->fit_phase_ms.clear();
 }
 
 struct IterOut {
@@ -347,14 +451,18 @@ IterOut iterate(p2g_ctx* c, bool nonneg, int iter) {
   const std::size_t RR = static_cast<std::size_t>(R) * R;
   cudaStream_t s = c->stream;
   const bool qf = small_rank(c);
+  for (cudaEvent_t& e : c->ev_it)
+    if (!e) P2G_CUDA(cudaEventCreate(&e));
+  P2G_CUDA(cudaEventRecord(c->ev_it[0], s));
   P2G_CUDA(cudaMemsetAsync(c->counters.get(), 0, sizeof(std::int32_t) * 32, s));
   {
-    DBuf<double>& part = scratch_partials(c, static_cast<std::size_t>(kMaxPartials + 4 * 148) * RR);
+    DBuf<double>& part = scratch_partials(c, procrustes_partials(c) * RR);
     const int np = procrustes_step(c, part.get());
     Phase ph(c, "m1_reduce");
     reduce_partials(part.get(), np, static_cast<std::int64_t>(RR), c->m1.get(), s);
     allreduce(c, c->m1.get(), RR);
   }
+  P2G_CUDA(cudaEventRecord(c->ev_it[1], s));
   {
     Phase ph(c, "solve_h");  // H_t -> Hp
     launch_solve_h(R, c->m1.get(), c->gramW.get(), c->gramV.get(), c->Hp.get(), c->nH.get(), c->gramH.get(),
@@ -408,7 +516,7 @@ IterOut iterate(p2g_ctx* c, bool nonneg, int iter) {
   }
   {
     Phase ph(c, "fit");
-    gram_w_cross(c, c->Wp.get(), c->m3.get());
+    gram_w_cross(c, c->Wp.get(), c->m3.get(), true, c->fault_kind == 1 && c->fault_iter == iter);
     launch_fit(R, c->gwc.get(), c->gramH.get(), c->gramV.get(), c->norm_x, c->gramW.get(), c->scal.get(), s);
   }
   swap_buf(c->H, c->Hp);
@@ -416,11 +524,21 @@ IterOut iterate(p2g_ctx* c, bool nonneg, int iter) {
   swap_buf(c->W, c->Wp);
   c->c_valid = true;  // mode 3 produced the Gram (R <= 16) or X V rows (R > 16) for the new V
   c->xv_valid = qf;   // and, for R <= 16, the X V rows in Ubuf
+  P2G_CUDA(cudaEventRecord(c->ev_it[2], s));
   // One host sync per iteration: fit scalars + error counters.
   P2G_CUDA(cudaMemcpyAsync(c->pinned, c->scal.get(), sizeof(double) * 4, cudaMemcpyDeviceToHost, s));
   P2G_CUDA(cudaMemcpyAsync(c->pinned + 4, c->counters.get(), sizeof(std::int32_t) * 8, cudaMemcpyDeviceToHost, s));
   P2G_CUDA(cudaStreamSynchronize(s));
   collect_timing(c);
+  {  // IterationStats (solver.hpp:70-77): procrustes (+ fused mode-1 partial), project (none: the loop is
+     // Q-based and never forms Y), cp (MTTKRP modes 2-3, the H/V/W updates and the fit scalars)
+    float a = 0.f, b = 0.f;
+    P2G_CUDA(cudaEventElapsedTime(&a, c->ev_it[0], c->ev_it[1]));
+    P2G_CUDA(cudaEventElapsedTime(&b, c->ev_it[1], c->ev_it[2]));
+    c->fit_phase_ms.push_back(a);
+    c->fit_phase_ms.push_back(0.0);
+    c->fit_phase_ms.push_back(b);
+  }
   const std::int32_t* cnt = reinterpret_cast<const std::int32_t*>(c->pinned + 4);
   if (std::getenv("P2G_DEBUG") && cnt[7] > 0) {
     if (small_rank(c))
@@ -480,12 +598,13 @@ extern "C" int p2g_create(int32_t device, int32_t rank, int32_t world, const cha
     P2G_CUDA(cudaSetDevice(device));
     cudaDeviceProp prop;
     P2G_CUDA(cudaGetDeviceProperties(&prop, device));
-    if (prop.major < 10) throw CudaError("libp2g is built for sm_100a (B200); found sm_" + std::to_string(prop.major) + std::to_string(prop.minor));
+    if (prop.major != 10 || prop.minor != 0)
+      throw CudaError("libp2g is built for sm_100a (B200) only; found sm_" + std::to_string(prop.major) +
+                      std::to_string(prop.minor));
     c->num_sms = prop.multiProcessorCount;
     P2G_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
     P2G_CUDA(cudaMallocHost(&c->pinned, 64 * sizeof(double)));
-    if (world > 1) {
-      if (!nccl_id) throw InvalidArgument("world > 1 needs an NCCL unique id");
+    if (world > 1 && nccl_id) {  // (without an id: a host collective must be set before the load)
       ncclUniqueId id;
       std::memcpy(&id, nccl_id, 128);
       c->nccl = new NcclState();
@@ -510,9 +629,29 @@ extern "C" int p2g_destroy(p2g_ctx* c) {
       cudaEventDestroy(c->ev_csc);
     }
     for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
+    for (cudaEvent_t e : c->ev_it)
+      if (e) cudaEventDestroy(e);
     if (c->pinned) cudaFreeHost(c->pinned);
+    if (c->coll_pinned) cudaFreeHost(c->coll_pinned);
     if (c->stream) cudaStreamDestroy(c->stream);
     delete c;
+  });
+}
+
+extern "C" int p2g_set_host_collective(p2g_ctx* c, p2g_host_allreduce_fn fn, void* user) {
+  return guarded([&] {
+    if (!c) throw InvalidArgument("null context");
+    c->host_coll = fn;
+    c->host_coll_user = user;
+  });
+}
+
+extern "C" int p2g_inject_fault(p2g_ctx* c, int32_t kind, int32_t iteration) {
+  return guarded([&] {
+    if (!c) throw InvalidArgument("null context");
+    if (kind < 0 || kind > 1) throw InvalidArgument("fault kind must be 0 (none) or 1 (W-NNLS failure)");
+    c->fault_kind = kind;
+    c->fault_iter = iteration;
   });
 }
 
@@ -605,6 +744,9 @@ extern "C" int p2g_load_csr(p2g_ctx* c, int64_t K, int64_t J, const int64_t* srp
         std::fprintf(stderr, "[p2g] load %-12s %8.2f ms\n", what,
                      std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tl0).count());
     };
+    if (c->world > 1 && !c->nccl && !c->host_coll)
+      throw InvalidArgument("world > 1 needs an NCCL unique id or a host collective");
+    c->shard_local = false;
     // IrregularTensor::from_slices (sparse.hpp:176-193) validation.
     if (J <= 0) throw DataError("tensor must have at least one column");
     if (K <= 0) throw DataError("tensor must have at least one slice");
@@ -674,7 +816,7 @@ extern "C" int p2g_load_csr(p2g_ctx* c, int64_t K, int64_t J, const int64_t* srp
     c->J = J;
     c->k_begin = parts[static_cast<std::size_t>(c->rank)].first;
     c->k_end = parts[static_cast<std::size_t>(c->rank)].second;
-    c->srp_host.assign(srp, srp + K + 1);
+    c->srp_host.assign(srp + c->k_begin, srp + c->k_end + 1);
     const int64_t row0 = srp[c->k_begin], row1 = srp[c->k_end];
     const int64_t nz0 = rp[row0], nz1 = rp[row1];
     c->NR = row1 - row0;
@@ -750,6 +892,125 @@ extern "C" int p2g_load_csr(p2g_ctx* c, int64_t K, int64_t J, const int64_t* srp
   });
 }
 
+/// Shard-local load: this rank's subjects only (arrays rebased to the shard).
+/// The CSR is checked on the device with the same rules as p2g_load_csr;
+/// the verdict (first failing check in rank order), the subject ranges and
+/// ||X||^2 are agreed collectively, so every rank sees the same error.
+extern "C" int p2g_load_shard(p2g_ctx* c, int64_t K, int64_t J, int64_t k_begin, int64_t k_end, const int64_t* srp,
+                              const int64_t* rp, const int32_t* ci, const double* val) {
+  return guarded([&] {
+    if (!c) throw InvalidArgument("null context");
+    set_device(c);
+    if (c->world > 1 && !c->nccl && !c->host_coll)
+      throw InvalidArgument("world > 1 needs an NCCL unique id or a host collective");
+    if (!srp || !rp) throw InvalidArgument("null CSR arrays");
+    const int64_t Kl = k_end - k_begin;
+    // ranges must tile [0, K) in rank order: gather every rank's (begin, end)
+    std::vector<double> rng(static_cast<std::size_t>(2 * c->world), 0.0);
+    rng[static_cast<std::size_t>(2 * c->rank)] = static_cast<double>(k_begin);
+    rng[static_cast<std::size_t>(2 * c->rank + 1)] = static_cast<double>(k_end);
+    allreduce_host(c, rng.data(), rng.size(), 0);
+    double expect = 0.0;
+    bool tiled = true;
+    for (int r = 0; r < c->world; ++r) {
+      tiled &= rng[static_cast<std::size_t>(2 * r)] == expect && rng[static_cast<std::size_t>(2 * r + 1)] > expect;
+      expect = rng[static_cast<std::size_t>(2 * r + 1)];
+    }
+    if (J <= 0) throw DataError("tensor must have at least one column");
+    if (K <= 0) throw DataError("tensor must have at least one slice");
+    if (!tiled || expect != static_cast<double>(K))
+      throw InvalidArgument("shard ranges must tile [0, K) in rank order with at least one subject per rank");
+    // local structure checks (host, cheap): error code per rank, agreed below
+    // 1 subj_row_ptr, 2 row_ptr start, then the device checks 3 row_ptr order,
+    // 4 column range, 5 column order
+    int code = 0;
+    if (srp[0] != 0) code = 1;
+    for (int64_t k = 0; k < Kl && !code; ++k)
+      if (srp[k + 1] < srp[k]) code = 1;
+    const int64_t NR = code ? 0 : srp[Kl];
+    if (!code && rp[0] != 0) code = 2;
+    sync_csc(c);
+    c->loaded = false;
+    c->K_total = K;
+    c->J = J;
+    c->k_begin = k_begin;
+    c->k_end = k_end;
+    c->NR = NR;
+    c->srp_host.assign(srp, srp + (code ? 1 : Kl + 1));
+    double norm_local = 0.0;
+    if (!code) {
+      const int64_t nnz = rp[NR];
+      if (nnz < 0) code = 3;
+      if (!code && nnz > 0 && (!ci || !val)) throw InvalidArgument("null CSR arrays");
+      if (!code) {
+        c->nnz = nnz;
+        c->max_rows = 0;
+        for (int64_t k = 0; k < Kl; ++k) c->max_rows = std::max<std::int64_t>(c->max_rows, srp[k + 1] - srp[k]);
+        c->srp.resize(static_cast<std::size_t>(Kl + 1));
+        c->rp.resize(static_cast<std::size_t>(NR + 1));
+        c->ci.resize(static_cast<std::size_t>(std::max<int64_t>(nnz, 1)));
+        c->val.resize(static_cast<std::size_t>(std::max<int64_t>(nnz, 1)));
+        P2G_CUDA(cudaMemcpyAsync(c->srp.get(), srp, sizeof(int64_t) * (Kl + 1), cudaMemcpyHostToDevice, c->stream));
+        P2G_CUDA(cudaMemcpyAsync(c->rp.get(), rp, sizeof(int64_t) * (NR + 1), cudaMemcpyHostToDevice, c->stream));
+        if (nnz > 0) {
+          P2G_CUDA(cudaMemcpyAsync(c->ci.get(), ci, sizeof(int32_t) * nnz, cudaMemcpyHostToDevice, c->stream));
+          P2G_CUDA(cudaMemcpyAsync(c->val.get(), val, sizeof(double) * nnz, cudaMemcpyHostToDevice, c->stream));
+        }
+        DBuf<unsigned long long> bad;
+        bad.resize(2);
+        DBuf<double> part;
+        part.resize(kNormBlocks);
+        P2G_CUDA(cudaMemsetAsync(bad.get(), 0xff, sizeof(unsigned long long) * 2, c->stream));
+        const int g = static_cast<int>(std::max<std::int64_t>(1, std::min<std::int64_t>((NR + 255) / 256, 148 * 8)));
+        k_check_rowptr<<<g, 256, 0, c->stream>>>(c->rp.get(), NR, bad.get());
+        k_sumsq<<<kNormBlocks, 256, 0, c->stream>>>(c->val.get(), nnz, part.get());
+        P2G_LAUNCHED(2);
+        unsigned long long hb[2];
+        std::vector<double> hp(kNormBlocks);
+        P2G_CUDA(cudaMemcpyAsync(hb, bad.get(), sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->stream));
+        P2G_CUDA(cudaStreamSynchronize(c->stream));
+        if (hb[0] != ~0ull) {
+          code = 3;
+        } else {
+          k_check_cols<<<g, 256, 0, c->stream>>>(c->rp.get(), c->ci.get(), NR, J, bad.get() + 1);
+          P2G_LAUNCHED(1);
+          P2G_CUDA(cudaMemcpyAsync(hb + 1, bad.get() + 1, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                                   c->stream));
+          P2G_CUDA(cudaMemcpyAsync(hp.data(), part.get(), sizeof(double) * kNormBlocks, cudaMemcpyDeviceToHost,
+                                   c->stream));
+          P2G_CUDA(cudaStreamSynchronize(c->stream));
+          if (hb[1] != ~0ull) code = (hb[1] & 3ull) == 2ull ? 4 : 5;
+          for (double v : hp) norm_local += v;
+        }
+      }
+    }
+    // agree: the lowest rank with an error decides (max of world - rank), then ||X||^2
+    double v[2] = {code ? static_cast<double>(c->world - c->rank) : 0.0, 0.0};
+    allreduce_host(c, v, 1, 1);
+    const int bad_rank = v[0] > 0.0 ? c->world - static_cast<int>(v[0]) : -1;
+    double cv[1] = {bad_rank == c->rank ? static_cast<double>(code) : 0.0};
+    allreduce_host(c, cv, 1, 0);
+    switch (static_cast<int>(cv[0])) {
+      case 1: throw DataError("subj_row_ptr must start at 0 and be non-decreasing");
+      case 2: throw DataError("row_ptr must start at 0");
+      case 3: throw DataError("row_ptr must be non-decreasing");
+      case 4: throw DataError("column index out of range");
+      case 5: throw DataError("column indices must be strictly ascending within a row");
+      default: break;
+    }
+    double nx[1] = {norm_local};
+    allreduce_host(c, nx, 1, 0);
+    c->norm_x = nx[0];
+    double tot[1] = {static_cast<double>(c->nnz)};
+    allreduce_host(c, tot, 1, 0);
+    c->nnz_total = static_cast<std::int64_t>(tot[0]);
+    build_csc(c);
+    c->loaded = true;
+    c->shard_local = true;
+    c->state_valid = false;
+  });
+}
+
 extern "C" int p2g_shard_info(const p2g_ctx* c, int64_t* k_begin, int64_t* k_end, int64_t* n_rows, int64_t* nnz) {
   return guarded([&] {
     require_loaded(c);
@@ -821,6 +1082,68 @@ extern "C" int p2g_fit(p2g_ctx* c, const p2g_fit_config* cfg, const double* H0, 
   });
 }
 
+extern "C" int p2g_initialize_eye(p2g_ctx* c, int32_t R, double* V_out) {
+  return guarded([&] {
+    require_loaded(c);
+    set_device(c);
+    if (!V_out) throw InvalidArgument("null output");
+    p2g_fit_config cfg{R, 1, 1.0, 1, 1, 0};
+    validate_fit(c, &cfg);
+    DBuf<double> C, V;
+    C.resize(static_cast<std::size_t>(c->J) * static_cast<std::size_t>(c->J));
+    V.resize(static_cast<std::size_t>(c->J) * R);
+    build_column_gram(c, C.get());
+    allreduce(c, C.get(), static_cast<std::size_t>(c->J) * static_cast<std::size_t>(c->J));
+    eye_vectors(c, C.get(), R, V.get());
+    download_colmajor(c, V.get(), c->J, R, V_out);
+  });
+}
+
+extern "C" int p2g_fit_phase_ms(const p2g_ctx* c, int32_t max_iters, double* out, int32_t* n_out) {
+  return guarded([&] {
+    if (!c || !out || !n_out) throw InvalidArgument("null argument");
+    const int n = static_cast<int>(std::min<std::size_t>(static_cast<std::size_t>(std::max(max_iters, 0)),
+                                                         c->fit_phase_ms.size() / 3));
+    std::memcpy(out, c->fit_phase_ms.data(), sizeof(double) * 3 * static_cast<std::size_t>(n));
+    *n_out = n;
+  });
+}
+
+extern "C" int p2g_fit_dumps(p2g_ctx* c, const p2g_fit_config* cfg, const double* H0, const double* V0,
+                             const double* W0, double* m1, double* m2, double* m3, double* H, double* V, double* W,
+                             double* fit_trace, int32_t* n_iters) {
+  return guarded([&] {
+    require_loaded(c);
+    if (!cfg) throw InvalidArgument("null config");
+    set_device(c);
+    validate_fit(c, cfg);
+    if (!(c->norm_x > 0.0)) throw DataError("tensor has no non-zero entries");
+    init_state(c, cfg, H0, V0, W0);
+    const int R = cfg->rank;
+    const std::size_t RR = static_cast<std::size_t>(R) * R, JR = static_cast<std::size_t>(c->J) * R,
+                      KR = static_cast<std::size_t>(Ks(c)) * R;
+    double prev_fit = 0.0;
+    int iters = 0;
+    for (int it = 1; it <= cfg->max_iters; ++it) {
+      const IterOut o = iterate(c, cfg->nonneg != 0, it);
+      const std::size_t t = static_cast<std::size_t>(it - 1);
+      // the loop kernels' own outputs of iteration `it` (cp.hpp:108,116,127 and the updated factors)
+      if (m1) download_colmajor(c, c->m1.get(), R, R, m1 + t * RR);
+      if (m2) download_colmajor(c, c->M2.get(), c->J, R, m2 + t * JR);
+      if (m3) download_colmajor(c, c->m3.get(), Ks(c), R, m3 + t * KR);
+      if (H) download_colmajor(c, c->H.get(), R, R, H + t * RR);
+      if (V) download_colmajor(c, c->V.get(), c->J, R, V + t * JR);
+      if (W) download_colmajor(c, c->W.get(), Ks(c), R, W + t * KR);
+      if (fit_trace) fit_trace[t] = o.fit;
+      ++iters;
+      const double change = std::abs(o.fit - prev_fit) / std::max(prev_fit, std::numeric_limits<double>::epsilon());
+      prev_fit = o.fit;
+      if (change < cfg->tol) break;
+    }
+    if (n_iters) *n_iters = iters;
+  });
+}
+
 extern "C" int p2g_bench_iterations(p2g_ctx* c, const p2g_fit_config* cfg, const double* H0, const double* V0,
                                     const double* W0, int32_t reset, int32_t iters, double* ms_per_iter,
                                     double* fit_trace) {
@@ -847,15 +1170,7 @@ extern "C" int p2g_bench_iterations(p2g_ctx* c, const p2g_fit_config* cfg, const
         float ms = 0.f;
         P2G_CUDA(cudaEventElapsedTime(&ms, e0, e1));
         double msd = ms;
-        if (c->world > 1) {  // max over ranks
-          c->scal.resize(8);
-          P2G_CUDA(cudaMemcpyAsync(c->scal.get() + 6, &msd, sizeof(double), cudaMemcpyHostToDevice, c->stream));
-          nccl_check(nccl_api().AllReduce(c->scal.get() + 6, c->scal.get() + 6, 1, ncclFloat64, ncclMax,
-                                          c->nccl->comm, c->stream),
-                     "allreduce max");
-          P2G_CUDA(cudaMemcpyAsync(&msd, c->scal.get() + 6, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-          P2G_CUDA(cudaStreamSynchronize(c->stream));
-        }
+        allreduce_host(c, &msd, 1, 1);  // max over ranks
         if (ms_per_iter) ms_per_iter[it] = msd;
         if (fit_trace) fit_trace[it] = o.fit;
       }
@@ -900,9 +1215,7 @@ extern "C" int p2g_procrustes(p2g_ctx* c, int32_t R, const double* H, const doub
     set_device(c);
     if (R < 1 || R > 40) throw InvalidArgument("rank out of range");
     if (!H || !V || !W) throw InvalidArgument("null factor");
-    for (int64_t k = c->k_begin; k < c->k_end; ++k)
-      if (c->srp_host[static_cast<std::size_t>(k + 1)] - c->srp_host[static_cast<std::size_t>(k)] < R)
-        throw InvalidArgument("rank exceeds observations in procrustes step");
+    if (first_short_subject(c, R).first >= 0) throw InvalidArgument("rank exceeds observations in procrustes step");
     alloc_state(c, R);
     upload_colmajor(c, H, R, R, c->H.get());
     upload_colmajor(c, V, c->J, R, c->V.get());
@@ -912,7 +1225,7 @@ extern "C" int p2g_procrustes(p2g_ctx* c, int32_t R, const double* H, const doub
     c->ew_valid = false;  // cold Jacobi start for a teacher-forced step
     const std::size_t RR = static_cast<std::size_t>(R) * R;
     P2G_CUDA(cudaMemsetAsync(c->counters.get(), 0, sizeof(std::int32_t) * 32, c->stream));
-    DBuf<double>& part = scratch_partials(c, static_cast<std::size_t>(kMaxPartials + 4 * 148) * RR);
+    DBuf<double>& part = scratch_partials(c, procrustes_partials(c) * RR);
     const int np = procrustes_step(c, part.get());
     reduce_partials(part.get(), np, static_cast<std::int64_t>(RR), c->m1.get(), c->stream);
     allreduce(c, c->m1.get(), RR);
@@ -1112,6 +1425,293 @@ extern "C" int p2g_mttkrp_packed(p2g_ctx* c, int32_t mode, int64_t K, int64_t J,
     d.out.resize(static_cast<std::size_t>(std::max<std::int64_t>(rows, 1)) * R);
     packed_mode(c, mode, K, J, R, d, d.H.get(), d.V.get(), d.W.get(), d.out.get());
     download_colmajor(c, d.out.get(), rows, R, out);
+  });
+}
+
+extern "C" int p2g_naive_mttkrp(p2g_ctx* c, int32_t mode, int64_t K, int64_t J, int32_t R, const int64_t* ycol_ptr,
+                                const int32_t* ycols, const double* Y, const double* H, const double* V,
+                                const double* W, double* out) {
+  return guarded([&] {
+    if (!c) throw InvalidArgument("null context");
+    set_device(c);
+    if (mode < 1 || mode > 3) throw InvalidArgument("mttkrp: mode must be 1, 2 or 3");
+    if (!H || !V || !W || !out) throw InvalidArgument("null factor");
+    PackedDev d;
+    upload_packed(c, K, J, R, ycol_ptr, ycols, Y, d);
+    check_finite_host(W, K * R, "khatri_rao left operand");  // kernels.hpp:37-38
+    check_finite_host(mode == 3 ? V : (mode == 1 ? V : H), (mode == 2 ? R : J) * static_cast<int64_t>(R),
+                      "khatri_rao right operand");
+    d.H.resize(static_cast<std::size_t>(R) * R);
+    d.V.resize(static_cast<std::size_t>(std::max<std::int64_t>(J, 1)) * R);
+    d.W.resize(static_cast<std::size_t>(std::max<std::int64_t>(K, 1)) * R);
+    upload_colmajor(c, H, R, R, d.H.get());
+    P2G_CUDA(cudaStreamSynchronize(c->stream));
+    upload_colmajor(c, V, J, R, d.V.get());
+    P2G_CUDA(cudaStreamSynchronize(c->stream));
+    upload_colmajor(c, W, K, R, d.W.get());
+    const std::int64_t rows = mode == 1 ? R : (mode == 2 ? J : K);
+    d.out.resize(static_cast<std::size_t>(std::max<std::int64_t>(rows, 1)) * R);
+    NaiveScratch s;
+    s.prepare(c, mode, K, J, R, d.ptr.get(), ycol_ptr[K]);
+    naive_mttkrp(c, s, mode, K, J, R, d.ptr.get(), d.cols.get(), d.Y.get(), ycol_ptr[K], d.H.get(), d.V.get(),
+                 d.W.get(), d.out.get());
+    P2G_CUDA(cudaMemcpyAsync(out, d.out.get(), sizeof(double) * rows * R, cudaMemcpyDeviceToHost, c->stream));
+    P2G_CUDA(cudaStreamSynchronize(c->stream));
+  });
+}
+
+extern "C" uint64_t p2g_naive_mttkrp_bytes(int64_t K, int64_t J, int64_t R, int32_t mode) {
+  try {
+    return naive_bytes(K, J, R, mode);
+  } catch (...) {
+    return 0;
+  }
+}
+
+namespace {
+/// generator.hpp:36-47: Householder QR of a seeded Gaussian rows x cols
+/// matrix (filled column-major from the stream), Q sign-fixed so diag(R) >= 0.
+/// Output row-major into q (rows x cols).
+void random_orthonormal(Rng& rng, std::int64_t rows, int cols, double* q) {
+  std::vector<double> A(static_cast<std::size_t>(rows * cols));  // column-major
+  for (int c = 0; c < cols; ++c)
+    for (std::int64_t r = 0; r < rows; ++r) A[static_cast<std::size_t>(c * rows + r)] = rng.normal();
+  std::vector<double> tau(static_cast<std::size_t>(cols)), rdiag(static_cast<std::size_t>(cols));
+  for (int c = 0; c < cols; ++c) {
+    double* a = A.data() + static_cast<std::size_t>(c) * rows;
+    double sig = 0.0;
+    for (std::int64_t r = c + 1; r < rows; ++r) sig += a[r] * a[r];
+    const double alpha = a[c];
+    double beta = alpha, t = 0.0;
+    if (sig != 0.0) {
+      beta = -std::copysign(std::sqrt(alpha * alpha + sig), alpha);
+      t = (beta - alpha) / beta;
+      const double inv = 1.0 / (alpha - beta);
+      for (std::int64_t r = c + 1; r < rows; ++r) a[r] *= inv;  // v = (1, a[c+1..])
+      for (int j = c + 1; j < cols; ++j) {
+        double* b = A.data() + static_cast<std::size_t>(j) * rows;
+        double dot = b[c];
+        for (std::int64_t r = c + 1; r < rows; ++r) dot += a[r] * b[r];
+        dot *= t;
+        b[c] -= dot;
+        for (std::int64_t r = c + 1; r < rows; ++r) b[r] -= dot * a[r];
+      }
+    }
+    tau[static_cast<std::size_t>(c)] = t;
+    rdiag[static_cast<std::size_t>(c)] = beta;
+  }
+  // Q = H_0 H_1 ... H_{cols-1} I(rows, cols), applied right to left
+  std::vector<double> Q(static_cast<std::size_t>(rows * cols), 0.0);
+  for (int c = 0; c < cols; ++c) Q[static_cast<std::size_t>(c) * rows + c] = 1.0;
+  for (int c = cols - 1; c >= 0; --c) {
+    const double* a = A.data() + static_cast<std::size_t>(c) * rows;
+    const double t = tau[static_cast<std::size_t>(c)];
+    if (t == 0.0) continue;
+    for (int j = 0; j < cols; ++j) {
+      double* qj = Q.data() + static_cast<std::size_t>(j) * rows;
+      double dot = qj[c];
+      for (std::int64_t r = c + 1; r < rows; ++r) dot += a[r] * qj[r];
+      dot *= t;
+      qj[c] -= dot;
+      for (std::int64_t r = c + 1; r < rows; ++r) qj[r] -= dot * a[r];
+    }
+  }
+  for (int c = 0; c < cols; ++c) {
+    const double sg = rdiag[static_cast<std::size_t>(c)] < 0.0 ? -1.0 : 1.0;
+    for (std::int64_t r = 0; r < rows; ++r)
+      q[r * cols + c] = sg * Q[static_cast<std::size_t>(c) * rows + r];
+  }
+}
+
+double median(std::vector<double> v) {
+  if (v.empty()) return 0.0;
+  std::sort(v.begin(), v.end());
+  const std::size_t n = v.size();
+  return n % 2 == 1 ? v[n / 2] : 0.5 * (v[n / 2 - 1] + v[n / 2]);
+}
+
+double device_sum(p2g_ctx* c, const double* d, std::int64_t n) {
+  std::vector<double> h(static_cast<std::size_t>(n));
+  P2G_CUDA(cudaMemcpyAsync(h.data(), d, sizeof(double) * n, cudaMemcpyDeviceToHost, c->stream));
+  P2G_CUDA(cudaStreamSynchronize(c->stream));
+  double s = 0.0;
+  for (double x : h) s += x;
+  return s;
+}
+}  // namespace
+
+/// bench_mttkrp (bench.hpp:90-215) on the device over the loaded tensor.
+extern "C" int p2g_bench_mttkrp(p2g_ctx* c, int32_t R, int32_t reps, uint64_t budget_bytes, uint64_t seed,
+                                p2g_bench_report* rep) {
+  return guarded([&] {
+    require_loaded(c);
+    set_device(c);
+    if (!rep) throw InvalidArgument("null report");
+    if (R < 1) throw InvalidArgument("bench: rank must be at least 1");
+    if (R > 40) throw InvalidArgument("rank above 40 unsupported on device");
+    if (reps < 1) throw InvalidArgument("bench: reps must be at least 1");
+    const std::int64_t K = Ks(c), J = c->J;
+    *rep = p2g_bench_report{};
+    rep->K = K;
+    rep->J = J;
+    rep->R = R;
+    rep->nnz = c->nnz;
+    rep->reps = reps;
+    if (budget_bytes == 0) {  // all free device memory minus a margin
+      std::size_t fr = 0, tot = 0;
+      P2G_CUDA(cudaMemGetInfo(&fr, &tot));
+      budget_bytes = fr > (2ull << 30) ? fr - (2ull << 30) : fr / 2;
+    }
+    rep->budget_bytes = budget_bytes;
+    // factors: one master stream, H, V, W uniform [0,1) column-major (bench.hpp:111-114)
+    Rng master(seed);
+    std::vector<double> H(static_cast<std::size_t>(R) * R), V(static_cast<std::size_t>(J) * R),
+        W(static_cast<std::size_t>(K) * R);
+    for (auto* m : {&H, &V, &W}) {
+      const std::int64_t rows = static_cast<std::int64_t>(m->size()) / R;
+      for (int cc = 0; cc < R; ++cc)
+        for (std::int64_t r = 0; r < rows; ++r) (*m)[static_cast<std::size_t>(cc * rows + r)] = master.uniform(0.0, 1.0);
+    }
+    // Y_k = Q_k^T X_k with seeded random orthonormal Q_k (bench.hpp:115-129), projected on the device
+    std::vector<double> Qh(static_cast<std::size_t>(c->NR) * R);
+    {
+      const int nt = static_cast<int>(std::max(1u, std::min(32u, std::thread::hardware_concurrency())));
+      std::vector<std::thread> th;
+      std::vector<int> bad(static_cast<std::size_t>(nt), -1);
+      auto work = [&](int t) {
+        for (std::int64_t k = K * t / nt; k < K * (t + 1) / nt; ++k) {
+          const std::int64_t I = c->srp_host[static_cast<std::size_t>(k + 1)] - c->srp_host[static_cast<std::size_t>(k)];
+          if (I < R) {
+            if (bad[static_cast<std::size_t>(t)] < 0) bad[static_cast<std::size_t>(t)] = static_cast<int>(k);
+            continue;
+          }
+          Rng rk(substream_seed(seed, static_cast<std::uint64_t>(c->k_begin + k) + 1));
+          random_orthonormal(rk, I, R, Qh.data() + (c->srp_host[static_cast<std::size_t>(k)] - c->srp_host[0]) * R);
+        }
+      };
+      for (int t = 1; t < nt; ++t) th.emplace_back(work, t);
+      work(0);
+      for (auto& x : th) x.join();
+      for (int b : bad)
+        if (b >= 0) throw DataError("rank exceeds observations for subject " + std::to_string(b));
+    }
+    std::vector<std::int64_t> ptr;
+    std::vector<std::int32_t> cols;
+    shard_cols(c, ptr, cols);
+    const std::int64_t nc = ptr.back();
+    PackedDev d;
+    {
+      // device Y + the per-column occurrence lists of the packed mode-2 kernel
+      d.ptr.resize(ptr.size());
+      d.cols.resize(std::max<std::size_t>(cols.size(), 1));
+      d.Y.resize(std::max<std::size_t>(static_cast<std::size_t>(nc) * R, 1));
+      P2G_CUDA(cudaMemcpyAsync(d.ptr.get(), ptr.data(), sizeof(std::int64_t) * ptr.size(), cudaMemcpyHostToDevice, c->stream));
+      if (nc)
+        P2G_CUDA(cudaMemcpyAsync(d.cols.get(), cols.data(), sizeof(std::int32_t) * nc, cudaMemcpyHostToDevice, c->stream));
+      std::vector<std::int64_t> cnt(static_cast<std::size_t>(J + 1), 0);
+      for (std::int64_t t = 0; t < nc; ++t) cnt[static_cast<std::size_t>(cols[static_cast<std::size_t>(t)]) + 1]++;
+      for (std::int64_t j = 0; j < J; ++j) cnt[static_cast<std::size_t>(j + 1)] += cnt[static_cast<std::size_t>(j)];
+      std::vector<std::int64_t> occ(static_cast<std::size_t>(2 * std::max<std::int64_t>(nc, 1)));
+      std::vector<std::int64_t> fill(cnt.begin(), cnt.end() - 1);
+      for (std::int64_t k = 0; k < K; ++k)
+        for (std::int64_t t = ptr[static_cast<std::size_t>(k)]; t < ptr[static_cast<std::size_t>(k + 1)]; ++t) {
+          const std::int64_t pos = fill[static_cast<std::size_t>(cols[static_cast<std::size_t>(t)])]++;
+          occ[static_cast<std::size_t>(2 * pos)] = t;
+          occ[static_cast<std::size_t>(2 * pos + 1)] = k;
+        }
+      d.occ_ptr.resize(cnt.size());
+      d.occ.resize(occ.size());
+      P2G_CUDA(cudaMemcpyAsync(d.occ_ptr.get(), cnt.data(), sizeof(std::int64_t) * cnt.size(), cudaMemcpyHostToDevice, c->stream));
+      P2G_CUDA(cudaMemcpyAsync(d.occ.get(), occ.data(), sizeof(std::int64_t) * occ.size(), cudaMemcpyHostToDevice, c->stream));
+      alloc_state(c, R);
+      P2G_CUDA(cudaMemcpyAsync(c->Q.get(), Qh.data(), sizeof(double) * c->NR * R, cudaMemcpyHostToDevice, c->stream));
+      launch_project(c, R, c->Q.get(), d.ptr.get(), d.cols.get(), d.Y.get(), c->stream);
+      d.H.resize(static_cast<std::size_t>(R) * R);
+      d.V.resize(static_cast<std::size_t>(std::max<std::int64_t>(J, 1)) * R);
+      d.W.resize(static_cast<std::size_t>(std::max<std::int64_t>(K, 1)) * R);
+      upload_colmajor(c, H.data(), R, R, d.H.get());
+      P2G_CUDA(cudaStreamSynchronize(c->stream));
+      upload_colmajor(c, V.data(), J, R, d.V.get());
+      P2G_CUDA(cudaStreamSynchronize(c->stream));
+      upload_colmajor(c, W.data(), K, R, d.W.get());
+      P2G_CUDA(cudaStreamSynchronize(c->stream));
+    }
+    const std::int64_t rows_of[3] = {R, J, K};
+    rep->specialized_device_bytes = static_cast<std::uint64_t>(
+        sizeof(double) * (static_cast<std::size_t>(nc) * R + static_cast<std::size_t>(R + J + K) * R +
+                          static_cast<std::size_t>(std::max<std::int64_t>(J, K)) * R) +
+        sizeof(std::int64_t) * (ptr.size() + 2 * static_cast<std::size_t>(nc) + static_cast<std::size_t>(J + 1)) +
+        sizeof(std::int32_t) * static_cast<std::size_t>(nc));
+    cudaEvent_t e0, e1;
+    P2G_CUDA(cudaEventCreate(&e0));
+    P2G_CUDA(cudaEventCreate(&e1));
+    auto timed = [&](auto&& fn) {
+      P2G_CUDA(cudaEventRecord(e0, c->stream));
+      fn();
+      P2G_CUDA(cudaEventRecord(e1, c->stream));
+      P2G_CUDA(cudaEventSynchronize(e1));
+      float ms = 0.f;
+      P2G_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+      return static_cast<double>(ms);
+    };
+    DBuf<double> out;
+    out.resize(static_cast<std::size_t>(std::max<std::int64_t>({R, J, K})) * R);
+    // specialized sweep (one warm-up sweep first: first-launch costs are not the kernels')
+    std::vector<std::vector<double>> sm(3);
+    std::vector<double> sweep;
+    for (int r = -1; r < reps; ++r) {
+      double sw = 0.0;
+      for (int mode = 1; mode <= 3; ++mode) {
+        const double ms = timed([&] { packed_mode(c, mode, K, J, R, d, d.H.get(), d.V.get(), d.W.get(), out.get()); });
+        if (r >= 0) {
+          sm[static_cast<std::size_t>(mode - 1)].push_back(ms);
+          rep->checksum_specialized += device_sum(c, out.get(), rows_of[mode - 1] * R);
+        }
+        sw += ms;
+      }
+      if (r >= 0) sweep.push_back(sw);
+    }
+    for (int m = 0; m < 3; ++m) rep->specialized_ms[m] = median(sm[static_cast<std::size_t>(m)]);
+    rep->specialized_sweep_ms = median(sweep);
+    // naive, budget-gated per mode (the materialisation bytes, mttkrp.hpp:241-253)
+    bool all = true;
+    std::vector<std::vector<double>> nm(3);
+    for (int mode = 1; mode <= 3; ++mode) {
+      rep->naive_bytes[mode - 1] = naive_bytes(K, J, R, mode);
+      if (rep->naive_bytes[mode - 1] > budget_bytes) {
+        rep->naive_oom[mode - 1] = 1;
+        rep->naive_ms[mode - 1] = -1.0;
+        all = false;
+        continue;
+      }
+      NaiveScratch s;
+      s.prepare(c, mode, K, J, R, d.ptr.get(), nc);
+      for (int r = -1; r < reps; ++r) {
+        const double ms = timed([&] {
+          naive_mttkrp(c, s, mode, K, J, R, d.ptr.get(), d.cols.get(), d.Y.get(), nc, d.H.get(), d.V.get(), d.W.get(),
+                       out.get());
+        });
+        if (r >= 0) {
+          nm[static_cast<std::size_t>(mode - 1)].push_back(ms);
+          // cuBLAS writes column-major: the same entries, so the same sum up to order
+          rep->checksum_naive += device_sum(c, out.get(), rows_of[mode - 1] * R);
+        }
+      }
+      rep->naive_ms[mode - 1] = median(nm[static_cast<std::size_t>(mode - 1)]);
+    }
+    if (all) {
+      std::vector<double> ns;
+      for (int r = 0; r < reps; ++r)
+        ns.push_back(nm[0][static_cast<std::size_t>(r)] + nm[1][static_cast<std::size_t>(r)] +
+                     nm[2][static_cast<std::size_t>(r)]);
+      rep->naive_sweep_ms = median(ns);
+      rep->speedup = rep->naive_sweep_ms / rep->specialized_sweep_ms;
+    } else {
+      rep->naive_sweep_oom = 1;
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    c->state_valid = false;
   });
 }
 

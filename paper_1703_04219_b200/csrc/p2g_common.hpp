@@ -3,6 +3,7 @@
 // is standardised; the generator and the initial factors depend on it).
 #pragma once
 
+#include <cmath>
 #include <cstdint>
 #include <limits>
 #include <random>
@@ -72,6 +73,19 @@ class Rng {
  public:
   explicit Rng(std::uint64_t seed) : gen_(seed) {}
   double uniform() { return static_cast<double>(gen_() >> 11) * 0x1.0p-53; }
+  double uniform(double lo, double hi) { return lo + (hi - lo) * uniform(); }
+  /// Box-Muller pair on the pinned uniform stream (common.hpp:92-104).
+  double normal() {
+    if (have_spare_) {
+      have_spare_ = false;
+      return spare_;
+    }
+    const double u1 = 1.0 - uniform(), u2 = uniform();
+    const double r = std::sqrt(-2.0 * std::log(u1)), a = 2.0 * M_PI * u2;
+    spare_ = r * std::sin(a);
+    have_spare_ = true;
+    return r * std::cos(a);
+  }
   std::uint64_t below(std::uint64_t n) {
     const std::uint64_t mx = std::numeric_limits<std::uint64_t>::max();
     const std::uint64_t limit = mx - mx % n;
@@ -84,6 +98,8 @@ class Rng {
 
  private:
   std::mt19937_64 gen_;
+  double spare_ = 0.0;
+  bool have_spare_ = false;
 };
 
 }  // namespace p2g

@@ -12,6 +12,8 @@
 
 #include "p2g_common.hpp"
 
+struct cublasContext;  // cuBLAS handle (cublasHandle_t), dlopen'ed on first use
+
 namespace p2g {
 
 #define P2G_CUDA(call)                                                                                   \
@@ -87,6 +89,14 @@ struct p2g_ctx {
   int rank = 0, world = 1;
   cudaStream_t stream = nullptr;
   p2g::NcclState* nccl = nullptr;
+  // Host-staged collective (p2g_set_host_collective): used instead of NCCL
+  // when set, e.g. by a gloo process group in tests.
+  int (*host_coll)(double*, int64_t, int32_t, void*) = nullptr;
+  void* host_coll_user = nullptr;
+  double* coll_pinned = nullptr;
+  std::size_t coll_pinned_n = 0;
+  // Fault injection (p2g_inject_fault): force a rank-local error at an iteration.
+  int fault_kind = 0, fault_iter = 0;
   int num_sms = 148;
 
   // Shard of the sparse tensor.
@@ -98,6 +108,7 @@ struct p2g_ctx {
   std::int64_t nnz_total = 0;
   double norm_x = 0.0;  // ||X||_F^2 over ALL subjects (allreduced)
   bool loaded = false;
+  bool shard_local = false;  // loaded by p2g_load_shard: W0 / W arguments are this rank's rows only
   p2g::DBuf<std::int64_t> srp, rp;
   p2g::DBuf<std::int32_t> ci;
   p2g::DBuf<double> val;
@@ -111,7 +122,7 @@ struct p2g_ctx {
   p2g::DBuf<double> G1, G2, G3, gramH; // R*R
   p2g::DBuf<double> gvraw, gwc;       // R*R, R*R+1
   p2g::DBuf<double> stage;            // host<->device staging (col-major)
-  std::vector<std::int64_t> srp_host;  // full subj_row_ptr (validation, shard bookkeeping)
+  std::vector<std::int64_t> srp_host;  // this shard's subj_row_ptr (global row numbers; validation)
   double* pinned = nullptr;           // small pinned host block for per-iteration scalars
   p2g::DBuf<double> pinvbuf;          // R*R
   p2g::DBuf<double> partials;         // scratch for per-block partials
@@ -154,6 +165,11 @@ struct p2g_ctx {
   bool polar_sweeps_valid = false;
   bool masks_valid = false;
   bool state_valid = false;
+
+  // Per-iteration phase times of the last p2g_fit (the reference's
+  // IterationStats ms_procrustes / ms_project / ms_cp, solver.hpp:70-77).
+  std::vector<double> fit_phase_ms;
+  cudaEvent_t ev_it[3] = {nullptr, nullptr, nullptr};
 
   // Timing.
   bool timing = false;
@@ -222,6 +238,28 @@ void launch_packed_mode13(int mode, std::int64_t K, std::int64_t J, int R, const
 void launch_packed_mode2(std::int64_t K, std::int64_t J, int R, const std::int64_t* ycol_ptr,
                          const std::int32_t* ycols, const double* Y, const double* H, const double* W,
                          const std::int64_t* occ_ptr, const std::int64_t* occ, double* out, cudaStream_t s);
+
+// Naive MTTKRP (k_naive.cu, mttkrp.hpp:198-253): materialised unfolding x
+// Khatri-Rao product on the device; scratch reused across calls.
+struct NaiveScratch {
+  DBuf<double> A, KRP;
+  DBuf<std::int64_t> subj_of;
+  cublasContext* blas = nullptr;
+  NaiveScratch() = default;
+  NaiveScratch(const NaiveScratch&) = delete;
+  NaiveScratch& operator=(const NaiveScratch&) = delete;
+  ~NaiveScratch();
+  void prepare(p2g_ctx* c, int mode, std::int64_t K, std::int64_t J, int R, const std::int64_t* ptr, std::int64_t nc);
+};
+std::uint64_t naive_bytes(std::int64_t K, std::int64_t J, std::int64_t R, int mode);
+void naive_mttkrp(p2g_ctx* c, NaiveScratch& s, int mode, std::int64_t K, std::int64_t J, int R,
+                  const std::int64_t* ptr, const std::int32_t* cols, const double* Y, std::int64_t nc, const double* H,
+                  const double* V, const double* W, double* out);
+
+// Eye initialisation (k_init.cu): C = sum_k X_k^T X_k of this shard into C
+// (J x J), then V (row-major J x R) = |top-R eigenvectors of C| (C destroyed).
+void build_column_gram(p2g_ctx* c, double* C);
+void eye_vectors(p2g_ctx* c, double* C, int R, double* V);
 
 // Dense helpers (k_dense.cu).
 int gram_partials(int R, std::int64_t n, const double* A, const double* B, double* partials, int max_blocks,
