@@ -167,6 +167,7 @@ inline std::pair<Parafac2Factors, FitTrace> fit_parafac2(const IrregularTensor& 
   detail::load(ctx, X);
   FitTrace trace;
   std::vector<double> Qp(static_cast<std::size_t>(X.to_csr().subj_row_ptr.back() * R));
+  std::vector<double> phases;
   auto run = [&](int iters, bool explicit_init, std::vector<double>& fit, std::vector<double>& res,
                  std::vector<double>& ms, p2g_fit_summary& sum) {
     // initialize() above already produced the reference's initial state
@@ -183,7 +184,6 @@ inline std::pair<Parafac2Factors, FitTrace> fit_parafac2(const IrregularTensor& 
     int32_t np = 0;
     check(p2g_fit_phase_ms(ctx, iters, phases.data(), &np));
   };
-  std::vector<double> phases;
   auto stats = [&](IterationStats& st, int i) {  // IterationStats timers (solver.hpp:278-297), device-timed
     st.ms_procrustes = phases[static_cast<std::size_t>(3 * i)];
     st.ms_project = phases[static_cast<std::size_t>(3 * i + 1)];
