@@ -52,6 +52,40 @@ __device__ __forceinline__ double rcp_nr(double x) {
   return y;
 }
 
+/// Shared-memory accesses at a 32-bit shared address plus a compile-time
+/// byte offset (ptxas folds a warp-uniform base into [R + UR + imm]).  The
+/// asm statements keep their source order, so a batch of loads written ahead
+/// of a batch of stores is issued that way.
+template <int IMM>
+__device__ __forceinline__ double lds64(unsigned a) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1+%2];" : "=d"(v) : "r"(a), "n"(IMM) : "memory");
+  return v;
+}
+template <int IMM>
+__device__ __forceinline__ double2 lds128(unsigned a) {
+  double2 v;
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2+%3];" : "=d"(v.x), "=d"(v.y) : "r"(a), "n"(IMM) : "memory");
+  return v;
+}
+template <int IMM>
+__device__ __forceinline__ void sts64(unsigned a, double v) {
+  asm volatile("st.shared.f64 [%0+%1], %2;" ::"r"(a), "n"(IMM), "d"(v) : "memory");
+}
+template <int IMM>
+__device__ __forceinline__ void sts128(unsigned a, double x, double y) {
+  asm volatile("st.shared.v2.f64 [%0+%1], {%2, %3};" ::"r"(a), "n"(IMM), "d"(x), "d"(y) : "memory");
+}
+__device__ __forceinline__ uint4 lds128u(unsigned a) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a) : "memory");
+  return v;
+}
+/// The shared address of p, made warp-uniform (a uniform register).
+__device__ __forceinline__ unsigned smem_uniform(const void* p) {
+  return __shfl_sync(kFull, static_cast<unsigned>(__cvta_generic_to_shared(p)), 0);
+}
+
 template <int RP>
 __device__ __forceinline__ void axpy_row(double (&acc)[RP], const double* __restrict__ vrow, double a, int R) {
 #pragma unroll

@@ -26,12 +26,15 @@
 // takes V_A (stored in Ewarm) as its preconditioner.
 #include <algorithm>
 #include <cstdlib>
+#include <type_traits>
 
 #include "dev_common.cuh"
 #include "p2g_ctx.hpp"
 
 namespace p2g {
 namespace {
+
+#include "jacobi_plan40.inc"
 
 constexpr int kLgMaxSweeps = 40;
 constexpr double kTinyL = 1e-24;  // M_pp below this x max diag: near-null column (covers D5's 1e-26)
@@ -79,16 +82,23 @@ struct LgArgs {
 constexpr double kTauL = 1e-4;   // Jacobi stop: max scaled off-diagonal (truncation error <= 3e-12 measured)
 constexpr double kSkipL = 1e-5;  // rotations below this scaled size are skipped (threshold Jacobi; the second-order correction covers them)
 
-template <int RP>
+template <int RP, bool EXACT = false>
 struct LgWarp {
+  // exact R = 40 runs the physical-order Jacobi round (jacobi_plan40.inc)
+  static constexpr bool kPhys = RP == 40 && EXACT;
   static constexpr int LDM = RP + 1;  // M: odd leading dimension (column walks conflict free)
   static constexpr int LDV = RP + 2;  // V'^T: even, 16-byte rows for the paired updates
-  static constexpr int kMat = RP * LDM;
-  static constexpr int kVt = RP * LDV;
+  static constexpr int LDP = RP + 1;  // kPhys: rotated rows of the physical-order M (odd stride)
+  static constexpr int kMat = kPhys ? RP * LDP : RP * LDM;  // M (kPhys: Jacobi buffer 0)
+  static constexpr int kVt = RP * LDV;                      // V'^T (kPhys: Jacobi buffer 1)
   static constexpr int NBLK = (RP / 2) * (RP / 2 - 1) / 2;  // off-diagonal 2 x 2 blocks (slot i1 < i2)
-  static constexpr int kTabD = ((NBLK + (RP - 1) * (RP / 2) + 7) / 8) * 2;  // uint16 tables, in doubles (even)
+  // CTA tables, in doubles (even): uint16 block and round-robin tables; kPhys: the per-lane
+  // plan (uint4 [12][32] blocks: two per block, uint4 [32] diagonal blocks) and the row
+  // rotations (int [RP])
+  static constexpr int kTabD = kPhys ? (16 * 13 * 32 + 4 * RP) / 8 : ((NBLK + (RP - 1) * (RP / 2) + 7) / 8) * 2;
   // M, V'^T, w, u (1/sqrt diag), then per pair slot and double-buffered: (c, s), t M_pq, int4 offsets
-  static constexpr int kWarpD = kMat + kVt + 2 * RP + 2 * (RP + RP / 2 + RP);
+  // (kPhys: (c, s) only)
+  static constexpr int kWarpD = kMat + kVt + 2 * RP + (kPhys ? 2 * RP : 2 * (RP + RP / 2 + RP));
   static constexpr int kWarpDE = (kWarpD + 1) & ~1;
   static constexpr int pick_wpb() {
     int w = 16;
@@ -171,15 +181,20 @@ __device__ __forceinline__ void warp_mm(int rows, int R, FA fa, FB fb, Epi epi) 
 
 template <int RP, bool EXACT>
 __global__ void __launch_bounds__(LgWarp<RP>::WPB * 32, 1) k_procrustes_large_w(LgArgs a) {
-  using L = LgWarp<RP>;
-  constexpr int LDM = L::LDM, LDV = L::LDV, NB = L::NB, WPB = L::WPB;
+  using L = LgWarp<RP, EXACT>;
+  constexpr int LDM = L::LDM, LDV = L::LDV, LDP = L::LDP, NB = L::NB, WPB = L::WPB;
   extern __shared__ __align__(16) double smem[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int R = EXACT ? RP : a.R;
   const int RR = R * R;
   const int m = (R + 1) & ~1, half = m / 2, nblk = half * (half - 1) / 2;
+  // exact R = 40: the physical-order Jacobi round (jacobi_plan40.inc)
+  constexpr bool kPhys = L::kPhys;
+  constexpr int LDVx = kPhys ? LDM : LDV;  // V'^T leading dimension after the sweeps
   std::uint16_t* blk = reinterpret_cast<std::uint16_t*>(smem);  // 2 x 2 block (slot i1, slot i2) of M
   std::uint16_t* sched = blk + L::NBLK;                         // round-robin (p, q) per (round, slot)
+  uint4* pplan = reinterpret_cast<uint4*>(smem);                // kPhys: [12][32] blocks, [32] diagonal
+  int* prot = reinterpret_cast<int*>(pplan + 13 * 32);          // kPhys: row rotations of the M layout
   double* M = smem + L::kTabD + wid * L::kWarpDE;
   double* Vt = M + L::kMat;  // V'^T: Vt[p * LDV + k] = V'(k, p)
   double* w = Vt + L::kVt;
@@ -189,6 +204,18 @@ __global__ void __launch_bounds__(LgWarp<RP>::WPB * 32, 1) k_procrustes_large_w(
   double2* rotb = reinterpret_cast<double2*>(u + RP);
   double* rtb = reinterpret_cast<double*>(rotb + RP);
   int4* ofsb = reinterpret_cast<int4*>(rtb + RP);
+  if constexpr (kPhys) {
+    // the plan as byte offsets: rot(i1) | rot(i2) << 16 (16 B per slot), the rest 8 B per element
+    for (int x = threadIdx.x; x < RP; x += blockDim.x) prot[x] = c_plan_rot[x];
+    for (int e = threadIdx.x; e < 6 * 32; e += blockDim.x) {  // block j of lane l: [2 j][l], [2 j + 1][l]
+      const int j = e >> 5, l = e & 31;
+      pplan[64 * j + l] = make_uint4(c_plan_blk[l][j][0] * 16u, c_plan_blk[l][j][1] * 8u, c_plan_blk[l][j][2] * 8u, 0u);
+      pplan[64 * j + 32 + l] = make_uint4(c_plan_blk[l][j][3] * 8u, c_plan_blk[l][j][4] * 8u, 0u, 0u);
+    }
+    for (int l = threadIdx.x; l < 32; l += blockDim.x)
+      pplan[12 * 32 + l] = l < 20 ? make_uint4(c_plan_diag[l][0] * 8u, c_plan_diag[l][1] * 8u, c_plan_diag[l][2] * 8u, 0u)
+                                 : make_uint4(0u, 0u, 0u, 0u);
+  } else
   for (int it = threadIdx.x; it < nblk; it += blockDim.x) {  // (the slots' own 2 x 2 blocks: param_store)
     int i1 = 0, r = it;
     while (r >= half - 1 - i1) {
@@ -197,6 +224,7 @@ __global__ void __launch_bounds__(LgWarp<RP>::WPB * 32, 1) k_procrustes_large_w(
     }
     blk[it] = static_cast<std::uint16_t>((i1 << 8) | (i1 + 1 + r));
   }
+  if constexpr (!kPhys)
   for (int it = threadIdx.x; it < (m - 1) * half; it += blockDim.x) {
     const int round = it / half, l = it - round * half;
     int p, q;
@@ -328,7 +356,18 @@ __global__ void __launch_bounds__(LgWarp<RP>::WPB * 32, 1) k_procrustes_large_w(
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
               const int j = 8 * bj + fn + h;
-              if (EXACT || (i < R && j < R)) {
+              if constexpr (kPhys) {
+                // upper triangle in physical (round-0) order: logical l sits at
+                // position 2l (l < 20), 2 (39 - l) + 1 (l >= 20; 39 -> 1)
+                if (bi > bj || i <= j) {
+                  const int xi = i == 39 ? 1 : (i < 20 ? 2 * i : 2 * (39 - i) + 1);
+                  const int xj = j == 39 ? 1 : (j < 20 ? 2 * j : 2 * (39 - j) + 1);
+                  const int x = min(xi, xj), y = max(xi, xj);
+                  const int c = y + prot[x];
+                  M[LDP * x + (c >= LDP ? c - LDP : c)] = acc[t][h];
+                }
+                finite &= isfinite(acc[t][h]);
+              } else if (EXACT || (i < R && j < R)) {
                 M[i * LDM + j] = acc[t][h];
                 M[j * LDM + i] = acc[t][h];
                 finite &= isfinite(acc[t][h]);
@@ -376,188 +415,414 @@ __global__ void __launch_bounds__(LgWarp<RP>::WPB * 32, 1) k_procrustes_large_w(
         flag = P2G_FLAG_ACCURATE;
         break;
       }
-      // V' = I; row `lane` of V' also in registers, in round-0 physical order
-      for (int e = lane; e < R * LDV; e += 32) {
-        const int p = e / LDV, kk = e - p * LDV;
-        Vt[e] = p == kk ? 1.0 : 0.0;
-      }
-      double vreg[kRegRows > 0 ? RP : 1];
-#pragma unroll
-      for (int x = 0; x < (kRegRows > 0 ? RP : 1); ++x) vreg[x] = rr_l0(RP, x) == lane ? 1.0 : 0.0;
       bool converged = false;
       int sweeps = 0;
       double off = 0.0;  // scaled off-diagonal mass at the start of the pass
-      for (int sweep = 0; sweep < kLgMaxSweeps; ++sweep, ++sweeps) {
-        double dmax = 0.0;
-        for (int j = 0; j < R; ++j) dmax = fmax(dmax, M[j * LDM + j]);
-        const double tiny = kTinyL * dmax;
-        for (int p = lane; p < R; p += 32) {
-          const double d = M[p * LDM + p];
-          u[p] = d > tiny ? 1.0 / sqrt(d) : 0.0;
-        }
-        __syncwarp();
-        double omax = 0.0, osum = 0.0;
-        for (int e = lane; e < RR; e += 32) {
-          const int p = e / R, q = e - p * R;
-          const double x = M[p < q ? p * LDM + q : q * LDM + p] * u[p] * u[q];
-          if (p != q) {
-            omax = fmax(omax, fabs(x));
-            osum = fma(x, x, osum);
-          }
-        }
-        omax = dev::warp_max(omax);
-        if (sweep == 0) {
-          off = dev::warp_sum(osum);
-          if (a.dbg && lane == 0) {
-            const int b = omax <= 0.0 ? 0 : min(9, max(0, static_cast<int>(floor(log10(omax))) + 9));
-            atomicAdd(a.dbg + 4 + b, 1);
-          }
-        }
-        if (omax <= kTauL) {
-          converged = true;
-          break;
-        }
-        // Rotation parameters of one round's slot (lanes < half store them).
-        // Split into the shared-memory loads and a pure-ALU tail, so that the
-        // tail of round r + 1 can be scheduled among round r's V' updates.
-        struct PIn {
+      double* Mx = M;    // after the sweeps: M' (logical order, full)
+      double* Vx = Vt;   // and V'^T (Vx[p * LDVx + k] = V'(k, p))
+      if constexpr (kPhys) {
+        // Physical-order round (jacobi_plan40.inc): slot i's
+        // pair sits at positions (2i, 2i + 1) of M, V' rows and V' row chunks;
+        // after each round every position's content moves one step along the
+        // fixed cycle sigma, so all addresses are static.  M ping-pongs between
+        // the M region (buffer 0) and the V'^T region (buffer 1).
+        constexpr int kBuf = L::kMat * 8;  // bytes from buffer 0 to buffer 1
+        const unsigned mb = dev::smem_uniform(M);
+        const unsigned rb = dev::smem_uniform(rotb);  // (c, s) per slot, 2 x 20 double2
+        const int ch = lane & 3, crow = 32 + (lane >> 2);
+        double vreg[RP], vch[10];  // V' row `lane`; positions 10 ch .. 10 ch + 9 of row crow
+#pragma unroll
+        for (int x = 0; x < RP; ++x) vreg[x] = rr_l0(RP, x) == lane ? 1.0 : 0.0;
+#pragma unroll
+        for (int k = 0; k < 10; ++k) vch[k] = rr_l0(RP, 10 * ch + k) == crow ? 1.0 : 0.0;
+        double tiny = 0.0;
+        struct Dg {
           double al, be, ga;
-          int p, q;
         };
-        auto param_load = [&](int round) {
-          PIn in;
-          const int pq = sched[round * half + (lane < half ? lane : 0)];
-          in.p = pq & 0xff;
-          in.q = pq >> 8;
-          const int qq = in.q != 0xff ? in.q : in.p;
-          in.al = M[in.p * LDM + in.p];
-          in.be = M[qq * LDM + qq];
-          in.ga = in.q != 0xff ? M[in.p < qq ? in.p * LDM + qq : qq * LDM + in.p] : 0.0;
-          return in;
+        // slot `lane` (< 20): its diagonal block from the buffer at `rd` ...
+        // this lane's static share of every round (pplan, byte offsets): blocks
+        // {rot(i1) | rot(i2) << 16, r_pp | r_pq, r_qp | r_qq}, {w_pp | w_pq, w_qp | w_qq}
+        // and (lanes < 20) its slot's diagonal block {r_pp | r_qq, r_pq | w_pp, w_qq | w_pq}
+        const unsigned pb = dev::smem_uniform(pplan) + 16u * lane;
+        auto par_load = [&](unsigned rd) {
+          Dg d{0.0, 0.0, 0.0};
+          if (lane < 20) {
+            const uint4 g = dev::lds128u(pb + 16u * 12 * 32);
+            const unsigned dg[3] = {g.x, g.y, g.z};
+            d.al = dev::lds64<0>(rd + (dg[0] & 0xffffu));
+            d.be = dev::lds64<0>(rd + (dg[0] >> 16));
+            d.ga = dev::lds64<0>(rd + (dg[1] & 0xffffu));
+          }
+          return d;
         };
-        auto param_store = [&](const PIn& in, int buf, bool diag) {
-          const bool on = in.q != 0xff && in.al > tiny && in.be > tiny &&
-                          in.ga * in.ga > (kSkipL * kSkipL) * (in.al * in.be);
-          // t = sign(zeta) / (|zeta| + sqrt(1 + zeta^2)), zeta = (be - al) / (2 ga),
-          // without divisions: t = sign(d) 2ga / (|d| + sqrt(d^2 + 4ga^2))
-          const double d = in.be - in.al, g2 = 2.0 * in.ga;
-          const double h = on ? fma(d, d, g2 * g2) : 1.0;
+        // ... its rotation (c, s) into the rot buffer at `ro`, the rotated
+        // block's sigma-images into the buffer at `wr` (rotation as in the
+        // generic path)
+        auto par_store = [&](const Dg& d, unsigned wr, unsigned ro) {
+          const bool on = d.al > tiny && d.be > tiny && d.ga * d.ga > (kSkipL * kSkipL) * (d.al * d.be);
+          const double dd = d.be - d.al, g2 = 2.0 * d.ga;
+          const double h = on ? fma(dd, dd, g2 * g2) : 1.0;
           const double rh = h * dev::rsqrt_nr(h);
-          const double tt = on ? (d >= 0.0 ? g2 : -g2) * dev::rcp_nr(fabs(d) + rh) : 0.0;
+          const double tt = on ? (dd >= 0.0 ? g2 : -g2) * dev::rcp_nr(fabs(dd) + rh) : 0.0;
           const double c = on ? dev::rsqrt_nr(fma(tt, tt, 1.0)) : 1.0;
-          if (lane < half) {
-            // the slot's own 2 x 2 block (M_pp, M_qq, M_pq) is updated here, by
-            // the lane that holds its old values: no other block of the round
-            // touches these entries, and the next parameter load follows the
-            // round's block updates
-            if (on && diag) {  // (not for the wrapped-around load of the sweep's last round)
-              const double dt = __dmul_rn(tt, in.ga);
-              M[in.p * LDM + in.p] = in.al - dt;
-              M[in.q * LDM + in.q] = in.be + dt;
-              M[in.p < in.q ? in.p * LDM + in.q : in.q * LDM + in.p] = 0.0;
-            }
-            rotb[buf * (RP / 2) + lane] = make_double2(c, c * tt);
-            rtb[buf * (RP / 2) + lane] = tt * in.ga;
-            ofsb[buf * (RP / 2) + lane] = in.q != 0xff ? make_int4(in.p * LDM, in.q * LDM, in.p, in.q)
-                                                      : make_int4(in.p * LDM, -1, in.p, -1);
+          const double dt = __dmul_rn(tt, d.ga);
+          if (lane < 20) {
+            const uint4 g = dev::lds128u(pb + 16u * 12 * 32);
+            const unsigned dg[3] = {g.x, g.y, g.z};
+            dev::sts128<0>(ro + 16u * lane, c, c * tt);
+            dev::sts64<0>(wr + (dg[1] >> 16), on ? d.al - dt : d.al);
+            dev::sts64<0>(wr + (dg[2] & 0xffffu), on ? d.be + dt : d.be);
+            dev::sts64<0>(wr + (dg[2] >> 16), on ? 0.0 : d.ga);
           }
         };
-        param_store(param_load(0), 0, true);
-        __syncwarp();
-        for (int round = 0; round < m - 1; ++round) {
-          const int buf = round & 1;
-          const double2* rot = rotb + buf * (RP / 2);
-          const int4* ofs = ofsb + buf * (RP / 2);
-          // M <- J^T M J over this lane's 2 x 2 blocks of slot pairs
+        // M <- J^T M J over this lane's six 2 x 2 blocks, two at a time (their
+        // loads ahead of their stores), written to their sigma-images
+        auto blocks = [&](unsigned rd, unsigned wr, unsigned ro) {
 #pragma unroll
-          for (int j = 0; j < kLaneBlk; ++j) {
-            const int b = lblk[j];
-            if (b < 0) continue;
-            const int i1 = b & 0xff, i2 = b >> 8;
-            const double2 r1 = rot[i1], r2 = rot[i2];
-            if (r1.y == 0.0 && r2.y == 0.0) continue;
-            const int4 o1 = ofs[i1], o2 = ofs[i2];
-            if (!EXACT && (o1.w < 0 || o2.w < 0)) {  // odd R: 1 x 2 block against the dummy slot's index
-              const bool d1 = o1.w < 0;
-              const int ar = d1 ? o1.x : o2.x, ac = d1 ? o1.z : o2.z;  // the single index (row / column offsets)
-              const int ur = d1 ? o2.x : o1.x, uc = d1 ? o2.z : o1.z;
-              const int vr = d1 ? o2.y : o1.y, vc = d1 ? o2.w : o1.w;
-              const double cc = d1 ? r2.x : r1.x, ss = d1 ? r2.y : r1.y;
-              const int au = ac < uc ? ar + uc : ur + ac, av = ac < vc ? ar + vc : vr + ac;
-              const double xu = M[au], xv = M[av];
-              M[au] = cc * xu - ss * xv;
-              M[av] = ss * xu + cc * xv;
-              continue;
+          for (int j0 = 0; j0 < 6; j0 += 2) {
+            double2 r1[2], r2[2];
+            double x[2][4];
+#pragma unroll
+            for (int v = 0; v < 2; ++v) {
+              const uint4 q = dev::lds128u(pb + 16u * 64 * (j0 + v));
+              r1[v] = dev::lds128<0>(ro + (q.x & 0xffffu));
+              r2[v] = dev::lds128<0>(ro + (q.x >> 16));
+              x[v][0] = dev::lds64<0>(rd + (q.y & 0xffffu));  // pp
+              x[v][1] = dev::lds64<0>(rd + (q.y >> 16));      // pq
+              x[v][2] = dev::lds64<0>(rd + (q.z & 0xffffu));  // qp
+              x[v][3] = dev::lds64<0>(rd + (q.z >> 16));      // qq
             }
-            const double c1 = r1.x, s1 = r1.y, c2 = r2.x, s2 = r2.y;
-            // upper-triangle (canonical) addresses: row index < column index
-            const int e11 = o1.z < o2.z ? o1.x + o2.z : o2.x + o1.z;
-            const int e12 = o1.z < o2.w ? o1.x + o2.w : o2.y + o1.z;
-            const int e21 = o1.w < o2.z ? o1.y + o2.z : o2.x + o1.w;
-            const int e22 = o1.w < o2.w ? o1.y + o2.w : o2.y + o1.w;
-            const double x11 = M[e11], x12 = M[e12], x21 = M[e21], x22 = M[e22];
-            const double y11 = c2 * x11 - s2 * x12, y12 = s2 * x11 + c2 * x12;
-            const double y21 = c2 * x21 - s2 * x22, y22 = s2 * x21 + c2 * x22;
-            const double z11 = c1 * y11 - s1 * y21, z21 = s1 * y11 + c1 * y21;
-            const double z12 = c1 * y12 - s1 * y22, z22 = s1 * y12 + c1 * y22;
-            M[e11] = z11;
-            M[e12] = z12;
-            M[e21] = z21;
-            M[e22] = z22;
+#pragma unroll
+            for (int v = 0; v < 2; ++v) {
+              const uint4 q = dev::lds128u(pb + 16u * (64 * (j0 + v) + 32));
+              const double c1 = r1[v].x, s1 = r1[v].y, c2 = r2[v].x, s2 = r2[v].y;
+              const double x11 = x[v][0], x12 = x[v][1], x21 = x[v][2], x22 = x[v][3];
+              const double y11 = c2 * x11 - s2 * x12, y12 = s2 * x11 + c2 * x12;
+              const double y21 = c2 * x21 - s2 * x22, y22 = s2 * x21 + c2 * x22;
+              dev::sts64<0>(wr + (q.x & 0xffffu), c1 * y11 - s1 * y21);
+              dev::sts64<0>(wr + (q.x >> 16), c1 * y12 - s1 * y22);
+              dev::sts64<0>(wr + (q.y & 0xffffu), s1 * y11 + c1 * y21);
+              dev::sts64<0>(wr + (q.y >> 16), s1 * y12 + c1 * y22);
+            }
+          }
+        };
+        // V' <- V' J on the register row and the row chunk, then one step along sigma
+        auto vupd = [&](unsigned ro) {
+#pragma unroll
+          for (int i = 0; i < RP / 2; ++i) {
+            const double2 r = dev::lds128<0>(ro + 16u * i);
+            const double x0 = vreg[2 * i], y0 = vreg[2 * i + 1];
+            vreg[2 * i] = r.x * x0 - r.y * y0;
+            vreg[2 * i + 1] = r.y * x0 + r.x * y0;
+          }
+          const double t0 = vreg[0];
+#pragma unroll
+          for (int l = 0; l < RP / 2 - 1; ++l) vreg[2 * l] = vreg[2 * l + 2];
+          vreg[RP - 2] = vreg[RP - 1];
+#pragma unroll
+          for (int l = RP / 2 - 1; l >= 2; --l) vreg[2 * l + 1] = vreg[2 * l - 1];
+          vreg[3] = t0;
+          const unsigned cb = ro + 80u * ch;
+#pragma unroll
+          for (int k = 0; k < 5; ++k) {
+            const double2 r = dev::lds128<0>(cb + 16u * k);
+            const double x0 = vch[2 * k], y0 = vch[2 * k + 1];
+            vch[2 * k] = r.x * x0 - r.y * y0;
+            vch[2 * k + 1] = r.y * x0 + r.x * y0;
+          }
+          // positions 10 ch + 8 <- 10 ch + 10 (next chunk) and 10 ch + 1 <- 10 ch - 1
+          // (previous chunk); chunk 0 holds the cycle's ends 3 <- 0 and 1 (fixed)
+          const double dn = __shfl_down_sync(dev::kFull, vch[0], 1);
+          const double up = __shfl_up_sync(dev::kFull, vch[9], 1);
+          const double o0 = vch[0], o1 = vch[1], o9 = vch[9];
+          vch[0] = vch[2];
+          vch[2] = vch[4];
+          vch[4] = vch[6];
+          vch[6] = vch[8];
+          vch[8] = ch == 3 ? o9 : dn;
+          vch[9] = vch[7];
+          vch[7] = vch[5];
+          vch[5] = vch[3];
+          vch[3] = ch == 0 ? o0 : o1;
+          vch[1] = ch == 0 ? o1 : up;
+        };
+        // one sweep (m - 1 = 39 rounds) from buffer A to buffer B: rounds in
+        // pairs (A -> B with rot buffer 0, B -> A with rot buffer 1), then the last
+        auto run_sweep = [&](unsigned A, unsigned B) {
+          par_store(par_load(A), B, rb);
+          __syncwarp();
+#pragma unroll 1
+          for (int rr = 0; rr < RP - 2; rr += 2) {
+            blocks(A, B, rb);
+            __syncwarp();
+            {
+              const Dg d = par_load(B);
+              vupd(rb);
+              par_store(d, A, rb + 320u);
+            }
+            __syncwarp();
+            blocks(B, A, rb + 320u);
+            __syncwarp();
+            {
+              const Dg d = par_load(A);
+              vupd(rb + 320u);
+              par_store(d, B, rb);
+            }
+            __syncwarp();
+          }
+          blocks(A, B, rb);
+          __syncwarp();
+          vupd(rb);
+          __syncwarp();
+        };
+        int cur = 0;  // the buffer holding M at sweep boundaries (round-0 arrangement)
+        auto at = [&](const double* Mc, int x, int y) {  // element (x <= y)
+          const int c = y + prot[x];
+          return Mc[LDP * x + (c >= LDP ? c - LDP : c)];
+        };
+        for (int sweep = 0; sweep < kLgMaxSweeps; ++sweep, ++sweeps) {
+          const double* Mc = M + cur * L::kMat;
+          const double d0 = at(Mc, lane, lane), d1 = lane < 8 ? at(Mc, 32 + lane, 32 + lane) : 0.0;
+          const double dmax = dev::warp_max(fmax(d0, d1));
+          tiny = kTinyL * dmax;
+          u[lane] = d0 > tiny ? 1.0 / sqrt(d0) : 0.0;
+          if (lane < 8) u[32 + lane] = d1 > tiny ? 1.0 / sqrt(d1) : 0.0;
+          __syncwarp();
+          // scaled off-diagonal: lane < 20 walks physical rows lane and 39 - lane
+          double omax = 0.0, osum = 0.0;
+          if (lane < 20) {
+#pragma unroll 1
+            for (int side = 0; side < 2; ++side) {
+              const int x = side ? RP - 1 - lane : lane;
+              const double ux = u[x];
+              const double* row = Mc + LDP * x;
+              int c = x + 1 + prot[x];
+              if (c >= LDP) c -= LDP;
+#pragma unroll 4
+              for (int y = x + 1; y < RP; ++y) {
+                const double v = row[c] * ux * u[y];
+                omax = fmax(omax, fabs(v));
+                osum = fma(v, v, osum);
+                c = c + 1 == LDP ? 0 : c + 1;
+              }
+            }
+          }
+          omax = dev::warp_max(omax);
+          if (sweep == 0) {
+            off = 2.0 * dev::warp_sum(osum);  // both triangles, as in the generic path
+            if (a.dbg && lane == 0) {
+              const int b = omax <= 0.0 ? 0 : min(9, max(0, static_cast<int>(floor(log10(omax))) + 9));
+              atomicAdd(a.dbg + 4 + b, 1);
+            }
+          }
+          if (omax <= kTauL) {
+            converged = true;
+            break;
+          }
+          run_sweep(mb + static_cast<unsigned>(cur * kBuf), mb + static_cast<unsigned>((cur ^ 1) * kBuf));
+          cur ^= 1;
+        }
+        // M' in logical order (full) into the other buffer, V'^T into this one
+        {
+          const double* Mc = M + cur * L::kMat;
+          double* Ml = M + (cur ^ 1) * L::kMat;
+          for (int e = lane; e < RP * RP; e += 32) {
+            const int p = e / RP, q = e - p * RP;
+            const int xp = p == RP - 1 ? 1 : (p < RP / 2 ? 2 * p : 2 * (RP - 1 - p) + 1);
+            const int xq = q == RP - 1 ? 1 : (q < RP / 2 ? 2 * q : 2 * (RP - 1 - q) + 1);
+            Ml[p * LDM + q] = at(Mc, min(xp, xq), max(xp, xq));
           }
           __syncwarp();
-          // next round's parameter loads (M is final for this round) ...
-          const PIn nxt = param_load(round + 1 < m - 1 ? round + 1 : 0);
-          // ... V' <- V' J.  Register rows: slot i's pair sits at positions
-          // (2i, 2i+1); afterwards every position moves one step along the
-          // fixed cycle 0 <- 2 <- ... <- RP-2 <- RP-1 <- RP-3 <- ... <- 3 <- 0
-          // (position 1, index RP-1, stays), which is how the round-robin's
-          // pairs advance, so the next round's pairs are again (2i, 2i+1) ...
-          if constexpr (kRegRows > 0) {
+          double* V2 = M + cur * L::kMat;
 #pragma unroll
-            for (int i = 0; i < RP / 2; ++i) {
-              const double2 r = rot[i];
-              const double x0 = vreg[2 * i], y0 = vreg[2 * i + 1];
-              vreg[2 * i] = r.x * x0 - r.y * y0;
-              vreg[2 * i + 1] = r.y * x0 + r.x * y0;
-            }
-            const double t0 = vreg[0];
+          for (int x = 0; x < RP; ++x) V2[rr_l0(RP, x) * LDM + lane] = vreg[x];
 #pragma unroll
-            for (int l = 0; l < RP / 2 - 1; ++l) vreg[2 * l] = vreg[2 * l + 2];
-            vreg[RP - 2] = vreg[RP - 1];
-#pragma unroll
-            for (int l = RP / 2 - 1; l >= 2; --l) vreg[2 * l + 1] = vreg[2 * l - 1];
-            vreg[3] = t0;
+          for (int k = 0; k < 10; ++k) V2[rr_l0(RP, 10 * ch + k) * LDM + crow] = vch[k];
+          __syncwarp();
+          Mx = Ml;
+          Vx = V2;
+        }
+      } else {
+      // V' = I; row `lane` of V' also in registers, in round-0 physical order
+        for (int e = lane; e < R * LDV; e += 32) {
+          const int p = e / LDV, kk = e - p * LDV;
+          Vt[e] = p == kk ? 1.0 : 0.0;
+        }
+        double vreg[kRegRows > 0 ? RP : 1];
+  #pragma unroll
+        for (int x = 0; x < (kRegRows > 0 ? RP : 1); ++x) vreg[x] = rr_l0(RP, x) == lane ? 1.0 : 0.0;
+        for (int sweep = 0; sweep < kLgMaxSweeps; ++sweep, ++sweeps) {
+          double dmax = 0.0;
+          for (int j = 0; j < R; ++j) dmax = fmax(dmax, M[j * LDM + j]);
+          const double tiny = kTinyL * dmax;
+          for (int p = lane; p < R; p += 32) {
+            const double d = M[p * LDM + p];
+            u[p] = d > tiny ? 1.0 / sqrt(d) : 0.0;
           }
-          // ... shared-memory rows: p, q of V'^T (offset p LDV = p LDM + p) over
-          // this lane's column pairs, branch-free so the parameter tail interleaves ...
-#pragma unroll
-          for (int j = 0; j < (kSmemKp > 0 ? kLaneVit : 0); ++j) {
-            const int v = lvit[j];
-            const int sl = v & 0xff, kc = (v >> 8) & 0xff;
-            const double2 r = rot[v < 0 ? 0 : sl];
-            const int4 o = ofs[v < 0 ? 0 : sl];
-            const bool on = v >= 0 && r.y != 0.0;
-            double2* vp = reinterpret_cast<double2*>(Vt + (on ? o.x + o.z + kc : 0));
-            double2* vq = reinterpret_cast<double2*>(Vt + (on ? o.y + o.w + kc : 0));
-            const double2 x = *vp, y = *vq;
-            if (on) {
-              *vp = make_double2(r.x * x.x - r.y * y.x, r.x * x.y - r.y * y.y);
-              *vq = make_double2(r.y * x.x + r.x * y.x, r.y * x.y + r.x * y.y);
+          __syncwarp();
+          double omax = 0.0, osum = 0.0;
+          for (int e = lane; e < RR; e += 32) {
+            const int p = e / R, q = e - p * R;
+            const double x = M[p < q ? p * LDM + q : q * LDM + p] * u[p] * u[q];
+            if (p != q) {
+              omax = fmax(omax, fabs(x));
+              osum = fma(x, x, osum);
             }
           }
-          // ... and the parameters into the other buffer
-          param_store(nxt, buf ^ 1, round + 1 < m - 1);
+          omax = dev::warp_max(omax);
+          if (sweep == 0) {
+            off = dev::warp_sum(osum);
+            if (a.dbg && lane == 0) {
+              const int b = omax <= 0.0 ? 0 : min(9, max(0, static_cast<int>(floor(log10(omax))) + 9));
+              atomicAdd(a.dbg + 4 + b, 1);
+            }
+          }
+          if (omax <= kTauL) {
+            converged = true;
+            break;
+          }
+          // Rotation parameters of one round's slot (lanes < half store them).
+          // Split into the shared-memory loads and a pure-ALU tail, so that the
+          // tail of round r + 1 can be scheduled among round r's V' updates.
+          struct PIn {
+            double al, be, ga;
+            int p, q;
+          };
+          auto param_load = [&](int round) {
+            PIn in;
+            const int pq = sched[round * half + (lane < half ? lane : 0)];
+            in.p = pq & 0xff;
+            in.q = pq >> 8;
+            const int qq = in.q != 0xff ? in.q : in.p;
+            in.al = M[in.p * LDM + in.p];
+            in.be = M[qq * LDM + qq];
+            in.ga = in.q != 0xff ? M[in.p < qq ? in.p * LDM + qq : qq * LDM + in.p] : 0.0;
+            return in;
+          };
+          auto param_store = [&](const PIn& in, int buf, bool diag) {
+            const bool on = in.q != 0xff && in.al > tiny && in.be > tiny &&
+                            in.ga * in.ga > (kSkipL * kSkipL) * (in.al * in.be);
+            // t = sign(zeta) / (|zeta| + sqrt(1 + zeta^2)), zeta = (be - al) / (2 ga),
+            // without divisions: t = sign(d) 2ga / (|d| + sqrt(d^2 + 4ga^2))
+            const double d = in.be - in.al, g2 = 2.0 * in.ga;
+            const double h = on ? fma(d, d, g2 * g2) : 1.0;
+            const double rh = h * dev::rsqrt_nr(h);
+            const double tt = on ? (d >= 0.0 ? g2 : -g2) * dev::rcp_nr(fabs(d) + rh) : 0.0;
+            const double c = on ? dev::rsqrt_nr(fma(tt, tt, 1.0)) : 1.0;
+            if (lane < half) {
+              // the slot's own 2 x 2 block (M_pp, M_qq, M_pq) is updated here, by
+              // the lane that holds its old values: no other block of the round
+              // touches these entries, and the next parameter load follows the
+              // round's block updates
+              if (on && diag) {  // (not for the wrapped-around load of the sweep's last round)
+                const double dt = __dmul_rn(tt, in.ga);
+                M[in.p * LDM + in.p] = in.al - dt;
+                M[in.q * LDM + in.q] = in.be + dt;
+                M[in.p < in.q ? in.p * LDM + in.q : in.q * LDM + in.p] = 0.0;
+              }
+              rotb[buf * (RP / 2) + lane] = make_double2(c, c * tt);
+              rtb[buf * (RP / 2) + lane] = tt * in.ga;
+              ofsb[buf * (RP / 2) + lane] = in.q != 0xff ? make_int4(in.p * LDM, in.q * LDM, in.p, in.q)
+                                                        : make_int4(in.p * LDM, -1, in.p, -1);
+            }
+          };
+          param_store(param_load(0), 0, true);
+          __syncwarp();
+          for (int round = 0; round < m - 1; ++round) {
+            const int buf = round & 1;
+            const double2* rot = rotb + buf * (RP / 2);
+            const int4* ofs = ofsb + buf * (RP / 2);
+            // M <- J^T M J over this lane's 2 x 2 blocks of slot pairs
+  #pragma unroll
+            for (int j = 0; j < kLaneBlk; ++j) {
+              const int b = lblk[j];
+              if (b < 0) continue;
+              const int i1 = b & 0xff, i2 = b >> 8;
+              const double2 r1 = rot[i1], r2 = rot[i2];
+              if (r1.y == 0.0 && r2.y == 0.0) continue;
+              const int4 o1 = ofs[i1], o2 = ofs[i2];
+              if (!EXACT && (o1.w < 0 || o2.w < 0)) {  // odd R: 1 x 2 block against the dummy slot's index
+                const bool d1 = o1.w < 0;
+                const int ar = d1 ? o1.x : o2.x, ac = d1 ? o1.z : o2.z;  // the single index (row / column offsets)
+                const int ur = d1 ? o2.x : o1.x, uc = d1 ? o2.z : o1.z;
+                const int vr = d1 ? o2.y : o1.y, vc = d1 ? o2.w : o1.w;
+                const double cc = d1 ? r2.x : r1.x, ss = d1 ? r2.y : r1.y;
+                const int au = ac < uc ? ar + uc : ur + ac, av = ac < vc ? ar + vc : vr + ac;
+                const double xu = M[au], xv = M[av];
+                M[au] = cc * xu - ss * xv;
+                M[av] = ss * xu + cc * xv;
+                continue;
+              }
+              const double c1 = r1.x, s1 = r1.y, c2 = r2.x, s2 = r2.y;
+              // upper-triangle (canonical) addresses: row index < column index
+              const int e11 = o1.z < o2.z ? o1.x + o2.z : o2.x + o1.z;
+              const int e12 = o1.z < o2.w ? o1.x + o2.w : o2.y + o1.z;
+              const int e21 = o1.w < o2.z ? o1.y + o2.z : o2.x + o1.w;
+              const int e22 = o1.w < o2.w ? o1.y + o2.w : o2.y + o1.w;
+              const double x11 = M[e11], x12 = M[e12], x21 = M[e21], x22 = M[e22];
+              const double y11 = c2 * x11 - s2 * x12, y12 = s2 * x11 + c2 * x12;
+              const double y21 = c2 * x21 - s2 * x22, y22 = s2 * x21 + c2 * x22;
+              const double z11 = c1 * y11 - s1 * y21, z21 = s1 * y11 + c1 * y21;
+              const double z12 = c1 * y12 - s1 * y22, z22 = s1 * y12 + c1 * y22;
+              M[e11] = z11;
+              M[e12] = z12;
+              M[e21] = z21;
+              M[e22] = z22;
+            }
+            __syncwarp();
+            // next round's parameter loads (M is final for this round) ...
+            const PIn nxt = param_load(round + 1 < m - 1 ? round + 1 : 0);
+            // ... V' <- V' J.  Register rows: slot i's pair sits at positions
+            // (2i, 2i+1); afterwards every position moves one step along the
+            // fixed cycle 0 <- 2 <- ... <- RP-2 <- RP-1 <- RP-3 <- ... <- 3 <- 0
+            // (position 1, index RP-1, stays), which is how the round-robin's
+            // pairs advance, so the next round's pairs are again (2i, 2i+1) ...
+            if constexpr (kRegRows > 0) {
+  #pragma unroll
+              for (int i = 0; i < RP / 2; ++i) {
+                const double2 r = rot[i];
+                const double x0 = vreg[2 * i], y0 = vreg[2 * i + 1];
+                vreg[2 * i] = r.x * x0 - r.y * y0;
+                vreg[2 * i + 1] = r.y * x0 + r.x * y0;
+              }
+              const double t0 = vreg[0];
+  #pragma unroll
+              for (int l = 0; l < RP / 2 - 1; ++l) vreg[2 * l] = vreg[2 * l + 2];
+              vreg[RP - 2] = vreg[RP - 1];
+  #pragma unroll
+              for (int l = RP / 2 - 1; l >= 2; --l) vreg[2 * l + 1] = vreg[2 * l - 1];
+              vreg[3] = t0;
+            }
+            // ... shared-memory rows: p, q of V'^T (offset p LDV = p LDM + p) over
+            // this lane's column pairs, branch-free so the parameter tail interleaves ...
+  #pragma unroll
+            for (int j = 0; j < (kSmemKp > 0 ? kLaneVit : 0); ++j) {
+              const int v = lvit[j];
+              const int sl = v & 0xff, kc = (v >> 8) & 0xff;
+              const double2 r = rot[v < 0 ? 0 : sl];
+              const int4 o = ofs[v < 0 ? 0 : sl];
+              const bool on = v >= 0 && r.y != 0.0;
+              double2* vp = reinterpret_cast<double2*>(Vt + (on ? o.x + o.z + kc : 0));
+              double2* vq = reinterpret_cast<double2*>(Vt + (on ? o.y + o.w + kc : 0));
+              const double2 x = *vp, y = *vq;
+              if (on) {
+                *vp = make_double2(r.x * x.x - r.y * y.x, r.x * x.y - r.y * y.y);
+                *vq = make_double2(r.y * x.x + r.x * y.x, r.y * x.y + r.x * y.y);
+              }
+            }
+            // ... and the parameters into the other buffer
+            param_store(nxt, buf ^ 1, round + 1 < m - 1);
+            __syncwarp();
+          }
+        }
+        // register rows back (whole sweeps bring positions back to round-0 order)
+        if constexpr (kRegRows > 0) {
+          if (lane < R) {
+  #pragma unroll
+            for (int x = 0; x < RP; ++x) Vt[rr_l0(RP, x) * LDV + lane] = vreg[x];
+          }
           __syncwarp();
         }
-      }
-      // register rows back (whole sweeps bring positions back to round-0 order)
-      if constexpr (kRegRows > 0) {
-        if (lane < R) {
-#pragma unroll
-          for (int x = 0; x < RP; ++x) Vt[rr_l0(RP, x) * LDV + lane] = vreg[x];
-        }
-        __syncwarp();
       }
       if (a.dbg && lane == 0) {
         atomicAdd(a.dbg + 16 + min(sweeps, 9), 1);
@@ -568,7 +833,7 @@ __global__ void __launch_bounds__(LgWarp<RP>::WPB * 32, 1) k_procrustes_large_w(
       }
       // E <- E V'
       warp_mm<RP, EXACT>(
-          R, R, [&](int i, int c) { return Es[i * R + c]; }, [&](int c, int j) { return Vt[j * LDV + c]; },
+          R, R, [&](int i, int c) { return Es[i * R + c]; }, [&](int c, int j) { return Vx[j * LDVx + c]; },
           [&](int i, int j, double v) { Ns[i * R + j] = v; });
       __syncwarp();
       warp_copy(Es, Ns, RR, lane);
@@ -579,8 +844,8 @@ __global__ void __launch_bounds__(LgWarp<RP>::WPB * 32, 1) k_procrustes_large_w(
       }
       double smax2 = 0.0, smin2 = 1e308;
       for (int j = 0; j < R; ++j) {
-        smax2 = fmax(smax2, M[j * LDM + j]);
-        smin2 = fmin(smin2, M[j * LDM + j]);
+        smax2 = fmax(smax2, Mx[j * LDM + j]);
+        smin2 = fmin(smin2, Mx[j * LDM + j]);
       }
       if (!(smax2 > 0.0) || !(smin2 > kTinyL * smax2)) {
         flag = P2G_FLAG_ACCURATE;
@@ -589,7 +854,7 @@ __global__ void __launch_bounds__(LgWarp<RP>::WPB * 32, 1) k_procrustes_large_w(
       if (pass == 0 && off > 0.25 && smin2 < 1e-6 * smax2) continue;
       // S' = M'^{-1/2} (second order about the diagonal) into M
       for (int p = lane; p < R; p += 32) {
-        const double s = sqrt(M[p * LDM + p]);
+        const double s = sqrt(Mx[p * LDM + p]);
         sv[p] = s;
         u[p] = 1.0 / s;
       }
@@ -598,7 +863,7 @@ __global__ void __launch_bounds__(LgWarp<RP>::WPB * 32, 1) k_procrustes_large_w(
         const int p = e / R, q = e - p * R;
         const double P = 1.0 / (sv[p] + sv[q]);
         Ns[e] = P;
-        Ts[e] = p == q ? 0.0 : P * M[p < q ? p * LDM + q : q * LDM + p];
+        Ts[e] = p == q ? 0.0 : P * Mx[p < q ? p * LDM + q : q * LDM + p];
       }
       __syncwarp();
       {
@@ -630,7 +895,7 @@ __global__ void __launch_bounds__(LgWarp<RP>::WPB * 32, 1) k_procrustes_large_w(
               const int j = 8 * b + 2 * fk + h;
               if (EXACT || (i < R && j < R)) {
                 const double corr = c1[b][h] - Ts[i * R + j] + Ns[i * R + j] * c2[b][h];
-                M[i * LDM + j] = (i == j ? u[i] : 0.0) + u[i] * u[j] * corr;
+                Mx[i * LDM + j] = (i == j ? u[i] : 0.0) + u[i] * u[j] * corr;
               }
             }
         }
@@ -638,7 +903,7 @@ __global__ void __launch_bounds__(LgWarp<RP>::WPB * 32, 1) k_procrustes_large_w(
       __syncwarp();
       // Y = V' S' into Ns, Z = Y E'^T into Ts
       warp_mm<RP, EXACT>(
-          R, R, [&](int i, int c) { return Vt[c * LDV + i]; }, [&](int c, int j) { return M[c * LDM + j]; },
+          R, R, [&](int i, int c) { return Vx[c * LDVx + i]; }, [&](int c, int j) { return Mx[c * LDM + j]; },
           [&](int i, int j, double v) { Ns[i * R + j] = v; });
       __syncwarp();
       warp_mm<RP, EXACT>(
@@ -665,7 +930,7 @@ __global__ void __launch_bounds__(LgWarp<RP>::WPB * 32, 1) k_procrustes_large_w(
 
 template <int RP, bool EXACT>
 int launch_large_w(p2g_ctx* c, LgArgs a, int max_partials, cudaStream_t s) {
-  using L = LgWarp<RP>;
+  using L = LgWarp<RP, EXACT>;
   auto kern = k_procrustes_large_w<RP, EXACT>;
   P2G_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(L::kSmem)));
   const std::int64_t K = a.X.K;
