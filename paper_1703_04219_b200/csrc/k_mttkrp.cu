@@ -209,14 +209,23 @@ __global__ void __launch_bounds__(WPB * 32)
 // its own row (lane (fm, fk) holds row fm, columns 8b + 2fk + {0, 1} in the
 // C layout); the column sums over rows are a 3-step shuffle over fm.
 // Per subject: Q read once (coalesced 32-byte sectors), CSR streamed once,
-// V rows from L2.
+// V rows from L2.  The tile's CSR entries (a contiguous range: its 8 rows)
+// are first staged in shared memory with coalesced loads, so a lane's
+// gather chain is a shared-memory read followed by the V-row load, and kU
+// entries of its row are in flight at once (the kernel is bound by the
+// latency of this chain, not by L2 throughput).
 // ---------------------------------------------------------------------------
+constexpr int kM3Stage = 256;  // staged entries per warp (a tile holds ~70 at cfg4)
+
 template <int RP, int WPB>
 __global__ void __launch_bounds__(WPB * 32)
     k_mode3_mma(ShardArgs X, int R, const double* __restrict__ Q, const double* __restrict__ H,
                 const double* __restrict__ V, double* __restrict__ M3, double* __restrict__ XV) {
   constexpr int NB = RP / 8;
+  constexpr int kU = 4;  // entries of a row in flight per lane
   __shared__ double Hs[RP * RP];  // H zero-padded to RP x RP, row-major
+  __shared__ double vst[WPB][kM3Stage];
+  __shared__ std::int32_t cst[WPB][kM3Stage];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, fm = lane >> 2, fk = lane & 3;
   for (int e = threadIdx.x; e < RP * RP; e += blockDim.x) {
     const int a = e / RP, c = e - a * RP;
@@ -248,26 +257,51 @@ __global__ void __launch_bounds__(WPB * 32)
       double xv[NB][2];
 #pragma unroll
       for (int b = 0; b < NB; ++b) xv[b][0] = xv[b][1] = 0.0;
-      if (iv) {
-        const std::int64_t p0 = X.rp[r0 + i], p1 = X.rp[r0 + i + 1];
-#pragma unroll 2
-        for (std::int64_t p = p0; p < p1; ++p) {
-          const double v = __ldg(X.val + p);
-          const double* vr = V + static_cast<std::int64_t>(__ldg(X.ci + p)) * R;
+      const std::int64_t pa = X.rp[r0 + i0], pb = X.rp[r0 + min(i0 + 8, I)];
+      const std::int64_t p0 = iv ? X.rp[r0 + i] : pa, p1 = iv ? X.rp[r0 + i + 1] : pa;
+      for (std::int64_t cb = pa; cb < pb; cb += kM3Stage) {
+        const int nc = static_cast<int>(pb - cb < kM3Stage ? pb - cb : kM3Stage);
+        __syncwarp();
+        for (int t = lane; t < nc; t += 32) {
+          cst[wid][t] = __ldg(X.ci + cb + t);
+          vst[wid][t] = __ldg(X.val + cb + t);
+        }
+        __syncwarp();
+        const int q0 = static_cast<int>((p0 > cb ? p0 : cb) - cb), q1 = static_cast<int>((p1 < cb + nc ? p1 : cb + nc) - cb);
+        // kU entries at a time (the same per-row accumulation order as the
+        // other paths: entries ascending)
+        for (int q = q0; q < q1; q += kU) {
+          double v[kU];
+          const double* vr[kU];
 #pragma unroll
-          for (int b = 0; b < NB; ++b) {
-            const int c = 8 * b + 2 * fk;
-            if (even) {
-              if (c < R) {
-                const double2 y = __ldg(reinterpret_cast<const double2*>(vr + c));
-                xv[b][0] = fma(v, y.x, xv[b][0]);
-                xv[b][1] = fma(v, y.y, xv[b][1]);
-              }
-            } else {
-              if (c < R) xv[b][0] = fma(v, __ldg(vr + c), xv[b][0]);
-              if (c + 1 < R) xv[b][1] = fma(v, __ldg(vr + c + 1), xv[b][1]);
-            }
+          for (int u = 0; u < kU; ++u) {
+            const bool on = q + u < q1;
+            v[u] = on ? vst[wid][q + u] : 0.0;
+            vr[u] = V + static_cast<std::int64_t>(on ? cst[wid][q + u] : 0) * R;
           }
+          double2 y[kU][NB];
+#pragma unroll
+          for (int u = 0; u < kU; ++u)
+#pragma unroll
+            for (int b = 0; b < NB; ++b) {
+              const int c = 8 * b + 2 * fk;
+              if (even) {
+                y[u][b] = (c < R && q + u < q1) ? __ldg(reinterpret_cast<const double2*>(vr[u] + c))
+                                                : make_double2(0.0, 0.0);
+              } else {
+                y[u][b].x = (c < R && q + u < q1) ? __ldg(vr[u] + c) : 0.0;
+                y[u][b].y = (c + 1 < R && q + u < q1) ? __ldg(vr[u] + c + 1) : 0.0;
+              }
+            }
+#pragma unroll
+          for (int u = 0; u < kU; ++u)
+            if (q + u < q1) {
+#pragma unroll
+              for (int b = 0; b < NB; ++b) {
+                xv[b][0] = fma(v[u], y[u][b].x, xv[b][0]);
+                xv[b][1] = fma(v[u], y[u][b].y, xv[b][1]);
+              }
+            }
         }
       }
       if (XV && iv) {  // X_k V rows for the next Procrustes step (it would re-gather them)
