@@ -154,56 +154,57 @@ __global__ void __launch_bounds__(128) k_seg_spmm(int R, std::int64_t nseg, std:
 /// R > 16: warp per segment.  A U row (8 R bytes) is one coalesced load over
 /// the lanes (lane l: columns 2l, 2l + 1); the segment's entries are staged 32
 /// at a time in registers and broadcast by shuffles, 4 U rows in flight.
-/// Warps take segments s = w, w + W, ... (W resident-ish warps), so the warps
-/// in flight work inside a window of about W consecutive segments -- one or
-/// two row blocks of U (21 MB each at R = 40) -- which stay in L2.  Same
-/// per-segment accumulation order as k_seg_spmm (entries ascending).
+/// Warps claim chunks of kSegChunk consecutive segments from a counter, so
+/// the warps in flight always work near one frontier -- one or two row blocks
+/// of U (21 MB each at R = 40), which stay in L2.  (A static grid-stride
+/// drifts: warps that drew short segments run ahead, and the window spread
+/// over ~20 row blocks, re-reading U from DRAM 3x.)  Same per-segment
+/// accumulation order as k_seg_spmm (entries ascending).
+constexpr int kSegChunk = 1;
+
 template <int RP>
-__global__ void __launch_bounds__(256) k_seg_spmm_w(int R, std::int64_t nseg, std::int64_t n,
+__global__ void __launch_bounds__(256) k_seg_spmm_w(std::int64_t nseg, std::int64_t n,
                                                     const std::int64_t* __restrict__ seg_beg,
                                                     const std::int32_t* __restrict__ crow,
                                                     const double* __restrict__ cval, const double* __restrict__ U,
-                                                    double* __restrict__ partial) {
-  static_assert(RP <= 64, "two columns per lane");
+                                                    double* __restrict__ partial, unsigned long long* next) {
+  static_assert(RP % 2 == 0 && RP <= 64, "exact even R, two columns per lane");
   const int lane = threadIdx.x & 31;
   const int c = 2 * lane;
-  const bool cv0 = c < R, cv1 = c + 1 < R;
-  const std::int64_t nw = static_cast<std::int64_t>(gridDim.x) * (blockDim.x >> 5);
-  for (std::int64_t s = static_cast<std::int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5); s < nseg;
-       s += nw) {
-    const std::int64_t q0 = seg_beg[s], q1 = s + 1 < nseg ? seg_beg[s + 1] : n;
-    double a0 = 0.0, a1 = 0.0;
-    for (std::int64_t qb = q0; qb < q1; qb += 32) {
-      const int m = static_cast<int>(q1 - qb < 32 ? q1 - qb : 32);
-      const std::int32_t rr = lane < m ? __ldg(crow + qb + lane) : 0;
-      const double vv = lane < m ? __ldg(cval + qb + lane) : 0.0;
-      for (int t = 0; t < m; t += 4) {
-        double v[4];
-        double2 y[4];
+  const bool cv = c < RP;
+  while (true) {
+    unsigned long long s0 = 0;
+    if (lane == 0) s0 = atomicAdd(next, static_cast<unsigned long long>(kSegChunk));
+    s0 = __shfl_sync(dev::kFull, s0, 0);
+    if (s0 >= static_cast<unsigned long long>(nseg)) break;
+    const std::int64_t s1 = static_cast<std::int64_t>(s0) + kSegChunk < nseg ? static_cast<std::int64_t>(s0) + kSegChunk : nseg;
+    for (std::int64_t s = static_cast<std::int64_t>(s0); s < s1; ++s) {
+      const std::int64_t q0 = seg_beg[s], q1 = s + 1 < nseg ? seg_beg[s + 1] : n;
+      double a0 = 0.0, a1 = 0.0;
+      for (std::int64_t qb = q0; qb < q1; qb += 32) {
+        const int m = static_cast<int>(q1 - qb < 32 ? q1 - qb : 32);
+        const std::int32_t rr = lane < m ? __ldg(crow + qb + lane) : 0;
+        const double vv = lane < m ? __ldg(cval + qb + lane) : 0.0;
+        for (int t = 0; t < m; t += 4) {
+          double v[4];
+          double2 y[4];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int r = __shfl_sync(dev::kFull, rr, (t + u) & 31);
-          v[u] = __shfl_sync(dev::kFull, vv, (t + u) & 31);
-          const double* urow = U + static_cast<std::int64_t>(r) * R;
-          const bool on = t + u < m;
-          if ((R & 1) == 0) {
-            y[u] = (on && cv0) ? __ldg(reinterpret_cast<const double2*>(urow + c)) : make_double2(0.0, 0.0);
-          } else {
-            y[u].x = (on && cv0) ? __ldg(urow + c) : 0.0;
-            y[u].y = (on && cv1) ? __ldg(urow + c + 1) : 0.0;
+          for (int u = 0; u < 4; ++u) {
+            const int r = __shfl_sync(dev::kFull, rr, (t + u) & 31);
+            v[u] = t + u < m ? __shfl_sync(dev::kFull, vv, (t + u) & 31) : 0.0;
+            y[u] = cv ? __ldg(reinterpret_cast<const double2*>(U + static_cast<std::size_t>(r) * RP + c))
+                      : make_double2(0.0, 0.0);
           }
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (t + u < m) {
+              a0 = fma(v[u], y[u].x, a0);
+              a1 = fma(v[u], y[u].y, a1);
+            }
         }
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-          if (t + u < m) {
-            a0 = fma(v[u], y[u].x, a0);
-            a1 = fma(v[u], y[u].y, a1);
-          }
       }
+      if (cv) *reinterpret_cast<double2*>(partial + s * RP + c) = make_double2(a0, a1);
     }
-    double* out = partial + s * R;
-    if (cv0) out[c] = a0;
-    if (cv1) out[c + 1] = a1;
   }
 }
 
@@ -390,19 +391,20 @@ void sync_csc(p2g_ctx* c) {
 template <int RP>
 static void seg_spmm(p2g_ctx* c, int R, const double* U, cudaStream_t s) {
   if constexpr (RP > 16) {
-    // resident blocks only: the window of segments in flight is then the
-    // ~W segments the grid-stride visits (a queued block would own segments
-    // spread over the whole range)
-    int per_sm = 0;
-    P2G_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_seg_spmm_w<RP>, 256, 0));
-    const int blocks = static_cast<int>(std::max<std::int64_t>(
-        1, std::min<std::int64_t>((c->nseg + 7) / 8, static_cast<std::int64_t>(c->num_sms) * std::max(per_sm, 1))));
-    k_seg_spmm_w<RP><<<blocks, 256, 0, s>>>(R, c->nseg, c->nnz, c->seg_beg.get(), c->csc_row.get(),
-                                             c->csc_val.get(), U, c->seg_part.get());
-  } else {
-    k_seg_spmm<RP><<<grid_for(c->nseg, 128), 128, 0, s>>>(R, c->nseg, c->nnz, c->seg_beg.get(), c->csc_row.get(),
-                                                          c->csc_val.get(), U, c->seg_part.get());
+    if (R == RP) {  // exact R: constant strides (R = 24, 32, 40)
+      c->seg_next.resize(1);
+      P2G_CUDA(cudaMemsetAsync(c->seg_next.get(), 0, sizeof(unsigned long long), s));
+      int per_sm = 0;
+      P2G_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_seg_spmm_w<RP>, 256, 0));
+      const int blocks = static_cast<int>(std::max<std::int64_t>(
+          1, std::min<std::int64_t>((c->nseg + 7) / 8, static_cast<std::int64_t>(c->num_sms) * std::max(per_sm, 1))));
+      k_seg_spmm_w<RP><<<blocks, 256, 0, s>>>(c->nseg, c->nnz, c->seg_beg.get(), c->csc_row.get(), c->csc_val.get(),
+                                               U, c->seg_part.get(), c->seg_next.get());
+      return;
+    }
   }
+  k_seg_spmm<RP><<<grid_for(c->nseg, 128), 128, 0, s>>>(R, c->nseg, c->nnz, c->seg_beg.get(), c->csc_row.get(),
+                                                        c->csc_val.get(), U, c->seg_part.get());
 }
 
 void launch_csc_mode2(p2g_ctx* c, int R, const double* U, double* M2, cudaStream_t s) {

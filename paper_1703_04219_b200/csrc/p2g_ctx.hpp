@@ -146,6 +146,7 @@ struct p2g_ctx {
   p2g::DBuf<std::int64_t> col_ptr, seg_ptr, seg_beg, seg_end;
   p2g::DBuf<std::int32_t> csc_row, seg_ids;
   p2g::DBuf<double> csc_val, seg_part, Ubuf;
+  p2g::DBuf<unsigned long long> seg_next;  // R > 16 CSC SpMM: next unclaimed segment chunk
   std::int64_t nseg = 0;
   // The CSC build runs on `side` behind the load's upload (phase A: the big
   // sort, overlapping the first Procrustes step) and is finished at its first
