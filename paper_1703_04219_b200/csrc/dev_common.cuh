@@ -81,6 +81,12 @@ __device__ __forceinline__ uint4 lds128u(unsigned a) {
   asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a) : "memory");
   return v;
 }
+/// 32-byte read-only global load (sm_100: LDG.E.256).
+__device__ __forceinline__ double4 ldg256(const double* p) {
+  double4 v;
+  asm volatile("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];" : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w) : "l"(p));
+  return v;
+}
 /// The shared address of p, made warp-uniform (a uniform register).
 __device__ __forceinline__ unsigned smem_uniform(const void* p) {
   return __shfl_sync(kFull, static_cast<unsigned>(__cvta_generic_to_shared(p)), 0);

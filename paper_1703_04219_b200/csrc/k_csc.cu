@@ -151,59 +151,80 @@ __global__ void __launch_bounds__(128) k_seg_spmm(int R, std::int64_t nseg, std:
   }
 }
 
-/// R > 16: warp per segment.  A U row (8 R bytes) is one coalesced load over
-/// the lanes (lane l: columns 2l, 2l + 1); the segment's entries are staged 32
-/// at a time in registers and broadcast by shuffles, 4 U rows in flight.
-/// Warps claim chunks of kSegChunk consecutive segments from a counter, so
-/// the warps in flight always work near one frontier -- one or two row blocks
-/// of U (21 MB each at R = 40), which stay in L2.  (A static grid-stride
-/// drifts: warps that drew short segments run ahead, and the window spread
-/// over ~20 row blocks, re-reading U from DRAM 3x.)  Same per-segment
-/// accumulation order as k_seg_spmm (entries ascending).
-constexpr int kSegChunk = 1;
-
+/// R > 16 (exact R, R % 4 == 0): warp per segment.  A U row (8 R bytes) is
+/// read by R / 4 lanes with 32-byte loads, so three lane groups take three
+/// entries per warp instruction (entries t = g mod 3 to group g, 4 in flight
+/// per group); the segment's entries are staged 32 at a time in registers and
+/// broadcast by shuffles, and the three group sums are added in a fixed order
+/// at the end of the segment (deterministic).  Warps claim segments one at a
+/// time from a counter, so the warps in flight always work near one frontier
+/// -- one row block of U (21 MB at R = 40), which stays in L2.  (A static
+/// grid-stride drifts: warps that drew short segments run ahead, and the
+/// window spread over ~20 row blocks, re-reading U from DRAM 3x; claiming
+/// chunks of 16 segments widened it the same way.)
 template <int RP>
 __global__ void __launch_bounds__(256) k_seg_spmm_w(std::int64_t nseg, std::int64_t n,
                                                     const std::int64_t* __restrict__ seg_beg,
                                                     const std::int32_t* __restrict__ crow,
                                                     const double* __restrict__ cval, const double* __restrict__ U,
                                                     double* __restrict__ partial, unsigned long long* next) {
-  static_assert(RP % 2 == 0 && RP <= 64, "exact even R, two columns per lane");
+  constexpr int kL = RP / 4;     // lanes per U row
+  constexpr int kG = 32 / kL;    // entries per warp instruction
+  static_assert(RP % 4 == 0 && kL <= 32 && kG >= 1, "exact R, multiple of 4");
   const int lane = threadIdx.x & 31;
-  const int c = 2 * lane;
-  const bool cv = c < RP;
+  const int g = lane / kL, sub = lane - g * kL;
+  const bool act = g < kG;
+  const int c = 4 * sub;
   while (true) {
     unsigned long long s0 = 0;
-    if (lane == 0) s0 = atomicAdd(next, static_cast<unsigned long long>(kSegChunk));
+    if (lane == 0) s0 = atomicAdd(next, 1ull);
     s0 = __shfl_sync(dev::kFull, s0, 0);
     if (s0 >= static_cast<unsigned long long>(nseg)) break;
-    const std::int64_t s1 = static_cast<std::int64_t>(s0) + kSegChunk < nseg ? static_cast<std::int64_t>(s0) + kSegChunk : nseg;
-    for (std::int64_t s = static_cast<std::int64_t>(s0); s < s1; ++s) {
-      const std::int64_t q0 = seg_beg[s], q1 = s + 1 < nseg ? seg_beg[s + 1] : n;
-      double a0 = 0.0, a1 = 0.0;
-      for (std::int64_t qb = q0; qb < q1; qb += 32) {
-        const int m = static_cast<int>(q1 - qb < 32 ? q1 - qb : 32);
-        const std::int32_t rr = lane < m ? __ldg(crow + qb + lane) : 0;
-        const double vv = lane < m ? __ldg(cval + qb + lane) : 0.0;
-        for (int t = 0; t < m; t += 4) {
-          double v[4];
-          double2 y[4];
+    const std::int64_t s = static_cast<std::int64_t>(s0);
+    const std::int64_t q0 = seg_beg[s], q1 = s + 1 < nseg ? seg_beg[s + 1] : n;
+    double4 a = make_double4(0.0, 0.0, 0.0, 0.0);
+    for (std::int64_t qb = q0; qb < q1; qb += 32) {
+      const int m = static_cast<int>(q1 - qb < 32 ? q1 - qb : 32);
+      const std::int32_t rr = lane < m ? __ldg(crow + qb + lane) : 0;
+      const double vv = lane < m ? __ldg(cval + qb + lane) : 0.0;
+      for (int t0 = 0; t0 < m; t0 += 4 * kG) {
+        double v[4];
+        double4 y[4];
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const int r = __shfl_sync(dev::kFull, rr, (t + u) & 31);
-            v[u] = t + u < m ? __shfl_sync(dev::kFull, vv, (t + u) & 31) : 0.0;
-            y[u] = cv ? __ldg(reinterpret_cast<const double2*>(U + static_cast<std::size_t>(r) * RP + c))
-                      : make_double2(0.0, 0.0);
-          }
+        for (int u = 0; u < 4; ++u) {
+          const int t = t0 + kG * u + g;  // this group's entry
+          const int r = __shfl_sync(dev::kFull, rr, t & 31);
+          const double w = __shfl_sync(dev::kFull, vv, t & 31);
+          const bool on = act && t < m;
+          v[u] = on ? w : 0.0;
+          y[u] = on ? dev::ldg256(U + static_cast<std::size_t>(r) * RP + c) : make_double4(0.0, 0.0, 0.0, 0.0);
+        }
 #pragma unroll
-          for (int u = 0; u < 4; ++u)
-            if (t + u < m) {
-              a0 = fma(v[u], y[u].x, a0);
-              a1 = fma(v[u], y[u].y, a1);
-            }
+        for (int u = 0; u < 4; ++u) {
+          a.x = fma(v[u], y[u].x, a.x);
+          a.y = fma(v[u], y[u].y, a.y);
+          a.z = fma(v[u], y[u].z, a.z);
+          a.w = fma(v[u], y[u].w, a.w);
         }
       }
-      if (cv) *reinterpret_cast<double2*>(partial + s * RP + c) = make_double2(a0, a1);
+    }
+    // group sums in a fixed order: group 0 + group 1 + ... (lanes sub + kL g)
+#pragma unroll
+    for (int h = 1; h < kG; ++h) {
+      const int src = sub + kL * h;
+      const double bx = __shfl_sync(dev::kFull, a.x, src), by = __shfl_sync(dev::kFull, a.y, src);
+      const double bz = __shfl_sync(dev::kFull, a.z, src), bw = __shfl_sync(dev::kFull, a.w, src);
+      if (g == 0) {
+        a.x += bx;
+        a.y += by;
+        a.z += bz;
+        a.w += bw;
+      }
+    }
+    if (g == 0) {
+      double* o = partial + s * RP + c;
+      *reinterpret_cast<double2*>(o) = make_double2(a.x, a.y);
+      *reinterpret_cast<double2*>(o + 2) = make_double2(a.z, a.w);
     }
   }
 }
@@ -391,7 +412,7 @@ void sync_csc(p2g_ctx* c) {
 template <int RP>
 static void seg_spmm(p2g_ctx* c, int R, const double* U, cudaStream_t s) {
   if constexpr (RP > 16) {
-    if (R == RP) {  // exact R: constant strides (R = 24, 32, 40)
+    if (R == RP) {  // exact R: constant strides, 32-byte row loads (R = 24, 32, 40)
       c->seg_next.resize(1);
       P2G_CUDA(cudaMemsetAsync(c->seg_next.get(), 0, sizeof(unsigned long long), s));
       int per_sm = 0;
