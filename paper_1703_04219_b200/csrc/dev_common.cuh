@@ -87,6 +87,10 @@ __device__ __forceinline__ double4 ldg256(const double* p) {
   asm volatile("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];" : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w) : "l"(p));
   return v;
 }
+/// 32-byte global store (sm_100: STG.E.256).
+__device__ __forceinline__ void stg256(double* p, double4 v) {
+  asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(v.x), "d"(v.y), "d"(v.z), "d"(v.w) : "memory");
+}
 /// The shared address of p, made warp-uniform (a uniform register).
 __device__ __forceinline__ unsigned smem_uniform(const void* p) {
   return __shfl_sync(kFull, static_cast<unsigned>(__cvta_generic_to_shared(p)), 0);

@@ -338,6 +338,116 @@ __global__ void __launch_bounds__(WPB * 32)
 }
 
 // ---------------------------------------------------------------------------
+// mode 3 for exact R in {24, 32, 40} (the fused loop's R > 16 path): warp per
+// subject in two phases.
+//  A. X_k V rows: kG = 32 / (R / 4) lane groups take kG rows at a time; a
+//     group reads a V row with R / 4 lanes of 32-byte loads (one row per
+//     group per instruction, 4 entries in flight).  The rows' CSR entries are
+//     staged 32 at a time in registers (coalesced) and broadcast by shuffles.
+//     Each row is written to XV (the next Procrustes step reads it) with
+//     32-byte stores.  Per-row accumulation order: entries ascending, as in
+//     the other paths.
+//  B. 8-row tiles of P = Q_k H (DMMA; Q fragments from HBM, H from shared
+//     memory) meet the matching fragment of the X_k V rows just written
+//     (L2-resident), and m3 = column sums of P o X_k V (3-step shuffle over
+//     the tile's rows), in the same order as k_mode3_mma.
+// ---------------------------------------------------------------------------
+template <int RP, int WPB>
+__global__ void __launch_bounds__(WPB * 32)
+    k_mode3_rows(ShardArgs X, const double* __restrict__ Q, const double* __restrict__ H,
+                 const double* __restrict__ V, double* __restrict__ M3, double* __restrict__ XV) {
+  constexpr int NB = RP / 8;
+  constexpr int kL = RP / 4, kG = 32 / kL;
+  static_assert(RP % 8 == 0, "exact R, multiple of 8");
+  __shared__ double Hs[RP * RP];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, fm = lane >> 2, fk = lane & 3;
+  const int g = lane / kL, sub = lane - g * kL;
+  const bool act = g < kG;
+  for (int e = threadIdx.x; e < RP * RP; e += blockDim.x) Hs[e] = H[e];
+  __syncthreads();
+  const std::int64_t nwarps = static_cast<std::int64_t>(gridDim.x) * WPB;
+  for (std::int64_t k = static_cast<std::int64_t>(blockIdx.x) * WPB + wid; k < X.K; k += nwarps) {
+    const std::int64_t r0 = X.srp[k];
+    const int I = static_cast<int>(X.srp[k + 1] - r0);
+    // A: X_k V rows
+    for (int i0 = 0; i0 < I; i0 += kG) {
+      const int i = i0 + g;
+      const bool iv = act && i < I;
+      const std::int64_t pa = X.rp[r0 + i0], pb = X.rp[r0 + (i0 + kG < I ? i0 + kG : I)];
+      const std::int64_t p0 = iv ? X.rp[r0 + i] : pa, p1 = iv ? X.rp[r0 + i + 1] : pa;
+      double4 acc = make_double4(0.0, 0.0, 0.0, 0.0);
+      for (std::int64_t cb = pa; cb < pb; cb += 32) {
+        const int m = static_cast<int>(pb - cb < 32 ? pb - cb : 32);
+        const std::int32_t cc = lane < m ? __ldg(X.ci + cb + lane) : 0;
+        const double vv = lane < m ? __ldg(X.val + cb + lane) : 0.0;
+        const int t0 = static_cast<int>((p0 > cb ? p0 : cb) - cb);
+        const int n = static_cast<int>((p1 < cb + m ? p1 : cb + m) - cb) - t0;
+        const int nmax = __reduce_max_sync(dev::kFull, n > 0 ? n : 0);
+        for (int u = 0; u < nmax; u += 4) {
+          double w[4];
+          double4 y[4];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const int t = t0 + u + j;
+            const int col = __shfl_sync(dev::kFull, cc, t & 31);
+            const double vj = __shfl_sync(dev::kFull, vv, t & 31);
+            const bool on = u + j < n;
+            w[j] = on ? vj : 0.0;
+            y[j] = on ? dev::ldg256(V + static_cast<std::size_t>(col) * RP + 4 * sub)
+                      : make_double4(0.0, 0.0, 0.0, 0.0);
+          }
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            if (u + j < n) {
+              acc.x = fma(w[j], y[j].x, acc.x);
+              acc.y = fma(w[j], y[j].y, acc.y);
+              acc.z = fma(w[j], y[j].z, acc.z);
+              acc.w = fma(w[j], y[j].w, acc.w);
+            }
+        }
+      }
+      if (iv) dev::stg256(XV + (r0 + i) * RP + 4 * sub, acc);
+    }
+    __syncwarp();
+    // B: m3 from P = Q_k H and the X_k V rows
+    double m3p[NB][2];
+#pragma unroll
+    for (int b = 0; b < NB; ++b) m3p[b][0] = m3p[b][1] = 0.0;
+    for (int i0 = 0; i0 < I; i0 += 8) {
+      const int i = i0 + fm;
+      const bool iv = i < I;
+      const double* qrow = Q + (r0 + i) * RP;
+      double acc[NB][2];
+#pragma unroll
+      for (int b = 0; b < NB; ++b) acc[b][0] = acc[b][1] = 0.0;
+#pragma unroll
+      for (int k4 = 0; k4 < RP; k4 += 4) {
+        const double x = iv ? __ldg(qrow + k4 + fk) : 0.0;
+#pragma unroll
+        for (int b = 0; b < NB; ++b) dev::dmma884(acc[b], x, Hs[(k4 + fk) * RP + 8 * b + fm]);
+      }
+      const double* xr = XV + (r0 + i) * RP;
+#pragma unroll
+      for (int b = 0; b < NB; ++b) {
+        const double2 xv = iv ? *reinterpret_cast<const double2*>(xr + 8 * b + 2 * fk) : make_double2(0.0, 0.0);
+        m3p[b][0] = fma(acc[b][0], xv.x, m3p[b][0]);
+        m3p[b][1] = fma(acc[b][1], xv.y, m3p[b][1]);
+      }
+    }
+#pragma unroll
+    for (int b = 0; b < NB; ++b)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        double t = m3p[b][h];
+        t += __shfl_xor_sync(dev::kFull, t, 4);
+        t += __shfl_xor_sync(dev::kFull, t, 8);
+        t += __shfl_xor_sync(dev::kFull, t, 16);
+        if (fm == 0) M3[k * RP + 8 * b + 2 * fk + h] = t;
+      }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // mode 1 from a given Q (the p2g_mttkrp_q hook; the fused loop gets M1 from
 // K1): m1 += Q_k^T (XV o W_k) through 32-row chunks.
 // ---------------------------------------------------------------------------
@@ -607,6 +717,22 @@ void launch_mode3(p2g_ctx* c, int R, const double* Q, const double* H, const dou
   const ShardArgs X = shard_args(c);
   if (R > 16) {  // the row-per-lane form spills above R = 16
     constexpr int WPB = 8;
+    if (XV_out && (R == 24 || R == 32 || R == 40)) {  // the fused loop: X V rows kept for Procrustes
+      // resident blocks only (the subjects are split statically over the grid)
+      auto run = [&](auto kern) {
+        int per_sm = 0;
+        P2G_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, WPB * 32, 0));
+        kern<<<grid_for(X.K, WPB, c->num_sms, std::max(per_sm, 1)), WPB * 32, 0, s>>>(X, Q, H, V, m3, XV_out);
+      };
+      if (R == 24)
+        run(k_mode3_rows<24, WPB>);
+      else if (R == 32)
+        run(k_mode3_rows<32, WPB>);
+      else
+        run(k_mode3_rows<40, WPB>);
+      P2G_LAUNCHED(1);
+      return;
+    }
     if (R <= 24)
       k_mode3_mma<24, WPB><<<grid_for(X.K, WPB, c->num_sms, 4), WPB * 32, 0, s>>>(X, R, Q, H, V, m3, XV_out);
     else if (R <= 32)
