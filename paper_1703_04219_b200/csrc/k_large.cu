@@ -110,6 +110,7 @@ struct LgWarp {
   static constexpr int NB = RP / 8;  // 8-wide tensor tiles (RP multiple of 8)
   // per-warp global slab: B, X~ (max_rows x R each), T, F, E, N, M1 (R x R), s (R)
   __host__ __device__ static std::size_t slab_doubles(std::int64_t max_rows, int R) {
+    if (kPhys) return 5 * static_cast<std::size_t>(R) * R + RP;  // R x R only: the rows are streamed
     return 2 * static_cast<std::size_t>(max_rows > 1 ? max_rows : 1) * R +
            5 * static_cast<std::size_t>(R) * R + RP;
   }
@@ -268,159 +269,121 @@ __global__ void __launch_bounds__(LgWarp<RP>::WPB * 32, 1) k_procrustes_large_w(
   const std::int64_t gw = static_cast<std::int64_t>(blockIdx.x) * WPB + wid;
   const std::int64_t nwarps = static_cast<std::int64_t>(gridDim.x) * WPB;
   double* slab = a.slab + gw * L::slab_doubles(a.max_rows, R);
-  double* Bs = slab;                  // I x R rows of B = X~ H^T E
-  double* Xs = Bs + a.max_rows * R;   // I x R rows of X~ = X V D
-  double* Ts = Xs + a.max_rows * R;   // H^T E; later A = P o N; later Z
-  double* Fs = Ts + RR;               // F = B^T X~
-  double* Es = Fs + RR;               // E (R x R)
-  double* Ns = Es + RR;               // scratch: E V', P, V' S'
-  double* M1 = Ns + RR;               // this warp's m1 partial
-  double* sv = M1 + RR;               // sqrt(M'_pp)
-  for (int e = lane; e < RR; e += 32) M1[e] = 0.0;
-  for (std::int64_t k = gw; k < a.X.K; k += nwarps) {
-    const std::int64_t r0 = a.X.srp[k];
-    const int I = static_cast<int>(a.X.srp[k + 1] - r0);
-    for (int r = lane; r < R; r += 32) w[r] = a.W[k * R + r];
-    double* Ek = a.Ewarm + k * RR;
-    if (a.ew_valid)
-      warp_copy(Es, Ek, RR, lane);
-    else
-      for (int e = lane; e < RR; e += 32) Es[e] = (e / R == e % R) ? 1.0 : 0.0;
-    __syncwarp();
-    // rows of X~ = X_k V D: from the previous mode-3 pass's X V rows when
-    // available (a coalesced copy), else gathered (lane per row)
-    if (a.XV) {  // 8 loads in flight per lane before the stores (they would alias)
-      const double* xs = a.XV + r0 * R;
-      const int n = I * R;
-      for (int e0 = 0; e0 < n; e0 += 256) {
-        double t[8];
+  if constexpr (kPhys) {
+    // Exact R = 40.  X~ = X_k V D is streamed in 8-row tiles from the X V rows
+    // of the last mode-3 pass (a.XV, always given): B = X~ T' is formed tile
+    // by tile and only its Gram M = B^T B is kept; after the sweeps
+    // Q = X~ W with W = T' Z (Z = V' S' E'^T) and m1 += Q^T X~ (= Z^T B^T X~),
+    // again tile by tile.  No I x R slab: the per-warp scratch is R x R only
+    // (E, T', two scratch matrices, the m1 partial), and the tiles live in
+    // the warp's shared memory (8 x 41 staging, T' and W at row stride 41).
+    constexpr int LDS = LDM;
+    double* const Es = slab;       // E (R x R): warm start in, V_A out
+    double* const Ts = Es + RR;    // T' = H^T E
+    double* const Ns = Ts + RR;    // scratch: E V', P, V' S'
+    double* const As = Ns + RR;    // scratch: A = P o N, Z
+    double* const M1 = As + RR;    // this warp's m1 partial
+    double* const sv = M1 + RR;    // sqrt(M'_pp)
+    double* const Ms0 = M;         // shared buffer 0 (the M region)
+    double* const Ms1 = M + L::kMat;  // shared buffer 1 (the V'^T region)
+    for (int e = lane; e < RR; e += 32) M1[e] = 0.0;
+    const int fm = lane >> 2, fk = lane & 3, fn = 2 * (lane & 3);
+    for (std::int64_t k = gw; k < a.X.K; k += nwarps) {
+      const std::int64_t r0 = a.X.srp[k];
+      const int I = static_cast<int>(a.X.srp[k + 1] - r0);
+      for (int r = lane; r < RP; r += 32) w[r] = a.W[k * RP + r];
+      double* Ek = a.Ewarm + k * RR;
+      if (a.ew_valid)
+        warp_copy(Es, Ek, RR, lane);
+      else
+        for (int e = lane; e < RR; e += 32) Es[e] = (e / RP == e % RP) ? 1.0 : 0.0;
+      const double* xvk = a.XV + r0 * RP;
+      int flag = P2G_FLAG_FULL_RANK;
+      for (int pass = 0; pass < 2; ++pass) {
+        __syncwarp();
+        // T' = H^T E into the slab and shared buffer 1
+        warp_mm<RP, true>(
+            RP, RP, [&](int i, int c) { return __ldg(a.H + c * RP + i); }, [&](int c, int j) { return Es[c * RP + j]; },
+            [&](int i, int j, double v) {
+              Ts[i * RP + j] = v;
+              Ms1[i * LDS + j] = v;
+            });
+        __syncwarp();
+        // M = B^T B over 8-row tiles of B = X~ T' (tiles staged in buffer 0)
+        bool finite = true;
+        {
+          double accM[NB * (NB + 1) / 2][2];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const int e = e0 + lane + 32 * u;
-          t[u] = e < n ? __ldg(xs + e) : 0.0;
-        }
+          for (int t = 0; t < NB * (NB + 1) / 2; ++t) accM[t][0] = accM[t][1] = 0.0;
+          for (int i0 = 0; i0 < I; i0 += 8) {
+            const int i = i0 + fm;
+            const bool iv = i < I;
+            const double* xr = xvk + static_cast<std::int64_t>(i) * RP;
+            double accB[NB][2];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const int e = e0 + lane + 32 * u;
-          if (e < n) Xs[e] = t[u] * w[e % R];
-        }
-      }
-    } else
-    for (int i = lane; i < I; i += 32) {
-      double xv[RP];
-      dev::csr_row_times<RP>(xv, a.X.ci, a.X.val, a.X.rp[r0 + i], a.X.rp[r0 + i + 1], a.V, R);
-      double* xrow = Xs + static_cast<std::int64_t>(i) * R;
+            for (int b = 0; b < NB; ++b) accB[b][0] = accB[b][1] = 0.0;
 #pragma unroll
-      for (int c = 0; c < RP; ++c)
-        if (c < R) xrow[c] = xv[c] * w[c];
-    }
-    int flag = P2G_FLAG_FULL_RANK;
-    for (int pass = 0; pass < 2; ++pass) {
-      __syncwarp();
-      // T' = H^T E, then B = X~ T' (= X_k V D H^T E)
-      warp_mm<RP, EXACT>(
-          R, R, [&](int i, int c) { return __ldg(a.H + c * R + i); }, [&](int c, int j) { return Es[c * R + j]; },
-          [&](int i, int j, double v) { Ts[i * R + j] = v; });
-      __syncwarp();
-      warp_mm<RP, EXACT>(
-          I, R, [&](int i, int c) { return Xs[i * R + c]; }, [&](int c, int j) { return Ts[c * R + j]; },
-          [&](int i, int j, double v) { Bs[i * R + j] = v; });
-      __syncwarp();
-      // M = B^T B (lower tiles) into shared memory, F = B^T X~ into the slab
-      bool finite = true;
-      {
-        const int fm = lane >> 2, fk = lane & 3, fn = 2 * (lane & 3);
-        double acc[NB * (NB + 1) / 2][2];
+            for (int k4 = 0; k4 < RP; k4 += 4) {
+              const double x = iv ? __ldg(xr + k4 + fk) * w[k4 + fk] : 0.0;
 #pragma unroll
-        for (int t = 0; t < NB * (NB + 1) / 2; ++t) acc[t][0] = acc[t][1] = 0.0;
-        for (int k4 = 0; k4 < I; k4 += 4) {
-          const int r = k4 + fk;
-          double f[NB];
+              for (int b = 0; b < NB; ++b) dev::dmma884(accB[b], x, Ms1[(k4 + fk) * LDS + 8 * b + fm]);
+            }
+            __syncwarp();
 #pragma unroll
-          for (int b = 0; b < NB; ++b) {
-            const int col = 8 * b + fm;
-            f[b] = (r < I && (EXACT || col < R)) ? Bs[static_cast<std::int64_t>(r) * R + col] : 0.0;
+            for (int b = 0; b < NB; ++b) {
+              Ms0[fm * LDS + 8 * b + fn] = accB[b][0];
+              Ms0[fm * LDS + 8 * b + fn + 1] = accB[b][1];
+            }
+            __syncwarp();
+#pragma unroll
+            for (int kk = 0; kk < 8; kk += 4) {
+              double f[NB];
+#pragma unroll
+              for (int b = 0; b < NB; ++b) f[b] = Ms0[(kk + fk) * LDS + 8 * b + fm];
+              int t = 0;
+#pragma unroll
+              for (int bi = 0; bi < NB; ++bi)
+#pragma unroll
+                for (int bj = 0; bj <= bi; ++bj) dev::dmma884(accM[t++], f[bi], f[bj]);
+            }
           }
+          __syncwarp();
+          // the upper triangle in physical (round-0) order into buffer 0:
+          // logical l sits at position 2l (l < 20), 2 (39 - l) + 1 (l >= 20; 39 -> 1)
           int t = 0;
 #pragma unroll
           for (int bi = 0; bi < NB; ++bi)
 #pragma unroll
-            for (int bj = 0; bj <= bi; ++bj) dev::dmma884(acc[t++], f[bi], f[bj]);
-        }
-        int t = 0;
+            for (int bj = 0; bj <= bi; ++bj, ++t) {
+              const int i = 8 * bi + fm;
 #pragma unroll
-        for (int bi = 0; bi < NB; ++bi)
-#pragma unroll
-          for (int bj = 0; bj <= bi; ++bj, ++t) {
-            const int i = 8 * bi + fm;
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-              const int j = 8 * bj + fn + h;
-              if constexpr (kPhys) {
-                // upper triangle in physical (round-0) order: logical l sits at
-                // position 2l (l < 20), 2 (39 - l) + 1 (l >= 20; 39 -> 1)
+              for (int h = 0; h < 2; ++h) {
+                const int j = 8 * bj + fn + h;
                 if (bi > bj || i <= j) {
                   const int xi = i == 39 ? 1 : (i < 20 ? 2 * i : 2 * (39 - i) + 1);
                   const int xj = j == 39 ? 1 : (j < 20 ? 2 * j : 2 * (39 - j) + 1);
                   const int x = min(xi, xj), y = max(xi, xj);
                   const int c = y + prot[x];
-                  M[LDP * x + (c >= LDP ? c - LDP : c)] = acc[t][h];
+                  M[LDP * x + (c >= LDP ? c - LDP : c)] = accM[t][h];
                 }
-                finite &= isfinite(acc[t][h]);
-              } else if (EXACT || (i < R && j < R)) {
-                M[i * LDM + j] = acc[t][h];
-                M[j * LDM + i] = acc[t][h];
-                finite &= isfinite(acc[t][h]);
+                finite &= isfinite(accM[t][h]);
               }
             }
-          }
-      }
-      {
-        const int fm = lane >> 2, fk = lane & 3, fn = 2 * (lane & 3);
-#pragma unroll 1
-        for (int bi = 0; bi < NB; ++bi) {
-          double acc[NB][2];
-#pragma unroll
-          for (int bj = 0; bj < NB; ++bj) acc[bj][0] = acc[bj][1] = 0.0;
-          for (int k4 = 0; k4 < I; k4 += 4) {
-            const int r = k4 + fk;
-            const int ci = 8 * bi + fm;
-            const double fa = (r < I && (EXACT || ci < R)) ? Bs[static_cast<std::int64_t>(r) * R + ci] : 0.0;
-#pragma unroll
-            for (int bj = 0; bj < NB; ++bj) {
-              const int cj = 8 * bj + fm;
-              const double fb = (r < I && (EXACT || cj < R)) ? Xs[static_cast<std::int64_t>(r) * R + cj] : 0.0;
-              dev::dmma884(acc[bj], fa, fb);
-            }
-          }
-#pragma unroll
-          for (int bj = 0; bj < NB; ++bj) {
-            const int i = 8 * bi + fm;
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-              const int j = 8 * bj + fn + h;
-              if (EXACT || (i < R && j < R)) {
-                Fs[i * R + j] = acc[bj][h];
-                finite &= isfinite(acc[bj][h]);
-              }
-            }
-          }
         }
-      }
-      finite = __all_sync(dev::kFull, finite);
-      __syncwarp();
-      if (!finite) {  // the accurate path re-checks the operand; no preconditioner from here
-        for (int e = lane; e < RR; e += 32) Es[e] = (e / R == e % R) ? 1.0 : 0.0;
+        finite = __all_sync(dev::kFull, finite);
         __syncwarp();
-        flag = P2G_FLAG_ACCURATE;
-        break;
-      }
-      bool converged = false;
-      int sweeps = 0;
-      double off = 0.0;  // scaled off-diagonal mass at the start of the pass
-      double* Mx = M;    // after the sweeps: M' (logical order, full)
-      double* Vx = Vt;   // and V'^T (Vx[p * LDVx + k] = V'(k, p))
-      if constexpr (kPhys) {
+        if (!finite) {  // the accurate path re-checks the operand; no preconditioner from here
+          for (int e = lane; e < RR; e += 32) Es[e] = (e / RP == e % RP) ? 1.0 : 0.0;
+          __syncwarp();
+          flag = P2G_FLAG_ACCURATE;
+          break;
+        }
+        bool converged = false;
+        int sweeps = 0;
+        double off = 0.0;  // scaled off-diagonal mass at the start of the pass
+        double* Mx = M;    // after the sweeps: M' (logical order, full)
+        double* Vx = Vt;   // and V'^T (Vx[p * LDVx + k] = V'(k, p))
+        {
         // Physical-order round (jacobi_plan40.inc): slot i's
         // pair sits at positions (2i, 2i + 1) of M, V' rows and V' row chunks;
         // after each round every position's content moves one step along the
@@ -642,189 +605,487 @@ __global__ void __launch_bounds__(LgWarp<RP>::WPB * 32, 1) k_procrustes_large_w(
           Mx = Ml;
           Vx = V2;
         }
-      } else {
-      // V' = I; row `lane` of V' also in registers, in round-0 physical order
-        for (int e = lane; e < R * LDV; e += 32) {
-          const int p = e / LDV, kk = e - p * LDV;
-          Vt[e] = p == kk ? 1.0 : 0.0;
         }
-        double vreg[kRegRows > 0 ? RP : 1];
-  #pragma unroll
-        for (int x = 0; x < (kRegRows > 0 ? RP : 1); ++x) vreg[x] = rr_l0(RP, x) == lane ? 1.0 : 0.0;
-        for (int sweep = 0; sweep < kLgMaxSweeps; ++sweep, ++sweeps) {
-          double dmax = 0.0;
-          for (int j = 0; j < R; ++j) dmax = fmax(dmax, M[j * LDM + j]);
-          const double tiny = kTinyL * dmax;
-          for (int p = lane; p < R; p += 32) {
-            const double d = M[p * LDM + p];
-            u[p] = d > tiny ? 1.0 / sqrt(d) : 0.0;
-          }
-          __syncwarp();
-          double omax = 0.0, osum = 0.0;
-          for (int e = lane; e < RR; e += 32) {
-            const int p = e / R, q = e - p * R;
-            const double x = M[p < q ? p * LDM + q : q * LDM + p] * u[p] * u[q];
-            if (p != q) {
-              omax = fmax(omax, fabs(x));
-              osum = fma(x, x, osum);
-            }
-          }
-          omax = dev::warp_max(omax);
-          if (sweep == 0) {
-            off = dev::warp_sum(osum);
-            if (a.dbg && lane == 0) {
-              const int b = omax <= 0.0 ? 0 : min(9, max(0, static_cast<int>(floor(log10(omax))) + 9));
-              atomicAdd(a.dbg + 4 + b, 1);
-            }
-          }
-          if (omax <= kTauL) {
-            converged = true;
-            break;
-          }
-          // Rotation parameters of one round's slot (lanes < half store them).
-          // Split into the shared-memory loads and a pure-ALU tail, so that the
-          // tail of round r + 1 can be scheduled among round r's V' updates.
-          struct PIn {
-            double al, be, ga;
-            int p, q;
-          };
-          auto param_load = [&](int round) {
-            PIn in;
-            const int pq = sched[round * half + (lane < half ? lane : 0)];
-            in.p = pq & 0xff;
-            in.q = pq >> 8;
-            const int qq = in.q != 0xff ? in.q : in.p;
-            in.al = M[in.p * LDM + in.p];
-            in.be = M[qq * LDM + qq];
-            in.ga = in.q != 0xff ? M[in.p < qq ? in.p * LDM + qq : qq * LDM + in.p] : 0.0;
-            return in;
-          };
-          auto param_store = [&](const PIn& in, int buf, bool diag) {
-            const bool on = in.q != 0xff && in.al > tiny && in.be > tiny &&
-                            in.ga * in.ga > (kSkipL * kSkipL) * (in.al * in.be);
-            // t = sign(zeta) / (|zeta| + sqrt(1 + zeta^2)), zeta = (be - al) / (2 ga),
-            // without divisions: t = sign(d) 2ga / (|d| + sqrt(d^2 + 4ga^2))
-            const double d = in.be - in.al, g2 = 2.0 * in.ga;
-            const double h = on ? fma(d, d, g2 * g2) : 1.0;
-            const double rh = h * dev::rsqrt_nr(h);
-            const double tt = on ? (d >= 0.0 ? g2 : -g2) * dev::rcp_nr(fabs(d) + rh) : 0.0;
-            const double c = on ? dev::rsqrt_nr(fma(tt, tt, 1.0)) : 1.0;
-            if (lane < half) {
-              // the slot's own 2 x 2 block (M_pp, M_qq, M_pq) is updated here, by
-              // the lane that holds its old values: no other block of the round
-              // touches these entries, and the next parameter load follows the
-              // round's block updates
-              if (on && diag) {  // (not for the wrapped-around load of the sweep's last round)
-                const double dt = __dmul_rn(tt, in.ga);
-                M[in.p * LDM + in.p] = in.al - dt;
-                M[in.q * LDM + in.q] = in.be + dt;
-                M[in.p < in.q ? in.p * LDM + in.q : in.q * LDM + in.p] = 0.0;
-              }
-              rotb[buf * (RP / 2) + lane] = make_double2(c, c * tt);
-              rtb[buf * (RP / 2) + lane] = tt * in.ga;
-              ofsb[buf * (RP / 2) + lane] = in.q != 0xff ? make_int4(in.p * LDM, in.q * LDM, in.p, in.q)
-                                                        : make_int4(in.p * LDM, -1, in.p, -1);
-            }
-          };
-          param_store(param_load(0), 0, true);
-          __syncwarp();
-          for (int round = 0; round < m - 1; ++round) {
-            const int buf = round & 1;
-            const double2* rot = rotb + buf * (RP / 2);
-            const int4* ofs = ofsb + buf * (RP / 2);
-            // M <- J^T M J over this lane's 2 x 2 blocks of slot pairs
-  #pragma unroll
-            for (int j = 0; j < kLaneBlk; ++j) {
-              const int b = lblk[j];
-              if (b < 0) continue;
-              const int i1 = b & 0xff, i2 = b >> 8;
-              const double2 r1 = rot[i1], r2 = rot[i2];
-              if (r1.y == 0.0 && r2.y == 0.0) continue;
-              const int4 o1 = ofs[i1], o2 = ofs[i2];
-              if (!EXACT && (o1.w < 0 || o2.w < 0)) {  // odd R: 1 x 2 block against the dummy slot's index
-                const bool d1 = o1.w < 0;
-                const int ar = d1 ? o1.x : o2.x, ac = d1 ? o1.z : o2.z;  // the single index (row / column offsets)
-                const int ur = d1 ? o2.x : o1.x, uc = d1 ? o2.z : o1.z;
-                const int vr = d1 ? o2.y : o1.y, vc = d1 ? o2.w : o1.w;
-                const double cc = d1 ? r2.x : r1.x, ss = d1 ? r2.y : r1.y;
-                const int au = ac < uc ? ar + uc : ur + ac, av = ac < vc ? ar + vc : vr + ac;
-                const double xu = M[au], xv = M[av];
-                M[au] = cc * xu - ss * xv;
-                M[av] = ss * xu + cc * xv;
-                continue;
-              }
-              const double c1 = r1.x, s1 = r1.y, c2 = r2.x, s2 = r2.y;
-              // upper-triangle (canonical) addresses: row index < column index
-              const int e11 = o1.z < o2.z ? o1.x + o2.z : o2.x + o1.z;
-              const int e12 = o1.z < o2.w ? o1.x + o2.w : o2.y + o1.z;
-              const int e21 = o1.w < o2.z ? o1.y + o2.z : o2.x + o1.w;
-              const int e22 = o1.w < o2.w ? o1.y + o2.w : o2.y + o1.w;
-              const double x11 = M[e11], x12 = M[e12], x21 = M[e21], x22 = M[e22];
-              const double y11 = c2 * x11 - s2 * x12, y12 = s2 * x11 + c2 * x12;
-              const double y21 = c2 * x21 - s2 * x22, y22 = s2 * x21 + c2 * x22;
-              const double z11 = c1 * y11 - s1 * y21, z21 = s1 * y11 + c1 * y21;
-              const double z12 = c1 * y12 - s1 * y22, z22 = s1 * y12 + c1 * y22;
-              M[e11] = z11;
-              M[e12] = z12;
-              M[e21] = z21;
-              M[e22] = z22;
-            }
-            __syncwarp();
-            // next round's parameter loads (M is final for this round) ...
-            const PIn nxt = param_load(round + 1 < m - 1 ? round + 1 : 0);
-            // ... V' <- V' J.  Register rows: slot i's pair sits at positions
-            // (2i, 2i+1); afterwards every position moves one step along the
-            // fixed cycle 0 <- 2 <- ... <- RP-2 <- RP-1 <- RP-3 <- ... <- 3 <- 0
-            // (position 1, index RP-1, stays), which is how the round-robin's
-            // pairs advance, so the next round's pairs are again (2i, 2i+1) ...
-            if constexpr (kRegRows > 0) {
-  #pragma unroll
-              for (int i = 0; i < RP / 2; ++i) {
-                const double2 r = rot[i];
-                const double x0 = vreg[2 * i], y0 = vreg[2 * i + 1];
-                vreg[2 * i] = r.x * x0 - r.y * y0;
-                vreg[2 * i + 1] = r.y * x0 + r.x * y0;
-              }
-              const double t0 = vreg[0];
-  #pragma unroll
-              for (int l = 0; l < RP / 2 - 1; ++l) vreg[2 * l] = vreg[2 * l + 2];
-              vreg[RP - 2] = vreg[RP - 1];
-  #pragma unroll
-              for (int l = RP / 2 - 1; l >= 2; --l) vreg[2 * l + 1] = vreg[2 * l - 1];
-              vreg[3] = t0;
-            }
-            // ... shared-memory rows: p, q of V'^T (offset p LDV = p LDM + p) over
-            // this lane's column pairs, branch-free so the parameter tail interleaves ...
-  #pragma unroll
-            for (int j = 0; j < (kSmemKp > 0 ? kLaneVit : 0); ++j) {
-              const int v = lvit[j];
-              const int sl = v & 0xff, kc = (v >> 8) & 0xff;
-              const double2 r = rot[v < 0 ? 0 : sl];
-              const int4 o = ofs[v < 0 ? 0 : sl];
-              const bool on = v >= 0 && r.y != 0.0;
-              double2* vp = reinterpret_cast<double2*>(Vt + (on ? o.x + o.z + kc : 0));
-              double2* vq = reinterpret_cast<double2*>(Vt + (on ? o.y + o.w + kc : 0));
-              const double2 x = *vp, y = *vq;
-              if (on) {
-                *vp = make_double2(r.x * x.x - r.y * y.x, r.x * x.y - r.y * y.y);
-                *vq = make_double2(r.y * x.x + r.x * y.x, r.y * x.y + r.x * y.y);
+        if (a.dbg && lane == 0) {
+          atomicAdd(a.dbg + 16 + min(sweeps, 9), 1);
+          atomicAdd(a.dbg + 0, sweeps);
+          atomicMax(a.dbg + 1, sweeps);
+          if (pass == 0) atomicAdd(a.dbg + 3, 1);
+          if (pass == 1) atomicAdd(a.dbg + 2, 1);
+        }
+        // E <- E V'
+        warp_mm<RP, true>(
+            RP, RP, [&](int i, int c) { return Es[i * RP + c]; }, [&](int c, int j) { return Vx[j * LDVx + c]; },
+            [&](int i, int j, double v) { Ns[i * RP + j] = v; });
+        __syncwarp();
+        warp_copy(Es, Ns, RR, lane);
+        __syncwarp();
+        if (!converged) {
+          flag = P2G_FLAG_ACCURATE;
+          break;
+        }
+        double smax2 = 0.0, smin2 = 1e308;
+        for (int j = 0; j < RP; ++j) {
+          smax2 = fmax(smax2, Mx[j * LDM + j]);
+          smin2 = fmin(smin2, Mx[j * LDM + j]);
+        }
+        if (!(smax2 > 0.0) || !(smin2 > kTinyL * smax2)) {
+          flag = P2G_FLAG_ACCURATE;
+          break;
+        }
+        if (pass == 0 && off > 0.25 && smin2 < 1e-6 * smax2) continue;
+        // S' = M'^{-1/2} (second order about the diagonal) into Mx
+        for (int p = lane; p < RP; p += 32) {
+          const double sq = sqrt(Mx[p * LDM + p]);
+          sv[p] = sq;
+          u[p] = 1.0 / sq;
+        }
+        __syncwarp();
+        for (int e = lane; e < RR; e += 32) {
+          const int p = e / RP, q = e - p * RP;
+          const double P = 1.0 / (sv[p] + sv[q]);
+          Ns[e] = P;
+          As[e] = p == q ? 0.0 : P * Mx[p < q ? p * LDM + q : q * LDM + p];
+        }
+        __syncwarp();
+        {
+#pragma unroll 1
+          for (int bi = 0; bi < NB; ++bi) {
+            const int i = 8 * bi + fm;
+            double c1[NB][2], c2[NB][2];
+#pragma unroll
+            for (int b = 0; b < NB; ++b) c1[b][0] = c1[b][1] = c2[b][0] = c2[b][1] = 0.0;
+#pragma unroll 2
+            for (int k4 = 0; k4 < RP; k4 += 4) {
+              const int c = k4 + fk;
+              const double x = As[i * RP + c];
+              const double xu = x * u[c];
+#pragma unroll
+              for (int b = 0; b < NB; ++b) {
+                const double y = As[c * RP + 8 * b + fm];
+                dev::dmma884(c1[b], xu, y);
+                dev::dmma884(c2[b], x, y);
               }
             }
-            // ... and the parameters into the other buffer
-            param_store(nxt, buf ^ 1, round + 1 < m - 1);
-            __syncwarp();
+#pragma unroll
+            for (int b = 0; b < NB; ++b)
+#pragma unroll
+              for (int h = 0; h < 2; ++h) {
+                const int j = 8 * b + fn + h;
+                const double corr = c1[b][h] - As[i * RP + j] + Ns[i * RP + j] * c2[b][h];
+                Mx[i * LDM + j] = (i == j ? u[i] : 0.0) + u[i] * u[j] * corr;
+              }
           }
         }
-        // register rows back (whole sweeps bring positions back to round-0 order)
-        if constexpr (kRegRows > 0) {
-          if (lane < R) {
-  #pragma unroll
-            for (int x = 0; x < RP; ++x) Vt[rr_l0(RP, x) * LDV + lane] = vreg[x];
+        __syncwarp();
+        // Y = V' S' into Ns, Z = Y E'^T into As, W = T' Z into shared memory (Vx's buffer)
+        warp_mm<RP, true>(
+            RP, RP, [&](int i, int c) { return Vx[c * LDVx + i]; }, [&](int c, int j) { return Mx[c * LDM + j]; },
+            [&](int i, int j, double v) { Ns[i * RP + j] = v; });
+        __syncwarp();
+        warp_mm<RP, true>(
+            RP, RP, [&](int i, int c) { return Ns[i * RP + c]; }, [&](int c, int j) { return Es[j * RP + c]; },
+            [&](int i, int j, double v) { As[i * RP + j] = v; });
+        __syncwarp();
+        double* const Wsm = Vx;  // (V' and S' are dead)
+        double* const Xst = Mx;  // 8 x 41 X~ tile, then the 8 x 41 Q tile
+        double* const Qst = Mx + 8 * LDS;
+        warp_mm<RP, true>(
+            RP, RP, [&](int i, int c) { return Ts[i * RP + c]; }, [&](int c, int j) { return As[c * RP + j]; },
+            [&](int i, int j, double v) { Wsm[i * LDS + j] = v; });
+        __syncwarp();
+        // Q = X~ W and m1 += Q^T X~, tile by tile
+        {
+          double m1a[NB][NB][2];
+#pragma unroll
+          for (int p = 0; p < NB; ++p)
+#pragma unroll
+            for (int b = 0; b < NB; ++b) m1a[p][b][0] = m1a[p][b][1] = 0.0;
+          double* Qk = a.Q + r0 * RP;
+          for (int i0 = 0; i0 < I; i0 += 8) {
+            // the tile's X~ rows (a contiguous 8 x 40 block of X V, coalesced) into Xst
+#pragma unroll
+            for (int v = 0; v < 10; ++v) {
+              const int e = lane + 32 * v, row = e / RP, col = e - row * RP;
+              Xst[row * LDS + col] = i0 + row < I ? __ldg(xvk + static_cast<std::int64_t>(i0) * RP + e) * w[col] : 0.0;
+            }
+            __syncwarp();
+            double accQ[NB][2];
+#pragma unroll
+            for (int b = 0; b < NB; ++b) accQ[b][0] = accQ[b][1] = 0.0;
+#pragma unroll
+            for (int k4 = 0; k4 < RP; k4 += 4) {
+              const double x = Xst[fm * LDS + k4 + fk];
+#pragma unroll
+              for (int b = 0; b < NB; ++b) dev::dmma884(accQ[b], x, Wsm[(k4 + fk) * LDS + 8 * b + fm]);
+            }
+            if (i0 + fm < I) {
+#pragma unroll
+              for (int b = 0; b < NB; ++b)
+                *reinterpret_cast<double2*>(Qk + static_cast<std::int64_t>(i0 + fm) * RP + 8 * b + fn) =
+                    make_double2(accQ[b][0], accQ[b][1]);
+            }
+#pragma unroll
+            for (int b = 0; b < NB; ++b) {
+              Qst[fm * LDS + 8 * b + fn] = accQ[b][0];
+              Qst[fm * LDS + 8 * b + fn + 1] = accQ[b][1];
+            }
+            __syncwarp();
+#pragma unroll
+            for (int kk = 0; kk < 8; kk += 4) {
+              double fq[NB], fx[NB];
+#pragma unroll
+              for (int b = 0; b < NB; ++b) {
+                fq[b] = Qst[(kk + fk) * LDS + 8 * b + fm];
+                fx[b] = Xst[(kk + fk) * LDS + 8 * b + fm];
+              }
+#pragma unroll
+              for (int p = 0; p < NB; ++p)
+#pragma unroll
+                for (int b = 0; b < NB; ++b) dev::dmma884(m1a[p][b], fq[p], fx[b]);
+            }
+            __syncwarp();
           }
+#pragma unroll
+          for (int p = 0; p < NB; ++p)
+#pragma unroll
+            for (int b = 0; b < NB; ++b)
+#pragma unroll
+              for (int h = 0; h < 2; ++h) M1[(8 * p + fm) * RP + 8 * b + fn + h] += m1a[p][b][h];
+        }
+        __syncwarp();
+        break;
+      }
+      warp_copy(Ek, Es, RR, lane);
+      if (lane == 0) a.flags[k] = flag;
+      __syncwarp();
+    }
+    for (int e = lane; e < RR; e += 32) a.m1_partials[gw * RR + e] = M1[e];
+    return;
+  }
+
+  double* Bs = slab;                  // I x R rows of B = X~ H^T E
+  double* Xs = Bs + a.max_rows * R;   // I x R rows of X~ = X V D
+  double* Ts = Xs + a.max_rows * R;   // H^T E; later A = P o N; later Z
+  double* Fs = Ts + RR;               // F = B^T X~
+  double* Es = Fs + RR;               // E (R x R)
+  double* Ns = Es + RR;               // scratch: E V', P, V' S'
+  double* M1 = Ns + RR;               // this warp's m1 partial
+  double* sv = M1 + RR;               // sqrt(M'_pp)
+  for (int e = lane; e < RR; e += 32) M1[e] = 0.0;
+  for (std::int64_t k = gw; k < a.X.K; k += nwarps) {
+    const std::int64_t r0 = a.X.srp[k];
+    const int I = static_cast<int>(a.X.srp[k + 1] - r0);
+    for (int r = lane; r < R; r += 32) w[r] = a.W[k * R + r];
+    double* Ek = a.Ewarm + k * RR;
+    if (a.ew_valid)
+      warp_copy(Es, Ek, RR, lane);
+    else
+      for (int e = lane; e < RR; e += 32) Es[e] = (e / R == e % R) ? 1.0 : 0.0;
+    __syncwarp();
+    // rows of X~ = X_k V D: from the previous mode-3 pass's X V rows when
+    // available (a coalesced copy), else gathered (lane per row)
+    if (a.XV) {  // 8 loads in flight per lane before the stores (they would alias)
+      const double* xs = a.XV + r0 * R;
+      const int n = I * R;
+      for (int e0 = 0; e0 < n; e0 += 256) {
+        double t[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int e = e0 + lane + 32 * u;
+          t[u] = e < n ? __ldg(xs + e) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int e = e0 + lane + 32 * u;
+          if (e < n) Xs[e] = t[u] * w[e % R];
+        }
+      }
+    } else
+    for (int i = lane; i < I; i += 32) {
+      double xv[RP];
+      dev::csr_row_times<RP>(xv, a.X.ci, a.X.val, a.X.rp[r0 + i], a.X.rp[r0 + i + 1], a.V, R);
+      double* xrow = Xs + static_cast<std::int64_t>(i) * R;
+#pragma unroll
+      for (int c = 0; c < RP; ++c)
+        if (c < R) xrow[c] = xv[c] * w[c];
+    }
+    int flag = P2G_FLAG_FULL_RANK;
+    for (int pass = 0; pass < 2; ++pass) {
+      __syncwarp();
+      // T' = H^T E, then B = X~ T' (= X_k V D H^T E)
+      warp_mm<RP, EXACT>(
+          R, R, [&](int i, int c) { return __ldg(a.H + c * R + i); }, [&](int c, int j) { return Es[c * R + j]; },
+          [&](int i, int j, double v) { Ts[i * R + j] = v; });
+      __syncwarp();
+      warp_mm<RP, EXACT>(
+          I, R, [&](int i, int c) { return Xs[i * R + c]; }, [&](int c, int j) { return Ts[c * R + j]; },
+          [&](int i, int j, double v) { Bs[i * R + j] = v; });
+      __syncwarp();
+      // M = B^T B (lower tiles) into shared memory, F = B^T X~ into the slab
+      bool finite = true;
+      {
+        const int fm = lane >> 2, fk = lane & 3, fn = 2 * (lane & 3);
+        double acc[NB * (NB + 1) / 2][2];
+#pragma unroll
+        for (int t = 0; t < NB * (NB + 1) / 2; ++t) acc[t][0] = acc[t][1] = 0.0;
+        for (int k4 = 0; k4 < I; k4 += 4) {
+          const int r = k4 + fk;
+          double f[NB];
+#pragma unroll
+          for (int b = 0; b < NB; ++b) {
+            const int col = 8 * b + fm;
+            f[b] = (r < I && (EXACT || col < R)) ? Bs[static_cast<std::int64_t>(r) * R + col] : 0.0;
+          }
+          int t = 0;
+#pragma unroll
+          for (int bi = 0; bi < NB; ++bi)
+#pragma unroll
+            for (int bj = 0; bj <= bi; ++bj) dev::dmma884(acc[t++], f[bi], f[bj]);
+        }
+        int t = 0;
+#pragma unroll
+        for (int bi = 0; bi < NB; ++bi)
+#pragma unroll
+          for (int bj = 0; bj <= bi; ++bj, ++t) {
+            const int i = 8 * bi + fm;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const int j = 8 * bj + fn + h;
+              if (EXACT || (i < R && j < R)) {
+                M[i * LDM + j] = acc[t][h];
+                M[j * LDM + i] = acc[t][h];
+                finite &= isfinite(acc[t][h]);
+              }
+            }
+          }
+      }
+      {
+        const int fm = lane >> 2, fk = lane & 3, fn = 2 * (lane & 3);
+#pragma unroll 1
+        for (int bi = 0; bi < NB; ++bi) {
+          double acc[NB][2];
+#pragma unroll
+          for (int bj = 0; bj < NB; ++bj) acc[bj][0] = acc[bj][1] = 0.0;
+          for (int k4 = 0; k4 < I; k4 += 4) {
+            const int r = k4 + fk;
+            const int ci = 8 * bi + fm;
+            const double fa = (r < I && (EXACT || ci < R)) ? Bs[static_cast<std::int64_t>(r) * R + ci] : 0.0;
+#pragma unroll
+            for (int bj = 0; bj < NB; ++bj) {
+              const int cj = 8 * bj + fm;
+              const double fb = (r < I && (EXACT || cj < R)) ? Xs[static_cast<std::int64_t>(r) * R + cj] : 0.0;
+              dev::dmma884(acc[bj], fa, fb);
+            }
+          }
+#pragma unroll
+          for (int bj = 0; bj < NB; ++bj) {
+            const int i = 8 * bi + fm;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const int j = 8 * bj + fn + h;
+              if (EXACT || (i < R && j < R)) {
+                Fs[i * R + j] = acc[bj][h];
+                finite &= isfinite(acc[bj][h]);
+              }
+            }
+          }
+        }
+      }
+      finite = __all_sync(dev::kFull, finite);
+      __syncwarp();
+      if (!finite) {  // the accurate path re-checks the operand; no preconditioner from here
+        for (int e = lane; e < RR; e += 32) Es[e] = (e / R == e % R) ? 1.0 : 0.0;
+        __syncwarp();
+        flag = P2G_FLAG_ACCURATE;
+        break;
+      }
+      bool converged = false;
+      int sweeps = 0;
+      double off = 0.0;  // scaled off-diagonal mass at the start of the pass
+      double* Mx = M;    // after the sweeps: M' (logical order, full)
+      double* Vx = Vt;   // and V'^T (Vx[p * LDVx + k] = V'(k, p))
+    // V' = I; row `lane` of V' also in registers, in round-0 physical order
+      for (int e = lane; e < R * LDV; e += 32) {
+        const int p = e / LDV, kk = e - p * LDV;
+        Vt[e] = p == kk ? 1.0 : 0.0;
+      }
+      double vreg[kRegRows > 0 ? RP : 1];
+#pragma unroll
+      for (int x = 0; x < (kRegRows > 0 ? RP : 1); ++x) vreg[x] = rr_l0(RP, x) == lane ? 1.0 : 0.0;
+      for (int sweep = 0; sweep < kLgMaxSweeps; ++sweep, ++sweeps) {
+        double dmax = 0.0;
+        for (int j = 0; j < R; ++j) dmax = fmax(dmax, M[j * LDM + j]);
+        const double tiny = kTinyL * dmax;
+        for (int p = lane; p < R; p += 32) {
+          const double d = M[p * LDM + p];
+          u[p] = d > tiny ? 1.0 / sqrt(d) : 0.0;
+        }
+        __syncwarp();
+        double omax = 0.0, osum = 0.0;
+        for (int e = lane; e < RR; e += 32) {
+          const int p = e / R, q = e - p * R;
+          const double x = M[p < q ? p * LDM + q : q * LDM + p] * u[p] * u[q];
+          if (p != q) {
+            omax = fmax(omax, fabs(x));
+            osum = fma(x, x, osum);
+          }
+        }
+        omax = dev::warp_max(omax);
+        if (sweep == 0) {
+          off = dev::warp_sum(osum);
+          if (a.dbg && lane == 0) {
+            const int b = omax <= 0.0 ? 0 : min(9, max(0, static_cast<int>(floor(log10(omax))) + 9));
+            atomicAdd(a.dbg + 4 + b, 1);
+          }
+        }
+        if (omax <= kTauL) {
+          converged = true;
+          break;
+        }
+        // Rotation parameters of one round's slot (lanes < half store them).
+        // Split into the shared-memory loads and a pure-ALU tail, so that the
+        // tail of round r + 1 can be scheduled among round r's V' updates.
+        struct PIn {
+          double al, be, ga;
+          int p, q;
+        };
+        auto param_load = [&](int round) {
+          PIn in;
+          const int pq = sched[round * half + (lane < half ? lane : 0)];
+          in.p = pq & 0xff;
+          in.q = pq >> 8;
+          const int qq = in.q != 0xff ? in.q : in.p;
+          in.al = M[in.p * LDM + in.p];
+          in.be = M[qq * LDM + qq];
+          in.ga = in.q != 0xff ? M[in.p < qq ? in.p * LDM + qq : qq * LDM + in.p] : 0.0;
+          return in;
+        };
+        auto param_store = [&](const PIn& in, int buf, bool diag) {
+          const bool on = in.q != 0xff && in.al > tiny && in.be > tiny &&
+                          in.ga * in.ga > (kSkipL * kSkipL) * (in.al * in.be);
+          // t = sign(zeta) / (|zeta| + sqrt(1 + zeta^2)), zeta = (be - al) / (2 ga),
+          // without divisions: t = sign(d) 2ga / (|d| + sqrt(d^2 + 4ga^2))
+          const double d = in.be - in.al, g2 = 2.0 * in.ga;
+          const double h = on ? fma(d, d, g2 * g2) : 1.0;
+          const double rh = h * dev::rsqrt_nr(h);
+          const double tt = on ? (d >= 0.0 ? g2 : -g2) * dev::rcp_nr(fabs(d) + rh) : 0.0;
+          const double c = on ? dev::rsqrt_nr(fma(tt, tt, 1.0)) : 1.0;
+          if (lane < half) {
+            // the slot's own 2 x 2 block (M_pp, M_qq, M_pq) is updated here, by
+            // the lane that holds its old values: no other block of the round
+            // touches these entries, and the next parameter load follows the
+            // round's block updates
+            if (on && diag) {  // (not for the wrapped-around load of the sweep's last round)
+              const double dt = __dmul_rn(tt, in.ga);
+              M[in.p * LDM + in.p] = in.al - dt;
+              M[in.q * LDM + in.q] = in.be + dt;
+              M[in.p < in.q ? in.p * LDM + in.q : in.q * LDM + in.p] = 0.0;
+            }
+            rotb[buf * (RP / 2) + lane] = make_double2(c, c * tt);
+            rtb[buf * (RP / 2) + lane] = tt * in.ga;
+            ofsb[buf * (RP / 2) + lane] = in.q != 0xff ? make_int4(in.p * LDM, in.q * LDM, in.p, in.q)
+                                                      : make_int4(in.p * LDM, -1, in.p, -1);
+          }
+        };
+        param_store(param_load(0), 0, true);
+        __syncwarp();
+        for (int round = 0; round < m - 1; ++round) {
+          const int buf = round & 1;
+          const double2* rot = rotb + buf * (RP / 2);
+          const int4* ofs = ofsb + buf * (RP / 2);
+          // M <- J^T M J over this lane's 2 x 2 blocks of slot pairs
+#pragma unroll
+          for (int j = 0; j < kLaneBlk; ++j) {
+            const int b = lblk[j];
+            if (b < 0) continue;
+            const int i1 = b & 0xff, i2 = b >> 8;
+            const double2 r1 = rot[i1], r2 = rot[i2];
+            if (r1.y == 0.0 && r2.y == 0.0) continue;
+            const int4 o1 = ofs[i1], o2 = ofs[i2];
+            if (!EXACT && (o1.w < 0 || o2.w < 0)) {  // odd R: 1 x 2 block against the dummy slot's index
+              const bool d1 = o1.w < 0;
+              const int ar = d1 ? o1.x : o2.x, ac = d1 ? o1.z : o2.z;  // the single index (row / column offsets)
+              const int ur = d1 ? o2.x : o1.x, uc = d1 ? o2.z : o1.z;
+              const int vr = d1 ? o2.y : o1.y, vc = d1 ? o2.w : o1.w;
+              const double cc = d1 ? r2.x : r1.x, ss = d1 ? r2.y : r1.y;
+              const int au = ac < uc ? ar + uc : ur + ac, av = ac < vc ? ar + vc : vr + ac;
+              const double xu = M[au], xv = M[av];
+              M[au] = cc * xu - ss * xv;
+              M[av] = ss * xu + cc * xv;
+              continue;
+            }
+            const double c1 = r1.x, s1 = r1.y, c2 = r2.x, s2 = r2.y;
+            // upper-triangle (canonical) addresses: row index < column index
+            const int e11 = o1.z < o2.z ? o1.x + o2.z : o2.x + o1.z;
+            const int e12 = o1.z < o2.w ? o1.x + o2.w : o2.y + o1.z;
+            const int e21 = o1.w < o2.z ? o1.y + o2.z : o2.x + o1.w;
+            const int e22 = o1.w < o2.w ? o1.y + o2.w : o2.y + o1.w;
+            const double x11 = M[e11], x12 = M[e12], x21 = M[e21], x22 = M[e22];
+            const double y11 = c2 * x11 - s2 * x12, y12 = s2 * x11 + c2 * x12;
+            const double y21 = c2 * x21 - s2 * x22, y22 = s2 * x21 + c2 * x22;
+            const double z11 = c1 * y11 - s1 * y21, z21 = s1 * y11 + c1 * y21;
+            const double z12 = c1 * y12 - s1 * y22, z22 = s1 * y12 + c1 * y22;
+            M[e11] = z11;
+            M[e12] = z12;
+            M[e21] = z21;
+            M[e22] = z22;
+          }
+          __syncwarp();
+          // next round's parameter loads (M is final for this round) ...
+          const PIn nxt = param_load(round + 1 < m - 1 ? round + 1 : 0);
+          // ... V' <- V' J.  Register rows: slot i's pair sits at positions
+          // (2i, 2i+1); afterwards every position moves one step along the
+          // fixed cycle 0 <- 2 <- ... <- RP-2 <- RP-1 <- RP-3 <- ... <- 3 <- 0
+          // (position 1, index RP-1, stays), which is how the round-robin's
+          // pairs advance, so the next round's pairs are again (2i, 2i+1) ...
+          if constexpr (kRegRows > 0) {
+#pragma unroll
+            for (int i = 0; i < RP / 2; ++i) {
+              const double2 r = rot[i];
+              const double x0 = vreg[2 * i], y0 = vreg[2 * i + 1];
+              vreg[2 * i] = r.x * x0 - r.y * y0;
+              vreg[2 * i + 1] = r.y * x0 + r.x * y0;
+            }
+            const double t0 = vreg[0];
+#pragma unroll
+            for (int l = 0; l < RP / 2 - 1; ++l) vreg[2 * l] = vreg[2 * l + 2];
+            vreg[RP - 2] = vreg[RP - 1];
+#pragma unroll
+            for (int l = RP / 2 - 1; l >= 2; --l) vreg[2 * l + 1] = vreg[2 * l - 1];
+            vreg[3] = t0;
+          }
+          // ... shared-memory rows: p, q of V'^T (offset p LDV = p LDM + p) over
+          // this lane's column pairs, branch-free so the parameter tail interleaves ...
+#pragma unroll
+          for (int j = 0; j < (kSmemKp > 0 ? kLaneVit : 0); ++j) {
+            const int v = lvit[j];
+            const int sl = v & 0xff, kc = (v >> 8) & 0xff;
+            const double2 r = rot[v < 0 ? 0 : sl];
+            const int4 o = ofs[v < 0 ? 0 : sl];
+            const bool on = v >= 0 && r.y != 0.0;
+            double2* vp = reinterpret_cast<double2*>(Vt + (on ? o.x + o.z + kc : 0));
+            double2* vq = reinterpret_cast<double2*>(Vt + (on ? o.y + o.w + kc : 0));
+            const double2 x = *vp, y = *vq;
+            if (on) {
+              *vp = make_double2(r.x * x.x - r.y * y.x, r.x * x.y - r.y * y.y);
+              *vq = make_double2(r.y * x.x + r.x * y.x, r.y * x.y + r.x * y.y);
+            }
+          }
+          // ... and the parameters into the other buffer
+          param_store(nxt, buf ^ 1, round + 1 < m - 1);
           __syncwarp();
         }
       }
-      if (a.dbg && lane == 0) {
+      // register rows back (whole sweeps bring positions back to round-0 order)
+      if constexpr (kRegRows > 0) {
+        if (lane < R) {
+#pragma unroll
+          for (int x = 0; x < RP; ++x) Vt[rr_l0(RP, x) * LDV + lane] = vreg[x];
+        }
+        __syncwarp();
+      }
+          if (a.dbg && lane == 0) {
         atomicAdd(a.dbg + 16 + min(sweeps, 9), 1);
         atomicAdd(a.dbg + 0, sweeps);
         atomicMax(a.dbg + 1, sweeps);
@@ -963,6 +1224,10 @@ int launch_procrustes_large(p2g_ctx* c, int R, const double* H, const double* V,
   a.max_rows = c->max_rows;
   a.dbg = std::getenv("P2G_DEBUG") ? c->counters.get() + 4 : nullptr;
   if (a.X.K == 0) return 0;
+  if (R == 40 && !a.XV) {  // the R = 40 kernel streams X V rows: form them (first step of a fit)
+    launch_xv_rows(c, R, V, c->Ubuf.get(), s);
+    a.XV = c->Ubuf.get();
+  }
   int blocks = 0;
   if (R == 24)
     blocks = launch_large_w<24, true>(c, a, max_blocks, s);

@@ -352,7 +352,7 @@ __global__ void __launch_bounds__(WPB * 32)
 //     (L2-resident), and m3 = column sums of P o X_k V (3-step shuffle over
 //     the tile's rows), in the same order as k_mode3_mma.
 // ---------------------------------------------------------------------------
-template <int RP, int WPB>
+template <int RP, int WPB, bool M3OUT = true>
 __global__ void __launch_bounds__(WPB * 32)
     k_mode3_rows(ShardArgs X, const double* __restrict__ Q, const double* __restrict__ H,
                  const double* __restrict__ V, double* __restrict__ M3, double* __restrict__ XV) {
@@ -363,8 +363,10 @@ __global__ void __launch_bounds__(WPB * 32)
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, fm = lane >> 2, fk = lane & 3;
   const int g = lane / kL, sub = lane - g * kL;
   const bool act = g < kG;
-  for (int e = threadIdx.x; e < RP * RP; e += blockDim.x) Hs[e] = H[e];
-  __syncthreads();
+  if constexpr (M3OUT) {
+    for (int e = threadIdx.x; e < RP * RP; e += blockDim.x) Hs[e] = H[e];
+    __syncthreads();
+  }
   const std::int64_t nwarps = static_cast<std::int64_t>(gridDim.x) * WPB;
   for (std::int64_t k = static_cast<std::int64_t>(blockIdx.x) * WPB + wid; k < X.K; k += nwarps) {
     const std::int64_t r0 = X.srp[k];
@@ -408,6 +410,7 @@ __global__ void __launch_bounds__(WPB * 32)
       }
       if (iv) dev::stg256(XV + (r0 + i) * RP + 4 * sub, acc);
     }
+    if constexpr (!M3OUT) continue;
     __syncwarp();
     // B: m3 from P = Q_k H and the X_k V rows
     double m3p[NB][2];
@@ -748,6 +751,25 @@ void launch_mode3(p2g_ctx* c, int R, const double* Q, const double* H, const dou
                      constexpr int WPB = fit_wpb(32 * CLD<RP_>, RP_ * RP_);
                      k_mode3<RP_, WPB><<<grid_for(X.K, WPB, c->num_sms), WPB * 32, 0, s>>>(X, R, Q, H, V, m3);
                    }));
+  P2G_LAUNCHED(1);
+}
+
+void launch_xv_rows(p2g_ctx* c, int R, const double* V, double* XV, cudaStream_t s) {
+  const ShardArgs X = shard_args(c);
+  constexpr int WPB = 8;
+  auto run = [&](auto kern) {
+    int per_sm = 0;
+    P2G_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, WPB * 32, 0));
+    kern<<<grid_for(X.K, WPB, c->num_sms, std::max(per_sm, 1)), WPB * 32, 0, s>>>(X, nullptr, nullptr, V, nullptr, XV);
+  };
+  if (R == 24)
+    run(k_mode3_rows<24, WPB, false>);
+  else if (R == 32)
+    run(k_mode3_rows<32, WPB, false>);
+  else if (R == 40)
+    run(k_mode3_rows<40, WPB, false>);
+  else
+    throw InvalidArgument("X V rows: exact R in {24, 32, 40}");
   P2G_LAUNCHED(1);
 }
 

@@ -224,6 +224,9 @@ void launch_nnls_thread(int R, std::int64_t n, const double* G, const double* B,
                         cudaStream_t s, const double* ginv = nullptr);
 void launch_mode2(p2g_ctx* c, int R, const double* Q, const double* H, const double* W, const double* nH,
                   double* M2, cudaStream_t s);
+/// X V rows (NR x R) of the shard into XV, exact R in {24, 32, 40} (the first
+/// R = 40 Procrustes step of a fit, before any mode-3 pass has left them).
+void launch_xv_rows(p2g_ctx* c, int R, const double* V, double* XV, cudaStream_t s);
 void launch_mode3(p2g_ctx* c, int R, const double* Q, const double* H, const double* V, double* m3,
                   cudaStream_t s, double* XV_out = nullptr);
 void launch_mode1_q(p2g_ctx* c, int R, const double* Q, const double* V, const double* W, double* m1_partials,
