@@ -110,7 +110,7 @@ struct LgWarp {
   static constexpr int NB = RP / 8;  // 8-wide tensor tiles (RP multiple of 8)
   // per-warp global slab: B, X~ (max_rows x R each), T, F, E, N, M1 (R x R), s (R)
   __host__ __device__ static std::size_t slab_doubles(std::int64_t max_rows, int R) {
-    if (kPhys) return 5 * static_cast<std::size_t>(R) * R + RP;  // R x R only: the rows are streamed
+    if (kPhys) return 3 * static_cast<std::size_t>(R) * R + RP;  // T', a scratch, the m1 partial (rows streamed, E in place)
     return 2 * static_cast<std::size_t>(max_rows > 1 ? max_rows : 1) * R +
            5 * static_cast<std::size_t>(R) * R + RP;
   }
@@ -271,17 +271,17 @@ __global__ void __launch_bounds__(LgWarp<RP>::WPB * 32, 1) k_procrustes_large_w(
   double* slab = a.slab + gw * L::slab_doubles(a.max_rows, R);
   if constexpr (kPhys) {
     // Exact R = 40.  X~ = X_k V D is streamed in 8-row tiles from the X V rows
-    // of the last mode-3 pass (a.XV, always given): B = X~ T' is formed tile
-    // by tile and only its Gram M = B^T B is kept; after the sweeps
-    // Q = X~ W with W = T' Z (Z = V' S' E'^T) and m1 += Q^T X~ (= Z^T B^T X~),
-    // again tile by tile.  No I x R slab: the per-warp scratch is R x R only
-    // (E, T', two scratch matrices, the m1 partial), and the tiles live in
-    // the warp's shared memory (8 x 41 staging, T' and W at row stride 41).
+    // of the last mode-3 pass (a.XV, always given): B = X~ T' (T' = H^T E) is
+    // formed tile by tile and only its Gram M = B^T B is kept; after the
+    // sweeps Q = X~ W with W = T' Z, Z = V' S' E'^T, and m1 += Q^T X~
+    // (= Z^T B^T X~ of the generic path), again tile by tile.  E is updated in
+    // place in Ewarm (a row tile of E' = E V' depends only on the same rows of
+    // E).  The product order is the generic path's: W = H^T (E' S' E'^T)
+    // measured 30x further from the oracle on cfg5's ill-conditioned subjects.
+    // Per-warp global scratch: T', one R x R scratch (A, then Y), the m1 partial.
     constexpr int LDS = LDM;
-    double* const Es = slab;       // E (R x R): warm start in, V_A out
-    double* const Ts = Es + RR;    // T' = H^T E
-    double* const Ns = Ts + RR;    // scratch: E V', P, V' S'
-    double* const As = Ns + RR;    // scratch: A = P o N, Z
+    double* const Ts = slab;       // T' = H^T E
+    double* const As = Ts + RR;    // scratch: A = P o N, then Y = V' S'
     double* const M1 = As + RR;    // this warp's m1 partial
     double* const sv = M1 + RR;    // sqrt(M'_pp)
     double* const Ms0 = M;         // shared buffer 0 (the M region)
@@ -292,18 +292,16 @@ __global__ void __launch_bounds__(LgWarp<RP>::WPB * 32, 1) k_procrustes_large_w(
       const std::int64_t r0 = a.X.srp[k];
       const int I = static_cast<int>(a.X.srp[k + 1] - r0);
       for (int r = lane; r < RP; r += 32) w[r] = a.W[k * RP + r];
-      double* Ek = a.Ewarm + k * RR;
-      if (a.ew_valid)
-        warp_copy(Es, Ek, RR, lane);
-      else
-        for (int e = lane; e < RR; e += 32) Es[e] = (e / RP == e % RP) ? 1.0 : 0.0;
+      double* Ek = a.Ewarm + k * RR;  // E: read and updated in place
+      if (!a.ew_valid)
+        for (int e = lane; e < RR; e += 32) Ek[e] = (e / RP == e % RP) ? 1.0 : 0.0;
       const double* xvk = a.XV + r0 * RP;
       int flag = P2G_FLAG_FULL_RANK;
       for (int pass = 0; pass < 2; ++pass) {
         __syncwarp();
         // T' = H^T E into the slab and shared buffer 1
         warp_mm<RP, true>(
-            RP, RP, [&](int i, int c) { return __ldg(a.H + c * RP + i); }, [&](int c, int j) { return Es[c * RP + j]; },
+            RP, RP, [&](int i, int c) { return __ldg(a.H + c * RP + i); }, [&](int c, int j) { return Ek[c * RP + j]; },
             [&](int i, int j, double v) {
               Ts[i * RP + j] = v;
               Ms1[i * LDS + j] = v;
@@ -373,7 +371,7 @@ __global__ void __launch_bounds__(LgWarp<RP>::WPB * 32, 1) k_procrustes_large_w(
         finite = __all_sync(dev::kFull, finite);
         __syncwarp();
         if (!finite) {  // the accurate path re-checks the operand; no preconditioner from here
-          for (int e = lane; e < RR; e += 32) Es[e] = (e / RP == e % RP) ? 1.0 : 0.0;
+          for (int e = lane; e < RR; e += 32) Ek[e] = (e / RP == e % RP) ? 1.0 : 0.0;
           __syncwarp();
           flag = P2G_FLAG_ACCURATE;
           break;
@@ -613,12 +611,10 @@ __global__ void __launch_bounds__(LgWarp<RP>::WPB * 32, 1) k_procrustes_large_w(
           if (pass == 0) atomicAdd(a.dbg + 3, 1);
           if (pass == 1) atomicAdd(a.dbg + 2, 1);
         }
-        // E <- E V'
+        // E <- E V', in place (row tile i of E' reads only row tile i of E)
         warp_mm<RP, true>(
-            RP, RP, [&](int i, int c) { return Es[i * RP + c]; }, [&](int c, int j) { return Vx[j * LDVx + c]; },
-            [&](int i, int j, double v) { Ns[i * RP + j] = v; });
-        __syncwarp();
-        warp_copy(Es, Ns, RR, lane);
+            RP, RP, [&](int i, int c) { return Ek[i * RP + c]; }, [&](int c, int j) { return Vx[j * LDVx + c]; },
+            [&](int i, int j, double v) { Ek[i * RP + j] = v; });
         __syncwarp();
         if (!converged) {
           flag = P2G_FLAG_ACCURATE;
@@ -634,7 +630,8 @@ __global__ void __launch_bounds__(LgWarp<RP>::WPB * 32, 1) k_procrustes_large_w(
           break;
         }
         if (pass == 0 && off > 0.25 && smin2 < 1e-6 * smax2) continue;
-        // S' = M'^{-1/2} (second order about the diagonal) into Mx
+        // S' = M'^{-1/2} (second order about the diagonal) into Mx; A = P o N in
+        // the slab, P_pq = 1 / (s_p + s_q) formed on the fly
         for (int p = lane; p < RP; p += 32) {
           const double sq = sqrt(Mx[p * LDM + p]);
           sv[p] = sq;
@@ -643,9 +640,7 @@ __global__ void __launch_bounds__(LgWarp<RP>::WPB * 32, 1) k_procrustes_large_w(
         __syncwarp();
         for (int e = lane; e < RR; e += 32) {
           const int p = e / RP, q = e - p * RP;
-          const double P = 1.0 / (sv[p] + sv[q]);
-          Ns[e] = P;
-          As[e] = p == q ? 0.0 : P * Mx[p < q ? p * LDM + q : q * LDM + p];
+          As[e] = p == q ? 0.0 : (1.0 / (sv[p] + sv[q])) * Mx[p < q ? p * LDM + q : q * LDM + p];
         }
         __syncwarp();
         {
@@ -672,26 +667,27 @@ __global__ void __launch_bounds__(LgWarp<RP>::WPB * 32, 1) k_procrustes_large_w(
 #pragma unroll
               for (int h = 0; h < 2; ++h) {
                 const int j = 8 * b + fn + h;
-                const double corr = c1[b][h] - As[i * RP + j] + Ns[i * RP + j] * c2[b][h];
+                const double corr = c1[b][h] - As[i * RP + j] + (1.0 / (sv[i] + sv[j])) * c2[b][h];
                 Mx[i * LDM + j] = (i == j ? u[i] : 0.0) + u[i] * u[j] * corr;
               }
           }
         }
         __syncwarp();
-        // Y = V' S' into Ns, Z = Y E'^T into As, W = T' Z into shared memory (Vx's buffer)
+        // Y = V' S' into the slab scratch, Z = Y E'^T into Mx's buffer, W = T' Z into Vx's
         warp_mm<RP, true>(
             RP, RP, [&](int i, int c) { return Vx[c * LDVx + i]; }, [&](int c, int j) { return Mx[c * LDM + j]; },
-            [&](int i, int j, double v) { Ns[i * RP + j] = v; });
-        __syncwarp();
-        warp_mm<RP, true>(
-            RP, RP, [&](int i, int c) { return Ns[i * RP + c]; }, [&](int c, int j) { return Es[j * RP + c]; },
             [&](int i, int j, double v) { As[i * RP + j] = v; });
         __syncwarp();
-        double* const Wsm = Vx;  // (V' and S' are dead)
-        double* const Xst = Mx;  // 8 x 41 X~ tile, then the 8 x 41 Q tile
+        double* const Zs = Mx;
+        warp_mm<RP, true>(
+            RP, RP, [&](int i, int c) { return As[i * RP + c]; }, [&](int c, int j) { return Ek[j * RP + c]; },
+            [&](int i, int j, double v) { Zs[i * LDS + j] = v; });
+        __syncwarp();
+        double* const Wsm = Vx;  // W = T' Z (V' is dead)
+        double* const Xst = Mx;  // then: 8 x 41 X~ tile and 8 x 41 Q tile (Z is dead)
         double* const Qst = Mx + 8 * LDS;
         warp_mm<RP, true>(
-            RP, RP, [&](int i, int c) { return Ts[i * RP + c]; }, [&](int c, int j) { return As[c * RP + j]; },
+            RP, RP, [&](int i, int c) { return Ts[i * RP + c]; }, [&](int c, int j) { return Zs[c * LDS + j]; },
             [&](int i, int j, double v) { Wsm[i * LDS + j] = v; });
         __syncwarp();
         // Q = X~ W and m1 += Q^T X~, tile by tile
@@ -756,7 +752,6 @@ __global__ void __launch_bounds__(LgWarp<RP>::WPB * 32, 1) k_procrustes_large_w(
         __syncwarp();
         break;
       }
-      warp_copy(Ek, Es, RR, lane);
       if (lane == 0) a.flags[k] = flag;
       __syncwarp();
     }
