@@ -594,7 +594,7 @@ void small_smem_optin() {
 }
 
 template <int RP>
-void nnls_launch(int R, std::int64_t n, const double* G, const double* B, double* X, int cap, std::int32_t* err,
+void nnls_launch(NnlsWork& ws, int R, std::int64_t n, const double* G, const double* B, double* X, int cap, std::int32_t* err,
                  const std::int32_t* rowlist, const std::int32_t* nlist, unsigned long long* masks, int warm,
                  cudaStream_t s) {
   constexpr int WPB = RP <= 16 ? 8 : 4;
@@ -604,38 +604,35 @@ void nnls_launch(int R, std::int64_t n, const double* G, const double* B, double
   P2G_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   const std::int64_t want = (n + WPB - 1) / WPB;
   const int blocks = static_cast<int>(std::max<std::int64_t>(1, std::min<std::int64_t>(want, 148 * 16)));
-  // pinv fallback workspace: one process drives one device, so a
-  // process-wide slab grown on demand is enough
-  static DBuf<double> slab;
-  slab.resize(static_cast<std::size_t>(blocks) * WPB * 3 * RP * RP);
-  static DBuf<double> ginv;
+  // pinv fallback workspace and G^{-1}: the context's (grown on demand)
+  ws.slab.resize(static_cast<std::size_t>(blocks) * WPB * 3 * RP * RP);
   const bool fast = !rowlist && RP > 16;
   if (fast) {
-    ginv.resize(static_cast<std::size_t>(RP) * RP + 1);
-    k_ginv<RP><<<1, 32, 0, s>>>(R, G, ginv.get());
+    ws.ginv.resize(static_cast<std::size_t>(RP) * RP + 1);
+    k_ginv<RP><<<1, 32, 0, s>>>(R, G, ws.ginv.get());
   }
-  kern<<<blocks, WPB * 32, smem, s>>>(R, n, G, B, X, cap, err, rowlist, nlist, masks, warm, slab.get(),
-                                      fast ? ginv.get() : nullptr);
+  kern<<<blocks, WPB * 32, smem, s>>>(R, n, G, B, X, cap, err, rowlist, nlist, masks, warm, ws.slab.get(),
+                                      fast ? ws.ginv.get() : nullptr);
 }
 
 template <int RP>
-void nnls_warp(int R, std::int64_t n, const double* G, const double* B, double* X, int cap, std::int32_t* err,
-               const std::int32_t* rowlist, const std::int32_t* nlist, unsigned long long* masks, int warm,
-               cudaStream_t s) {
-  nnls_launch<RP>(R, n, G, B, X, cap, err, rowlist, nlist, masks, warm, s);
+void nnls_warp(NnlsWork& ws, int R, std::int64_t n, const double* G, const double* B, double* X, int cap,
+               std::int32_t* err, const std::int32_t* rowlist, const std::int32_t* nlist, unsigned long long* masks,
+               int warm, cudaStream_t s) {
+  nnls_launch<RP>(ws, R, n, G, B, X, cap, err, rowlist, nlist, masks, warm, s);
 }
 
-void nnls_warp_any(int R, std::int64_t n, const double* G, const double* B, double* X, int cap, std::int32_t* err,
+void nnls_warp_any(NnlsWork& ws, int R, std::int64_t n, const double* G, const double* B, double* X, int cap, std::int32_t* err,
                    const std::int32_t* rowlist, const std::int32_t* nlist, cudaStream_t s,
                    unsigned long long* masks = nullptr, int warm = 0) {
   if (R <= 8)
-    nnls_warp<8>(R, n, G, B, X, cap, err, rowlist, nlist, masks, warm, s);
+    nnls_warp<8>(ws, R, n, G, B, X, cap, err, rowlist, nlist, masks, warm, s);
   else if (R <= 16)
-    nnls_warp<16>(R, n, G, B, X, cap, err, rowlist, nlist, masks, warm, s);
+    nnls_warp<16>(ws, R, n, G, B, X, cap, err, rowlist, nlist, masks, warm, s);
   else if (R <= 32)
-    nnls_warp<32>(R, n, G, B, X, cap, err, rowlist, nlist, masks, warm, s);
+    nnls_warp<32>(ws, R, n, G, B, X, cap, err, rowlist, nlist, masks, warm, s);
   else if (R <= 40)
-    nnls_warp<40>(R, n, G, B, X, cap, err, rowlist, nlist, masks, warm, s);
+    nnls_warp<40>(ws, R, n, G, B, X, cap, err, rowlist, nlist, masks, warm, s);
   else
     throw InvalidArgument("rank above 40 unsupported");
 }
@@ -656,17 +653,16 @@ void reduce_partials(const double* partials, int nparts, std::int64_t len, doubl
   P2G_LAUNCHED(1);
 }
 
-/// G^{-1} of an R <= 16 Gram into a process-wide buffer (out[R*R] = validity),
-/// for the thread-per-row NNLS's cold start.
-const double* launch_ginv_small(int R, const double* G, cudaStream_t s) {
-  static DBuf<double> buf;
-  buf.resize(16 * 16 + 1);
-  k_ginv<16><<<1, 32, 0, s>>>(R, G, buf.get());
+/// G^{-1} of an R <= 16 Gram into the context's workspace (out[R*R] =
+/// validity), for the thread-per-row NNLS's cold start.
+const double* launch_ginv_small(NnlsWork& ws, int R, const double* G, cudaStream_t s) {
+  ws.ginv_small.resize(16 * 16 + 1);
+  k_ginv<16><<<1, 32, 0, s>>>(R, G, ws.ginv_small.get());
   P2G_LAUNCHED(1);
-  return buf.get();
+  return ws.ginv_small.get();
 }
 
-void launch_nnls_rows(int R, std::int64_t n, const double* G, const double* B, double* X, int max_iter,
+void launch_nnls_rows(NnlsWork& ws, int R, std::int64_t n, const double* G, const double* B, double* X, int max_iter,
                       std::int32_t* err, std::int32_t* work, cudaStream_t s, unsigned* masks, int warm,
                       unsigned long long* masks64) {
   if (n == 0) return;
@@ -675,13 +671,13 @@ void launch_nnls_rows(int R, std::int64_t n, const double* G, const double* B, d
     // thread per row; rows whose passive Cholesky meets a non-positive pivot
     // are re-solved by the warp kernel with the pseudo-inverse (work[0] = count).
     P2G_CUDA(cudaMemsetAsync(work, 0, sizeof(std::int32_t), s));
-    const double* gi = (masks && !warm) ? launch_ginv_small(R, G, s) : nullptr;  // cold rows: G^{-1} b support
+    const double* gi = (masks && !warm) ? launch_ginv_small(ws, R, G, s) : nullptr;  // cold rows: G^{-1} b support
     launch_nnls_thread(R, n, G, B, X, max_iter, err, work + 1, work, masks, warm, s, gi);
-    nnls_warp_any(R, n, G, B, X, cap, err, work + 1, work, s);
+    nnls_warp_any(ws, R, n, G, B, X, cap, err, work + 1, work, s);
     P2G_LAUNCHED(1);
     return;
   }
-  nnls_warp_any(R, n, G, B, X, cap, err, nullptr, nullptr, s, masks64, masks64 ? warm : 0);
+  nnls_warp_any(ws, R, n, G, B, X, cap, err, nullptr, nullptr, s, masks64, masks64 ? warm : 0);
   P2G_LAUNCHED(1);
 }
 

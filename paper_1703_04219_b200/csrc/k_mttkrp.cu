@@ -81,77 +81,6 @@ __global__ void __launch_bounds__(WPB * 32)
   }
 }
 
-// ---------------------------------------------------------------------------
-// mode 2 with on-chip accumulation.  The J x R output does not fit one SM's
-// shared memory (J=5000, R=10: 400 KB), so output columns are split into
-// groups of rg with J*rg doubles per CTA; CTA (range, group) streams its
-// subject range once, forms U' = Q_k (H diag(W_k o nH)) restricted to the
-// group's columns (R*rg FMA per row: no redundant flops across groups), and
-// accumulates X_k^T U' with shared-memory fp64 adds.  Each CTA writes its
-// J x rg slice of a per-range partial; partials are summed in a fixed order.
-// ---------------------------------------------------------------------------
-template <int RP>
-__global__ void __launch_bounds__(512)
-    k_mode2_smem(ShardArgs X, int R, int rg, int ngroups, int nranges, const double* __restrict__ Q,
-                 const double* __restrict__ H, const double* __restrict__ W, const double* __restrict__ nH,
-                 double* __restrict__ partials) {
-  extern __shared__ double sm[];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int nw = blockDim.x >> 5;
-  const int group = blockIdx.x % ngroups, range = blockIdx.x / ngroups;
-  const int c0 = group * rg;
-  const int cg = min(rg, R - c0);  // columns of this group
-  const std::int64_t J = X.J;
-  double* acc = sm;                               // J * rg
-  double* HW = acc + J * rg + wid * (RP * RP + 32 * CLD<RP>);
-  double* ch = HW + RP * RP;
-  for (std::int64_t e = threadIdx.x; e < J * rg; e += blockDim.x) acc[e] = 0.0;
-  __syncthreads();
-  const std::int64_t k0 = X.K * range / nranges, k1 = X.K * (range + 1) / nranges;
-  for (std::int64_t k = k0 + wid; k < k1; k += nw) {
-    const std::int64_t r0 = X.srp[k];
-    const int I = static_cast<int>(X.srp[k + 1] - r0);
-    for (int e = lane; e < R * cg; e += 32) {  // HW(a, c) for the group's columns, row-major R x cg
-      const int a = e / cg, c = e - (e / cg) * cg;
-      HW[a * cg + c] = H[a * R + c0 + c] * W[k * R + c0 + c] * (nH ? nH[c0 + c] : 1.0);
-    }
-    __syncwarp();
-    for (int b0 = 0; b0 < I; b0 += 32) {
-      const int nr = min(32, I - b0);
-      stage_rows<RP>(ch, Q + (r0 + b0) * R, nr, R, lane);
-      if (lane < nr) {
-        double u[RP];
-#pragma unroll
-        for (int c = 0; c < RP; ++c) {
-          double s = 0.0;
-          if (c < cg) {
-#pragma unroll
-            for (int a = 0; a < RP; ++a)
-              if (a < R) s = fma(ch[lane * CLD<RP> + a], HW[a * cg + c], s);
-          }
-          u[c] = s;
-        }
-        const std::int64_t p0 = X.rp[r0 + b0 + lane], p1 = X.rp[r0 + b0 + lane + 1];
-        for (std::int64_t p = p0; p < p1; ++p) {
-          const int j = __ldg(X.ci + p);
-          const double v = __ldg(X.val + p);
-          double* dst = acc + static_cast<std::int64_t>(j) * rg;
-#pragma unroll
-          for (int c = 0; c < RP; ++c)
-            if (c < cg) atomicAdd(dst + c, v * u[c]);
-        }
-      }
-      __syncwarp();
-    }
-  }
-  __syncthreads();
-  double* out = partials + static_cast<std::int64_t>(range) * J * R;
-  for (std::int64_t e = threadIdx.x; e < J * cg; e += blockDim.x) {
-    const std::int64_t j = e / cg;
-    const int c = static_cast<int>(e - j * cg);
-    out[j * R + c0 + c] = acc[j * rg + c];
-  }
-}
 
 // ---------------------------------------------------------------------------
 // mode 3: one warp per subject; M3(k,c) = sum_i (Q_k H)(i,c) (X_k V)(i,c).
@@ -673,6 +602,33 @@ int grid_for(std::int64_t warps, int wpb, int num_sms, int per_sm = 8) {
     }                                                       \
   } while (0)
 
+// R <= 16 only (row-per-lane kernels that spill at larger R; their callers
+// take the R > 16 branch first, so no larger instantiation is emitted).
+#define P2G_RP_DISPATCH_SMALL(R, CALL)                        \
+  do {                                                        \
+    if ((R) <= 2) {                                           \
+      constexpr int RP_ = 2;                                  \
+      CALL;                                                   \
+    } else if ((R) <= 4) {                                    \
+      constexpr int RP_ = 4;                                  \
+      CALL;                                                   \
+    } else if ((R) <= 5) {                                    \
+      constexpr int RP_ = 5;                                  \
+      CALL;                                                   \
+    } else if ((R) <= 8) {                                    \
+      constexpr int RP_ = 8;                                  \
+      CALL;                                                   \
+    } else if ((R) <= 10) {                                   \
+      constexpr int RP_ = 10;                                 \
+      CALL;                                                   \
+    } else if ((R) <= 16) {                                   \
+      constexpr int RP_ = 16;                                 \
+      CALL;                                                   \
+    } else {                                                  \
+      throw InvalidArgument("rank above 16 on a small-R path"); \
+    }                                                         \
+  } while (0)
+
 static ShardArgs shard_args(p2g_ctx* c) {
   return ShardArgs{c->srp.get(), c->rp.get(), c->ci.get(), c->val.get(), c->k_end - c->k_begin, c->NR, c->nnz, c->J};
 }
@@ -680,33 +636,10 @@ static ShardArgs shard_args(p2g_ctx* c) {
 void launch_mode2(p2g_ctx* c, int R, const double* Q, const double* H, const double* W, const double* nH, double* M2,
                   cudaStream_t s) {
   const ShardArgs X = shard_args(c);
-  // On-chip accumulation when a column group of >= 1 fits shared memory.
-  constexpr std::size_t kSmemBudget = 220 * 1024;
-  const int warps = 16;
-  std::size_t per_warp = 0;
-  P2G_RP_DISPATCH2(R, per_warp = sizeof(double) * (RP_ * RP_ + 32 * RP_));
-  const std::size_t room = kSmemBudget > warps * per_warp ? kSmemBudget - warps * per_warp : 0;
-  const std::int64_t rg_fit = static_cast<std::int64_t>(room / (sizeof(double) * std::max<std::int64_t>(c->J, 1)));
-  // Disabled: shared-memory fp64 atomicAdd lowers to an ATOMS.CAST.SPIN CAS
-  // loop on sm_100a and measured 14.3 ms vs 5.4 ms for L2 reductions (cfg2).
-  constexpr bool kOnChip = false;
-  if (kOnChip && rg_fit >= 1 && X.K > 0) {
-    const int ngroups = static_cast<int>((R + std::min<std::int64_t>(rg_fit, R) - 1) / std::min<std::int64_t>(rg_fit, R));
-    const int rg = (R + ngroups - 1) / ngroups;
-    const int nranges = static_cast<int>(std::max<std::int64_t>(1, std::min<std::int64_t>(c->num_sms / ngroups, X.K)));
-    const std::size_t smem = sizeof(double) * static_cast<std::size_t>(c->J) * rg + warps * per_warp;
-    c->m2part.resize(static_cast<std::size_t>(nranges) * c->J * R);
-    P2G_RP_DISPATCH2(R, ({
-                       auto kern = k_mode2_smem<RP_>;
-                       P2G_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                     static_cast<int>(smem)));
-                       kern<<<ngroups * nranges, warps * 32, smem, s>>>(X, R, rg, ngroups, nranges, Q, H, W, nH,
-                                                                       c->m2part.get());
-                     }));
-    P2G_LAUNCHED(1);
-    reduce_partials(c->m2part.get(), nranges, c->J * R, M2, s);
-    return;
-  }
+  // L2 fp64 reductions (the packed/hook path; the fused loop uses the
+  // atomics-free CSC form).  On-chip accumulation was measured and dropped:
+  // shared-memory fp64 atomicAdd lowers to an ATOMS.CAST.SPIN CAS loop on
+  // sm_100a (14.3 ms vs 5.4 ms at cfg2).
   P2G_CUDA(cudaMemsetAsync(M2, 0, sizeof(double) * c->J * R, s));
   P2G_RP_DISPATCH2(R, ({
                      constexpr int WPB = fit_wpb(RP_ * RP_ + 32 * CLD<RP_>, 0);
@@ -718,7 +651,7 @@ void launch_mode2(p2g_ctx* c, int R, const double* Q, const double* H, const dou
 void launch_mode3(p2g_ctx* c, int R, const double* Q, const double* H, const double* V, double* m3,
                   cudaStream_t s, double* XV_out) {
   const ShardArgs X = shard_args(c);
-  if (R > 16) {  // the row-per-lane form spills above R = 16
+  if (R > 16 || XV_out) {  // the row-per-lane form spills above R = 16; the large-R loop wants X V rows
     constexpr int WPB = 8;
     if (XV_out && (R == 24 || R == 32 || R == 40)) {  // the fused loop: X V rows kept for Procrustes
       // resident blocks only (the subjects are split statically over the grid)
@@ -747,10 +680,10 @@ void launch_mode3(p2g_ctx* c, int R, const double* Q, const double* H, const dou
     P2G_LAUNCHED(1);
     return;
   }
-  P2G_RP_DISPATCH2(R, ({
-                     constexpr int WPB = fit_wpb(32 * CLD<RP_>, RP_ * RP_);
-                     k_mode3<RP_, WPB><<<grid_for(X.K, WPB, c->num_sms), WPB * 32, 0, s>>>(X, R, Q, H, V, m3);
-                   }));
+  P2G_RP_DISPATCH_SMALL(R, ({
+                         constexpr int WPB = fit_wpb(32 * CLD<RP_>, RP_ * RP_);
+                         k_mode3<RP_, WPB><<<grid_for(X.K, WPB, c->num_sms), WPB * 32, 0, s>>>(X, R, Q, H, V, m3);
+                       }));
   P2G_LAUNCHED(1);
 }
 

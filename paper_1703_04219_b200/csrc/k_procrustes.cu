@@ -1,24 +1,14 @@
-// K1 — per-subject Procrustes step fused with the mode-1 MTTKRP partial.
+// Accurate Procrustes path over the flagged subjects, fused with their
+// mode-1 MTTKRP partial.
 //
-// Replaces procrustes_update (solver.hpp:173-193) over all subjects
-// (solver.hpp:279-284) and mttkrp_mode1 (mttkrp.hpp:81-106) in its Q form
-// M1 = sum_k Q_k^T (X_k V) diag(W_k), which shares X_k V with the Procrustes
-// target (SURVEY.md §3.2 fusion facts).
-//
-// Math (per subject k, D = diag(W_k), T = D H^T):
-//   XV = X_k V                          (CSR gather, V rows via L1/L2)
-//   C  = XV^T XV                        (R x R, lower triangle per lane)
-//   G  = A^T A = T^T C T,  A = XV T     (A = M^T of solver.hpp:189-190)
-//   G  = E diag(lambda) E^T             (warp Jacobi, shared memory)
-//   Q  = A G^{-1/2} = XV P,  P = T E diag(lambda^-1/2) E^T
-//   m1_k = Q^T XV D = P^T C D
-// A is never stored: pass 2 recomputes XV rows and writes Q = XV P.
-//
-// The Gram route squares the condition number, so subjects with
-// lambda_min < kFastRatio * lambda_max (or A == 0, or non-finite G) are
-// flagged and solved by k_procrustes_accurate below: a one-sided Jacobi SVD
-// of A (backward stable like Eigen's JacobiSVD, kernels.hpp:105) with the
-// canonical rank-deficiency rule D5 (oracle/p2_oracle.hpp canonical_polar).
+// Replaces procrustes_update (solver.hpp:173-193) for the subjects the fast
+// paths (k_polar_small for R <= 16, k_procrustes_large_w for R > 16) flag
+// P2G_FLAG_ACCURATE: rank-deficient or ill-conditioned targets, non-finite
+// operands, non-converged Jacobi.  k_procrustes_accurate is a one-sided
+// Jacobi SVD of A = X_k V diag(W_k) H^T (backward stable like Eigen's
+// JacobiSVD, kernels.hpp:105), preconditioned with the fast path's
+// eigenvectors, with the canonical rank-deficiency rule D5
+// (oracle/p2_oracle.hpp canonical_polar).  m1_k = Q_k^T (X_k V) diag(W_k).
 #include <algorithm>
 
 #include <cub/device/device_select.cuh>
@@ -31,7 +21,6 @@ namespace p2g {
 namespace {
 
 constexpr double kNullRatio = 1e-26;  // sigma^2 <= kNullRatio * sigma_max^2 -> null direction (D5, round-off level)
-constexpr double kFastRatio = 1e-6;   // lambda_min >= kFastRatio * lambda_max -> fast path
 
 struct K1Args {
   ShardArgs X;
@@ -52,178 +41,6 @@ struct K1Args {
   double* Chat;
 };
 
-template <int RP>
-struct K1Smem {
-  static constexpr int kMat = RP * RP;
-  // per warp: C, T, B1, G, E, B2, M1acc + chunk(32*RP) + s(RP) + cs(RP+2) + pq(RP+2 ints)
-  static constexpr int kPerWarpDoubles = 7 * kMat + 32 * RP + RP + (RP + 2) + (RP + 2);
-};
-
-template <int RP, int WPB>
-__global__ void __launch_bounds__(WPB * 32) k_procrustes(K1Args a) {
-  extern __shared__ double smem[];
-  const int lane = threadIdx.x & 31;
-  const int wid = threadIdx.x >> 5;
-  const int R = a.R;
-  const int RR = R * R;
-  double* Hs = smem;  // block-shared H
-  double* base = smem + RP * RP + wid * K1Smem<RP>::kPerWarpDoubles;
-  double* C = base;
-  double* T = C + RP * RP;
-  double* B1 = T + RP * RP;
-  double* G = B1 + RP * RP;
-  double* E = G + RP * RP;
-  double* B2 = E + RP * RP;
-  double* M1 = B2 + RP * RP;
-  double* chunk = M1 + RP * RP;
-  double* s = chunk + 32 * RP;
-  double* cs = s + RP;
-  int* pq = reinterpret_cast<int*>(cs + RP + 2);
-
-  for (int e = threadIdx.x; e < RR; e += blockDim.x) Hs[e] = a.H[e];
-  for (int e = lane; e < RR; e += 32) M1[e] = 0.0;
-  __syncthreads();
-
-  // Lower-triangle entries of C owned by this lane.
-  constexpr int kTri = (RP * (RP + 1) / 2 + 31) / 32;
-  const int ntri = R * (R + 1) / 2;
-  int ea[kTri], eb[kTri];
-#pragma unroll
-  for (int t = 0; t < kTri; ++t) {
-    const int e = lane + 32 * t;
-    int x = 0;
-    while ((x + 1) * (x + 2) / 2 <= e) ++x;
-    ea[t] = x;
-    eb[t] = e - x * (x + 1) / 2;
-  }
-
-  const std::int64_t nwarps = static_cast<std::int64_t>(gridDim.x) * WPB;
-  for (std::int64_t k = static_cast<std::int64_t>(blockIdx.x) * WPB + wid; k < a.X.K; k += nwarps) {
-    const std::int64_t r0 = a.X.srp[k];
-    const int I = static_cast<int>(a.X.srp[k + 1] - r0);
-    for (int r = lane; r < R; r += 32) s[r] = a.W[k * R + r];  // R may exceed 32
-    __syncwarp();
-
-    // ---- pass 1: C = XV^T XV -------------------------------------------
-    double cacc[kTri];
-#pragma unroll
-    for (int t = 0; t < kTri; ++t) cacc[t] = 0.0;
-    for (int b = 0; b < I; b += 32) {
-      const int i = b + lane;
-      const int nr = min(32, I - b);
-      double xv[RP];
-      if (i < I) {
-        dev::csr_row_times<RP>(xv, a.X.ci, a.X.val, a.X.rp[r0 + i], a.X.rp[r0 + i + 1], a.V, R);
-      } else {
-#pragma unroll
-        for (int r = 0; r < RP; ++r) xv[r] = 0.0;
-      }
-#pragma unroll
-      for (int r = 0; r < RP; ++r) chunk[lane * RP + r] = xv[r];
-      __syncwarp();
-#pragma unroll
-      for (int t = 0; t < kTri; ++t) {
-        if (lane + 32 * t < ntri) {
-          double acc = cacc[t];
-          for (int rr = 0; rr < nr; ++rr) acc = fma(chunk[rr * RP + ea[t]], chunk[rr * RP + eb[t]], acc);
-          cacc[t] = acc;
-        }
-      }
-      __syncwarp();
-    }
-#pragma unroll
-    for (int t = 0; t < kTri; ++t)
-      if (lane + 32 * t < ntri) {
-        C[ea[t] * R + eb[t]] = cacc[t];
-        C[eb[t] * R + ea[t]] = cacc[t];
-      }
-    // T = D H^T
-    for (int e = lane; e < RR; e += 32) {
-      const int i = e / R, j = e - (e / R) * R;
-      T[e] = s[i] * Hs[j * R + i];
-    }
-    __syncwarp();
-    dev::wmm(B1, C, T, R, lane);    // C T
-    dev::wmm_tn(G, T, B1, R, lane);  // T^T C T
-    double gmax = 0.0;
-    bool finite = true;
-    for (int e = lane; e < RR; e += 32) {
-      const double g = G[e];
-      finite &= isfinite(g);
-      gmax = fmax(gmax, fabs(g));
-    }
-    finite = __all_sync(dev::kFull, finite);
-    gmax = dev::warp_max(gmax);
-    if (!finite || gmax == 0.0) {
-      if (lane == 0) a.flags[k] = P2G_FLAG_ACCURATE;  // accurate path decides
-      __syncwarp();
-      continue;
-    }
-    dev::warp_jacobi_eig(G, E, R, cs, pq, lane);
-    double lmax = -1e308, lmin = 1e308;
-    for (int i = lane; i < R; i += 32) {
-      const double l = G[i * R + i];
-      lmax = fmax(lmax, l);
-      lmin = fmin(lmin, l);
-    }
-    lmax = dev::warp_max(lmax);
-    lmin = -dev::warp_max(-lmin);
-    if (!(lmax > 0.0) || !(lmin >= kFastRatio * lmax)) {
-      if (lane == 0) a.flags[k] = P2G_FLAG_ACCURATE;
-      __syncwarp();
-      continue;
-    }
-    // B1 = E diag(lambda^-1/2); B2 = B1 E^T = G^{-1/2}; B1 = T B2 = P
-    for (int e = lane; e < RR; e += 32) {
-      const int j = e - (e / R) * R;
-      B1[e] = E[e] * rsqrt(G[j * R + j]);
-    }
-    __syncwarp();
-    dev::wmm_nt(B2, B1, E, R, lane);
-    dev::wmm(B1, T, B2, R, lane);
-    // m1_k = P^T C D
-    for (int e = lane; e < RR; e += 32) {
-      const int i = e / R, j = e - (e / R) * R;
-      double acc = 0.0;
-      for (int c = 0; c < R; ++c) acc = fma(B1[c * R + i], C[c * R + j], acc);
-      M1[e] = fma(acc, s[j], M1[e]);
-    }
-    // ---- pass 2: Q rows = XV P, staged through smem for coalesced stores
-    for (int b = 0; b < I; b += 32) {
-      const int i = b + lane;
-      const int nr = min(32, I - b);
-      if (i < I) {
-        double xv[RP];
-        dev::csr_row_times<RP>(xv, a.X.ci, a.X.val, a.X.rp[r0 + i], a.X.rp[r0 + i + 1], a.V, R);
-#pragma unroll
-        for (int c = 0; c < RP; ++c) {
-          if (c < R) {
-            double q = 0.0;
-#pragma unroll
-            for (int r = 0; r < RP; ++r)
-              if (r < R) q = fma(xv[r], B1[r * R + c], q);
-            chunk[lane * RP + c] = q;
-          }
-        }
-      }
-      __syncwarp();
-      double* qdst = a.Q + (r0 + b) * R;
-      for (int idx = lane; idx < nr * R; idx += 32) qdst[idx] = chunk[(idx / R) * RP + (idx - (idx / R) * R)];
-      __syncwarp();
-    }
-    if (lane == 0) a.flags[k] = P2G_FLAG_FULL_RANK;
-    __syncwarp();
-  }
-  // Block reduction of the per-warp m1 accumulators, fixed order.
-  __syncthreads();
-  if (wid == 0) {
-    for (int e = lane; e < RR; e += 32) {
-      double acc = 0.0;
-      for (int w = 0; w < WPB; ++w) acc += smem[RP * RP + w * K1Smem<RP>::kPerWarpDoubles + 6 * RP * RP + e];
-      a.m1_partials[static_cast<std::int64_t>(blockIdx.x) * RR + e] = acc;
-    }
-  }
-}
 
 // ---------------------------------------------------------------------------
 // Accurate path: one-sided Jacobi SVD of A = XV D H^T, canonical rule D5.
@@ -696,28 +513,6 @@ __global__ void __launch_bounds__(WPB * 32) k_procrustes_accurate(K1Args a, doub
   }
 }
 
-template <int RP>
-constexpr int k1_wpb() {
-  return RP <= 16 ? 8 : (RP <= 32 ? 4 : 2);
-}
-
-template <int RP>
-int launch_k1(p2g_ctx* c, const K1Args& a, int max_blocks, cudaStream_t s) {
-  constexpr int WPB = k1_wpb<RP>();
-  const std::size_t smem = sizeof(double) * (RP * RP + WPB * K1Smem<RP>::kPerWarpDoubles);
-  auto kern = k_procrustes<RP, WPB>;
-  P2G_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-  int per_sm = 0;
-  P2G_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, WPB * 32, smem));
-  per_sm = std::max(per_sm, 1);
-  std::int64_t want = (a.X.K + WPB - 1) / WPB;
-  int blocks = static_cast<int>(std::min<std::int64_t>(want, static_cast<std::int64_t>(per_sm) * c->num_sms));
-  blocks = std::max(1, std::min(blocks, max_blocks));
-  kern<<<blocks, WPB * 32, smem, s>>>(a);
-  P2G_LAUNCHED(1);
-  return blocks;
-}
-
 __global__ void k_flag_bytes(std::int64_t K, const std::int32_t* __restrict__ flags, unsigned char* __restrict__ out) {
   for (std::int64_t k = static_cast<std::int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; k < K;
        k += static_cast<std::int64_t>(gridDim.x) * blockDim.x)
@@ -800,23 +595,6 @@ void launch_acc(p2g_ctx* c, const K1Args& a, double* m1p, cudaStream_t s) {
       throw InvalidArgument("rank above 40 unsupported"); \
     }                                                    \
   } while (0)
-
-int launch_procrustes(p2g_ctx* c, int R, const double* H, const double* V, const double* W, double* Q,
-                      std::int32_t* flags, double* m1_partials, int max_blocks, cudaStream_t s) {
-  K1Args a{};
-  a.X = ShardArgs{c->srp.get(), c->rp.get(), c->ci.get(), c->val.get(), c->k_end - c->k_begin, c->NR, c->nnz, c->J};
-  a.R = R;
-  a.H = H;
-  a.V = V;
-  a.W = W;
-  a.Q = Q;
-  a.flags = flags;
-  a.m1_partials = m1_partials;
-  a.counters = c->counters.get();
-  int blocks = 0;
-  P2G_RP_DISPATCH(R, blocks = launch_k1<RP_>(c, a, max_blocks, s));
-  return blocks;
-}
 
 int launch_procrustes_accurate(p2g_ctx* c, int R, const double* H, const double* V, const double* W, double* Q,
                                std::int32_t* flags, double* m1_partials, const double* Ebuf, double* Shat,

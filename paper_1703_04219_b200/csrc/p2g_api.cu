@@ -484,7 +484,7 @@ IterOut iterate(p2g_ctx* c, bool nonneg, int iter) {
   {
     Phase ph(c, "update_v");  // V_t -> Vp
     if (nonneg) {
-      launch_nnls_rows(R, c->J, c->G2.get(), c->M2.get(), c->Vp.get(), 0, c->counters.get() + 1, c->redo.get(), s,
+      launch_nnls_rows(c->nnls_ws, R, c->J, c->G2.get(), c->M2.get(), c->Vp.get(), 0, c->counters.get() + 1, c->redo.get(), s,
                        c->mask_v.get(), c->masks_valid ? 1 : 0, c->mask64_v.get());
     } else {
       launch_pinv(R, c->G2.get(), c->pinvbuf.get(), s);
@@ -506,7 +506,7 @@ IterOut iterate(p2g_ctx* c, bool nonneg, int iter) {
   {
     Phase ph(c, "update_w");  // W_t -> Wp
     if (nonneg) {
-      launch_nnls_rows(R, Ks(c), c->G3.get(), c->m3.get(), c->Wp.get(), 0, c->counters.get() + 1, c->redo.get(), s,
+      launch_nnls_rows(c->nnls_ws, R, Ks(c), c->G3.get(), c->m3.get(), c->Wp.get(), 0, c->counters.get() + 1, c->redo.get(), s,
                        c->mask_w.get(), c->masks_valid ? 1 : 0, c->mask64_w.get());
       c->masks_valid = true;
     } else {
@@ -1777,7 +1777,7 @@ extern "C" int p2g_cp_als_iteration(p2g_ctx* c, int64_t K, int64_t J, int32_t R,
     packed_mode(c, 2, K, J, R, d, dH.get(), dV.get(), dW.get(), M2.get());
     if (nonneg) {
       work.resize(static_cast<std::size_t>(std::max<std::int64_t>(J, K)) + 1);
-      launch_nnls_rows(R, J, G2.get(), M2.get(), dV.get(), 0, err.get(), work.get(), s);
+      launch_nnls_rows(c->nnls_ws, R, J, G2.get(), M2.get(), dV.get(), 0, err.get(), work.get(), s);
     } else {
       launch_pinv(R, G2.get(), pinv.get(), s);
       launch_rows_times(R, J, M2.get(), pinv.get(), dV.get(), s);
@@ -1790,7 +1790,7 @@ extern "C" int p2g_cp_als_iteration(p2g_ctx* c, int64_t K, int64_t J, int32_t R,
     packed_mode(c, 3, K, J, R, d, dH.get(), dV.get(), dW.get(), m3.get());
     if (nonneg) {
       work.resize(static_cast<std::size_t>(std::max<std::int64_t>(J, K)) + 1);
-      launch_nnls_rows(R, K, G3.get(), m3.get(), dW.get(), 0, err.get(), work.get(), s);
+      launch_nnls_rows(c->nnls_ws, R, K, G3.get(), m3.get(), dW.get(), 0, err.get(), work.get(), s);
     } else {
       launch_pinv(R, G3.get(), pinv.get(), s);
       launch_rows_times(R, K, m3.get(), pinv.get(), dW.get(), s);
@@ -1837,7 +1837,7 @@ extern "C" int p2g_nnls_rowwise(p2g_ctx* c, const double* G, const double* B, in
     upload_colmajor(c, B, n, R, dB.get());
     DBuf<std::int32_t> work;
     work.resize(static_cast<std::size_t>(n) + 1);
-    launch_nnls_rows(R, n, dG.get(), dB.get(), dX.get(), max_iter, err.get(), work.get(), c->stream);
+    launch_nnls_rows(c->nnls_ws, R, n, dG.get(), dB.get(), dX.get(), max_iter, err.get(), work.get(), c->stream);
     std::int32_t herr = 0;
     P2G_CUDA(cudaMemcpyAsync(&herr, err.get(), sizeof(herr), cudaMemcpyDeviceToHost, c->stream));
     P2G_CUDA(cudaStreamSynchronize(c->stream));

@@ -82,6 +82,14 @@ struct ShardArgs {
 
 struct NcclState;  // opaque, defined in p2g_api.cu
 
+/// Device workspace of the NNLS kernels (per context: two contexts, or two
+/// streams, never share one).
+struct NnlsWork {
+  DBuf<double> slab;        // pinv fallback, 3 RP^2 per warp
+  DBuf<double> ginv;        // G^{-1} (+ validity) for the warm fast path, R > 16
+  DBuf<double> ginv_small;  // G^{-1} (+ validity) for the cold thread-per-row start, R <= 16
+};
+
 }  // namespace p2g
 
 struct p2g_ctx {
@@ -130,6 +138,7 @@ struct p2g_ctx {
   p2g::DBuf<std::int32_t> flags;      // K_s
   p2g::DBuf<std::int32_t> fb_list;    // compacted fallback subject ids
   p2g::DBuf<std::int32_t> counters;   // [0]=n_fallback, [1]=nnls error, ...
+  p2g::NnlsWork nnls_ws;
   p2g::DBuf<double> acc_scratch;      // accurate Procrustes path slabs
   p2g::DBuf<std::int32_t> acc_list;   // flagged subjects (ascending) + count
   p2g::DBuf<unsigned char> acc_bytes, acc_temp;
@@ -183,11 +192,6 @@ struct p2g_ctx {
 namespace p2g {
 
 // ---- launchers (defined in the kernel translation units) ----
-// K1: Procrustes fast path fused with the mode-1 partial.  Writes Q rows of
-// fast subjects, flags (0 = fast, 2 = needs accurate path), and per-block
-// R x R m1 partials (count returned).
-int launch_procrustes(p2g_ctx* c, int R, const double* H, const double* V, const double* W, double* Q,
-                      std::int32_t* flags, double* m1_partials, int max_blocks, cudaStream_t s);
 // Accurate Jacobi-SVD path over the subjects flagged P2G_FLAG_ACCURATE;
 // writes one R x R m1 partial per block (count = procrustes_accurate_blocks).
 void build_csc(p2g_ctx* c);
@@ -204,8 +208,11 @@ int launch_procrustes_accurate(p2g_ctx* c, int R, const double* H, const double*
                                double* Chat, cudaStream_t s);
 int procrustes_accurate_blocks(p2g_ctx* c, int R);
 
-// Small-rank pipeline (k_small.cu, R <= 16).
-constexpr int kSmallRankMax = 16;
+// Small-rank (Q-free, thread-per-subject) pipeline (k_small.cu) up to R = 12;
+// larger R takes the warp-per-subject pipeline (k_large.cu).  Its R = 16
+// instantiation of k_polar_small spilled 14.6 KB per thread (ptxas), so
+// R = 13..16 runs faster on the large-R path.
+constexpr int kSmallRankMax = 12;
 void launch_gram_c(p2g_ctx* c, int R, const double* V, double* Cbuf, cudaStream_t s);
 int launch_polar_small(p2g_ctx* c, int R, const double* H, const double* W, const double* Cbuf, double* Sbuf,
                        double* Ewarm, int warm, std::int32_t* flags, double* m1_partials, int max_blocks,
@@ -272,7 +279,9 @@ void reduce_partials(const double* partials, int nparts, std::int64_t len, doubl
 // work: n+1 ints of scratch (thread-per-row path for R <= 16) or null.
 // masks / masks64: n passive-set bit masks (R <= 16 / R <= 64) carried across
 // calls for the warm start (warm != 0 uses them), or null.
-void launch_nnls_rows(int R, std::int64_t n, const double* G, const double* B, double* X, int max_iter,
+// ws: the NNLS device workspace (pinv-fallback slab, G^{-1} for the warm fast
+// path and the cold thread-per-row start), owned by the caller's context.
+void launch_nnls_rows(NnlsWork& ws, int R, std::int64_t n, const double* G, const double* B, double* X, int max_iter,
                       std::int32_t* err, std::int32_t* work, cudaStream_t s, unsigned* masks = nullptr,
                       int warm = 0, unsigned long long* masks64 = nullptr);
 void launch_rows_times(int R, std::int64_t n, const double* B, const double* P, double* X,

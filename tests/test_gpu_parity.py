@@ -257,7 +257,8 @@ def test_cfg2_prefix_parity(ctx, oracle, p2g):
     assert rel_err(Q, d["Q"]) <= TOL_STEP and rel_err(m1, d["m1"]) <= TOL_STEP
 
 
-@pytest.mark.parametrize("cfg_id,R,K", [(3, 40, 1500), (5, 40, 1500), (3, 24, 800), (5, 17, 800), (3, 33, 600)])
+@pytest.mark.parametrize("cfg_id,R,K", [(3, 40, 1500), (5, 40, 1500), (3, 24, 800), (5, 17, 800), (3, 33, 600),
+                                        (2, 13, 1500), (5, 16, 800)])
 def test_large_rank_prefix_parity(ctx, oracle, p2g, cfg_id, R, K):
     """R > 16 (warp-per-subject pipeline, R > 32 crosses the warp width) on
     prefixes of the BASELINE R=40 configs: teacher-forced Procrustes + M1 each
