@@ -1193,7 +1193,8 @@ int launch_large_w(p2g_ctx* c, LgArgs a, int max_partials, cudaStream_t s) {
   const int blocks = static_cast<int>(std::max<std::int64_t>(
       1, std::min<std::int64_t>({(K + L::WPB - 1) / L::WPB, static_cast<std::int64_t>(c->num_sms),
                                  static_cast<std::int64_t>(max_partials / L::WPB)})));
-  c->acc_scratch.resize(static_cast<std::size_t>(blocks) * L::WPB * L::slab_doubles(a.max_rows, a.R));
+  grow_scratch(c->acc_scratch, static_cast<std::size_t>(blocks) * L::WPB * L::slab_doubles(a.max_rows, a.R),
+               "large-rank Procrustes path", a.max_rows);
   a.slab = c->acc_scratch.get();
   kern<<<blocks, L::WPB * 32, L::kSmem, s>>>(a);
   return blocks * L::WPB;  // one m1 partial per warp
@@ -1217,7 +1218,7 @@ int launch_procrustes_large(p2g_ctx* c, int R, const double* H, const double* V,
   a.Ewarm = Ewarm;
   a.ew_valid = ew_valid;
   a.max_rows = c->max_rows;
-  a.dbg = std::getenv("P2G_DEBUG") ? c->counters.get() + 4 : nullptr;
+  a.dbg = c->opt.debug ? c->counters.get() + 4 : nullptr;
   if (a.X.K == 0) return 0;
   if (R == 40 && !a.XV) {  // the R = 40 kernel streams X V rows: form them (first step of a fit)
     launch_xv_rows(c, R, V, c->Ubuf.get(), s);

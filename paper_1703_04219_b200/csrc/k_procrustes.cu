@@ -622,7 +622,8 @@ int launch_procrustes_accurate(p2g_ctx* c, int R, const double* H, const double*
   // R x R work matrices (AccSmem).
   std::size_t per_warp = 0;
   P2G_RP_DISPATCH(R, per_warp = AccSmem<RP_>::slab(c->max_rows, R));
-  c->acc_scratch.resize(static_cast<std::size_t>(blocks) * wpb * per_warp);
+  grow_scratch(c->acc_scratch, static_cast<std::size_t>(blocks) * wpb * per_warp, "accurate Procrustes path",
+               c->max_rows);
   a.scratch = c->acc_scratch.get();
   P2G_RP_DISPATCH(R, launch_acc<RP_>(c, a, m1_partials, s));
   return blocks;

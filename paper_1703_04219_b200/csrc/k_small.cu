@@ -869,7 +869,7 @@ static int polar_launch(p2g_ctx* c, std::int64_t K, int R, const double* H, cons
   const int blocks = grid_cap((K + 31) / 32, WPB, c->num_sms, std::max(per_sm, 1));
   const int nb = std::min(blocks, max_blocks);
   kern<<<nb, WPB * 32, smem, s>>>(K, R, H, W, Cbuf, Sbuf, Ewarm, warm, flags, m1p,
-                                  std::getenv("P2G_DEBUG") ? c->counters.get() + 4 : nullptr, perm, sweeps_out);
+                                  c->opt.debug ? c->counters.get() + 4 : nullptr, perm, sweeps_out);
   return nb;
 }
 
@@ -880,7 +880,7 @@ int launch_polar_small(p2g_ctx* c, int R, const double* H, const double* W, cons
   // order subjects by the previous step's sweep counts (stable, 5-bit keys)
   c->polar_sweeps.resize(static_cast<std::size_t>(std::max<std::int64_t>(K, 1)));
   const std::int32_t* perm = nullptr;
-  if (c->polar_sweeps_valid && K > 0 && !std::getenv("P2G_POLAR_NOSORT")) {
+  if (c->polar_sweeps_valid && K > 0 && c->opt.polar_sort) {
     c->polar_perm.resize(static_cast<std::size_t>(2 * K));
     c->polar_keys.resize(static_cast<std::size_t>(K));
     std::int32_t* iota = c->polar_perm.get() + K;

@@ -315,7 +315,7 @@ int procrustes_step(p2g_ctx* c, double* part) {
     {
       Phase ph(c, "polar");
       n1 = launch_polar_small(c, R, c->H.get(), c->W.get(), c->Cbuf.get(), c->Sbuf.get(), c->Ewarm.get(),
-                              (c->ew_valid && std::getenv("P2G_WARM")) ? 1 : 0, c->flags.get(), part,
+                              (c->ew_valid && c->opt.polar_warm) ? 1 : 0, c->flags.get(), part,
                               kMaxPartials, s);
       c->ew_valid = true;
     }
@@ -540,7 +540,7 @@ IterOut iterate(p2g_ctx* c, bool nonneg, int iter) {
     c->fit_phase_ms.push_back(b);
   }
   const std::int32_t* cnt = reinterpret_cast<const std::int32_t*>(c->pinned + 4);
-  if (std::getenv("P2G_DEBUG") && cnt[7] > 0) {
+  if (c->opt.debug && cnt[7] > 0) {
     if (small_rank(c))
       std::fprintf(stderr, "[p2g] iter %d polar sweeps: mean %.2f max %d mean-warp-max %.2f\n", iter,
                    static_cast<double>(cnt[4]) / static_cast<double>(std::max<std::int64_t>(Ks(c), 1)), cnt[5],
@@ -602,6 +602,10 @@ extern "C" int p2g_create(int32_t device, int32_t rank, int32_t world, const cha
       throw CudaError("libp2g is built for sm_100a (B200) only; found sm_" + std::to_string(prop.major) +
                       std::to_string(prop.minor));
     c->num_sms = prop.multiProcessorCount;
+    c->opt.debug = std::getenv("P2G_DEBUG") != nullptr;
+    c->opt.timing = std::getenv("P2G_TIMING") != nullptr;
+    c->opt.polar_warm = std::getenv("P2G_WARM") != nullptr;
+    c->opt.polar_sort = std::getenv("P2G_POLAR_NOSORT") == nullptr;
     P2G_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
     P2G_CUDA(cudaMallocHost(&c->pinned, 64 * sizeof(double)));
     if (world > 1 && nccl_id) {  // (without an id: a host collective must be set before the load)
@@ -737,7 +741,7 @@ extern "C" int p2g_load_csr(p2g_ctx* c, int64_t K, int64_t J, const int64_t* srp
   return guarded([&] {
     if (!c) throw InvalidArgument("null context");
     set_device(c);
-    const bool tim = std::getenv("P2G_TIMING") != nullptr;
+    const bool tim = c->opt.timing;
     const auto tl0 = std::chrono::steady_clock::now();
     auto lap = [&](const char* what) {
       if (tim)
@@ -1035,7 +1039,7 @@ extern "C" int p2g_fit(p2g_ctx* c, const p2g_fit_config* cfg, const double* H0, 
     validate_fit(c, cfg);
     if (!(c->norm_x > 0.0)) throw DataError("tensor has no non-zero entries");
     init_state(c, cfg, H0, V0, W0);
-    if (std::getenv("P2G_TIMING")) {
+    if (c->opt.timing) {
       P2G_CUDA(cudaStreamSynchronize(c->stream));
       std::fprintf(stderr, "[p2g] fit init_state %8.2f ms\n",
                    std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count());
@@ -1069,7 +1073,7 @@ extern "C" int p2g_fit(p2g_ctx* c, const p2g_fit_config* cfg, const double* H0, 
     if (flags_out)
       P2G_CUDA(cudaMemcpyAsync(flags_out, c->flags.get(), sizeof(int32_t) * Ks(c), cudaMemcpyDeviceToHost, c->stream));
     P2G_CUDA(cudaStreamSynchronize(c->stream));
-    if (std::getenv("P2G_TIMING"))
+    if (c->opt.timing)
       std::fprintf(stderr, "[p2g] fit total      %8.2f ms (%d iterations)\n",
                    std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count(), iters);
     if (summary) {

@@ -61,6 +61,22 @@ struct DBuf {
   T* get() const { return p; }
 };
 
+/// Grows a per-warp scratch buffer to `count` elements, refusing with a clear
+/// message when the device cannot hold it (the generic large-R and accurate
+/// Procrustes paths size their slabs by the longest subject, max_rows).
+template <typename T>
+inline void grow_scratch(DBuf<T>& b, std::size_t count, const char* what, std::int64_t max_rows) {
+  if (count <= b.n && b.p) return;
+  std::size_t free_b = 0, total_b = 0;
+  P2G_CUDA(cudaMemGetInfo(&free_b, &total_b));
+  const std::size_t need = count * sizeof(T);
+  if (need > free_b + b.n * sizeof(T))
+    throw CudaError(std::string(what) + ": per-warp scratch for subjects of up to " + std::to_string(max_rows) +
+                    " rows needs " + std::to_string(need >> 20) + " MiB, " + std::to_string(free_b >> 20) +
+                    " MiB free on the device");
+  b.resize(count);
+}
+
 /// Per-phase device timing collected by the fused loop (bench / profiling).
 struct PhaseTimer {
   std::vector<std::string> names;
@@ -139,6 +155,15 @@ struct p2g_ctx {
   p2g::DBuf<std::int32_t> fb_list;    // compacted fallback subject ids
   p2g::DBuf<std::int32_t> counters;   // [0]=n_fallback, [1]=nnls error, ...
   p2g::NnlsWork nnls_ws;
+  // Diagnostics and experiment switches, read once from the environment at
+  // p2g_create (P2G_DEBUG, P2G_TIMING, P2G_WARM, P2G_POLAR_NOSORT); the
+  // defaults are the production configuration.
+  struct Options {
+    bool debug = false;        // sweep / convergence counters to stderr (adds atomics)
+    bool timing = false;       // per-phase event timing on every call
+    bool polar_warm = false;   // R <= 12: warm-start the polar Jacobi from the last eigenvectors
+    bool polar_sort = true;    // R <= 12: order subjects by last sweep count (load balance)
+  } opt;
   p2g::DBuf<double> acc_scratch;      // accurate Procrustes path slabs
   p2g::DBuf<std::int32_t> acc_list;   // flagged subjects (ascending) + count
   p2g::DBuf<unsigned char> acc_bytes, acc_temp;
