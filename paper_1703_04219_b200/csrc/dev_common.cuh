@@ -81,6 +81,11 @@ __device__ __forceinline__ uint4 lds128u(unsigned a) {
   asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a) : "memory");
   return v;
 }
+__device__ __forceinline__ unsigned lds32u(unsigned a) {
+  unsigned v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+  return v;
+}
 /// 32-byte read-only global load (sm_100: LDG.E.256).
 __device__ __forceinline__ double4 ldg256(const double* p) {
   double4 v;

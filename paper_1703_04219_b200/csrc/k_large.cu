@@ -93,9 +93,9 @@ struct LgWarp {
   static constexpr int kVt = RP * LDV;                      // V'^T (kPhys: Jacobi buffer 1)
   static constexpr int NBLK = (RP / 2) * (RP / 2 - 1) / 2;  // off-diagonal 2 x 2 blocks (slot i1 < i2)
   // CTA tables, in doubles (even): uint16 block and round-robin tables; kPhys: the per-lane
-  // plan (uint4 [12][32] blocks: two per block, uint4 [32] diagonal blocks) and the row
+  // plan (uint4 [6][32] and uint [6][32] per block, uint4 [32] diagonal blocks) and the row
   // rotations (int [RP])
-  static constexpr int kTabD = kPhys ? (16 * 13 * 32 + 4 * RP) / 8 : ((NBLK + (RP - 1) * (RP / 2) + 7) / 8) * 2;
+  static constexpr int kTabD = kPhys ? (16 * 7 * 32 + 4 * 6 * 32 + 4 * RP) / 8 : ((NBLK + (RP - 1) * (RP / 2) + 7) / 8) * 2;
   // M, V'^T, w, u (1/sqrt diag), then per pair slot and double-buffered: (c, s), t M_pq, int4 offsets
   // (kPhys: (c, s) only)
   static constexpr int kWarpD = kMat + kVt + 2 * RP + (kPhys ? 2 * RP : 2 * (RP + RP / 2 + RP));
@@ -194,8 +194,9 @@ __global__ void __launch_bounds__(LgWarp<RP>::WPB * 32, 1) k_procrustes_large_w(
   constexpr int LDVx = kPhys ? LDM : LDV;  // V'^T leading dimension after the sweeps
   std::uint16_t* blk = reinterpret_cast<std::uint16_t*>(smem);  // 2 x 2 block (slot i1, slot i2) of M
   std::uint16_t* sched = blk + L::NBLK;                         // round-robin (p, q) per (round, slot)
-  uint4* pplan = reinterpret_cast<uint4*>(smem);                // kPhys: [12][32] blocks, [32] diagonal
-  int* prot = reinterpret_cast<int*>(pplan + 13 * 32);          // kPhys: row rotations of the M layout
+  uint4* pplan = reinterpret_cast<uint4*>(smem);                // kPhys: [6][32] blocks, [32] diagonal
+  unsigned* pplan5 = reinterpret_cast<unsigned*>(pplan + 7 * 32);  // kPhys: [6][32] 5th word of a block
+  int* prot = reinterpret_cast<int*>(pplan5 + 6 * 32);          // kPhys: row rotations of the M layout
   double* M = smem + L::kTabD + wid * L::kWarpDE;
   double* Vt = M + L::kMat;  // V'^T: Vt[p * LDV + k] = V'(k, p)
   double* w = Vt + L::kVt;
@@ -208,13 +209,14 @@ __global__ void __launch_bounds__(LgWarp<RP>::WPB * 32, 1) k_procrustes_large_w(
   if constexpr (kPhys) {
     // the plan as byte offsets: rot(i1) | rot(i2) << 16 (16 B per slot), the rest 8 B per element
     for (int x = threadIdx.x; x < RP; x += blockDim.x) prot[x] = c_plan_rot[x];
-    for (int e = threadIdx.x; e < 6 * 32; e += blockDim.x) {  // block j of lane l: [2 j][l], [2 j + 1][l]
+    for (int e = threadIdx.x; e < 6 * 32; e += blockDim.x) {  // block j of lane l: [j][l] (4 words) + [j][l]
       const int j = e >> 5, l = e & 31;
-      pplan[64 * j + l] = make_uint4(c_plan_blk[l][j][0] * 16u, c_plan_blk[l][j][1] * 8u, c_plan_blk[l][j][2] * 8u, 0u);
-      pplan[64 * j + 32 + l] = make_uint4(c_plan_blk[l][j][3] * 8u, c_plan_blk[l][j][4] * 8u, 0u, 0u);
+      pplan[32 * j + l] = make_uint4(c_plan_blk[l][j][0] * 16u, c_plan_blk[l][j][1] * 8u, c_plan_blk[l][j][2] * 8u,
+                                     c_plan_blk[l][j][3] * 8u);
+      pplan5[32 * j + l] = c_plan_blk[l][j][4] * 8u;
     }
     for (int l = threadIdx.x; l < 32; l += blockDim.x)
-      pplan[12 * 32 + l] = l < 20 ? make_uint4(c_plan_diag[l][0] * 8u, c_plan_diag[l][1] * 8u, c_plan_diag[l][2] * 8u, 0u)
+      pplan[6 * 32 + l] = l < 20 ? make_uint4(c_plan_diag[l][0] * 8u, c_plan_diag[l][1] * 8u, c_plan_diag[l][2] * 8u, 0u)
                                  : make_uint4(0u, 0u, 0u, 0u);
   } else
   for (int it = threadIdx.x; it < nblk; it += blockDim.x) {  // (the slots' own 2 x 2 blocks: param_store)
@@ -402,13 +404,14 @@ __global__ void __launch_bounds__(LgWarp<RP>::WPB * 32, 1) k_procrustes_large_w(
         };
         // slot `lane` (< 20): its diagonal block from the buffer at `rd` ...
         // this lane's static share of every round (pplan, byte offsets): blocks
-        // {rot(i1) | rot(i2) << 16, r_pp | r_pq, r_qp | r_qq}, {w_pp | w_pq, w_qp | w_qq}
+        // {rot(i1) | rot(i2) << 16, r_pp | r_pq, r_qp | r_qq, w_pp | w_pq} + {w_qp | w_qq}
         // and (lanes < 20) its slot's diagonal block {r_pp | r_qq, r_pq | w_pp, w_qq | w_pq}
         const unsigned pb = dev::smem_uniform(pplan) + 16u * lane;
+        const unsigned p5 = dev::smem_uniform(pplan5) + 4u * lane;
         auto par_load = [&](unsigned rd) {
           Dg d{0.0, 0.0, 0.0};
           if (lane < 20) {
-            const uint4 g = dev::lds128u(pb + 16u * 12 * 32);
+            const uint4 g = dev::lds128u(pb + 16u * 6 * 32);
             const unsigned dg[3] = {g.x, g.y, g.z};
             d.al = dev::lds64<0>(rd + (dg[0] & 0xffffu));
             d.be = dev::lds64<0>(rd + (dg[0] >> 16));
@@ -428,7 +431,7 @@ __global__ void __launch_bounds__(LgWarp<RP>::WPB * 32, 1) k_procrustes_large_w(
           const double c = on ? dev::rsqrt_nr(fma(tt, tt, 1.0)) : 1.0;
           const double dt = __dmul_rn(tt, d.ga);
           if (lane < 20) {
-            const uint4 g = dev::lds128u(pb + 16u * 12 * 32);
+            const uint4 g = dev::lds128u(pb + 16u * 6 * 32);
             const unsigned dg[3] = {g.x, g.y, g.z};
             dev::sts128<0>(ro + 16u * lane, c, c * tt);
             dev::sts64<0>(wr + (dg[1] >> 16), on ? d.al - dt : d.al);
@@ -444,8 +447,11 @@ __global__ void __launch_bounds__(LgWarp<RP>::WPB * 32, 1) k_procrustes_large_w(
             double2 r1[2], r2[2];
             double x[2][4];
 #pragma unroll
+            unsigned q4[2];
+#pragma unroll
             for (int v = 0; v < 2; ++v) {
-              const uint4 q = dev::lds128u(pb + 16u * 64 * (j0 + v));
+              const uint4 q = dev::lds128u(pb + 16u * 32 * (j0 + v));
+              q4[v] = q.w;
               r1[v] = dev::lds128<0>(ro + (q.x & 0xffffu));
               r2[v] = dev::lds128<0>(ro + (q.x >> 16));
               x[v][0] = dev::lds64<0>(rd + (q.y & 0xffffu));  // pp
@@ -455,15 +461,15 @@ __global__ void __launch_bounds__(LgWarp<RP>::WPB * 32, 1) k_procrustes_large_w(
             }
 #pragma unroll
             for (int v = 0; v < 2; ++v) {
-              const uint4 q = dev::lds128u(pb + 16u * (64 * (j0 + v) + 32));
+              const unsigned w5 = dev::lds32u(p5 + 4u * 32 * (j0 + v));
               const double c1 = r1[v].x, s1 = r1[v].y, c2 = r2[v].x, s2 = r2[v].y;
               const double x11 = x[v][0], x12 = x[v][1], x21 = x[v][2], x22 = x[v][3];
               const double y11 = c2 * x11 - s2 * x12, y12 = s2 * x11 + c2 * x12;
               const double y21 = c2 * x21 - s2 * x22, y22 = s2 * x21 + c2 * x22;
-              dev::sts64<0>(wr + (q.x & 0xffffu), c1 * y11 - s1 * y21);
-              dev::sts64<0>(wr + (q.x >> 16), c1 * y12 - s1 * y22);
-              dev::sts64<0>(wr + (q.y & 0xffffu), s1 * y11 + c1 * y21);
-              dev::sts64<0>(wr + (q.y >> 16), s1 * y12 + c1 * y22);
+              dev::sts64<0>(wr + (q4[v] & 0xffffu), c1 * y11 - s1 * y21);
+              dev::sts64<0>(wr + (q4[v] >> 16), c1 * y12 - s1 * y22);
+              dev::sts64<0>(wr + (w5 & 0xffffu), s1 * y11 + c1 * y21);
+              dev::sts64<0>(wr + (w5 >> 16), s1 * y12 + c1 * y22);
             }
           }
         };
