@@ -480,10 +480,11 @@ def main():
             dt = float(tt.item())
         h2d = (X.subj_row_ptr.nbytes + X.row_ptr.nbytes + X.col_idx.nbytes + X.val.nbytes + H0.nbytes + V0.nbytes
                + W0.nbytes)
-        d2h = res.H.nbytes + res.V.nbytes + res.W.nbytes + qv.nbytes + res.flags.nbytes + 8 * 3 * e2e_iters
+        # whole-job bytes: every rank returns its shard's Q_k and W rows (and H, V, the trace)
+        d2h = (res.H.nbytes + res.V.nbytes + 8 * X.K * R + 8 * X.n_rows * R + 4 * X.K + 8 * 3 * e2e_iters)
         e2e = {"value": X.nnz * e2e_iters / dt, "unit": "nnz/s", "h2d_bytes_per_step": h2d // e2e_iters,
                "d2h_bytes_per_step": d2h // e2e_iters, "iterations_per_call": e2e_iters, "sec_per_call": dt,
-               "load_s": t_load, "fit_s": dt - t_load, "q_bytes": qv.nbytes,
+               "load_s": t_load, "fit_s": dt - t_load, "q_bytes": 8 * X.n_rows * R,
                "what": "load(pinned CSR) + fit_parafac2 with every Q_k, H, V, W returned to pinned host memory",
                "fit_final": float(res.fit[-1])}
         del pin, Xp, qt, qv, outs
