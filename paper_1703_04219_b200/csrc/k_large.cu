@@ -446,7 +446,6 @@ __global__ void __launch_bounds__(LgWarp<RP>::WPB * 32, 1) k_procrustes_large_w(
           for (int j0 = 0; j0 < 6; j0 += 2) {
             double2 r1[2], r2[2];
             double x[2][4];
-#pragma unroll
             unsigned q4[2];
 #pragma unroll
             for (int v = 0; v < 2; ++v) {
