@@ -90,12 +90,14 @@ struct LgWarp {
   static constexpr int LDV = RP + 2;  // V'^T: even, 16-byte rows for the paired updates
   static constexpr int LDP = RP + 1;  // kPhys: rotated rows of the physical-order M (odd stride)
   static constexpr int kMat = kPhys ? RP * LDP : RP * LDM;  // M (kPhys: Jacobi buffer 0)
-  static constexpr int kVt = RP * LDV;                      // V'^T (kPhys: Jacobi buffer 1)
+  static constexpr int kVt = kPhys ? RP * LDP : RP * LDV;   // V'^T (kPhys: Jacobi buffer 1)
   static constexpr int NBLK = (RP / 2) * (RP / 2 - 1) / 2;  // off-diagonal 2 x 2 blocks (slot i1 < i2)
   // CTA tables, in doubles (even): uint16 block and round-robin tables; kPhys: the per-lane
-  // plan (uint4 [6][32] and uint [6][32] per block, uint4 [32] diagonal blocks) and the row
-  // rotations (int [RP])
-  static constexpr int kTabD = kPhys ? (16 * 7 * 32 + 4 * 6 * 32 + 4 * RP) / 8 : ((NBLK + (RP - 1) * (RP / 2) + 7) / 8) * 2;
+  // plan (uint4 [6][32] and uint [6][32] per block, uint4 [32] diagonal blocks), the element
+  // addresses (uint16 [820], by triangular index) and the elements in address order (uint [820])
+  static constexpr int kTri = RP * (RP + 1) / 2;
+  static constexpr int kTabD =
+      kPhys ? ((16 * 7 * 32 + 4 * 6 * 32 + 6 * kTri + 15) / 16) * 2 : ((NBLK + (RP - 1) * (RP / 2) + 7) / 8) * 2;
   // M, V'^T, w, u (1/sqrt diag), then per pair slot and double-buffered: (c, s), t M_pq, int4 offsets
   // (kPhys: (c, s) only)
   static constexpr int kWarpD = kMat + kVt + 2 * RP + (kPhys ? 2 * RP : 2 * (RP + RP / 2 + RP));
@@ -183,7 +185,7 @@ __device__ __forceinline__ void warp_mm(int rows, int R, FA fa, FB fb, Epi epi) 
 template <int RP, bool EXACT>
 __global__ void __launch_bounds__(LgWarp<RP>::WPB * 32, 1) k_procrustes_large_w(LgArgs a) {
   using L = LgWarp<RP, EXACT>;
-  constexpr int LDM = L::LDM, LDV = L::LDV, LDP = L::LDP, NB = L::NB, WPB = L::WPB;
+  constexpr int LDM = L::LDM, LDV = L::LDV, NB = L::NB, WPB = L::WPB;
   extern __shared__ __align__(16) double smem[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int R = EXACT ? RP : a.R;
@@ -196,7 +198,8 @@ __global__ void __launch_bounds__(LgWarp<RP>::WPB * 32, 1) k_procrustes_large_w(
   std::uint16_t* sched = blk + L::NBLK;                         // round-robin (p, q) per (round, slot)
   uint4* pplan = reinterpret_cast<uint4*>(smem);                // kPhys: [6][32] blocks, [32] diagonal
   unsigned* pplan5 = reinterpret_cast<unsigned*>(pplan + 7 * 32);  // kPhys: [6][32] 5th word of a block
-  int* prot = reinterpret_cast<int*>(pplan5 + 6 * 32);          // kPhys: row rotations of the M layout
+  unsigned* pelem = pplan5 + 6 * 32;  // kPhys: M's elements in address order (addr | x << 16 | y << 24)
+  std::uint16_t* paddr = reinterpret_cast<std::uint16_t*>(pelem + L::kTri);  // kPhys: address of (x <= y)
   double* M = smem + L::kTabD + wid * L::kWarpDE;
   double* Vt = M + L::kMat;  // V'^T: Vt[p * LDV + k] = V'(k, p)
   double* w = Vt + L::kVt;
@@ -208,7 +211,10 @@ __global__ void __launch_bounds__(LgWarp<RP>::WPB * 32, 1) k_procrustes_large_w(
   int4* ofsb = reinterpret_cast<int4*>(rtb + RP);
   if constexpr (kPhys) {
     // the plan as byte offsets: rot(i1) | rot(i2) << 16 (16 B per slot), the rest 8 B per element
-    for (int x = threadIdx.x; x < RP; x += blockDim.x) prot[x] = c_plan_rot[x];
+    for (int e = threadIdx.x; e < L::kTri; e += blockDim.x) {
+      pelem[e] = c_plan_elem[e];
+      paddr[e] = c_plan_addr[e];
+    }
     for (int e = threadIdx.x; e < 6 * 32; e += blockDim.x) {  // block j of lane l: [j][l] (4 words) + [j][l]
       const int j = e >> 5, l = e & 31;
       pplan[32 * j + l] = make_uint4(c_plan_blk[l][j][0] * 16u, c_plan_blk[l][j][1] * 8u, c_plan_blk[l][j][2] * 8u,
@@ -363,8 +369,7 @@ __global__ void __launch_bounds__(LgWarp<RP>::WPB * 32, 1) k_procrustes_large_w(
                   const int xi = i == 39 ? 1 : (i < 20 ? 2 * i : 2 * (39 - i) + 1);
                   const int xj = j == 39 ? 1 : (j < 20 ? 2 * j : 2 * (39 - j) + 1);
                   const int x = min(xi, xj), y = max(xi, xj);
-                  const int c = y + prot[x];
-                  M[LDP * x + (c >= LDP ? c - LDP : c)] = accM[t][h];
+                  M[paddr[x * (2 * RP + 1 - x) / 2 + y - x]] = accM[t][h];
                 }
                 finite &= isfinite(accM[t][h]);
               }
@@ -543,8 +548,7 @@ __global__ void __launch_bounds__(LgWarp<RP>::WPB * 32, 1) k_procrustes_large_w(
         };
         int cur = 0;  // the buffer holding M at sweep boundaries (round-0 arrangement)
         auto at = [&](const double* Mc, int x, int y) {  // element (x <= y)
-          const int c = y + prot[x];
-          return Mc[LDP * x + (c >= LDP ? c - LDP : c)];
+          return Mc[paddr[x * (2 * RP + 1 - x) / 2 + y - x]];
         };
         for (int sweep = 0; sweep < kLgMaxSweeps; ++sweep, ++sweeps) {
           const double* Mc = M + cur * L::kMat;
@@ -554,23 +558,23 @@ __global__ void __launch_bounds__(LgWarp<RP>::WPB * 32, 1) k_procrustes_large_w(
           u[lane] = d0 > tiny ? 1.0 / sqrt(d0) : 0.0;
           if (lane < 8) u[32 + lane] = d1 > tiny ? 1.0 / sqrt(d1) : 0.0;
           __syncwarp();
-          // scaled off-diagonal: lane < 20 walks physical rows lane and 39 - lane
+          // scaled off-diagonal over the elements in address order (the diagonal adds 1 each)
           double omax = 0.0, osum = 0.0;
-          if (lane < 20) {
-#pragma unroll 1
-            for (int side = 0; side < 2; ++side) {
-              const int x = side ? RP - 1 - lane : lane;
-              const double ux = u[x];
-              const double* row = Mc + LDP * x;
-              int c = x + 1 + prot[x];
-              if (c >= LDP) c -= LDP;
-#pragma unroll 4
-              for (int y = x + 1; y < RP; ++y) {
-                const double v = row[c] * ux * u[y];
-                omax = fmax(omax, fabs(v));
-                osum = fma(v, v, osum);
-                c = c + 1 == LDP ? 0 : c + 1;
-              }
+#pragma unroll 2
+          for (int e0 = 0; e0 < L::kTri; e0 += 64) {
+            const int ea = e0 + lane, eb = e0 + 32 + lane;
+            const unsigned pa = pelem[ea < L::kTri ? ea : 0], pb2 = pelem[eb < L::kTri ? eb : 0];
+            const double va = Mc[pa & 0xffffu] * u[(pa >> 16) & 0xffu] * u[pa >> 24];
+            const double vb = Mc[pb2 & 0xffffu] * u[(pb2 >> 16) & 0xffu] * u[pb2 >> 24];
+            const bool oa = ea < L::kTri && ((pa >> 16) & 0xffu) != (pa >> 24);
+            const bool ob = eb < L::kTri && ((pb2 >> 16) & 0xffu) != (pb2 >> 24);
+            if (oa) {
+              omax = fmax(omax, fabs(va));
+              osum = fma(va, va, osum);
+            }
+            if (ob) {
+              omax = fmax(omax, fabs(vb));
+              osum = fma(vb, vb, osum);
             }
           }
           omax = dev::warp_max(omax);

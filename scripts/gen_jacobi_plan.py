@@ -11,11 +11,17 @@ lane -> block assignment is chosen to minimise shared-memory bank conflicts
 (64-bit accesses served per half-warp over 16 bank pairs, 128-bit per
 quarter-warp over 8 groups of four banks -- the model ncu's counts follow).
 
-Element (x, y), x <= y, of the upper triangle is stored at
-    41 x + (y + rot(x)) mod 41
-(each row is rotated inside its odd 41-double stride: with an even stride all
-entries of one kind (pp, pq, qp, qq) would share an address parity and half
-the bank pairs, a 2x conflict for every 64-bit access).
+Element addresses.  Every address is static and comes from a table, so the
+layout is free: element e of the upper triangle is read by exactly one
+(instruction, half-warp) group and written (as the sigma-image of a rotated
+entry) by exactly one.  Elements are the edges of a bipartite multigraph
+between read groups and write groups, every group has at most 16 elements, and
+a 64-bit access is conflict-free when the 16 lanes of a half-warp hit 16
+different bank pairs.  By Koenig's theorem the edges have a proper colouring
+with 16 colours: colour = bank pair, address = 16 * row + colour.  Every M
+access of the round then costs the ideal two wavefronts (round 2's rotated
+41-stride rows measured 4).  The lane -> block assignment is annealed only for
+the 128-bit loads of the slots' (c, s) pairs.
 
 Per lane l, block j (j < 6; 190 off-diagonal 2 x 2 blocks of slot pairs
 i1 < i2 in 192 (lane, j) places, 2 empty): i1, i2, the two row bases of the
@@ -28,7 +34,7 @@ import math
 import os
 import random
 
-RP, H, LDM = 40, 20, 41
+RP, H = 40, 20
 NLANE, NJ = 32, 6
 
 
@@ -42,33 +48,17 @@ def sigma(x):
     return x - 2 if x % 2 == 0 else x + 2
 
 
-def addr(x, y, swz):
-    if x > y:
-        x, y = y, x
-    return LDM * x + (y + swz[x]) % LDM
-
-
 BLOCKS = [(i1, i2) for i1 in range(H) for i2 in range(i1 + 1, H)]
+SUB = ((0, 0), (0, 1), (1, 0), (1, 1))  # pp, pq, qp, qq
 
 
-def block_acc(b, swz):
-    i1, i2 = b
-    rd = [addr(2 * i1 + a, 2 * i2 + c, swz) for a in (0, 1) for c in (0, 1)]
-    wr = [addr(sigma(2 * i1 + a), sigma(2 * i2 + c), swz) for a in (0, 1) for c in (0, 1)]
-    return rd + wr
-
-
-def diag_acc(i, swz):
-    p, q = 2 * i, 2 * i + 1
-    rd = [addr(p, p, swz), addr(q, q, swz), addr(p, q, swz)]
-    wr = [addr(sigma(p), sigma(p), swz), addr(sigma(q), sigma(q), swz), addr(sigma(p), sigma(q), swz)]
-    return rd + wr
+def up(x, y):
+    return (x, y) if x <= y else (y, x)
 
 
 def wavefronts(addrs):
     """64-bit shared accesses of one warp instruction, served per half-warp:
-    per half, the largest number of distinct doubles on one bank pair (ncu,
-    round-1 and round-2 kernels: random 64-bit addresses cost ~6.5)."""
+    per half, the largest number of distinct doubles on one bank pair."""
     t = 0
     for h in (addrs[:16], addrs[16:]):
         c = {}
@@ -92,86 +82,170 @@ def wavefronts128(units):
     return t
 
 
-def group_cost(grp, acc):
-    t = 0
-    for k in range(8):
-        t += wavefronts([acc[b][k] if b is not None else None for b in grp])
-    for side in (0, 1):  # rot[i1], rot[i2]: (c, s) pairs of the 20 slots
-        t += wavefronts128([b[side] if b is not None else 0 for b in grp])
-    return t
-
-
-def diag_cost(swz):
-    acc = [diag_acc(i, swz) for i in range(H)]
-    return sum(wavefronts([a[k] for a in acc]) for k in range(6))
+def rot_cost(grp):
+    """(c, s) loads of a block group: rot[i1], rot[i2] of the 20 slots."""
+    return sum(wavefronts128([b[side] if b is not None else 0 for b in grp]) for side in (0, 1))
 
 
 def anneal(seed, iters):
+    """lane -> block places minimising the (c, s) load wavefronts."""
     rnd = random.Random(seed)
-    swz = [rnd.randrange(LDM) for _ in range(RP)]
-    acc = {b: block_acc(b, swz) for b in BLOCKS}
     places = BLOCKS[:] + [None] * (NLANE * NJ - len(BLOCKS))
     rnd.shuffle(places)
     grp = [places[j * NLANE:(j + 1) * NLANE] for j in range(NJ)]
-    costs = [group_cost(g, acc) for g in grp]
-    dcost = diag_cost(swz)
-    cur = sum(costs) + dcost
+    costs = [rot_cost(g) for g in grp]
     for it in range(iters):
-        temp = 1.5 * (1 - it / iters) + 0.02
-        if rnd.random() < 0.03:  # re-draw one row's rotation
-            x = rnd.randrange(RP)
-            old = swz[x]
-            swz[x] = rnd.randrange(LDM)
-            acc2 = {b: block_acc(b, swz) for b in BLOCKS}
-            costs2 = [group_cost(g, acc2) for g in grp]
-            d2 = diag_cost(swz)
-            new = sum(costs2) + d2
-            if new <= cur or rnd.random() < math.exp(-(new - cur) / temp):
-                acc, costs, dcost, cur = acc2, costs2, d2, new
-            else:
-                swz[x] = old
-            continue
+        temp = 1.0 * (1 - it / iters) + 0.02
         g1, g2 = rnd.randrange(NJ), rnd.randrange(NJ)
         a, b = rnd.randrange(NLANE), rnd.randrange(NLANE)
         if g1 == g2 and a == b:
             continue
         grp[g1][a], grp[g2][b] = grp[g2][b], grp[g1][a]
-        c1 = group_cost(grp[g1], acc)
-        c2 = group_cost(grp[g2], acc) if g2 != g1 else 0
+        c1 = rot_cost(grp[g1])
+        c2 = rot_cost(grp[g2]) if g2 != g1 else 0
         d = c1 + c2 - costs[g1] - (costs[g2] if g2 != g1 else 0)
         if d <= 0 or rnd.random() < math.exp(-d / temp):
             costs[g1] = c1
             if g2 != g1:
                 costs[g2] = c2
-            cur += d
         else:
             grp[g1][a], grp[g2][b] = grp[g2][b], grp[g1][a]
-    return cur, swz, grp, costs, dcost
+    return sum(costs), grp
+
+
+def access_groups(grp):
+    """element -> [read group, write group].  Elements: (x, y), x <= y, and four
+    private dummies per empty (lane, j) place (read and written in place, so the
+    round needs no branch)."""
+    edges = {}
+    for j in range(NJ):
+        for lane in range(NLANE):
+            b, half = grp[j][lane], lane // 16
+            for e, (a, c) in enumerate(SUB):
+                g = ("B", j, e, half)
+                if b is None:
+                    edges[("dummy", j, lane, e)] = [g, g]
+                    continue
+                x, y = 2 * b[0] + a, 2 * b[1] + c
+                edges.setdefault((x, y), [None, None])[0] = g
+                edges.setdefault(up(sigma(x), sigma(y)), [None, None])[1] = g
+    for i in range(H):
+        p, q, half = 2 * i, 2 * i + 1, i // 16
+        for k, (x, y) in enumerate(((p, p), (q, q), (p, q))):
+            edges.setdefault((x, y), [None, None])[0] = ("D", k, half)
+            edges.setdefault(up(sigma(x), sigma(y)), [None, None])[1] = ("D", k, half)
+    real = [e for e in edges if e[0] != "dummy"]
+    assert len(real) == RP * (RP + 1) // 2 and all(r is not None and w is not None for r, w in edges.values())
+    return edges
+
+
+def edge_colouring(edges, ncol=16):
+    """Proper edge colouring of the bipartite multigraph (read groups | write
+    groups) with `ncol` colours (every group has at most `ncol` elements):
+    the alternating-path construction behind Koenig's theorem."""
+    at = {}  # (side, group) -> {colour: element}
+    col = {}
+    for el, (r, w) in sorted(edges.items(), key=lambda kv: str(kv[0])):
+        u, v = (0, r), (1, w)
+        cu, cv = at.setdefault(u, {}), at.setdefault(v, {})
+        a = next(c for c in range(ncol) if c not in cu)
+        b = next(c for c in range(ncol) if c not in cv)
+        if a != b and a in cv:
+            # flip the a/b path that starts at v along colour a: afterwards a is free at v (and still at u:
+            # the path alternates sides and can only end at u through colour a, which u lacks)
+            path, node, want = [], v, a
+            while want in at[node]:
+                e2 = at[node][want]
+                path.append((e2, want))
+                r2, w2 = edges[e2]
+                node = (0, r2) if node[0] == 1 else (1, w2)
+                want = b if want == a else a
+            for e2, c in path:
+                r2, w2 = edges[e2]
+                del at[(0, r2)][c], at[(1, w2)][c]
+            for e2, c in path:
+                r2, w2 = edges[e2]
+                c2 = b if c == a else a
+                at[(0, r2)][c2] = e2
+                at[(1, w2)][c2] = e2
+                col[e2] = c2
+        col[el] = a
+        cu[a] = el
+        cv[a] = el
+    for g, m in at.items():
+        assert len(m) <= ncol
+    for el, (r, w) in edges.items():
+        assert at[(0, r)][col[el]] == el and at[(1, w)][col[el]] == el
+    return col
+
+
+def layout(grp):
+    """element -> address (in doubles): 16 * row + bank pair."""
+    edges = access_groups(grp)
+    col = edge_colouring(edges)
+    rows = [0] * 16
+    addr = {}
+    for el in sorted(edges, key=lambda e: (e[0] == "dummy", str(type(e[0])), e)):
+        c = col[el]
+        addr[el] = 16 * rows[c] + c
+        rows[c] += 1
+    return addr, 16 * max(rows)
+
+
+def round_wavefronts(grp, addr):
+    t = 0
+    for j in range(NJ):
+        for e, (a, c) in enumerate(SUB):
+            rd, wr = [], []
+            for lane in range(NLANE):
+                b = grp[j][lane]
+                if b is None:
+                    rd.append(addr[("dummy", j, lane, e)])
+                    wr.append(addr[("dummy", j, lane, e)])
+                else:
+                    x, y = 2 * b[0] + a, 2 * b[1] + c
+                    rd.append(addr[(x, y)])
+                    wr.append(addr[up(sigma(x), sigma(y))])
+            t += wavefronts(rd) + wavefronts(wr)
+    for k in range(3):
+        rd, wr = [], []
+        for i in range(H):
+            x, y = ((2 * i, 2 * i), (2 * i + 1, 2 * i + 1), (2 * i, 2 * i + 1))[k]
+            rd.append(addr[(x, y)])
+            wr.append(addr[up(sigma(x), sigma(y))])
+        t += wavefronts(rd + [None] * 12) + wavefronts(wr + [None] * 12)
+    return t
 
 
 def main():
     best = None
     for seed in range(4):
-        r = anneal(seed, 200000)
-        print(f"seed {seed}: wavefronts per round {r[0]} (blocks {sum(r[3])}, diagonal {r[4]})")
+        r = anneal(seed, 100000)
+        print(f"seed {seed}: (c, s) load wavefronts per round {r[0]}")
         if best is None or r[0] < best[0]:
             best = r
-    cur, swz, grp, costs, dcost = best
-    ideal = NJ * (8 * 2 + 2 * 4) + 6 * 2
-    # an unused slot of the canonical layout (element (39, 0)): target of the
-    # two empty (lane, j) places, so the round needs no branch
-    dummy = LDM * 39 + (0 + swz[39]) % LDM
-    used = {addr(x, y, swz) for x in range(RP) for y in range(x, RP)}
-    assert dummy not in used and len(used) == RP * (RP + 1) // 2
+    rcost, grp = best
+    addr, size = layout(grp)
+    mw = round_wavefronts(grp, addr)
+    ideal = NJ * 8 * 2 + 6 * 2
+    assert mw == ideal, (mw, ideal)
+    assert len(set(addr.values())) == len(addr) and size <= RP * (RP + 1)
+    tri = [addr[(x, y)] for x in range(RP) for y in range(x, RP)]  # x (81 - x) / 2 + y - x
+    by_addr = sorted((addr[(x, y)], x, y) for x in range(RP) for y in range(x, RP))
     lines = [
         "// Generated by scripts/gen_jacobi_plan.py -- do not edit.",
-        f"// R = 40 Jacobi round plan: {cur} shared-memory wavefronts per round for the M",
-        f"// block and diagonal-block accesses (ideal {ideal}; whole-warp 64-bit bank model).",
-        "// Element (x, y), x <= y, of M (physical positions) sits at 41 x + (y + c_plan_rot[x]) % 41.",
-        f"__constant__ int c_plan_rot[{RP}] = {{" + ", ".join(str(v) for v in swz) + "};",
+        f"// R = 40 Jacobi round plan: {mw} shared-memory wavefronts per round for the M block and",
+        f"// diagonal-block accesses (= ideal: bank pairs by bipartite edge colouring), {rcost} for the (c, s) loads.",
+        f"// The physical-order upper triangle of M occupies {size} doubles of a Jacobi buffer.",
+        f"constexpr int kPlanDoubles = {size};",
+        "// address (in doubles) of element (x, y), x <= y (physical positions), at x (81 - x) / 2 + y - x",
+        f"__constant__ unsigned short c_plan_addr[{len(tri)}] = {{" + ", ".join(str(v) for v in tri) + "};",
+        "// the same elements in address order: addr | x << 16 | y << 24",
+        f"__constant__ unsigned c_plan_elem[{len(by_addr)}] = {{" +
+        ", ".join(f"{a | x << 16 | y << 24}u" for a, x, y in by_addr) + "};",
         "// per lane, per block j: {i1 | i2 << 16, r_pp | r_pq << 16, r_qp | r_qq << 16,",
-        "//                         w_pp | w_pq << 16, w_qp | w_qq << 16}  (element indices; the w_*",
-        "// are the sigma-images of the rotated entries; empty places: slot 0, the dummy slot)",
+        "//                         w_pp | w_pq << 16, w_qp | w_qq << 16}  (element addresses; the w_*",
+        "// are the sigma-images of the rotated entries; empty places: slot 0, private dummy cells)",
         f"__constant__ unsigned c_plan_blk[{NLANE}][{NJ}][5] = {{",
     ]
     for lane in range(NLANE):
@@ -179,17 +253,23 @@ def main():
         for j in range(NJ):
             b = grp[j][lane]
             if b is None:
-                ent.append("{0u, %du, %du, %du, %du}" % ((dummy | dummy << 16,) * 4))
-                continue
-            a = block_acc(b, swz)
-            ent.append("{%du, %du, %du, %du, %du}" % (b[0] | b[1] << 16, a[0] | a[1] << 16, a[2] | a[3] << 16,
+                d = [addr[("dummy", j, lane, e)] for e in range(4)]
+                a = d + d
+                ids = 0
+            else:
+                a = [addr[(2 * b[0] + x, 2 * b[1] + y)] for x, y in SUB] + \
+                    [addr[up(sigma(2 * b[0] + x), sigma(2 * b[1] + y))] for x, y in SUB]
+                ids = b[0] | b[1] << 16
+            ent.append("{%du, %du, %du, %du, %du}" % (ids, a[0] | a[1] << 16, a[2] | a[3] << 16,
                                                       a[4] | a[5] << 16, a[6] | a[7] << 16))
         lines.append("    {" + ", ".join(ent) + "},")
     lines.append("};")
     lines.append("// per slot i: {r_pp | r_qq << 16, r_pq | w_pp << 16, w_qq | w_pq << 16}")
     lines.append(f"__constant__ unsigned c_plan_diag[{H}][3] = {{")
     for i in range(H):
-        a = diag_acc(i, swz)
+        p, q = 2 * i, 2 * i + 1
+        a = [addr[(p, p)], addr[(q, q)], addr[(p, q)], addr[up(sigma(p), sigma(p))], addr[up(sigma(q), sigma(q))],
+             addr[up(sigma(p), sigma(q))]]
         lines.append("    {%du, %du, %du}," % (a[0] | a[1] << 16, a[2] | a[3] << 16, a[4] | a[5] << 16))
     lines.append("};")
     lines.append("")
@@ -197,7 +277,7 @@ def main():
                        "jacobi_plan40.inc")
     with open(out, "w") as f:
         f.write("\n".join(lines))
-    print(f"wrote {out}: {cur} wavefronts per round (ideal {ideal})")
+    print(f"wrote {out}: {mw} M wavefronts per round (ideal {ideal}), buffer {size} doubles")
 
 
 if __name__ == "__main__":
