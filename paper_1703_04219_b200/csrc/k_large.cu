@@ -404,8 +404,18 @@ __global__ void __launch_bounds__(LgWarp<RP>::WPB * 32, 1) k_procrustes_large_w(
 #pragma unroll
         for (int k = 0; k < 10; ++k) vch[k] = rr_l0(RP, 10 * ch + k) == crow ? 1.0 : 0.0;
         double tiny = 0.0;
+        // Scaled ("fast") rotations: M = D M~ D off the diagonal and V' = V~ D with a scale d_x per
+        // position (both columns of a rotation shrink by the same cosine), so a rotation is
+        // col_p += na col_q, col_q += nb col_p with na = -t d_q / d_p, nb = t d_p / d_q: two FMAs per
+        // element pair instead of four operations, and a dependency depth of one.  The diagonal
+        // entries stay unscaled (only the slot lanes touch them).  (d_x, 1 / d_x) follow the positions
+        // along sigma in the tail of each Jacobi buffer.
+        constexpr unsigned kDs = kPlanDoubles * 8u;
+        static_assert(kPlanDoubles + 2 * RP <= L::kMat, "scales behind the elements");
+        const unsigned dsp = kDs + 16u * (lane == 0 ? 3 : 2 * lane - 2);                    // sigma(2 lane)
+        const unsigned dsq = kDs + 16u * (lane == 0 ? 1 : (lane == 19 ? 38 : 2 * lane + 3));  // sigma(2 lane + 1)
         struct Dg {
-          double al, be, ga;
+          double al, be, gs;  // M_pp, M_qq (true), M~_pq (scaled)
         };
         // slot `lane` (< 20): its diagonal block from the buffer at `rd` ...
         // this lane's static share of every round (pplan, byte offsets): blocks
@@ -420,28 +430,36 @@ __global__ void __launch_bounds__(LgWarp<RP>::WPB * 32, 1) k_procrustes_large_w(
             const unsigned dg[3] = {g.x, g.y, g.z};
             d.al = dev::lds64<0>(rd + (dg[0] & 0xffffu));
             d.be = dev::lds64<0>(rd + (dg[0] >> 16));
-            d.ga = dev::lds64<0>(rd + (dg[1] & 0xffffu));
+            d.gs = dev::lds64<0>(rd + (dg[1] & 0xffffu));
           }
           return d;
         };
         // ... its rotation (c, s) into the rot buffer at `ro`, the rotated
         // block's sigma-images into the buffer at `wr` (rotation as in the
         // generic path)
-        auto par_store = [&](const Dg& d, unsigned wr, unsigned ro) {
-          const bool on = d.al > tiny && d.be > tiny && d.ga * d.ga > (kSkipL * kSkipL) * (d.al * d.be);
-          const double dd = d.be - d.al, g2 = 2.0 * d.ga;
+        auto par_store = [&](const Dg& d, unsigned rd, unsigned wr, unsigned ro) {
+          // (d, 1 / d) of positions 2 lane, 2 lane + 1
+          const double2 sp = lane < 20 ? dev::lds128<0>(rd + kDs + 32u * lane) : make_double2(1.0, 1.0);
+          const double2 sq = lane < 20 ? dev::lds128<0>(rd + kDs + 32u * lane + 16u) : make_double2(1.0, 1.0);
+          const double ga = d.gs * (sp.x * sq.x);
+          const bool on = d.al > tiny && d.be > tiny && ga * ga > (kSkipL * kSkipL) * (d.al * d.be);
+          const double dd = d.be - d.al, g2 = 2.0 * ga;
           const double h = on ? fma(dd, dd, g2 * g2) : 1.0;
           const double rh = h * dev::rsqrt_nr(h);
           const double tt = on ? (dd >= 0.0 ? g2 : -g2) * dev::rcp_nr(fabs(dd) + rh) : 0.0;
-          const double c = on ? dev::rsqrt_nr(fma(tt, tt, 1.0)) : 1.0;
-          const double dt = __dmul_rn(tt, d.ga);
+          const double dt = __dmul_rn(tt, ga);
           if (lane < 20) {
             const uint4 g = dev::lds128u(pb + 16u * 6 * 32);
             const unsigned dg[3] = {g.x, g.y, g.z};
-            dev::sts128<0>(ro + 16u * lane, c, c * tt);
+            dev::sts128<0>(ro + 16u * lane, -tt * (sq.x * sp.y), tt * (sp.x * sq.y));
             dev::sts64<0>(wr + (dg[1] >> 16), on ? d.al - dt : d.al);
             dev::sts64<0>(wr + (dg[2] & 0xffffu), on ? d.be + dt : d.be);
-            dev::sts64<0>(wr + (dg[2] >> 16), on ? 0.0 : d.ga);
+            dev::sts64<0>(wr + (dg[2] >> 16), on ? 0.0 : d.gs);
+            // the positions' scales shrink by c = (1 + t^2)^{-1/2} and move along sigma
+            const double t2 = fma(tt, tt, 1.0);
+            const double c = on ? dev::rsqrt_nr(t2) : 1.0, ic = on ? t2 * c : 1.0;
+            dev::sts128<0>(wr + dsp, c * sp.x, ic * sp.y);
+            dev::sts128<0>(wr + dsq, c * sq.x, ic * sq.y);
           }
         };
         // M <- J^T M J over this lane's six 2 x 2 blocks, two at a time (their
@@ -466,14 +484,14 @@ __global__ void __launch_bounds__(LgWarp<RP>::WPB * 32, 1) k_procrustes_large_w(
 #pragma unroll
             for (int v = 0; v < 2; ++v) {
               const unsigned w5 = dev::lds32u(p5 + 4u * 32 * (j0 + v));
-              const double c1 = r1[v].x, s1 = r1[v].y, c2 = r2[v].x, s2 = r2[v].y;
+              const double a1 = r1[v].x, b1 = r1[v].y, a2 = r2[v].x, b2 = r2[v].y;
               const double x11 = x[v][0], x12 = x[v][1], x21 = x[v][2], x22 = x[v][3];
-              const double y11 = c2 * x11 - s2 * x12, y12 = s2 * x11 + c2 * x12;
-              const double y21 = c2 * x21 - s2 * x22, y22 = s2 * x21 + c2 * x22;
-              dev::sts64<0>(wr + (q4[v] & 0xffffu), c1 * y11 - s1 * y21);
-              dev::sts64<0>(wr + (q4[v] >> 16), c1 * y12 - s1 * y22);
-              dev::sts64<0>(wr + (w5 & 0xffffu), s1 * y11 + c1 * y21);
-              dev::sts64<0>(wr + (w5 >> 16), s1 * y12 + c1 * y22);
+              const double y11 = fma(a2, x12, x11), y12 = fma(b2, x11, x12);
+              const double y21 = fma(a2, x22, x21), y22 = fma(b2, x21, x22);
+              dev::sts64<0>(wr + (q4[v] & 0xffffu), fma(a1, y21, y11));
+              dev::sts64<0>(wr + (q4[v] >> 16), fma(a1, y22, y12));
+              dev::sts64<0>(wr + (w5 & 0xffffu), fma(b1, y11, y21));
+              dev::sts64<0>(wr + (w5 >> 16), fma(b1, y12, y22));
             }
           }
         };
@@ -483,8 +501,8 @@ __global__ void __launch_bounds__(LgWarp<RP>::WPB * 32, 1) k_procrustes_large_w(
           for (int i = 0; i < RP / 2; ++i) {
             const double2 r = dev::lds128<0>(ro + 16u * i);
             const double x0 = vreg[2 * i], y0 = vreg[2 * i + 1];
-            vreg[2 * i] = r.x * x0 - r.y * y0;
-            vreg[2 * i + 1] = r.y * x0 + r.x * y0;
+            vreg[2 * i] = fma(r.x, y0, x0);
+            vreg[2 * i + 1] = fma(r.y, x0, y0);
           }
           const double t0 = vreg[0];
 #pragma unroll
@@ -498,8 +516,8 @@ __global__ void __launch_bounds__(LgWarp<RP>::WPB * 32, 1) k_procrustes_large_w(
           for (int k = 0; k < 5; ++k) {
             const double2 r = dev::lds128<0>(cb + 16u * k);
             const double x0 = vch[2 * k], y0 = vch[2 * k + 1];
-            vch[2 * k] = r.x * x0 - r.y * y0;
-            vch[2 * k + 1] = r.y * x0 + r.x * y0;
+            vch[2 * k] = fma(r.x, y0, x0);
+            vch[2 * k + 1] = fma(r.y, x0, y0);
           }
           // positions 10 ch + 8 <- 10 ch + 10 (next chunk) and 10 ch + 1 <- 10 ch - 1
           // (previous chunk); chunk 0 holds the cycle's ends 3 <- 0 and 1 (fixed)
@@ -520,43 +538,54 @@ __global__ void __launch_bounds__(LgWarp<RP>::WPB * 32, 1) k_procrustes_large_w(
         // one sweep (m - 1 = 39 rounds) from buffer A to buffer B: rounds in
         // pairs (A -> B with rot buffer 0, B -> A with rot buffer 1), then the last
         auto run_sweep = [&](unsigned A, unsigned B) {
-          par_store(par_load(A), B, rb);
+          par_store(par_load(A), A, B, rb);
           __syncwarp();
+          // one round per iteration (the two buffers and the two rotation buffers swap roles):
+          // the loop body stays small for the instruction caches
+          unsigned ra = A, wb = B, ro = rb, ro2 = rb + 320u;
 #pragma unroll 1
-          for (int rr = 0; rr < RP - 2; rr += 2) {
-            blocks(A, B, rb);
+          for (int rr = 0; rr < RP - 2; ++rr) {
+            blocks(ra, wb, ro);
             __syncwarp();
             {
-              const Dg d = par_load(B);
-              vupd(rb);
-              par_store(d, A, rb + 320u);
+              const Dg d = par_load(wb);
+              vupd(ro);
+              par_store(d, wb, ra, ro2);
             }
             __syncwarp();
-            blocks(B, A, rb + 320u);
-            __syncwarp();
-            {
-              const Dg d = par_load(A);
-              vupd(rb + 320u);
-              par_store(d, B, rb);
-            }
-            __syncwarp();
+            const unsigned t1 = ra, t2 = ro;
+            ra = wb;
+            wb = t1;
+            ro = ro2;
+            ro2 = t2;
           }
-          blocks(A, B, rb);
+          blocks(ra, wb, ro);
           __syncwarp();
-          vupd(rb);
+          vupd(ro);
           __syncwarp();
         };
         int cur = 0;  // the buffer holding M at sweep boundaries (round-0 arrangement)
+        for (int x = lane; x < RP; x += 32) M[kPlanDoubles + 2 * x] = M[kPlanDoubles + 2 * x + 1] = 1.0;
         auto at = [&](const double* Mc, int x, int y) {  // element (x <= y)
           return Mc[paddr[x * (2 * RP + 1 - x) / 2 + y - x]];
         };
         for (int sweep = 0; sweep < kLgMaxSweeps; ++sweep, ++sweeps) {
-          const double* Mc = M + cur * L::kMat;
+          double* Mc = M + cur * L::kMat;
           const double d0 = at(Mc, lane, lane), d1 = lane < 8 ? at(Mc, 32 + lane, 32 + lane) : 0.0;
           const double dmax = dev::warp_max(fmax(d0, d1));
           tiny = kTinyL * dmax;
-          u[lane] = d0 > tiny ? 1.0 / sqrt(d0) : 0.0;
-          if (lane < 8) u[32 + lane] = d1 > tiny ? 1.0 / sqrt(d1) : 0.0;
+          // u_x = d_x / sqrt(M_xx): M~_xy u_x u_y is the scaled off-diagonal; 1 / d_x refreshed (no drift)
+          {
+            double* ds = Mc + kPlanDoubles;
+            const double s0 = ds[2 * lane];
+            u[lane] = d0 > tiny ? s0 / sqrt(d0) : 0.0;
+            ds[2 * lane + 1] = 1.0 / s0;
+            if (lane < 8) {
+              const double s1 = ds[2 * (32 + lane)];
+              u[32 + lane] = d1 > tiny ? s1 / sqrt(d1) : 0.0;
+              ds[2 * (32 + lane) + 1] = 1.0 / s1;
+            }
+          }
           __syncwarp();
           // scaled off-diagonal over the elements in address order (the diagonal adds 1 each)
           double omax = 0.0, osum = 0.0;
@@ -596,18 +625,22 @@ __global__ void __launch_bounds__(LgWarp<RP>::WPB * 32, 1) k_procrustes_large_w(
         {
           const double* Mc = M + cur * L::kMat;
           double* Ml = M + (cur ^ 1) * L::kMat;
+          __syncwarp();
+          for (int x = lane; x < RP; x += 32) u[x] = Mc[kPlanDoubles + 2 * x];  // the positions' scales
+          __syncwarp();
           for (int e = lane; e < RP * RP; e += 32) {
             const int p = e / RP, q = e - p * RP;
             const int xp = p == RP - 1 ? 1 : (p < RP / 2 ? 2 * p : 2 * (RP - 1 - p) + 1);
             const int xq = q == RP - 1 ? 1 : (q < RP / 2 ? 2 * q : 2 * (RP - 1 - q) + 1);
-            Ml[p * LDM + q] = at(Mc, min(xp, xq), max(xp, xq));
+            const double v = at(Mc, min(xp, xq), max(xp, xq));
+            Ml[p * LDM + q] = p == q ? v : v * (u[xp] * u[xq]);
           }
           __syncwarp();
           double* V2 = M + cur * L::kMat;
 #pragma unroll
-          for (int x = 0; x < RP; ++x) V2[rr_l0(RP, x) * LDM + lane] = vreg[x];
+          for (int x = 0; x < RP; ++x) V2[rr_l0(RP, x) * LDM + lane] = vreg[x] * u[x];
 #pragma unroll
-          for (int k = 0; k < 10; ++k) V2[rr_l0(RP, 10 * ch + k) * LDM + crow] = vch[k];
+          for (int k = 0; k < 10; ++k) V2[rr_l0(RP, 10 * ch + k) * LDM + crow] = vch[k] * u[10 * ch + k];
           __syncwarp();
           Mx = Ml;
           Vx = V2;
