@@ -52,6 +52,12 @@ __device__ __forceinline__ double rcp_nr(double x) {
   return y;
 }
 
+/// Bulk (TMA) prefetch of `bytes` (a multiple of 16) at the 16-byte aligned global address p
+/// into L2: one instruction by one lane, no destination buffer.
+__device__ __forceinline__ void prefetch_l2_bulk(const void* p, unsigned bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
 /// Shared-memory accesses at a 32-bit shared address plus a compile-time
 /// byte offset (ptxas folds a warp-uniform base into [R + UR + imm]).  The
 /// asm statements keep their source order, so a batch of loads written ahead

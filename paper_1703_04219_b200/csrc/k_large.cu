@@ -112,7 +112,7 @@ struct LgWarp {
   static constexpr int NB = RP / 8;  // 8-wide tensor tiles (RP multiple of 8)
   // per-warp global slab: B, X~ (max_rows x R each), T, F, E, N, M1 (R x R), s (R)
   __host__ __device__ static std::size_t slab_doubles(std::int64_t max_rows, int R) {
-    if (kPhys) return 3 * static_cast<std::size_t>(R) * R + RP;  // T', a scratch, the m1 partial (rows streamed, E in place)
+    if (kPhys) return static_cast<std::size_t>(R) * R + RP;  // the m1 partial and sqrt(diag M') (rows streamed, E in place)
     return 2 * static_cast<std::size_t>(max_rows > 1 ? max_rows : 1) * R +
            5 * static_cast<std::size_t>(R) * R + RP;
   }
@@ -286,11 +286,13 @@ __global__ void __launch_bounds__(LgWarp<RP>::WPB * 32, 1) k_procrustes_large_w(
     // place in Ewarm (a row tile of E' = E V' depends only on the same rows of
     // E).  The product order is the generic path's: W = H^T (E' S' E'^T)
     // measured 30x further from the oracle on cfg5's ill-conditioned subjects.
-    // Per-warp global scratch: T', one R x R scratch (A, then Y), the m1 partial.
+    // After the sweeps every R x R operand lives in the warp's two shared buffers
+    // (the ~24 KB of L1 left beside 229 KB of shared memory cannot hold per-warp
+    // global scratch, whose reads were L2 round trips): W is formed as
+    // ((H^T E') S') E'^T, each product in place over its left operand's row tiles.
+    // Per-warp global scratch: the m1 partial and sqrt(diag M').
     constexpr int LDS = LDM;
-    double* const Ts = slab;       // T' = H^T E
-    double* const As = Ts + RR;    // scratch: A = P o N, then Y = V' S'
-    double* const M1 = As + RR;    // this warp's m1 partial
+    double* const M1 = slab;       // this warp's m1 partial
     double* const sv = M1 + RR;    // sqrt(M'_pp)
     double* const Ms0 = M;         // shared buffer 0 (the M region)
     double* const Ms1 = M + L::kMat;  // shared buffer 1 (the V'^T region)
@@ -304,16 +306,19 @@ __global__ void __launch_bounds__(LgWarp<RP>::WPB * 32, 1) k_procrustes_large_w(
       if (!a.ew_valid)
         for (int e = lane; e < RR; e += 32) Ek[e] = (e / RP == e % RP) ? 1.0 : 0.0;
       const double* xvk = a.XV + r0 * RP;
+      // the next subject's E and X V rows on their way into L2 while this one's sweeps run
+      if (lane == 0 && k + nwarps < a.X.K) {
+        const std::int64_t kn = k + nwarps, rn = a.X.srp[kn];
+        if (a.ew_valid) dev::prefetch_l2_bulk(a.Ewarm + kn * RR, RR * 8u);
+        dev::prefetch_l2_bulk(a.XV + rn * RP, static_cast<unsigned>(a.X.srp[kn + 1] - rn) * (RP * 8u));
+      }
       int flag = P2G_FLAG_FULL_RANK;
       for (int pass = 0; pass < 2; ++pass) {
         __syncwarp();
         // T' = H^T E into the slab and shared buffer 1
         warp_mm<RP, true>(
             RP, RP, [&](int i, int c) { return __ldg(a.H + c * RP + i); }, [&](int c, int j) { return Ek[c * RP + j]; },
-            [&](int i, int j, double v) {
-              Ts[i * RP + j] = v;
-              Ms1[i * LDS + j] = v;
-            });
+            [&](int i, int j, double v) { Ms1[i * LDS + j] = v; });
         __syncwarp();
         // M = B^T B over 8-row tiles of B = X~ T' (tiles staged in buffer 0)
         bool finite = true;
@@ -672,8 +677,8 @@ __global__ void __launch_bounds__(LgWarp<RP>::WPB * 32, 1) k_procrustes_large_w(
           break;
         }
         if (pass == 0 && off > 0.25 && smin2 < 1e-6 * smax2) continue;
-        // S' = M'^{-1/2} (second order about the diagonal) into Mx; A = P o N in
-        // the slab, P_pq = 1 / (s_p + s_q) formed on the fly
+        // S' = M'^{-1/2} (second order about the diagonal): A = P o N in place over M'
+        // (P_pq = 1 / (s_p + s_q)), S' into V''s buffer (V' is dead: E' = E V' is stored)
         for (int p = lane; p < RP; p += 32) {
           const double sq = sqrt(Mx[p * LDM + p]);
           sv[p] = sq;
@@ -682,9 +687,10 @@ __global__ void __launch_bounds__(LgWarp<RP>::WPB * 32, 1) k_procrustes_large_w(
         __syncwarp();
         for (int e = lane; e < RR; e += 32) {
           const int p = e / RP, q = e - p * RP;
-          As[e] = p == q ? 0.0 : (1.0 / (sv[p] + sv[q])) * Mx[p < q ? p * LDM + q : q * LDM + p];
+          Mx[p * LDM + q] = p == q ? 0.0 : dev::rcp_nr(sv[p] + sv[q]) * Mx[p * LDM + q];
         }
         __syncwarp();
+        double* const Sx = Vx;
         {
 #pragma unroll 1
           for (int bi = 0; bi < NB; ++bi) {
@@ -695,11 +701,11 @@ __global__ void __launch_bounds__(LgWarp<RP>::WPB * 32, 1) k_procrustes_large_w(
 #pragma unroll 2
             for (int k4 = 0; k4 < RP; k4 += 4) {
               const int c = k4 + fk;
-              const double x = As[i * RP + c];
+              const double x = Mx[i * LDM + c];
               const double xu = x * u[c];
 #pragma unroll
               for (int b = 0; b < NB; ++b) {
-                const double y = As[c * RP + 8 * b + fm];
+                const double y = Mx[c * LDM + 8 * b + fm];
                 dev::dmma884(c1[b], xu, y);
                 dev::dmma884(c2[b], x, y);
               }
@@ -709,29 +715,29 @@ __global__ void __launch_bounds__(LgWarp<RP>::WPB * 32, 1) k_procrustes_large_w(
 #pragma unroll
               for (int h = 0; h < 2; ++h) {
                 const int j = 8 * b + fn + h;
-                const double corr = c1[b][h] - As[i * RP + j] + (1.0 / (sv[i] + sv[j])) * c2[b][h];
-                Mx[i * LDM + j] = (i == j ? u[i] : 0.0) + u[i] * u[j] * corr;
+                const double corr = c1[b][h] - Mx[i * LDM + j] + dev::rcp_nr(sv[i] + sv[j]) * c2[b][h];
+                Sx[i * LDM + j] = (i == j ? u[i] : 0.0) + u[i] * u[j] * corr;
               }
           }
         }
         __syncwarp();
-        // Y = V' S' into the slab scratch, Z = Y E'^T into Mx's buffer, W = T' Z into Vx's
+        // T'' = H^T E' over A, then ((T'' S') E'^T) in place: the DMMA of a row tile is warp-wide,
+        // so every lane has read the tile's left operand before any lane's epilogue overwrites it
+        double* const Wsm = Mx;
         warp_mm<RP, true>(
-            RP, RP, [&](int i, int c) { return Vx[c * LDVx + i]; }, [&](int c, int j) { return Mx[c * LDM + j]; },
-            [&](int i, int j, double v) { As[i * RP + j] = v; });
-        __syncwarp();
-        double* const Zs = Mx;
-        warp_mm<RP, true>(
-            RP, RP, [&](int i, int c) { return As[i * RP + c]; }, [&](int c, int j) { return Ek[j * RP + c]; },
-            [&](int i, int j, double v) { Zs[i * LDS + j] = v; });
-        __syncwarp();
-        double* const Wsm = Vx;  // W = T' Z (V' is dead)
-        double* const Xst = Mx;  // then: 8 x 41 X~ tile and 8 x 41 Q tile (Z is dead)
-        double* const Qst = Mx + 8 * LDS;
-        warp_mm<RP, true>(
-            RP, RP, [&](int i, int c) { return Ts[i * RP + c]; }, [&](int c, int j) { return Zs[c * LDS + j]; },
+            RP, RP, [&](int i, int c) { return __ldg(a.H + c * RP + i); }, [&](int c, int j) { return Ek[c * RP + j]; },
             [&](int i, int j, double v) { Wsm[i * LDS + j] = v; });
         __syncwarp();
+        warp_mm<RP, true>(
+            RP, RP, [&](int i, int c) { return Wsm[i * LDS + c]; }, [&](int c, int j) { return Sx[c * LDM + j]; },
+            [&](int i, int j, double v) { Wsm[i * LDS + j] = v; });
+        __syncwarp();
+        warp_mm<RP, true>(
+            RP, RP, [&](int i, int c) { return Wsm[i * LDS + c]; }, [&](int c, int j) { return Ek[j * RP + c]; },
+            [&](int i, int j, double v) { Wsm[i * LDS + j] = v; });
+        __syncwarp();
+        double* const Xst = Sx;  // then: 8 x 41 X~ tile and 8 x 41 Q tile (S' is dead)
+        double* const Qst = Sx + 8 * LDS;
         // Q = X~ W and m1 += Q^T X~, tile by tile
         {
           double m1a[NB][NB][2];
