@@ -547,9 +547,13 @@ __global__ void __launch_bounds__(LgWarp<RP>::WPB * 32, 1) k_procrustes_large_w(
           __syncwarp();
           // one round per iteration (the two buffers and the two rotation buffers swap roles):
           // the loop body stays small for the instruction caches
-          unsigned ra = A, wb = B, ro = rb, ro2 = rb + 320u;
 #pragma unroll 1
           for (int rr = 0; rr < RP - 2; ++rr) {
+            // roles by round parity, computed from the (uniform) round counter so that the
+            // addresses stay in uniform registers (one wavefront per same-address load)
+            const unsigned par = static_cast<unsigned>(rr) & 1u;
+            const unsigned ra = par ? B : A, wb = par ? A : B;
+            const unsigned ro = rb + 320u * par, ro2 = rb + 320u * (par ^ 1u);
             blocks(ra, wb, ro);
             __syncwarp();
             {
@@ -558,12 +562,8 @@ __global__ void __launch_bounds__(LgWarp<RP>::WPB * 32, 1) k_procrustes_large_w(
               par_store(d, wb, ra, ro2);
             }
             __syncwarp();
-            const unsigned t1 = ra, t2 = ro;
-            ra = wb;
-            wb = t1;
-            ro = ro2;
-            ro2 = t2;
           }
+          const unsigned ra = A, wb = B, ro = rb;  // 38 rounds done: round 39 as round 1
           blocks(ra, wb, ro);
           __syncwarp();
           vupd(ro);
