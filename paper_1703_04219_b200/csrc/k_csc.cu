@@ -244,52 +244,75 @@ __global__ void k_seg_reduce(int R, std::int64_t J, const std::int64_t* __restri
 }
 
 /// U = Q_k H diag(W_k o nH) row factors for R > 16 on the fp64 tensor cores:
-/// warp per subject, HW_k (R x R, zero-padded to RP) in the warp's shared
-/// memory, 8-row tiles of Q_k as DMMA A fragments straight from HBM, U rows
-/// stored from the C fragments (16-byte pairs).
+/// warp per subject.  H (zero-padded to RP x RP) is shared by every subject, so
+/// one copy per CTA sits in shared memory (row stride RP + 4: the B fragments of
+/// a half-warp, 4 rows x 4 columns, fall on 16 different bank pairs) and the
+/// per-subject column scale w_k o nH is applied to the C fragments instead of
+/// being folded into a per-warp copy of H (round 1: 12.8 KB per warp rebuilt per
+/// subject, 16 warps per SM).  8-row tiles of Q_k are DMMA A fragments straight
+/// from HBM, two tiles' loads in flight; U rows stored as 16-byte pairs.
 template <int RP, int WPB>
 __global__ void __launch_bounds__(WPB * 32)
     k_urows(ShardArgs X, int R, const double* __restrict__ Q, const double* __restrict__ H,
             const double* __restrict__ W, const double* __restrict__ nH, double* __restrict__ U) {
-  constexpr int NB = RP / 8;
-  extern __shared__ double sm[];
+  constexpr int NB = RP / 8, LDH = RP + 4;
+  __shared__ double Hs[RP * LDH];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, fm = lane >> 2, fk = lane & 3;
-  double* HW = sm + wid * RP * RP;  // RP x RP row-major
+  for (int e = threadIdx.x; e < RP * RP; e += blockDim.x) {
+    const int a = e / RP, c = e - a * RP;
+    Hs[a * LDH + c] = (a < R && c < R) ? H[a * R + c] : 0.0;
+  }
+  __syncthreads();
   const bool even = (R & 1) == 0;
+  const unsigned hb = static_cast<unsigned>(__cvta_generic_to_shared(Hs)) + 8u * static_cast<unsigned>(fk * LDH + fm);
   const std::int64_t nwarps = static_cast<std::int64_t>(gridDim.x) * WPB;
   for (std::int64_t k = static_cast<std::int64_t>(blockIdx.x) * WPB + wid; k < X.K; k += nwarps) {
-    __syncwarp();
-    for (int e = lane; e < RP * RP; e += 32) {
-      const int a = e / RP, c = e - a * RP;
-      HW[e] = (a < R && c < R) ? H[a * R + c] * W[k * R + c] * nH[c] : 0.0;
-    }
-    __syncwarp();
     const std::int64_t r0 = X.srp[k];
     const int I = static_cast<int>(X.srp[k + 1] - r0);
-    for (int i0 = 0; i0 < I; i0 += 8) {
-      const int i = i0 + fm;
-      const bool iv = i < I;
-      const double* qrow = Q + (r0 + i) * R;
-      double acc[NB][2];
+    double sc[NB][2];  // this lane's columns of w_k o nH
 #pragma unroll
-      for (int b = 0; b < NB; ++b) acc[b][0] = acc[b][1] = 0.0;
+    for (int b = 0; b < NB; ++b)
 #pragma unroll
-      for (int k4 = 0; k4 < RP; k4 += 4) {
-        const int c = k4 + fk;
-        const double x = (iv && c < R) ? __ldg(qrow + c) : 0.0;
-#pragma unroll
-        for (int b = 0; b < NB; ++b) dev::dmma884(acc[b], x, HW[c * RP + 8 * b + fm]);
+      for (int h = 0; h < 2; ++h) {
+        const int c = 8 * b + 2 * fk + h;
+        sc[b][h] = c < R ? __ldg(W + k * R + c) * __ldg(nH + c) : 0.0;
       }
-      if (iv) {
-        double* urow = U + (r0 + i) * R;
+    for (int i0 = 0; i0 < I; i0 += 16) {
+      double x[2][RP / 4];
 #pragma unroll
-        for (int b = 0; b < NB; ++b) {
-          const int c = 8 * b + 2 * fk;
-          if (even) {
-            if (c < R) *reinterpret_cast<double2*>(urow + c) = make_double2(acc[b][0], acc[b][1]);
-          } else {
-            if (c < R) urow[c] = acc[b][0];
-            if (c + 1 < R) urow[c + 1] = acc[b][1];
+      for (int t = 0; t < 2; ++t) {
+        const int i = i0 + 8 * t + fm;
+        const double* qrow = Q + (r0 + i) * R;
+#pragma unroll
+        for (int k4 = 0; k4 < RP; k4 += 4) {
+          const int c = k4 + fk;
+          x[t][k4 / 4] = (i < I && c < R) ? __ldg(qrow + c) : 0.0;
+        }
+      }
+#pragma unroll
+      for (int t = 0; t < 2; ++t) {
+        const int i = i0 + 8 * t + fm;
+        if (i0 + 8 * t >= I) break;
+        double acc[NB][2];
+#pragma unroll
+        for (int b = 0; b < NB; ++b) acc[b][0] = acc[b][1] = 0.0;
+#pragma unroll
+        for (int k4 = 0; k4 < RP; k4 += 4)
+#pragma unroll
+          for (int b = 0; b < NB; ++b)  // (asm loads: kept in the loop, not hoisted into 100 registers)
+            dev::dmma884(acc[b], x[t][k4 / 4], dev::lds64<0>(hb + 8u * static_cast<unsigned>(k4 * LDH + 8 * b)));
+        if (i < I) {
+          double* urow = U + (r0 + i) * R;
+#pragma unroll
+          for (int b = 0; b < NB; ++b) {
+            const int c = 8 * b + 2 * fk;
+            const double u0 = acc[b][0] * sc[b][0], u1 = acc[b][1] * sc[b][1];
+            if (even) {
+              if (c < R) *reinterpret_cast<double2*>(urow + c) = make_double2(u0, u1);
+            } else {
+              if (c < R) urow[c] = u0;
+              if (c + 1 < R) urow[c + 1] = u1;
+            }
           }
         }
       }
@@ -464,12 +487,11 @@ template <int RP>
 static void urows(p2g_ctx* c, int R, const double* Q, const double* H, const double* W, const double* nH, double* U,
                   cudaStream_t s) {
   constexpr int WPB = 8;
-  const std::size_t smem = sizeof(double) * WPB * RP * RP;
   auto kern = k_urows<RP, WPB>;
-  P2G_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   const ShardArgs X{c->srp.get(), c->rp.get(), c->ci.get(), c->val.get(), c->k_end - c->k_begin, c->NR, c->nnz, c->J};
-  const int blocks = static_cast<int>(std::max<std::int64_t>(1, std::min<std::int64_t>((X.K + WPB - 1) / WPB, 148 * 8)));
-  kern<<<blocks, WPB * 32, smem, s>>>(X, R, Q, H, W, nH, U);
+  const int blocks =
+      static_cast<int>(std::max<std::int64_t>(1, std::min<std::int64_t>((X.K + WPB - 1) / WPB, c->num_sms * 8)));
+  kern<<<blocks, WPB * 32, 0, s>>>(X, R, Q, H, W, nH, U);
 }
 
 void launch_urows_large(p2g_ctx* c, int R, const double* Q, const double* H, const double* W, const double* nH,
