@@ -250,9 +250,10 @@ __global__ void k_seg_reduce(int R, std::int64_t J, const std::int64_t* __restri
 /// per-subject column scale w_k o nH is applied to the C fragments instead of
 /// being folded into a per-warp copy of H (round 1: 12.8 KB per warp rebuilt per
 /// subject, 16 warps per SM).  8-row tiles of Q_k are DMMA A fragments straight
-/// from HBM, two tiles' loads in flight; U rows stored as 16-byte pairs.
+/// from HBM (one tile's ten loads in flight per lane, 24+ warps per SM); U rows
+/// stored as 16-byte pairs.
 template <int RP, int WPB>
-__global__ void __launch_bounds__(WPB * 32)
+__global__ void __launch_bounds__(WPB * 32, 3)
     k_urows(ShardArgs X, int R, const double* __restrict__ Q, const double* __restrict__ H,
             const double* __restrict__ W, const double* __restrict__ nH, double* __restrict__ U) {
   constexpr int NB = RP / 8, LDH = RP + 4;
@@ -277,42 +278,34 @@ __global__ void __launch_bounds__(WPB * 32)
         const int c = 8 * b + 2 * fk + h;
         sc[b][h] = c < R ? __ldg(W + k * R + c) * __ldg(nH + c) : 0.0;
       }
-    for (int i0 = 0; i0 < I; i0 += 16) {
-      double x[2][RP / 4];
+    for (int i0 = 0; i0 < I; i0 += 8) {
+      const int i = i0 + fm;
+      const double* qrow = Q + (r0 + i) * R;
+      double x[RP / 4];
 #pragma unroll
-      for (int t = 0; t < 2; ++t) {
-        const int i = i0 + 8 * t + fm;
-        const double* qrow = Q + (r0 + i) * R;
-#pragma unroll
-        for (int k4 = 0; k4 < RP; k4 += 4) {
-          const int c = k4 + fk;
-          x[t][k4 / 4] = (i < I && c < R) ? __ldg(qrow + c) : 0.0;
-        }
+      for (int k4 = 0; k4 < RP; k4 += 4) {
+        const int c = k4 + fk;
+        x[k4 / 4] = (i < I && c < R) ? __ldg(qrow + c) : 0.0;
       }
+      double acc[NB][2];
 #pragma unroll
-      for (int t = 0; t < 2; ++t) {
-        const int i = i0 + 8 * t + fm;
-        if (i0 + 8 * t >= I) break;
-        double acc[NB][2];
+      for (int b = 0; b < NB; ++b) acc[b][0] = acc[b][1] = 0.0;
 #pragma unroll
-        for (int b = 0; b < NB; ++b) acc[b][0] = acc[b][1] = 0.0;
+      for (int k4 = 0; k4 < RP; k4 += 4)
 #pragma unroll
-        for (int k4 = 0; k4 < RP; k4 += 4)
+        for (int b = 0; b < NB; ++b)  // (asm loads: kept in the loop, not hoisted into 100 registers)
+          dev::dmma884(acc[b], x[k4 / 4], dev::lds64<0>(hb + 8u * static_cast<unsigned>(k4 * LDH + 8 * b)));
+      if (i < I) {
+        double* urow = U + (r0 + i) * R;
 #pragma unroll
-          for (int b = 0; b < NB; ++b)  // (asm loads: kept in the loop, not hoisted into 100 registers)
-            dev::dmma884(acc[b], x[t][k4 / 4], dev::lds64<0>(hb + 8u * static_cast<unsigned>(k4 * LDH + 8 * b)));
-        if (i < I) {
-          double* urow = U + (r0 + i) * R;
-#pragma unroll
-          for (int b = 0; b < NB; ++b) {
-            const int c = 8 * b + 2 * fk;
-            const double u0 = acc[b][0] * sc[b][0], u1 = acc[b][1] * sc[b][1];
-            if (even) {
-              if (c < R) *reinterpret_cast<double2*>(urow + c) = make_double2(u0, u1);
-            } else {
-              if (c < R) urow[c] = u0;
-              if (c + 1 < R) urow[c + 1] = u1;
-            }
+        for (int b = 0; b < NB; ++b) {
+          const int c = 8 * b + 2 * fk;
+          const double u0 = acc[b][0] * sc[b][0], u1 = acc[b][1] * sc[b][1];
+          if (even) {
+            if (c < R) *reinterpret_cast<double2*>(urow + c) = make_double2(u0, u1);
+          } else {
+            if (c < R) urow[c] = u0;
+            if (c + 1 < R) urow[c + 1] = u1;
           }
         }
       }
