@@ -100,7 +100,7 @@ struct LgWarp {
       kPhys ? ((16 * 7 * 32 + 4 * 6 * 32 + 6 * kTri + 15) / 16) * 2 : ((NBLK + (RP - 1) * (RP / 2) + 7) / 8) * 2;
   // M, V'^T, w, u (1/sqrt diag), then per pair slot and double-buffered: (c, s), t M_pq, int4 offsets
   // (kPhys: (c, s) only)
-  static constexpr int kWarpD = kMat + kVt + 2 * RP + (kPhys ? 2 * RP : 2 * (RP + RP / 2 + RP));
+  static constexpr int kWarpD = kMat + kVt + 2 * RP + (kPhys ? 2 * RP + 2 : 2 * (RP + RP / 2 + RP));  // kPhys: + 2 mbarriers
   static constexpr int kWarpDE = (kWarpD + 1) & ~1;
   static constexpr int pick_wpb() {
     int w = 16;
@@ -298,6 +298,17 @@ __global__ void __launch_bounds__(LgWarp<RP>::WPB * 32, 1) k_procrustes_large_w(
     double* const Ms1 = M + L::kMat;  // shared buffer 1 (the V'^T region)
     for (int e = lane; e < RR; e += 32) M1[e] = 0.0;
     const int fm = lane >> 2, fk = lane & 3, fn = 2 * (lane & 3);
+    // X V row tiles (8 rows x 320 B, contiguous in HBM) arrive by TMA bulk copies into two
+    // staging slots behind the B tile of buffer 0, one mbarrier per slot, two tiles in flight
+    const unsigned mbar0 = dev::smem_uniform(rotb + RP), mbar1 = mbar0 + 8u;
+    const unsigned st0 = dev::smem_uniform(Ms0 + 8 * LDS), st1 = st0 + 8u * 8 * RP;
+    unsigned ph0 = 0, ph1 = 0;
+    if (lane == 0) {
+      dev::mbar_init(mbar0, 1);
+      dev::mbar_init(mbar1, 1);
+      dev::fence_mbar_init();
+    }
+    __syncwarp();
     for (std::int64_t k = gw; k < a.X.K; k += nwarps) {
       const std::int64_t r0 = a.X.srp[k];
       const int I = static_cast<int>(a.X.srp[k + 1] - r0);
@@ -326,20 +337,36 @@ __global__ void __launch_bounds__(LgWarp<RP>::WPB * 32, 1) k_procrustes_large_w(
           double accM[NB * (NB + 1) / 2][2];
 #pragma unroll
           for (int t = 0; t < NB * (NB + 1) / 2; ++t) accM[t][0] = accM[t][1] = 0.0;
-          for (int i0 = 0; i0 < I; i0 += 8) {
-            const int i = i0 + fm;
+          auto tile_in = [&](int t, unsigned st, unsigned mbar) {  // rows 8 t .. of X V into a staging slot
+            const int rows = I - 8 * t < 8 ? I - 8 * t : 8;
+            if (lane == 0) dev::bulk_g2s(st, xvk + static_cast<std::int64_t>(8 * t) * RP, rows * (RP * 8u), mbar);
+          };
+          const int ntiles = (I + 7) >> 3;
+          dev::fence_proxy_async();  // the slots were last written by this warp's own stores
+          __syncwarp();
+          if (ntiles > 0) tile_in(0, st0, mbar0);
+          if (ntiles > 1) tile_in(1, st1, mbar1);
+          for (int t = 0; t < ntiles; ++t) {
+            const int i = 8 * t + fm;
             const bool iv = i < I;
-            const double* xr = xvk + static_cast<std::int64_t>(i) * RP;
+            const bool odd = t & 1;
+            const unsigned st = odd ? st1 : st0;
+            dev::mbar_wait(odd ? mbar1 : mbar0, odd ? ph1 : ph0);
+            if (odd)
+              ph1 ^= 1u;
+            else
+              ph0 ^= 1u;
             double accB[NB][2];
 #pragma unroll
             for (int b = 0; b < NB; ++b) accB[b][0] = accB[b][1] = 0.0;
 #pragma unroll
             for (int k4 = 0; k4 < RP; k4 += 4) {
-              const double x = iv ? __ldg(xr + k4 + fk) * w[k4 + fk] : 0.0;
+              const double x = iv ? dev::lds64<0>(st + 8u * (fm * RP + k4 + fk)) * w[k4 + fk] : 0.0;
 #pragma unroll
               for (int b = 0; b < NB; ++b) dev::dmma884(accB[b], x, Ms1[(k4 + fk) * LDS + 8 * b + fm]);
             }
-            __syncwarp();
+            __syncwarp();  // every lane has read the slot: refill it with tile t + 2
+            if (t + 2 < ntiles) tile_in(t + 2, st, odd ? mbar1 : mbar0);
 #pragma unroll
             for (int b = 0; b < NB; ++b) {
               Ms0[fm * LDS + 8 * b + fn] = accB[b][0];
@@ -351,11 +378,11 @@ __global__ void __launch_bounds__(LgWarp<RP>::WPB * 32, 1) k_procrustes_large_w(
               double f[NB];
 #pragma unroll
               for (int b = 0; b < NB; ++b) f[b] = Ms0[(kk + fk) * LDS + 8 * b + fm];
-              int t = 0;
+              int t2 = 0;
 #pragma unroll
               for (int bi = 0; bi < NB; ++bi)
 #pragma unroll
-                for (int bj = 0; bj <= bi; ++bj) dev::dmma884(accM[t++], f[bi], f[bj]);
+                for (int bj = 0; bj <= bi; ++bj) dev::dmma884(accM[t2++], f[bi], f[bj]);
             }
           }
           __syncwarp();
