@@ -429,12 +429,16 @@ __global__ void __launch_bounds__(LgWarp<RP>::WPB * 32, 1) k_procrustes_large_w(
         constexpr int kBuf = L::kMat * 8;  // bytes from buffer 0 to buffer 1
         const unsigned mb = dev::smem_uniform(M);
         const unsigned rb = dev::smem_uniform(rotb);  // (c, s) per slot, 2 x 20 double2
-        const int ch = lane & 3, crow = 32 + (lane >> 2);
-        double vreg[RP], vch[10];  // V' row `lane`; positions 10 ch .. 10 ch + 9 of row crow
+        // V' in registers as 32 tiles of 5 rows x 10 positions (5 slots): lane (rg, ch) holds rows
+        // 5 rg .. 5 rg + 4 at positions 10 ch .. 10 ch + 9, so a lane needs 5 of the round's 20 rotation
+        // pairs (5 loads instead of the 25 of a row-per-lane layout; the sigma step crosses chunks
+        // with two shuffles per row)
+        const int ch = lane & 3, rg = lane >> 2;
+        double vt[5][10];
 #pragma unroll
-        for (int x = 0; x < RP; ++x) vreg[x] = rr_l0(RP, x) == lane ? 1.0 : 0.0;
+        for (int r = 0; r < 5; ++r)
 #pragma unroll
-        for (int k = 0; k < 10; ++k) vch[k] = rr_l0(RP, 10 * ch + k) == crow ? 1.0 : 0.0;
+          for (int k = 0; k < 10; ++k) vt[r][k] = rr_l0(RP, 10 * ch + k) == 5 * rg + r ? 1.0 : 0.0;
         double tiny = 0.0;
         // Scaled ("fast") rotations: M = D M~ D off the diagonal and V' = V~ D with a scale d_x per
         // position (both columns of a rotation shrink by the same cosine), so a rotation is
@@ -527,45 +531,38 @@ __global__ void __launch_bounds__(LgWarp<RP>::WPB * 32, 1) k_procrustes_large_w(
             }
           }
         };
-        // V' <- V' J on the register row and the row chunk, then one step along sigma
+        // V' <- V' J on the register tile, then one step along sigma
         auto vupd = [&](unsigned ro) {
-#pragma unroll
-          for (int i = 0; i < RP / 2; ++i) {
-            const double2 r = dev::lds128<0>(ro + 16u * i);
-            const double x0 = vreg[2 * i], y0 = vreg[2 * i + 1];
-            vreg[2 * i] = fma(r.x, y0, x0);
-            vreg[2 * i + 1] = fma(r.y, x0, y0);
-          }
-          const double t0 = vreg[0];
-#pragma unroll
-          for (int l = 0; l < RP / 2 - 1; ++l) vreg[2 * l] = vreg[2 * l + 2];
-          vreg[RP - 2] = vreg[RP - 1];
-#pragma unroll
-          for (int l = RP / 2 - 1; l >= 2; --l) vreg[2 * l + 1] = vreg[2 * l - 1];
-          vreg[3] = t0;
           const unsigned cb = ro + 80u * ch;
 #pragma unroll
           for (int k = 0; k < 5; ++k) {
             const double2 r = dev::lds128<0>(cb + 16u * k);
-            const double x0 = vch[2 * k], y0 = vch[2 * k + 1];
-            vch[2 * k] = fma(r.x, y0, x0);
-            vch[2 * k + 1] = fma(r.y, x0, y0);
+#pragma unroll
+            for (int q = 0; q < 5; ++q) {
+              const double x0 = vt[q][2 * k], y0 = vt[q][2 * k + 1];
+              vt[q][2 * k] = fma(r.x, y0, x0);
+              vt[q][2 * k + 1] = fma(r.y, x0, y0);
+            }
           }
           // positions 10 ch + 8 <- 10 ch + 10 (next chunk) and 10 ch + 1 <- 10 ch - 1
           // (previous chunk); chunk 0 holds the cycle's ends 3 <- 0 and 1 (fixed)
-          const double dn = __shfl_down_sync(dev::kFull, vch[0], 1);
-          const double up = __shfl_up_sync(dev::kFull, vch[9], 1);
-          const double o0 = vch[0], o1 = vch[1], o9 = vch[9];
-          vch[0] = vch[2];
-          vch[2] = vch[4];
-          vch[4] = vch[6];
-          vch[6] = vch[8];
-          vch[8] = ch == 3 ? o9 : dn;
-          vch[9] = vch[7];
-          vch[7] = vch[5];
-          vch[5] = vch[3];
-          vch[3] = ch == 0 ? o0 : o1;
-          vch[1] = ch == 0 ? o1 : up;
+#pragma unroll
+          for (int q = 0; q < 5; ++q) {
+            double* v = vt[q];
+            const double dn = __shfl_down_sync(dev::kFull, v[0], 1);
+            const double up = __shfl_up_sync(dev::kFull, v[9], 1);
+            const double o0 = v[0], o1 = v[1], o9 = v[9];
+            v[0] = v[2];
+            v[2] = v[4];
+            v[4] = v[6];
+            v[6] = v[8];
+            v[8] = ch == 3 ? o9 : dn;
+            v[9] = v[7];
+            v[7] = v[5];
+            v[5] = v[3];
+            v[3] = ch == 0 ? o0 : o1;
+            v[1] = ch == 0 ? o1 : up;
+          }
         };
         // one sweep (m - 1 = 39 rounds) from buffer A to buffer B: rounds in
         // pairs (A -> B with rot buffer 0, B -> A with rot buffer 1), then the last
@@ -670,9 +667,9 @@ __global__ void __launch_bounds__(LgWarp<RP>::WPB * 32, 1) k_procrustes_large_w(
           __syncwarp();
           double* V2 = M + cur * L::kMat;
 #pragma unroll
-          for (int x = 0; x < RP; ++x) V2[rr_l0(RP, x) * LDM + lane] = vreg[x] * u[x];
+          for (int q = 0; q < 5; ++q)
 #pragma unroll
-          for (int k = 0; k < 10; ++k) V2[rr_l0(RP, 10 * ch + k) * LDM + crow] = vch[k] * u[10 * ch + k];
+            for (int k = 0; k < 10; ++k) V2[rr_l0(RP, 10 * ch + k) * LDM + 5 * rg + q] = vt[q][k] * u[10 * ch + k];
           __syncwarp();
           Mx = Ml;
           Vx = V2;
