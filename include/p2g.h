@@ -303,6 +303,13 @@ int p2g_bench_mttkrp(p2g_ctx* ctx, int32_t R, int32_t reps, uint64_t budget_byte
 int p2g_pinv_small(p2g_ctx* ctx, const double* G, int32_t n, double* out);
 int p2g_gram(p2g_ctx* ctx, const double* A, int64_t rows, int32_t cols, double* out);
 
+/* economy_svd (kernels.hpp:92-107): thin SVD M = P diag(sigma) Z^T of the
+ * column-major rows x cols matrix M, rho = min(rows, cols); P is rows x rho,
+ * Z is cols x rho (both column-major), sigma non-increasing.  A zero matrix
+ * yields zero singular values and identity-block factors (kernels.hpp:101-104);
+ * non-finite entries: P2G_ENUMERICAL ("svd operand").  min(rows, cols) <= 128. */
+int p2g_economy_svd(p2g_ctx* ctx, const double* M, int64_t rows, int64_t cols, double* P, double* sigma, double* Z);
+
 /* ---------------------------------------------------------------------------
  * Ingest and export (host side).  No GPU needed.
  * ------------------------------------------------------------------------- */

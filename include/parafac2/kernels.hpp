@@ -3,6 +3,8 @@
 // khatri_rao and hadamard (not on the hot path) stay on the host.
 #pragma once
 
+#include <algorithm>
+
 #include "common.hpp"
 
 namespace parafac2 {
@@ -41,6 +43,24 @@ inline Matrix pinv_small(const Matrix& G) {
   if (G.rows() != G.cols()) throw std::invalid_argument("pinv_small: matrix must be square");
   Matrix out(G.rows(), G.cols());
   check(p2g_pinv_small(Device::get().ctx(), G.data(), static_cast<int32_t>(G.rows()), out.data()));
+  return out;
+}
+
+/// kernels.hpp:89-93.
+struct EconomySvd {
+  Matrix P;      // left singular vectors, m x rho
+  Vector sigma;  // singular values, non-increasing, length rho
+  Matrix Z;      // right singular vectors, n x rho
+};
+
+/// kernels.hpp:95-107 -> p2g_economy_svd (device, one-sided Jacobi): thin SVD
+/// M = P diag(sigma) Z^T, rho = min(m, n); a zero matrix yields zero singular
+/// values and identity-block factors; non-finite entries: NumericalError.
+inline EconomySvd economy_svd(const Matrix& M) {
+  const Index rho = std::min(M.rows(), M.cols());
+  EconomySvd out{Matrix(M.rows(), rho), Vector(static_cast<std::size_t>(rho)), Matrix(M.cols(), rho)};
+  check(p2g_economy_svd(Device::get().ctx(), M.data(), M.rows(), M.cols(), out.P.data(), out.sigma.data(),
+                        out.Z.data()));
   return out;
 }
 

@@ -12,6 +12,7 @@ argument meaning follow the reference's C++ entry points
     cp_als_iteration  cp.hpp:99-145         -> Context.cp_als_iteration
     nnls_rowwise      kernels.hpp:194-211   -> Context.nnls_rowwise
     pinv_small / gram kernels.hpp:57-87     -> Context.pinv_small / gram
+    economy_svd       kernels.hpp:89-107    -> Context.economy_svd
     partition_weighted parallel.hpp:51-79   -> partition_weighted
 
 Errors map like the reference's exception types: ``InvalidArgument``
@@ -131,6 +132,7 @@ _SIGS = {
     "p2g_cp_als_iteration": (ctypes.c_int, [_P, _I64, _I64, _I32, _P, _P, _P, _P, _P, _P, _I32, _I32, _P, _P]),
     "p2g_nnls_rowwise": (ctypes.c_int, [_P, _P, _P, _I64, _I32, _I32, _P]),
     "p2g_pinv_small": (ctypes.c_int, [_P, _P, _I32, _P]),
+    "p2g_economy_svd": (ctypes.c_int, [_P, _P, _I64, _I64, _P, _P, _P]),
     "p2g_gram": (ctypes.c_int, [_P, _P, _I64, _I32, _P]),
     "p2g_load_shard": (ctypes.c_int, [_P, _I64, _I64, _I64, _I64, _P, _P, _P, _P]),
     "p2g_set_host_collective": (ctypes.c_int, [_P, _P, _P]),
@@ -788,6 +790,18 @@ class Context:
         out = np.empty(G.shape, order="F")
         _check(self._lib.p2g_pinv_small(self._h, _ptr(G), G.shape[0], _ptr(out)))
         return out
+
+    def economy_svd(self, M):
+        """economy_svd (kernels.hpp:95-107): (P, sigma, Z) with M = P diag(sigma) Z^T."""
+        M = _f64(M)
+        if M.ndim != 2 or M.shape[0] < 1 or M.shape[1] < 1:
+            raise InvalidArgument("economy_svd: need a non-empty matrix")
+        rho = min(M.shape)
+        P = np.empty((M.shape[0], rho), order="F")
+        sig = np.empty(rho)
+        Z = np.empty((M.shape[1], rho), order="F")
+        _check(self._lib.p2g_economy_svd(self._h, _ptr(M), M.shape[0], M.shape[1], _ptr(P), _ptr(sig), _ptr(Z)))
+        return P, sig, Z
 
     def gram(self, A):
         A = _f64(A)

@@ -1865,6 +1865,55 @@ extern "C" int p2g_pinv_small(p2g_ctx* c, const double* G, int32_t n, double* ou
   });
 }
 
+extern "C" int p2g_economy_svd(p2g_ctx* c, const double* M, int64_t rows, int64_t cols, double* P, double* sigma,
+                               double* Z) {
+  return guarded([&] {
+    if (!c) throw InvalidArgument("null context");
+    set_device(c);
+    const std::int64_t rho = std::min(rows, cols);
+    if (rows < 1 || cols < 1 || rho > svd_max_cols() || std::max(rows, cols) > (1 << 24) || !M || !P || !sigma || !Z)
+      throw InvalidArgument("economy_svd: need 1 <= min(rows, cols) <= 128");
+    check_finite_host(M, rows * cols, "svd operand");
+    double amax = 0.0;
+    for (std::int64_t e = 0; e < rows * cols; ++e) amax = std::max(amax, std::fabs(M[e]));
+    if (amax == 0.0) {  // kernels.hpp:101-104
+      std::fill(P, P + rows * rho, 0.0);
+      std::fill(Z, Z + cols * rho, 0.0);
+      std::fill(sigma, sigma + rho, 0.0);
+      for (std::int64_t j = 0; j < rho; ++j) P[j * rows + j] = Z[j * cols + j] = 1.0;
+      return;
+    }
+    // W = M (rows >= cols) or M^T (the column-major bytes of M are M^T row-major), scaled by 1 / max |entry|
+    const bool tall = rows >= cols;
+    const int mm = static_cast<int>(tall ? rows : cols), nn = static_cast<int>(rho);
+    std::vector<double> h(static_cast<std::size_t>(rows * cols));
+    for (std::int64_t e = 0; e < rows * cols; ++e) h[static_cast<std::size_t>(e)] = M[e] / amax;
+    DBuf<double> dW, dV, dU, dVo, dS;
+    DBuf<std::int32_t> dst;
+    dW.resize(static_cast<std::size_t>(mm) * nn);
+    dV.resize(static_cast<std::size_t>(nn) * nn);
+    dU.resize(static_cast<std::size_t>(mm) * nn);
+    dVo.resize(static_cast<std::size_t>(nn) * nn);
+    dS.resize(static_cast<std::size_t>(nn));
+    dst.resize(1);
+    if (tall)
+      upload_colmajor(c, h.data(), rows, cols, dW.get());
+    else
+      P2G_CUDA(cudaMemcpyAsync(dW.get(), h.data(), sizeof(double) * h.size(), cudaMemcpyHostToDevice, c->stream));
+    launch_economy_svd(mm, nn, dW.get(), dV.get(), dU.get(), dVo.get(), dS.get(), dst.get(), c->stream);
+    P2G_LAUNCHED(1);
+    std::int32_t st = 0;
+    P2G_CUDA(cudaMemcpyAsync(&st, dst.get(), sizeof(st), cudaMemcpyDeviceToHost, c->stream));
+    P2G_CUDA(cudaMemcpyAsync(sigma, dS.get(), sizeof(double) * nn, cudaMemcpyDeviceToHost, c->stream));
+    // tall: P = U (rows x rho), Z = V (cols x cols); wide: M^T = Z Sigma P^T, so Z = U (cols x rho), P = V
+    download_colmajor(c, dU.get(), mm, nn, tall ? P : Z);
+    download_colmajor(c, dVo.get(), nn, nn, tall ? Z : P);
+    P2G_CUDA(cudaStreamSynchronize(c->stream));
+    if (st != 0) throw NumericalError("economy_svd did not converge");
+    for (int j = 0; j < nn; ++j) sigma[j] *= amax;
+  });
+}
+
 extern "C" int p2g_gram(p2g_ctx* c, const double* A, int64_t rows, int32_t cols, double* out) {
   return guarded([&] {
     if (!c) throw InvalidArgument("null context");

@@ -312,6 +312,10 @@ void launch_nnls_rows(NnlsWork& ws, int R, std::int64_t n, const double* G, cons
 void launch_rows_times(int R, std::int64_t n, const double* B, const double* P, double* X,
                        cudaStream_t s);  // X = B * P (row-major rows)
 void launch_pinv(int n, const double* G, double* out, cudaStream_t s);
+/// economy_svd (kernels.hpp:92-107), k_svd.cu: one-sided Jacobi SVD of W (mm x nn row-major, mm >= nn).
+int svd_max_cols();
+void launch_economy_svd(int mm, int nn, double* W, double* V, double* Uo, double* Vo, double* sig, int* status,
+                        cudaStream_t s);
 // Replicated R x R steps of the CP iteration (cp.hpp:99-145):
 void launch_solve_h(int R, const double* m1, const double* gramW, const double* gramV, double* H, double* nH,
                     double* gramH, double* G2, cudaStream_t s);  // H update + normalize + G2 for the V step

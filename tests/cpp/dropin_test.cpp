@@ -141,6 +141,14 @@ int main() {
     CHECK(std::abs(x(0, 0) - 1.0 / 3) < 1e-12 && std::abs(x(0, 1) - 1.0 / 3) < 1e-12);
     CHECK(throws<NumericalError>([] { nnls_rowwise(Matrix::Identity(2, 2), Matrix::FromRows(1, 2, {3, 4}), 1, 1); }));
   }
+  // test_kernels.cpp:133-154 — economy_svd of a diagonal and of a zero matrix
+  {
+    EconomySvd svd = economy_svd(Matrix::FromRows(2, 2, {3, 0, 0, 2}));
+    CHECK(svd.sigma.size() == 2 && std::abs(svd.sigma[0] - 3.0) < 1e-12 && std::abs(svd.sigma[1] - 2.0) < 1e-12);
+    for (Index c = 0; c < 2; ++c) CHECK(std::abs(std::abs(svd.P(c, c)) - 1.0) < 1e-12);
+    EconomySvd z = economy_svd(Matrix::Zero(2, 3));
+    CHECK(z.sigma.size() == 2 && z.sigma[0] == 0.0 && z.sigma[1] == 0.0 && z.P(0, 0) == 1.0 && z.Z(1, 1) == 1.0);
+  }
   // test_cp.cpp:77-94 — rank-1 closed form
   {
     auto Y = ProjectedSlices::from_dense(2, {Matrix::FromRows(1, 2, {2, 4})});

@@ -100,6 +100,37 @@ def test_nnls_pinv_gram_vs_oracle(ctx, oracle, p2g):  # test_kernels.cpp:85-254
     assert np.array_equal(ctx.gram(np.array([[1.0, 2], [3, 4]])), [[10, 14], [14, 20]])
 
 
+def test_economy_svd(ctx, oracle, p2g):  # test_kernels.cpp:133-175
+    o = oracle
+    P, sig, Z = ctx.economy_svd(np.array([[3.0, 0], [0, 2]]))  # diagonal: recovers the diagonal
+    assert sig.shape == (2,) and abs(sig[0] - 3.0) < 1e-12 and abs(sig[1] - 2.0) < 1e-12
+    for c in range(2):
+        assert abs(abs(P[c, c]) - 1.0) < 1e-12 and abs((P[:, c] * Z[:, c]).sum() - 1.0) < 1e-12
+    P, sig, Z = ctx.economy_svd(np.zeros((2, 3)))  # zero matrix: zero sigma, identity-block bases
+    assert sig.shape == (2,) and (sig == 0.0).all()
+    assert np.array_equal(P, np.eye(2)) and np.array_equal(Z, np.eye(3)[:, :2])
+    rng = o.Rng(14)
+    shapes = [(1 + rng.below(6), 1 + rng.below(8)) for _ in range(20)] + [(60, 40), (40, 60), (97, 10), (5, 33)]
+    for rows, cols in shapes:  # random matrices: reconstruction, orthonormal factors, ordered sigma, oracle's sigma
+        m = o.random_matrix(rng, rows, cols)
+        P, sig, Z = ctx.economy_svd(m)
+        rho = min(rows, cols)
+        assert P.shape == (rows, rho) and Z.shape == (cols, rho) and sig.shape == (rho,)
+        assert np.linalg.norm(P @ np.diag(sig) @ Z.T - m) < 1e-10 * max(1.0, np.linalg.norm(m))
+        assert np.linalg.norm(P.T @ P - np.eye(rho)) < 1e-10 and np.linalg.norm(Z.T @ Z - np.eye(rho)) < 1e-10
+        assert (np.diff(sig) <= 0).all() and sig[-1] >= 0.0
+        _, sref, _ = o.economy_svd(m)
+        assert np.abs(sig - np.asarray(sref)).max() <= 1e-12 * max(1.0, sig[0])
+    # rank-deficient: an orthonormal completion of the null columns, exact reconstruction
+    a = o.random_matrix(rng, 9, 2)
+    m = a @ o.random_matrix(rng, 2, 5)
+    P, sig, Z = ctx.economy_svd(m)
+    assert np.linalg.norm(P @ np.diag(sig) @ Z.T - m) < 1e-10 * np.linalg.norm(m) and sig[2] <= 1e-13 * sig[0]
+    assert np.linalg.norm(P.T @ P - np.eye(5)) < 1e-10 and np.linalg.norm(Z.T @ Z - np.eye(5)) < 1e-10
+    with pytest.raises(p2g.NumericalError, match="svd operand"):
+        ctx.economy_svd(np.array([[1.0, np.nan], [0.0, 1.0]]))
+
+
 def test_cp_als_iteration_vs_oracle(ctx, oracle):  # cp.hpp:99-145
     o = oracle
     rng = o.Rng(32)
