@@ -434,11 +434,23 @@ def main():
                         "flop_model": ("8 sum(I_k) R^2 + 11 K R^3" if dom == "procrustes" else "13 K R^3"),
                         "ms_per_launch": cand[dom][0], "share_of_step": share, "hbm_view": hbm_view,
                         "note": "fp64 has no tcgen05 kind (SURVEY F8); peak = measured DFMA rate"}
-        else:
-            roofline = {"bound": "hbm", "kernel": dom, "achieved": hbm_view["achieved"], "peak": peak,
-                        "unit": "GB/s", "frac": hbm_view["frac"], "traffic": traffic, "peak_kind": peak_kind,
-                        "algorithmic_bytes_per_launch": ab[akey], "ms_per_launch": cand[dom][0],
-                        "share_of_step": share}
+            # the pipe that actually limits the R = 40 kernel: shared-memory wavefronts of
+            # the Jacobi rounds.  Count = ncu's l1tex shared wavefronts of one full-size launch
+            # (profiles/ncu_r02_full.txt, iteration 4), peak = one wavefront per SM and clock.
+            try:
+                tr = json.load(open(os.path.join(ROOT, "profiles", "traffic_r02.json"))).get(f"cfg{cfg_id}", {})
+                wf, wf_ms = tr.get(dom + "_smem_wavefronts"), tr.get(dom + "_ncu_ms")
+            except Exception:
+                wf = wf_ms = None
+            if wf and wf_ms and world == 1:
+                props = torch.cuda.get_device_properties(local)
+                wf_peak = props.multi_processor_count * (clk.summary().get("sm_mhz") or 1965.0) * 1e6
+                roofline["smem_view"] = {"bound": "shared-memory pipe", "wavefronts_per_launch": wf,
+                                         "ncu_ms_per_launch": wf_ms, "achieved": wf / (wf_ms * 1e-3),
+                                         "peak": wf_peak, "unit": "wavefronts/s",
+                                         "frac": wf / (wf_ms * 1e-3) / wf_peak,
+                                         "note": "count and duration of the same ncu-captured launch (iteration 4; "
+                                                 "the sweep count, hence both, is data dependent)"}
     iter_gbs = ab["iteration"] / (ms_step * 1e-3) / 1e9
 
     # end-to-end through the public API, every byte the reference's
