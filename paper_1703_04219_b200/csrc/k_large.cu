@@ -151,33 +151,41 @@ template <int RP, bool EXACT, class FA, class FB, class Epi>
 __device__ __forceinline__ void warp_mm(int rows, int R, FA fa, FB fb, Epi epi) {
   constexpr int NB = RP / 8;
   const int lane = threadIdx.x & 31, fm = lane >> 2, fk = lane & 3;
+  // two 8-row tiles per pass: every B fragment (a shared-memory or global load per lane) feeds two
+  // DMMAs; the accumulation order per output element is that of one tile at a time
 #pragma unroll 1
-  for (int i0 = 0; i0 < rows; i0 += 8) {
-    const int i = i0 + fm;
-    const bool iv = i < rows;
-    double acc[NB][2];
+  for (int i0 = 0; i0 < rows; i0 += 16) {
+    const int ia = i0 + fm, ib = i0 + 8 + fm;
+    const bool va = ia < rows, vb = ib < rows;
+    double acc[2][NB][2];
 #pragma unroll
-    for (int b = 0; b < NB; ++b) acc[b][0] = acc[b][1] = 0.0;
+    for (int b = 0; b < NB; ++b) acc[0][b][0] = acc[0][b][1] = acc[1][b][0] = acc[1][b][1] = 0.0;
 #pragma unroll 2
     for (int k4 = 0; k4 < RP; k4 += 4) {
       const int c = k4 + fk;
       const bool cv = EXACT || c < R;
-      const double x = (iv && cv) ? fa(i, c) : 0.0;
+      const double xa = (va && cv) ? fa(ia, c) : 0.0;
+      const double xb = (vb && cv) ? fa(ib, c) : 0.0;
 #pragma unroll
       for (int b = 0; b < NB; ++b) {
         const int j = 8 * b + fm;
         const double y = (cv && (EXACT || j < R)) ? fb(c, j) : 0.0;
-        dev::dmma884(acc[b], x, y);
+        dev::dmma884(acc[0][b], xa, y);
+        dev::dmma884(acc[1][b], xb, y);
       }
     }
-    if (iv) {
 #pragma unroll
-      for (int b = 0; b < NB; ++b)
+    for (int t = 0; t < 2; ++t) {
+      const int i = t ? ib : ia;
+      if (i < rows) {
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int j = 8 * b + 2 * fk + h;
-          if (EXACT || j < R) epi(i, j, acc[b][h]);
-        }
+        for (int b = 0; b < NB; ++b)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int j = 8 * b + 2 * fk + h;
+            if (EXACT || j < R) epi(i, j, acc[t][b][h]);
+          }
+      }
     }
   }
 }
